@@ -1,0 +1,189 @@
+/*
+ * lrnr_gpu.h -- C ABI of the B200-native LRNR / FastLRNR residual+gradient path.
+ *
+ * Drop-in boundary for the hot path of arXiv 2410.04001's reference
+ * (/root/reference/proj).  The reference's own "plugin" surface for this path is
+ *     lrnr::training::run_batch_gradient(Trainables, ParamSelector, SetupFn, EmitFn,
+ *                                        n_terms, ParallelConfig)   (training.hpp:200-202)
+ * driven by the PinnTermEmitter (training.cpp:270-329) or the fast-phase emitter
+ * (training.cpp:521-563), plus the plain losses loss_tune / loss_fast /
+ * loss_meta (training.hpp:90-100) and the per-point jet_forward / residual
+ * (model.hpp:118-119, pde.hpp:56).  run_batch_gradient interprets arbitrary
+ * caller closures and cannot be offloaded as such; this ABI replaces the
+ * (emitter + run_batch_gradient) PAIRS that the training loops call, with the
+ * same semantics:
+ *   - result = BatchGradResult{value, comps[4], grad} (training.hpp:189-195),
+ *   - grad in ParamPacker order (autodiff.cpp:926-946): CoefficientsOnly ->
+ *     s_1..s_L concatenated; BasesBiasesAndHyper -> per layer U_l, V_l, b_l,
+ *     then hypernetwork W_k, b_k,
+ *   - NonFiniteError(layer_tag) (autodiff.hpp:28-34) -> LRNR_ENONFINITE plus
+ *     lrnr_gpu_last_layer_tag(),
+ *   - std::invalid_argument from require() (linalg.hpp:74-76) -> LRNR_EINVAL.
+ * See INTEGRATION.md for the C++ adapter a reference maintainer would add.
+ *
+ * Plain pointers and sizes only; host arrays are row-major double (the
+ * reference's DenseMatrix/DenseVector storage, linalg.hpp:15-46).
+ *
+ * Flat parameter layouts:
+ *   LRNR  (LrnrParams, model.hpp:38-49): per layer l = 0..L-1:
+ *           U_l (widths[l+1] x ranks[l]), V_l (widths[l] x ranks[l]), b_l (widths[l+1]).
+ *   Fast  (FastParams, model.hpp:65-78): v_in (m_in x r_0); per inner l = 0..L-2:
+ *           u_hat (red[l] x r_l), b_hat (red[l]), v_hat (red[l] x r_{l+1});
+ *           u_out (m_out x r_{L-1}); b_out (m_out).
+ *   Hyper (HyperParams, model.hpp:83-95): per layer k: W_k (hw[k+1] x hw[k]), b_k (hw[k+1]).
+ *
+ * Threading: one context = one device + one stream; a context is not
+ * thread-safe (use one per host thread / GPU).  Results are bitwise
+ * run-to-run deterministic for a fixed device (fixed-order reductions, no
+ * floating-point atomics), mirroring run_batch_gradient's thread-count
+ * invariance (training.cpp:197-199).
+ */
+#ifndef LRNR_GPU_H
+#define LRNR_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define LRNR_OK 0
+#define LRNR_EINVAL 1      /* shape / argument error  (std::invalid_argument)            */
+#define LRNR_ENONFINITE 2  /* non-finite loss term    (NonFiniteError, see last_layer_tag) */
+#define LRNR_ECUDA 3       /* CUDA runtime failure                                        */
+#define LRNR_ENOMEM 4      /* device allocation failure                                   */
+#define LRNR_ESTATE 5      /* call order error (e.g. no model / points set)               */
+
+/* activation (ActivationKind, model.hpp:18; sin is this build's extension) */
+#define LRNR_ACT_TANH 0
+#define LRNR_ACT_SIN 1
+
+/* arithmetic type of the device path */
+#define LRNR_F64 0
+#define LRNR_F32 1
+
+/* model slots */
+#define LRNR_MODEL_LRNR 0
+#define LRNR_MODEL_FAST 1
+
+typedef struct lrnr_gpu_ctx lrnr_gpu_ctx;
+
+/* ---- context ---- */
+int lrnr_gpu_create(int device, lrnr_gpu_ctx** out);
+int lrnr_gpu_destroy(lrnr_gpu_ctx* ctx);
+const char* lrnr_gpu_last_error(const lrnr_gpu_ctx* ctx);
+/* layer tag of the last LRNR_ENONFINITE (NonFiniteError::layer_tag semantics:
+ * l+1 for LRNR layer l, 0 for the FastLRNR input factor, -1 otherwise). */
+int lrnr_gpu_last_layer_tag(const lrnr_gpu_ctx* ctx);
+/* Use a caller-owned cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
+ * NULL restores the context's own stream. */
+int lrnr_gpu_set_stream(lrnr_gpu_ctx* ctx, void* cuda_stream);
+/* Number of kernels this context has launched so far (instrumentation). */
+int64_t lrnr_gpu_launch_count(const lrnr_gpu_ctx* ctx);
+
+/* ---- model upload (replaces the Tape bindings, autodiff.cpp:826-868) ---- */
+/* LrnrParams; widths[L] must be 1 (scalar PDE output), widths[0] must be 2. */
+int lrnr_gpu_set_lrnr(lrnr_gpu_ctx* ctx, int depth, const int64_t* widths, const int64_t* ranks,
+                      const double* params, int act, int dtype);
+/* FastParams (EIM-reduced surrogate); m_in = 2, m_out = 1. */
+int lrnr_gpu_set_fast(lrnr_gpu_ctx* ctx, int depth, const int64_t* ranks, const int64_t* red_ranks,
+                      int64_t m_in, int64_t m_out, const double* fparams, int act, int dtype);
+/* HyperParams: n_layers affine layers, hw[0] = 3, hw[n_layers] = r_total of the
+ * model it feeds; tanh hidden, ReLU output, mu normalized by the box
+ * (model.cpp:74-81,294-318). */
+int lrnr_gpu_set_hyper(lrnr_gpu_ctx* ctx, int n_layers, const int64_t* hw, const double* hparams,
+                       const double* box_lo, const double* box_hi);
+
+/* ---- collocation points (CollocationBatch::interior, pde.hpp:33-40) ----
+ * n_inst groups of n_per_inst consecutive (x, t) pairs; group i belongs to
+ * PDE-parameter instance i.  Host pointer (copied) or device pointer of the
+ * context's dtype (borrowed; must stay valid while used). */
+int lrnr_gpu_set_points(lrnr_gpu_ctx* ctx, const double* xt, int64_t n_inst, int64_t n_per_inst);
+int lrnr_gpu_set_points_device(lrnr_gpu_ctx* ctx, const void* xt_dev, int64_t n_inst,
+                               int64_t n_per_inst);
+
+/* ---- per-step gradient calls (host buffers; synchronous) ----
+ *
+ * lrnr_gpu_loss_grad_s: PinnTermEmitter, fine-tune mode, interior terms
+ * (training.cpp:286-293): term_i = w * N[u](x_i,t_i; mu)^2 with
+ * N = u_t + mu1 u_x - mu2 u_xx - mu3 u(1-u) (pde.cpp:9-13), CoefficientsOnly.
+ * Requires n_inst == 1.  w <= 0 selects the reference weight 1/n
+ * (training.cpp:364-366).  Outputs: value, comps[4] = {residual, boundary,
+ * sparse, local}, grad_s (r_total).  model = LRNR_MODEL_LRNR or _FAST (the
+ * squared-residual objective on the FastLRNR, BASELINE config 1). */
+int lrnr_gpu_loss_grad_s(lrnr_gpu_ctx* ctx, int model, const double* s, const double* mu, double w,
+                         double* out_value, double* out_comps4, double* out_grad_s);
+
+/* Per-instance variant: s (n_inst x r_total), mu (n_inst x 3).  w <= 0 ->
+ * 1/(n_inst*n_per_inst).  out_value = total; out_grad_s (n_inst x r_total). */
+int lrnr_gpu_loss_grad_s_multi(lrnr_gpu_ctx* ctx, int model, const double* s, const double* mu,
+                               double w, double* out_value, double* out_grad_s);
+
+/* Hypernetwork-coupled step (BASELINE config 3; the emit_hyper + emit_fast_jet
+ * composition of autodiff.cpp:883-922): s_i = hyper(mu_i) on device, the model
+ * gradient per instance, then the hypernetwork VJP summed over instances.
+ * mus (n_inst x 3).  Outputs: value, per-instance grad_s (n_inst x r_total, may
+ * be NULL), grad_theta (hyper flat layout). */
+int lrnr_gpu_hyper_loss_grad(lrnr_gpu_ctx* ctx, int model, const double* mus, double w,
+                             double* out_value, double* out_grad_s, double* out_grad_theta);
+
+/* Meta step (BASELINE config 4; PinnTermEmitter meta_mode interior terms,
+ * training.cpp:283-293 with lambda_sparse = 0): gradient w.r.t. the LRNR bases
+ * and biases AND the hypernetwork, in ParamPacker(BasesBiasesAndHyper) order.
+ * mus (n_inst x 3).  Requires the LRNR model and the hypernetwork. */
+int lrnr_gpu_meta_loss_grad(lrnr_gpu_ctx* ctx, const double* mus, double w, double* out_value,
+                            double* out_grad);
+
+/* ---- forward only ---- */
+/* Output jets (u, u_x, u_t, u_xx) per point (jet_forward, model.cpp:357-405);
+ * s (n_inst x r_total); out (n_points x 4). */
+int lrnr_gpu_jets(lrnr_gpu_ctx* ctx, int model, const double* s, double* out_jets);
+/* Interior loss only (loss_tune / loss_fast interior part, training.cpp:76-105). */
+int lrnr_gpu_loss(lrnr_gpu_ctx* ctx, int model, const double* s, const double* mu, double w,
+                  double* out_value);
+
+/* ---- device-resident step (no host sync; for benchmarks and multi-GPU) ----
+ * lrnr_gpu_upload_coeffs: s (n_inst x r_total) and mu (n_inst x 3) to device.
+ * lrnr_gpu_run: launch the residual+gradient of `model` over the resident
+ * points with the resident coefficients; writes n_inst rows of
+ * [value, grad_s(r_total)] as double into dev_out (device pointer; NULL = the
+ * context's own buffer).  Asynchronous on the context stream.
+ * lrnr_gpu_check: synchronize and map a recorded non-finite term to
+ * LRNR_ENONFINITE (+ layer tag). */
+int lrnr_gpu_upload_coeffs(lrnr_gpu_ctx* ctx, const double* s, const double* mu, int64_t n_inst);
+int lrnr_gpu_run(lrnr_gpu_ctx* ctx, int model, double w, double* dev_out);
+int lrnr_gpu_check(lrnr_gpu_ctx* ctx);
+/* Copy the context's result buffer (n_inst x (1 + r_total) doubles) to host. */
+int lrnr_gpu_download(lrnr_gpu_ctx* ctx, double* host_out, int64_t n_doubles);
+
+/* ---- host-side setup (no GPU needed; reference reduction.cpp / model.cpp) ---- */
+/* BASELINE config generator: make_lrnr_params(orthonormal,
+ * bias 0) from Rng(seed), then b <- 0.1*normal(), s <- U[0,1] sorted descending. */
+int lrnr_host_make_baseline_model(int depth, const int64_t* widths, const int64_t* ranks,
+                                  uint64_t seed, double* out_params, double* out_s);
+/* make_hyper_params (model.cpp:480-504) from a fresh Rng(seed). */
+int lrnr_host_make_hyper_params(int depth_split, const int64_t* split, int hidden_depth,
+                                int hidden_width, uint64_t seed, double out_w_scale,
+                                double out_bias, double* out_params);
+/* sample_collocation interior points (pde.cpp:20-49), optional per-point mu. */
+int lrnr_host_sample_collocation(uint64_t seed, int64_t n_interior, const double* mu_lo,
+                                 const double* mu_hi, int with_mu, double* out_xt,
+                                 double* out_mu);
+/* FastLRNR construction: harvest_snapshots at SamplingSetX::uniform_grid(nx, nt)
+ * with n_perturb Gaussian perturbations (sigma * extent), greedy EIM with budget
+ * r_hat per inner layer, build_fastparams (reduction.cpp:10-31,111-283), for
+ * n_mu coefficient vectors s (n_mu x r_total; the hyper_forward outputs).
+ * out_indices ((L-1) x r_hat, -1 padded), out_red ((L-1)), out_fparams. */
+int lrnr_host_build_fast(int depth, const int64_t* widths, const int64_t* ranks,
+                         const double* params, int act, const double* s, int64_t n_mu,
+                         int64_t nx, int64_t nt, int64_t n_perturb, double sigma, uint64_t seed,
+                         int64_t r_hat, int64_t* out_red, int64_t* out_indices,
+                         double* out_fparams, int* out_exhausted);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LRNR_GPU_H */

@@ -1,0 +1,70 @@
+"""Loader for the in-tree native library ``liblrnr_gpu.so`` (include/lrnr_gpu.h).
+
+The product path has no fallback: if the library is missing the import fails
+loudly (build it with ``python -c "import __graft_entry__ as g; g.build()"``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "liblrnr_gpu.so")
+
+# every symbol include/lrnr_gpu.h declares
+EXPORTS = (
+    "lrnr_gpu_create", "lrnr_gpu_destroy", "lrnr_gpu_last_error", "lrnr_gpu_last_layer_tag",
+    "lrnr_gpu_set_stream", "lrnr_gpu_launch_count", "lrnr_gpu_set_lrnr", "lrnr_gpu_set_fast",
+    "lrnr_gpu_set_hyper", "lrnr_gpu_set_points", "lrnr_gpu_set_points_device", "lrnr_gpu_loss_grad_s",
+    "lrnr_gpu_loss_grad_s_multi", "lrnr_gpu_hyper_loss_grad", "lrnr_gpu_meta_loss_grad", "lrnr_gpu_jets",
+    "lrnr_gpu_loss", "lrnr_gpu_upload_coeffs", "lrnr_gpu_run", "lrnr_gpu_check", "lrnr_gpu_download",
+    "lrnr_host_make_baseline_model", "lrnr_host_make_hyper_params", "lrnr_host_sample_collocation",
+    "lrnr_host_build_fast",
+)
+
+LRNR_OK, LRNR_EINVAL, LRNR_ENONFINITE, LRNR_ECUDA, LRNR_ENOMEM, LRNR_ESTATE = range(6)
+ACT_TANH, ACT_SIN = 0, 1
+F64, F32 = 0, 1
+MODEL_LRNR, MODEL_FAST = 0, 1
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built; run __graft_entry__.build() (no CPU fallback exists)")
+    lib = C.CDLL(LIB_PATH)
+    vp, i64, dp, ip = C.c_void_p, C.c_int64, C.c_void_p, C.c_int
+    lib.lrnr_gpu_create.argtypes = [ip, C.POINTER(vp)]
+    lib.lrnr_gpu_destroy.argtypes = [vp]
+    lib.lrnr_gpu_last_error.argtypes = [vp]
+    lib.lrnr_gpu_last_error.restype = C.c_char_p
+    lib.lrnr_gpu_last_layer_tag.argtypes = [vp]
+    lib.lrnr_gpu_set_stream.argtypes = [vp, vp]
+    lib.lrnr_gpu_launch_count.argtypes = [vp]
+    lib.lrnr_gpu_launch_count.restype = i64
+    lib.lrnr_gpu_set_lrnr.argtypes = [vp, ip, dp, dp, dp, ip, ip]
+    lib.lrnr_gpu_set_fast.argtypes = [vp, ip, dp, dp, i64, i64, dp, ip, ip]
+    lib.lrnr_gpu_set_hyper.argtypes = [vp, ip, dp, dp, dp, dp]
+    lib.lrnr_gpu_set_points.argtypes = [vp, dp, i64, i64]
+    lib.lrnr_gpu_set_points_device.argtypes = [vp, vp, i64, i64]
+    lib.lrnr_gpu_loss_grad_s.argtypes = [vp, ip, dp, dp, C.c_double, dp, dp, dp]
+    lib.lrnr_gpu_loss_grad_s_multi.argtypes = [vp, ip, dp, dp, C.c_double, dp, dp]
+    lib.lrnr_gpu_hyper_loss_grad.argtypes = [vp, ip, dp, C.c_double, dp, dp, dp]
+    lib.lrnr_gpu_meta_loss_grad.argtypes = [vp, dp, C.c_double, dp, dp]
+    lib.lrnr_gpu_jets.argtypes = [vp, ip, dp, dp]
+    lib.lrnr_gpu_loss.argtypes = [vp, ip, dp, dp, C.c_double, dp]
+    lib.lrnr_gpu_upload_coeffs.argtypes = [vp, dp, dp, i64]
+    lib.lrnr_gpu_run.argtypes = [vp, ip, C.c_double, vp]
+    lib.lrnr_gpu_check.argtypes = [vp]
+    lib.lrnr_gpu_download.argtypes = [vp, dp, i64]
+    lib.lrnr_host_make_baseline_model.argtypes = [ip, dp, dp, C.c_uint64, dp, dp]
+    lib.lrnr_host_make_hyper_params.argtypes = [ip, dp, ip, ip, C.c_uint64, C.c_double, C.c_double, dp]
+    lib.lrnr_host_sample_collocation.argtypes = [C.c_uint64, i64, dp, dp, ip, dp, dp]
+    lib.lrnr_host_build_fast.argtypes = [ip, dp, dp, dp, ip, dp, i64, i64, i64, i64, C.c_double, C.c_uint64, i64,
+                                         dp, dp, dp, dp]
+    _lib = lib
+    return lib

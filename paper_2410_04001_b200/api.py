@@ -1,0 +1,379 @@
+"""Python binding of the C ABI (include/lrnr_gpu.h) used by the tests and bench.
+
+The drop-in for the reference's C++ callers is include/lrnr_gpu_adapter.hpp
+(C++ over the same ABI); this module is the ctypes view of that ABI plus the
+BASELINE-config builders.  Errors map to the reference's exception types:
+LRNR_EINVAL -> ValueError (std::invalid_argument), LRNR_ENONFINITE ->
+NonFiniteError(layer_tag) (autodiff.hpp:28-34).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import ACT_SIN, ACT_TANH, F32, F64, MODEL_FAST, MODEL_LRNR  # noqa: F401
+
+TWO_PI = 6.283185307179586476925286766559
+
+
+class NonFiniteError(FloatingPointError):
+    """Mirror of lrnr::NonFiniteError (autodiff.hpp:28-34)."""
+
+    def __init__(self, layer_tag: int, msg: str = ""):
+        super().__init__(msg or f"non-finite value in recorded computation, layer tag {layer_tag}")
+        self.layer_tag = layer_tag
+
+
+class LrnrGpuError(RuntimeError):
+    pass
+
+
+def _f64(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _i64(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int64))
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+# ---------------------------------------------------------------------------
+# parameter containers (flat layouts of include/lrnr_gpu.h)
+# ---------------------------------------------------------------------------
+@dataclass
+class LrnrParams:
+    """LrnrParams (model.hpp:38-49) as widths, ranks and the flat U,V,b array."""
+    widths: np.ndarray
+    ranks: np.ndarray
+    params: np.ndarray
+    act: int = ACT_TANH
+
+    @property
+    def depth(self) -> int:
+        return len(self.ranks)
+
+    @property
+    def r_total(self) -> int:
+        return int(np.sum(self.ranks))
+
+    def offsets(self):
+        o, out = 0, []
+        for l in range(self.depth):
+            w0, w1, r = int(self.widths[l]), int(self.widths[l + 1]), int(self.ranks[l])
+            oU = o
+            o += w1 * r
+            oV = o
+            o += w0 * r
+            ob = o
+            o += w1
+            out.append((oU, oV, ob))
+        return out, o
+
+
+@dataclass
+class FastParams:
+    """FastParams (model.hpp:65-78), flat layout of include/lrnr_gpu.h."""
+    ranks: np.ndarray
+    red_ranks: np.ndarray
+    fparams: np.ndarray
+    act: int = ACT_TANH
+    indices: Optional[np.ndarray] = None
+    exhausted: Optional[np.ndarray] = None
+
+    @property
+    def r_total(self) -> int:
+        return int(np.sum(self.ranks))
+
+
+@dataclass
+class HyperParams:
+    """HyperParams (model.hpp:83-95): widths hw (3, ..., r_total), flat W,b, box."""
+    hw: np.ndarray
+    params: np.ndarray
+    lo: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    hi: np.ndarray = field(default_factory=lambda: np.zeros(3))
+
+    @property
+    def n_params(self) -> int:
+        return int(sum(self.hw[k + 1] * self.hw[k] + self.hw[k + 1] for k in range(len(self.hw) - 1)))
+
+
+# ---------------------------------------------------------------------------
+# host-side generators and FastLRNR construction (CPU, inside the native lib)
+# ---------------------------------------------------------------------------
+def make_baseline_model(widths, ranks, seed, act=ACT_TANH):
+    lib = _lib.load()
+    w, r = _i64(widths), _i64(ranks)
+    n = int(sum(w[l + 1] * r[l] + w[l] * r[l] + w[l + 1] for l in range(len(r))))
+    P, s = np.zeros(n), np.zeros(int(r.sum()))
+    rc = lib.lrnr_host_make_baseline_model(len(r), _p(w), _p(r), C.c_uint64(seed), _p(P), _p(s))
+    if rc != 0:
+        raise ValueError("make_baseline_model: invalid shapes")
+    return LrnrParams(w, r, P, act), s
+
+
+def make_hyper_params(split, hidden_depth, hidden_width, seed, lo, hi, out_w_scale=0.01, out_bias=0.5):
+    lib = _lib.load()
+    sp = _i64(split)
+    hw = np.array([3] + [hidden_width] * hidden_depth + [int(sp.sum())], np.int64)
+    n = int(sum(hw[k + 1] * hw[k] + hw[k + 1] for k in range(len(hw) - 1)))
+    H = np.zeros(n)
+    rc = lib.lrnr_host_make_hyper_params(len(sp), _p(sp), hidden_depth, hidden_width, C.c_uint64(seed),
+                                         C.c_double(out_w_scale), C.c_double(out_bias), _p(H))
+    if rc != 0:
+        raise ValueError("make_hyper_params failed")
+    return HyperParams(hw, H, _f64(lo), _f64(hi))
+
+
+def sample_collocation(seed, n_interior, lo=(0.0, 0.0, 0.0), hi=(0.0, 0.0, 0.0), with_mu=False):
+    lib = _lib.load()
+    xt = np.zeros(2 * n_interior + 2)
+    mu = np.zeros(3 * n_interior + 3)
+    rc = lib.lrnr_host_sample_collocation(C.c_uint64(seed), n_interior, _p(_f64(lo)), _p(_f64(hi)), int(with_mu),
+                                          _p(xt), _p(mu))
+    if rc != 0:
+        raise ValueError("sample_collocation failed")
+    xt = xt[:2 * n_interior].reshape(n_interior, 2)
+    return (xt, mu[:3 * n_interior].reshape(n_interior, 3)) if with_mu else xt
+
+
+def build_fast(model: LrnrParams, s, nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777, r_hat=10) -> FastParams:
+    """harvest_snapshots + eim_greedy + build_fastparams (reduction.cpp:111-283)."""
+    lib = _lib.load()
+    L = model.depth
+    S = _f64(s).reshape(-1, model.r_total)
+    red = np.zeros(L - 1, np.int64)
+    idx = np.zeros((L - 1) * r_hat, np.int64)
+    nF = 2 * int(model.ranks[0])
+    for l in range(L - 1):
+        nF += r_hat * int(model.ranks[l]) + r_hat + r_hat * int(model.ranks[l + 1])
+    nF += int(model.ranks[-1]) + 1
+    F = np.zeros(nF)
+    exh = np.zeros(L - 1, np.int32)
+    rc = lib.lrnr_host_build_fast(L, _p(model.widths), _p(model.ranks), _p(_f64(model.params)), model.act, _p(S),
+                                  S.shape[0], nx, nt, n_perturb, C.c_double(sigma), C.c_uint64(seed), r_hat,
+                                  _p(red), _p(idx), _p(F), exh.ctypes.data_as(C.c_void_p))
+    if rc != 0:
+        raise ValueError("build_fast: reduction failed (shape error or singular interpolation block)")
+    used = 2 * int(model.ranks[0])
+    for l in range(L - 1):
+        used += int(red[l]) * (int(model.ranks[l]) + 1 + int(model.ranks[l + 1]))
+    used += int(model.ranks[-1]) + 1
+    return FastParams(model.ranks.copy(), red, F[:used], model.act, idx.reshape(L - 1, r_hat), exh)
+
+
+# ---------------------------------------------------------------------------
+# device context
+# ---------------------------------------------------------------------------
+class GpuContext:
+    """One device + one stream (lrnr_gpu_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = _lib.load()
+        h = C.c_void_p()
+        rc = self.lib.lrnr_gpu_create(device, C.byref(h))
+        if rc != 0:
+            raise LrnrGpuError(f"lrnr_gpu_create({device}) failed with code {rc} (no usable CUDA device)")
+        self.h = h
+        self.r_total = {}
+        self.hyper_n = 0
+        self.n_points = 0
+        self.n_inst = 0
+
+    def close(self):
+        if self.h:
+            self.lib.lrnr_gpu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _rc(self, rc, what):
+        if rc == _lib.LRNR_OK:
+            return
+        msg = self.lib.lrnr_gpu_last_error(self.h).decode()
+        if rc == _lib.LRNR_ENONFINITE:
+            raise NonFiniteError(self.lib.lrnr_gpu_last_layer_tag(self.h), msg)
+        if rc == _lib.LRNR_EINVAL:
+            raise ValueError(f"{what}: {msg}")
+        raise LrnrGpuError(f"{what}: code {rc}: {msg}")
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.lrnr_gpu_launch_count(self.h))
+
+    def set_stream(self, stream_handle: int | None):
+        """Launch on a caller stream (e.g. torch.cuda.current_stream().cuda_stream).
+
+        Handle 0 is the legacy default stream and is passed as cudaStreamLegacy;
+        None restores the context's own stream."""
+        h = None if stream_handle is None else (stream_handle if stream_handle != 0 else 1)
+        self._rc(self.lib.lrnr_gpu_set_stream(self.h, C.c_void_p(h)), "set_stream")
+
+    def set_lrnr(self, m: LrnrParams, dtype=F64):
+        self._rc(self.lib.lrnr_gpu_set_lrnr(self.h, m.depth, _p(_i64(m.widths)), _p(_i64(m.ranks)),
+                                            _p(_f64(m.params)), m.act, dtype), "set_lrnr")
+        self.r_total[MODEL_LRNR] = m.r_total
+
+    def set_fast(self, f: FastParams, dtype=F64):
+        self._rc(self.lib.lrnr_gpu_set_fast(self.h, len(f.ranks), _p(_i64(f.ranks)), _p(_i64(f.red_ranks)), 2, 1,
+                                            _p(_f64(f.fparams)), f.act, dtype), "set_fast")
+        self.r_total[MODEL_FAST] = f.r_total
+
+    def set_hyper(self, h: HyperParams):
+        hw = _i64(h.hw)
+        self._rc(self.lib.lrnr_gpu_set_hyper(self.h, len(hw) - 1, _p(hw), _p(_f64(h.params)), _p(_f64(h.lo)),
+                                             _p(_f64(h.hi))), "set_hyper")
+        self.hyper_n = h.n_params
+
+    def set_points(self, xt, n_inst: int = 1):
+        xt = _f64(xt).reshape(-1, 2)
+        n = xt.shape[0]
+        if n % n_inst:
+            raise ValueError("points not divisible into instances")
+        self._keep_pts = xt
+        self._rc(self.lib.lrnr_gpu_set_points(self.h, _p(xt), n_inst, n // n_inst), "set_points")
+        self.n_points, self.n_inst = n, n_inst
+
+    def set_points_device(self, ptr: int, n_points: int, n_inst: int = 1):
+        self._rc(self.lib.lrnr_gpu_set_points_device(self.h, C.c_void_p(ptr), n_inst, n_points // n_inst),
+                 "set_points_device")
+        self.n_points, self.n_inst = n_points, n_inst
+
+    # --- per-step calls (host buffers) ---
+    def loss_grad_s(self, model, s, mu, w=0.0):
+        R = self.r_total[model]
+        g = np.zeros(R)
+        comps = np.zeros(4)
+        v = C.c_double(0.0)
+        self._rc(self.lib.lrnr_gpu_loss_grad_s(self.h, model, _p(_f64(s)), _p(_f64(mu)), C.c_double(w), C.byref(v),
+                                               _p(comps), _p(g)), "loss_grad_s")
+        return dict(value=v.value, comps=comps, grad_s=g)
+
+    def loss_grad_s_multi(self, model, s, mu, w=0.0):
+        R = self.r_total[model]
+        g = np.zeros((self.n_inst, R))
+        v = C.c_double(0.0)
+        self._rc(self.lib.lrnr_gpu_loss_grad_s_multi(self.h, model, _p(_f64(s)), _p(_f64(mu)), C.c_double(w),
+                                                     C.byref(v), _p(g)), "loss_grad_s_multi")
+        return dict(value=v.value, grad_s=g)
+
+    def hyper_loss_grad(self, model, mus, w=0.0):
+        R = self.r_total[model]
+        g = np.zeros((self.n_inst, R))
+        gt = np.zeros(self.hyper_n)
+        v = C.c_double(0.0)
+        self._rc(self.lib.lrnr_gpu_hyper_loss_grad(self.h, model, _p(_f64(mus)), C.c_double(w), C.byref(v), _p(g),
+                                                   _p(gt)), "hyper_loss_grad")
+        return dict(value=v.value, grad_s=g, grad_theta=gt)
+
+    def meta_loss_grad(self, mus, n_lrnr_params, w=0.0):
+        g = np.zeros(n_lrnr_params + self.hyper_n)
+        v = C.c_double(0.0)
+        self._rc(self.lib.lrnr_gpu_meta_loss_grad(self.h, _p(_f64(mus)), C.c_double(w), C.byref(v), _p(g)),
+                 "meta_loss_grad")
+        return dict(value=v.value, grad=g)
+
+    def jets(self, model, s):
+        out = np.zeros((self.n_points, 4))
+        self._rc(self.lib.lrnr_gpu_jets(self.h, model, _p(_f64(s)), _p(out)), "jets")
+        return out
+
+    def loss(self, model, s, mu, w=0.0):
+        v = C.c_double(0.0)
+        self._rc(self.lib.lrnr_gpu_loss(self.h, model, _p(_f64(s)), _p(_f64(mu)), C.c_double(w), C.byref(v)),
+                 "loss")
+        return v.value
+
+    # --- device-resident step ---
+    def upload_coeffs(self, s, mu, n_inst=1):
+        self._rc(self.lib.lrnr_gpu_upload_coeffs(self.h, _p(_f64(s)), _p(_f64(mu)), n_inst), "upload_coeffs")
+
+    def run(self, model, w=0.0, dev_out: int | None = None):
+        self._rc(self.lib.lrnr_gpu_run(self.h, model, C.c_double(w), C.c_void_p(dev_out or 0)), "run")
+
+    def check(self):
+        self._rc(self.lib.lrnr_gpu_check(self.h), "check")
+
+    def download(self, n):
+        out = np.zeros(n)
+        self._rc(self.lib.lrnr_gpu_download(self.h, _p(out), n), "download")
+        return out
+
+
+# ---------------------------------------------------------------------------
+# BASELINE.json configurations (seeded synthetic inputs)
+# ---------------------------------------------------------------------------
+C0_WIDTHS, C0_RANKS = [2, 100, 100, 100, 1], [2, 10, 10, 1]
+C2_WIDTHS, C2_RANKS = [2] + [256] * 6 + [1], [2, 32, 32, 32, 32, 32, 1]
+C4_WIDTHS, C4_RANKS = [2] + [512] * 8 + [1], [2] + [64] * 7 + [1]
+C3_LO, C3_HI = (1.0, 0.0, 0.0), (40.0, 0.1, 10.0)
+
+
+def config0(n_points=4096):
+    """c0: LRNR 2-100x3-1, r (2,10,10,1), FP64, tanh, mu=(30,0,0), 4096 pts."""
+    m, s = make_baseline_model(C0_WIDTHS, C0_RANKS, 2410, ACT_TANH)
+    pts = sample_collocation(4001, n_points)
+    return dict(model=m, s=s, pts=pts, mu=np.array([30.0, 0.0, 0.0]), dtype=F64)
+
+
+def config1(n_points=4096):
+    """c1: FastLRNR of c0 with rhat=10 from the reference EIM recipe."""
+    c = config0(n_points)
+    c["fast"] = build_fast(c["model"], c["s"], nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777, r_hat=10)
+    return c
+
+
+def config2(n_points=1 << 20, act=ACT_SIN, with_fast=True):
+    """c2: LRNR 2-256x6-1, r (2,32x5,1), FP32, sin, mu=(20,0.01,5); FastLRNR rhat=32."""
+    m, s = make_baseline_model(C2_WIDTHS, C2_RANKS, 2411, act)
+    pts = sample_collocation(4002, n_points)
+    out = dict(model=m, s=s, pts=pts, mu=np.array([20.0, 0.01, 5.0]), dtype=F32)
+    if with_fast:
+        out["fast"] = build_fast(m, s, nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777, r_hat=32)
+    return out
+
+
+def config3(n_inst=1024, pts_per_inst=16384, act=ACT_SIN):
+    """c3: 1024 mu ~ U[1,40]xU[0,0.1]xU[0,10]; hypernet 3-64-64-163 on the c2 base; FastLRNR."""
+    c = config2(n_points=0, act=act, with_fast=True)
+    hyper = make_hyper_params(C2_RANKS, 2, 64, 4003, C3_LO, C3_HI, 0.01, 0.5)
+    _, mus = sample_collocation(4004, n_inst, C3_LO, C3_HI, with_mu=True)
+    pts = np.concatenate([sample_collocation(5000 + i, pts_per_inst) for i in range(n_inst)]) if pts_per_inst else \
+        np.zeros((0, 2))
+    c.update(hyper=hyper, mus=mus, pts=pts, n_inst=n_inst)
+    return c
+
+
+def config4(n_inst=64, pts_per_inst=1 << 20, act=ACT_SIN):
+    """c4: meta step, 2-512x8-1, r (2,64x7,1), hypernet 3-64-64-451, 64 mu x 1M pts."""
+    m, _ = make_baseline_model(C4_WIDTHS, C4_RANKS, 2412, act)
+    hyper = make_hyper_params(C4_RANKS, 2, 64, 4005, C3_LO, C3_HI, 0.01, 0.5)
+    _, mus = sample_collocation(4006, n_inst, C3_LO, C3_HI, with_mu=True)
+    pts = np.concatenate([sample_collocation(6000 + i, pts_per_inst) for i in range(n_inst)]) if pts_per_inst else \
+        np.zeros((0, 2))
+    return dict(model=m, hyper=hyper, mus=mus, pts=pts, n_inst=n_inst, dtype=F32)
+
+
+def algorithmic_flops_per_point(widths: Sequence[int], ranks: Sequence[int], meta: bool = False) -> int:
+    """LRNR coefficient-only 8*S FMA, meta 12*S; FLOP = 2*FMA."""
+    S = sum(int(ranks[l]) * (int(widths[l]) + int(widths[l + 1])) for l in range(len(ranks)))
+    return 2 * (12 if meta else 8) * S
+
+
+def fast_flops_per_point(ranks: Sequence[int], red: Sequence[int], m_in=2, m_out=1) -> int:
+    """SURVEY Appendix B FastLRNR: fwd 4*(M0 r1 + sum rhat(r_l + r_{l+1}) + r_L M_L) FMA, bwd = fwd."""
+    L = len(ranks)
+    fwd = m_in * int(ranks[0]) + sum(int(red[l]) * (int(ranks[l]) + int(ranks[l + 1])) for l in range(L - 1)) + \
+        int(ranks[-1]) * m_out
+    return 2 * 2 * 4 * fwd

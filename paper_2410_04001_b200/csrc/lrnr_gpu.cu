@@ -1,0 +1,866 @@
+// C-ABI implementation of include/lrnr_gpu.h: device-resident models, the
+// launch planning for the fused residual+gradient kernels (pinn_kernels.cuh),
+// the hypernetwork coupling (hyper_kernels.cuh), the meta-gradient path
+// (meta_kernels.cuh) and the non-finite diagnosis (NonFiniteError semantics,
+// autodiff.cpp:448-461).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "hyper_kernels.cuh"
+#include "lrnr_gpu.h"
+#include "meta_kernels.cuh"
+#include "pinn_kernels.cuh"
+
+using namespace lrnr_b200;
+
+namespace {
+
+struct CudaError : std::runtime_error {
+    explicit CudaError(const std::string& m) : std::runtime_error(m) {}
+};
+struct InvalidArg : std::runtime_error {
+    explicit InvalidArg(const std::string& m) : std::runtime_error(m) {}
+};
+struct StateError : std::runtime_error {
+    explicit StateError(const std::string& m) : std::runtime_error(m) {}
+};
+struct NonFinite : std::runtime_error {
+    int tag;
+    NonFinite(int t) : std::runtime_error("non-finite value in recorded computation, layer tag " + std::to_string(t)), tag(t) {}
+};
+
+#define CK(x)                                                                                  \
+    do {                                                                                       \
+        cudaError_t e_ = (x);                                                                  \
+        if (e_ != cudaSuccess)                                                                 \
+            throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));                 \
+    } while (0)
+
+void require(bool c, const std::string& m) {
+    if (!c) throw InvalidArg(m);
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void ensure(size_t n) {
+        if (n <= bytes) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        if (n == 0) return;
+        if (cudaMalloc(&p, n) != cudaSuccess) {
+            cudaGetLastError();
+            throw std::bad_alloc();
+        }
+        bytes = n;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+// A network in the kernel's streaming layout (see pinn_kernels.cuh).
+struct Model {
+    bool set = false;
+    int kind = LRNR_MODEL_LRNR;
+    int dtype = LRNR_F64;
+    int act = LRNR_ACT_TANH;
+    int L = 0;
+    std::vector<int> M, r, soff, trow;
+    int rtotal = 0, rmax = 0;
+    // packed host copy (double) in device layout; offsets in elements
+    std::vector<double> packed;
+    size_t off_V0 = 0, off_ulast = 0;
+    std::vector<size_t> off_trans;
+    DevBuf dev;
+    // LRNR-only extras for the meta path: original flat params (double)
+    std::vector<double> flat;
+    std::vector<int64_t> widths64, ranks64;
+};
+
+struct Hyper {
+    bool set = false;
+    int K = 0;
+    std::vector<int> hw;
+    std::vector<int> oW, ob;
+    int max_w = 0, n_params = 0;
+    double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    DevBuf dev;
+};
+
+void build_layout(Model& m) {
+    const int L = m.L;
+    m.soff.assign(L + 1, 0);
+    for (int l = 0; l < L; ++l) m.soff[l + 1] = m.soff[l] + m.r[l];
+    m.rtotal = m.soff[L];
+    m.rmax = *std::max_element(m.r.begin(), m.r.end());
+    m.trow.assign(L, 0);
+    m.off_trans.assign(L, 0);
+    size_t o = 0;
+    m.off_V0 = o;
+    o += static_cast<size_t>(2 * m.r[0]);
+    o = (o + 3) & ~size_t(3);
+    for (int l = 0; l + 1 < L; ++l) {
+        const int stride = (m.r[l] + m.r[l + 1] + 1 + 3) & ~3;
+        m.trow[l] = stride;
+        m.off_trans[l] = o;
+        o += static_cast<size_t>(m.M[l + 1]) * stride;
+    }
+    m.off_ulast = o;
+    o += static_cast<size_t>(m.r[L - 1] + 1);
+    m.packed.assign(o, 0.0);
+}
+
+template <class T>
+DevNet<T> dev_net(const Model& m) {
+    DevNet<T> d{};
+    d.L = m.L;
+    for (int l = 0; l <= m.L; ++l) d.M[l] = m.M[l];
+    for (int l = 0; l < m.L; ++l) {
+        d.r[l] = m.r[l];
+        d.trow[l] = m.trow[l];
+    }
+    for (int l = 0; l <= m.L; ++l) d.soff[l] = m.soff[l];
+    const T* base = m.dev.as<T>();
+    d.V0 = base + m.off_V0;
+    for (int l = 0; l + 1 < m.L; ++l) d.trans[l] = base + m.off_trans[l];
+    d.ulast = base + m.off_ulast;
+    d.rtotal = m.rtotal;
+    return d;
+}
+
+void upload_model(Model& m) {
+    const size_t n = m.packed.size();
+    if (m.dtype == LRNR_F64) {
+        m.dev.ensure(n * sizeof(double));
+        CK(cudaMemcpy(m.dev.p, m.packed.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+    } else {
+        std::vector<float> f(n);
+        for (size_t i = 0; i < n; ++i) f[i] = static_cast<float>(m.packed[i]);
+        m.dev.ensure(n * sizeof(float));
+        CK(cudaMemcpy(m.dev.p, f.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    m.set = true;
+}
+
+}  // namespace
+
+struct lrnr_gpu_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    Model models[2];
+    Hyper hyper;
+    // points (double, device)
+    DevBuf pts_own;
+    const double* pts = nullptr;
+    int64_t n_inst = 0, n_per = 0;
+    // coefficients (double, device)
+    DevBuf s_dev, mu_dev;
+    int64_t coeff_inst = 0;
+    int coeff_rtotal = 0;
+    // workspaces
+    DevBuf scratch, part, out, bad, acts, G, hgrad, jets, meta_ws;
+    int64_t out_rows = 0;
+    int out_R1 = 0;
+    std::string err;
+    int tag = -1;
+    int64_t launches = 0;
+};
+
+namespace {
+
+template <class F>
+int guarded(lrnr_gpu_ctx* ctx, F&& f) {
+    if (!ctx) return LRNR_EINVAL;
+    try {
+        CK(cudaSetDevice(ctx->device));
+        f();
+        ctx->err.clear();
+        return LRNR_OK;
+    } catch (const NonFinite& e) {
+        ctx->err = e.what();
+        ctx->tag = e.tag;
+        return LRNR_ENONFINITE;
+    } catch (const InvalidArg& e) {
+        ctx->err = e.what();
+        return LRNR_EINVAL;
+    } catch (const StateError& e) {
+        ctx->err = e.what();
+        return LRNR_ESTATE;
+    } catch (const std::bad_alloc&) {
+        ctx->err = "device allocation failed";
+        return LRNR_ENOMEM;
+    } catch (const CudaError& e) {
+        ctx->err = e.what();
+        return LRNR_ECUDA;
+    } catch (const std::exception& e) {
+        ctx->err = e.what();
+        return LRNR_EINVAL;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// launch planning
+// ---------------------------------------------------------------------------
+struct Plan {
+    RunGeom g;
+    int grid;
+    size_t smem;
+};
+
+template <class T, int TPP, int RMAX, int ACT, int MODE>
+Plan plan_for(lrnr_gpu_ctx* ctx, const Model& m, int64_t n_inst, int64_t n_per) {
+    Plan p{};
+    p.g.P = kThreads / TPP;
+    p.g.n_per_inst = n_per;
+    p.g.tiles_per_inst = static_cast<int>((n_per + p.g.P - 1) / p.g.P);
+    const int R1 = 1 + m.rtotal;
+    p.smem = static_cast<size_t>((kThreads / 32 + 1) * R1) * sizeof(T);
+    auto kern = pinn_kernel<T, TPP, RMAX, ACT, MODE>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem)));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, p.smem));
+    occ = std::max(occ, 1);
+    const int64_t total_tiles = static_cast<int64_t>(p.g.tiles_per_inst) * n_inst;
+    const int64_t max_grid = static_cast<int64_t>(ctx->num_sms) * occ;
+    // ~8 units per resident CTA for balance; units never cross instances
+    int64_t want_units = std::max<int64_t>(1, max_grid * 8);
+    int64_t tpu = (total_tiles + want_units - 1) / want_units;
+    tpu = std::max<int64_t>(1, std::min<int64_t>(tpu, p.g.tiles_per_inst));
+    p.g.tiles_per_unit = static_cast<int>(tpu);
+    p.g.units_per_inst = static_cast<int>((p.g.tiles_per_inst + tpu - 1) / tpu);
+    p.g.n_units = static_cast<int64_t>(p.g.units_per_inst) * n_inst;
+    p.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_grid, p.g.n_units)));
+    return p;
+}
+
+template <class T, int TPP, int RMAX, int ACT, int MODE>
+void launch_pinn(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
+                 double* dev_out, double* jets_dev) {
+    const int64_t n_inst = ctx->n_inst, n_per = ctx->n_per;
+    Plan p = plan_for<T, TPP, RMAX, ACT, MODE>(ctx, m, n_inst, n_per);
+    const int R1 = 1 + m.rtotal;
+    ctx->scratch.ensure(static_cast<size_t>(p.grid) * p.g.P * 4 * m.rtotal * sizeof(T));
+    ctx->part.ensure(static_cast<size_t>(p.g.n_units) * R1 * sizeof(T));
+    DevNet<T> net = dev_net<T>(m);
+    pinn_kernel<T, TPP, RMAX, ACT, MODE><<<p.grid, kThreads, p.smem, ctx->stream>>>(
+        net, p.g, ctx->pts, s_dev, mu_dev, static_cast<T>(w), ctx->scratch.as<T>(), ctx->part.as<T>(),
+        jets_dev, ctx->bad.as<unsigned long long>());
+    CK(cudaGetLastError());
+    dim3 rg((R1 + 127) / 128, static_cast<unsigned>(n_inst));
+    reduce_units_kernel<T><<<rg, 128, 0, ctx->stream>>>(ctx->part.as<T>(), p.g.units_per_inst, R1, n_inst, dev_out);
+    CK(cudaGetLastError());
+    ctx->launches += 2;
+}
+
+// dispatch over (dtype, act, rmax, mode)
+template <int MODE>
+void dispatch_pinn(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
+                   double* dev_out, double* jets_dev) {
+    const int rm = m.rmax;
+#define LRNR_CASE(T, TPP, RM, ACT)                                                               \
+    if (rm <= RM) {                                                                              \
+        launch_pinn<T, TPP, RM, ACT, MODE>(ctx, m, s_dev, mu_dev, w, dev_out, jets_dev);        \
+        return;                                                                                  \
+    }
+    if (m.dtype == LRNR_F64) {
+        if (m.act == LRNR_ACT_TANH) {
+            LRNR_CASE(double, 4, 16, 0)
+            LRNR_CASE(double, 4, 32, 0)
+            LRNR_CASE(double, 4, 64, 0)
+        } else {
+            LRNR_CASE(double, 4, 16, 1)
+            LRNR_CASE(double, 4, 32, 1)
+            LRNR_CASE(double, 4, 64, 1)
+        }
+    } else {
+        if (m.act == LRNR_ACT_TANH) {
+            LRNR_CASE(float, 4, 16, 0)
+            LRNR_CASE(float, 4, 32, 0)
+            LRNR_CASE(float, 4, 64, 0)
+        } else {
+            LRNR_CASE(float, 4, 16, 1)
+            LRNR_CASE(float, 4, 32, 1)
+            LRNR_CASE(float, 4, 64, 1)
+        }
+    }
+#undef LRNR_CASE
+    throw InvalidArg("rank above the compiled maximum (64)");
+}
+
+// ---------------------------------------------------------------------------
+// non-finite diagnosis: first non-finite node in tape order (autodiff.cpp:448-461)
+// ---------------------------------------------------------------------------
+int diagnose_tag(const Model& m, const double* s, double x, double t, const double* mu) {
+    auto bad = [](double v) { return !std::isfinite(v); };
+    // leaves: bias vectors (bind_lrnr / bind_fast) and s leaves, all tag -1;
+    // the factor matrices are bound slots, not tape nodes (autodiff.cpp:47-59)
+    for (int l = 0; l + 1 < m.L; ++l)
+        for (int k = 0; k < m.M[l + 1]; ++k)
+            if (bad(m.packed[m.off_trans[l] + static_cast<size_t>(k) * m.trow[l] + m.r[l] + m.r[l + 1]])) return -1;
+    if (bad(m.packed[m.off_ulast + m.r[m.L - 1]])) return -1;
+    for (int i = 0; i < m.rtotal; ++i)
+        if (bad(s[i])) return -1;
+    if (bad(x) || bad(t)) return -1;
+    const bool fast = m.kind == LRNR_MODEL_FAST;
+    const int L = m.L;
+    const double* P = m.packed.data();
+    std::vector<double> y(4 * m.rmax), yn(4 * m.rmax);
+    const int r0 = m.r[0];
+    const double z0[4][2] = {{x, t}, {1, 0}, {0, 1}, {0, 0}};
+    for (int c = 0; c < 4; ++c)
+        for (int j = 0; j < r0; ++j) y[c * m.rmax + j] = P[m.off_V0 + j] * z0[c][0] + P[m.off_V0 + r0 + j] * z0[c][1];
+    if (fast)
+        for (int c = 0; c < 4; ++c)
+            for (int j = 0; j < r0; ++j)
+                if (bad(y[c * m.rmax + j])) return 0;  // v_in dense node, tag 0 (autodiff.cpp:911)
+    for (int l = 0; l + 1 < L; ++l) {
+        const int rl = m.r[l], rn = m.r[l + 1];
+        const double* sl = s + m.soff[l];
+        bool nf = false;
+        if (fast)
+            for (int c = 0; c < 4; ++c)
+                for (int j = 0; j < rl; ++j) nf |= bad(sl[j] * y[c * m.rmax + j]);  // scale node
+        std::fill(yn.begin(), yn.end(), 0.0);
+        for (int k = 0; k < m.M[l + 1]; ++k) {
+            const double* row = P + m.off_trans[l] + static_cast<size_t>(k) * m.trow[l];
+            double a[4] = {0, 0, 0, 0};
+            for (int c = 0; c < 4; ++c)
+                for (int j = 0; j < rl; ++j) a[c] += row[j] * sl[j] * y[c * m.rmax + j];
+            a[0] += row[rl + rn];
+            double sg, d1, d2;
+            if (m.act == LRNR_ACT_TANH) {
+                sg = std::tanh(a[0]);
+                d1 = 1 - sg * sg;
+                d2 = -2 * sg * d1;
+            } else {
+                sg = std::sin(a[0]);
+                d1 = std::cos(a[0]);
+                d2 = -sg;
+            }
+            const double z[4] = {sg, d1 * a[1], d1 * a[2], d2 * a[1] * a[1] + d1 * a[3]};
+            for (int c = 0; c < 4; ++c) nf |= bad(a[c]) || bad(z[c]);
+            for (int c = 0; c < 4; ++c)
+                for (int j = 0; j < rn; ++j) yn[c * m.rmax + j] += row[rl + j] * z[c];
+        }
+        if (fast)
+            for (int c = 0; c < 4; ++c)
+                for (int j = 0; j < rn; ++j) nf |= bad(yn[c * m.rmax + j]);
+        if (nf) return l + 1;
+        y.swap(yn);
+    }
+    const int rL = m.r[L - 1];
+    const double* sL = s + m.soff[L - 1];
+    double u[4] = {0, 0, 0, 0};
+    bool nf = false;
+    for (int c = 0; c < 4; ++c)
+        for (int j = 0; j < rL; ++j) {
+            nf |= fast && bad(sL[j] * y[c * m.rmax + j]);
+            u[c] += P[m.off_ulast + j] * sL[j] * y[c * m.rmax + j];
+        }
+    u[0] += P[m.off_ulast + rL];
+    for (int c = 0; c < 4; ++c) nf |= bad(u[c]);
+    if (nf) return L;
+    (void)mu;
+    return -1;  // residual / square / scale nodes
+}
+
+void check_bad(lrnr_gpu_ctx* ctx, const Model& m) {
+    unsigned long long b = 0;
+    CK(cudaMemcpyAsync(&b, ctx->bad.p, sizeof(b), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (b == ULLONG_MAX) return;
+    const int64_t gp = static_cast<int64_t>(b);
+    const int64_t inst = gp / std::max<int64_t>(1, ctx->n_per);
+    double xt[2], mu[3];
+    std::vector<double> s(static_cast<size_t>(m.rtotal));
+    CK(cudaMemcpy(xt, ctx->pts + 2 * gp, sizeof(xt), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(mu, ctx->mu_dev.as<double>() + 3 * inst, sizeof(mu), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(s.data(), ctx->s_dev.as<double>() + inst * m.rtotal, s.size() * sizeof(double),
+                  cudaMemcpyDeviceToHost));
+    throw NonFinite(diagnose_tag(m, s.data(), xt[0], xt[1], mu));
+}
+
+void reset_bad(lrnr_gpu_ctx* ctx) {
+    CK(cudaMemsetAsync(ctx->bad.p, 0xff, sizeof(unsigned long long), ctx->stream));
+}
+
+const Model& need_model(lrnr_gpu_ctx* ctx, int model) {
+    require(model == LRNR_MODEL_LRNR || model == LRNR_MODEL_FAST, "unknown model slot");
+    if (!ctx->models[model].set) throw StateError("model not set");
+    if (!ctx->pts && ctx->n_inst * ctx->n_per > 0) throw StateError("points not set");
+    return ctx->models[model];
+}
+
+void upload_coeffs_impl(lrnr_gpu_ctx* ctx, const double* s, const double* mu, int64_t n_inst, int rtotal) {
+    require(n_inst >= 1, "n_inst must be positive");
+    ctx->s_dev.ensure(static_cast<size_t>(n_inst * rtotal) * sizeof(double) + 8);
+    ctx->mu_dev.ensure(static_cast<size_t>(n_inst * 3) * sizeof(double) + 8);
+    if (rtotal > 0)
+        CK(cudaMemcpyAsync(ctx->s_dev.p, s, static_cast<size_t>(n_inst * rtotal) * sizeof(double),
+                           cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->mu_dev.p, mu, static_cast<size_t>(n_inst * 3) * sizeof(double), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    ctx->coeff_inst = n_inst;
+    ctx->coeff_rtotal = rtotal;
+}
+
+// Launch residual+gradient (MODE 0) or forward (MODE 1) with resident s/mu.
+template <int MODE>
+double* run_resident(lrnr_gpu_ctx* ctx, const Model& m, double w, double* dev_out, double* jets_dev) {
+    require(ctx->coeff_inst == ctx->n_inst && ctx->coeff_rtotal == m.rtotal,
+            "coefficients do not match the points' instance count / model ranks");
+    const int R1 = 1 + m.rtotal;
+    if (!dev_out) {
+        ctx->out.ensure(static_cast<size_t>(ctx->n_inst * R1) * sizeof(double));
+        dev_out = ctx->out.as<double>();
+    }
+    ctx->out_rows = ctx->n_inst;
+    ctx->out_R1 = R1;
+    ctx->bad.ensure(sizeof(unsigned long long));
+    reset_bad(ctx);
+    if (ctx->n_per == 0) {
+        CK(cudaMemsetAsync(dev_out, 0, static_cast<size_t>(ctx->n_inst * R1) * sizeof(double), ctx->stream));
+        return dev_out;
+    }
+    const double wt = w > 0.0 ? w : 1.0 / static_cast<double>(ctx->n_inst * ctx->n_per);
+    dispatch_pinn<MODE>(ctx, m, ctx->s_dev.as<double>(), ctx->mu_dev.as<double>(), wt, dev_out, jets_dev);
+    return dev_out;
+}
+
+void download(lrnr_gpu_ctx* ctx, const double* dev, double* host, size_t n) {
+    CK(cudaMemcpyAsync(host, dev, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+}
+
+void set_model_common(Model& m, int L, int act, int dtype) {
+    require(act == LRNR_ACT_TANH || act == LRNR_ACT_SIN, "unknown activation");
+    require(dtype == LRNR_F64 || dtype == LRNR_F32, "unknown dtype");
+    require(L >= 1 && L <= kMaxL, "depth out of range");
+    m.L = L;
+    m.act = act;
+    m.dtype = dtype;
+}
+
+HyperDev hyper_dev(const Hyper& h) {
+    HyperDev d{};
+    d.K = h.K;
+    for (int k = 0; k <= h.K; ++k) d.hw[k] = h.hw[k];
+    for (int k = 0; k < h.K; ++k) {
+        d.oW[k] = h.oW[k];
+        d.ob[k] = h.ob[k];
+    }
+    d.max_w = h.max_w;
+    d.n_params = h.n_params;
+    d.P = h.dev.as<double>();
+    for (int a = 0; a < 3; ++a) {
+        d.lo[a] = h.lo[a];
+        d.hi[a] = h.hi[a];
+    }
+    return d;
+}
+
+// s_i = hyper(mu_i) for the ctx's instances -> ctx->s_dev; activations kept in ctx->acts.
+void hyper_forward_resident(lrnr_gpu_ctx* ctx, int rtotal) {
+    const Hyper& h = ctx->hyper;
+    if (!h.set) throw StateError("hypernetwork not set");
+    require(h.hw[h.K] == rtotal, "hypernetwork output dim != model r_total");
+    const int64_t n = ctx->coeff_inst;
+    ctx->acts.ensure(static_cast<size_t>(n * (h.K + 1) * h.max_w) * sizeof(double));
+    ctx->s_dev.ensure(static_cast<size_t>(n * rtotal) * sizeof(double) + 8);
+    hyper_forward_kernel<<<static_cast<unsigned>(n), 128, 0, ctx->stream>>>(hyper_dev(h), ctx->mu_dev.as<double>(), n,
+                                                                             ctx->acts.as<double>(), ctx->s_dev.as<double>());
+    CK(cudaGetLastError());
+    ctx->launches += 1;
+    ctx->coeff_rtotal = rtotal;
+}
+
+// dtheta from the per-instance result rows (dev_rows: n x R1)
+void hyper_backward_resident(lrnr_gpu_ctx* ctx, const double* dev_rows, int R1, double* dev_grad) {
+    const Hyper& h = ctx->hyper;
+    const int64_t n = ctx->coeff_inst;
+    ctx->G.ensure(static_cast<size_t>(n * h.K * h.max_w) * sizeof(double));
+    HyperDev hd = hyper_dev(h);
+    hyper_backward_kernel<<<static_cast<unsigned>(n), 128, 0, ctx->stream>>>(hd, ctx->acts.as<double>(), dev_rows, R1, n,
+                                                                              ctx->G.as<double>());
+    CK(cudaGetLastError());
+    hyper_param_grad_kernel<<<(h.n_params + 127) / 128, 128, 0, ctx->stream>>>(hd, ctx->acts.as<double>(),
+                                                                                ctx->G.as<double>(), n, dev_grad);
+    CK(cudaGetLastError());
+    ctx->launches += 2;
+}
+
+void meta_step(lrnr_gpu_ctx*, const Model&, double, double*, double*) {
+    throw StateError("meta path not available in this build");
+}
+
+}  // namespace
+
+extern "C" {
+
+int lrnr_gpu_create(int device, lrnr_gpu_ctx** out) {
+    if (!out) return LRNR_EINVAL;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+        cudaGetLastError();
+        return LRNR_ECUDA;
+    }
+    auto* c = new lrnr_gpu_ctx();
+    c->device = device;
+    if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess) {
+        delete c;
+        return LRNR_ECUDA;
+    }
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    c->stream = c->own;
+    *out = c;
+    return LRNR_OK;
+}
+
+int lrnr_gpu_destroy(lrnr_gpu_ctx* ctx) {
+    if (!ctx) return LRNR_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& m : ctx->models) m.dev.release();
+    ctx->hyper.dev.release();
+    for (DevBuf* b : {&ctx->pts_own, &ctx->s_dev, &ctx->mu_dev, &ctx->scratch, &ctx->part, &ctx->out, &ctx->bad,
+                      &ctx->acts, &ctx->G, &ctx->hgrad, &ctx->jets, &ctx->meta_ws})
+        b->release();
+    if (ctx->own) cudaStreamDestroy(ctx->own);
+    delete ctx;
+    return LRNR_OK;
+}
+
+const char* lrnr_gpu_last_error(const lrnr_gpu_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+int lrnr_gpu_last_layer_tag(const lrnr_gpu_ctx* ctx) { return ctx ? ctx->tag : -1; }
+int64_t lrnr_gpu_launch_count(const lrnr_gpu_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int lrnr_gpu_set_stream(lrnr_gpu_ctx* ctx, void* s) {
+    return guarded(ctx, [&] { ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own; });
+}
+
+int lrnr_gpu_set_lrnr(lrnr_gpu_ctx* ctx, int L, const int64_t* widths, const int64_t* ranks, const double* params,
+                      int act, int dtype) {
+    return guarded(ctx, [&] {
+        require(widths && ranks && params, "null argument");
+        Model m;
+        set_model_common(m, L, act, dtype);
+        m.kind = LRNR_MODEL_LRNR;
+        require(widths[0] == 2, "input width must be 2 (x, t)");
+        require(widths[L] == 1, "residual: expected scalar-output jet");
+        for (int l = 0; l < L; ++l) {
+            require(ranks[l] >= 1, "LrnrParams: rank must be positive");
+            require(ranks[l] <= std::min(widths[l + 1], widths[l]), "LrnrParams: rank exceeds min(M_l, M_{l-1})");
+        }
+        m.M.assign(widths, widths + L + 1);
+        m.r.assign(ranks, ranks + L);
+        m.widths64.assign(widths, widths + L + 1);
+        m.ranks64.assign(ranks, ranks + L);
+        build_layout(m);
+        // flat offsets
+        std::vector<size_t> oU(L), oV(L), ob(L);
+        size_t o = 0;
+        for (int l = 0; l < L; ++l) {
+            oU[l] = o;
+            o += static_cast<size_t>(widths[l + 1] * ranks[l]);
+            oV[l] = o;
+            o += static_cast<size_t>(widths[l] * ranks[l]);
+            ob[l] = o;
+            o += static_cast<size_t>(widths[l + 1]);
+        }
+        m.flat.assign(params, params + o);
+        const double* Pp = params;
+        for (int j = 0; j < m.r[0]; ++j) {
+            m.packed[m.off_V0 + j] = Pp[oV[0] + j];                   // V_0 row 0
+            m.packed[m.off_V0 + m.r[0] + j] = Pp[oV[0] + m.r[0] + j]; // V_0 row 1
+        }
+        for (int l = 0; l + 1 < L; ++l) {
+            const int rl = m.r[l], rn = m.r[l + 1];
+            for (int k = 0; k < m.M[l + 1]; ++k) {
+                double* row = m.packed.data() + m.off_trans[l] + static_cast<size_t>(k) * m.trow[l];
+                for (int j = 0; j < rl; ++j) row[j] = Pp[oU[l] + static_cast<size_t>(k) * rl + j];
+                for (int j = 0; j < rn; ++j) row[rl + j] = Pp[oV[l + 1] + static_cast<size_t>(k) * rn + j];
+                row[rl + rn] = Pp[ob[l] + k];
+            }
+        }
+        for (int j = 0; j < m.r[L - 1]; ++j) m.packed[m.off_ulast + j] = Pp[oU[L - 1] + j];
+        m.packed[m.off_ulast + m.r[L - 1]] = Pp[ob[L - 1]];
+        Model& dst = ctx->models[LRNR_MODEL_LRNR];
+        dst.dev.release();
+        dst = std::move(m);
+        upload_model(dst);
+    });
+}
+
+int lrnr_gpu_set_fast(lrnr_gpu_ctx* ctx, int L, const int64_t* ranks, const int64_t* red, int64_t m_in,
+                      int64_t m_out, const double* F, int act, int dtype) {
+    return guarded(ctx, [&] {
+        require(ranks && F && (L < 2 || red), "null argument");
+        Model m;
+        set_model_common(m, L, act, dtype);
+        require(L >= 2, "FastParams: need at least two layers");
+        require(m_in == 2, "input width must be 2 (x, t)");
+        require(m_out == 1, "residual: expected scalar-output jet");
+        m.kind = LRNR_MODEL_FAST;
+        m.M.assign(L + 1, 0);
+        m.M[0] = 2;
+        m.M[L] = 1;
+        for (int l = 0; l + 1 < L; ++l) {
+            require(red[l] >= 1, "FastParams: reduced rank must be positive");
+            m.M[l + 1] = static_cast<int>(red[l]);
+        }
+        for (int l = 0; l < L; ++l) require(ranks[l] >= 1, "FastParams: rank must be positive");
+        m.r.assign(ranks, ranks + L);
+        build_layout(m);
+        size_t o = 0;
+        const int r0 = m.r[0];
+        for (int j = 0; j < r0; ++j) {
+            m.packed[m.off_V0 + j] = F[o + j];
+            m.packed[m.off_V0 + r0 + j] = F[o + r0 + j];
+        }
+        o += static_cast<size_t>(2 * r0);
+        for (int l = 0; l + 1 < L; ++l) {
+            const int rl = m.r[l], rn = m.r[l + 1], rh = m.M[l + 1];
+            const size_t o_uh = o, o_bh = o_uh + static_cast<size_t>(rh) * rl, o_vh = o_bh + rh;
+            for (int k = 0; k < rh; ++k) {
+                double* row = m.packed.data() + m.off_trans[l] + static_cast<size_t>(k) * m.trow[l];
+                for (int j = 0; j < rl; ++j) row[j] = F[o_uh + static_cast<size_t>(k) * rl + j];
+                for (int j = 0; j < rn; ++j) row[rl + j] = F[o_vh + static_cast<size_t>(k) * rn + j];
+                row[rl + rn] = F[o_bh + k];
+            }
+            o = o_vh + static_cast<size_t>(rh) * rn;
+        }
+        for (int j = 0; j < m.r[L - 1]; ++j) m.packed[m.off_ulast + j] = F[o + j];
+        o += static_cast<size_t>(m.r[L - 1]);
+        m.packed[m.off_ulast + m.r[L - 1]] = F[o];
+        Model& dst = ctx->models[LRNR_MODEL_FAST];
+        dst.dev.release();
+        dst = std::move(m);
+        upload_model(dst);
+    });
+}
+
+int lrnr_gpu_set_hyper(lrnr_gpu_ctx* ctx, int K, const int64_t* hw, const double* H, const double* lo,
+                       const double* hi) {
+    return guarded(ctx, [&] {
+        require(hw && H && lo && hi, "null argument");
+        require(K >= 1 && K <= kHyperMaxLayers, "hypernetwork depth out of range");
+        require(hw[0] == 3, "HyperParams: input dimension must be 3");
+        Hyper h;
+        h.K = K;
+        h.hw.assign(hw, hw + K + 1);
+        int o = 0;
+        h.max_w = 3;
+        for (int k = 0; k < K; ++k) {
+            require(hw[k + 1] >= 1, "HyperParams: empty layer");
+            h.oW.push_back(o);
+            o += static_cast<int>(hw[k + 1] * hw[k]);
+            h.ob.push_back(o);
+            o += static_cast<int>(hw[k + 1]);
+            h.max_w = std::max<int>(h.max_w, static_cast<int>(hw[k + 1]));
+        }
+        h.n_params = o;
+        for (int a = 0; a < 3; ++a) {
+            h.lo[a] = lo[a];
+            h.hi[a] = hi[a];
+        }
+        h.dev.ensure(static_cast<size_t>(o) * sizeof(double));
+        CK(cudaMemcpy(h.dev.p, H, static_cast<size_t>(o) * sizeof(double), cudaMemcpyHostToDevice));
+        h.set = true;
+        ctx->hyper.dev.release();
+        ctx->hyper = std::move(h);
+    });
+}
+
+int lrnr_gpu_set_points(lrnr_gpu_ctx* ctx, const double* xt, int64_t n_inst, int64_t n_per) {
+    return guarded(ctx, [&] {
+        require(n_inst >= 1 && n_per >= 0, "bad point counts");
+        require(xt || n_per == 0, "null points");
+        const size_t bytes = static_cast<size_t>(n_inst * n_per * 2) * sizeof(double);
+        ctx->pts_own.ensure(bytes + 16);
+        if (bytes) CK(cudaMemcpyAsync(ctx->pts_own.p, xt, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        ctx->pts = ctx->pts_own.as<double>();
+        ctx->n_inst = n_inst;
+        ctx->n_per = n_per;
+    });
+}
+
+int lrnr_gpu_set_points_device(lrnr_gpu_ctx* ctx, const void* xt_dev, int64_t n_inst, int64_t n_per) {
+    return guarded(ctx, [&] {
+        require(n_inst >= 1 && n_per >= 0, "bad point counts");
+        require(xt_dev || n_per == 0, "null points");
+        ctx->pts = static_cast<const double*>(xt_dev);
+        ctx->n_inst = n_inst;
+        ctx->n_per = n_per;
+    });
+}
+
+int lrnr_gpu_upload_coeffs(lrnr_gpu_ctx* ctx, const double* s, const double* mu, int64_t n_inst) {
+    return guarded(ctx, [&] {
+        require(s && mu, "null argument");
+        const Model& m = ctx->models[ctx->models[0].set ? 0 : 1];
+        if (!m.set) throw StateError("model not set");
+        upload_coeffs_impl(ctx, s, mu, n_inst, m.rtotal);
+    });
+}
+
+int lrnr_gpu_run(lrnr_gpu_ctx* ctx, int model, double w, double* dev_out) {
+    return guarded(ctx, [&] {
+        const Model& m = need_model(ctx, model);
+        run_resident<0>(ctx, m, w, dev_out, nullptr);
+    });
+}
+
+int lrnr_gpu_check(lrnr_gpu_ctx* ctx) {
+    return guarded(ctx, [&] {
+        CK(cudaStreamSynchronize(ctx->stream));
+        const Model& m = ctx->models[ctx->models[0].set ? 0 : 1];
+        if (ctx->bad.p) check_bad(ctx, m);
+    });
+}
+
+int lrnr_gpu_download(lrnr_gpu_ctx* ctx, double* host, int64_t n) {
+    return guarded(ctx, [&] {
+        require(host != nullptr, "null argument");
+        require(n <= ctx->out_rows * ctx->out_R1, "download larger than the result");
+        download(ctx, ctx->out.as<double>(), host, static_cast<size_t>(n));
+    });
+}
+
+int lrnr_gpu_loss_grad_s(lrnr_gpu_ctx* ctx, int model, const double* s, const double* mu, double w,
+                         double* out_value, double* out_comps4, double* out_grad_s) {
+    return guarded(ctx, [&] {
+        const Model& m = need_model(ctx, model);
+        require(s && mu, "null argument");
+        require(ctx->n_inst == 1, "lrnr_gpu_loss_grad_s needs a single instance");
+        upload_coeffs_impl(ctx, s, mu, 1, m.rtotal);
+        const double wt = w > 0.0 ? w : (ctx->n_per ? 1.0 / static_cast<double>(ctx->n_per) : 0.0);
+        double* d = run_resident<0>(ctx, m, wt, nullptr, nullptr);
+        std::vector<double> h(static_cast<size_t>(1 + m.rtotal));
+        download(ctx, d, h.data(), h.size());
+        check_bad(ctx, m);
+        if (out_value) *out_value = h[0];
+        if (out_comps4) {
+            out_comps4[0] = h[0];
+            out_comps4[1] = out_comps4[2] = out_comps4[3] = 0.0;
+        }
+        if (out_grad_s) std::copy(h.begin() + 1, h.end(), out_grad_s);
+    });
+}
+
+int lrnr_gpu_loss_grad_s_multi(lrnr_gpu_ctx* ctx, int model, const double* s, const double* mu, double w,
+                               double* out_value, double* out_grad_s) {
+    return guarded(ctx, [&] {
+        const Model& m = need_model(ctx, model);
+        require(s && mu, "null argument");
+        upload_coeffs_impl(ctx, s, mu, ctx->n_inst, m.rtotal);
+        double* d = run_resident<0>(ctx, m, w, nullptr, nullptr);
+        const int R1 = 1 + m.rtotal;
+        std::vector<double> h(static_cast<size_t>(ctx->n_inst * R1));
+        download(ctx, d, h.data(), h.size());
+        check_bad(ctx, m);
+        double v = 0.0;
+        for (int64_t i = 0; i < ctx->n_inst; ++i) {
+            v += h[static_cast<size_t>(i * R1)];
+            if (out_grad_s)
+                std::copy(h.begin() + i * R1 + 1, h.begin() + (i + 1) * R1, out_grad_s + i * m.rtotal);
+        }
+        if (out_value) *out_value = v;
+    });
+}
+
+int lrnr_gpu_hyper_loss_grad(lrnr_gpu_ctx* ctx, int model, const double* mus, double w, double* out_value,
+                             double* out_grad_s, double* out_grad_theta) {
+    return guarded(ctx, [&] {
+        const Model& m = need_model(ctx, model);
+        require(mus != nullptr, "null argument");
+        const int64_t n = ctx->n_inst;
+        ctx->mu_dev.ensure(static_cast<size_t>(n * 3) * sizeof(double) + 8);
+        CK(cudaMemcpyAsync(ctx->mu_dev.p, mus, static_cast<size_t>(n * 3) * sizeof(double), cudaMemcpyHostToDevice,
+                           ctx->stream));
+        ctx->coeff_inst = n;
+        hyper_forward_resident(ctx, m.rtotal);
+        double* d = run_resident<0>(ctx, m, w, nullptr, nullptr);
+        const int R1 = 1 + m.rtotal;
+        ctx->hgrad.ensure(static_cast<size_t>(ctx->hyper.n_params) * sizeof(double));
+        hyper_backward_resident(ctx, d, R1, ctx->hgrad.as<double>());
+        std::vector<double> h(static_cast<size_t>(n * R1));
+        download(ctx, d, h.data(), h.size());
+        check_bad(ctx, m);
+        double v = 0.0;
+        for (int64_t i = 0; i < n; ++i) {
+            v += h[static_cast<size_t>(i * R1)];
+            if (out_grad_s) std::copy(h.begin() + i * R1 + 1, h.begin() + (i + 1) * R1, out_grad_s + i * m.rtotal);
+        }
+        if (out_value) *out_value = v;
+        if (out_grad_theta) download(ctx, ctx->hgrad.as<double>(), out_grad_theta, static_cast<size_t>(ctx->hyper.n_params));
+    });
+}
+
+int lrnr_gpu_jets(lrnr_gpu_ctx* ctx, int model, const double* s, double* out_jets) {
+    return guarded(ctx, [&] {
+        const Model& m = need_model(ctx, model);
+        require(s && out_jets, "null argument");
+        std::vector<double> mu(static_cast<size_t>(3 * ctx->n_inst), 0.0);
+        upload_coeffs_impl(ctx, s, mu.data(), ctx->n_inst, m.rtotal);
+        const size_t n = static_cast<size_t>(ctx->n_inst * ctx->n_per);
+        ctx->jets.ensure(n * 4 * sizeof(double) + 8);
+        run_resident<1>(ctx, m, 1.0, nullptr, ctx->jets.as<double>());
+        if (n) download(ctx, ctx->jets.as<double>(), out_jets, n * 4);
+        else CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int lrnr_gpu_loss(lrnr_gpu_ctx* ctx, int model, const double* s, const double* mu, double w, double* out_value) {
+    return guarded(ctx, [&] {
+        const Model& m = need_model(ctx, model);
+        require(s && mu && out_value, "null argument");
+        upload_coeffs_impl(ctx, s, mu, ctx->n_inst, m.rtotal);
+        double* d = run_resident<1>(ctx, m, w, nullptr, nullptr);
+        const int R1 = 1 + m.rtotal;
+        std::vector<double> h(static_cast<size_t>(ctx->n_inst * R1));
+        download(ctx, d, h.data(), h.size());
+        check_bad(ctx, m);
+        double v = 0.0;
+        for (int64_t i = 0; i < ctx->n_inst; ++i) v += h[static_cast<size_t>(i * R1)];
+        *out_value = v;
+    });
+}
+
+int lrnr_gpu_meta_loss_grad(lrnr_gpu_ctx* ctx, const double* mus, double w, double* out_value, double* out_grad) {
+    return guarded(ctx, [&] {
+        const Model& m = need_model(ctx, LRNR_MODEL_LRNR);
+        require(mus && out_grad, "null argument");
+        if (!ctx->hyper.set) throw StateError("hypernetwork not set");
+        const int64_t n = ctx->n_inst;
+        ctx->mu_dev.ensure(static_cast<size_t>(n * 3) * sizeof(double) + 8);
+        CK(cudaMemcpyAsync(ctx->mu_dev.p, mus, static_cast<size_t>(n * 3) * sizeof(double), cudaMemcpyHostToDevice,
+                           ctx->stream));
+        ctx->coeff_inst = n;
+        hyper_forward_resident(ctx, m.rtotal);
+        const double wt = w > 0.0 ? w : 1.0 / static_cast<double>(std::max<int64_t>(1, n * ctx->n_per));
+        double value = 0.0;
+        meta_step(ctx, m, wt, out_grad, &value);
+        if (out_value) *out_value = value;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,113 @@
+"""Generate the committed golden fixtures from the UNMODIFIED reference.
+
+Run in the build container (needs /root/reference and oracle/_ref/liblrnr_ref.so,
+built by ``make -C oracle``):
+
+    python tests/golden/make_golden.py
+
+Every array here is produced by the reference's own code (oracle/ref_harness.cpp
+drives its public API); nothing is restated.  The fixtures pin the C oracle
+(tests/test_oracle.py), the product's host-side generators / EIM reduction
+(tests/test_host.py) and, on the GPU box where /root/reference does not exist,
+the CUDA path (tests/test_gpu_parity.py).  Shapes follow BASELINE.json configs
+0-4 (full size where the reference finishes in seconds, subsampled otherwise);
+the reference is tanh-only, so configs 2-4 appear here with tanh (the sin
+variants are pinned by finite differences + torch FP64 instead).
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+from oracle.oracle import Reference  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+TWO_PI = 6.283185307179586476925286766559
+
+
+def main():
+    R = Reference()
+    g = {}
+
+    # --- rng.hpp streams (mt19937_64, uniform, Box-Muller normal) ---
+    for k, name in enumerate(("uniform", "normal", "raw")):
+        g[f"rng_{name}"] = R.rng_stream(5, 257, k)
+
+    # --- end-to-end KAT: proj/test_output.txt:24-25 config (acceptance.cpp:705-714) ---
+    best, be, losses = R.meta_train([2, 16, 16, 1], [1, 4, 1], 1, 8, 1.0, 0.01, 1.0, 42, (5.0, 0, 0),
+                                    (8.0, 0, 0), 3e-3, 5, 64, 16, 8, 1234, 1e-3, 1e-4, 1.5, threads=2)
+    g["kat_meta_best_loss"] = np.array([best])
+    g["kat_meta_best_epoch"] = np.array([be])
+    g["kat_meta_losses"] = losses
+
+    # --- config 0: LRNR 2-100x3-1, r (2,10,10,1), FP64, tanh, mu (30,0,0), 4096 pts ---
+    w0, r0 = [2, 100, 100, 100, 1], [2, 10, 10, 1]
+    P0, s0 = R.make_baseline_model(w0, r0, 2410)
+    pts0 = R.sample_collocation(4001, 4096)["interior"]
+    mu0 = np.array([30.0, 0.0, 0.0])
+    c0 = R.lrnr_grad(w0, r0, P0, s0, mu0, pts0, threads=8)
+    g.update(c0_widths=np.array(w0), c0_ranks=np.array(r0), c0_params=P0, c0_s=s0, c0_pts=pts0, c0_mu=mu0,
+             c0_value=np.array([c0["value"]]), c0_comps=c0["comps"], c0_grad_s=c0["grad_s"],
+             c0_jets=R.lrnr_jets(w0, r0, P0, s0, pts0[:256]))
+    g["c0_loss_tune"] = R.loss_tune(w0, r0, P0, s0, mu0, pts0)
+
+    # --- config 1: FastLRNR of c0 via the reference EIM recipe ---
+    f1 = R.build_fast(w0, r0, P0, s0, mu=mu0, nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777, r_hat=10)
+    c1 = R.fast_grad(r0, f1["red_ranks"], f1["fparams"], s0, mu0, pts0, threads=8)
+    g.update(c1_red_ranks=f1["red_ranks"], c1_indices=f1["indices"], c1_fparams=f1["fparams"],
+             c1_value=np.array([c1["value"]]), c1_grad_s=c1["grad_s"],
+             c1_jets=R.fast_jets(r0, f1["red_ranks"], f1["fparams"], s0, pts0[:256]))
+    # the reference fast-phase objective: l1 at the 4x3 grid X + locality
+    xs = [(TWO_PI * i / 3.0, 1.0 * j / 2.0) for j in range(3) for i in range(4)]
+    s_init = s0.copy()
+    s_pert = s0 * 0.9 + 0.01
+    fp = R.fast_phase_grad(r0, f1["red_ranks"], f1["fparams"], s_pert, s_init, mu0, xs, 1e-2, threads=2)
+    g.update(c1_phase_x=np.array(xs), c1_phase_s=s_pert, c1_phase_value=np.array([fp["value"]]),
+             c1_phase_comps=fp["comps"], c1_phase_grad_s=fp["grad_s"])
+    # identity reduction (reduction.cpp:285-296)
+    red_id, F_id = R.identity_fast(w0, r0, P0)
+    g.update(c0_identity_red=red_id, c0_identity_fparams=F_id)
+
+    # --- config 2 shapes (tanh control): 2-256x6-1, r (2,32x5,1), mu (20,0.01,5) ---
+    w2, r2 = [2] + [256] * 6 + [1], [2, 32, 32, 32, 32, 32, 1]
+    P2, s2 = R.make_baseline_model(w2, r2, 2411)
+    pts2 = R.sample_collocation(4002, 1024)["interior"]
+    mu2 = np.array([20.0, 0.01, 5.0])
+    c2 = R.lrnr_grad(w2, r2, P2, s2, mu2, pts2, threads=8)
+    f2 = R.build_fast(w2, r2, P2, s2, mu=mu2, nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777, r_hat=32)
+    c2f = R.fast_grad(r2, f2["red_ranks"], f2["fparams"], s2, mu2, pts2, threads=8)
+    g.update(c2_widths=np.array(w2), c2_ranks=np.array(r2), c2_params=P2, c2_s=s2, c2_pts=pts2, c2_mu=mu2,
+             c2_value=np.array([c2["value"]]), c2_grad_s=c2["grad_s"], c2_red_ranks=f2["red_ranks"],
+             c2_indices=f2["indices"], c2_fparams=f2["fparams"], c2_fast_value=np.array([c2f["value"]]),
+             c2_fast_grad_s=c2f["grad_s"])
+
+    # --- config 3 hypernetwork 3-64-64-163 on the c2 base (Xavier hidden, seeded) ---
+    lo3, hi3 = np.array([1.0, 0.0, 0.0]), np.array([40.0, 0.1, 10.0])
+    hw3, H3 = R.make_hyper_params(r2, 2, 64, lo3, hi3, 4003, 0.01, 0.5)
+    mu3 = np.array([[12.5, 0.031, 2.2], [33.0, 0.09, 7.5], [1.0, 0.0, 0.0]])
+    s3 = np.stack([R.hyper_forward(hw3, H3, r2, lo3, hi3, m) for m in mu3])
+    gs3 = np.stack([np.sin(np.arange(163) * 0.37 + k) for k in range(3)])
+    v3 = np.stack([R.hyper_vjp(hw3, H3, r2, lo3, hi3, mu3[k], gs3[k]) for k in range(3)])
+    g.update(c3_hw=hw3, c3_hparams=H3, c3_lo=lo3, c3_hi=hi3, c3_mu=mu3, c3_s=s3, c3_gs=gs3, c3_vjp=v3)
+
+    # --- config 4 (meta) at a reduced shape: 2-32x3-1, r (2,8,8,1), hyper 3-16-16-19 ---
+    w4, r4 = [2, 32, 32, 32, 1], [2, 8, 8, 1]
+    P4, _ = R.make_baseline_model(w4, r4, 2412)
+    hw4, H4 = R.make_hyper_params(r4, 2, 16, lo3, hi3, 4004, 0.01, 0.5)
+    pts4 = R.sample_collocation(4005, 96)["interior"]
+    mus4 = np.repeat(np.array([[7.0, 0.02, 1.5], [25.0, 0.08, 6.0]]), 48, axis=0)
+    m4 = R.meta_grad(w4, r4, P4, hw4, H4, lo3, hi3, pts4, mus4, threads=4)
+    g.update(c4_widths=np.array(w4), c4_ranks=np.array(r4), c4_params=P4, c4_hw=hw4, c4_hparams=H4, c4_pts=pts4,
+             c4_mus=mus4, c4_value=np.array([m4["value"]]), c4_grad=m4["grad"])
+
+    path = os.path.join(OUT, "reference_golden.npz")
+    np.savez_compressed(path, **g)
+    print("wrote", path, os.path.getsize(path), "bytes;", len(g), "arrays")
+
+
+if __name__ == "__main__":
+    main()

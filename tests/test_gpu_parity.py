@@ -1,0 +1,259 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the C oracle, on seeded inputs; size-independent properties at
+BASELINE.json's full sizes.
+
+Tolerances (BASELINE.json north_star / SURVEY 8(c1)):
+  FP64 (configs 0, 1): floor-relative <= 1e-10 on dL/ds, loss <= 1e-12 relative.
+  FP32 (configs 2, 3): normwise <= 1e-4 on dL/ds (and dL/dtheta); loss <= 1e-4 relative.
+"""
+import numpy as np
+import pytest
+
+import paper_2410_04001_b200 as pkg
+from conftest import floor_rel, normwise
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-10
+TOL32_NORM = 1e-4
+TOL32_LOSS = 1e-4
+
+
+def lrnr_from_golden(g, prefix, act=pkg.ACT_TANH):
+    return pkg.LrnrParams(g[prefix + "_widths"], g[prefix + "_ranks"], g[prefix + "_params"], act)
+
+
+# ----------------------------------------------------------------------------
+# config 0 / 1 (FP64) against the reference's own outputs
+# ----------------------------------------------------------------------------
+def test_c0_lrnr_fp64_matches_reference(gpu, golden):
+    m = lrnr_from_golden(golden, "c0")
+    gpu.set_lrnr(m, pkg.F64)
+    gpu.set_points(golden["c0_pts"])
+    r = gpu.loss_grad_s(pkg.MODEL_LRNR, golden["c0_s"], golden["c0_mu"])
+    assert abs(r["value"] - golden["c0_value"][0]) <= 1e-12 * abs(golden["c0_value"][0])
+    assert floor_rel(r["grad_s"], golden["c0_grad_s"]) <= TOL64
+    np.testing.assert_allclose(r["comps"], golden["c0_comps"], rtol=1e-12, atol=0)
+
+
+def test_c1_fast_fp64_matches_reference(gpu, golden):
+    f = pkg.FastParams(golden["c0_ranks"], golden["c1_red_ranks"], golden["c1_fparams"], pkg.ACT_TANH)
+    gpu.set_fast(f, pkg.F64)
+    gpu.set_points(golden["c0_pts"])
+    r = gpu.loss_grad_s(pkg.MODEL_FAST, golden["c0_s"], golden["c0_mu"])
+    assert abs(r["value"] - golden["c1_value"][0]) <= 1e-12 * abs(golden["c1_value"][0])
+    assert floor_rel(r["grad_s"], golden["c1_grad_s"]) <= TOL64
+    # the paper's approximation metric: FastLRNR vs full-LRNR gradient
+    rel = normwise(r["grad_s"], golden["c0_grad_s"])
+    assert 0.0 < rel < 1.0
+
+
+def test_c0_jets_match_reference(gpu, golden):
+    m = lrnr_from_golden(golden, "c0")
+    gpu.set_lrnr(m, pkg.F64)
+    gpu.set_points(golden["c0_pts"][:256])
+    j = gpu.jets(pkg.MODEL_LRNR, golden["c0_s"])
+    np.testing.assert_allclose(j, golden["c0_jets"], rtol=1e-12, atol=1e-13)
+    f = pkg.FastParams(golden["c0_ranks"], golden["c1_red_ranks"], golden["c1_fparams"], pkg.ACT_TANH)
+    gpu.set_fast(f, pkg.F64)
+    jf = gpu.jets(pkg.MODEL_FAST, golden["c0_s"])
+    np.testing.assert_allclose(jf, golden["c1_jets"], rtol=1e-12, atol=1e-13)
+
+
+def test_c0_loss_only_matches_loss_tune(gpu, golden):
+    m = lrnr_from_golden(golden, "c0")
+    gpu.set_lrnr(m, pkg.F64)
+    gpu.set_points(golden["c0_pts"])
+    v = gpu.loss(pkg.MODEL_LRNR, golden["c0_s"], golden["c0_mu"])
+    assert abs(v - golden["c0_loss_tune"][0]) <= 1e-12 * abs(golden["c0_loss_tune"][0])
+
+
+def test_identity_reduction_equals_lrnr(gpu, golden):
+    """FastLRNR == LRNR under the identity reduction (test_model.cpp:298-315)."""
+    m = lrnr_from_golden(golden, "c0")
+    f = pkg.FastParams(golden["c0_ranks"], golden["c0_identity_red"], golden["c0_identity_fparams"], pkg.ACT_TANH)
+    gpu.set_lrnr(m, pkg.F64)
+    gpu.set_fast(f, pkg.F64)
+    gpu.set_points(golden["c0_pts"][:512])
+    a = gpu.loss_grad_s(pkg.MODEL_LRNR, golden["c0_s"], golden["c0_mu"])
+    b = gpu.loss_grad_s(pkg.MODEL_FAST, golden["c0_s"], golden["c0_mu"])
+    assert abs(a["value"] - b["value"]) <= 1e-12 * abs(a["value"])
+    assert floor_rel(b["grad_s"], a["grad_s"]) <= 1e-10
+
+
+# ----------------------------------------------------------------------------
+# config 2 shapes (FP32): tanh against the reference, sin against the oracle
+# ----------------------------------------------------------------------------
+def test_c2_tanh_fp32_matches_reference(gpu, golden):
+    m = lrnr_from_golden(golden, "c2")
+    gpu.set_lrnr(m, pkg.F32)
+    gpu.set_points(golden["c2_pts"])
+    r = gpu.loss_grad_s(pkg.MODEL_LRNR, golden["c2_s"], golden["c2_mu"])
+    assert abs(r["value"] - golden["c2_value"][0]) <= TOL32_LOSS * abs(golden["c2_value"][0])
+    assert normwise(r["grad_s"], golden["c2_grad_s"]) <= TOL32_NORM
+    f = pkg.FastParams(golden["c2_ranks"], golden["c2_red_ranks"], golden["c2_fparams"], pkg.ACT_TANH)
+    gpu.set_fast(f, pkg.F32)
+    rf = gpu.loss_grad_s(pkg.MODEL_FAST, golden["c2_s"], golden["c2_mu"])
+    # the EIM interpolation blocks amplify FP32 rounding (V_hat = (P^T Xi)^-T ...): loss to 1e-4
+    assert abs(rf["value"] - golden["c2_fast_value"][0]) <= TOL32_LOSS * abs(golden["c2_fast_value"][0])
+    assert normwise(rf["grad_s"], golden["c2_fast_grad_s"]) <= TOL32_NORM
+
+
+@pytest.mark.parametrize("dtype", [pkg.F32, pkg.F64])
+def test_c2_sin_matches_oracle(gpu, oracle, dtype):
+    c = pkg.config2(n_points=2048, act=pkg.ACT_SIN)
+    m, f = c["model"], c["fast"]
+    gpu.set_lrnr(m, dtype)
+    gpu.set_fast(f, dtype)
+    gpu.set_points(c["pts"])
+    want = oracle.lrnr_grad(m.widths, m.ranks, m.params, c["s"], c["mu"], c["pts"], act=pkg.ACT_SIN)
+    got = gpu.loss_grad_s(pkg.MODEL_LRNR, c["s"], c["mu"])
+    wantf = oracle.fast_grad(f.ranks, f.red_ranks, f.fparams, c["s"], c["mu"], c["pts"], act=pkg.ACT_SIN)
+    gotf = gpu.loss_grad_s(pkg.MODEL_FAST, c["s"], c["mu"])
+    if dtype == pkg.F64:
+        assert abs(got["value"] - want["value"]) <= 1e-12 * abs(want["value"])
+        assert floor_rel(got["grad_s"], want["grad_s"]) <= TOL64
+        assert floor_rel(gotf["grad_s"], wantf["grad_s"]) <= TOL64
+    else:
+        assert abs(got["value"] - want["value"]) <= TOL32_LOSS * abs(want["value"])
+        assert normwise(got["grad_s"], want["grad_s"]) <= TOL32_NORM
+        assert normwise(gotf["grad_s"], wantf["grad_s"]) <= TOL32_NORM
+
+
+# ----------------------------------------------------------------------------
+# config 3: hypernetwork -> FastLRNR per instance + hypernet VJP
+# ----------------------------------------------------------------------------
+def test_c3_hyper_fast_matches_oracle(gpu, oracle):
+    n_inst, per = 6, 333
+    c = pkg.config3(n_inst=n_inst, pts_per_inst=per, act=pkg.ACT_SIN)
+    f, h = c["fast"], c["hyper"]
+    gpu.set_fast(f, pkg.F32)
+    gpu.set_hyper(h)
+    gpu.set_points(c["pts"], n_inst=n_inst)
+    got = gpu.hyper_loss_grad(pkg.MODEL_FAST, c["mus"])
+    w = 1.0 / (n_inst * per)
+    val = 0.0
+    gth = np.zeros(h.n_params)
+    for i in range(n_inst):
+        s_i = oracle.hyper_forward(h.hw, h.params, h.lo, h.hi, c["mus"][i])
+        r = oracle.fast_grad(f.ranks, f.red_ranks, f.fparams, s_i, c["mus"][i], c["pts"][i * per:(i + 1) * per], w=w,
+                             act=pkg.ACT_SIN)
+        val += r["value"]
+        assert normwise(got["grad_s"][i], r["grad_s"]) <= TOL32_NORM
+        oracle.hyper_vjp(h.hw, h.params, h.lo, h.hi, c["mus"][i], r["grad_s"], out=gth)
+    assert abs(got["value"] - val) <= TOL32_LOSS * abs(val)
+    assert normwise(got["grad_theta"], gth) <= TOL32_NORM
+
+
+def test_hyper_forward_vjp_match_reference(gpu, golden):
+    """Hypernetwork forward + VJP (c3 shape) against the reference (FP64 path)."""
+    split = golden["c2_ranks"]
+    h = pkg.HyperParams(golden["c3_hw"], golden["c3_hparams"], golden["c3_lo"], golden["c3_hi"])
+    # identity-like use: a FastLRNR whose gradient we replace is not needed; check through the c3 call with a
+    # constant-residual-free probe: compare s via jets of a 1-point problem is indirect, so use loss_grad with
+    # the identity of hyper_forward through the multi path instead.
+    f = pkg.FastParams(golden["c2_ranks"], golden["c2_red_ranks"], golden["c2_fparams"], pkg.ACT_TANH)
+    gpu.set_fast(f, pkg.F64)
+    gpu.set_hyper(h)
+    mus = golden["c3_mu"]
+    pts = np.tile(golden["c2_pts"][:64], (len(mus), 1))
+    gpu.set_points(pts, n_inst=len(mus))
+    got = gpu.hyper_loss_grad(pkg.MODEL_FAST, mus)
+    # per-instance s must equal the reference's hyper_forward: check via the multi path with those s
+    gm = gpu.loss_grad_s_multi(pkg.MODEL_FAST, golden["c3_s"], mus)
+    np.testing.assert_allclose(got["grad_s"], gm["grad_s"], rtol=1e-12, atol=1e-15)
+    assert abs(got["value"] - gm["value"]) <= 1e-13 * abs(gm["value"])
+    assert split.sum() == golden["c3_s"].shape[1]
+
+
+# ----------------------------------------------------------------------------
+# edge cases (empty / ragged / single point / non-finite), determinism
+# ----------------------------------------------------------------------------
+def test_empty_batch_returns_zeros(gpu, golden):
+    m = lrnr_from_golden(golden, "c0")
+    gpu.set_lrnr(m, pkg.F64)
+    gpu.set_points(np.zeros((0, 2)))
+    r = gpu.loss_grad_s(pkg.MODEL_LRNR, golden["c0_s"], golden["c0_mu"])
+    assert r["value"] == 0.0 and not r["grad_s"].any()
+
+
+@pytest.mark.parametrize("n", [1, 31, 33, 97, 1000])
+def test_ragged_sizes_match_oracle(gpu, oracle, golden, n):
+    m = lrnr_from_golden(golden, "c0")
+    gpu.set_lrnr(m, pkg.F64)
+    pts = golden["c0_pts"][:n]
+    gpu.set_points(pts)
+    got = gpu.loss_grad_s(pkg.MODEL_LRNR, golden["c0_s"], golden["c0_mu"])
+    want = oracle.lrnr_grad(m.widths, m.ranks, m.params, golden["c0_s"], golden["c0_mu"], pts)
+    assert abs(got["value"] - want["value"]) <= 1e-12 * abs(want["value"])
+    assert floor_rel(got["grad_s"], want["grad_s"]) <= TOL64
+
+
+def test_nonfinite_maps_to_nonfinite_error(gpu, golden):
+    m = lrnr_from_golden(golden, "c0")
+    P = m.params.copy()
+    widths, ranks = m.widths, m.ranks
+    # poison the layer-2 bias (b_1): a_2 becomes inf -> AffineFactoredJet tag 2 ... but b leaves come first
+    # in tape order, so the reference reports -1 (leaf); poison U_1 instead -> first bad node is layer 2.
+    o = 0
+    for l in range(1):
+        o += widths[l + 1] * ranks[l] + widths[l] * ranks[l] + widths[l + 1]
+    P[o] = np.inf  # U_1[0,0]
+    gpu.set_lrnr(pkg.LrnrParams(widths, ranks, P), pkg.F64)
+    gpu.set_points(golden["c0_pts"][:64])
+    with pytest.raises(pkg.NonFiniteError) as ei:
+        gpu.loss_grad_s(pkg.MODEL_LRNR, golden["c0_s"], golden["c0_mu"])
+    assert ei.value.layer_tag == 2
+
+
+def test_nonfinite_leaf_reports_minus_one(gpu, golden):
+    m = lrnr_from_golden(golden, "c0")
+    gpu.set_lrnr(m, pkg.F64)
+    gpu.set_points(golden["c0_pts"][:64])
+    s = golden["c0_s"].copy()
+    s[3] = np.nan
+    with pytest.raises(pkg.NonFiniteError) as ei:
+        gpu.loss_grad_s(pkg.MODEL_LRNR, s, golden["c0_mu"])
+    assert ei.value.layer_tag == -1
+
+
+def test_bitwise_deterministic(gpu, golden):
+    m = lrnr_from_golden(golden, "c2")
+    gpu.set_lrnr(m, pkg.F32)
+    gpu.set_points(golden["c2_pts"])
+    a = gpu.loss_grad_s(pkg.MODEL_LRNR, golden["c2_s"], golden["c2_mu"])
+    b = gpu.loss_grad_s(pkg.MODEL_LRNR, golden["c2_s"], golden["c2_mu"])
+    assert a["value"] == b["value"] and np.array_equal(a["grad_s"], b["grad_s"])
+
+
+def test_invalid_shapes_raise_value_error(gpu):
+    bad = pkg.LrnrParams(np.array([2, 4, 1]), np.array([3, 1]), np.zeros(100))
+    with pytest.raises(ValueError):
+        gpu.set_lrnr(bad, pkg.F64)
+
+
+# ----------------------------------------------------------------------------
+# full BASELINE size (config 2, 1M points): size-independent properties
+# ----------------------------------------------------------------------------
+@pytest.mark.slow
+def test_c2_full_size_linearity_and_subsample(gpu, oracle):
+    c = pkg.config2(n_points=1 << 20, act=pkg.ACT_SIN, with_fast=False)
+    m = c["model"]
+    n = c["pts"].shape[0]
+    gpu.set_lrnr(m, pkg.F32)
+    gpu.set_points(c["pts"])
+    full = gpu.loss_grad_s(pkg.MODEL_LRNR, c["s"], c["mu"], w=1.0 / n)
+    # linearity over a disjoint split: L(all) = L(A) + L(B), grad likewise (same weight 1/n)
+    h = n // 2
+    gpu.set_points(c["pts"][:h])
+    a = gpu.loss_grad_s(pkg.MODEL_LRNR, c["s"], c["mu"], w=1.0 / n)
+    gpu.set_points(c["pts"][h:])
+    b = gpu.loss_grad_s(pkg.MODEL_LRNR, c["s"], c["mu"], w=1.0 / n)
+    assert abs(full["value"] - (a["value"] + b["value"])) <= 1e-6 * abs(full["value"])
+    assert normwise(full["grad_s"], a["grad_s"] + b["grad_s"]) <= 1e-5
+    # a strided 1/256 subsample of the full batch against the FP64 oracle
+    sub = c["pts"][::256]
+    gpu.set_points(sub)
+    got = gpu.loss_grad_s(pkg.MODEL_LRNR, c["s"], c["mu"])
+    want = oracle.lrnr_grad(m.widths, m.ranks, m.params, c["s"], c["mu"], sub, act=pkg.ACT_SIN)
+    assert normwise(got["grad_s"], want["grad_s"]) <= TOL32_NORM
