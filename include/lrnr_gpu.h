@@ -158,6 +158,10 @@ int lrnr_gpu_check(lrnr_gpu_ctx* ctx);
 /* Copy the context's result buffer (n_inst x (1 + r_total) doubles) to host. */
 int lrnr_gpu_download(lrnr_gpu_ctx* ctx, double* host_out, int64_t n_doubles);
 
+/* Achievable FMA-pipe rate of this device (dtype LRNR_F32 / LRNR_F64), TFLOP/s,
+ * from a full-chip independent-chain FMA kernel; the roofline denominator. */
+int lrnr_gpu_fma_peak(lrnr_gpu_ctx* ctx, int dtype, double* out_tflops);
+
 /* ---- host-side setup (no GPU needed; reference reduction.cpp / model.cpp) ---- */
 /* BASELINE config generator: make_lrnr_params(orthonormal,
  * bias 0) from Rng(seed), then b <- 0.1*normal(), s <- U[0,1] sorted descending. */

@@ -18,6 +18,7 @@ EXPORTS = (
     "lrnr_gpu_set_hyper", "lrnr_gpu_set_points", "lrnr_gpu_set_points_device", "lrnr_gpu_loss_grad_s",
     "lrnr_gpu_loss_grad_s_multi", "lrnr_gpu_hyper_loss_grad", "lrnr_gpu_meta_loss_grad", "lrnr_gpu_jets",
     "lrnr_gpu_loss", "lrnr_gpu_upload_coeffs", "lrnr_gpu_run", "lrnr_gpu_check", "lrnr_gpu_download",
+    "lrnr_gpu_fma_peak",
     "lrnr_host_make_baseline_model", "lrnr_host_make_hyper_params", "lrnr_host_sample_collocation",
     "lrnr_host_build_fast",
 )
@@ -61,6 +62,7 @@ def load() -> C.CDLL:
     lib.lrnr_gpu_run.argtypes = [vp, ip, C.c_double, vp]
     lib.lrnr_gpu_check.argtypes = [vp]
     lib.lrnr_gpu_download.argtypes = [vp, dp, i64]
+    lib.lrnr_gpu_fma_peak.argtypes = [vp, ip, dp]
     lib.lrnr_host_make_baseline_model.argtypes = [ip, dp, dp, C.c_uint64, dp, dp]
     lib.lrnr_host_make_hyper_params.argtypes = [ip, dp, ip, ip, C.c_uint64, C.c_double, C.c_double, dp]
     lib.lrnr_host_sample_collocation.argtypes = [C.c_uint64, i64, dp, dp, ip, dp, dp]

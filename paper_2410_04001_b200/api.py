@@ -295,6 +295,11 @@ class GpuContext:
                  "loss")
         return v.value
 
+    def fma_peak_tflops(self, dtype=F32):
+        v = C.c_double(0.0)
+        self._rc(self.lib.lrnr_gpu_fma_peak(self.h, dtype, C.byref(v)), "fma_peak")
+        return v.value
+
     # --- device-resident step ---
     def upload_coeffs(self, s, mu, n_inst=1):
         self._rc(self.lib.lrnr_gpu_upload_coeffs(self.h, _p(_f64(s)), _p(_f64(mu)), n_inst), "upload_coeffs")

@@ -507,6 +507,27 @@ void hyper_backward_resident(lrnr_gpu_ctx* ctx, const double* dev_rows, int R1, 
     ctx->launches += 2;
 }
 
+// FMA-pipe calibration: 16 independent 3-register FMA chains per thread,
+// full-chip grid.  Gives the achievable FP32/FP64 FMA rate the roofline is
+// compared against (MEASURED_PEAKS.json carries only HBM and bf16 tensor).
+template <typename T>
+__global__ void __launch_bounds__(256) fma_peak_kernel(T* out, int iters, T b) {
+    T acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = T(threadIdx.x + i);
+    T a = T(blockIdx.x) * T(1e-7);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = fma(acc[i], a, b);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = fma(acc[i], b, a);
+    }
+    T s = T(0);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s += acc[i];
+    if (s == T(12345.678)) out[0] = s;
+}
+
 void meta_step(lrnr_gpu_ctx*, const Model&, double, double*, double*) {
     throw StateError("meta path not available in this build");
 }
@@ -860,6 +881,36 @@ int lrnr_gpu_meta_loss_grad(lrnr_gpu_ctx* ctx, const double* mus, double w, doub
         double value = 0.0;
         meta_step(ctx, m, wt, out_grad, &value);
         if (out_value) *out_value = value;
+    });
+}
+
+int lrnr_gpu_fma_peak(lrnr_gpu_ctx* ctx, int dtype, double* out_tflops) {
+    return guarded(ctx, [&] {
+        require(out_tflops != nullptr, "null argument");
+        const int blocks = ctx->num_sms * 8, threads = 256;
+        const int iters = dtype == LRNR_F64 ? 2048 : 8192;
+        DevBuf o;
+        o.ensure(16);
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        float ms = 0.f;
+        for (int rep = 0; rep < 3; ++rep) {
+            CK(cudaEventRecord(e0, ctx->stream));
+            if (dtype == LRNR_F64)
+                fma_peak_kernel<double><<<blocks, threads, 0, ctx->stream>>>(o.as<double>(), iters, 0.999);
+            else
+                fma_peak_kernel<float><<<blocks, threads, 0, ctx->stream>>>(o.as<float>(), iters, 0.999f);
+            CK(cudaGetLastError());
+            CK(cudaEventRecord(e1, ctx->stream));
+            CK(cudaEventSynchronize(e1));
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        o.release();
+        const double flops = 2.0 * 32.0 * iters * static_cast<double>(blocks) * threads;
+        *out_tflops = flops / (ms * 1e-3) / 1e12;
     });
 }
 
