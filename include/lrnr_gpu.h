@@ -80,6 +80,13 @@ int lrnr_gpu_last_layer_tag(const lrnr_gpu_ctx* ctx);
 /* Use a caller-owned cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
  * NULL restores the context's own stream. */
 int lrnr_gpu_set_stream(lrnr_gpu_ctx* ctx, void* cuda_stream);
+/* Options.  LRNR_OPT_FAST_SINCOS (FP32 sin networks): 1 = sin/cos from the SFU
+ * approximations after a Cody-Waite reduction (~1e-6 absolute), 0 = libdevice
+ * sincosf (default).  LRNR_OPT_KERNEL: 0 = tile-GEMM kernel v2 where the shape
+ * allows (ranks <= 64), 1 = force the per-point streaming kernel v1. */
+#define LRNR_OPT_FAST_SINCOS 1
+#define LRNR_OPT_KERNEL 2
+int lrnr_gpu_set_option(lrnr_gpu_ctx* ctx, int opt, int value);
 /* Number of kernels this context has launched so far (instrumentation). */
 int64_t lrnr_gpu_launch_count(const lrnr_gpu_ctx* ctx);
 
@@ -98,8 +105,8 @@ int lrnr_gpu_set_hyper(lrnr_gpu_ctx* ctx, int n_layers, const int64_t* hw, const
 
 /* ---- collocation points (CollocationBatch::interior, pde.hpp:33-40) ----
  * n_inst groups of n_per_inst consecutive (x, t) pairs; group i belongs to
- * PDE-parameter instance i.  Host pointer (copied) or device pointer of the
- * context's dtype (borrowed; must stay valid while used). */
+ * PDE-parameter instance i.  Host pointer (copied) or device pointer to the
+ * same double (x, t) pairs (borrowed; must stay valid while used). */
 int lrnr_gpu_set_points(lrnr_gpu_ctx* ctx, const double* xt, int64_t n_inst, int64_t n_per_inst);
 int lrnr_gpu_set_points_device(lrnr_gpu_ctx* ctx, const void* xt_dev, int64_t n_inst,
                                int64_t n_per_inst);

@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(PKG, "liblrnr_gpu.so")
 # every symbol include/lrnr_gpu.h declares
 EXPORTS = (
     "lrnr_gpu_create", "lrnr_gpu_destroy", "lrnr_gpu_last_error", "lrnr_gpu_last_layer_tag",
-    "lrnr_gpu_set_stream", "lrnr_gpu_launch_count", "lrnr_gpu_set_lrnr", "lrnr_gpu_set_fast",
+    "lrnr_gpu_set_stream", "lrnr_gpu_set_option", "lrnr_gpu_launch_count", "lrnr_gpu_set_lrnr", "lrnr_gpu_set_fast",
     "lrnr_gpu_set_hyper", "lrnr_gpu_set_points", "lrnr_gpu_set_points_device", "lrnr_gpu_loss_grad_s",
     "lrnr_gpu_loss_grad_s_multi", "lrnr_gpu_hyper_loss_grad", "lrnr_gpu_meta_loss_grad", "lrnr_gpu_jets",
     "lrnr_gpu_loss", "lrnr_gpu_upload_coeffs", "lrnr_gpu_run", "lrnr_gpu_check", "lrnr_gpu_download",
@@ -27,6 +27,7 @@ LRNR_OK, LRNR_EINVAL, LRNR_ENONFINITE, LRNR_ECUDA, LRNR_ENOMEM, LRNR_ESTATE = ra
 ACT_TANH, ACT_SIN = 0, 1
 F64, F32 = 0, 1
 MODEL_LRNR, MODEL_FAST = 0, 1
+OPT_FAST_SINCOS, OPT_KERNEL = 1, 2
 
 _lib = None
 
@@ -45,6 +46,7 @@ def load() -> C.CDLL:
     lib.lrnr_gpu_last_error.restype = C.c_char_p
     lib.lrnr_gpu_last_layer_tag.argtypes = [vp]
     lib.lrnr_gpu_set_stream.argtypes = [vp, vp]
+    lib.lrnr_gpu_set_option.argtypes = [vp, ip, ip]
     lib.lrnr_gpu_launch_count.argtypes = [vp]
     lib.lrnr_gpu_launch_count.restype = i64
     lib.lrnr_gpu_set_lrnr.argtypes = [vp, ip, dp, dp, dp, ip, ip]

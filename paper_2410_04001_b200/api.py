@@ -295,6 +295,9 @@ class GpuContext:
                  "loss")
         return v.value
 
+    def set_option(self, opt: int, value: int):
+        self._rc(self.lib.lrnr_gpu_set_option(self.h, opt, value), "set_option")
+
     def fma_peak_tflops(self, dtype=F32):
         v = C.c_double(0.0)
         self._rc(self.lib.lrnr_gpu_fma_peak(self.h, dtype, C.byref(v)), "fma_peak")

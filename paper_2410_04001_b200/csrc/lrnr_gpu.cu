@@ -18,6 +18,7 @@
 #include "lrnr_gpu.h"
 #include "meta_kernels.cuh"
 #include "pinn_kernels.cuh"
+#include "pinn_v2.cuh"
 
 using namespace lrnr_b200;
 
@@ -91,6 +92,17 @@ struct Model {
     // LRNR-only extras for the meta path: original flat params (double)
     std::vector<double> flat;
     std::vector<int64_t> widths64, ranks64;
+    // kernel-v2 (tile-GEMM) layout: chunk blocks + per-tile schedule
+    struct V2 {
+        bool ok = false;
+        int KC = 0, NG = 0, PT1 = 0, RPMAX = 0, P = 0;
+        std::vector<int> rp, nc, yoff;
+        int ystride = 0;
+        std::vector<double> blocks;
+        std::vector<int64_t> sched_off;
+        std::vector<int> sched_cnt;
+        DevBuf dblocks, dsched_off, dsched_bytes;
+    } v2;
 };
 
 struct Hyper {
@@ -144,6 +156,13 @@ DevNet<T> dev_net(const Model& m) {
     return d;
 }
 
+void release_model(Model& m) {
+    m.dev.release();
+    m.v2.dblocks.release();
+    m.v2.dsched_off.release();
+    m.v2.dsched_bytes.release();
+}
+
 void upload_model(Model& m) {
     const size_t n = m.packed.size();
     if (m.dtype == LRNR_F64) {
@@ -156,6 +175,123 @@ void upload_model(Model& m) {
         CK(cudaMemcpy(m.dev.p, f.data(), n * sizeof(float), cudaMemcpyHostToDevice));
     }
     m.set = true;
+}
+
+// Kernel-v2 layout (pinn_v2.cuh): per transition l and chunk c of KC neurons,
+//   forward block  [U^T (rp_l x KC, permuted cols) | b (KC, permuted) | V (KC x rp_{l+1})]
+//   backward block [U^T | b | V^T (rp_{l+1} x KC, permuted cols) | U (KC x rp_l)]
+// with column q = ng*4 + kk holding local neuron ng + NG*kk (conflict-free Z/G
+// stores in phase 1), zero padding for ranks (to multiples of 4) and neurons.
+void build_v2(Model& m) {
+    auto& v = m.v2;
+    v = Model::V2{};
+    const int L = m.L;
+    int maxr = 0, maxM = 0;
+    for (int l = 0; l < L; ++l) maxr = std::max(maxr, m.r[l]);
+    for (int l = 1; l < L; ++l) maxM = std::max(maxM, m.M[l]);
+    if (maxr > 64) return;  // the streaming kernel v1 handles larger ranks
+    v.RPMAX = maxr <= 32 ? 32 : 64;
+    // rank classes: 4 (first / last layers: r <= 4) or RPMAX
+    v.rp.resize(L);
+    for (int l = 0; l < L; ++l) v.rp[l] = m.r[l] <= 4 ? 4 : v.RPMAX;
+    if (m.dtype == LRNR_F64) {
+        v.P = 32;
+        v.NG = 8;
+        v.PT1 = 1;
+    } else if (v.RPMAX == 64) {
+        v.P = 32;
+        v.NG = 16;
+        v.PT1 = 2;
+    } else if (maxM <= 32) {
+        v.P = 64;
+        v.NG = 8;
+        v.PT1 = 1;
+    } else {
+        v.P = 64;
+        v.NG = 16;
+        v.PT1 = 2;
+    }
+    v.KC = 4 * v.NG;
+    const int KC = v.KC, NG = v.NG;
+    v.nc.assign(L, 0);
+    v.yoff.assign(L, 0);
+    int yo = 0;
+    for (int l = 0; l < L; ++l) {
+        v.yoff[l] = yo;
+        yo += v.P * v.rp[l] * 4;
+    }
+    v.ystride = yo;
+    std::vector<int64_t> fwd_off(L), bwd_off(L);
+    std::vector<int> fwd_cnt(L), bwd_cnt(L);
+    std::vector<std::vector<int64_t>> foff(L), boff(L);
+    auto pad8 = [](size_t n) { return (n + 7) & ~size_t(7); };
+    for (int l = 0; l + 1 < L; ++l) {
+        const int rl = m.r[l], rn = m.r[l + 1], rpl = v.rp[l], rpn = v.rp[l + 1], M = m.M[l + 1];
+        v.nc[l] = (M + KC - 1) / KC;
+        const double* rows = m.packed.data() + m.off_trans[l];
+        auto U = [&](int k, int j) { return (k < M && j < rl) ? rows[static_cast<size_t>(k) * m.trow[l] + j] : 0.0; };
+        auto V = [&](int k, int j) { return (k < M && j < rn) ? rows[static_cast<size_t>(k) * m.trow[l] + rl + j] : 0.0; };
+        auto B = [&](int k) { return k < M ? rows[static_cast<size_t>(k) * m.trow[l] + rl + rn] : 0.0; };
+        const size_t nf = pad8(static_cast<size_t>(rpl * KC + KC + KC * rpn));
+        const size_t nb = pad8(static_cast<size_t>(rpl * KC + KC + rpn * KC + KC * rpl));
+        for (int c = 0; c < v.nc[l]; ++c) {
+            const int k0 = c * KC;
+            auto kq = [&](int q) { return k0 + (q / 4) + NG * (q % 4); };
+            // forward block
+            foff[l].push_back(static_cast<int64_t>(v.blocks.size()));
+            size_t o = v.blocks.size();
+            v.blocks.resize(o + nf, 0.0);
+            double* B0 = v.blocks.data() + o;
+            for (int j = 0; j < rpl; ++j)
+                for (int q = 0; q < KC; ++q) B0[j * KC + q] = U(kq(q), j);
+            for (int q = 0; q < KC; ++q) B0[rpl * KC + q] = B(kq(q));
+            for (int kl = 0; kl < KC; ++kl)
+                for (int j = 0; j < rpn; ++j) B0[rpl * KC + KC + kl * rpn + j] = V(k0 + kl, j);
+            // backward block
+            boff[l].push_back(static_cast<int64_t>(v.blocks.size()));
+            o = v.blocks.size();
+            v.blocks.resize(o + nb, 0.0);
+            double* B1 = v.blocks.data() + o;
+            for (int j = 0; j < rpl; ++j)
+                for (int q = 0; q < KC; ++q) B1[j * KC + q] = U(kq(q), j);
+            for (int q = 0; q < KC; ++q) B1[rpl * KC + q] = B(kq(q));
+            for (int j = 0; j < rpn; ++j)
+                for (int q = 0; q < KC; ++q) B1[rpl * KC + KC + j * KC + q] = V(kq(q), j);
+            for (int kl = 0; kl < KC; ++kl)
+                for (int j = 0; j < rpl; ++j) B1[rpl * KC + KC + rpn * KC + kl * rpl + j] = U(k0 + kl, j);
+        }
+        fwd_cnt[l] = static_cast<int>(nf);
+        bwd_cnt[l] = static_cast<int>(nb);
+    }
+    for (int l = 0; l + 1 < L; ++l)
+        for (int c = 0; c < v.nc[l]; ++c) {
+            v.sched_off.push_back(foff[l][c]);
+            v.sched_cnt.push_back(fwd_cnt[l]);
+        }
+    for (int l = L - 2; l >= 0; --l)
+        for (int c = 0; c < v.nc[l]; ++c) {
+            v.sched_off.push_back(boff[l][c]);
+            v.sched_cnt.push_back(bwd_cnt[l]);
+        }
+    const size_t esz = m.dtype == LRNR_F64 ? 8 : 4;
+    const size_t nbl = std::max<size_t>(v.blocks.size(), 8);
+    v.dblocks.ensure(nbl * esz);
+    if (m.dtype == LRNR_F64) {
+        if (!v.blocks.empty()) CK(cudaMemcpy(v.dblocks.p, v.blocks.data(), v.blocks.size() * 8, cudaMemcpyHostToDevice));
+    } else {
+        std::vector<float> f(v.blocks.begin(), v.blocks.end());
+        if (!f.empty()) CK(cudaMemcpy(v.dblocks.p, f.data(), f.size() * 4, cudaMemcpyHostToDevice));
+    }
+    const size_t ns = std::max<size_t>(v.sched_off.size(), 1);
+    std::vector<int> bytes(v.sched_cnt.size());
+    for (size_t i = 0; i < bytes.size(); ++i) bytes[i] = static_cast<int>(v.sched_cnt[i] * esz);
+    v.dsched_off.ensure(ns * sizeof(int64_t));
+    v.dsched_bytes.ensure(ns * sizeof(int));
+    if (!v.sched_off.empty()) {
+        CK(cudaMemcpy(v.dsched_off.p, v.sched_off.data(), v.sched_off.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(v.dsched_bytes.p, bytes.data(), bytes.size() * sizeof(int), cudaMemcpyHostToDevice));
+    }
+    v.ok = true;
 }
 
 }  // namespace
@@ -182,6 +318,8 @@ struct lrnr_gpu_ctx {
     std::string err;
     int tag = -1;
     int64_t launches = 0;
+    int opt_fast_sincos = 0;  // LRNR_OPT_FAST_SINCOS
+    int opt_kernel = 0;       // LRNR_OPT_KERNEL: 0 auto (v2 where supported), 1 force v1
 };
 
 namespace {
@@ -268,6 +406,92 @@ void launch_pinn(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const d
     reduce_units_kernel<T><<<rg, 128, 0, ctx->stream>>>(ctx->part.as<T>(), p.g.units_per_inst, R1, n_inst, dev_out);
     CK(cudaGetLastError());
     ctx->launches += 2;
+}
+
+// ---- kernel v2 (tile GEMM) ----
+template <class T, int P, int PT1, int NG, int RPMAX, int ACT, bool FAST>
+void launch_v2(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
+               double* dev_out) {
+    using S = v2::Smem<T, P, 4 * NG, RPMAX>;
+    constexpr int NT = v2::JG * P;
+    const int64_t n_inst = ctx->n_inst, n_per = ctx->n_per;
+    const int R1 = 1 + m.rtotal;
+    const size_t smem = static_cast<size_t>(S::OFF_ACC + R1) * sizeof(T);
+    auto kern = v2::pinn_tile_kernel<T, P, PT1, NG, RPMAX, ACT, FAST>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem));
+    if (occ < 1) throw InvalidArg("kernel v2 does not fit on an SM for this shape");
+    RunGeom g{};
+    g.P = P;
+    g.n_per_inst = n_per;
+    g.tiles_per_inst = static_cast<int>((n_per + P - 1) / P);
+    const int64_t total_tiles = static_cast<int64_t>(g.tiles_per_inst) * n_inst;
+    const int64_t max_grid = static_cast<int64_t>(ctx->num_sms) * occ;
+    int64_t tpu = (total_tiles + max_grid * 4 - 1) / (max_grid * 4);
+    tpu = std::max<int64_t>(1, std::min<int64_t>(tpu, g.tiles_per_inst));
+    g.tiles_per_unit = static_cast<int>(tpu);
+    g.units_per_inst = static_cast<int>((g.tiles_per_inst + tpu - 1) / tpu);
+    g.n_units = static_cast<int64_t>(g.units_per_inst) * n_inst;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_grid, g.n_units)));
+    const auto& v = m.v2;
+    ctx->scratch.ensure(static_cast<size_t>(grid) * v.ystride * sizeof(T) + 64);
+    ctx->part.ensure(static_cast<size_t>(g.n_units) * R1 * sizeof(T));
+    v2::NetV2<T> net{};
+    net.L = m.L;
+    for (int l = 0; l <= m.L; ++l) net.M[l] = m.M[l];
+    for (int l = 0; l < m.L; ++l) {
+        net.r[l] = m.r[l];
+        net.rp[l] = v.rp[l];
+        net.nc[l] = v.nc[l];
+        net.yoff[l] = v.yoff[l];
+    }
+    for (int l = 0; l <= m.L; ++l) net.soff[l] = m.soff[l];
+    net.ystride = v.ystride;
+    net.rtotal = m.rtotal;
+    net.blocks = v.dblocks.as<T>();
+    net.sched_off = v.dsched_off.as<int64_t>();
+    net.sched_bytes = v.dsched_bytes.as<int>();
+    net.sched_len = static_cast<int>(v.sched_off.size());
+    const T* base = m.dev.as<T>();
+    net.V0 = base + m.off_V0;
+    net.ulast = base + m.off_ulast;
+    kern<<<grid, NT, smem, ctx->stream>>>(net, g, ctx->pts, s_dev, mu_dev, static_cast<T>(w),
+                                               ctx->scratch.as<T>(), ctx->part.as<T>(),
+                                               ctx->bad.as<unsigned long long>());
+    CK(cudaGetLastError());
+    dim3 rg((R1 + 127) / 128, static_cast<unsigned>(n_inst));
+    reduce_units_kernel<T><<<rg, 128, 0, ctx->stream>>>(ctx->part.as<T>(), g.units_per_inst, R1, n_inst, dev_out);
+    CK(cudaGetLastError());
+    ctx->launches += 2;
+}
+
+bool dispatch_v2(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
+                 double* dev_out) {
+    const auto& v = m.v2;
+    if (!v.ok || ctx->opt_kernel == 1) return false;
+    const bool fast = ctx->opt_fast_sincos != 0;
+#define V2CASE(T_, P_, PT1_, NG_, RP_, ACT_, FAST_)                                             \
+    if (v.P == P_ && v.PT1 == PT1_ && v.NG == NG_ && v.RPMAX == RP_ && m.act == ACT_ && fast == FAST_) { \
+        launch_v2<T_, P_, PT1_, NG_, RP_, ACT_, FAST_>(ctx, m, s_dev, mu_dev, w, dev_out);     \
+        return true;                                                                           \
+    }
+    if (m.dtype == LRNR_F32) {
+        V2CASE(float, 64, 2, 16, 32, 1, false)
+        V2CASE(float, 64, 2, 16, 32, 1, true)
+        V2CASE(float, 64, 2, 16, 32, 0, false)
+        V2CASE(float, 64, 1, 8, 32, 1, false)
+        V2CASE(float, 64, 1, 8, 32, 1, true)
+        V2CASE(float, 64, 1, 8, 32, 0, false)
+        V2CASE(float, 32, 2, 16, 64, 1, false)
+        V2CASE(float, 32, 2, 16, 64, 1, true)
+        V2CASE(float, 32, 2, 16, 64, 0, false)
+    } else {
+        V2CASE(double, 32, 1, 8, 32, 0, false)
+        V2CASE(double, 32, 1, 8, 32, 1, false)
+    }
+#undef V2CASE
+    return false;
 }
 
 // dispatch over (dtype, act, rmax, mode)
@@ -441,6 +665,8 @@ double* run_resident(lrnr_gpu_ctx* ctx, const Model& m, double w, double* dev_ou
         return dev_out;
     }
     const double wt = w > 0.0 ? w : 1.0 / static_cast<double>(ctx->n_inst * ctx->n_per);
+    if (MODE == 0 && dispatch_v2(ctx, m, ctx->s_dev.as<double>(), ctx->mu_dev.as<double>(), wt, dev_out))
+        return dev_out;
     dispatch_pinn<MODE>(ctx, m, ctx->s_dev.as<double>(), ctx->mu_dev.as<double>(), wt, dev_out, jets_dev);
     return dev_out;
 }
@@ -560,7 +786,7 @@ int lrnr_gpu_destroy(lrnr_gpu_ctx* ctx) {
     if (!ctx) return LRNR_OK;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    for (auto& m : ctx->models) m.dev.release();
+    for (auto& m : ctx->models) release_model(m);
     ctx->hyper.dev.release();
     for (DevBuf* b : {&ctx->pts_own, &ctx->s_dev, &ctx->mu_dev, &ctx->scratch, &ctx->part, &ctx->out, &ctx->bad,
                       &ctx->acts, &ctx->G, &ctx->hgrad, &ctx->jets, &ctx->meta_ws})
@@ -573,6 +799,14 @@ int lrnr_gpu_destroy(lrnr_gpu_ctx* ctx) {
 const char* lrnr_gpu_last_error(const lrnr_gpu_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 int lrnr_gpu_last_layer_tag(const lrnr_gpu_ctx* ctx) { return ctx ? ctx->tag : -1; }
 int64_t lrnr_gpu_launch_count(const lrnr_gpu_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int lrnr_gpu_set_option(lrnr_gpu_ctx* ctx, int opt, int value) {
+    return guarded(ctx, [&] {
+        if (opt == LRNR_OPT_FAST_SINCOS) ctx->opt_fast_sincos = value;
+        else if (opt == LRNR_OPT_KERNEL) ctx->opt_kernel = value;
+        else throw InvalidArg("unknown option");
+    });
+}
 
 int lrnr_gpu_set_stream(lrnr_gpu_ctx* ctx, void* s) {
     return guarded(ctx, [&] { ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own; });
@@ -625,9 +859,10 @@ int lrnr_gpu_set_lrnr(lrnr_gpu_ctx* ctx, int L, const int64_t* widths, const int
         for (int j = 0; j < m.r[L - 1]; ++j) m.packed[m.off_ulast + j] = Pp[oU[L - 1] + j];
         m.packed[m.off_ulast + m.r[L - 1]] = Pp[ob[L - 1]];
         Model& dst = ctx->models[LRNR_MODEL_LRNR];
-        dst.dev.release();
+        release_model(dst);
         dst = std::move(m);
         upload_model(dst);
+        build_v2(dst);
     });
 }
 
@@ -673,9 +908,10 @@ int lrnr_gpu_set_fast(lrnr_gpu_ctx* ctx, int L, const int64_t* ranks, const int6
         o += static_cast<size_t>(m.r[L - 1]);
         m.packed[m.off_ulast + m.r[L - 1]] = F[o];
         Model& dst = ctx->models[LRNR_MODEL_FAST];
-        dst.dev.release();
+        release_model(dst);
         dst = std::move(m);
         upload_model(dst);
+        build_v2(dst);
     });
 }
 
