@@ -15,106 +15,15 @@
 #include <vector>
 
 #include "hyper_kernels.cuh"
-#include "lrnr_gpu.h"
+#include "internal.h"
 #include "meta_kernels.cuh"
-#include "pinn_kernels.cuh"
-#include "pinn_v2.cuh"
+#include "instances.h"
 
 using namespace lrnr_b200;
+using namespace lrnr_b200::detail;
 
-namespace {
-
-struct CudaError : std::runtime_error {
-    explicit CudaError(const std::string& m) : std::runtime_error(m) {}
-};
-struct InvalidArg : std::runtime_error {
-    explicit InvalidArg(const std::string& m) : std::runtime_error(m) {}
-};
-struct StateError : std::runtime_error {
-    explicit StateError(const std::string& m) : std::runtime_error(m) {}
-};
-struct NonFinite : std::runtime_error {
-    int tag;
-    NonFinite(int t) : std::runtime_error("non-finite value in recorded computation, layer tag " + std::to_string(t)), tag(t) {}
-};
-
-#define CK(x)                                                                                  \
-    do {                                                                                       \
-        cudaError_t e_ = (x);                                                                  \
-        if (e_ != cudaSuccess)                                                                 \
-            throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));                 \
-    } while (0)
-
-void require(bool c, const std::string& m) {
-    if (!c) throw InvalidArg(m);
-}
-
-struct DevBuf {
-    void* p = nullptr;
-    size_t bytes = 0;
-    void ensure(size_t n) {
-        if (n <= bytes) return;
-        if (p) cudaFree(p);
-        p = nullptr;
-        bytes = 0;
-        if (n == 0) return;
-        if (cudaMalloc(&p, n) != cudaSuccess) {
-            cudaGetLastError();
-            throw std::bad_alloc();
-        }
-        bytes = n;
-    }
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        bytes = 0;
-    }
-    template <class T>
-    T* as() const {
-        return static_cast<T*>(p);
-    }
-};
-
-// A network in the kernel's streaming layout (see pinn_kernels.cuh).
-struct Model {
-    bool set = false;
-    int kind = LRNR_MODEL_LRNR;
-    int dtype = LRNR_F64;
-    int act = LRNR_ACT_TANH;
-    int L = 0;
-    std::vector<int> M, r, soff, trow;
-    int rtotal = 0, rmax = 0;
-    // packed host copy (double) in device layout; offsets in elements
-    std::vector<double> packed;
-    size_t off_V0 = 0, off_ulast = 0;
-    std::vector<size_t> off_trans;
-    DevBuf dev;
-    // LRNR-only extras for the meta path: original flat params (double)
-    std::vector<double> flat;
-    std::vector<int64_t> widths64, ranks64;
-    // kernel-v2 (tile-GEMM) layout: chunk blocks + per-tile schedule
-    struct V2 {
-        bool ok = false;
-        int KC = 0, NG = 0, PT1 = 0, RPMAX = 0, P = 0;
-        std::vector<int> rp, nc, yoff;
-        int ystride = 0;
-        std::vector<double> blocks;
-        std::vector<int64_t> sched_off;
-        std::vector<int> sched_cnt;
-        DevBuf dblocks, dsched_off, dsched_bytes;
-    } v2;
-};
-
-struct Hyper {
-    bool set = false;
-    int K = 0;
-    std::vector<int> hw;
-    std::vector<int> oW, ob;
-    int max_w = 0, n_params = 0;
-    double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
-    DevBuf dev;
-};
-
+namespace lrnr_b200 {
+namespace detail {
 void build_layout(Model& m) {
     const int L = m.L;
     m.soff.assign(L + 1, 0);
@@ -136,24 +45,6 @@ void build_layout(Model& m) {
     m.off_ulast = o;
     o += static_cast<size_t>(m.r[L - 1] + 1);
     m.packed.assign(o, 0.0);
-}
-
-template <class T>
-DevNet<T> dev_net(const Model& m) {
-    DevNet<T> d{};
-    d.L = m.L;
-    for (int l = 0; l <= m.L; ++l) d.M[l] = m.M[l];
-    for (int l = 0; l < m.L; ++l) {
-        d.r[l] = m.r[l];
-        d.trow[l] = m.trow[l];
-    }
-    for (int l = 0; l <= m.L; ++l) d.soff[l] = m.soff[l];
-    const T* base = m.dev.as<T>();
-    d.V0 = base + m.off_V0;
-    for (int l = 0; l + 1 < m.L; ++l) d.trans[l] = base + m.off_trans[l];
-    d.ulast = base + m.off_ulast;
-    d.rtotal = m.rtotal;
-    return d;
 }
 
 void release_model(Model& m) {
@@ -294,33 +185,8 @@ void build_v2(Model& m) {
     v.ok = true;
 }
 
-}  // namespace
-
-struct lrnr_gpu_ctx {
-    int device = 0;
-    int num_sms = 148;
-    cudaStream_t own = nullptr;
-    cudaStream_t stream = nullptr;
-    Model models[2];
-    Hyper hyper;
-    // points (double, device)
-    DevBuf pts_own;
-    const double* pts = nullptr;
-    int64_t n_inst = 0, n_per = 0;
-    // coefficients (double, device)
-    DevBuf s_dev, mu_dev;
-    int64_t coeff_inst = 0;
-    int coeff_rtotal = 0;
-    // workspaces
-    DevBuf scratch, part, out, bad, acts, G, hgrad, jets, meta_ws;
-    int64_t out_rows = 0;
-    int out_R1 = 0;
-    std::string err;
-    int tag = -1;
-    int64_t launches = 0;
-    int opt_fast_sincos = 0;  // LRNR_OPT_FAST_SINCOS
-    int opt_kernel = 0;       // LRNR_OPT_KERNEL: 0 auto (v2 where supported), 1 force v1
-};
+}  // namespace detail
+}  // namespace lrnr_b200
 
 namespace {
 
@@ -357,115 +223,6 @@ int guarded(lrnr_gpu_ctx* ctx, F&& f) {
 // ---------------------------------------------------------------------------
 // launch planning
 // ---------------------------------------------------------------------------
-struct Plan {
-    RunGeom g;
-    int grid;
-    size_t smem;
-};
-
-template <class T, int TPP, int RMAX, int ACT, int MODE>
-Plan plan_for(lrnr_gpu_ctx* ctx, const Model& m, int64_t n_inst, int64_t n_per) {
-    Plan p{};
-    p.g.P = kThreads / TPP;
-    p.g.n_per_inst = n_per;
-    p.g.tiles_per_inst = static_cast<int>((n_per + p.g.P - 1) / p.g.P);
-    const int R1 = 1 + m.rtotal;
-    p.smem = static_cast<size_t>((kThreads / 32 + 1) * R1) * sizeof(T);
-    auto kern = pinn_kernel<T, TPP, RMAX, ACT, MODE>;
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem)));
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, p.smem));
-    occ = std::max(occ, 1);
-    const int64_t total_tiles = static_cast<int64_t>(p.g.tiles_per_inst) * n_inst;
-    const int64_t max_grid = static_cast<int64_t>(ctx->num_sms) * occ;
-    // ~8 units per resident CTA for balance; units never cross instances
-    int64_t want_units = std::max<int64_t>(1, max_grid * 8);
-    int64_t tpu = (total_tiles + want_units - 1) / want_units;
-    tpu = std::max<int64_t>(1, std::min<int64_t>(tpu, p.g.tiles_per_inst));
-    p.g.tiles_per_unit = static_cast<int>(tpu);
-    p.g.units_per_inst = static_cast<int>((p.g.tiles_per_inst + tpu - 1) / tpu);
-    p.g.n_units = static_cast<int64_t>(p.g.units_per_inst) * n_inst;
-    p.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_grid, p.g.n_units)));
-    return p;
-}
-
-template <class T, int TPP, int RMAX, int ACT, int MODE>
-void launch_pinn(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
-                 double* dev_out, double* jets_dev) {
-    const int64_t n_inst = ctx->n_inst, n_per = ctx->n_per;
-    Plan p = plan_for<T, TPP, RMAX, ACT, MODE>(ctx, m, n_inst, n_per);
-    const int R1 = 1 + m.rtotal;
-    ctx->scratch.ensure(static_cast<size_t>(p.grid) * p.g.P * 4 * m.rtotal * sizeof(T));
-    ctx->part.ensure(static_cast<size_t>(p.g.n_units) * R1 * sizeof(T));
-    DevNet<T> net = dev_net<T>(m);
-    pinn_kernel<T, TPP, RMAX, ACT, MODE><<<p.grid, kThreads, p.smem, ctx->stream>>>(
-        net, p.g, ctx->pts, s_dev, mu_dev, static_cast<T>(w), ctx->scratch.as<T>(), ctx->part.as<T>(),
-        jets_dev, ctx->bad.as<unsigned long long>());
-    CK(cudaGetLastError());
-    dim3 rg((R1 + 127) / 128, static_cast<unsigned>(n_inst));
-    reduce_units_kernel<T><<<rg, 128, 0, ctx->stream>>>(ctx->part.as<T>(), p.g.units_per_inst, R1, n_inst, dev_out);
-    CK(cudaGetLastError());
-    ctx->launches += 2;
-}
-
-// ---- kernel v2 (tile GEMM) ----
-template <class T, int P, int PT1, int NG, int RPMAX, int ACT, bool FAST>
-void launch_v2(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
-               double* dev_out) {
-    using S = v2::Smem<T, P, 4 * NG, RPMAX>;
-    constexpr int NT = v2::JG * P;
-    const int64_t n_inst = ctx->n_inst, n_per = ctx->n_per;
-    const int R1 = 1 + m.rtotal;
-    const size_t smem = static_cast<size_t>(S::OFF_ACC + R1) * sizeof(T);
-    auto kern = v2::pinn_tile_kernel<T, P, PT1, NG, RPMAX, ACT, FAST>;
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem));
-    if (occ < 1) throw InvalidArg("kernel v2 does not fit on an SM for this shape");
-    RunGeom g{};
-    g.P = P;
-    g.n_per_inst = n_per;
-    g.tiles_per_inst = static_cast<int>((n_per + P - 1) / P);
-    const int64_t total_tiles = static_cast<int64_t>(g.tiles_per_inst) * n_inst;
-    const int64_t max_grid = static_cast<int64_t>(ctx->num_sms) * occ;
-    int64_t tpu = (total_tiles + max_grid * 4 - 1) / (max_grid * 4);
-    tpu = std::max<int64_t>(1, std::min<int64_t>(tpu, g.tiles_per_inst));
-    g.tiles_per_unit = static_cast<int>(tpu);
-    g.units_per_inst = static_cast<int>((g.tiles_per_inst + tpu - 1) / tpu);
-    g.n_units = static_cast<int64_t>(g.units_per_inst) * n_inst;
-    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_grid, g.n_units)));
-    const auto& v = m.v2;
-    ctx->scratch.ensure(static_cast<size_t>(grid) * v.ystride * sizeof(T) + 64);
-    ctx->part.ensure(static_cast<size_t>(g.n_units) * R1 * sizeof(T));
-    v2::NetV2<T> net{};
-    net.L = m.L;
-    for (int l = 0; l <= m.L; ++l) net.M[l] = m.M[l];
-    for (int l = 0; l < m.L; ++l) {
-        net.r[l] = m.r[l];
-        net.rp[l] = v.rp[l];
-        net.nc[l] = v.nc[l];
-        net.yoff[l] = v.yoff[l];
-    }
-    for (int l = 0; l <= m.L; ++l) net.soff[l] = m.soff[l];
-    net.ystride = v.ystride;
-    net.rtotal = m.rtotal;
-    net.blocks = v.dblocks.as<T>();
-    net.sched_off = v.dsched_off.as<int64_t>();
-    net.sched_bytes = v.dsched_bytes.as<int>();
-    net.sched_len = static_cast<int>(v.sched_off.size());
-    const T* base = m.dev.as<T>();
-    net.V0 = base + m.off_V0;
-    net.ulast = base + m.off_ulast;
-    kern<<<grid, NT, smem, ctx->stream>>>(net, g, ctx->pts, s_dev, mu_dev, static_cast<T>(w),
-                                               ctx->scratch.as<T>(), ctx->part.as<T>(),
-                                               ctx->bad.as<unsigned long long>());
-    CK(cudaGetLastError());
-    dim3 rg((R1 + 127) / 128, static_cast<unsigned>(n_inst));
-    reduce_units_kernel<T><<<rg, 128, 0, ctx->stream>>>(ctx->part.as<T>(), g.units_per_inst, R1, n_inst, dev_out);
-    CK(cudaGetLastError());
-    ctx->launches += 2;
-}
-
 bool dispatch_v2(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
                  double* dev_out) {
     const auto& v = m.v2;

@@ -1,0 +1,91 @@
+"""CPU, world_size 2 over gloo: the multi-GPU decomposition of the path.
+
+Each rank computes its shard's [loss, dL/ds] rows (points sharded for config 2,
+whole instances for config 3) with the FP64 oracle standing in for the device
+sweep, then the rows are summed with the same all-reduce helper bench.py uses
+(NCCL on the GPU box).  The result must equal the single-process sweep over
+all points / instances."""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    from oracle.oracle import Oracle
+    from paper_2410_04001_b200.dist import allreduce_sum_, shard_instances, shard_range
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    O = Oracle()
+    g = dict(np.load(os.path.join(ROOT, "tests", "golden", "reference_golden.npz")))
+    # config-2 style: points sharded, weight 1/N_global
+    pts = g["c2_pts"]
+    n = len(pts)
+    lo, hi = shard_range(n, world, rank)
+    r = O.lrnr_grad(g["c2_widths"], g["c2_ranks"], g["c2_params"], g["c2_s"], g["c2_mu"], pts[lo:hi], w=1.0 / n)
+    row = torch.tensor(np.concatenate([[r["value"]], r["grad_s"]]))
+    allreduce_sum_(row)
+    # config-3 style: instances sharded, hypernetwork gradient summed
+    mus = g["c3_mu"]
+    a, b = shard_instances(len(mus), world, rank)
+    hw, H, lo3, hi3 = g["c3_hw"], g["c3_hparams"], g["c3_lo"], g["c3_hi"]
+    sub = pts[:64]
+    ght = np.zeros(H.size)
+    for i in range(a, b):
+        s_i = O.hyper_forward(hw, H, lo3, hi3, mus[i])
+        ri = O.fast_grad(g["c2_ranks"], g["c2_red_ranks"], g["c2_fparams"], s_i, mus[i], sub,
+                         w=1.0 / (len(mus) * len(sub)))
+        O.hyper_vjp(hw, H, lo3, hi3, mus[i], ri["grad_s"], out=ght)
+    th = torch.tensor(ght)
+    allreduce_sum_(th)
+    if rank == 0:
+        q.put((row.numpy(), th.numpy()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_gloo_sharding_equals_single_process(oracle, golden):
+    torch = pytest.importorskip("torch")
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(k, 2, port, q)) for k in range(2)]
+    for p in procs:
+        p.start()
+    row, th = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = golden
+    full = oracle.lrnr_grad(g["c2_widths"], g["c2_ranks"], g["c2_params"], g["c2_s"], g["c2_mu"], g["c2_pts"])
+    assert abs(row[0] - full["value"]) <= 1e-13 * full["value"]
+    np.testing.assert_allclose(row[1:], full["grad_s"], rtol=1e-11, atol=1e-14 * np.abs(full["grad_s"]).max())
+    mus = g["c3_mu"]
+    sub = g["c2_pts"][:64]
+    ref = np.zeros(g["c3_hparams"].size)
+    for i in range(len(mus)):
+        s_i = oracle.hyper_forward(g["c3_hw"], g["c3_hparams"], g["c3_lo"], g["c3_hi"], mus[i])
+        ri = oracle.fast_grad(g["c2_ranks"], g["c2_red_ranks"], g["c2_fparams"], s_i, mus[i], sub,
+                              w=1.0 / (len(mus) * len(sub)))
+        oracle.hyper_vjp(g["c3_hw"], g["c3_hparams"], g["c3_lo"], g["c3_hi"], mus[i], ri["grad_s"], out=ref)
+    np.testing.assert_allclose(th, ref, rtol=1e-11, atol=1e-14 * np.abs(ref).max())

@@ -1,0 +1,104 @@
+"""CPU: host-side setup of the product library (generators, FastLRNR EIM
+construction) bit-exact against the reference's golden vectors, and the C ABI
+surface (every symbol include/lrnr_gpu.h declares is exported; errors map to
+the reference's exception types).  No GPU compute here."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2410_04001_b200 as pkg
+from paper_2410_04001_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_generators_bit_exact(golden):
+    m, s = pkg.make_baseline_model(golden["c0_widths"], golden["c0_ranks"], 2410)
+    assert np.array_equal(m.params, golden["c0_params"]) and np.array_equal(s, golden["c0_s"])
+    m2, s2 = pkg.make_baseline_model(golden["c2_widths"], golden["c2_ranks"], 2411)
+    assert np.array_equal(m2.params, golden["c2_params"]) and np.array_equal(s2, golden["c2_s"])
+    assert np.array_equal(pkg.sample_collocation(4001, 4096), golden["c0_pts"])
+    assert np.array_equal(pkg.sample_collocation(4002, 1024), golden["c2_pts"])
+    h = pkg.make_hyper_params(golden["c2_ranks"], 2, 64, 4003, golden["c3_lo"], golden["c3_hi"], 0.01, 0.5)
+    assert np.array_equal(h.hw, golden["c3_hw"]) and np.array_equal(h.params, golden["c3_hparams"])
+
+
+def test_eim_reduction_bit_exact_c1(golden):
+    """harvest_snapshots + eim_greedy + build_fastparams: index selection bit-for-bit."""
+    m = pkg.LrnrParams(golden["c0_widths"], golden["c0_ranks"], golden["c0_params"], pkg.ACT_TANH)
+    f = pkg.build_fast(m, golden["c0_s"], nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777, r_hat=10)
+    assert np.array_equal(f.indices, golden["c1_indices"])
+    assert np.array_equal(f.red_ranks, golden["c1_red_ranks"])
+    assert np.array_equal(f.fparams, golden["c1_fparams"])
+
+
+def test_eim_reduction_bit_exact_c2(golden):
+    m = pkg.LrnrParams(golden["c2_widths"], golden["c2_ranks"], golden["c2_params"], pkg.ACT_TANH)
+    f = pkg.build_fast(m, golden["c2_s"], nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777, r_hat=32)
+    assert np.array_equal(f.indices, golden["c2_indices"])
+    assert np.array_equal(f.red_ranks, golden["c2_red_ranks"])
+    assert np.array_equal(f.fparams, golden["c2_fparams"])
+
+
+def test_eim_rejects_bad_shapes():
+    m = pkg.LrnrParams(np.array([2, 4, 1]), np.array([3, 1]), np.zeros(64))
+    with pytest.raises(ValueError):
+        pkg.build_fast(m, np.ones(4))
+
+
+def test_flop_model_matches_survey():
+    """68,880 / 1,323,088 / 7,364,688 FLOP per point; meta 11,047,032."""
+    assert pkg.algorithmic_flops_per_point([2, 100, 100, 100, 1], [2, 10, 10, 1]) == 68880
+    assert pkg.algorithmic_flops_per_point([2] + [256] * 6 + [1], [2] + [32] * 5 + [1]) == 1323088
+    assert pkg.algorithmic_flops_per_point([2] + [512] * 8 + [1], [2] + [64] * 7 + [1]) == 7364688
+    assert pkg.algorithmic_flops_per_point([2] + [512] * 8 + [1], [2] + [64] * 7 + [1], meta=True) == 11047032
+    assert pkg.fast_flops_per_point([2, 10, 10, 1], [10, 10, 10]) == 6960
+    assert pkg.fast_flops_per_point([2] + [32] * 5 + [1], [32] * 6) == 165456
+
+
+def test_abi_exports_every_declared_symbol():
+    header = open(os.path.join(ROOT, "include", "lrnr_gpu.h")).read()
+    declared = set(re.findall(r"^\w[\w\s\*]*?\b(lrnr_(?:gpu|host)_\w+)\s*\(", header, re.M))
+    assert len(declared) >= 25
+    lib = C.CDLL(_lib.LIB_PATH)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(_lib.EXPORTS)
+
+
+def test_abi_context_errors_without_a_device():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(pkg.LrnrGpuError):
+        pkg.GpuContext(0)
+
+
+def test_abi_null_and_bad_arguments_are_einval():
+    lib = _lib.load()
+    assert lib.lrnr_gpu_create(0, None) == _lib.LRNR_EINVAL
+    assert lib.lrnr_gpu_destroy(None) == _lib.LRNR_OK
+    assert lib.lrnr_gpu_set_points(None, None, 1, 1) == _lib.LRNR_EINVAL
+    assert lib.lrnr_gpu_last_layer_tag(None) == -1
+    w = np.array([2, 4, 1], np.int64)
+    r = np.array([3, 1], np.int64)  # rank exceeds min(M_l, M_{l-1})
+    P = np.zeros(64)
+    s = np.zeros(4)
+    rc = lib.lrnr_host_make_baseline_model(2, w.ctypes.data_as(C.c_void_p), r.ctypes.data_as(C.c_void_p),
+                                           C.c_uint64(1), P.ctypes.data_as(C.c_void_p), s.ctypes.data_as(C.c_void_p))
+    assert rc == _lib.LRNR_EINVAL
+
+
+def test_dist_shard_ranges_cover_exactly():
+    from paper_2410_04001_b200.dist import shard_range
+
+    for n in (0, 1, 7, 1 << 20, 1000003):
+        for world in (1, 2, 3, 8):
+            spans = [shard_range(n, world, k) for k in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(spans[k][1] == spans[k + 1][0] for k in range(world - 1))
+            sizes = [b - a for a, b in spans]
+            assert max(sizes) - min(sizes) <= 1
