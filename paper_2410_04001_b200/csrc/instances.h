@@ -32,11 +32,19 @@
     template void lrnr_b200::detail::launch_pinn<T, TPP, RM, ACT, MODE>(                                  \
         lrnr_gpu_ctx*, const lrnr_b200::detail::Model&, const double*, const double*, double, double*, double*);
 #define LRNR_TILE_EXTERN(T, P, PT1, NG, RP, ACT, FAST)                                                   \
-    extern template void lrnr_b200::detail::launch_v2<T, P, PT1, NG, RP, ACT, FAST>(                      \
-        lrnr_gpu_ctx*, const lrnr_b200::detail::Model&, const double*, const double*, double, double*);
+    extern template void lrnr_b200::detail::launch_v2<T, P, PT1, NG, RP, ACT, FAST, false>(               \
+        lrnr_gpu_ctx*, const lrnr_b200::detail::Model&, const double*, const double*, double, double*, double*);
 #define LRNR_TILE_INST(T, P, PT1, NG, RP, ACT, FAST)                                                     \
-    template void lrnr_b200::detail::launch_v2<T, P, PT1, NG, RP, ACT, FAST>(                             \
-        lrnr_gpu_ctx*, const lrnr_b200::detail::Model&, const double*, const double*, double, double*);
+    template void lrnr_b200::detail::launch_v2<T, P, PT1, NG, RP, ACT, FAST, false>(                      \
+        lrnr_gpu_ctx*, const lrnr_b200::detail::Model&, const double*, const double*, double, double*, double*);
+// meta (dU/dV/db) variants of the tile kernel: (T, ACT, RPMAX); P = 32, KC = 32
+#define LRNR_META(X) X(float, 1, 64) X(float, 1, 32) X(float, 0, 64) X(float, 0, 32) X(double, 0, 32) X(double, 1, 32)
+#define LRNR_META_EXTERN(T, ACT, RP)                                                                    \
+    extern template void lrnr_b200::detail::launch_v2<T, 32, 1, 8, RP, ACT, false, true>(                  \
+        lrnr_gpu_ctx*, const lrnr_b200::detail::Model&, const double*, const double*, double, double*, double*);
+#define LRNR_META_INST(T, ACT, RP)                                                                      \
+    template void lrnr_b200::detail::launch_v2<T, 32, 1, 8, RP, ACT, false, true>(                         \
+        lrnr_gpu_ctx*, const lrnr_b200::detail::Model&, const double*, const double*, double, double*, double*);
 
 #ifndef LRNR_INSTANTIATING
 LRNR_V1_F64(LRNR_V1_EXTERN)
@@ -44,4 +52,5 @@ LRNR_V1_F32(LRNR_V1_EXTERN)
 LRNR_TILE_F32(LRNR_TILE_EXTERN)
 LRNR_TILE_F32R64(LRNR_TILE_EXTERN)
 LRNR_TILE_F64(LRNR_TILE_EXTERN)
+LRNR_META(LRNR_META_EXTERN)
 #endif

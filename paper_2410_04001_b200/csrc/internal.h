@@ -97,7 +97,7 @@ struct Model {
         std::vector<int64_t> sched_off;
         std::vector<int> sched_cnt;
         DevBuf dblocks, dsched_off, dsched_bytes;
-    } v2;
+    } v2, v2meta;
 };
 
 struct Hyper {
@@ -113,7 +113,7 @@ struct Hyper {
 void build_layout(Model& m);
 void release_model(Model& m);
 void upload_model(Model& m);
-void build_v2(Model& m);
+void build_v2(Model& m, bool meta = false);
 
 template <class T>
 DevNet<T> dev_net(const Model& m) {
@@ -216,15 +216,16 @@ void launch_pinn(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const d
 }
 
 // ---- kernel v2 (tile GEMM) ----
-template <class T, int P, int PT1, int NG, int RPMAX, int ACT, bool FAST>
+template <class T, int P, int PT1, int NG, int RPMAX, int ACT, bool FAST, bool META = false>
 void launch_v2(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
-               double* dev_out) {
-    using S = v2::Smem<T, P, 4 * NG, RPMAX>;
+               double* dev_out, double* wg_out = nullptr) {
+    using S = v2::Smem<T, P, 4 * NG, RPMAX, META>;
     constexpr int NT = v2::JG * P;
     const int64_t n_inst = ctx->n_inst, n_per = ctx->n_per;
     const int R1 = 1 + m.rtotal;
-    const size_t smem = static_cast<size_t>(S::OFF_ACC + R1) * sizeof(T);
-    auto kern = v2::pinn_tile_kernel<T, P, PT1, NG, RPMAX, ACT, FAST>;
+    if (META && R1 > 1024) throw InvalidArg("meta path supports r_total < 1024");
+    const size_t smem = static_cast<size_t>(std::max(S::OFF_ACC + R1, S::END)) * sizeof(T);
+    auto kern = v2::pinn_tile_kernel<T, P, PT1, NG, RPMAX, ACT, FAST, META>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem));
@@ -241,7 +242,7 @@ void launch_v2(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
     g.units_per_inst = static_cast<int>((g.tiles_per_inst + tpu - 1) / tpu);
     g.n_units = static_cast<int64_t>(g.units_per_inst) * n_inst;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_grid, g.n_units)));
-    const auto& v = m.v2;
+    const auto& v = META ? m.v2meta : m.v2;
     ctx->scratch.ensure(static_cast<size_t>(grid) * v.ystride * sizeof(T) + 64);
     ctx->part.ensure(static_cast<size_t>(g.n_units) * R1 * sizeof(T));
     v2::NetV2<T> net{};
@@ -263,10 +264,34 @@ void launch_v2(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
     const T* base = m.dev.as<T>();
     net.V0 = base + m.off_V0;
     net.ulast = base + m.off_ulast;
+    T* wg = nullptr;
+    int64_t n_params = 0;
+    if (META) {
+        int64_t o = 0;
+        for (int l = 0; l < m.L; ++l) {
+            net.oU[l] = o;
+            o += static_cast<int64_t>(m.M[l + 1]) * m.r[l];
+            net.oV[l] = o;
+            o += static_cast<int64_t>(m.M[l]) * m.r[l];
+            net.ob[l] = o;
+            o += m.M[l + 1];
+        }
+        n_params = o;
+        net.wg_stride = (o + 31) & ~int64_t(31);
+        ctx->meta_ws.ensure(static_cast<size_t>(grid) * net.wg_stride * sizeof(T));
+        wg = ctx->meta_ws.as<T>();
+        CK(cudaMemsetAsync(wg, 0, static_cast<size_t>(grid) * net.wg_stride * sizeof(T), ctx->stream));
+    }
     kern<<<grid, NT, smem, ctx->stream>>>(net, g, ctx->pts, s_dev, mu_dev, static_cast<T>(w),
                                                ctx->scratch.as<T>(), ctx->part.as<T>(),
-                                               ctx->bad.as<unsigned long long>());
+                                               ctx->bad.as<unsigned long long>(), wg);
     CK(cudaGetLastError());
+    if (META) {
+        reduce_rows_kernel<T><<<static_cast<unsigned>((n_params + 255) / 256), 256, 0, ctx->stream>>>(
+            wg, grid, net.wg_stride, n_params, wg_out);
+        CK(cudaGetLastError());
+        ctx->launches += 1;
+    }
     dim3 rg((R1 + 127) / 128, static_cast<unsigned>(n_inst));
     reduce_units_kernel<T><<<rg, 128, 0, ctx->stream>>>(ctx->part.as<T>(), g.units_per_inst, R1, n_inst, dev_out);
     CK(cudaGetLastError());

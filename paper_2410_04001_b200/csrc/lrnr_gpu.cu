@@ -52,6 +52,9 @@ void release_model(Model& m) {
     m.v2.dblocks.release();
     m.v2.dsched_off.release();
     m.v2.dsched_bytes.release();
+    m.v2meta.dblocks.release();
+    m.v2meta.dsched_off.release();
+    m.v2meta.dsched_bytes.release();
 }
 
 void upload_model(Model& m) {
@@ -73,8 +76,8 @@ void upload_model(Model& m) {
 //   backward block [U^T | b | V^T (rp_{l+1} x KC, permuted cols) | U (KC x rp_l)]
 // with column q = ng*4 + kk holding local neuron ng + NG*kk (conflict-free Z/G
 // stores in phase 1), zero padding for ranks (to multiples of 4) and neurons.
-void build_v2(Model& m) {
-    auto& v = m.v2;
+void build_v2(Model& m, bool meta) {
+    auto& v = meta ? m.v2meta : m.v2;
     v = Model::V2{};
     const int L = m.L;
     int maxr = 0, maxM = 0;
@@ -85,7 +88,7 @@ void build_v2(Model& m) {
     // rank classes: 4 (first / last layers: r <= 4) or RPMAX
     v.rp.resize(L);
     for (int l = 0; l < L; ++l) v.rp[l] = m.r[l] <= 4 ? 4 : v.RPMAX;
-    if (m.dtype == LRNR_F64) {
+    if (m.dtype == LRNR_F64 || meta) {
         v.P = 32;
         v.NG = 8;
         v.PT1 = 1;
@@ -511,8 +514,48 @@ __global__ void __launch_bounds__(256) fma_peak_kernel(T* out, int iters, T b) {
     if (s == T(12345.678)) out[0] = s;
 }
 
-void meta_step(lrnr_gpu_ctx*, const Model&, double, double*, double*) {
-    throw StateError("meta path not available in this build");
+// Meta step: per-instance s from the hypernetwork (already in ctx->s_dev),
+// the META tile kernel for (loss, dL/ds per instance, dU/dV/b), then the
+// hypernetwork VJP of the per-instance dL/ds.  Output: ParamPacker order.
+void meta_step(lrnr_gpu_ctx* ctx, Model& m, double w, double* out_grad, double* out_value) {
+    if (!m.v2meta.ok) build_v2(m, true);
+    const auto& v = m.v2meta;
+    if (!v.ok) throw InvalidArg("meta path supports ranks <= 64");
+    const int R1 = 1 + m.rtotal;
+    int64_t n_lrnr = 0;
+    for (int l = 0; l < m.L; ++l) n_lrnr += static_cast<int64_t>(m.M[l + 1]) * m.r[l] + static_cast<int64_t>(m.M[l]) * m.r[l] + m.M[l + 1];
+    const int64_t n_hyper = ctx->hyper.n_params;
+    ctx->out.ensure(static_cast<size_t>(ctx->n_inst * R1) * sizeof(double));
+    ctx->hgrad.ensure(static_cast<size_t>(n_lrnr + n_hyper) * sizeof(double));
+    double* rows = ctx->out.as<double>();
+    double* gout = ctx->hgrad.as<double>();
+    ctx->out_rows = ctx->n_inst;
+    ctx->out_R1 = R1;
+    ctx->bad.ensure(sizeof(unsigned long long));
+    reset_bad(ctx);
+    if (ctx->n_per == 0) {
+        CK(cudaMemsetAsync(rows, 0, static_cast<size_t>(ctx->n_inst * R1) * sizeof(double), ctx->stream));
+        CK(cudaMemsetAsync(gout, 0, static_cast<size_t>(n_lrnr) * sizeof(double), ctx->stream));
+    } else {
+        const double* sd = ctx->s_dev.as<double>();
+        const double* md = ctx->mu_dev.as<double>();
+        const int RP = v.RPMAX;
+        if (m.dtype == LRNR_F32 && m.act == LRNR_ACT_SIN && RP == 64) launch_v2<float, 32, 1, 8, 64, 1, false, true>(ctx, m, sd, md, w, rows, gout);
+        else if (m.dtype == LRNR_F32 && m.act == LRNR_ACT_SIN && RP == 32) launch_v2<float, 32, 1, 8, 32, 1, false, true>(ctx, m, sd, md, w, rows, gout);
+        else if (m.dtype == LRNR_F32 && m.act == LRNR_ACT_TANH && RP == 64) launch_v2<float, 32, 1, 8, 64, 0, false, true>(ctx, m, sd, md, w, rows, gout);
+        else if (m.dtype == LRNR_F32 && m.act == LRNR_ACT_TANH && RP == 32) launch_v2<float, 32, 1, 8, 32, 0, false, true>(ctx, m, sd, md, w, rows, gout);
+        else if (m.dtype == LRNR_F64 && m.act == LRNR_ACT_TANH && RP == 32) launch_v2<double, 32, 1, 8, 32, 0, false, true>(ctx, m, sd, md, w, rows, gout);
+        else if (m.dtype == LRNR_F64 && m.act == LRNR_ACT_SIN && RP == 32) launch_v2<double, 32, 1, 8, 32, 1, false, true>(ctx, m, sd, md, w, rows, gout);
+        else throw InvalidArg("meta path: unsupported dtype / rank combination");
+    }
+    hyper_backward_resident(ctx, rows, R1, gout + n_lrnr);
+    std::vector<double> h(static_cast<size_t>(ctx->n_inst * R1));
+    download(ctx, rows, h.data(), h.size());
+    check_bad(ctx, m);
+    double val = 0.0;
+    for (int64_t i = 0; i < ctx->n_inst; ++i) val += h[static_cast<size_t>(i * R1)];
+    *out_value = val;
+    download(ctx, gout, out_grad, static_cast<size_t>(n_lrnr + n_hyper));
 }
 
 }  // namespace
@@ -861,7 +904,7 @@ int lrnr_gpu_loss(lrnr_gpu_ctx* ctx, int model, const double* s, const double* m
 
 int lrnr_gpu_meta_loss_grad(lrnr_gpu_ctx* ctx, const double* mus, double w, double* out_value, double* out_grad) {
     return guarded(ctx, [&] {
-        const Model& m = need_model(ctx, LRNR_MODEL_LRNR);
+        Model& m = const_cast<Model&>(need_model(ctx, LRNR_MODEL_LRNR));
         require(mus && out_grad, "null argument");
         if (!ctx->hyper.set) throw StateError("hypernetwork not set");
         const int64_t n = ctx->n_inst;

@@ -57,6 +57,9 @@ struct NetV2 {
     int sched_len;         // entries per tile (forward chunks then backward chunks)
     const T* V0;           // 2 x r[0]
     const T* ulast;        // r[L-1] values then b_{L-1}[0]
+    // META: flat ParamPacker offsets of U_l, V_l, b_l (autodiff.cpp:926-934)
+    int64_t oU[kMaxL], oV[kMaxL], ob[kMaxL];
+    int64_t wg_stride;     // per-CTA partial-gradient stride (elements)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -154,7 +157,7 @@ __device__ __forceinline__ void act3(T a, T& sg, T& d1, T& d2, T& d3) {
 }
 
 // Shared-memory carve-up (elements of T).
-template <typename T, int P, int KC, int RPMAX>
+template <typename T, int P, int KC, int RPMAX, bool META = false>
 struct Smem {
     static constexpr int ZS = KC * 4 + 4;      // Z/G point stride (padded: conflict-free phase-2 reads)
     static constexpr int SS = RPMAX * 4 + 4;   // SY/ST point stride
@@ -165,15 +168,18 @@ struct Smem {
     static constexpr int OFF_B0 = ((OFF_ST + P * SS + 31) / 32) * 32;
     static constexpr int OFF_B1 = OFF_B0 + ((BUF + 31) / 32) * 32;
     static constexpr int OFF_RED = OFF_B1 + ((BUF + 31) / 32) * 32;
-    static constexpr int OFF_ACC = OFF_RED + P * RPMAX + P;
+    static constexpr int OFF_ACC = OFF_RED + P * RPMAX + 2 * P;
+    static constexpr int OFF_ZZ = ((OFF_ACC + 1024 + 31) / 32) * 32;  // META: Z chunk (needs r_total < 1024)
+    static constexpr int OFF_XT = OFF_ZZ + (META ? P * ZS : 0);        // META: (x, t) of the tile
+    static constexpr int END = OFF_XT + (META ? 2 * P : 0);
 };
 
-template <typename T, int P, int PT1, int NG, int RPMAX, int ACT, bool FAST>
+template <typename T, int P, int PT1, int NG, int RPMAX, int ACT, bool FAST, bool META = false>
 struct Tile {
     static constexpr int NT = JG * P;
     static constexpr int KC = 4 * NG;
     static constexpr int NJ = RPMAX / (4 * JG);
-    using S = Smem<T, P, KC, RPMAX>;
+    using S = Smem<T, P, KC, RPMAX, META>;
     static_assert(NG * (P / PT1) == NT, "phase-1 mapping must cover the CTA");
     static_assert(RPMAX % (4 * JG) == 0, "RPMAX multiple of 32");
 
@@ -223,7 +229,7 @@ struct Tile {
     static __device__ __forceinline__ void bwd_phase1(const T* __restrict__ UT, const T* __restrict__ bb,
                                                       const T* __restrict__ VT, const T* __restrict__ SY,
                                                       const T* __restrict__ ST, T* __restrict__ Zg, int ng,
-                                                      int pg) {
+                                                      int pg, T* __restrict__ Zz = nullptr) {
         T a1[PT1][4][4], dz[PT1][4][4];
 #pragma unroll
         for (int i = 0; i < PT1; ++i)
@@ -278,7 +284,68 @@ struct Tile {
                 const T gav = g0 * d1 + g1 * d2 * ax + g2 * d2 * at + g3 * (d3 * ax * ax + d2 * aw);
                 const T gax = g1 * d1 + g3 * T(2) * d2 * ax;
                 st4(Zg + (pg * PT1 + i) * S::ZS + (ng + NG * kk) * 4, gav, gax, g2 * d1, g3 * d1);
+                if constexpr (META)
+                    st4(Zz + (pg * PT1 + i) * S::ZS + (ng + NG * kk) * 4, sg, d1 * ax, d1 * at, d2 * ax * ax + d1 * aw);
             }
+    }
+
+    // META phase 3 (AffineFactoredJet VJP w.r.t. the factors, autodiff.cpp:501-505,524-534,553-560):
+    //   dU_l[k][j]      += sum_{p,c} G[p][k][c] SY[p][j][c]
+    //   dV_{l+1}[k][j'] += sum_{p,c} Z[p][k][c] ST[p][j'][c]
+    //   db_l[k]         += sum_p G[p][k][0]
+    // accumulated over the tile in registers, then added into this CTA's
+    // partial-gradient rows (fixed order -> deterministic).
+    template <int RL, int RN>
+    static __device__ __forceinline__ void phase3(const T* __restrict__ Gs, const T* __restrict__ Zs,
+                                                  const T* __restrict__ SY, const T* __restrict__ ST,
+                                                  T* __restrict__ wg, int64_t oU, int64_t oV, int64_t ob, int k0,
+                                                  int M, int rl_true, int rn_true, int tid) {
+        constexpr int KQ = KC / 4;
+        constexpr int NU = KQ * (RL / 4), NV = KQ * (RN / 4);
+        for (int idx = tid; idx < NU + NV; idx += NT) {
+            const bool isU = idx < NU;
+            const int e = isU ? idx : idx - NU;
+            const int kq = e % KQ, jq = e / KQ;
+            const T* A = isU ? Gs : Zs;
+            const T* B = isU ? SY : ST;
+            T acc[4][4], db[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                db[a] = T(0);
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b] = T(0);
+            }
+#pragma unroll 4
+            for (int p = 0; p < P; ++p) {
+                T g[4][4], y[4][4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    ld4(A + p * S::ZS + (kq * 4 + a) * 4, g[a]);
+                    ld4(B + p * S::SS + (jq * 4 + a) * 4, y[a]);
+                }
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    db[a] += g[a][0];
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) acc[a][b] = fma(g[a][c], y[b][c], acc[a][b]);
+                }
+            }
+            const int rtrue = isU ? rl_true : rn_true;
+            const int64_t base = isU ? oU : oV;
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int k = k0 + kq * 4 + a;
+                if (k >= M) continue;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int j = jq * 4 + b;
+                    if (j < rtrue) wg[base + static_cast<int64_t>(k) * rtrue + j] += acc[a][b];
+                }
+                if (isU && jq == 0) wg[ob + k] += db[a];
+            }
+        }
     }
 
     // phase 2: acc += Zg[p2] * Mat (Mat = KC x RN, row stride RN)
@@ -305,12 +372,13 @@ struct Tile {
     }
 };
 
-template <typename T, int P, int PT1, int NG, int RPMAX, int ACT, bool FAST>
+template <typename T, int P, int PT1, int NG, int RPMAX, int ACT, bool FAST, bool META = false>
 __global__ void __launch_bounds__(JG * P, 1)
 pinn_tile_kernel(const NetV2<T> net, const RunGeom g, const double* __restrict__ pts,
                  const double* __restrict__ svec, const double* __restrict__ mus, const T w,
-                 T* __restrict__ scratch, T* __restrict__ part, unsigned long long* __restrict__ bad) {
-    using K = Tile<T, P, PT1, NG, RPMAX, ACT, FAST>;
+                 T* __restrict__ scratch, T* __restrict__ part, unsigned long long* __restrict__ bad,
+                 T* __restrict__ wgrad = nullptr) {
+    using K = Tile<T, P, PT1, NG, RPMAX, ACT, FAST, META>;
     using S = typename K::S;
     constexpr int NT = K::NT;
     constexpr int KC = K::KC;
@@ -324,7 +392,10 @@ pinn_tile_kernel(const NetV2<T> net, const RunGeom g, const double* __restrict__
     constexpr int BUFSTRIDE = S::OFF_B1 - S::OFF_B0;
     T* red = sm + S::OFF_RED;
     T* acc = sm + S::OFF_ACC;
+    T* Zz = sm + S::OFF_ZZ;
+    T* xts = sm + S::OFF_XT;
     __shared__ __align__(8) uint64_t mbar[2];
+    T* wg = META ? wgrad + static_cast<int64_t>(blockIdx.x) * net.wg_stride : nullptr;
 
     const int tid = threadIdx.x;
     const int ng = tid % NG;
@@ -388,6 +459,10 @@ pinn_tile_kernel(const NetV2<T> net, const RunGeom g, const double* __restrict__
                 const int64_t gp = inst * g.n_per_inst + pi;
                 const T x = valid ? T(pts[2 * gp]) : T(0);
                 const T t = valid ? T(pts[2 * gp + 1]) : T(0);
+                if (META && jg == 0) {
+                    xts[2 * p2] = x;
+                    xts[2 * p2 + 1] = t;
+                }
                 const int r0 = net.r[0], rp0 = net.rp[0];
                 for (int jj = jg; jj < rp0; jj += JG) {
                     T y4[4] = {T(0), T(0), T(0), T(0)};
@@ -471,6 +546,7 @@ pinn_tile_kernel(const NetV2<T> net, const RunGeom g, const double* __restrict__
                     const T gN = valid ? T(2) * N * w : T(0);
                     const T gu[4] = {gN * (-mu2 * (T(1) - T(2) * u[0])), gN * mu0, gN, -gN * mu1};
                     red[P * RPMAX + p] = term;
+                    if constexpr (META) red[P * RPMAX + P + p] = gu[0];
                     for (int j = 0; j < rpL; ++j) {
                         const T uj = j < rL ? net.ulast[j] : T(0);
                         const T sj = j < rL ? T(sL[j]) : T(0);
@@ -479,6 +555,13 @@ pinn_tile_kernel(const NetV2<T> net, const RunGeom g, const double* __restrict__
                         T cd = T(0);
 #pragma unroll
                         for (int c = 0; c < 4; ++c) cd = fma(uj * gu[c], y4[c], cd);
+                        if constexpr (META) {
+                            // dU_{L-1}[0][j] contribution sum_c gu[c] * sy[j][c]
+                            T du = T(0);
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) du = fma(gu[c], sj * y4[c], du);
+                            Zz[p * S::ZS + j] = du;
+                        }
                         red[p * RPMAX + j] = cd;
                         st4(ST + p * S::SS + j * 4, sj * uj * gu[0], sj * uj * gu[1], sj * uj * gu[2],
                             sj * uj * gu[3]);
@@ -494,6 +577,19 @@ pinn_tile_kernel(const NetV2<T> net, const RunGeom g, const double* __restrict__
                     T sacc = T(0);
                     for (int p = 0; p < P; ++p) sacc += red[P * RPMAX + p];
                     acc[0] += sacc;
+                }
+                if constexpr (META) {
+                    if (tid >= 32 && tid < 32 + rL) {
+                        const int j = tid - 32;
+                        T du = T(0);
+                        for (int p = 0; p < P; ++p) du += Zz[p * S::ZS + j];
+                        wg[net.oU[L - 1] + j] += du;
+                    }
+                    if (tid == NT - 2) {
+                        T dbl = T(0);
+                        for (int p = 0; p < P; ++p) dbl += red[P * RPMAX + P + p];
+                        wg[net.ob[L - 1]] += dbl;
+                    }
                 }
                 __syncthreads();
             }
@@ -524,15 +620,34 @@ pinn_tile_kernel(const NetV2<T> net, const RunGeom g, const double* __restrict__
                     const T* VT = bb + KC;
                     const T* Um = VT + rn * KC;
                     if (rl == 4) {
-                        if (rn == 4) K::template bwd_phase1<4, 4>(UT, bb, VT, SY, ST, Zg, ng, pg);
-                        else K::template bwd_phase1<4, RPMAX>(UT, bb, VT, SY, ST, Zg, ng, pg);
+                        if (rn == 4) K::template bwd_phase1<4, 4>(UT, bb, VT, SY, ST, Zg, ng, pg, Zz);
+                        else K::template bwd_phase1<4, RPMAX>(UT, bb, VT, SY, ST, Zg, ng, pg, Zz);
                     } else {
-                        if (rn == 4) K::template bwd_phase1<RPMAX, 4>(UT, bb, VT, SY, ST, Zg, ng, pg);
-                        else K::template bwd_phase1<RPMAX, RPMAX>(UT, bb, VT, SY, ST, Zg, ng, pg);
+                        if (rn == 4) K::template bwd_phase1<RPMAX, 4>(UT, bb, VT, SY, ST, Zg, ng, pg, Zz);
+                        else K::template bwd_phase1<RPMAX, RPMAX>(UT, bb, VT, SY, ST, Zg, ng, pg, Zz);
                     }
                     __syncthreads();
                     if (rl == 4) K::template phase2<4>(Zg, Um, tacc, p2, jg);
                     else K::template phase2<RPMAX>(Zg, Um, tacc, p2, jg);
+                    if constexpr (META) {
+                        const int k0 = ch * KC;
+                        const int M = net.M[l + 1];
+                        if (rl == 4) {
+                            if (rn == 4)
+                                K::template phase3<4, 4>(Zg, Zz, SY, ST, wg, net.oU[l], net.oV[l + 1], net.ob[l], k0, M,
+                                                         net.r[l], net.r[l + 1], tid);
+                            else
+                                K::template phase3<4, RPMAX>(Zg, Zz, SY, ST, wg, net.oU[l], net.oV[l + 1], net.ob[l],
+                                                             k0, M, net.r[l], net.r[l + 1], tid);
+                        } else {
+                            if (rn == 4)
+                                K::template phase3<RPMAX, 4>(Zg, Zz, SY, ST, wg, net.oU[l], net.oV[l + 1], net.ob[l],
+                                                             k0, M, net.r[l], net.r[l + 1], tid);
+                            else
+                                K::template phase3<RPMAX, RPMAX>(Zg, Zz, SY, ST, wg, net.oU[l], net.oV[l + 1],
+                                                                 net.ob[l], k0, M, net.r[l], net.r[l + 1], tid);
+                        }
+                    }
                     __syncthreads();
                 }
                 // dL/ds_l partials and ST = s_l (.) T
@@ -560,6 +675,21 @@ pinn_tile_kernel(const NetV2<T> net, const RunGeom g, const double* __restrict__
                     T sacc = T(0);
                     for (int p = 0; p < P; ++p) sacc += red[p * RPMAX + tid];
                     acc[1 + net.soff[l] + tid] += sacc;
+                }
+                __syncthreads();
+            }
+            if constexpr (META) {
+                // dV_0[i][j] = sum_{p,c} z0[p][c][i] st_0[p][j][c], z0 = (x,t),(1,0),(0,1),(0,0)
+                const int r0 = net.r[0];
+                if (tid < 2 * r0) {
+                    const int i = tid / r0, j = tid % r0;
+                    T dv = T(0);
+                    for (int p = 0; p < P; ++p) {
+                        T st[4];
+                        ld4(ST + p * S::SS + j * 4, st);
+                        dv += xts[2 * p + i] * st[0] + st[1 + i];
+                    }
+                    wg[net.oV[0] + i * r0 + j] += dv;
                 }
                 __syncthreads();
             }

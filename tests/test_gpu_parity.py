@@ -257,3 +257,47 @@ def test_c2_full_size_linearity_and_subsample(gpu, oracle):
     got = gpu.loss_grad_s(pkg.MODEL_LRNR, c["s"], c["mu"])
     want = oracle.lrnr_grad(m.widths, m.ranks, m.params, c["s"], c["mu"], sub, act=pkg.ACT_SIN)
     assert normwise(got["grad_s"], want["grad_s"]) <= TOL32_NORM
+
+
+# ----------------------------------------------------------------------------
+# config 4 (meta): bases, biases and hypernetwork, ParamPacker order
+# ----------------------------------------------------------------------------
+def test_meta_fp64_matches_reference(gpu, golden):
+    g = golden
+    m = pkg.LrnrParams(g["c4_widths"], g["c4_ranks"], g["c4_params"], pkg.ACT_TANH)
+    h = pkg.HyperParams(g["c4_hw"], g["c4_hparams"], g["c3_lo"], g["c3_hi"])
+    gpu.set_lrnr(m, pkg.F64)
+    gpu.set_hyper(h)
+    mus = g["c4_mus"]
+    uniq = [mus[0], mus[-1]]
+    assert np.array_equal(np.concatenate([np.tile(uniq[0], (48, 1)), np.tile(uniq[1], (48, 1))]), mus)
+    gpu.set_points(g["c4_pts"], n_inst=2)
+    r = gpu.meta_loss_grad(np.array(uniq), m.params.size)
+    assert abs(r["value"] - g["c4_value"][0]) <= 1e-12 * g["c4_value"][0]
+    assert normwise(r["grad"], g["c4_grad"]) <= 1e-10
+    assert floor_rel(r["grad"], g["c4_grad"], floor=1e-6) <= 1e-8
+
+
+@pytest.mark.parametrize("act", [pkg.ACT_SIN, pkg.ACT_TANH])
+def test_meta_c4_shape_fp32_matches_oracle(gpu, oracle, act):
+    n_inst, per = 2, 96
+    c = pkg.config4(n_inst=n_inst, pts_per_inst=per, act=act)
+    m, h = c["model"], c["hyper"]
+    gpu.set_lrnr(m, pkg.F32)
+    gpu.set_hyper(h)
+    gpu.set_points(c["pts"], n_inst=n_inst)
+    got = gpu.meta_loss_grad(c["mus"], m.params.size)
+    w = 1.0 / (n_inst * per)
+    nP = m.params.size
+    want = np.zeros(nP + h.n_params)
+    val = 0.0
+    for i in range(n_inst):
+        s_i = oracle.hyper_forward(h.hw, h.params, h.lo, h.hi, c["mus"][i])
+        r = oracle.lrnr_grad(m.widths, m.ranks, m.params, s_i, c["mus"][i], c["pts"][i * per:(i + 1) * per], w=w,
+                             act=act, params_grad=True)
+        val += r["value"]
+        want[:nP] += r["grad_params"]
+        oracle.hyper_vjp(h.hw, h.params, h.lo, h.hi, c["mus"][i], r["grad_s"], out=want[nP:])
+    assert abs(got["value"] - val) <= TOL32_LOSS * abs(val)
+    assert normwise(got["grad"], want) <= TOL32_NORM
+    assert normwise(got["grad"][nP:], want[nP:]) <= TOL32_NORM
