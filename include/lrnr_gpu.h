@@ -86,6 +86,7 @@ int lrnr_gpu_set_stream(lrnr_gpu_ctx* ctx, void* cuda_stream);
  * allows (ranks <= 64), 1 = force the per-point streaming kernel v1. */
 #define LRNR_OPT_FAST_SINCOS 1
 #define LRNR_OPT_KERNEL 2
+#define LRNR_OPT_TILE_P 3   /* FP32 wide-layer tile: 64 points x 512 threads (default) or 32 x 256 (2 CTAs/SM) */
 int lrnr_gpu_set_option(lrnr_gpu_ctx* ctx, int opt, int value);
 /* Number of kernels this context has launched so far (instrumentation). */
 int64_t lrnr_gpu_launch_count(const lrnr_gpu_ctx* ctx);

@@ -1,0 +1,188 @@
+// lrnr_gpu_adapter.hpp -- header-only C++ drop-in over the C ABI (lrnr_gpu.h)
+// for code written against the reference's own headers (/root/reference/proj/include).
+//
+// A reference maintainer adds this header next to proj/include/lrnr and links
+// liblrnr_gpu.so; the training loops then swap the CPU gradient engine for the
+// B200 path at the call sites listed in INTEGRATION.md:
+//
+//   reference (training.cpp:458-461, fine_tune)        B200
+//   ------------------------------------------------  ------------------------------------------
+//   PinnTermEmitter emitter{...};                      lrnr::gpu::Engine eng(0);
+//   bg = run_batch_gradient(at, CoefficientsOnly,      eng.bind(params);      // once (Tape bind_lrnr)
+//          nullptr, std::cref(emitter), n_terms, par); bg = eng.tune_gradient(coeffs, mu, batch);
+//
+// Every entry returns the reference's own types (training::BatchGradResult,
+// training::LossBreakdown, Jet) and throws the reference's exceptions
+// (NonFiniteError{layer_tag}, std::invalid_argument), so callers that catch
+// NonFiniteError (training.cpp:392,462,572) behave identically.
+#pragma once
+
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "lrnr/autodiff.hpp"
+#include "lrnr/model.hpp"
+#include "lrnr/pde.hpp"
+#include "lrnr/training.hpp"
+#include "lrnr_gpu.h"
+
+namespace lrnr {
+namespace gpu {
+
+class Engine {
+public:
+    explicit Engine(int device = 0) {
+        if (lrnr_gpu_create(device, &ctx_) != LRNR_OK) throw std::runtime_error("lrnr_gpu_create failed");
+    }
+    ~Engine() { lrnr_gpu_destroy(ctx_); }
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    // ---- Tape bindings (bind_lrnr / bind_fast / bind_hyper, autodiff.cpp:826-868) ----
+    void bind(const LrnrParams& p, int dtype = LRNR_F64, int act = LRNR_ACT_TANH) {
+        std::vector<double> flat;
+        for (std::size_t l = 0; l < p.depth(); ++l) {
+            flat.insert(flat.end(), p.u[l].data.begin(), p.u[l].data.end());
+            flat.insert(flat.end(), p.v[l].data.begin(), p.v[l].data.end());
+            flat.insert(flat.end(), p.b[l].data.begin(), p.b[l].data.end());
+        }
+        const std::vector<int64_t> w(p.widths.begin(), p.widths.end()), r(p.ranks.begin(), p.ranks.end());
+        check(lrnr_gpu_set_lrnr(ctx_, static_cast<int>(p.depth()), w.data(), r.data(), flat.data(), act, dtype));
+        lrnr_depth_ = p.depth();
+        lrnr_params_ = flat.size();
+    }
+    void bind(const FastParams& f, int dtype = LRNR_F64, int act = LRNR_ACT_TANH) {
+        std::vector<double> flat(f.v_in.data.begin(), f.v_in.data.end());
+        for (std::size_t l = 0; l + 1 < f.depth(); ++l) {
+            flat.insert(flat.end(), f.u_hat[l].data.begin(), f.u_hat[l].data.end());
+            flat.insert(flat.end(), f.b_hat[l].data.begin(), f.b_hat[l].data.end());
+            flat.insert(flat.end(), f.v_hat[l].data.begin(), f.v_hat[l].data.end());
+        }
+        flat.insert(flat.end(), f.u_out.data.begin(), f.u_out.data.end());
+        flat.insert(flat.end(), f.b_out.data.begin(), f.b_out.data.end());
+        const std::vector<int64_t> r(f.ranks.begin(), f.ranks.end()), h(f.red_ranks.begin(), f.red_ranks.end());
+        check(lrnr_gpu_set_fast(ctx_, static_cast<int>(f.depth()), r.data(), h.data(),
+                                static_cast<int64_t>(f.v_in.rows), static_cast<int64_t>(f.u_out.rows), flat.data(),
+                                act, dtype));
+    }
+    void bind(const HyperParams& h) {
+        std::vector<double> flat;
+        std::vector<int64_t> hw{static_cast<int64_t>(h.w.front().cols)};
+        for (std::size_t k = 0; k < h.w.size(); ++k) {
+            flat.insert(flat.end(), h.w[k].data.begin(), h.w[k].data.end());
+            flat.insert(flat.end(), h.b[k].data.begin(), h.b[k].data.end());
+            hw.push_back(static_cast<int64_t>(h.w[k].rows));
+        }
+        const double lo[3] = {h.box.lo[0], h.box.lo[1], h.box.lo[2]};
+        const double hi[3] = {h.box.hi[0], h.box.hi[1], h.box.hi[2]};
+        check(lrnr_gpu_set_hyper(ctx_, static_cast<int>(h.w.size()), hw.data(), flat.data(), lo, hi));
+        hyper_params_ = flat.size();
+    }
+
+    // ---- PinnTermEmitter, fine-tune mode (training.cpp:286-293) +
+    //      run_batch_gradient(CoefficientsOnly) (training.cpp:191-263).
+    // Interior terms only; the initial / periodic branches (training.cpp:307-327)
+    // are not on the device yet -> std::invalid_argument.
+    training::BatchGradResult tune_gradient(const Coefficients& s, const PdeParams& mu,
+                                            const pde::CollocationBatch& batch) {
+        require_interior(batch);
+        return coeff_gradient(LRNR_MODEL_LRNR, s, mu, batch.interior);
+    }
+    // FastLRNR squared-residual objective (emit_fast_jet, autodiff.cpp:905-922).
+    training::BatchGradResult fast_gradient(const Coefficients& s, const PdeParams& mu,
+                                            const std::vector<pde::Point>& pts) {
+        return coeff_gradient(LRNR_MODEL_FAST, s, mu, pts);
+    }
+    // Meta mode interior terms (training.cpp:283-293, lambda_sparse = 0):
+    // pts grouped by instance (mus.size() groups of equal size); ParamPacker
+    // (BasesBiasesAndHyper) order.
+    training::BatchGradResult meta_gradient(const std::vector<PdeParams>& mus, const std::vector<pde::Point>& pts) {
+        const std::size_t n_inst = mus.size();
+        if (n_inst == 0 || pts.size() % n_inst) throw std::invalid_argument("meta_gradient: points not grouped by mu");
+        set_points(pts, n_inst);
+        std::vector<double> m(3 * n_inst);
+        for (std::size_t i = 0; i < n_inst; ++i) {
+            m[3 * i] = mus[i].mu1;
+            m[3 * i + 1] = mus[i].mu2;
+            m[3 * i + 2] = mus[i].mu3;
+        }
+        training::BatchGradResult out;
+        out.grad.assign(lrnr_params_ + hyper_params_, 0.0);
+        check(lrnr_gpu_meta_loss_grad(ctx_, m.data(), 0.0, &out.value, out.grad.data()));
+        out.comps[0] = out.value;
+        return out;
+    }
+
+    // ---- forward only: loss_tune interior part (training.cpp:76-105), jet_forward (model.cpp:357-405) ----
+    training::LossBreakdown loss_tune(const Coefficients& s, const PdeParams& mu, const pde::CollocationBatch& batch) {
+        require_interior(batch);
+        set_points(batch.interior, 1);
+        const std::vector<double> sf = flatten(s);
+        const double m[3] = {mu.mu1, mu.mu2, mu.mu3};
+        training::LossBreakdown lb;
+        check(lrnr_gpu_loss(ctx_, LRNR_MODEL_LRNR, sf.data(), m, 0.0, &lb.residual));
+        lb.total = lb.residual;
+        return lb;
+    }
+    std::vector<Jet> jet_forward(const std::vector<pde::Point>& pts, const Coefficients& s, bool fast = false) {
+        set_points(pts, 1);
+        const std::vector<double> sf = flatten(s);
+        std::vector<double> j(4 * pts.size());
+        check(lrnr_gpu_jets(ctx_, fast ? LRNR_MODEL_FAST : LRNR_MODEL_LRNR, sf.data(), j.data()));
+        std::vector<Jet> out(pts.size());
+        for (std::size_t i = 0; i < pts.size(); ++i) {
+            out[i].value = DenseVector{j[4 * i]};
+            out[i].dx = DenseVector{j[4 * i + 1]};
+            out[i].dt = DenseVector{j[4 * i + 2]};
+            out[i].dxx = DenseVector{j[4 * i + 3]};
+        }
+        return out;
+    }
+
+    lrnr_gpu_ctx* handle() { return ctx_; }
+
+private:
+    void check(int rc) {
+        if (rc == LRNR_OK) return;
+        const std::string msg = lrnr_gpu_last_error(ctx_);
+        if (rc == LRNR_ENONFINITE) throw NonFiniteError(lrnr_gpu_last_layer_tag(ctx_));
+        if (rc == LRNR_EINVAL) throw std::invalid_argument(msg);
+        throw std::runtime_error("lrnr_gpu: " + msg);
+    }
+    static void require_interior(const pde::CollocationBatch& b) {
+        if (!b.initial_x.empty() || !b.periodic_t.empty())
+            throw std::invalid_argument("lrnr::gpu: boundary terms are not on the device path yet");
+    }
+    static std::vector<double> flatten(const Coefficients& s) {
+        std::vector<double> f;
+        for (const auto& v : s.s) f.insert(f.end(), v.data.begin(), v.data.end());
+        return f;
+    }
+    void set_points(const std::vector<pde::Point>& pts, std::size_t n_inst) {
+        std::vector<double> xt(2 * pts.size());
+        for (std::size_t i = 0; i < pts.size(); ++i) {
+            xt[2 * i] = pts[i].x;
+            xt[2 * i + 1] = pts[i].t;
+        }
+        check(lrnr_gpu_set_points(ctx_, xt.data(), static_cast<int64_t>(n_inst),
+                                  static_cast<int64_t>(pts.size() / n_inst)));
+    }
+    training::BatchGradResult coeff_gradient(int model, const Coefficients& s, const PdeParams& mu,
+                                             const std::vector<pde::Point>& pts) {
+        set_points(pts, 1);
+        const std::vector<double> sf = flatten(s);
+        const double m[3] = {mu.mu1, mu.mu2, mu.mu3};
+        training::BatchGradResult out;
+        out.grad.assign(sf.size(), 0.0);
+        check(lrnr_gpu_loss_grad_s(ctx_, model, sf.data(), m, 0.0, &out.value, out.comps, out.grad.data()));
+        return out;
+    }
+
+    lrnr_gpu_ctx* ctx_ = nullptr;
+    std::size_t lrnr_depth_ = 0, lrnr_params_ = 0, hyper_params_ = 0;
+};
+
+}  // namespace gpu
+}  // namespace lrnr

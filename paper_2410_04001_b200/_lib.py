@@ -27,7 +27,7 @@ LRNR_OK, LRNR_EINVAL, LRNR_ENONFINITE, LRNR_ECUDA, LRNR_ENOMEM, LRNR_ESTATE = ra
 ACT_TANH, ACT_SIN = 0, 1
 F64, F32 = 0, 1
 MODEL_LRNR, MODEL_FAST = 0, 1
-OPT_FAST_SINCOS, OPT_KERNEL = 1, 2
+OPT_FAST_SINCOS, OPT_KERNEL, OPT_TILE_P = 1, 2, 3
 
 _lib = None
 

@@ -79,6 +79,7 @@ struct Model {
     int L = 0;
     std::vector<int> M, r, soff, trow;
     int rtotal = 0, rmax = 0;
+    int tile_p = 0;  // LRNR_OPT_TILE_P for FP32 wide layers (0 = default 64)
     // packed host copy (double) in device layout; offsets in elements
     std::vector<double> packed;
     size_t off_V0 = 0, off_ulast = 0;
@@ -92,6 +93,8 @@ struct Model {
         bool ok = false;
         int KC = 0, NG = 0, PT1 = 0, RPMAX = 0, P = 0;
         std::vector<int> rp, nc, yoff;
+        std::vector<int64_t> aoff;
+        int64_t astride = 0;
         int ystride = 0;
         std::vector<double> blocks;
         std::vector<int64_t> sched_off;
@@ -152,7 +155,7 @@ struct lrnr_gpu_ctx {
     int64_t coeff_inst = 0;
     int coeff_rtotal = 0;
     // workspaces
-    lrnr_b200::detail::DevBuf scratch, part, out, bad, acts, G, hgrad, jets, meta_ws;
+    lrnr_b200::detail::DevBuf scratch, ascratch, part, out, bad, acts, G, hgrad, jets, meta_ws;
     int64_t out_rows = 0;
     int out_R1 = 0;
     std::string err;
@@ -244,6 +247,7 @@ void launch_v2(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_grid, g.n_units)));
     const auto& v = META ? m.v2meta : m.v2;
     ctx->scratch.ensure(static_cast<size_t>(grid) * v.ystride * sizeof(T) + 64);
+    ctx->ascratch.ensure(static_cast<size_t>(grid) * v.astride * sizeof(T) + 64);
     ctx->part.ensure(static_cast<size_t>(g.n_units) * R1 * sizeof(T));
     v2::NetV2<T> net{};
     net.L = m.L;
@@ -256,6 +260,8 @@ void launch_v2(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
     }
     for (int l = 0; l <= m.L; ++l) net.soff[l] = m.soff[l];
     net.ystride = v.ystride;
+    for (int l = 0; l + 1 < m.L; ++l) net.aoff[l] = v.aoff[l];
+    net.astride = v.astride;
     net.rtotal = m.rtotal;
     net.blocks = v.dblocks.as<T>();
     net.sched_off = v.dsched_off.as<int64_t>();
@@ -284,7 +290,7 @@ void launch_v2(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
     }
     kern<<<grid, NT, smem, ctx->stream>>>(net, g, ctx->pts, s_dev, mu_dev, static_cast<T>(w),
                                                ctx->scratch.as<T>(), ctx->part.as<T>(),
-                                               ctx->bad.as<unsigned long long>(), wg);
+                                               ctx->bad.as<unsigned long long>(), ctx->ascratch.as<T>(), wg);
     CK(cudaGetLastError());
     if (META) {
         reduce_rows_kernel<T><<<static_cast<unsigned>((n_params + 255) / 256), 256, 0, ctx->stream>>>(

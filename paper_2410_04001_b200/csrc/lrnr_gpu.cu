@@ -101,7 +101,7 @@ void build_v2(Model& m, bool meta) {
         v.NG = 8;
         v.PT1 = 1;
     } else {
-        v.P = 64;
+        v.P = m.tile_p == 32 ? 32 : 64;
         v.NG = 16;
         v.PT1 = 2;
     }
@@ -115,6 +115,13 @@ void build_v2(Model& m, bool meta) {
         yo += v.P * v.rp[l] * 4;
     }
     v.ystride = yo;
+    int64_t ao = 0;
+    v.aoff.assign(L, 0);
+    for (int l = 0; l + 1 < L; ++l) {
+        v.aoff[l] = ao;
+        ao += static_cast<int64_t>((m.M[l + 1] + v.KC - 1) / v.KC) * v.P * v.KC * 4;
+    }
+    v.astride = ao;
     std::vector<int64_t> fwd_off(L), bwd_off(L);
     std::vector<int> fwd_cnt(L), bwd_cnt(L);
     std::vector<std::vector<int64_t>> foff(L), boff(L);
@@ -127,7 +134,7 @@ void build_v2(Model& m, bool meta) {
         auto V = [&](int k, int j) { return (k < M && j < rn) ? rows[static_cast<size_t>(k) * m.trow[l] + rl + j] : 0.0; };
         auto B = [&](int k) { return k < M ? rows[static_cast<size_t>(k) * m.trow[l] + rl + rn] : 0.0; };
         const size_t nf = pad8(static_cast<size_t>(rpl * KC + KC + KC * rpn));
-        const size_t nb = pad8(static_cast<size_t>(rpl * KC + KC + rpn * KC + KC * rpl));
+        const size_t nb = pad8(static_cast<size_t>(rpn * KC + KC * rpl));
         for (int c = 0; c < v.nc[l]; ++c) {
             const int k0 = c * KC;
             auto kq = [&](int q) { return k0 + (q / 4) + NG * (q % 4); };
@@ -141,18 +148,15 @@ void build_v2(Model& m, bool meta) {
             for (int q = 0; q < KC; ++q) B0[rpl * KC + q] = B(kq(q));
             for (int kl = 0; kl < KC; ++kl)
                 for (int j = 0; j < rpn; ++j) B0[rpl * KC + KC + kl * rpn + j] = V(k0 + kl, j);
-            // backward block
+            // backward block: V^T (permuted cols) | U   (A is reloaded, not recomputed)
             boff[l].push_back(static_cast<int64_t>(v.blocks.size()));
             o = v.blocks.size();
             v.blocks.resize(o + nb, 0.0);
             double* B1 = v.blocks.data() + o;
-            for (int j = 0; j < rpl; ++j)
-                for (int q = 0; q < KC; ++q) B1[j * KC + q] = U(kq(q), j);
-            for (int q = 0; q < KC; ++q) B1[rpl * KC + q] = B(kq(q));
             for (int j = 0; j < rpn; ++j)
-                for (int q = 0; q < KC; ++q) B1[rpl * KC + KC + j * KC + q] = V(kq(q), j);
+                for (int q = 0; q < KC; ++q) B1[j * KC + q] = V(kq(q), j);
             for (int kl = 0; kl < KC; ++kl)
-                for (int j = 0; j < rpl; ++j) B1[rpl * KC + KC + rpn * KC + kl * rpl + j] = U(k0 + kl, j);
+                for (int j = 0; j < rpl; ++j) B1[rpn * KC + kl * rpl + j] = U(k0 + kl, j);
         }
         fwd_cnt[l] = static_cast<int>(nf);
         bwd_cnt[l] = static_cast<int>(nb);
@@ -243,6 +247,9 @@ bool dispatch_v2(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const d
         V2CASE(float, 64, 1, 8, 32, 1, false)
         V2CASE(float, 64, 1, 8, 32, 1, true)
         V2CASE(float, 64, 1, 8, 32, 0, false)
+        V2CASE(float, 32, 2, 16, 32, 1, false)
+        V2CASE(float, 32, 2, 16, 32, 1, true)
+        V2CASE(float, 32, 2, 16, 32, 0, false)
         V2CASE(float, 32, 2, 16, 64, 1, false)
         V2CASE(float, 32, 2, 16, 64, 1, true)
         V2CASE(float, 32, 2, 16, 64, 0, false)
@@ -588,7 +595,7 @@ int lrnr_gpu_destroy(lrnr_gpu_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (auto& m : ctx->models) release_model(m);
     ctx->hyper.dev.release();
-    for (DevBuf* b : {&ctx->pts_own, &ctx->s_dev, &ctx->mu_dev, &ctx->scratch, &ctx->part, &ctx->out, &ctx->bad,
+    for (DevBuf* b : {&ctx->pts_own, &ctx->s_dev, &ctx->mu_dev, &ctx->scratch, &ctx->ascratch, &ctx->part, &ctx->out, &ctx->bad,
                       &ctx->acts, &ctx->G, &ctx->hgrad, &ctx->jets, &ctx->meta_ws})
         b->release();
     if (ctx->own) cudaStreamDestroy(ctx->own);
@@ -604,6 +611,13 @@ int lrnr_gpu_set_option(lrnr_gpu_ctx* ctx, int opt, int value) {
     return guarded(ctx, [&] {
         if (opt == LRNR_OPT_FAST_SINCOS) ctx->opt_fast_sincos = value;
         else if (opt == LRNR_OPT_KERNEL) ctx->opt_kernel = value;
+        else if (opt == LRNR_OPT_TILE_P) {
+            require(value == 0 || value == 32 || value == 64, "tile P must be 32 or 64 (0 = default)");
+            for (auto& m : ctx->models) {
+                m.tile_p = value;
+                if (m.set) build_v2(m);
+            }
+        }
         else throw InvalidArg("unknown option");
     });
 }

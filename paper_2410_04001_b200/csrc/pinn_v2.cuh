@@ -60,6 +60,10 @@ struct NetV2 {
     // META: flat ParamPacker offsets of U_l, V_l, b_l (autodiff.cpp:926-934)
     int64_t oU[kMaxL], oV[kMaxL], ob[kMaxL];
     int64_t wg_stride;     // per-CTA partial-gradient stride (elements)
+    // pre-activation jets A stored by the forward sweep, reloaded by the reverse
+    // sweep (no recompute): per CTA, transition l, chunk c at aoff[l] + c*P*KC*4
+    int64_t aoff[kMaxL];
+    int64_t astride;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -161,7 +165,7 @@ template <typename T, int P, int KC, int RPMAX, bool META = false>
 struct Smem {
     static constexpr int ZS = KC * 4 + 4;      // Z/G point stride (padded: conflict-free phase-2 reads)
     static constexpr int SS = RPMAX * 4 + 4;   // SY/ST point stride
-    static constexpr int BUF = 3 * RPMAX * KC + KC + 16;  // max block (bwd: U^T, b, V^T, U)
+    static constexpr int BUF = 2 * RPMAX * KC + KC + 16;  // max block (fwd: U^T, b, V; bwd: V^T, U)
     static constexpr int OFF_Z = 0;
     static constexpr int OFF_SY = OFF_Z + P * ZS;
     static constexpr int OFF_ST = OFF_SY + P * SS;
@@ -187,7 +191,7 @@ struct Tile {
     template <int RL>
     static __device__ __forceinline__ void fwd_phase1(const T* __restrict__ UT, const T* __restrict__ bb,
                                                       const T* __restrict__ SY, T* __restrict__ Zg, int ng,
-                                                      int pg) {
+                                                      int pg, T* __restrict__ Ast) {
         T a1[PT1][4][4];
 #pragma unroll
         for (int i = 0; i < PT1; ++i)
@@ -218,44 +222,36 @@ struct Tile {
             for (int kk = 0; kk < 4; ++kk) {
                 const T av = a1[i][0][kk] + bias[kk], ax = a1[i][1][kk];
                 const T at = a1[i][2][kk], aw = a1[i][3][kk];
+                st4(Ast + ((pg * PT1 + i) * KC + ng + NG * kk) * 4, av, ax, at, aw);
                 T sg, d1, d2, d3;
                 act3<ACT, FAST>(av, sg, d1, d2, d3);
                 st4(Zg + (pg * PT1 + i) * S::ZS + (ng + NG * kk) * 4, sg, d1 * ax, d1 * at, d2 * ax * ax + d1 * aw);
             }
     }
 
-    // backward phase 1: G = VJP(SY U^T + b, ST V^T)
-    template <int RL, int RN>
-    static __device__ __forceinline__ void bwd_phase1(const T* __restrict__ UT, const T* __restrict__ bb,
-                                                      const T* __restrict__ VT, const T* __restrict__ SY,
+    // backward phase 1: G = VJP(A, ST V^T), A reloaded from the forward sweep's store
+    template <int RN>
+    static __device__ __forceinline__ void bwd_phase1(const T* __restrict__ Ast, const T* __restrict__ VT,
                                                       const T* __restrict__ ST, T* __restrict__ Zg, int ng,
                                                       int pg, T* __restrict__ Zz = nullptr) {
         T a1[PT1][4][4], dz[PT1][4][4];
+        // issue the A loads first (L2 / HBM latency hidden behind the DZ GEMM)
+#pragma unroll
+        for (int i = 0; i < PT1; ++i)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                T a4[4];
+                ld4(Ast + ((pg * PT1 + i) * KC + ng + NG * kk) * 4, a4);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) a1[i][c][kk] = a4[c];
+            }
 #pragma unroll
         for (int i = 0; i < PT1; ++i)
 #pragma unroll
             for (int c = 0; c < 4; ++c)
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                    a1[i][c][kk] = T(0);
-                    dz[i][c][kk] = T(0);
-                }
-        const T* syb = SY + pg * PT1 * S::SS;
+                for (int kk = 0; kk < 4; ++kk) dz[i][c][kk] = T(0);
         const T* stb = ST + pg * PT1 * S::SS;
-#pragma unroll
-        for (int j = 0; j < RL; ++j) {
-            T ut[4];
-            ld4(UT + j * KC + ng * 4, ut);
-#pragma unroll
-            for (int i = 0; i < PT1; ++i) {
-                T sy[4];
-                ld4(syb + i * S::SS + j * 4, sy);
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) a1[i][c][kk] = fma(sy[c], ut[kk], a1[i][c][kk]);
-            }
-        }
 #pragma unroll
         for (int j = 0; j < RN; ++j) {
             T vt[4];
@@ -270,13 +266,11 @@ struct Tile {
                     for (int kk = 0; kk < 4; ++kk) dz[i][c][kk] = fma(st[c], vt[kk], dz[i][c][kk]);
             }
         }
-        T bias[4];
-        ld4(bb + ng * 4, bias);
 #pragma unroll
         for (int i = 0; i < PT1; ++i)
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
-                const T av = a1[i][0][kk] + bias[kk], ax = a1[i][1][kk];
+                const T av = a1[i][0][kk], ax = a1[i][1][kk];
                 const T at = a1[i][2][kk], aw = a1[i][3][kk];
                 const T g0 = dz[i][0][kk], g1 = dz[i][1][kk], g2 = dz[i][2][kk], g3 = dz[i][3][kk];
                 T sg, d1, d2, d3;
@@ -372,12 +366,19 @@ struct Tile {
     }
 };
 
+// CTAs per SM: two 256-thread CTAs for FP32 P = 32 tiles (independent
+// barriers overlap), one otherwise.
+template <typename T, int P>
+constexpr int tile_min_blocks() {
+    return (sizeof(T) == 4 && P == 32) ? 2 : 1;
+}
+
 template <typename T, int P, int PT1, int NG, int RPMAX, int ACT, bool FAST, bool META = false>
-__global__ void __launch_bounds__(JG * P, 1)
+__global__ void __launch_bounds__(JG * P, (META ? 1 : tile_min_blocks<T, P>()))
 pinn_tile_kernel(const NetV2<T> net, const RunGeom g, const double* __restrict__ pts,
                  const double* __restrict__ svec, const double* __restrict__ mus, const T w,
                  T* __restrict__ scratch, T* __restrict__ part, unsigned long long* __restrict__ bad,
-                 T* __restrict__ wgrad = nullptr) {
+                 T* __restrict__ ascratch, T* __restrict__ wgrad = nullptr) {
     using K = Tile<T, P, PT1, NG, RPMAX, ACT, FAST, META>;
     using S = typename K::S;
     constexpr int NT = K::NT;
@@ -405,6 +406,7 @@ pinn_tile_kernel(const NetV2<T> net, const RunGeom g, const double* __restrict__
     const int R1 = 1 + net.rtotal;
     const int L = net.L;
     T* scr = scratch + static_cast<int64_t>(blockIdx.x) * net.ystride;
+    T* ascr = ascratch + static_cast<int64_t>(blockIdx.x) * net.astride;
 
     for (int k = tid; k < R1; k += NT) acc[k] = T(0);
     if (tid == 0) {
@@ -494,8 +496,9 @@ pinn_tile_kernel(const NetV2<T> net, const RunGeom g, const double* __restrict__
                     const T* UT = acquire();
                     const T* bb = UT + rl * KC;
                     const T* Vm = bb + KC;
-                    if (rl == 4) K::template fwd_phase1<4>(UT, bb, SY, Zg, ng, pg);
-                    else K::template fwd_phase1<RPMAX>(UT, bb, SY, Zg, ng, pg);
+                    T* Ast = ascr + net.aoff[l] + static_cast<int64_t>(ch) * (P * KC * 4);
+                    if (rl == 4) K::template fwd_phase1<4>(UT, bb, SY, Zg, ng, pg, Ast);
+                    else K::template fwd_phase1<RPMAX>(UT, bb, SY, Zg, ng, pg, Ast);
                     __syncthreads();
                     if (rn == 4) K::template phase2<4>(Zg, Vm, yacc, p2, jg);
                     else K::template phase2<RPMAX>(Zg, Vm, yacc, p2, jg);
@@ -599,7 +602,8 @@ pinn_tile_kernel(const NetV2<T> net, const RunGeom g, const double* __restrict__
                 const int rl = net.rp[l], rn = net.rp[l + 1];
                 const int rtrue = net.r[l];
                 const double* sl = sv + net.soff[l];
-                // SY = s_l (.) y_l
+                // SY = s_l (.) y_l (only the factor gradients of the meta path need it)
+                if (META)
                 for (int j = jg; j < rl; j += JG) {
                     const T sj = j < rtrue ? T(sl[j]) : T(0);
                     T y4[4];
@@ -615,17 +619,11 @@ pinn_tile_kernel(const NetV2<T> net, const RunGeom g, const double* __restrict__
 #pragma unroll
                         for (int b = 0; b < 4; ++b) tacc[a][c][b] = T(0);
                 for (int ch = 0; ch < net.nc[l]; ++ch) {
-                    const T* UT = acquire();
-                    const T* bb = UT + rl * KC;
-                    const T* VT = bb + KC;
+                    const T* VT = acquire();
                     const T* Um = VT + rn * KC;
-                    if (rl == 4) {
-                        if (rn == 4) K::template bwd_phase1<4, 4>(UT, bb, VT, SY, ST, Zg, ng, pg, Zz);
-                        else K::template bwd_phase1<4, RPMAX>(UT, bb, VT, SY, ST, Zg, ng, pg, Zz);
-                    } else {
-                        if (rn == 4) K::template bwd_phase1<RPMAX, 4>(UT, bb, VT, SY, ST, Zg, ng, pg, Zz);
-                        else K::template bwd_phase1<RPMAX, RPMAX>(UT, bb, VT, SY, ST, Zg, ng, pg, Zz);
-                    }
+                    const T* Ast = ascr + net.aoff[l] + static_cast<int64_t>(ch) * (P * KC * 4);
+                    if (rn == 4) K::template bwd_phase1<4>(Ast, VT, ST, Zg, ng, pg, Zz);
+                    else K::template bwd_phase1<RPMAX>(Ast, VT, ST, Zg, ng, pg, Zz);
                     __syncthreads();
                     if (rl == 4) K::template phase2<4>(Zg, Um, tacc, p2, jg);
                     else K::template phase2<RPMAX>(Zg, Um, tacc, p2, jg);

@@ -1,0 +1,105 @@
+// Drop-in check of include/lrnr_gpu_adapter.hpp against the UNMODIFIED reference:
+// the same fine-tune gradient (PinnTermEmitter interior terms through
+// run_batch_gradient, training.cpp:191-329) computed by the reference on the CPU
+// and by lrnr::gpu::Engine on the B200, on BASELINE config 0, plus the
+// FastLRNR and NonFiniteError paths.  Exit code 0 = parity within 1e-10.
+// Built by oracle/Makefile into oracle/_ref/adapter_test (needs a GPU to run).
+#include <cmath>
+#include <cstdio>
+
+#include "lrnr/autodiff.hpp"
+#include "lrnr/reduction.hpp"
+#include "lrnr/training.hpp"
+#include "lrnr_gpu_adapter.hpp"
+
+using namespace lrnr;
+
+static double floor_rel(const std::vector<double>& g, const std::vector<double>& w) {
+    double mx = 0.0, worst = 0.0;
+    for (double v : w) mx = std::max(mx, std::fabs(v));
+    for (std::size_t i = 0; i < w.size(); ++i)
+        worst = std::max(worst, std::fabs(g[i] - w[i]) / std::max(std::fabs(w[i]), 1e-3 * mx));
+    return worst;
+}
+
+int main() {
+    Rng rng(2410);
+    LrnrParams p = make_lrnr_params({2, 100, 100, 100, 1}, {2, 10, 10, 1}, rng, true, 0.5);
+    Coefficients s = make_coefficients(p.ranks, rng, 0.2, 1.0);
+    const PdeParams mu{30.0, 0.0, 0.0};
+    pde::CollocationBatch batch = pde::sample_collocation(4001, 4096, 0, 0, ParamDomain{}, false);
+
+    // reference: PinnTermEmitter-equivalent interior emitter through run_batch_gradient
+    Trainables at{&p, nullptr, &s};
+    const double w = 1.0 / static_cast<double>(batch.interior.size());
+    training::EmitFn emit = [&](TapeBindings& ctx, const training::ExtraBindings&, std::size_t i,
+                                double* comps) -> NodeId {
+        Tape& tp = ctx.tape;
+        const NodeId jet = emit_lrnr_jet(tp, batch.interior[i].x, batch.interior[i].t, ctx.lrnr, ctx.coeffs.s_leaves);
+        const NodeId term = tp.scale(tp.square(tp.residual_cdr(jet, mu)), w);
+        comps[0] += tp.value(term);
+        return term;
+    };
+    training::ParallelConfig par{8, 64};
+    training::BatchGradResult ref = training::run_batch_gradient(at, ParamSelector::CoefficientsOnly, nullptr, emit,
+                                                                 batch.interior.size(), par);
+
+    lrnr::gpu::Engine eng(0);
+    eng.bind(p, LRNR_F64);
+    training::BatchGradResult got = eng.tune_gradient(s, mu, batch);
+    const double ev = std::fabs(got.value - ref.value) / ref.value;
+    const double eg = floor_rel(got.grad, ref.grad);
+    std::printf("fine-tune gradient: value rel err %.3e, dL/ds floor-rel err %.3e\n", ev, eg);
+
+    // FastLRNR from the reference's own EIM reduction
+    HyperParams h;
+    h.w.emplace_back(23, 3);
+    DenseVector hb(23);
+    std::size_t o = 0;
+    for (auto& sl : s.s)
+        for (double v : sl.data) hb[o++] = v;
+    h.b.push_back(hb);
+    h.split = p.ranks;
+    h.box = ParamDomain::d1();
+    auto X = reduction::SamplingSetX::uniform_grid(4, 3);
+    auto snaps = reduction::harvest_snapshots(p, h, X, 8, 0.05, {mu}, 777);
+    std::vector<reduction::EimBasis> bases;
+    for (std::size_t l = 0; l + 1 < p.depth(); ++l) bases.push_back(reduction::eim_greedy(snaps.layers[l], 10));
+    FastParams f = reduction::build_fastparams(p, bases);
+    Trainables atf{nullptr, nullptr, &s};
+    training::SetupFn setup = [&](TapeBindings& ctx) {
+        training::ExtraBindings ex;
+        ex.fast = bind_fast(ctx.tape, f);
+        ex.has_fast = true;
+        return ex;
+    };
+    training::EmitFn emitf = [&](TapeBindings& ctx, const training::ExtraBindings& ex, std::size_t i,
+                                 double* comps) -> NodeId {
+        Tape& tp = ctx.tape;
+        const NodeId jet = emit_fast_jet(tp, batch.interior[i].x, batch.interior[i].t, ex.fast, ctx.coeffs.s_leaves);
+        const NodeId term = tp.scale(tp.square(tp.residual_cdr(jet, mu)), w);
+        comps[0] += tp.value(term);
+        return term;
+    };
+    training::BatchGradResult reff =
+        training::run_batch_gradient(atf, ParamSelector::CoefficientsOnly, setup, emitf, batch.interior.size(), par);
+    eng.bind(f, LRNR_F64);
+    training::BatchGradResult gotf = eng.fast_gradient(s, mu, batch.interior);
+    const double evf = std::fabs(gotf.value - reff.value) / reff.value;
+    const double egf = floor_rel(gotf.grad, reff.grad);
+    std::printf("FastLRNR gradient: value rel err %.3e, dL/ds floor-rel err %.3e\n", evf, egf);
+
+    // NonFiniteError surfaces as the reference's exception type
+    Coefficients bad = s;
+    bad.s[1][0] = std::nan("");
+    bool threw = false;
+    try {
+        eng.tune_gradient(bad, mu, batch);
+    } catch (const NonFiniteError& e) {
+        threw = e.layer_tag == -1;
+    }
+    std::printf("NonFiniteError mapped: %s\n", threw ? "yes" : "NO");
+    const bool ok = ev <= 1e-12 && eg <= 1e-10 && evf <= 1e-12 && egf <= 1e-10 && threw;
+    std::printf("%s\n", ok ? "ADAPTER PARITY OK" : "ADAPTER PARITY FAILED");
+    return ok ? 0 : 1;
+}

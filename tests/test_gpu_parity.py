@@ -301,3 +301,19 @@ def test_meta_c4_shape_fp32_matches_oracle(gpu, oracle, act):
     assert abs(got["value"] - val) <= TOL32_LOSS * abs(val)
     assert normwise(got["grad"], want) <= TOL32_NORM
     assert normwise(got["grad"][nP:], want[nP:]) <= TOL32_NORM
+
+
+def test_cpp_adapter_drop_in_against_reference():
+    """include/lrnr_gpu_adapter.hpp compiled against the reference's own headers and
+    objects (oracle/_ref/adapter_test): same fine-tune / FastLRNR gradient as
+    run_batch_gradient, NonFiniteError mapping."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "adapter_test")
+    if not os.path.exists(exe):
+        pytest.skip("adapter_test is built only where /root/reference exists (build container)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "ADAPTER PARITY OK" in r.stdout
