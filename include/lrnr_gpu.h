@@ -81,9 +81,13 @@ int lrnr_gpu_last_layer_tag(const lrnr_gpu_ctx* ctx);
  * NULL restores the context's own stream. */
 int lrnr_gpu_set_stream(lrnr_gpu_ctx* ctx, void* cuda_stream);
 /* Options.  LRNR_OPT_FAST_SINCOS (FP32 sin networks): 1 = sin/cos from the SFU
- * approximations after a Cody-Waite reduction (~1e-6 absolute), 0 = libdevice
- * sincosf (default).  LRNR_OPT_KERNEL: 0 = tile-GEMM kernel v2 where the shape
- * allows (ranks <= 64), 1 = force the per-point streaming kernel v1. */
+ * approximations after a Cody-Waite reduction (~4e-7 absolute), 0 = polynomial
+ * sin/cos after a 3-term reduction (~1.5 ulp, default).  LRNR_OPT_KERNEL:
+ * 0 = auto (default): FP32 LRNR with ranks <= 32 on the tcgen05 tensor-core
+ * tile kernel (3xTF32), other FP32/FP64 shapes with ranks <= 64 on the FMA
+ * tile-GEMM kernel, the rest on the per-point streaming kernel;
+ * 1 = force the streaming kernel, 2 = tensor-core kernel wherever it applies
+ * (also FastLRNR), 3 = FMA tile kernel (no tensor cores). */
 #define LRNR_OPT_FAST_SINCOS 1
 #define LRNR_OPT_KERNEL 2
 #define LRNR_OPT_TILE_P 3   /* FP32 wide-layer tile: 64 points x 512 threads (default) or 32 x 256 (2 CTAs/SM) */

@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "liblrnr_gpu.so")
+LIB_PATH = os.environ.get("LRNR_GPU_LIB") or os.path.join(PKG, "liblrnr_gpu.so")
 
 # every symbol include/lrnr_gpu.h declares
 EXPORTS = (
@@ -28,6 +28,8 @@ ACT_TANH, ACT_SIN = 0, 1
 F64, F32 = 0, 1
 MODEL_LRNR, MODEL_FAST = 0, 1
 OPT_FAST_SINCOS, OPT_KERNEL, OPT_TILE_P = 1, 2, 3
+# LRNR_OPT_KERNEL values
+KERNEL_AUTO, KERNEL_STREAM, KERNEL_TC, KERNEL_FMA_TILE = 0, 1, 2, 3
 
 _lib = None
 

@@ -101,6 +101,18 @@ struct Model {
         std::vector<int> sched_cnt;
         DevBuf dblocks, dsched_off, dsched_bytes;
     } v2, v2meta;
+    // tensor-core (tcgen05, 3xTF32) layout: chunk blocks with hi / lo canonical tiles
+    struct TC {
+        bool ok = false;
+        std::vector<int> rk, rn, nc, yoff;
+        std::vector<int64_t> aoff;
+        int64_t astride = 0;
+        int ystride = 0;
+        std::vector<float> blocks;
+        std::vector<int64_t> sched_off;
+        std::vector<int> sched_cnt;
+        DevBuf dblocks, dsched_off, dsched_bytes;
+    } tc;
 };
 
 struct Hyper {
@@ -117,6 +129,7 @@ void build_layout(Model& m);
 void release_model(Model& m);
 void upload_model(Model& m);
 void build_v2(Model& m, bool meta = false);
+void build_tc(Model& m);
 
 template <class T>
 DevNet<T> dev_net(const Model& m) {
@@ -162,7 +175,7 @@ struct lrnr_gpu_ctx {
     int tag = -1;
     int64_t launches = 0;
     int opt_fast_sincos = 0;  // LRNR_OPT_FAST_SINCOS
-    int opt_kernel = 0;       // LRNR_OPT_KERNEL: 0 auto (v2 where supported), 1 force v1
+    int opt_kernel = 0;       // LRNR_OPT_KERNEL: 0 auto, 1 streaming, 2 tensor core, 3 FMA tile
 };
 
 namespace lrnr_b200 {

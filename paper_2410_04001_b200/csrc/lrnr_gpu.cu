@@ -18,6 +18,7 @@
 #include "internal.h"
 #include "meta_kernels.cuh"
 #include "instances.h"
+#include "pinn_tc.cuh"
 
 using namespace lrnr_b200;
 using namespace lrnr_b200::detail;
@@ -55,6 +56,9 @@ void release_model(Model& m) {
     m.v2meta.dblocks.release();
     m.v2meta.dsched_off.release();
     m.v2meta.dsched_bytes.release();
+    m.tc.dblocks.release();
+    m.tc.dsched_off.release();
+    m.tc.dsched_bytes.release();
 }
 
 void upload_model(Model& m) {
@@ -192,6 +196,117 @@ void build_v2(Model& m, bool meta) {
     v.ok = true;
 }
 
+// tf32 round-to-nearest (ties away), as cvt.rna.tf32.f32
+static float tf32_rna(float x) {
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    if ((u & 0x7F800000u) != 0x7F800000u) u = (u + 0x1000u) & 0xFFFFE000u;
+    float r;
+    std::memcpy(&r, &u, 4);
+    return r;
+}
+
+// Tensor-core layout (pinn_tc.cuh): per transition l and chunk of 32 neurons,
+//   forward block  [U_H | U_L (B: N = 32 neurons x K = rk_l, K-major canonical) |
+//                   bias (32) | VT_H | VT_L (B: N = rn_{l+1} x K = 32 neurons)]
+//   backward block [V_H | V_L (N = 32 neurons x K = rk_{l+1}) | UT_H | UT_L (N = rn_l x K = 32)]
+// hi = tf32(x), lo = x - hi (3xTF32).
+void build_tc(Model& m) {
+    auto& v = m.tc;
+    v = Model::TC{};
+    if (m.dtype != LRNR_F32) return;
+    const int L = m.L;
+    const int KC = tc::KC;
+    for (int l = 0; l < L; ++l)
+        if (m.r[l] > tc::RP) return;
+    v.rk.resize(L);
+    v.rn.resize(L);
+    for (int l = 0; l < L; ++l) {
+        v.rk[l] = (m.r[l] + 7) & ~7;
+        v.rn[l] = m.r[l] <= 16 ? 16 : 32;
+    }
+    v.nc.assign(L, 0);
+    v.yoff.assign(L, 0);
+    v.aoff.assign(L, 0);
+    int yo = 0;
+    for (int l = 0; l < L; ++l) {
+        v.yoff[l] = yo;
+        yo += tc::P * m.r[l] * 4;
+    }
+    v.ystride = yo;
+    int64_t ao = 0;
+    for (int l = 0; l + 1 < L; ++l) {
+        v.nc[l] = (m.M[l + 1] + KC - 1) / KC;
+        v.aoff[l] = ao;
+        ao += static_cast<int64_t>(v.nc[l]) * tc::P * KC * 4;
+    }
+    v.astride = ao;
+    std::vector<std::vector<int64_t>> foff(L), boff(L);
+    std::vector<int> fcnt(L), bcnt(L);
+    auto put = [](float* hi, float* lo, int off, double x) {
+        const float f = static_cast<float>(x);
+        const float h = tf32_rna(f);
+        hi[off] = h;
+        lo[off] = f - h;
+    };
+    for (int l = 0; l + 1 < L; ++l) {
+        const int rl = m.r[l], rn = m.r[l + 1], M = m.M[l + 1];
+        const int rkl = v.rk[l], rkn = v.rk[l + 1], rnl = v.rn[l], rnn = v.rn[l + 1];
+        const double* rows = m.packed.data() + m.off_trans[l];
+        auto U = [&](int k, int j) { return (k < M && j < rl) ? rows[static_cast<size_t>(k) * m.trow[l] + j] : 0.0; };
+        auto V = [&](int k, int j) { return (k < M && j < rn) ? rows[static_cast<size_t>(k) * m.trow[l] + rl + j] : 0.0; };
+        auto B = [&](int k) { return k < M ? rows[static_cast<size_t>(k) * m.trow[l] + rl + rn] : 0.0; };
+        const int nf = 2 * KC * rkl + 32 + 2 * rnn * KC;
+        const int nb = 2 * KC * rkn + 2 * rnl * KC;
+        fcnt[l] = nf;
+        bcnt[l] = nb;
+        for (int c = 0; c < v.nc[l]; ++c) {
+            const int k0 = c * KC;
+            size_t o = v.blocks.size();
+            foff[l].push_back(static_cast<int64_t>(o));
+            v.blocks.resize(o + nf, 0.f);
+            float* f = v.blocks.data() + o;
+            float *UH = f, *UL = f + KC * rkl, *bias = UL + KC * rkl, *VTH = bias + 32, *VTL = VTH + rnn * KC;
+            for (int n = 0; n < KC; ++n)
+                for (int j = 0; j < rkl; ++j) put(UH, UL, umma::kmaj_off(n, j, KC), U(k0 + n, j));
+            for (int n = 0; n < KC; ++n) bias[n] = static_cast<float>(B(k0 + n));
+            for (int j = 0; j < rnn; ++j)
+                for (int n = 0; n < KC; ++n) put(VTH, VTL, umma::kmaj_off(j, n, rnn), V(k0 + n, j));
+            o = v.blocks.size();
+            boff[l].push_back(static_cast<int64_t>(o));
+            v.blocks.resize(o + nb, 0.f);
+            float* bb = v.blocks.data() + o;
+            float *VH = bb, *VL = bb + KC * rkn, *UTH = VL + KC * rkn, *UTL = UTH + rnl * KC;
+            for (int n = 0; n < KC; ++n)
+                for (int j = 0; j < rkn; ++j) put(VH, VL, umma::kmaj_off(n, j, KC), V(k0 + n, j));
+            for (int j = 0; j < rnl; ++j)
+                for (int n = 0; n < KC; ++n) put(UTH, UTL, umma::kmaj_off(j, n, rnl), U(k0 + n, j));
+        }
+    }
+    for (int l = 0; l + 1 < L; ++l)
+        for (int c = 0; c < v.nc[l]; ++c) {
+            v.sched_off.push_back(foff[l][c]);
+            v.sched_cnt.push_back(fcnt[l]);
+        }
+    for (int l = L - 2; l >= 0; --l)
+        for (int c = 0; c < v.nc[l]; ++c) {
+            v.sched_off.push_back(boff[l][c]);
+            v.sched_cnt.push_back(bcnt[l]);
+        }
+    v.dblocks.ensure(std::max<size_t>(v.blocks.size(), 8) * 4);
+    if (!v.blocks.empty()) CK(cudaMemcpy(v.dblocks.p, v.blocks.data(), v.blocks.size() * 4, cudaMemcpyHostToDevice));
+    const size_t ns = std::max<size_t>(v.sched_off.size(), 1);
+    std::vector<int> bytes(v.sched_cnt.size());
+    for (size_t i = 0; i < bytes.size(); ++i) bytes[i] = v.sched_cnt[i] * 4;
+    v.dsched_off.ensure(ns * sizeof(int64_t));
+    v.dsched_bytes.ensure(ns * sizeof(int));
+    if (!v.sched_off.empty()) {
+        CK(cudaMemcpy(v.dsched_off.p, v.sched_off.data(), v.sched_off.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(v.dsched_bytes.p, bytes.data(), bytes.size() * sizeof(int), cudaMemcpyHostToDevice));
+    }
+    v.ok = true;
+}
+
 }  // namespace detail
 }  // namespace lrnr_b200
 
@@ -230,10 +345,85 @@ int guarded(lrnr_gpu_ctx* ctx, F&& f) {
 // ---------------------------------------------------------------------------
 // launch planning
 // ---------------------------------------------------------------------------
+template <int ACT, bool FAST>
+void launch_tc(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
+               double* dev_out) {
+    const auto& v = m.tc;
+    const int64_t n_inst = ctx->n_inst, n_per = ctx->n_per;
+    const int R1 = 1 + m.rtotal;
+    if (R1 > 1024) throw InvalidArg("tensor-core path supports r_total < 1024");
+    const size_t smem = static_cast<size_t>(tc::SMEM_FLOATS) * sizeof(float);
+    auto kern = tc::pinn_tc_kernel<ACT, FAST>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    RunGeom g{};
+    g.P = tc::P;
+    g.n_per_inst = n_per;
+    g.tiles_per_inst = static_cast<int>((n_per + tc::P - 1) / tc::P);
+    const int64_t total_tiles = static_cast<int64_t>(g.tiles_per_inst) * n_inst;
+    const int64_t max_grid = ctx->num_sms;  // one CTA per SM: it owns all 512 TMEM columns
+    int64_t tpu = (total_tiles + max_grid * 4 - 1) / (max_grid * 4);
+    tpu = std::max<int64_t>(1, std::min<int64_t>(tpu, g.tiles_per_inst));
+    g.tiles_per_unit = static_cast<int>(tpu);
+    g.units_per_inst = static_cast<int>((g.tiles_per_inst + tpu - 1) / tpu);
+    g.n_units = static_cast<int64_t>(g.units_per_inst) * n_inst;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_grid, g.n_units)));
+    ctx->scratch.ensure(static_cast<size_t>(grid) * v.ystride * sizeof(float) + 64);
+    ctx->ascratch.ensure(static_cast<size_t>(grid) * v.astride * sizeof(float) + 64);
+    ctx->part.ensure(static_cast<size_t>(g.n_units) * R1 * sizeof(float));
+    tc::NetTC<> net{};
+    net.L = m.L;
+    for (int l = 0; l <= m.L; ++l) {
+        net.M[l] = m.M[l];
+        net.soff[l] = m.soff[l];
+    }
+    for (int l = 0; l < m.L; ++l) {
+        net.r[l] = m.r[l];
+        net.rk[l] = v.rk[l];
+        net.rn[l] = v.rn[l];
+        net.nc[l] = v.nc[l];
+        net.yoff[l] = v.yoff[l];
+        net.aoff[l] = v.aoff[l];
+    }
+    net.ystride = v.ystride;
+    net.astride = v.astride;
+    net.rtotal = m.rtotal;
+    net.blocks = v.dblocks.as<float>();
+    net.sched_off = v.dsched_off.as<int64_t>();
+    net.sched_bytes = v.dsched_bytes.as<int>();
+    net.sched_len = static_cast<int>(v.sched_off.size());
+    const float* base = m.dev.as<float>();
+    net.V0 = base + m.off_V0;
+    net.ulast = base + m.off_ulast;
+    kern<<<grid, tc::NT, smem, ctx->stream>>>(net, g, ctx->pts, s_dev, mu_dev, static_cast<float>(w),
+                                              ctx->scratch.as<float>(), ctx->ascratch.as<float>(),
+                                              ctx->part.as<float>(), ctx->bad.as<unsigned long long>());
+    CK(cudaGetLastError());
+    dim3 rg((R1 + 127) / 128, static_cast<unsigned>(n_inst));
+    reduce_units_kernel<float><<<rg, 128, 0, ctx->stream>>>(ctx->part.as<float>(), g.units_per_inst, R1, n_inst, dev_out);
+    CK(cudaGetLastError());
+    ctx->launches += 2;
+}
+
+bool dispatch_tc(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
+                 double* dev_out) {
+    // auto (0): the tensor-core kernel for the wide FP32 LRNR; the narrow FastLRNR
+    // stays on the FMA tile kernel (measured faster there).  2 forces it.
+    const bool want = ctx->opt_kernel == 2 || (ctx->opt_kernel == 0 && m.kind == LRNR_MODEL_LRNR);
+    if (!m.tc.ok || !want) return false;
+    const bool fast = ctx->opt_fast_sincos != 0;
+    if (m.act == LRNR_ACT_SIN) {
+        if (fast) launch_tc<1, true>(ctx, m, s_dev, mu_dev, w, dev_out);
+        else launch_tc<1, false>(ctx, m, s_dev, mu_dev, w, dev_out);
+    } else {
+        launch_tc<0, false>(ctx, m, s_dev, mu_dev, w, dev_out);
+    }
+    return true;
+}
+
 bool dispatch_v2(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
                  double* dev_out) {
     const auto& v = m.v2;
-    if (!v.ok || ctx->opt_kernel == 1) return false;
+    if (!v.ok || ctx->opt_kernel == 1) return false;  // 0 / 2 (not tc-eligible) / 3 (force)
     const bool fast = ctx->opt_fast_sincos != 0;
 #define V2CASE(T_, P_, PT1_, NG_, RP_, ACT_, FAST_)                                             \
     if (v.P == P_ && v.PT1 == PT1_ && v.NG == NG_ && v.RPMAX == RP_ && m.act == ACT_ && fast == FAST_) { \
@@ -432,6 +622,8 @@ double* run_resident(lrnr_gpu_ctx* ctx, const Model& m, double w, double* dev_ou
         return dev_out;
     }
     const double wt = w > 0.0 ? w : 1.0 / static_cast<double>(ctx->n_inst * ctx->n_per);
+    if (MODE == 0 && dispatch_tc(ctx, m, ctx->s_dev.as<double>(), ctx->mu_dev.as<double>(), wt, dev_out))
+        return dev_out;
     if (MODE == 0 && dispatch_v2(ctx, m, ctx->s_dev.as<double>(), ctx->mu_dev.as<double>(), wt, dev_out))
         return dev_out;
     dispatch_pinn<MODE>(ctx, m, ctx->s_dev.as<double>(), ctx->mu_dev.as<double>(), wt, dev_out, jets_dev);
@@ -677,6 +869,7 @@ int lrnr_gpu_set_lrnr(lrnr_gpu_ctx* ctx, int L, const int64_t* widths, const int
         dst = std::move(m);
         upload_model(dst);
         build_v2(dst);
+        build_tc(dst);
     });
 }
 
@@ -726,6 +919,7 @@ int lrnr_gpu_set_fast(lrnr_gpu_ctx* ctx, int L, const int64_t* ranks, const int6
         dst = std::move(m);
         upload_model(dst);
         build_v2(dst);
+        build_tc(dst);
     });
 }
 
@@ -932,6 +1126,19 @@ int lrnr_gpu_meta_loss_grad(lrnr_gpu_ctx* ctx, const double* mus, double w, doub
         meta_step(ctx, m, wt, out_grad, &value);
         if (out_value) *out_value = value;
     });
+}
+
+// dev aid: per-phase cycle counters of the tensor-core kernel (CTA 0), filled
+// only when built with -DLRNR_TC_TIMING; zeros otherwise.
+int lrnr_dev_tc_timing(unsigned long long* out16) {
+#ifdef LRNR_TC_TIMING
+    cudaMemcpyFromSymbol(out16, tc::g_tc_timing, 16 * sizeof(unsigned long long));
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(tc::g_tc_timing, z, sizeof(z));
+#else
+    for (int i = 0; i < 16; ++i) out16[i] = 0;
+#endif
+    return 0;
 }
 
 int lrnr_gpu_fma_peak(lrnr_gpu_ctx* ctx, int dtype, double* out_tflops) {

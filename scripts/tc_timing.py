@@ -1,0 +1,35 @@
+"""Per-phase cycle breakdown of the tensor-core kernel, CTA 0 (dev aid).
+LRNR_GPU_LIB=scripts/liblrnr_gpu_timing.so python scripts/tc_timing.py"""
+import sys, os, ctypes as C
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import paper_2410_04001_b200 as pkg
+from paper_2410_04001_b200 import _lib
+lib = _lib.load()
+n = 148 * 128 * 4
+c = pkg.config2(n_points=n, with_fast=False)
+ctx = pkg.GpuContext(0)
+ctx.set_option(_lib.OPT_KERNEL, 2)
+ctx.set_option(_lib.OPT_FAST_SINCOS, int(sys.argv[1]) if len(sys.argv) > 1 else 0)
+ctx.set_lrnr(c['model'], pkg.F32); ctx.set_points(c['pts'])
+ctx.loss_grad_s(pkg.MODEL_LRNR, c['s'], c['mu'])
+out = (C.c_ulonglong * 16)()
+lib.lrnr_dev_tc_timing(out)
+ctx.loss_grad_s(pkg.MODEL_LRNR, c['s'], c['mu'])
+lib.lrnr_dev_tc_timing(out)
+names = ["fwd: wait P2(ch-1) + add_y", "fwd: P1/P2 issue -> chunk top", "fwd: wait mma1 (P1)", "fwd: epilogue act jet + A store",
+         "fwd: Z split/st + sync", "fwd: trans-end wait P2", "fwd: trans end Y->SY", "output layer",
+         "bwd: wait P2(ch-1) + add_t", "bwd: chunk top + A loads", "bwd: wait mma1 (P1)", "bwd: epilogue VJP",
+         "bwd: G split/st + sync", "bwd: trans-end wait P2", "bwd: trans end + ds reduce", "-"]
+tot = sum(out[:15])
+tiles = 4
+for i in range(15):
+    print(f"{names[i]:40s} {out[i]/tiles:12.0f} cycles/tile  {out[i]/tot*100:5.1f}%")
+print(f"tid0 fwd issue P1+P2 (incl. weight wait): {out[15]/tiles/48:.0f} cycles/chunk")
+print("total cycles per tile", tot / tiles, " chunks per tile", 96)
+import time
+import torch
+for _ in range(2): ctx.loss_grad_s(pkg.MODEL_LRNR, c['s'], c['mu'])
+torch.cuda.synchronize(); t0 = time.perf_counter()
+for _ in range(5): ctx.loss_grad_s(pkg.MODEL_LRNR, c['s'], c['mu'])
+print(f"host-timed per call (n={n}): {(time.perf_counter()-t0)/5*1e3:.3f} ms")

@@ -19,6 +19,23 @@ TOL32_NORM = 1e-4
 TOL32_LOSS = 1e-4
 
 
+# FP32 kernel choices (LRNR_OPT_KERNEL): auto = tcgen05 for the LRNR + FMA tile
+# for FastLRNR; forced tcgen05 (FastLRNR too); FMA tile; per-point streaming
+FP32_KERNELS = [pkg.KERNEL_AUTO, pkg.KERNEL_TC, pkg.KERNEL_FMA_TILE, pkg.KERNEL_STREAM]
+
+
+@pytest.fixture
+def opts(gpu):
+    """Set context options for one test; restore the defaults afterwards."""
+
+    def apply(kernel=pkg.KERNEL_AUTO, fast_sincos=0):
+        gpu.set_option(pkg.OPT_KERNEL, kernel)
+        gpu.set_option(pkg.OPT_FAST_SINCOS, fast_sincos)
+
+    yield apply
+    apply()
+
+
 def lrnr_from_golden(g, prefix, act=pkg.ACT_TANH):
     return pkg.LrnrParams(g[prefix + "_widths"], g[prefix + "_ranks"], g[prefix + "_params"], act)
 
@@ -84,7 +101,9 @@ def test_identity_reduction_equals_lrnr(gpu, golden):
 # ----------------------------------------------------------------------------
 # config 2 shapes (FP32): tanh against the reference, sin against the oracle
 # ----------------------------------------------------------------------------
-def test_c2_tanh_fp32_matches_reference(gpu, golden):
+@pytest.mark.parametrize("kernel", FP32_KERNELS)
+def test_c2_tanh_fp32_matches_reference(gpu, golden, opts, kernel):
+    opts(kernel)
     m = lrnr_from_golden(golden, "c2")
     gpu.set_lrnr(m, pkg.F32)
     gpu.set_points(golden["c2_pts"])
@@ -99,8 +118,12 @@ def test_c2_tanh_fp32_matches_reference(gpu, golden):
     assert normwise(rf["grad_s"], golden["c2_fast_grad_s"]) <= TOL32_NORM
 
 
-@pytest.mark.parametrize("dtype", [pkg.F32, pkg.F64])
-def test_c2_sin_matches_oracle(gpu, oracle, dtype):
+@pytest.mark.parametrize(
+    "dtype,kernel,fast_sincos",
+    [(pkg.F64, pkg.KERNEL_AUTO, 0)] + [(pkg.F32, k, fs) for k in FP32_KERNELS for fs in (0, 1)],
+)
+def test_c2_sin_matches_oracle(gpu, oracle, opts, dtype, kernel, fast_sincos):
+    opts(kernel, fast_sincos)
     c = pkg.config2(n_points=2048, act=pkg.ACT_SIN)
     m, f = c["model"], c["fast"]
     gpu.set_lrnr(m, dtype)
@@ -224,6 +247,59 @@ def test_bitwise_deterministic(gpu, golden):
     a = gpu.loss_grad_s(pkg.MODEL_LRNR, golden["c2_s"], golden["c2_mu"])
     b = gpu.loss_grad_s(pkg.MODEL_LRNR, golden["c2_s"], golden["c2_mu"])
     assert a["value"] == b["value"] and np.array_equal(a["grad_s"], b["grad_s"])
+
+
+@pytest.mark.parametrize("kernel", [pkg.KERNEL_TC, pkg.KERNEL_FMA_TILE])
+@pytest.mark.parametrize("n", [1, 127, 129, 1000])
+def test_c2_fp32_ragged_tiles_match_oracle(gpu, oracle, opts, kernel, n):
+    """Partial point tiles (128-point TMEM tiles / 64-point FMA tiles) on the FP32 kernels."""
+    opts(kernel)
+    c = pkg.config2(n_points=n, act=pkg.ACT_SIN, with_fast=False)
+    m = c["model"]
+    gpu.set_lrnr(m, pkg.F32)
+    gpu.set_points(c["pts"])
+    got = gpu.loss_grad_s(pkg.MODEL_LRNR, c["s"], c["mu"])
+    want = oracle.lrnr_grad(m.widths, m.ranks, m.params, c["s"], c["mu"], c["pts"], act=pkg.ACT_SIN)
+    assert abs(got["value"] - want["value"]) <= TOL32_LOSS * abs(want["value"])
+    assert normwise(got["grad_s"], want["grad_s"]) <= TOL32_NORM
+
+
+@pytest.mark.parametrize("kernel", [pkg.KERNEL_TC, pkg.KERNEL_FMA_TILE])
+def test_c2_fp32_multi_instance_matches_oracle(gpu, oracle, opts, kernel):
+    """Several PDE instances (own s, mu, ragged point counts padded per instance)."""
+    opts(kernel)
+    c = pkg.config2(n_points=0, act=pkg.ACT_SIN, with_fast=False)
+    m = c["model"]
+    n_inst, n_per = 3, 300
+    pts = pkg.sample_collocation(91, n_inst * n_per)
+    rng = np.random.default_rng(5)
+    S = np.stack([c["s"] * (1.0 + 0.1 * rng.standard_normal(c["s"].shape)) for _ in range(n_inst)])
+    MU = np.array([[20.0, 0.01, 5.0], [5.0, 0.05, 1.0], [35.0, 0.002, 8.0]])
+    gpu.set_lrnr(m, pkg.F32)
+    gpu.set_points(pts, n_inst=n_inst)
+    got = gpu.loss_grad_s_multi(pkg.MODEL_LRNR, S, MU, w=1.0 / n_per)  # oracle weight: 1 / n per instance
+    total = 0.0
+    for i in range(n_inst):
+        sl = pts[i * n_per:(i + 1) * n_per]
+        want = oracle.lrnr_grad(m.widths, m.ranks, m.params, S[i], MU[i], sl, act=pkg.ACT_SIN)
+        total += want["value"]
+        assert normwise(got["grad_s"][i], want["grad_s"]) <= TOL32_NORM
+    assert abs(got["value"] - total) <= TOL32_LOSS * abs(total)
+
+
+def test_c2_fp32_tc_nonfinite_tag(gpu, golden, opts):
+    """The tensor-core path reports the reference's NonFiniteError layer tag."""
+    opts(pkg.KERNEL_TC)
+    m = lrnr_from_golden(golden, "c2")
+    P = m.params.copy()
+    widths, ranks = m.widths, m.ranks
+    o = widths[1] * ranks[0] + widths[0] * ranks[0] + widths[1]
+    P[o] = np.inf  # U_1[0,0] -> first non-finite node is layer 2
+    gpu.set_lrnr(pkg.LrnrParams(widths, ranks, P), pkg.F32)
+    gpu.set_points(golden["c2_pts"][:256])
+    with pytest.raises(pkg.NonFiniteError) as ei:
+        gpu.loss_grad_s(pkg.MODEL_LRNR, golden["c2_s"], golden["c2_mu"])
+    assert ei.value.layer_tag == 2
 
 
 def test_invalid_shapes_raise_value_error(gpu):
