@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--points", type=int, default=0, help="points per GPU (default: the config's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--kernel", type=int, default=0,
+                    help="LRNR_OPT_KERNEL: 0 auto (tcgen05 LRNR, FMA tile FastLRNR), 1 streaming, 2 tcgen05, 3 FMA tile")
+    ap.add_argument("--fast-sincos", type=int, default=0, help="LRNR_OPT_FAST_SINCOS (SFU sin/cos)")
     return ap.parse_args()
 
 
@@ -106,6 +109,24 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # workloads
 # ---------------------------------------------------------------------------
+def measured_peak(key, fallback):
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)[key])
+    except Exception:
+        return fallback
+
+
+def traffic_per_launch():
+    """DRAM bytes (read + write) per launch of the dominant kernel, from the committed
+    ncu --set full capture (profiles/traffic.json, written from the .ncu-rep)."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")) as f:
+            return json.load(f)["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def build_workload(pkg, cfg, rank, points):
     if cfg == "c2":
         n = points or (1 << 20)
@@ -230,6 +251,8 @@ def run_ours(args):
     torch.cuda.set_stream(stream)
     ctx = pkg.GpuContext(local)
     ctx.set_stream(stream.cuda_stream)
+    ctx.set_option(pkg.OPT_KERNEL, args.kernel)
+    ctx.set_option(pkg.OPT_FAST_SINCOS, args.fast_sincos)
     for model, params in wl["models"]:
         (ctx.set_lrnr if model == pkg.MODEL_LRNR else ctx.set_fast)(params, wl["dtype"])
     # inputs resident in HBM for the device-timed value
@@ -289,11 +312,20 @@ def run_ours(args):
     peak = max(peak_meas, nominal)
     k_ms = kern_ms[0] / args.steps
     achieved = wl["flops"][0] * n / (k_ms * 1e-3) / 1e12
+    lrnr_on_tc = wl["dtype"] == pkg.F32 and args.kernel in (pkg.KERNEL_AUTO, pkg.KERNEL_TC)
     roofline = {"bound": "fp32-fma" if wl["dtype"] == pkg.F32 else "fp64-fma", "achieved": achieved, "peak": peak,
-                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
-                "kernel": "pinn_kernel (LRNR sweep)", "flop_per_point": wl["flops"][0],
+                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic_per_launch(),
+                "kernel": ("pinn_tc_kernel (tcgen05 3xTF32 LRNR sweep)" if lrnr_on_tc else
+                           "pinn_tile_kernel (FMA LRNR sweep)"),
+                "flop_per_point": wl["flops"][0],
                 "peak_source": f"max(nominal {nominal:.1f} = 148 SM x {128 if wl['dtype'] == pkg.F32 else 64} lanes "
                                f"x 2 x 1.965 GHz, measured FMA microbenchmark {peak_meas:.1f})"}
+    if lrnr_on_tc:
+        # the same algorithmic FLOPs against the tensor pipe: 3 TF32 products per FP32
+        # multiply-add, TF32 dense = bf16 dense / 2 (MEASURED_PEAKS.json burst figure)
+        bf16 = measured_peak("bf16_tflops", 2250.0)
+        roofline["tensor_3xtf32"] = {"peak": bf16 / 2 / 3, "frac": achieved / (bf16 / 2 / 3),
+                                     "peak_source": f"bf16 dense {bf16:.1f} TFLOP/s / 2 (tf32) / 3 (3xTF32)"}
     per_kernel = {}
     for i, (model, _) in enumerate(wl["models"]):
         kms = kern_ms[i] / args.steps
@@ -309,6 +341,8 @@ def run_ours(args):
     if not args.no_e2e:
         pinned = torch.from_numpy(np.ascontiguousarray(c["pts"])).pin_memory().numpy()
         ctx2 = pkg.GpuContext(local)
+        ctx2.set_option(pkg.OPT_KERNEL, args.kernel)
+        ctx2.set_option(pkg.OPT_FAST_SINCOS, args.fast_sincos)
         for model, params in wl["models"]:
             (ctx2.set_lrnr if model == pkg.MODEL_LRNR else ctx2.set_fast)(params, wl["dtype"])
 
@@ -348,7 +382,8 @@ def run_ours(args):
                 "vs_baseline": None, "dtype": "f32" if wl["dtype"] == pkg.F32 else "f64", "data": "synthetic",
                 "config": {"workload": wl["workload"], "points_per_gpu": n,
                            "parallelism": f"dp{world} (points sharded by rank, NCCL all-reduce of [loss, dL/ds])",
-                           "l2": "flushed between timed steps (256 MiB write outside the step events)"},
+                           "l2": "flushed between timed steps (256 MiB write outside the step events)",
+                           "kernel_option": args.kernel, "fast_sincos": args.fast_sincos},
                 "roofline": roofline, "kernels": per_kernel, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk.summary()}
         print(json.dumps(line))
