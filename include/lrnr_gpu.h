@@ -133,6 +133,32 @@ int lrnr_gpu_loss_grad_s(lrnr_gpu_ctx* ctx, int model, const double* s, const do
 int lrnr_gpu_loss_grad_s_multi(lrnr_gpu_ctx* ctx, int model, const double* s, const double* mu,
                                double w, double* out_value, double* out_grad_s);
 
+/* ---- full solve-step term set ----
+ * lrnr_gpu_set_boundary: the boundary points of the following
+ * lrnr_gpu_terms_grad calls, as in CollocationBatch::initial_x / periodic_t
+ * (pde.hpp:29-40) or the classified points of the fast phase's sampling set X
+ * (reduction.cpp:27-31: t == 0 -> initial x; x == 0 or 2pi -> periodic t).
+ *
+ * lrnr_gpu_terms_grad: one solve step's loss and dL/ds over every term kind, in
+ * BatchGradResult form (training.hpp:189-195):
+ *   interior   (points of lrnr_gpu_set_points, single instance): w_int N^2 | w_int |N|
+ *   initial    w_ic (u(x,0) - sin x)^2        | w_ic |u(x,0) - sin x|
+ *   periodic   w_bc (u(0,t) - u(2pi,t))^2      | w_bc |u(0,t) - u(2pi,t)|
+ *   locality   lambda_local * sum ||s - s_init||_1   (when s_init != NULL)
+ * objective LRNR_OBJ_SQUARED = the fine-tune PinnTermEmitter (training.cpp:286-327),
+ * LRNR_OBJ_ABS = the fast-phase emitter (training.cpp:521-559; there the
+ * reference weights are 1.0).  Weights <= 0 -> 1/n of that kind (safe_inv,
+ * training.cpp:364-366).  out_comps = {residual, boundary, sparse (0), local}.
+ * Boundary terms run a forward pass over the boundary points, then a seeded
+ * reverse pass; |N| interior terms use the streaming kernel. */
+#define LRNR_OBJ_SQUARED 0
+#define LRNR_OBJ_ABS 1
+int lrnr_gpu_set_boundary(lrnr_gpu_ctx* ctx, const double* initial_x, int64_t n_ic, const double* periodic_t,
+                          int64_t n_bc);
+int lrnr_gpu_terms_grad(lrnr_gpu_ctx* ctx, int model, const double* s, const double* mu, int objective, double w_int,
+                        double w_ic, double w_bc, const double* s_init, double lambda_local, double* out_value,
+                        double* out_comps, double* out_grad_s);
+
 /* Hypernetwork-coupled step (BASELINE config 3; the emit_hyper + emit_fast_jet
  * composition of autodiff.cpp:883-922): s_i = hyper(mu_i) on device, the model
  * gradient per instance, then the hypernetwork VJP summed over instances.

@@ -25,6 +25,7 @@
 #include "lrnr/autodiff.hpp"
 #include "lrnr/model.hpp"
 #include "lrnr/pde.hpp"
+#include "lrnr/reduction.hpp"
 #include "lrnr/training.hpp"
 #include "lrnr_gpu.h"
 
@@ -81,19 +82,43 @@ public:
         hyper_params_ = flat.size();
     }
 
-    // ---- PinnTermEmitter, fine-tune mode (training.cpp:286-293) +
-    //      run_batch_gradient(CoefficientsOnly) (training.cpp:191-263).
-    // Interior terms only; the initial / periodic branches (training.cpp:307-327)
-    // are not on the device yet -> std::invalid_argument.
+    // ---- PinnTermEmitter, fine-tune mode (training.cpp:286-327) +
+    //      run_batch_gradient(CoefficientsOnly) (training.cpp:191-263): interior
+    //      w N^2, initial w (u(x,0) - sin x)^2 and periodic w (u(0,t) - u(2pi,t))^2
+    //      terms with the fine_tune weights 1/n per kind (training.cpp:446-450).
     training::BatchGradResult tune_gradient(const Coefficients& s, const PdeParams& mu,
                                             const pde::CollocationBatch& batch) {
-        require_interior(batch);
-        return coeff_gradient(LRNR_MODEL_LRNR, s, mu, batch.interior);
+        set_points(batch.interior, 1);
+        set_boundary(batch.initial_x, batch.periodic_t);
+        return terms(LRNR_MODEL_LRNR, s, mu, LRNR_OBJ_SQUARED, 0.0, nullptr, 0.0);
     }
-    // FastLRNR squared-residual objective (emit_fast_jet, autodiff.cpp:905-922).
+    // FastLRNR squared-residual objective over interior points (emit_fast_jet,
+    // autodiff.cpp:905-922; BASELINE config 1).
     training::BatchGradResult fast_gradient(const Coefficients& s, const PdeParams& mu,
                                             const std::vector<pde::Point>& pts) {
         return coeff_gradient(LRNR_MODEL_FAST, s, mu, pts);
+    }
+    // The fast-phase emitter of fast_solve (training.cpp:521-559): |N| at the
+    // interior points of X, |u - sin x| at initial points, |u(0,t) - u(2pi,t)| at
+    // periodic points (classify_point, reduction.cpp:27-31), plus
+    // lambda_local * sum_l ||s_l - s_init_l||_1 when lambda_local > 0.
+    training::BatchGradResult fast_phase_gradient(const Coefficients& s, const Coefficients& s_init,
+                                                  const PdeParams& mu, const reduction::SamplingSetX& X,
+                                                  double lambda_local) {
+        std::vector<pde::Point> interior;
+        std::vector<double> ic, per;
+        for (const pde::Point& p : X.points) {
+            switch (reduction::classify_point(p)) {
+                case reduction::PointKind::Interior: interior.push_back(p); break;
+                case reduction::PointKind::Initial: ic.push_back(p.x); break;
+                default: per.push_back(p.t); break;
+            }
+        }
+        set_points(interior, 1);
+        set_boundary(ic, per);
+        const std::vector<double> s0 = flatten(s_init);
+        return terms(LRNR_MODEL_FAST, s, mu, LRNR_OBJ_ABS, 1.0, lambda_local > 0.0 ? s0.data() : nullptr,
+                     lambda_local);
     }
     // Meta mode interior terms (training.cpp:283-293, lambda_sparse = 0):
     // pts grouped by instance (mus.size() groups of equal size); ParamPacker
@@ -115,15 +140,19 @@ public:
         return out;
     }
 
-    // ---- forward only: loss_tune interior part (training.cpp:76-105), jet_forward (model.cpp:357-405) ----
+    // ---- forward only: loss_tune (training.cpp:139-163), jet_forward (model.cpp:357-405) ----
     training::LossBreakdown loss_tune(const Coefficients& s, const PdeParams& mu, const pde::CollocationBatch& batch) {
-        require_interior(batch);
         set_points(batch.interior, 1);
-        const std::vector<double> sf = flatten(s);
-        const double m[3] = {mu.mu1, mu.mu2, mu.mu3};
+        set_boundary(batch.initial_x, batch.periodic_t);
         training::LossBreakdown lb;
-        check(lrnr_gpu_loss(ctx_, LRNR_MODEL_LRNR, sf.data(), m, 0.0, &lb.residual));
-        lb.total = lb.residual;
+        try {
+            const training::BatchGradResult r = terms(LRNR_MODEL_LRNR, s, mu, LRNR_OBJ_SQUARED, 0.0, nullptr, 0.0);
+            lb.residual = r.comps[0];
+            lb.boundary = r.comps[1];
+        } catch (const NonFiniteError&) {
+            throw NonFiniteError(-1);  // loss_tune's own check (training.cpp:161)
+        }
+        lb.total = lb.residual + lb.boundary;
         return lb;
     }
     std::vector<Jet> jet_forward(const std::vector<pde::Point>& pts, const Coefficients& s, bool fast = false) {
@@ -151,10 +180,6 @@ private:
         if (rc == LRNR_EINVAL) throw std::invalid_argument(msg);
         throw std::runtime_error("lrnr_gpu: " + msg);
     }
-    static void require_interior(const pde::CollocationBatch& b) {
-        if (!b.initial_x.empty() || !b.periodic_t.empty())
-            throw std::invalid_argument("lrnr::gpu: boundary terms are not on the device path yet");
-    }
     static std::vector<double> flatten(const Coefficients& s) {
         std::vector<double> f;
         for (const auto& v : s.s) f.insert(f.end(), v.data.begin(), v.data.end());
@@ -168,6 +193,20 @@ private:
         }
         check(lrnr_gpu_set_points(ctx_, xt.data(), static_cast<int64_t>(n_inst),
                                   static_cast<int64_t>(pts.size() / n_inst)));
+    }
+    void set_boundary(const std::vector<double>& ic, const std::vector<double>& per) {
+        check(lrnr_gpu_set_boundary(ctx_, ic.data(), static_cast<int64_t>(ic.size()), per.data(),
+                                    static_cast<int64_t>(per.size())));
+    }
+    training::BatchGradResult terms(int model, const Coefficients& s, const PdeParams& mu, int objective, double w,
+                                    const double* s_init, double lambda_local) {
+        const std::vector<double> sf = flatten(s);
+        const double m[3] = {mu.mu1, mu.mu2, mu.mu3};
+        training::BatchGradResult out;
+        out.grad.assign(sf.size(), 0.0);
+        check(lrnr_gpu_terms_grad(ctx_, model, sf.data(), m, objective, w, w, w, s_init, lambda_local, &out.value,
+                                  out.comps, out.grad.data()));
+        return out;
     }
     training::BatchGradResult coeff_gradient(int model, const Coefficients& s, const PdeParams& mu,
                                              const std::vector<pde::Point>& pts) {

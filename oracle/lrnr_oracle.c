@@ -803,6 +803,165 @@ int orc_fast_grad(int L, const int64_t* r, const int64_t* rh, int64_t m_in, int6
     return bad ? 2 : 0;
 }
 
+/* ------------------------------------------------------------------------ */
+/* Full term set of one solve step: PinnTermEmitter fine-tune terms          */
+/* (training.cpp:286-327: interior w N^2, initial w (u(x,0) - sin x)^2,      */
+/* periodic w (u(0,t) - u(2pi,t))^2) or the fast-phase emitter's l1 terms    */
+/* (training.cpp:521-549: |N|, |u - sin x|, |u(0,t) - u(2pi,t)|), plus the   */
+/* locality term lambda * sum_l ||s_l - s_init_l||_1 (training.cpp:550-559,  */
+/* L1ToTarget VJP autodiff.cpp:791-802).  Term order = the emitters' index   */
+/* order: interior, initial, periodic, locality; run_batch_gradient's fixed  */
+/* chunking (training.cpp:191-263).  model 0 = LRNR (P = LrnrParams flat,    */
+/* dims L, w, r), 1 = FastLRNR (P = FastParams flat, dims L, r, rh, m_in =   */
+/* w[0], m_out = w[1]).  objective 0 = squared (Scale(Square(.)) VJP         */
+/* 2 * r * w), 1 = abs (Abs VJP sgn, 0 at 0; autodiff.cpp:745-750).          */
+/* comps = {residual, boundary, sparse (0), local}.                          */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    int kind;
+    lr_net lr;
+    fa_net fa;
+    int64_t ws_len, g_len, r_total;
+} any_net;
+
+static const double* any_fwd(const any_net* a, const double* s, double x, double t, double* ws) {
+    if (a->kind == 0) {
+        lr_forward(&a->lr, s, x, t, ws);
+        return ws + a->lr.oa[a->lr.L];
+    }
+    fa_forward(&a->fa, s, x, t, ws);
+    return ws + a->fa.ou;
+}
+
+/* gA: scratch of g_len doubles whose first 4 entries are the output-jet seed */
+static void any_bwd(const any_net* a, const double* s, double* ws, double* gA, double* ds) {
+    if (a->kind == 0) lr_backward(&a->lr, s, ws, gA, ds, NULL);
+    else fa_backward(&a->fa, s, ws, gA, ds);
+}
+
+static double sgn0(double v) { return v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : 0.0); }
+
+int orc_terms_grad(int model, int L, const int64_t* w, const int64_t* r, const int64_t* rh, const double* P,
+                   int act, const double* s, const double* mu, const double* pts, int64_t n_int,
+                   const double* ic_x, int64_t n_ic, const double* per_t, int64_t n_bc, double w_int,
+                   double w_ic, double w_bc, int objective, const double* s_init, double lambda_local,
+                   int64_t chunk, double* out_value, double* out_comps, double* out_grad_s) {
+    if (L < 1 || L > ORC_MAXL || chunk < 1 || (objective != 0 && objective != 1)) return 1;
+    any_net a;
+    memset(&a, 0, sizeof(a));
+    a.kind = model;
+    if (model == 0) {
+        if (w[L] != 1) return 1;
+        lr_init(&a.lr, L, w, r, P, act);
+        a.ws_len = a.lr.ws_len;
+        a.g_len = 4 * a.lr.max_w + 4;
+        a.r_total = a.lr.r_total;
+    } else {
+        if (w[0] != 2 || w[1] != 1 || L < 2) return 1;
+        fa_init(&a.fa, L, r, rh, w[0], w[1], P, act);
+        a.ws_len = a.fa.ws_len;
+        a.g_len = 4;
+        a.r_total = a.fa.r_total;
+    }
+    const int has_local = s_init != NULL && lambda_local > 0.0;
+    const int64_t n_terms = n_int + n_ic + n_bc + (has_local ? 1 : 0);
+    const int64_t n_chunks = (n_terms + chunk - 1) / chunk;
+    const int64_t G = a.r_total, stride = 5 + G; /* value, comps[4], grad */
+    double* part = (double*)calloc((size_t)(n_chunks > 0 ? n_chunks : 1) * (size_t)stride, sizeof(double));
+    int bad = 0;
+#pragma omp parallel
+    {
+        double* ws0 = (double*)malloc((size_t)a.ws_len * sizeof(double));
+        double* ws1 = (double*)malloc((size_t)a.ws_len * sizeof(double));
+        double* g0 = (double*)malloc((size_t)a.g_len * sizeof(double));
+        double* g1 = (double*)malloc((size_t)a.g_len * sizeof(double));
+#pragma omp for schedule(static)
+        for (int64_t c = 0; c < n_chunks; ++c) {
+            double* pc = part + c * stride;
+            const int64_t lo = c * chunk, hi = lo + chunk < n_terms ? lo + chunk : n_terms;
+            for (int64_t idx = lo; idx < hi; ++idx) {
+                double term;
+                int comp;
+                for (int k = 0; k < 4; ++k) g0[k] = g1[k] = 0.0;
+                if (idx < n_int) {
+                    const double* u = any_fwd(&a, s, pts[2 * idx], pts[2 * idx + 1], ws0);
+                    const double N = cdr_residual(u, mu);
+                    double gN;
+                    if (objective == 0) {
+                        term = w_int * (N * N);
+                        gN = 2.0 * N * w_int;
+                    } else {
+                        term = w_int * fabs(N);
+                        gN = sgn0(N) * w_int;
+                    }
+                    cdr_vjp(u, mu, gN, g0);
+                    any_bwd(&a, s, ws0, g0, pc + 5);
+                    comp = 0;
+                } else if (idx < n_int + n_ic) {
+                    const double x = ic_x[idx - n_int];
+                    const double* u = any_fwd(&a, s, x, 0.0, ws0);
+                    const double d = u[0] - sin(x);
+                    if (objective == 0) {
+                        term = w_ic * (d * d);
+                        g0[0] = 2.0 * d * w_ic;
+                    } else {
+                        term = w_ic * fabs(d);
+                        g0[0] = sgn0(d) * w_ic;
+                    }
+                    any_bwd(&a, s, ws0, g0, pc + 5);
+                    comp = 1;
+                } else if (idx < n_int + n_ic + n_bc) {
+                    const double t = per_t[idx - n_int - n_ic];
+                    const double* u0 = any_fwd(&a, s, 0.0, t, ws0);
+                    const double* u1 = any_fwd(&a, s, ORC_TWO_PI, t, ws1);
+                    const double d = u0[0] - u1[0];
+                    double gd;
+                    if (objective == 0) {
+                        term = w_bc * (d * d);
+                        gd = 2.0 * d * w_bc;
+                    } else {
+                        term = w_bc * fabs(d);
+                        gd = sgn0(d) * w_bc;
+                    }
+                    g0[0] = gd;
+                    g1[0] = -gd;
+                    any_bwd(&a, s, ws0, g0, pc + 5);
+                    any_bwd(&a, s, ws1, g1, pc + 5);
+                    comp = 1;
+                } else {
+                    term = 0.0;
+                    for (int64_t i = 0; i < G; ++i) {
+                        const double d = s[i] - s_init[i];
+                        term += fabs(d);
+                        pc[5 + i] += lambda_local * sgn0(d);
+                    }
+                    term *= lambda_local;
+                    comp = 3;
+                }
+                if (!isfinite(term)) {
+#pragma omp atomic write
+                    bad = 1;
+                }
+                pc[0] += term;
+                pc[1 + comp] += term;
+            }
+        }
+        free(ws0);
+        free(ws1);
+        free(g0);
+        free(g1);
+    }
+    for (int64_t k = 0; k < 5 + G; ++k) {
+        double acc = 0.0;
+        for (int64_t c = 0; c < n_chunks; ++c) acc += part[c * stride + k];
+        if (k == 0) *out_value = acc;
+        else if (k < 5) out_comps[k - 1] = acc;
+        else out_grad_s[k - 5] = acc;
+    }
+    free(part);
+    return bad ? 2 : 0;
+}
+
 int orc_fast_jets(int L, const int64_t* r, const int64_t* rh, int64_t m_in, int64_t m_out,
                   const double* P, int act, const double* s, const double* pts, int64_t n,
                   double* out_jets) {

@@ -167,6 +167,37 @@ class Oracle:
             out["terms"] = tv[:n]
         return out
 
+    def terms_grad(self, model, dims, P, s, mu, pts=(), ic_x=(), per_t=(), w_int=None, w_ic=None, w_bc=None,
+                   objective=0, s_init=None, lambda_local=0.0, act=0, chunk=64):
+        """Full solve-step term set (orc_terms_grad): model 0 = LRNR with dims = (widths, ranks),
+        1 = FastLRNR with dims = (ranks, red_ranks); weights default to 1/n of each kind
+        (training.cpp:364-366); objective 0 = squared, 1 = abs."""
+        pts = _f64(pts).reshape(-1, 2)
+        icx, pt = _f64(ic_x).reshape(-1), _f64(per_t).reshape(-1)
+        inv = lambda n: 1.0 / n if n else 0.0  # noqa: E731
+        w_int = inv(pts.shape[0]) if w_int is None else w_int
+        w_ic = inv(icx.shape[0]) if w_ic is None else w_ic
+        w_bc = inv(pt.shape[0]) if w_bc is None else w_bc
+        if model == 0:
+            wv, rv = _i64(dims[0]), _i64(dims[1])
+            L, rh = len(rv), None
+        else:
+            rv, hv = _i64(dims[0]), _i64(dims[1])
+            wv, L, rh = _i64([2, 1]), len(rv), hv
+        gs = np.zeros(int(rv.sum()))
+        comps = np.zeros(4)
+        val = C.c_double(0.0)
+        si = None if s_init is None else _f64(s_init)
+        rc = self.lib.orc_terms_grad(C.c_int(model), C.c_int(L), _ptr(wv), _ptr(rv), _ptr(rh), _ptr(_f64(P)),
+                                     C.c_int(act), _ptr(_f64(s)), _ptr(_f64(mu)), _ptr(pts), C.c_int64(pts.shape[0]),
+                                     _ptr(icx), C.c_int64(icx.shape[0]), _ptr(pt), C.c_int64(pt.shape[0]),
+                                     C.c_double(w_int), C.c_double(w_ic), C.c_double(w_bc), C.c_int(objective),
+                                     _ptr(si), C.c_double(lambda_local), C.c_int64(chunk), C.byref(val),
+                                     _ptr(comps), _ptr(gs))
+        if rc == 1:
+            raise OracleError("orc_terms_grad: invalid arguments")
+        return dict(value=val.value, comps=comps, grad_s=gs, nonfinite=(rc == 2))
+
     def fast_jets(self, ranks, red, F, s, pts, act=0):
         rv, hv = _i64(ranks), _i64(red)
         pts = _f64(pts).reshape(-1, 2)
@@ -309,6 +340,26 @@ class Reference:
                                               _ptr(xpts), C.c_int64(xpts.shape[0]), C.c_double(lambda_local),
                                               C.c_int(threads), C.c_int(chunk), C.byref(val), _ptr(comps), _ptr(gs)),
                  "fast_phase_grad")
+        return dict(value=val.value, comps=comps, grad_s=gs)
+
+    def tune_grad_full(self, widths, ranks, P, s, mu, pts, ic_x=(), per_t=(), w_int=None, w_ic=None, w_bc=None,
+                       threads=1, chunk=64):
+        """Fine-tune PinnTermEmitter terms: interior + initial + periodic (training.cpp:286-327)."""
+        wv, rv = _i64(widths), _i64(ranks)
+        pts = _f64(pts).reshape(-1, 2)
+        icx, pt = _f64(ic_x).reshape(-1), _f64(per_t).reshape(-1)
+        inv = lambda n: 1.0 / n if n else 0.0  # noqa: E731
+        w_int = inv(pts.shape[0]) if w_int is None else w_int
+        w_ic = inv(icx.shape[0]) if w_ic is None else w_ic
+        w_bc = inv(pt.shape[0]) if w_bc is None else w_bc
+        gs = np.zeros(int(rv.sum()))
+        comps = np.zeros(4)
+        val = C.c_double(0.0)
+        self._rc(self.lib.ref_tune_grad_full(C.c_int(len(rv)), _ptr(wv), _ptr(rv), _ptr(_f64(P)), _ptr(_f64(s)),
+                                             _ptr(_f64(mu)), _ptr(pts), C.c_int64(pts.shape[0]), _ptr(icx),
+                                             C.c_int64(icx.shape[0]), _ptr(pt), C.c_int64(pt.shape[0]),
+                                             C.c_double(w_int), C.c_double(w_ic), C.c_double(w_bc), C.c_int(threads),
+                                             C.c_int(chunk), C.byref(val), _ptr(comps), _ptr(gs)), "tune_grad_full")
         return dict(value=val.value, comps=comps, grad_s=gs)
 
     def lrnr_jets(self, widths, ranks, P, s, pts):

@@ -361,6 +361,54 @@ int ref_lrnr_grad(int L, const int64_t* widths, const int64_t* ranks, const doub
     });
 }
 
+// The full fine-tune PinnTermEmitter term set (training.cpp:286-327, fine-tune
+// mode, lambda_sparse = 0): interior w_int N^2, initial w_ic (u(x,0) - sin x)^2,
+// periodic w_bc (u(0,t) - u(2pi,t))^2, in the emitter's index order; built with
+// the reference's own tape ops (the emitter struct itself is file-local).
+int ref_tune_grad_full(int L, const int64_t* widths, const int64_t* ranks, const double* params,
+                       const double* s, const double* mu, const double* pts, int64_t n,
+                       const double* ic_x, int64_t n_ic, const double* per_t, int64_t n_bc, double w_int,
+                       double w_ic, double w_bc, int threads, int chunk, double* out_value,
+                       double* out_comps, double* out_grad) {
+    return guarded([&] {
+        LrnrParams p = unpack_lrnr(L, widths, ranks, params);
+        Coefficients c = unpack_s(p, s);
+        const PdeParams m = mu_of(mu);
+        Trainables at{&p, nullptr, &c};
+        training::EmitFn emit = [&](TapeBindings& ctx, const training::ExtraBindings&,
+                                    std::size_t idx, double* comps) -> NodeId {
+            Tape& tp = ctx.tape;
+            const std::size_t ni = static_cast<std::size_t>(n), nc = static_cast<std::size_t>(n_ic);
+            if (idx < ni) {
+                const NodeId jet = emit_lrnr_jet(tp, pts[2 * idx], pts[2 * idx + 1], ctx.lrnr,
+                                                 ctx.coeffs.s_leaves);
+                const NodeId term = tp.scale(tp.square(tp.residual_cdr(jet, m)), w_int);
+                comps[0] += tp.value(term);
+                return term;
+            }
+            if (idx < ni + nc) {
+                const double x = ic_x[idx - ni];
+                const NodeId jet = emit_lrnr_jet(tp, x, 0.0, ctx.lrnr, ctx.coeffs.s_leaves);
+                const NodeId r = tp.sub_const(tp.pick_value(jet, 0), std::sin(x));
+                const NodeId term = tp.scale(tp.square(r), w_ic);
+                comps[1] += tp.value(term);
+                return term;
+            }
+            const double t = per_t[idx - ni - nc];
+            const NodeId j0 = emit_lrnr_jet(tp, 0.0, t, ctx.lrnr, ctx.coeffs.s_leaves);
+            const NodeId j1 = emit_lrnr_jet(tp, pde::kTwoPi, t, ctx.lrnr, ctx.coeffs.s_leaves);
+            const NodeId r = tp.sub(tp.pick_value(j0, 0), tp.pick_value(j1, 0));
+            const NodeId term = tp.scale(tp.square(r), w_bc);
+            comps[1] += tp.value(term);
+            return term;
+        };
+        training::BatchGradResult bg = training::run_batch_gradient(
+            at, ParamSelector::CoefficientsOnly, nullptr, emit, static_cast<std::size_t>(n + n_ic + n_bc),
+            par_of(threads, chunk));
+        copy_result(bg, out_value, out_comps, out_grad);
+    });
+}
+
 // FastLRNR interior MSE through bind_fast + emit_fast_jet (training.cpp:513-531
 // emitter structure with the BASELINE c1 squared-residual objective).
 int ref_fast_grad(int L, const int64_t* ranks, const int64_t* red, int64_t m_in, int64_t m_out,

@@ -16,6 +16,7 @@ EXPORTS = (
     "lrnr_gpu_create", "lrnr_gpu_destroy", "lrnr_gpu_last_error", "lrnr_gpu_last_layer_tag",
     "lrnr_gpu_set_stream", "lrnr_gpu_set_option", "lrnr_gpu_launch_count", "lrnr_gpu_set_lrnr", "lrnr_gpu_set_fast",
     "lrnr_gpu_set_hyper", "lrnr_gpu_set_points", "lrnr_gpu_set_points_device", "lrnr_gpu_loss_grad_s",
+    "lrnr_gpu_set_boundary", "lrnr_gpu_terms_grad",
     "lrnr_gpu_loss_grad_s_multi", "lrnr_gpu_hyper_loss_grad", "lrnr_gpu_meta_loss_grad", "lrnr_gpu_jets",
     "lrnr_gpu_loss", "lrnr_gpu_upload_coeffs", "lrnr_gpu_run", "lrnr_gpu_check", "lrnr_gpu_download",
     "lrnr_gpu_fma_peak",
@@ -30,6 +31,8 @@ MODEL_LRNR, MODEL_FAST = 0, 1
 OPT_FAST_SINCOS, OPT_KERNEL, OPT_TILE_P = 1, 2, 3
 # LRNR_OPT_KERNEL values
 KERNEL_AUTO, KERNEL_STREAM, KERNEL_TC, KERNEL_FMA_TILE = 0, 1, 2, 3
+# lrnr_gpu_terms_grad objectives
+OBJ_SQUARED, OBJ_ABS = 0, 1
 
 _lib = None
 
@@ -57,6 +60,9 @@ def load() -> C.CDLL:
     lib.lrnr_gpu_set_points.argtypes = [vp, dp, i64, i64]
     lib.lrnr_gpu_set_points_device.argtypes = [vp, vp, i64, i64]
     lib.lrnr_gpu_loss_grad_s.argtypes = [vp, ip, dp, dp, C.c_double, dp, dp, dp]
+    lib.lrnr_gpu_set_boundary.argtypes = [vp, dp, i64, dp, i64]
+    lib.lrnr_gpu_terms_grad.argtypes = [vp, ip, dp, dp, ip, C.c_double, C.c_double, C.c_double, dp, C.c_double,
+                                        dp, dp, dp]
     lib.lrnr_gpu_loss_grad_s_multi.argtypes = [vp, ip, dp, dp, C.c_double, dp, dp]
     lib.lrnr_gpu_hyper_loss_grad.argtypes = [vp, ip, dp, C.c_double, dp, dp, dp]
     lib.lrnr_gpu_meta_loss_grad.argtypes = [vp, dp, C.c_double, dp, dp]

@@ -17,7 +17,8 @@ import numpy as np
 from . import _lib
 from ._lib import ACT_SIN, ACT_TANH, F32, F64, MODEL_FAST, MODEL_LRNR  # noqa: F401
 from ._lib import (  # noqa: F401
-    KERNEL_AUTO, KERNEL_FMA_TILE, KERNEL_STREAM, KERNEL_TC, OPT_FAST_SINCOS, OPT_KERNEL, OPT_TILE_P,
+    KERNEL_AUTO, KERNEL_FMA_TILE, KERNEL_STREAM, KERNEL_TC, OBJ_ABS, OBJ_SQUARED, OPT_FAST_SINCOS, OPT_KERNEL,
+    OPT_TILE_P,
 )
 
 TWO_PI = 6.283185307179586476925286766559
@@ -261,6 +262,24 @@ class GpuContext:
         v = C.c_double(0.0)
         self._rc(self.lib.lrnr_gpu_loss_grad_s(self.h, model, _p(_f64(s)), _p(_f64(mu)), C.c_double(w), C.byref(v),
                                                _p(comps), _p(g)), "loss_grad_s")
+        return dict(value=v.value, comps=comps, grad_s=g)
+
+    def set_boundary(self, initial_x=(), periodic_t=()):
+        """Boundary points (CollocationBatch::initial_x / periodic_t) for terms_grad."""
+        ic, pt = _f64(initial_x).reshape(-1), _f64(periodic_t).reshape(-1)
+        self._rc(self.lib.lrnr_gpu_set_boundary(self.h, _p(ic), ic.shape[0], _p(pt), pt.shape[0]), "set_boundary")
+        self.n_ic, self.n_bc = ic.shape[0], pt.shape[0]
+
+    def terms_grad(self, model, s, mu, objective=OBJ_SQUARED, w_int=0.0, w_ic=0.0, w_bc=0.0, s_init=None,
+                   lambda_local=0.0):
+        """One solve step over interior + initial + periodic (+ locality) terms."""
+        g = np.zeros(self.r_total[model])
+        comps = np.zeros(4)
+        v = C.c_double(0.0)
+        si = None if s_init is None else _f64(s_init)
+        self._rc(self.lib.lrnr_gpu_terms_grad(self.h, model, _p(_f64(s)), _p(_f64(mu)), objective, C.c_double(w_int),
+                                              C.c_double(w_ic), C.c_double(w_bc), _p(si), C.c_double(lambda_local),
+                                              C.byref(v), _p(comps), _p(g)), "terms_grad")
         return dict(value=v.value, comps=comps, grad_s=g)
 
     def loss_grad_s_multi(self, model, s, mu, w=0.0):

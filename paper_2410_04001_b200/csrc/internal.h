@@ -153,6 +153,13 @@ DevNet<T> dev_net(const Model& m) {
 }  // namespace lrnr_b200
 
 struct lrnr_gpu_ctx {
+    // per-point term specs for the streaming kernel (boundary / fast-phase terms);
+    // nullptr + objective 0 = the interior squared residual
+    const lrnr_b200::TermSpec* term_spec = nullptr;
+    int term_objective = 0;
+    // boundary points (lrnr_gpu_set_boundary): [initial (x, 0)] [periodic (0, t), (2pi, t)] pairs
+    lrnr_b200::detail::DevBuf bnd_pts, bnd_x, bnd_spec, bnd_jets;
+    int64_t n_ic = 0, n_bc = 0;
     int device = 0;
     int num_sms = 148;
     cudaStream_t own = nullptr;
@@ -223,7 +230,7 @@ void launch_pinn(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const d
     DevNet<T> net = dev_net<T>(m);
     pinn_kernel<T, TPP, RMAX, ACT, MODE><<<p.grid, kThreads, p.smem, ctx->stream>>>(
         net, p.g, ctx->pts, s_dev, mu_dev, static_cast<T>(w), ctx->scratch.as<T>(), ctx->part.as<T>(),
-        jets_dev, ctx->bad.as<unsigned long long>());
+        jets_dev, ctx->bad.as<unsigned long long>(), ctx->term_spec, ctx->term_objective);
     CK(cudaGetLastError());
     dim3 rg((R1 + 127) / 128, static_cast<unsigned>(n_inst));
     reduce_units_kernel<T><<<rg, 128, 0, ctx->stream>>>(ctx->part.as<T>(), p.g.units_per_inst, R1, n_inst, dev_out);

@@ -487,6 +487,50 @@ void dispatch_pinn(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const
 }
 
 // ---------------------------------------------------------------------------
+// boundary terms (PinnTermEmitter initial / periodic branches, training.cpp:307-327;
+// fast-phase value terms, :533-549).  Points: [initial (x_i, 0)] then periodic
+// pairs [(0, t_j), (2pi, t_j)]; the pair's term needs both u values, so a
+// forward pass over the boundary points comes first and this kernel turns its
+// output jets into per-point term specs for the seeded reverse pass.
+// ---------------------------------------------------------------------------
+constexpr double kTwoPi = 6.283185307179586476925286766559;  // pde.hpp:21
+
+__global__ void boundary_spec_kernel(const double* __restrict__ jets, const double* __restrict__ sin_x,
+                                     int64_t n_ic, int64_t n_bc, double w_ic, double w_bc, int abs_obj,
+                                     TermSpec* __restrict__ spec) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int kind = abs_obj ? 3 : 2;
+    if (i < n_ic) {
+        spec[i] = TermSpec{sin_x[i], w_ic, w_ic, kind, 0};
+    } else if (i < n_ic + 2 * n_bc) {
+        const int64_t j = i - n_ic, first = n_ic + (j & ~int64_t(1));
+        if ((j & 1) == 0)  // u(0,t) - u(2pi,t): the term, target = the partner's u
+            spec[i] = TermSpec{jets[4 * (first + 1)], w_bc, w_bc, kind, 0};
+        else               // u(2pi,t) - u(0,t): seed only (its gradient is the negative)
+            spec[i] = TermSpec{jets[4 * first], 0.0, w_bc, kind, 0};
+    }
+}
+
+// Temporarily point the context's point set at another device array (one instance).
+struct PointSwap {
+    lrnr_gpu_ctx* ctx;
+    const double* pts;
+    int64_t n_inst, n_per;
+    PointSwap(lrnr_gpu_ctx* c, const double* p, int64_t n) : ctx(c), pts(c->pts), n_inst(c->n_inst), n_per(c->n_per) {
+        c->pts = p;
+        c->n_inst = 1;
+        c->n_per = n;
+    }
+    ~PointSwap() {
+        ctx->pts = pts;
+        ctx->n_inst = n_inst;
+        ctx->n_per = n_per;
+        ctx->term_spec = nullptr;
+        ctx->term_objective = 0;
+    }
+};
+
+// ---------------------------------------------------------------------------
 // non-finite diagnosis: first non-finite node in tape order (autodiff.cpp:448-461)
 // ---------------------------------------------------------------------------
 int diagnose_tag(const Model& m, const double* s, double x, double t, const double* mu) {
@@ -627,6 +671,22 @@ double* run_resident(lrnr_gpu_ctx* ctx, const Model& m, double w, double* dev_ou
     if (MODE == 0 && dispatch_v2(ctx, m, ctx->s_dev.as<double>(), ctx->mu_dev.as<double>(), wt, dev_out))
         return dev_out;
     dispatch_pinn<MODE>(ctx, m, ctx->s_dev.as<double>(), ctx->mu_dev.as<double>(), wt, dev_out, jets_dev);
+    return dev_out;
+}
+
+// The streaming kernel only (per-point term specs / |N| objective / forward jets).
+template <int MODE>
+double* run_resident_stream(lrnr_gpu_ctx* ctx, const Model& m, double w, double* jets_dev) {
+    require(ctx->coeff_inst == ctx->n_inst && ctx->coeff_rtotal == m.rtotal,
+            "coefficients do not match the points' instance count / model ranks");
+    const int R1 = 1 + m.rtotal;
+    ctx->out.ensure(static_cast<size_t>(ctx->n_inst * R1) * sizeof(double));
+    double* dev_out = ctx->out.as<double>();
+    ctx->out_rows = ctx->n_inst;
+    ctx->out_R1 = R1;
+    ctx->bad.ensure(sizeof(unsigned long long));
+    reset_bad(ctx);
+    dispatch_pinn<MODE>(ctx, m, ctx->s_dev.as<double>(), ctx->mu_dev.as<double>(), w, dev_out, jets_dev);
     return dev_out;
 }
 
@@ -1028,6 +1088,109 @@ int lrnr_gpu_loss_grad_s(lrnr_gpu_ctx* ctx, int model, const double* s, const do
             out_comps4[1] = out_comps4[2] = out_comps4[3] = 0.0;
         }
         if (out_grad_s) std::copy(h.begin() + 1, h.end(), out_grad_s);
+    });
+}
+
+int lrnr_gpu_set_boundary(lrnr_gpu_ctx* ctx, const double* initial_x, int64_t n_ic, const double* periodic_t,
+                          int64_t n_bc) {
+    return guarded(ctx, [&] {
+        require(n_ic >= 0 && n_bc >= 0, "bad boundary counts");
+        require((initial_x || n_ic == 0) && (periodic_t || n_bc == 0), "null boundary points");
+        const int64_t nb = n_ic + 2 * n_bc;
+        std::vector<double> xt(static_cast<size_t>(2 * nb)), sx(static_cast<size_t>(n_ic));
+        for (int64_t i = 0; i < n_ic; ++i) {
+            xt[2 * i] = initial_x[i];
+            xt[2 * i + 1] = 0.0;
+            sx[i] = std::sin(initial_x[i]);  // host libm, as the reference's std::sin
+        }
+        for (int64_t j = 0; j < n_bc; ++j) {
+            const int64_t o = n_ic + 2 * j;
+            xt[2 * o] = 0.0;
+            xt[2 * o + 1] = periodic_t[j];
+            xt[2 * o + 2] = kTwoPi;
+            xt[2 * o + 3] = periodic_t[j];
+        }
+        ctx->bnd_pts.ensure(xt.size() * sizeof(double) + 16);
+        ctx->bnd_x.ensure(sx.size() * sizeof(double) + 16);
+        ctx->bnd_spec.ensure(static_cast<size_t>(nb) * sizeof(TermSpec) + 16);
+        ctx->bnd_jets.ensure(static_cast<size_t>(4 * nb) * sizeof(double) + 16);
+        if (nb) CK(cudaMemcpyAsync(ctx->bnd_pts.p, xt.data(), xt.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                   ctx->stream));
+        if (n_ic) CK(cudaMemcpyAsync(ctx->bnd_x.p, sx.data(), sx.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                     ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));  // host staging vectors go out of scope
+        ctx->n_ic = n_ic;
+        ctx->n_bc = n_bc;
+    });
+}
+
+int lrnr_gpu_terms_grad(lrnr_gpu_ctx* ctx, int model, const double* s, const double* mu, int objective, double w_int,
+                        double w_ic, double w_bc, const double* s_init, double lambda_local, double* out_value,
+                        double* out_comps4, double* out_grad_s) {
+    return guarded(ctx, [&] {
+        require(model == LRNR_MODEL_LRNR || model == LRNR_MODEL_FAST, "unknown model slot");
+        const Model& m = ctx->models[model];
+        if (!m.set) throw StateError("model not set");
+        require(s && mu, "null argument");
+        require(objective == LRNR_OBJ_SQUARED || objective == LRNR_OBJ_ABS, "unknown objective");
+        const int64_t n_int = ctx->pts ? ctx->n_inst * ctx->n_per : 0;
+        require(n_int == 0 || ctx->n_inst == 1, "lrnr_gpu_terms_grad needs a single instance");
+        auto inv = [](int64_t n) { return n ? 1.0 / static_cast<double>(n) : 0.0; };  // safe_inv
+        const double wi = w_int > 0.0 ? w_int : inv(n_int);
+        const double wc = w_ic > 0.0 ? w_ic : inv(ctx->n_ic);
+        const double wb = w_bc > 0.0 ? w_bc : inv(ctx->n_bc);
+        const int R1 = 1 + m.rtotal;
+        std::vector<double> grad(static_cast<size_t>(m.rtotal), 0.0), h(static_cast<size_t>(R1));
+        double comps[4] = {0.0, 0.0, 0.0, 0.0};
+        upload_coeffs_impl(ctx, s, mu, 1, m.rtotal);
+        auto accumulate = [&](int comp) {
+            comps[comp] += h[0];
+            for (int i = 0; i < m.rtotal; ++i) grad[i] += h[1 + i];
+        };
+        // interior terms: the fused kernels for w N^2; |N| on the streaming kernel
+        if (n_int > 0) {
+            double* d;
+            if (objective == LRNR_OBJ_SQUARED) {
+                d = run_resident<0>(ctx, m, wi, nullptr, nullptr);
+            } else {
+                PointSwap keep(ctx, ctx->pts, n_int);
+                ctx->term_objective = 1;
+                d = run_resident_stream<0>(ctx, m, wi, nullptr);
+            }
+            download(ctx, d, h.data(), h.size());
+            check_bad(ctx, m);
+            accumulate(0);
+        }
+        // boundary terms: forward pass for u, specs, seeded reverse pass
+        const int64_t nb = ctx->n_ic + 2 * ctx->n_bc;
+        if (nb > 0) {
+            PointSwap keep(ctx, ctx->bnd_pts.as<double>(), nb);
+            run_resident_stream<1>(ctx, m, 1.0, ctx->bnd_jets.as<double>());
+            boundary_spec_kernel<<<static_cast<unsigned>((nb + 127) / 128), 128, 0, ctx->stream>>>(
+                ctx->bnd_jets.as<double>(), ctx->bnd_x.as<double>(), ctx->n_ic, ctx->n_bc, wc, wb,
+                objective == LRNR_OBJ_ABS, ctx->bnd_spec.as<TermSpec>());
+            CK(cudaGetLastError());
+            ++ctx->launches;
+            ctx->term_spec = ctx->bnd_spec.as<TermSpec>();
+            double* d = run_resident_stream<0>(ctx, m, 1.0, nullptr);
+            download(ctx, d, h.data(), h.size());
+            check_bad(ctx, m);
+            accumulate(1);
+        }
+        // locality: lambda * sum_l ||s_l - s_init_l||_1 (training.cpp:550-559, autodiff.cpp:791-802)
+        if (s_init && lambda_local > 0.0) {
+            double acc = 0.0;
+            for (int i = 0; i < m.rtotal; ++i) {
+                const double dv = s[i] - s_init[i];
+                acc += std::fabs(dv);
+                grad[i] += lambda_local * (dv > 0.0 ? 1.0 : (dv < 0.0 ? -1.0 : 0.0));
+            }
+            comps[3] = lambda_local * acc;
+            if (!std::isfinite(comps[3])) throw NonFinite(-1);
+        }
+        if (out_value) *out_value = comps[0] + comps[1] + comps[3];
+        if (out_comps4) std::copy(comps, comps + 4, out_comps4);
+        if (out_grad_s) std::copy(grad.begin(), grad.end(), out_grad_s);
     });
 }
 

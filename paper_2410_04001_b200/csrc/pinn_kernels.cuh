@@ -51,6 +51,19 @@ struct DevNet {
     int rtotal;
 };
 
+// One loss term per point: kind 0 = w N^2, 1 = w |N| (interior, N = CDR
+// residual), 2 = w (u - target)^2, 3 = w |u - target| (value terms: initial
+// u(x,0) - sin x, periodic u(0,t) - u(2pi,t) with the partner's u as target).
+// w_term scales the term's value, w_seed its gradient; a periodic pair puts the
+// term on its first point and a seed-only (w_term = 0) copy on the second.
+struct TermSpec {
+    double target;
+    double w_term;
+    double w_seed;
+    int kind;
+    int pad;
+};
+
 struct RunGeom {
     int64_t n_per_inst;     // points per instance
     int tiles_per_inst;
@@ -145,13 +158,22 @@ __device__ __forceinline__ void warp_sum_store(T (&v)[RMAX], int r, T* dst, int 
     }
 }
 
+template <typename T>
+__device__ __forceinline__ T sgn0(T v) {
+    return v > T(0) ? T(1) : (v < T(0) ? T(-1) : T(0));
+}
+
 // MODE 0: residual + dL/ds;  MODE 1: forward only (loss terms + output jets).
+// Per-point term (TermSpec, internal.h): spec == nullptr -> every point is an
+// interior term of `objective` (0: w N^2, 1: w |N|); otherwise spec[point]
+// gives the kind (adds 2: w (u - c)^2, 3: w |u - c|), the target c and the
+// term / seed weights (training.cpp:286-327, 521-549).
 template <typename T, int TPP, int RMAX, int ACT, int MODE>
 __global__ void __launch_bounds__(kThreads)
 pinn_kernel(const DevNet<T> net, const RunGeom g, const double* __restrict__ pts,
             const double* __restrict__ svec, const double* __restrict__ mus, const T w,
             T* __restrict__ scratch, T* __restrict__ part, double* __restrict__ jets_out,
-            unsigned long long* __restrict__ bad) {
+            unsigned long long* __restrict__ bad, const TermSpec* __restrict__ spec, const int objective) {
     constexpr int SPT = 4 / TPP;
     constexpr int NW = kThreads / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -297,7 +319,18 @@ pinn_kernel(const DevNet<T> net, const RunGeom g, const double* __restrict__ pts
             T u4[4];
             gather4<TPP>(u, u4, base);
             const T N = u4[2] + mu0 * u4[1] - mu1 * u4[3] - mu2 * u4[0] * (T(1) - u4[0]);
-            const T term = valid ? w * (N * N) : T(0);
+            int kind = objective;
+            T tw = w, sw = w, tgt = T(0);
+            if (spec != nullptr && valid) {
+                const TermSpec sp = spec[gp];
+                kind = sp.kind;
+                tgt = T(sp.target);
+                tw = T(sp.w_term);
+                sw = T(sp.w_seed);
+            }
+            const T d = u4[0] - tgt;  // value kinds: u - c
+            T term = kind == 0 ? tw * (N * N) : (kind == 1 ? tw * fabs(N) : (kind == 2 ? tw * (d * d) : tw * fabs(d)));
+            term = valid ? term : T(0);
             if (valid && q == 0 && !finite_val(term)) atomicMin(bad, static_cast<unsigned long long>(gp));
             {
                 T tv = q == 0 ? term : T(0);
@@ -315,13 +348,20 @@ pinn_kernel(const DevNet<T> net, const RunGeom g, const double* __restrict__ pts
                 }
             } else {
                 // ---- reverse sweep ----
-                const T gN = valid ? T(2) * N * w : T(0);
                 T gu[SPT];
+                if (kind <= 1) {
+                    const T gN = valid ? (kind == 0 ? T(2) * N * sw : sgn0(N) * sw) : T(0);
 #pragma unroll
-                for (int i = 0; i < SPT; ++i) {
-                    const int c = q * SPT + i;
-                    gu[i] = c == 0 ? gN * (-mu2 * (T(1) - T(2) * u4[0]))
-                                   : (c == 1 ? gN * mu0 : (c == 2 ? gN : -gN * mu1));
+                    for (int i = 0; i < SPT; ++i) {
+                        const int c = q * SPT + i;
+                        gu[i] = c == 0 ? gN * (-mu2 * (T(1) - T(2) * u4[0]))
+                                       : (c == 1 ? gN * mu0 : (c == 2 ? gN : -gN * mu1));
+                    }
+                } else {
+                    // value terms seed the value slot only (PickValue VJP, autodiff.cpp:715-760)
+                    const T gd = valid ? (kind == 2 ? T(2) * d * sw : sgn0(d) * sw) : T(0);
+#pragma unroll
+                    for (int i = 0; i < SPT; ++i) gu[i] = (q * SPT + i) == 0 ? gd : T(0);
                 }
                 T st[SPT][RMAX];
                 {

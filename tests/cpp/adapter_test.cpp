@@ -2,7 +2,8 @@
 // the same fine-tune gradient (PinnTermEmitter interior terms through
 // run_batch_gradient, training.cpp:191-329) computed by the reference on the CPU
 // and by lrnr::gpu::Engine on the B200, on BASELINE config 0, plus the
-// FastLRNR and NonFiniteError paths.  Exit code 0 = parity within 1e-10.
+// boundary terms, the FastLRNR gradient, the fast-phase objective and the
+// NonFiniteError path.  Exit code 0 = parity within 1e-10.
 // Built by oracle/Makefile into oracle/_ref/adapter_test (needs a GPU to run).
 #include <cmath>
 #include <cstdio>
@@ -89,6 +90,93 @@ int main() {
     const double egf = floor_rel(gotf.grad, reff.grad);
     std::printf("FastLRNR gradient: value rel err %.3e, dL/ds floor-rel err %.3e\n", evf, egf);
 
+    // full fine-tune batch: interior + initial + periodic terms (PinnTermEmitter,
+    // training.cpp:286-327) with the fine_tune weights 1/n per kind
+    pde::CollocationBatch fb = pde::sample_collocation(4007, 1024, 256, 256, ParamDomain{}, false);
+    const double wi = 1.0 / fb.interior.size(), wc = 1.0 / fb.initial_x.size(), wb = 1.0 / fb.periodic_t.size();
+    training::EmitFn emit_full = [&](TapeBindings& ctx, const training::ExtraBindings&, std::size_t idx,
+                                     double* comps) -> NodeId {
+        Tape& tp = ctx.tape;
+        const std::size_t ni = fb.interior.size(), nc = fb.initial_x.size();
+        if (idx < ni) {
+            const NodeId jet = emit_lrnr_jet(tp, fb.interior[idx].x, fb.interior[idx].t, ctx.lrnr, ctx.coeffs.s_leaves);
+            const NodeId term = tp.scale(tp.square(tp.residual_cdr(jet, mu)), wi);
+            comps[0] += tp.value(term);
+            return term;
+        }
+        if (idx < ni + nc) {
+            const double x = fb.initial_x[idx - ni];
+            const NodeId jet = emit_lrnr_jet(tp, x, 0.0, ctx.lrnr, ctx.coeffs.s_leaves);
+            const NodeId term = tp.scale(tp.square(tp.sub_const(tp.pick_value(jet, 0), std::sin(x))), wc);
+            comps[1] += tp.value(term);
+            return term;
+        }
+        const double t = fb.periodic_t[idx - ni - nc];
+        const NodeId j0 = emit_lrnr_jet(tp, 0.0, t, ctx.lrnr, ctx.coeffs.s_leaves);
+        const NodeId j1 = emit_lrnr_jet(tp, pde::kTwoPi, t, ctx.lrnr, ctx.coeffs.s_leaves);
+        const NodeId term = tp.scale(tp.square(tp.sub(tp.pick_value(j0, 0), tp.pick_value(j1, 0))), wb);
+        comps[1] += tp.value(term);
+        return term;
+    };
+    training::BatchGradResult ref_full = training::run_batch_gradient(
+        at, ParamSelector::CoefficientsOnly, nullptr, emit_full,
+        fb.interior.size() + fb.initial_x.size() + fb.periodic_t.size(), par);
+    training::BatchGradResult got_full = eng.tune_gradient(s, mu, fb);
+    const double evb = std::fabs(got_full.value - ref_full.value) / ref_full.value;
+    const double ecb = std::fabs(got_full.comps[1] - ref_full.comps[1]) / ref_full.comps[1];
+    const double egb = floor_rel(got_full.grad, ref_full.grad);
+    std::printf("fine-tune with boundary terms: value %.3e, boundary comp %.3e, dL/ds %.3e\n", evb, ecb, egb);
+
+    // fast-phase emitter (training.cpp:521-559): l1 terms at X + locality
+    Coefficients s_pert = s;
+    for (auto& sl : s_pert.s)
+        for (double& v : sl.data) v = 0.9 * v + 0.01;
+    const double lambda = 1e-2;
+    training::EmitFn emit_phase = [&](TapeBindings& ctx, const training::ExtraBindings& ex, std::size_t idx,
+                                      double* comps) -> NodeId {
+        Tape& tp = ctx.tape;
+        if (idx < X.points.size()) {
+            const pde::Point pt = X.points[idx];
+            switch (reduction::classify_point(pt)) {
+                case reduction::PointKind::Interior: {
+                    const NodeId term =
+                        tp.abs_val(tp.residual_cdr(emit_fast_jet(tp, pt.x, pt.t, ex.fast, ctx.coeffs.s_leaves), mu));
+                    comps[0] += tp.value(term);
+                    return term;
+                }
+                case reduction::PointKind::Initial: {
+                    const NodeId jet = emit_fast_jet(tp, pt.x, 0.0, ex.fast, ctx.coeffs.s_leaves);
+                    const NodeId term = tp.abs_val(tp.sub_const(tp.pick_value(jet, 0), std::sin(pt.x)));
+                    comps[1] += tp.value(term);
+                    return term;
+                }
+                default: {
+                    const NodeId j0 = emit_fast_jet(tp, 0.0, pt.t, ex.fast, ctx.coeffs.s_leaves);
+                    const NodeId j1 = emit_fast_jet(tp, pde::kTwoPi, pt.t, ex.fast, ctx.coeffs.s_leaves);
+                    const NodeId term = tp.abs_val(tp.sub(tp.pick_value(j0, 0), tp.pick_value(j1, 0)));
+                    comps[1] += tp.value(term);
+                    return term;
+                }
+            }
+        }
+        std::vector<NodeId> ids;
+        std::vector<double> ws;
+        for (std::size_t l = 0; l < ctx.coeffs.s_leaves.size(); ++l) {
+            ids.push_back(tp.l1_to_target(ctx.coeffs.s_leaves[l], s.s[l].data.data(), s.s[l].len()));
+            ws.push_back(lambda);
+        }
+        const NodeId term = tp.weighted_sum(ids, ws);
+        comps[3] += tp.value(term);
+        return term;
+    };
+    Trainables atp{nullptr, nullptr, &s_pert};
+    training::BatchGradResult ref_phase = training::run_batch_gradient(atp, ParamSelector::CoefficientsOnly, setup,
+                                                                       emit_phase, X.points.size() + 1, par);
+    training::BatchGradResult got_phase = eng.fast_phase_gradient(s_pert, s, mu, X, lambda);
+    const double evp = std::fabs(got_phase.value - ref_phase.value) / ref_phase.value;
+    const double egp = floor_rel(got_phase.grad, ref_phase.grad);
+    std::printf("fast-phase objective: value %.3e, dL/ds %.3e\n", evp, egp);
+
     // NonFiniteError surfaces as the reference's exception type
     Coefficients bad = s;
     bad.s[1][0] = std::nan("");
@@ -99,7 +187,8 @@ int main() {
         threw = e.layer_tag == -1;
     }
     std::printf("NonFiniteError mapped: %s\n", threw ? "yes" : "NO");
-    const bool ok = ev <= 1e-12 && eg <= 1e-10 && evf <= 1e-12 && egf <= 1e-10 && threw;
+    const bool ok = ev <= 1e-12 && eg <= 1e-10 && evf <= 1e-12 && egf <= 1e-10 && evb <= 1e-12 && ecb <= 1e-12 &&
+                    egb <= 1e-10 && evp <= 1e-12 && egp <= 1e-10 && threw;
     std::printf("%s\n", ok ? "ADAPTER PARITY OK" : "ADAPTER PARITY FAILED");
     return ok ? 0 : 1;
 }

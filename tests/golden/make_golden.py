@@ -55,6 +55,13 @@ def main():
              c0_jets=R.lrnr_jets(w0, r0, P0, s0, pts0[:256]))
     g["c0_loss_tune"] = R.loss_tune(w0, r0, P0, s0, mu0, pts0)
 
+    # the full fine-tune PinnTermEmitter term set (interior + initial + periodic,
+    # training.cpp:286-327) on a fine_tune-style batch (pde::sample_collocation)
+    fb = R.sample_collocation(4007, 1024, 256, 256)
+    ft = R.tune_grad_full(w0, r0, P0, s0, mu0, fb["interior"], fb["initial_x"], fb["periodic_t"], threads=4)
+    g.update(c0_full_pts=fb["interior"], c0_full_ic_x=fb["initial_x"], c0_full_per_t=fb["periodic_t"],
+             c0_full_value=np.array([ft["value"]]), c0_full_comps=ft["comps"], c0_full_grad_s=ft["grad_s"])
+
     # --- config 1: FastLRNR of c0 via the reference EIM recipe ---
     f1 = R.build_fast(w0, r0, P0, s0, mu=mu0, nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777, r_hat=10)
     c1 = R.fast_grad(r0, f1["red_ranks"], f1["fparams"], s0, mu0, pts0, threads=8)

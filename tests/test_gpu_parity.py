@@ -393,3 +393,113 @@ def test_cpp_adapter_drop_in_against_reference():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "ADAPTER PARITY OK" in r.stdout
+
+
+# ----------------------------------------------------------------------------
+# full solve-step term set (boundary terms, fast-phase l1 objective + locality)
+# ----------------------------------------------------------------------------
+def classify_phase_points(X):
+    two_pi = 6.283185307179586476925286766559
+    pts, ic, pt = [], [], []
+    for x, t in X:
+        if t == 0.0:
+            ic.append(x)
+        elif x == 0.0 or x == two_pi:
+            pt.append(t)
+        else:
+            pts.append((x, t))
+    return np.array(pts).reshape(-1, 2), np.array(ic), np.array(pt)
+
+
+def test_full_tune_terms_fp64_match_reference(gpu, golden):
+    """Interior + initial + periodic PinnTermEmitter terms on the device (training.cpp:286-327)."""
+    g = golden
+    gpu.set_lrnr(lrnr_from_golden(g, "c0"), pkg.F64)
+    gpu.set_points(g["c0_full_pts"])
+    gpu.set_boundary(g["c0_full_ic_x"], g["c0_full_per_t"])
+    try:
+        r = gpu.terms_grad(pkg.MODEL_LRNR, g["c0_s"], g["c0_mu"])
+    finally:
+        gpu.set_boundary()
+    assert abs(r["value"] - g["c0_full_value"][0]) <= 1e-12 * abs(g["c0_full_value"][0])
+    np.testing.assert_allclose(r["comps"], g["c0_full_comps"], rtol=1e-12, atol=0)
+    assert floor_rel(r["grad_s"], g["c0_full_grad_s"]) <= TOL64
+
+
+def test_fast_phase_objective_fp64_matches_reference(gpu, golden):
+    """The fast-phase emitter on the device: |N|, |u - sin x|, |u(0,t) - u(2pi,t)|, lambda ||s - s0||_1."""
+    g = golden
+    pts, ic, pt = classify_phase_points(g["c1_phase_x"])
+    gpu.set_fast(pkg.FastParams(g["c0_ranks"], g["c1_red_ranks"], g["c1_fparams"], pkg.ACT_TANH), pkg.F64)
+    gpu.set_points(pts)
+    gpu.set_boundary(ic, pt)
+    try:
+        r = gpu.terms_grad(pkg.MODEL_FAST, g["c1_phase_s"], g["c0_mu"], objective=pkg.OBJ_ABS, w_int=1.0, w_ic=1.0,
+                           w_bc=1.0, s_init=g["c0_s"], lambda_local=1e-2)
+    finally:
+        gpu.set_boundary()
+    assert abs(r["value"] - g["c1_phase_value"][0]) <= 1e-12 * abs(g["c1_phase_value"][0])
+    np.testing.assert_allclose(r["comps"], g["c1_phase_comps"], rtol=1e-12, atol=1e-300)
+    assert floor_rel(r["grad_s"], g["c1_phase_grad_s"]) <= TOL64
+
+
+@pytest.mark.parametrize("objective", [pkg.OBJ_SQUARED, pkg.OBJ_ABS])
+@pytest.mark.parametrize("model", [pkg.MODEL_LRNR, pkg.MODEL_FAST])
+def test_c2_fp32_terms_match_oracle(gpu, oracle, model, objective):
+    """FP32 c2 shapes (sin): every term kind, both models, both objectives against the FP64 oracle."""
+    c = pkg.config2(n_points=1024, act=pkg.ACT_SIN)
+    m, f = c["model"], c["fast"]
+    rng = np.random.default_rng(11)
+    ic, pt = rng.uniform(0, 2 * np.pi, 200), rng.uniform(0, 1, 150)
+    if model == pkg.MODEL_LRNR:
+        gpu.set_lrnr(m, pkg.F32)
+        dims, P = (m.widths, m.ranks), m.params
+    else:
+        gpu.set_fast(f, pkg.F32)
+        dims, P = (f.ranks, f.red_ranks), f.fparams
+    s_init = c["s"] * 1.05
+    gpu.set_points(c["pts"])
+    gpu.set_boundary(ic, pt)
+    try:
+        got = gpu.terms_grad(model, c["s"], c["mu"], objective=objective, s_init=s_init, lambda_local=1e-3)
+    finally:
+        gpu.set_boundary()
+    want = oracle.terms_grad(0 if model == pkg.MODEL_LRNR else 1, dims, P, c["s"], c["mu"], c["pts"], ic, pt,
+                             objective=objective, s_init=s_init, lambda_local=1e-3, act=pkg.ACT_SIN)
+    assert abs(got["value"] - want["value"]) <= TOL32_LOSS * abs(want["value"])
+    np.testing.assert_allclose(got["comps"], want["comps"], rtol=TOL32_LOSS, atol=1e-12)
+    assert normwise(got["grad_s"], want["grad_s"]) <= TOL32_NORM
+
+
+def test_boundary_only_terms(gpu, golden, oracle):
+    """No interior points: only the initial / periodic terms contribute."""
+    g = golden
+    m = lrnr_from_golden(g, "c0")
+    gpu.set_lrnr(m, pkg.F64)
+    gpu.set_points(np.zeros((0, 2)))
+    gpu.set_boundary(g["c0_full_ic_x"][:17], g["c0_full_per_t"][:9])
+    try:
+        r = gpu.terms_grad(pkg.MODEL_LRNR, g["c0_s"], g["c0_mu"])
+    finally:
+        gpu.set_boundary()
+    want = oracle.terms_grad(0, (m.widths, m.ranks), m.params, g["c0_s"], g["c0_mu"], np.zeros((0, 2)),
+                             g["c0_full_ic_x"][:17], g["c0_full_per_t"][:9])
+    assert r["comps"][0] == 0.0
+    assert abs(r["value"] - want["value"]) <= 1e-12 * abs(want["value"])
+    assert floor_rel(r["grad_s"], want["grad_s"]) <= TOL64
+
+
+def test_boundary_nonfinite_maps_to_nonfinite_error(gpu, golden):
+    """A non-finite s leaf seen only through the boundary terms -> NonFiniteError(-1)."""
+    g = golden
+    gpu.set_lrnr(lrnr_from_golden(g, "c0"), pkg.F64)
+    gpu.set_points(np.zeros((0, 2)))
+    gpu.set_boundary(np.array([0.5, 1.5]), np.array([0.25]))
+    s = g["c0_s"].copy()
+    s[5] = np.nan
+    try:
+        with pytest.raises(pkg.NonFiniteError) as ei:
+            gpu.terms_grad(pkg.MODEL_LRNR, s, g["c0_mu"])
+    finally:
+        gpu.set_boundary()
+    assert ei.value.layer_tag == -1
