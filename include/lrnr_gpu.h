@@ -174,6 +174,19 @@ int lrnr_gpu_hyper_loss_grad(lrnr_gpu_ctx* ctx, int model, const double* mus, do
 int lrnr_gpu_meta_loss_grad(lrnr_gpu_ctx* ctx, const double* mus, double w, double* out_value,
                             double* out_grad);
 
+/* meta_train's step with its regularizers (training.cpp:283-305, 368-389), on
+ * the same resident points / mus as lrnr_gpu_meta_loss_grad:
+ *   + lambda_sparse * w * sum_l banded_decay(s_l(mu), gamma) per interior term
+ *     (Tape::banded_decay_penalty, autodiff.cpp:346-360) -> out_comps[2];
+ *   + lambda_ortho * sum_l (||U_l^T U_l - I||_F^2 + ||V_l^T V_l - I||_F^2)
+ *     (gram_ortho_penalty, autodiff.cpp:322-342; meta_train's grad() term)
+ *     -> out_ortho.
+ * out_value = interior + sparse + ortho (meta_train's `loss`), out_grad =
+ * bg.grad + ro.grad in ParamPacker (BasesBiasesAndHyper) order. */
+int lrnr_gpu_meta_terms_grad(lrnr_gpu_ctx* ctx, const double* mus, double w, double lambda_sparse, double gamma,
+                             double lambda_ortho, double* out_value, double* out_comps, double* out_ortho,
+                             double* out_grad);
+
 /* ---- forward only ---- */
 /* Output jets (u, u_x, u_t, u_xx) per point (jet_forward, model.cpp:357-405);
  * s (n_inst x r_total); out (n_points x 4). */

@@ -140,6 +140,30 @@ public:
         return out;
     }
 
+    // meta_train's step (training.cpp:368-389): interior terms + lambda_sparse
+    // banded decay per term (comps[2]) + the lambda_ortho Gram term (returned in
+    // *ortho, as meta_train's `ro`); value = bg.value + ro.value, grad = bg + ro.
+    training::BatchGradResult meta_gradient(const std::vector<PdeParams>& mus, const std::vector<pde::Point>& pts,
+                                            double lambda_sparse, double gamma, double lambda_ortho,
+                                            double* ortho = nullptr) {
+        const std::size_t n_inst = mus.size();
+        if (n_inst == 0 || pts.size() % n_inst) throw std::invalid_argument("meta_gradient: points not grouped by mu");
+        set_points(pts, n_inst);
+        std::vector<double> m(3 * n_inst);
+        for (std::size_t i = 0; i < n_inst; ++i) {
+            m[3 * i] = mus[i].mu1;
+            m[3 * i + 1] = mus[i].mu2;
+            m[3 * i + 2] = mus[i].mu3;
+        }
+        training::BatchGradResult out;
+        out.grad.assign(lrnr_params_ + hyper_params_, 0.0);
+        double ro = 0.0;
+        check(lrnr_gpu_meta_terms_grad(ctx_, m.data(), 0.0, lambda_sparse, gamma, lambda_ortho, &out.value, out.comps,
+                                       &ro, out.grad.data()));
+        if (ortho) *ortho = ro;
+        return out;
+    }
+
     // ---- forward only: loss_tune (training.cpp:139-163), jet_forward (model.cpp:357-405) ----
     training::LossBreakdown loss_tune(const Coefficients& s, const PdeParams& mu, const pde::CollocationBatch& batch) {
         set_points(batch.interior, 1);

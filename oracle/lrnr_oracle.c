@@ -962,6 +962,48 @@ int orc_terms_grad(int model, int L, const int64_t* w, const int64_t* r, const i
     return bad ? 2 : 0;
 }
 
+/* Tape::banded_decay_penalty (autodiff.cpp:346-360) and its VJP (:779-790):
+ * returns sum_i ReLU(-f_i + gamma f_{i+1}); g[i] -= coef, g[i+1] += gamma coef
+ * where the hinge is active. */
+double orc_banded_decay(const double* f, int64_t n, double gamma, double coef, double* g) {
+    double acc = 0.0;
+    for (int64_t i = 0; i + 1 < n; ++i) {
+        const double arg = -f[i] + gamma * f[i + 1];
+        if (arg > 0.0) {
+            acc += arg;
+            if (g) {
+                g[i] -= coef;
+                g[i + 1] += gamma * coef;
+            }
+        }
+    }
+    return acc;
+}
+
+/* Tape::gram_ortho_penalty (autodiff.cpp:322-342) and the GramOrtho VJP
+ * (:761-777): returns ||A^T A - I||_F^2 of a rows x r row-major A;
+ * gA += 4 coef A E with E = A^T A - I. */
+double orc_gram_penalty(const double* A, int64_t rows, int64_t r, double coef, double* gA) {
+    double* e = (double*)malloc((size_t)(r * r) * sizeof(double));
+    for (int64_t i = 0; i < r; ++i)
+        for (int64_t j = 0; j < r; ++j) {
+            double dot = 0.0;
+            for (int64_t k = 0; k < rows; ++k) dot += A[k * r + i] * A[k * r + j];
+            e[i * r + j] = dot - (i == j ? 1.0 : 0.0);
+        }
+    double acc = 0.0;
+    for (int64_t i = 0; i < r * r; ++i) acc += e[i] * e[i];
+    if (gA)
+        for (int64_t i = 0; i < rows; ++i)
+            for (int64_t j = 0; j < r; ++j) {
+                double a = 0.0;
+                for (int64_t k = 0; k < r; ++k) a += A[i * r + k] * e[k * r + j];
+                gA[i * r + j] += 4.0 * coef * a;
+            }
+    free(e);
+    return acc;
+}
+
 int orc_fast_jets(int L, const int64_t* r, const int64_t* rh, int64_t m_in, int64_t m_out,
                   const double* P, int act, const double* s, const double* pts, int64_t n,
                   double* out_jets) {

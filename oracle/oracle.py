@@ -198,6 +198,41 @@ class Oracle:
             raise OracleError("orc_terms_grad: invalid arguments")
         return dict(value=val.value, comps=comps, grad_s=gs, nonfinite=(rc == 2))
 
+    def meta_regs(self, widths, ranks, P, s_inst, n_per, w, lambda_sparse, gamma, lambda_ortho):
+        """meta_train's regularizers for points grouped by instance (s_inst: n_inst x r_total):
+        sparse = sum_i n_per * lambda * w * sum_l banded(s_l(mu_i)) with its dL/ds_i rows, and
+        ortho = lambda_o * sum_l (gram(U_l) + gram(V_l)) with its dL/dparams (ParamPacker order)."""
+        self.lib.orc_banded_decay.restype = C.c_double
+        self.lib.orc_gram_penalty.restype = C.c_double
+        wv, rv = _i64(widths), _i64(ranks)
+        s_inst = np.atleast_2d(_f64(s_inst))
+        ds = np.zeros_like(s_inst)
+        coef = lambda_sparse * w * n_per
+        sparse = 0.0
+        offs = np.concatenate([[0], np.cumsum(rv)])
+        for i in range(s_inst.shape[0]):
+            acc = 0.0
+            for l in range(len(rv)):
+                f = np.ascontiguousarray(s_inst[i, offs[l]:offs[l + 1]])
+                g = np.zeros_like(f)
+                acc += self.lib.orc_banded_decay(_ptr(f), C.c_int64(f.size), C.c_double(gamma), C.c_double(coef),
+                                                 _ptr(g))
+                ds[i, offs[l]:offs[l + 1]] += g
+            sparse += coef * acc
+        P = _f64(P)
+        gP = np.zeros_like(P)
+        ortho, o = 0.0, 0
+        for l in range(len(rv)):
+            for rows in (wv[l + 1], wv[l]):
+                A = np.ascontiguousarray(P[o:o + rows * rv[l]])
+                g = np.zeros_like(A)
+                ortho += lambda_ortho * self.lib.orc_gram_penalty(_ptr(A), C.c_int64(rows), C.c_int64(rv[l]),
+                                                                  C.c_double(lambda_ortho), _ptr(g))
+                gP[o:o + rows * rv[l]] += g
+                o += rows * rv[l]
+            o += wv[l + 1]
+        return dict(sparse=sparse, ds=ds, ortho=ortho, grad_params=gP)
+
     def fast_jets(self, ranks, red, F, s, pts, act=0):
         rv, hv = _i64(ranks), _i64(red)
         pts = _f64(pts).reshape(-1, 2)
@@ -418,6 +453,24 @@ class Reference:
                                         _ptr(_f64(mus).reshape(-1)), C.c_int64(n), C.c_double(w), C.c_int(threads),
                                         C.c_int(chunk), C.byref(val), _ptr(out)), "meta_grad")
         return dict(value=val.value, grad=out)
+
+    def meta_grad_reg(self, widths, ranks, P, hw, H, lo, hi, pts, mus, lambda_sparse, gamma, lambda_ortho, w=None,
+                      threads=1, chunk=64):
+        """meta_train's step gradient with the sparse (banded decay) and ortho (Gram) regularizers."""
+        wv, rv, hwv = _i64(widths), _i64(ranks), _i64(hw)
+        pts = _f64(pts).reshape(-1, 2)
+        n = pts.shape[0]
+        w = (1.0 / n if n else 0.0) if w is None else w
+        out = np.zeros(lrnr_param_count(wv, rv) + hyper_param_count(hwv))
+        comps = np.zeros(4)
+        val, ortho = C.c_double(0.0), C.c_double(0.0)
+        self._rc(self.lib.ref_meta_grad_reg(C.c_int(len(rv)), _ptr(wv), _ptr(rv), _ptr(_f64(P)),
+                                            C.c_int(len(hwv) - 1), _ptr(hwv), _ptr(_f64(H)), _ptr(_f64(lo)),
+                                            _ptr(_f64(hi)), _ptr(pts), _ptr(_f64(mus).reshape(-1)), C.c_int64(n),
+                                            C.c_double(w), C.c_double(lambda_sparse), C.c_double(gamma),
+                                            C.c_double(lambda_ortho), C.c_int(threads), C.c_int(chunk), C.byref(val),
+                                            _ptr(comps), C.byref(ortho), _ptr(out)), "meta_grad_reg")
+        return dict(value=val.value, comps=comps, ortho=ortho.value, grad=out)
 
     def build_fast(self, widths, ranks, P, s, mu=(0.0, 0.0, 0.0), nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777,
                    r_hat=10):

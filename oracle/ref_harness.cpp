@@ -574,6 +574,64 @@ int ref_meta_grad(int L, const int64_t* widths, const int64_t* ranks, const doub
     });
 }
 
+// Meta step with meta_train's regularizers (training.cpp:283-305, 368-389):
+// interior terms w N^2 through the hypernetwork plus, per interior term,
+// lambda_sparse * w * sum_l banded_decay(s_l(mu), gamma) (the emitter's
+// weighted_sum), and lambda_ortho * sum_l (gram(U_l) + gram(V_l)) from grad().
+// out_comps = BatchGradResult comps; out_ortho = ro.value; out_grad = bg + ro.
+int ref_meta_grad_reg(int L, const int64_t* widths, const int64_t* ranks, const double* params, int K,
+                      const int64_t* hw, const double* hparams, const double* lo, const double* hi,
+                      const double* pts, const double* mus, int64_t n, double w, double lambda_sparse,
+                      double gamma, double lambda_ortho, int threads, int chunk, double* out_value,
+                      double* out_comps, double* out_ortho, double* out_grad) {
+    return guarded([&] {
+        LrnrParams p = unpack_lrnr(L, widths, ranks, params);
+        HyperParams h = unpack_hyper(K, hw, hparams, L, ranks, lo, hi);
+        Trainables at{&p, &h, nullptr};
+        training::EmitFn emit = [&](TapeBindings& ctx, const training::ExtraBindings&,
+                                    std::size_t i, double* comps) -> NodeId {
+            Tape& tp = ctx.tape;
+            const PdeParams m = mu_of(mus + 3 * i);
+            const std::vector<NodeId> s_nodes = emit_hyper(tp, m, ctx.hyper);
+            const NodeId jet = emit_lrnr_jet(tp, pts[2 * i], pts[2 * i + 1], ctx.lrnr, s_nodes);
+            const NodeId term = tp.scale(tp.square(tp.residual_cdr(jet, m)), w);
+            comps[0] += tp.value(term);
+            if (lambda_sparse > 0.0) {
+                std::vector<NodeId> ids{term};
+                std::vector<double> ws{1.0};
+                for (const NodeId sn : s_nodes) {
+                    ids.push_back(tp.banded_decay_penalty(sn, gamma));
+                    ws.push_back(lambda_sparse * w);
+                }
+                const NodeId tot = tp.weighted_sum(ids, ws);
+                comps[2] += tp.value(tot) - tp.value(term);
+                return tot;
+            }
+            return term;
+        };
+        training::BatchGradResult bg = training::run_batch_gradient(
+            at, ParamSelector::BasesBiasesAndHyper, nullptr, emit, static_cast<std::size_t>(n),
+            par_of(threads, chunk));
+        GradResult ro = grad(
+            [&](TapeBindings& ctx) {
+                std::vector<NodeId> ids;
+                std::vector<double> ws;
+                for (std::size_t l = 0; l < ctx.at.lrnr->depth(); ++l) {
+                    ids.push_back(ctx.tape.gram_ortho_penalty(ctx.lrnr.u_slots[l]));
+                    ws.push_back(lambda_ortho);
+                    ids.push_back(ctx.tape.gram_ortho_penalty(ctx.lrnr.v_slots[l]));
+                    ws.push_back(lambda_ortho);
+                }
+                return ctx.tape.weighted_sum(ids, ws);
+            },
+            at, ParamSelector::BasesBiasesAndHyper);
+        *out_value = bg.value + ro.value;
+        for (int k = 0; k < 4; ++k) out_comps[k] = bg.comps[k];
+        *out_ortho = ro.value;
+        for (std::size_t i = 0; i < bg.grad.size(); ++i) out_grad[i] = bg.grad[i] + ro.grad[i];
+    });
+}
+
 // ---- FastLRNR construction (reduction.cpp:10-31,111-283) ----
 // Constant hypernetwork (zero W, bias = s) so hyper_forward(mu) == s.
 int ref_build_fast(int L, const int64_t* widths, const int64_t* ranks, const double* params,

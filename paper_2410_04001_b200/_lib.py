@@ -16,7 +16,7 @@ EXPORTS = (
     "lrnr_gpu_create", "lrnr_gpu_destroy", "lrnr_gpu_last_error", "lrnr_gpu_last_layer_tag",
     "lrnr_gpu_set_stream", "lrnr_gpu_set_option", "lrnr_gpu_launch_count", "lrnr_gpu_set_lrnr", "lrnr_gpu_set_fast",
     "lrnr_gpu_set_hyper", "lrnr_gpu_set_points", "lrnr_gpu_set_points_device", "lrnr_gpu_loss_grad_s",
-    "lrnr_gpu_set_boundary", "lrnr_gpu_terms_grad",
+    "lrnr_gpu_set_boundary", "lrnr_gpu_terms_grad", "lrnr_gpu_meta_terms_grad",
     "lrnr_gpu_loss_grad_s_multi", "lrnr_gpu_hyper_loss_grad", "lrnr_gpu_meta_loss_grad", "lrnr_gpu_jets",
     "lrnr_gpu_loss", "lrnr_gpu_upload_coeffs", "lrnr_gpu_run", "lrnr_gpu_check", "lrnr_gpu_download",
     "lrnr_gpu_fma_peak",
@@ -66,6 +66,7 @@ def load() -> C.CDLL:
     lib.lrnr_gpu_loss_grad_s_multi.argtypes = [vp, ip, dp, dp, C.c_double, dp, dp]
     lib.lrnr_gpu_hyper_loss_grad.argtypes = [vp, ip, dp, C.c_double, dp, dp, dp]
     lib.lrnr_gpu_meta_loss_grad.argtypes = [vp, dp, C.c_double, dp, dp]
+    lib.lrnr_gpu_meta_terms_grad.argtypes = [vp, dp, C.c_double, C.c_double, C.c_double, C.c_double, dp, dp, dp, dp]
     lib.lrnr_gpu_jets.argtypes = [vp, ip, dp, dp]
     lib.lrnr_gpu_loss.argtypes = [vp, ip, dp, dp, C.c_double, dp]
     lib.lrnr_gpu_upload_coeffs.argtypes = [vp, dp, dp, i64]

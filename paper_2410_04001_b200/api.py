@@ -306,6 +306,16 @@ class GpuContext:
                  "meta_loss_grad")
         return dict(value=v.value, grad=g)
 
+    def meta_terms_grad(self, mus, n_lrnr_params, lambda_sparse=0.0, gamma=1.5, lambda_ortho=0.0, w=0.0):
+        """meta_train's step: interior terms + sparse (banded decay) + ortho (Gram) regularizers."""
+        g = np.zeros(n_lrnr_params + self.hyper_n)
+        comps = np.zeros(4)
+        v, ro = C.c_double(0.0), C.c_double(0.0)
+        self._rc(self.lib.lrnr_gpu_meta_terms_grad(self.h, _p(_f64(mus)), C.c_double(w), C.c_double(lambda_sparse),
+                                                   C.c_double(gamma), C.c_double(lambda_ortho), C.byref(v),
+                                                   _p(comps), C.byref(ro), _p(g)), "meta_terms_grad")
+        return dict(value=v.value, comps=comps, ortho=ro.value, grad=g)
+
     def jets(self, model, s):
         out = np.zeros((self.n_points, 4))
         self._rc(self.lib.lrnr_gpu_jets(self.h, model, _p(_f64(s)), _p(out)), "jets")

@@ -87,6 +87,7 @@ struct Model {
     DevBuf dev;
     // LRNR-only extras for the meta path: original flat params (double)
     std::vector<double> flat;
+    DevBuf flat_dev;  // flat on the device (meta Gram regularizer), uploaded on first use
     std::vector<int64_t> widths64, ranks64;
     // kernel-v2 (tile-GEMM) layout: chunk blocks + per-tile schedule
     struct V2 {
@@ -175,7 +176,7 @@ struct lrnr_gpu_ctx {
     int64_t coeff_inst = 0;
     int coeff_rtotal = 0;
     // workspaces
-    lrnr_b200::detail::DevBuf scratch, ascratch, part, out, bad, acts, G, hgrad, jets, meta_ws;
+    lrnr_b200::detail::DevBuf scratch, ascratch, part, out, bad, acts, G, hgrad, jets, meta_ws, gram_ws;
     int64_t out_rows = 0;
     int out_R1 = 0;
     std::string err;

@@ -64,6 +64,12 @@ struct TermSpec {
     int pad;
 };
 
+// per-layer offsets of s_l inside the coefficient vector (meta regularizers)
+struct BandLayout {
+    int L;
+    int off[kMaxL + 1];
+};
+
 struct RunGeom {
     int64_t n_per_inst;     // points per instance
     int tiles_per_inst;

@@ -111,6 +111,15 @@ def main():
     g.update(c4_widths=np.array(w4), c4_ranks=np.array(r4), c4_params=P4, c4_hw=hw4, c4_hparams=H4, c4_pts=pts4,
              c4_mus=mus4, c4_value=np.array([m4["value"]]), c4_grad=m4["grad"])
 
+    # meta_train's regularizers on the same step: lambda_sparse banded decay per
+    # interior term (training.cpp:295-305) and lambda_ortho Gram penalties (:378-389)
+    # (parameters scaled by 1.1 so the bases are off the Stiefel manifold and the
+    # Gram penalty is non-trivial)
+    P4r = P4 * 1.1
+    m4r = R.meta_grad_reg(w4, r4, P4r, hw4, H4, lo3, hi3, pts4, mus4, 1e-2, 1.5, 1e-3, threads=4)
+    g.update(c4_reg=np.array([1e-2, 1.5, 1e-3]), c4_reg_params=P4r, c4_reg_value=np.array([m4r["value"]]), c4_reg_comps=m4r["comps"],
+             c4_reg_ortho=np.array([m4r["ortho"]]), c4_reg_grad=m4r["grad"])
+
     path = os.path.join(OUT, "reference_golden.npz")
     np.savez_compressed(path, **g)
     print("wrote", path, os.path.getsize(path), "bytes;", len(g), "arrays")

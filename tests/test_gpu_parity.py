@@ -379,6 +379,53 @@ def test_meta_c4_shape_fp32_matches_oracle(gpu, oracle, act):
     assert normwise(got["grad"][nP:], want[nP:]) <= TOL32_NORM
 
 
+def test_meta_regularizers_fp64_match_reference(gpu, golden):
+    """meta_train's step with lambda_sparse banded decay and lambda_ortho Gram penalties."""
+    g = golden
+    lam_sp, gamma, lam_o = g["c4_reg"]
+    m = pkg.LrnrParams(g["c4_widths"], g["c4_ranks"], g["c4_reg_params"], pkg.ACT_TANH)
+    gpu.set_lrnr(m, pkg.F64)
+    gpu.set_hyper(pkg.HyperParams(g["c4_hw"], g["c4_hparams"], g["c3_lo"], g["c3_hi"]))
+    gpu.set_points(g["c4_pts"], n_inst=2)
+    r = gpu.meta_terms_grad(np.array([g["c4_mus"][0], g["c4_mus"][-1]]), m.params.size, lam_sp, gamma, lam_o)
+    assert abs(r["value"] - g["c4_reg_value"][0]) <= 1e-12 * g["c4_reg_value"][0]
+    np.testing.assert_allclose(r["comps"], g["c4_reg_comps"], rtol=1e-12, atol=0)
+    assert abs(r["ortho"] - g["c4_reg_ortho"][0]) <= 1e-12 * g["c4_reg_ortho"][0]
+    assert normwise(r["grad"], g["c4_reg_grad"]) <= 1e-10
+
+
+@pytest.mark.parametrize("act", [pkg.ACT_SIN, pkg.ACT_TANH])
+def test_meta_regularizers_c4_shape_fp32_match_oracle(gpu, oracle, act):
+    n_inst, per = 2, 96
+    c = pkg.config4(n_inst=n_inst, pts_per_inst=per, act=act)
+    m, h = c["model"], c["hyper"]
+    P = m.params * 1.05  # off the Stiefel manifold: non-trivial Gram penalty
+    m = pkg.LrnrParams(m.widths, m.ranks, P, act)
+    lam = (1e-2, 1.5, 1e-4)
+    gpu.set_lrnr(m, pkg.F32)
+    gpu.set_hyper(h)
+    gpu.set_points(c["pts"], n_inst=n_inst)
+    got = gpu.meta_terms_grad(c["mus"], m.params.size, *lam)
+    w = 1.0 / (n_inst * per)
+    nP = m.params.size
+    S = np.stack([oracle.hyper_forward(h.hw, h.params, h.lo, h.hi, mu) for mu in c["mus"]])
+    regs = oracle.meta_regs(m.widths, m.ranks, P, S, per, w, *lam)
+    want = np.zeros(nP + h.n_params)
+    val = 0.0
+    for i in range(n_inst):
+        r = oracle.lrnr_grad(m.widths, m.ranks, P, S[i], c["mus"][i], c["pts"][i * per:(i + 1) * per], w=w, act=act,
+                             params_grad=True)
+        val += r["value"]
+        want[:nP] += r["grad_params"]
+        oracle.hyper_vjp(h.hw, h.params, h.lo, h.hi, c["mus"][i], r["grad_s"] + regs["ds"][i], out=want[nP:])
+    want[:nP] += regs["grad_params"]
+    assert abs(got["comps"][0] - val) <= TOL32_LOSS * abs(val)
+    assert abs(got["comps"][2] - regs["sparse"]) <= 1e-6 * abs(regs["sparse"])  # FP64 on the device
+    assert abs(got["ortho"] - regs["ortho"]) <= 1e-10 * abs(regs["ortho"])
+    assert normwise(got["grad"], want) <= TOL32_NORM
+    assert normwise(got["grad"][nP:], want[nP:]) <= TOL32_NORM
+
+
 def test_cpp_adapter_drop_in_against_reference():
     """include/lrnr_gpu_adapter.hpp compiled against the reference's own headers and
     objects (oracle/_ref/adapter_test): same fine-tune / FastLRNR gradient as
