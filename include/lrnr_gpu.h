@@ -159,6 +159,30 @@ int lrnr_gpu_terms_grad(lrnr_gpu_ctx* ctx, int model, const double* s, const dou
                         double w_ic, double w_bc, const double* s_init, double lambda_local, double* out_value,
                         double* out_comps, double* out_grad_s);
 
+/* ---- solve loops on the device ----
+ * lrnr_gpu_fine_tune: fine_tune (training.cpp:428-496) for the bound LRNR:
+ * from s_init (= hyper_forward(mu, theta) in the reference), `epochs` epochs of
+ * the PinnTermEmitter terms over a batch re-sampled every epoch exactly as
+ * pde::sample_collocation(epoch_seed(seed, e), n_int, n_ic, n_bc) (bit-identical
+ * host generator, double-buffered pinned upload overlapped with the device),
+ * adam_step (autodiff.cpp:1062-1075, lr, beta 0.9/0.999, eps 1e-8),
+ * project_nonnegative_coeffs and the best iterate, all on the device.
+ * lrnr_gpu_fast_solve: fast_solve (training.cpp:498-607) for the bound
+ * FastLRNR on the sampling set X (n_x points, classified as classify_point
+ * does): the l1 terms + lambda_local ||s - s_init||_1, the divergence stop
+ * (loss > 1e3 x the first loss), Adam + projection + best iterate; one epoch
+ * is captured as a CUDA graph and replayed with no host synchronization.
+ * Outputs: out_s = best coefficients (r_total), out_losses[e] = the epoch's
+ * loss for the recorded epochs (capacity `epochs`), out_n_records, out_flags
+ * (1 = aborted on a non-finite value, 2 = diverged), best loss / epoch.
+ * Both overwrite the context's resident coefficients and keep its points. */
+int lrnr_gpu_fine_tune(lrnr_gpu_ctx* ctx, const double* s_init, const double* mu, double lr, int64_t epochs,
+                       int64_t n_int, int64_t n_ic, int64_t n_bc, uint64_t seed, double* out_s, double* out_best_loss,
+                       int64_t* out_best_epoch, double* out_losses, int64_t* out_n_records, int* out_flags);
+int lrnr_gpu_fast_solve(lrnr_gpu_ctx* ctx, const double* s_init, const double* mu, const double* X, int64_t n_x,
+                        double lambda_local, double lr, int64_t epochs, double* out_s, double* out_best_loss,
+                        int64_t* out_best_epoch, double* out_losses, int64_t* out_n_records, int* out_flags);
+
 /* Hypernetwork-coupled step (BASELINE config 3; the emit_hyper + emit_fast_jet
  * composition of autodiff.cpp:883-922): s_i = hyper(mu_i) on device, the model
  * gradient per instance, then the hypernetwork VJP summed over instances.
@@ -226,6 +250,10 @@ int lrnr_host_make_hyper_params(int depth_split, const int64_t* split, int hidde
 int lrnr_host_sample_collocation(uint64_t seed, int64_t n_interior, const double* mu_lo,
                                  const double* mu_hi, int with_mu, double* out_xt,
                                  double* out_mu);
+/* training.cpp:20-26 and pde.cpp:20-49 (no mu): the fine_tune epoch batch. */
+uint64_t lrnr_host_epoch_seed(uint64_t base, int64_t epoch);
+int lrnr_host_sample_batch(uint64_t seed, int64_t n_int, int64_t n_ic, int64_t n_bc, double* out_xt,
+                           double* out_ic_x, double* out_per_t);
 /* FastLRNR construction: harvest_snapshots at SamplingSetX::uniform_grid(nx, nt)
  * with n_perturb Gaussian perturbations (sigma * extent), greedy EIM with budget
  * r_hat per inner layer, build_fastparams (reduction.cpp:10-31,111-283), for

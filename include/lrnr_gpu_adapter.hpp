@@ -164,6 +164,39 @@ public:
         return out;
     }
 
+    // ---- the solve loops (training.cpp:428-607) on the device: drop-ins for
+    // training::fine_tune / training::fast_solve (L1 evaluation (eval_interval)
+    // and wall-clock fields are not produced: records carry epoch and loss).
+    training::SolveResult fine_tune(const PdeParams& mu, const HyperParams& theta, const training::PhaseConfig& cfg) {
+        training::SolveResult out;
+        out.coeffs = hyper_forward(mu, theta);
+        out.report.phase = "fine-tune";
+        if (cfg.epochs == 0) return out;
+        const std::vector<double> s0 = flatten(out.coeffs);
+        const double m[3] = {mu.mu1, mu.mu2, mu.mu3};
+        solve_into(out, lrnr_gpu_fine_tune, cfg.epochs, s0.data(), m, cfg.lr, static_cast<int64_t>(cfg.epochs),
+                   static_cast<int64_t>(cfg.n_interior), static_cast<int64_t>(cfg.n_initial),
+                   static_cast<int64_t>(cfg.n_periodic), static_cast<uint64_t>(cfg.seed));
+        return out;
+    }
+    training::SolveResult fast_solve(const PdeParams& mu, const HyperParams& theta, const reduction::SamplingSetX& X,
+                                     const training::PhaseConfig& cfg, double lambda_local) {
+        training::SolveResult out;
+        out.coeffs = hyper_forward(mu, theta);
+        out.report.phase = lambda_local > 0.0 ? "fast" : "fast-naive";
+        if (cfg.epochs == 0) return out;
+        const std::vector<double> s0 = flatten(out.coeffs);
+        const double m[3] = {mu.mu1, mu.mu2, mu.mu3};
+        std::vector<double> xt;
+        for (const pde::Point& p : X.points) {
+            xt.push_back(p.x);
+            xt.push_back(p.t);
+        }
+        solve_into(out, lrnr_gpu_fast_solve, cfg.epochs, s0.data(), m, xt.data(),
+                   static_cast<int64_t>(X.points.size()), lambda_local, cfg.lr, static_cast<int64_t>(cfg.epochs));
+        return out;
+    }
+
     // ---- forward only: loss_tune (training.cpp:139-163), jet_forward (model.cpp:357-405) ----
     training::LossBreakdown loss_tune(const Coefficients& s, const PdeParams& mu, const pde::CollocationBatch& batch) {
         set_points(batch.interior, 1);
@@ -217,6 +250,27 @@ private:
         }
         check(lrnr_gpu_set_points(ctx_, xt.data(), static_cast<int64_t>(n_inst),
                                   static_cast<int64_t>(pts.size() / n_inst)));
+    }
+    template <class Fn, class... A>
+    void solve_into(training::SolveResult& out, Fn fn, std::size_t epochs, A... args) {
+        std::vector<double> s(flatten(out.coeffs).size()), losses(epochs);
+        double best = 0.0;
+        int64_t best_e = 0, n_rec = 0;
+        int flags = 0;
+        check(fn(ctx_, args..., s.data(), &best, &best_e, losses.data(), &n_rec, &flags));
+        for (int64_t e = 0; e < n_rec; ++e) {
+            training::EpochRecord rec;
+            rec.epoch = static_cast<std::size_t>(e + 1);
+            rec.loss = losses[e];
+            out.report.records.push_back(rec);
+        }
+        out.report.aborted_nonfinite = (flags & 1) != 0;
+        out.report.diverged = (flags & 2) != 0;
+        out.report.best_loss = best;
+        out.report.best_epoch = static_cast<std::size_t>(best_e);
+        std::size_t o = 0;
+        for (auto& v : out.coeffs.s)
+            for (double& x : v.data) x = s[o++];
     }
     void set_boundary(const std::vector<double>& ic, const std::vector<double>& per) {
         check(lrnr_gpu_set_boundary(ctx_, ic.data(), static_cast<int64_t>(ic.size()), per.data(),

@@ -1399,3 +1399,137 @@ int orc_meta_train(int L, const int64_t* w, const int64_t* r, int hyper_depth, i
     free(gtot);
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* The solve loops (training.cpp:428-607): fine_tune and fast_solve.         */
+/* Initial coefficients s_init stand for hyper_forward(mu, theta).           */
+/* Per epoch: the term gradient (orc_terms_grad), the EpochRecord loss, the  */
+/* divergence stop (fast_solve: loss > 1e3 x the first loss), best-iterate,  */
+/* adam_step (autodiff.cpp:1062-1075, beta 0.9 / 0.999, eps 1e-8) and        */
+/* project_nonnegative_coeffs (autodiff.cpp:967-977).  NonFiniteError ->     */
+/* aborted (+ diverged in fast_solve) and stop.  flags: 1 aborted, 2 diverged.*/
+/* ------------------------------------------------------------------------ */
+static int solve_loop(int model, int L, const int64_t* w, const int64_t* r, const int64_t* rh, const double* P,
+                      int act, const double* s_init, const double* mu, double lr, int64_t epochs, int fast,
+                      /* fine_tune batch recipe */ int64_t n_int, int64_t n_ic, int64_t n_bc, uint64_t seed,
+                      /* fast_solve sampling set (classified) */ const double* fx_int, int64_t fn_int,
+                      const double* fx_ic, int64_t fn_ic, const double* fx_bc, int64_t fn_bc, double lambda_local,
+                      int64_t chunk, double* out_s, double* out_best_loss, int64_t* out_best_epoch,
+                      double* out_losses, int64_t* out_n_records, int* out_flags) {
+    int64_t G = 0;
+    for (int l = 0; l < L; ++l) G += r[l];
+    double* x = (double*)malloc((size_t)G * sizeof(double));
+    double* best = (double*)malloc((size_t)G * sizeof(double));
+    double* m = (double*)calloc((size_t)G, sizeof(double));
+    double* v = (double*)calloc((size_t)G, sizeof(double));
+    double* g = (double*)malloc((size_t)G * sizeof(double));
+    memcpy(x, s_init, (size_t)G * sizeof(double));
+    memcpy(best, s_init, (size_t)G * sizeof(double));
+    double best_loss = INFINITY, initial = NAN, comps[4];
+    int64_t best_e = 0, n_rec = 0, t_adam = 0;
+    int flags = 0, rc = 0;
+    const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
+    double* pint = (double*)malloc((size_t)(2 * n_int + 1) * sizeof(double));
+    double* pic = (double*)malloc((size_t)(n_ic + 1) * sizeof(double));
+    double* pper = (double*)malloc((size_t)(n_bc + 1) * sizeof(double));
+    for (int64_t e = 1; e <= epochs; ++e) {
+        double value;
+        int st;
+        if (!fast) {
+            const double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+            orc_sample_collocation(epoch_seed(seed, e), n_int, n_ic, n_bc, lo, hi, 0, pint, pic, pper, NULL, NULL,
+                                   NULL);
+            st = orc_terms_grad(model, L, w, r, rh, P, act, x, mu, pint, n_int, pic, n_ic, pper, n_bc,
+                                n_int ? 1.0 / (double)n_int : 0.0, n_ic ? 1.0 / (double)n_ic : 0.0,
+                                n_bc ? 1.0 / (double)n_bc : 0.0, 0, NULL, 0.0, chunk, &value, comps, g);
+        } else {
+            st = orc_terms_grad(model, L, w, r, rh, P, act, x, mu, fx_int, fn_int, fx_ic, fn_ic, fx_bc, fn_bc, 1.0,
+                                1.0, 1.0, 1, lambda_local > 0.0 ? s_init : NULL, lambda_local, chunk, &value, comps,
+                                g);
+        }
+        if (st == 1) {
+            rc = 1;
+            break;
+        }
+        if (st == 2) {
+            flags |= fast ? 3 : 1;
+            break;
+        }
+        out_losses[n_rec++] = value;
+        if (fast) {
+            if (e == 1) initial = value;
+            if (value > 1e3 * initial) {
+                flags |= 2;
+                break;
+            }
+        }
+        if (value < best_loss) {
+            best_loss = value;
+            best_e = e;
+            memcpy(best, x, (size_t)G * sizeof(double));
+        }
+        t_adam += 1;
+        const double b1t = 1.0 - pow(b1, (double)t_adam);
+        const double b2t = 1.0 - pow(b2, (double)t_adam);
+        for (int64_t i = 0; i < G; ++i) {
+            m[i] = b1 * m[i] + (1.0 - b1) * g[i];
+            v[i] = b2 * v[i] + (1.0 - b2) * g[i] * g[i];
+            const double mhat = m[i] / b1t;
+            const double vhat = v[i] / b2t;
+            x[i] -= lr * mhat / (sqrt(vhat) + eps);
+            if (x[i] < 0.0) x[i] = 0.0;
+        }
+    }
+    memcpy(out_s, best, (size_t)G * sizeof(double));
+    *out_best_loss = best_loss;
+    *out_best_epoch = best_e;
+    *out_n_records = n_rec;
+    *out_flags = flags;
+    free(x);
+    free(best);
+    free(m);
+    free(v);
+    free(g);
+    free(pint);
+    free(pic);
+    free(pper);
+    return rc;
+}
+
+int orc_fine_tune(int L, const int64_t* w, const int64_t* r, const double* P, int act, const double* s_init,
+                  const double* mu, double lr, int64_t epochs, int64_t n_int, int64_t n_ic, int64_t n_bc,
+                  uint64_t seed, int64_t chunk, double* out_s, double* out_best_loss, int64_t* out_best_epoch,
+                  double* out_losses, int64_t* out_n_records, int* out_flags) {
+    return solve_loop(0, L, w, r, NULL, P, act, s_init, mu, lr, epochs, 0, n_int, n_ic, n_bc, seed, NULL, 0, NULL,
+                      0, NULL, 0, 0.0, chunk, out_s, out_best_loss, out_best_epoch, out_losses, out_n_records,
+                      out_flags);
+}
+
+/* X is the fast phase's sampling set, classified with classify_point (reduction.cpp:27-31). */
+int orc_fast_solve(int L, const int64_t* r, const int64_t* rh, const double* F, int act, const double* s_init,
+                   const double* mu, const double* X, int64_t n_x, double lambda_local, double lr, int64_t epochs,
+                   int64_t chunk, double* out_s, double* out_best_loss, int64_t* out_best_epoch, double* out_losses,
+                   int64_t* out_n_records, int* out_flags) {
+    double* xi = (double*)malloc((size_t)(2 * n_x + 1) * sizeof(double));
+    double* xc = (double*)malloc((size_t)(n_x + 1) * sizeof(double));
+    double* xb = (double*)malloc((size_t)(n_x + 1) * sizeof(double));
+    int64_t ni = 0, nc = 0, nb = 0;
+    for (int64_t i = 0; i < n_x; ++i) {
+        const double x = X[2 * i], t = X[2 * i + 1];
+        if (t == 0.0) xc[nc++] = x;
+        else if (x == 0.0 || x == ORC_TWO_PI) xb[nb++] = t;
+        else {
+            xi[2 * ni] = x;
+            xi[2 * ni + 1] = t;
+            ++ni;
+        }
+    }
+    const int64_t w2[2] = {2, 1};
+    const int rc = solve_loop(1, L, w2, r, rh, F, act, s_init, mu, lr, epochs, 1, 0, 0, 0, 0, xi, ni, xc, nc, xb,
+                              nb, lambda_local, chunk, out_s, out_best_loss, out_best_epoch, out_losses,
+                              out_n_records, out_flags);
+    free(xi);
+    free(xc);
+    free(xb);
+    return rc;
+}

@@ -233,6 +233,33 @@ class Oracle:
             o += wv[l + 1]
         return dict(sparse=sparse, ds=ds, ortho=ortho, grad_params=gP)
 
+    def fine_tune(self, widths, ranks, P, s_init, mu, lr, epochs, n_int, n_ic, n_bc, seed, act=0, chunk=64):
+        """fine_tune (training.cpp:428-496) from s_init = hyper_forward(mu)."""
+        wv, rv = _i64(widths), _i64(ranks)
+        return self._solve(self.lib.orc_fine_tune, int(rv.sum()), epochs, C.c_int(len(rv)), _ptr(wv), _ptr(rv),
+                           _ptr(_f64(P)), C.c_int(act), _ptr(_f64(s_init)), _ptr(_f64(mu)), C.c_double(lr),
+                           C.c_int64(epochs), C.c_int64(n_int), C.c_int64(n_ic), C.c_int64(n_bc), C.c_uint64(seed),
+                           C.c_int64(chunk))
+
+    def fast_solve(self, ranks, red, F, s_init, mu, X, lambda_local, lr, epochs, act=0, chunk=64):
+        """fast_solve (training.cpp:498-607) on the sampling set X."""
+        rv, hv = _i64(ranks), _i64(red)
+        X = _f64(X).reshape(-1, 2)
+        return self._solve(self.lib.orc_fast_solve, int(rv.sum()), epochs, C.c_int(len(rv)), _ptr(rv), _ptr(hv),
+                           _ptr(_f64(F)), C.c_int(act), _ptr(_f64(s_init)), _ptr(_f64(mu)), _ptr(X),
+                           C.c_int64(X.shape[0]), C.c_double(lambda_local), C.c_double(lr), C.c_int64(epochs),
+                           C.c_int64(chunk))
+
+    def _solve(self, fn, G, epochs, *args):
+        s = np.zeros(G)
+        losses = np.zeros(max(1, epochs))
+        bl, be, nr, fl = C.c_double(0.0), C.c_int64(0), C.c_int64(0), C.c_int(0)
+        rc = fn(*args, _ptr(s), C.byref(bl), C.byref(be), _ptr(losses), C.byref(nr), C.byref(fl))
+        if rc:
+            raise OracleError("solve loop: invalid arguments")
+        return dict(s=s, best_loss=bl.value, best_epoch=be.value, losses=losses[:nr.value], aborted=bool(fl.value & 1),
+                    diverged=bool(fl.value & 2))
+
     def fast_jets(self, ranks, red, F, s, pts, act=0):
         rv, hv = _i64(ranks), _i64(red)
         pts = _f64(pts).reshape(-1, 2)
@@ -396,6 +423,28 @@ class Reference:
                                              C.c_double(w_int), C.c_double(w_ic), C.c_double(w_bc), C.c_int(threads),
                                              C.c_int(chunk), C.byref(val), _ptr(comps), _ptr(gs)), "tune_grad_full")
         return dict(value=val.value, comps=comps, grad_s=gs)
+
+    def fine_tune(self, widths, ranks, P, s_init, mu, lr, epochs, n_int, n_ic, n_bc, seed, threads=2):
+        wv, rv = _i64(widths), _i64(ranks)
+        return self._solve(self.lib.ref_fine_tune, int(rv.sum()), epochs, C.c_int(len(rv)), _ptr(wv), _ptr(rv),
+                           _ptr(_f64(P)), _ptr(_f64(s_init)), _ptr(_f64(mu)), C.c_double(lr), C.c_int64(epochs),
+                           C.c_int64(n_int), C.c_int64(n_ic), C.c_int64(n_bc), C.c_uint64(seed), C.c_int(threads))
+
+    def fast_solve(self, ranks, red, F, s_init, mu, X, lambda_local, lr, epochs, threads=2):
+        rv, hv = _i64(ranks), _i64(red)
+        X = _f64(X).reshape(-1, 2)
+        return self._solve(self.lib.ref_fast_solve, int(rv.sum()), epochs, C.c_int(len(rv)), _ptr(rv), _ptr(hv),
+                           C.c_int64(2), C.c_int64(1), _ptr(_f64(F)), _ptr(_f64(s_init)), _ptr(_f64(mu)), _ptr(X),
+                           C.c_int64(X.shape[0]), C.c_double(lambda_local), C.c_double(lr), C.c_int64(epochs),
+                           C.c_int(threads))
+
+    def _solve(self, fn, G, epochs, *args):
+        s = np.zeros(G)
+        losses = np.zeros(max(1, epochs))
+        bl, be, nr, fl = C.c_double(0.0), C.c_int64(0), C.c_int64(0), C.c_int(0)
+        self._rc(fn(*args, _ptr(s), C.byref(bl), C.byref(be), _ptr(losses), C.byref(nr), C.byref(fl)), "solve")
+        return dict(s=s, best_loss=bl.value, best_epoch=be.value, losses=losses[:nr.value], aborted=bool(fl.value & 1),
+                    diverged=bool(fl.value & 2))
 
     def lrnr_jets(self, widths, ranks, P, s, pts):
         wv, rv = _i64(widths), _i64(ranks)

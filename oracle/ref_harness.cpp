@@ -632,6 +632,72 @@ int ref_meta_grad_reg(int L, const int64_t* widths, const int64_t* ranks, const 
     });
 }
 
+// ---- the reference's own solve loops (training.cpp:428-607) ----
+// A constant hypernetwork (W = 0, b = s_init) makes hyper_forward(mu) == s_init
+// (s_init >= 0: the output ReLU passes it unchanged).
+static HyperParams constant_hyper(const std::vector<std::size_t>& ranks, const double* s_init) {
+    HyperParams h;
+    std::size_t r_total = 0;
+    for (auto r : ranks) r_total += r;
+    h.w.emplace_back(r_total, 3);
+    DenseVector b(r_total);
+    for (std::size_t i = 0; i < r_total; ++i) b[i] = s_init[i];
+    h.b.push_back(std::move(b));
+    h.split = ranks;
+    h.box = ParamDomain::d1();
+    return h;
+}
+
+static void copy_solve(const training::SolveResult& r, double* out_s, double* out_best_loss, int64_t* out_best_epoch,
+                       double* out_losses, int64_t* out_n_records, int* out_flags) {
+    std::size_t o = 0;
+    for (const auto& v : r.coeffs.s)
+        for (double x : v.data) out_s[o++] = x;
+    *out_best_loss = r.report.best_loss;
+    *out_best_epoch = static_cast<int64_t>(r.report.best_epoch);
+    *out_n_records = static_cast<int64_t>(r.report.records.size());
+    for (std::size_t e = 0; e < r.report.records.size(); ++e) out_losses[e] = r.report.records[e].loss;
+    *out_flags = (r.report.aborted_nonfinite ? 1 : 0) | (r.report.diverged ? 2 : 0);
+}
+
+int ref_fine_tune(int L, const int64_t* widths, const int64_t* ranks, const double* params, const double* s_init,
+                  const double* mu, double lr, int64_t epochs, int64_t n_int, int64_t n_ic, int64_t n_bc,
+                  uint64_t seed, int threads, double* out_s, double* out_best_loss, int64_t* out_best_epoch,
+                  double* out_losses, int64_t* out_n_records, int* out_flags) {
+    return guarded([&] {
+        LrnrParams p = unpack_lrnr(L, widths, ranks, params);
+        HyperParams h = constant_hyper(p.ranks, s_init);
+        training::PhaseConfig cfg;
+        cfg.lr = lr;
+        cfg.epochs = static_cast<std::size_t>(epochs);
+        cfg.n_interior = static_cast<std::size_t>(n_int);
+        cfg.n_initial = static_cast<std::size_t>(n_ic);
+        cfg.n_periodic = static_cast<std::size_t>(n_bc);
+        cfg.seed = seed;
+        cfg.eval_interval = 0;
+        training::SolveResult r = training::fine_tune(mu_of(mu), p, h, cfg, par_of(threads, 64), nullptr);
+        copy_solve(r, out_s, out_best_loss, out_best_epoch, out_losses, out_n_records, out_flags);
+    });
+}
+
+int ref_fast_solve(int L, const int64_t* ranks, const int64_t* red, int64_t m_in, int64_t m_out,
+                   const double* fparams, const double* s_init, const double* mu, const double* xpts, int64_t n_x,
+                   double lambda_local, double lr, int64_t epochs, int threads, double* out_s,
+                   double* out_best_loss, int64_t* out_best_epoch, double* out_losses, int64_t* out_n_records,
+                   int* out_flags) {
+    return guarded([&] {
+        FastParams f = unpack_fast(L, ranks, red, m_in, m_out, fparams);
+        HyperParams h = constant_hyper(f.ranks, s_init);
+        reduction::SamplingSetX X;
+        for (int64_t i = 0; i < n_x; ++i) X.points.push_back({xpts[2 * i], xpts[2 * i + 1]});
+        training::PhaseConfig cfg;
+        cfg.lr = lr;
+        cfg.epochs = static_cast<std::size_t>(epochs);
+        training::SolveResult r = training::fast_solve(mu_of(mu), h, f, X, cfg, lambda_local, par_of(threads, 64));
+        copy_solve(r, out_s, out_best_loss, out_best_epoch, out_losses, out_n_records, out_flags);
+    });
+}
+
 // ---- FastLRNR construction (reduction.cpp:10-31,111-283) ----
 // Constant hypernetwork (zero W, bias = s) so hyper_forward(mu) == s.
 int ref_build_fast(int L, const int64_t* widths, const int64_t* ranks, const double* params,

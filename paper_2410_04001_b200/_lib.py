@@ -16,7 +16,8 @@ EXPORTS = (
     "lrnr_gpu_create", "lrnr_gpu_destroy", "lrnr_gpu_last_error", "lrnr_gpu_last_layer_tag",
     "lrnr_gpu_set_stream", "lrnr_gpu_set_option", "lrnr_gpu_launch_count", "lrnr_gpu_set_lrnr", "lrnr_gpu_set_fast",
     "lrnr_gpu_set_hyper", "lrnr_gpu_set_points", "lrnr_gpu_set_points_device", "lrnr_gpu_loss_grad_s",
-    "lrnr_gpu_set_boundary", "lrnr_gpu_terms_grad", "lrnr_gpu_meta_terms_grad",
+    "lrnr_gpu_set_boundary", "lrnr_gpu_terms_grad", "lrnr_gpu_meta_terms_grad", "lrnr_gpu_fine_tune",
+    "lrnr_gpu_fast_solve", "lrnr_host_epoch_seed", "lrnr_host_sample_batch",
     "lrnr_gpu_loss_grad_s_multi", "lrnr_gpu_hyper_loss_grad", "lrnr_gpu_meta_loss_grad", "lrnr_gpu_jets",
     "lrnr_gpu_loss", "lrnr_gpu_upload_coeffs", "lrnr_gpu_run", "lrnr_gpu_check", "lrnr_gpu_download",
     "lrnr_gpu_fma_peak",
@@ -63,6 +64,11 @@ def load() -> C.CDLL:
     lib.lrnr_gpu_set_boundary.argtypes = [vp, dp, i64, dp, i64]
     lib.lrnr_gpu_terms_grad.argtypes = [vp, ip, dp, dp, ip, C.c_double, C.c_double, C.c_double, dp, C.c_double,
                                         dp, dp, dp]
+    lib.lrnr_gpu_fine_tune.argtypes = [vp, dp, dp, C.c_double, i64, i64, i64, i64, C.c_uint64, dp, dp, dp, dp, dp, dp]
+    lib.lrnr_gpu_fast_solve.argtypes = [vp, dp, dp, dp, i64, C.c_double, C.c_double, i64, dp, dp, dp, dp, dp, dp]
+    lib.lrnr_host_epoch_seed.argtypes = [C.c_uint64, i64]
+    lib.lrnr_host_epoch_seed.restype = C.c_uint64
+    lib.lrnr_host_sample_batch.argtypes = [C.c_uint64, i64, i64, i64, dp, dp, dp]
     lib.lrnr_gpu_loss_grad_s_multi.argtypes = [vp, ip, dp, dp, C.c_double, dp, dp]
     lib.lrnr_gpu_hyper_loss_grad.argtypes = [vp, ip, dp, C.c_double, dp, dp, dp]
     lib.lrnr_gpu_meta_loss_grad.argtypes = [vp, dp, C.c_double, dp, dp]

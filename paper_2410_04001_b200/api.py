@@ -316,6 +316,25 @@ class GpuContext:
                                                    _p(comps), C.byref(ro), _p(g)), "meta_terms_grad")
         return dict(value=v.value, comps=comps, ortho=ro.value, grad=g)
 
+    def fine_tune(self, s_init, mu, lr=1e-2, epochs=400, n_int=1024, n_ic=256, n_bc=256, seed=1234):
+        """fine_tune (training.cpp:428-496) on the device for the bound LRNR."""
+        return self._solve(self.lib.lrnr_gpu_fine_tune, self.r_total[MODEL_LRNR], epochs, _p(_f64(s_init)),
+                           _p(_f64(mu)), C.c_double(lr), epochs, n_int, n_ic, n_bc, C.c_uint64(seed))
+
+    def fast_solve(self, s_init, mu, X, lambda_local=1e-2, lr=1e-2, epochs=400):
+        """fast_solve (training.cpp:498-607) on the device for the bound FastLRNR (one CUDA graph per epoch)."""
+        X = _f64(X).reshape(-1, 2)
+        return self._solve(self.lib.lrnr_gpu_fast_solve, self.r_total[MODEL_FAST], epochs, _p(_f64(s_init)),
+                           _p(_f64(mu)), _p(X), X.shape[0], C.c_double(lambda_local), C.c_double(lr), epochs)
+
+    def _solve(self, fn, G, epochs, *args):
+        s = np.zeros(G)
+        losses = np.zeros(max(1, epochs))
+        bl, be, nr, fl = C.c_double(0.0), C.c_int64(0), C.c_int64(0), C.c_int(0)
+        self._rc(fn(self.h, *args, _p(s), C.byref(bl), C.byref(be), _p(losses), C.byref(nr), C.byref(fl)), "solve")
+        return dict(s=s, best_loss=bl.value, best_epoch=be.value, losses=losses[:nr.value], aborted=bool(fl.value & 1),
+                    diverged=bool(fl.value & 2))
+
     def jets(self, model, s):
         out = np.zeros((self.n_points, 4))
         self._rc(self.lib.lrnr_gpu_jets(self.h, model, _p(_f64(s)), _p(out)), "jets")

@@ -161,6 +161,9 @@ struct lrnr_gpu_ctx {
     // boundary points (lrnr_gpu_set_boundary): [initial (x, 0)] [periodic (0, t), (2pi, t)] pairs
     lrnr_b200::detail::DevBuf bnd_pts, bnd_x, bnd_spec, bnd_jets;
     int64_t n_ic = 0, n_bc = 0;
+    // solve loops (lrnr_gpu_fine_tune / lrnr_gpu_fast_solve)
+    lrnr_b200::detail::DevBuf solve_rows, solve_state, solve_m, solve_v, solve_best, solve_s0, solve_bt, solve_losses,
+        solve_pts[2], solve_bnd[2], solve_sinx[2];
     int device = 0;
     int num_sms = 148;
     cudaStream_t own = nullptr;

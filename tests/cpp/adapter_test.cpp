@@ -177,6 +177,42 @@ int main() {
     const double egp = floor_rel(got_phase.grad, ref_phase.grad);
     std::printf("fast-phase objective: value %.3e, dL/ds %.3e\n", evp, egp);
 
+    // the solve loops: the reference's own training::fine_tune / fast_solve vs the device loops
+    HyperParams hc;  // constant hypernetwork: hyper_forward(mu) == s
+    hc.w.emplace_back(23, 3);
+    hc.b.push_back(hb);
+    hc.split = p.ranks;
+    hc.box = ParamDomain::d1();
+    training::PhaseConfig cfg;
+    cfg.epochs = 30;
+    cfg.n_interior = 256;
+    cfg.n_initial = 64;
+    cfg.n_periodic = 64;
+    cfg.eval_interval = 0;
+    training::SolveResult rft = training::fine_tune(mu, p, hc, cfg, par, nullptr);
+    eng.bind(p, LRNR_F64);
+    training::SolveResult gft = eng.fine_tune(mu, hc, cfg);
+    double eft = 0.0;
+    bool sft = rft.report.records.size() == gft.report.records.size() && rft.report.best_epoch == gft.report.best_epoch;
+    for (std::size_t e = 0; sft && e < rft.report.records.size(); ++e)
+        eft = std::max(eft, std::fabs(gft.report.records[e].loss - rft.report.records[e].loss) / rft.report.records[e].loss);
+    std::printf("fine_tune loop (30 epochs): losses max rel err %.3e, best epoch %zu / %zu\n", eft,
+                gft.report.best_epoch, rft.report.best_epoch);
+    training::PhaseConfig fcfg;
+    fcfg.epochs = 200;
+    training::SolveResult rfs = training::fast_solve(mu, hc, f, X, fcfg, 1e-2, par);
+    training::SolveResult gfs = eng.fast_solve(mu, hc, X, fcfg, 1e-2);
+    double efs = 0.0;
+    bool sfs = rfs.report.records.size() == gfs.report.records.size() && rfs.report.best_epoch == gfs.report.best_epoch &&
+               rfs.report.diverged == gfs.report.diverged;
+    for (std::size_t e = 0; sfs && e < rfs.report.records.size(); ++e)
+        efs = std::max(efs, std::fabs(gfs.report.records[e].loss - rfs.report.records[e].loss) / rfs.report.records[e].loss);
+    double efs_s = 0.0;
+    for (std::size_t l = 0; l < rfs.coeffs.s.size(); ++l)
+        for (std::size_t i = 0; i < rfs.coeffs.s[l].len(); ++i)
+            efs_s = std::max(efs_s, std::fabs(gfs.coeffs.s[l][i] - rfs.coeffs.s[l][i]));
+    std::printf("fast_solve loop (200 epochs): losses max rel err %.3e, best s max abs err %.3e\n", efs, efs_s);
+
     // NonFiniteError surfaces as the reference's exception type
     Coefficients bad = s;
     bad.s[1][0] = std::nan("");
@@ -188,7 +224,8 @@ int main() {
     }
     std::printf("NonFiniteError mapped: %s\n", threw ? "yes" : "NO");
     const bool ok = ev <= 1e-12 && eg <= 1e-10 && evf <= 1e-12 && egf <= 1e-10 && evb <= 1e-12 && ecb <= 1e-12 &&
-                    egb <= 1e-10 && evp <= 1e-12 && egp <= 1e-10 && threw;
+                    egb <= 1e-10 && evp <= 1e-12 && egp <= 1e-10 && sft && eft <= 1e-10 && sfs && efs <= 1e-10 &&
+                    efs_s <= 1e-10 && threw;
     std::printf("%s\n", ok ? "ADAPTER PARITY OK" : "ADAPTER PARITY FAILED");
     return ok ? 0 : 1;
 }

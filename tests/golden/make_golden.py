@@ -75,6 +75,15 @@ def main():
     fp = R.fast_phase_grad(r0, f1["red_ranks"], f1["fparams"], s_pert, s_init, mu0, xs, 1e-2, threads=2)
     g.update(c1_phase_x=np.array(xs), c1_phase_s=s_pert, c1_phase_value=np.array([fp["value"]]),
              c1_phase_comps=fp["comps"], c1_phase_grad_s=fp["grad_s"])
+    # the reference's own solve loops (training.cpp:428-607) from s_init = s0
+    ft = R.fine_tune(w0, r0, P0, s0, mu0, 1e-2, 40, 256, 64, 64, 1234, threads=4)
+    g.update(c0_ft_cfg=np.array([1e-2, 40, 256, 64, 64, 1234]), c0_ft_s=ft["s"], c0_ft_losses=ft["losses"],
+             c0_ft_best=np.array([ft["best_loss"], ft["best_epoch"]]))
+    for tag, lr in (("a", 1e-2), ("b", 5e-2)):  # well-conditioned: the l1 sign terms make large lr chaotic
+        fs = R.fast_solve(r0, f1["red_ranks"], f1["fparams"], s0, mu0, xs, 1e-2, lr, 200, threads=2)
+        g.update({f"c1_fs{tag}_cfg": np.array([1e-2, lr, 200]), f"c1_fs{tag}_s": fs["s"],
+                  f"c1_fs{tag}_losses": fs["losses"], f"c1_fs{tag}_best": np.array([fs["best_loss"], fs["best_epoch"]])})
+
     # identity reduction (reduction.cpp:285-296)
     red_id, F_id = R.identity_fast(w0, r0, P0)
     g.update(c0_identity_red=red_id, c0_identity_fparams=F_id)

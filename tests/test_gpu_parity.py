@@ -550,3 +550,48 @@ def test_boundary_nonfinite_maps_to_nonfinite_error(gpu, golden):
     finally:
         gpu.set_boundary()
     assert ei.value.layer_tag == -1
+
+
+# ----------------------------------------------------------------------------
+# solve loops on the device: fine_tune, fast_solve (CUDA graph)
+# ----------------------------------------------------------------------------
+def test_fine_tune_fp64_matches_reference(gpu, golden):
+    g = golden
+    lr, ep, ni, nc, nb, seed = g["c0_ft_cfg"]
+    gpu.set_lrnr(lrnr_from_golden(g, "c0"), pkg.F64)
+    r = gpu.fine_tune(g["c0_s"], g["c0_mu"], lr, int(ep), int(ni), int(nc), int(nb), int(seed))
+    np.testing.assert_allclose(r["losses"], g["c0_ft_losses"], rtol=1e-10, atol=0)
+    np.testing.assert_allclose(r["s"], g["c0_ft_s"], rtol=0, atol=1e-10)
+    assert r["best_epoch"] == g["c0_ft_best"][1] and not r["aborted"]
+
+
+@pytest.mark.parametrize("tag", ["a", "b"])
+def test_fast_solve_fp64_matches_reference(gpu, golden, tag):
+    g = golden
+    lam, lr, ep = g[f"c1_fs{tag}_cfg"]
+    gpu.set_fast(pkg.FastParams(g["c0_ranks"], g["c1_red_ranks"], g["c1_fparams"], pkg.ACT_TANH), pkg.F64)
+    r = gpu.fast_solve(g["c0_s"], g["c0_mu"], g["c1_phase_x"], lam, lr, int(ep))
+    np.testing.assert_allclose(r["losses"], g[f"c1_fs{tag}_losses"], rtol=1e-10, atol=0)
+    np.testing.assert_allclose(r["s"], g[f"c1_fs{tag}_s"], rtol=0, atol=1e-10)
+    assert r["best_epoch"] == g[f"c1_fs{tag}_best"][1] and not r["diverged"]
+
+
+def test_fast_solve_nonfinite_start_aborts(gpu, golden):
+    g = golden
+    gpu.set_fast(pkg.FastParams(g["c0_ranks"], g["c1_red_ranks"], g["c1_fparams"], pkg.ACT_TANH), pkg.F64)
+    s = g["c0_s"].copy()
+    s[2] = np.nan
+    r = gpu.fast_solve(s, g["c0_mu"], g["c1_phase_x"], 1e-2, 1e-2, 5)
+    assert r["aborted"] and r["diverged"] and len(r["losses"]) == 0 and r["best_epoch"] == 0
+
+
+def test_fine_tune_fp32_c2_shape_tracks_oracle(gpu, oracle):
+    """FP32 sin c2 shape: the device loop (tensor-core interior kernel) tracks the FP64 oracle loop."""
+    c = pkg.config2(n_points=0, act=pkg.ACT_SIN, with_fast=False)
+    m = c["model"]
+    gpu.set_lrnr(m, pkg.F32)
+    r = gpu.fine_tune(c["s"], c["mu"], 1e-2, 8, 512, 128, 128, 99)
+    want = oracle.fine_tune(m.widths, m.ranks, m.params, c["s"], c["mu"], 1e-2, 8, 512, 128, 128, 99,
+                            act=pkg.ACT_SIN)
+    np.testing.assert_allclose(r["losses"], want["losses"], rtol=1e-3, atol=0)
+    assert normwise(r["s"], want["s"]) <= 1e-4
