@@ -86,8 +86,11 @@ int lrnr_gpu_set_stream(lrnr_gpu_ctx* ctx, void* cuda_stream);
  * 0 = auto (default): FP32 LRNR with ranks <= 32 on the tcgen05 tensor-core
  * tile kernel (3xTF32), other FP32/FP64 shapes with ranks <= 64 on the FMA
  * tile-GEMM kernel, the rest on the per-point streaming kernel;
+ * batches below ~16 points per SM on the small-batch latency kernel (one CTA
+ * per point, threads across neurons / ranks);
  * 1 = force the streaming kernel, 2 = tensor-core kernel wherever it applies
- * (also FastLRNR), 3 = FMA tile kernel (no tensor cores). */
+ * (also FastLRNR), 3 = FMA tile kernel (no tensor cores), 4 = small-batch
+ * kernel at any size. */
 #define LRNR_OPT_FAST_SINCOS 1
 #define LRNR_OPT_KERNEL 2
 #define LRNR_OPT_TILE_P 3   /* FP32 wide-layer tile: 64 points x 512 threads (default) or 32 x 256 (2 CTAs/SM) */

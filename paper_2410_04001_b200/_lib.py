@@ -31,7 +31,7 @@ F64, F32 = 0, 1
 MODEL_LRNR, MODEL_FAST = 0, 1
 OPT_FAST_SINCOS, OPT_KERNEL, OPT_TILE_P = 1, 2, 3
 # LRNR_OPT_KERNEL values
-KERNEL_AUTO, KERNEL_STREAM, KERNEL_TC, KERNEL_FMA_TILE = 0, 1, 2, 3
+KERNEL_AUTO, KERNEL_STREAM, KERNEL_TC, KERNEL_FMA_TILE, KERNEL_SMALL = 0, 1, 2, 3, 4
 # lrnr_gpu_terms_grad objectives
 OBJ_SQUARED, OBJ_ABS = 0, 1
 

@@ -47,6 +47,19 @@
     template void lrnr_b200::detail::launch_v2<T, 32, 1, 8, RP, ACT, false, true>(                         \
         lrnr_gpu_ctx*, const lrnr_b200::detail::Model&, const double*, const double*, double, double*, double*);
 
+
+
+// small-batch latency kernel: (T, ACT, MODE)
+#define LRNR_SMALL(X) \
+    X(float, 0, 0) X(float, 1, 0) X(float, 0, 1) X(float, 1, 1) \
+    X(double, 0, 0) X(double, 1, 0) X(double, 0, 1) X(double, 1, 1)
+#define LRNR_SMALL_EXTERN(T, ACT, MODE)                                                                   \
+    extern template void lrnr_b200::detail::launch_small<T, ACT, MODE>(                                    \
+        lrnr_gpu_ctx*, const lrnr_b200::detail::Model&, const double*, const double*, double, double*, double*);
+#define LRNR_SMALL_INST(T, ACT, MODE)                                                                     \
+    template void lrnr_b200::detail::launch_small<T, ACT, MODE>(                                           \
+        lrnr_gpu_ctx*, const lrnr_b200::detail::Model&, const double*, const double*, double, double*, double*);
+
 #ifndef LRNR_INSTANTIATING
 LRNR_V1_F64(LRNR_V1_EXTERN)
 LRNR_V1_F32(LRNR_V1_EXTERN)
@@ -54,4 +67,5 @@ LRNR_TILE_F32(LRNR_TILE_EXTERN)
 LRNR_TILE_F32R64(LRNR_TILE_EXTERN)
 LRNR_TILE_F64(LRNR_TILE_EXTERN)
 LRNR_META(LRNR_META_EXTERN)
+LRNR_SMALL(LRNR_SMALL_EXTERN)
 #endif

@@ -15,6 +15,7 @@
 #include "lrnr_gpu.h"
 #include "pinn_kernels.cuh"
 #include "pinn_v2.cuh"
+#include "pinn_small.cuh"
 
 namespace lrnr_b200 {
 namespace detail {
@@ -238,6 +239,36 @@ void launch_pinn(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const d
     CK(cudaGetLastError());
     dim3 rg((R1 + 127) / 128, static_cast<unsigned>(n_inst));
     reduce_units_kernel<T><<<rg, 128, 0, ctx->stream>>>(ctx->part.as<T>(), p.g.units_per_inst, R1, n_inst, dev_out);
+    CK(cudaGetLastError());
+    ctx->launches += 2;
+}
+
+// ---- small-batch latency kernel (pinn_small.cuh): one CTA per point ----
+small::Geom small_geom(const Model& m, int64_t n_inst, int64_t n_per);
+size_t small_smem_bytes(const Model& m, size_t elem);
+
+template <class T, int ACT, int MODE>
+void launch_small(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
+                  double* dev_out, double* jets_dev) {
+    const int64_t n_inst = ctx->n_inst, n_per = ctx->n_per;
+    small::Geom g = small_geom(m, n_inst, n_per);
+    const size_t smem = small_smem_bytes(m, sizeof(T));
+    auto kern = small::pinn_small_kernel<T, ACT, MODE>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, small::NT, smem));
+    occ = std::max(occ, 1);
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g.n_total, int64_t(ctx->num_sms) * occ)));
+    const int R1 = 1 + m.rtotal;
+    ctx->part.ensure(static_cast<size_t>(g.n_total) * R1 * sizeof(T));
+    DevNet<T> net = dev_net<T>(m);
+    kern<<<grid, small::NT, smem, ctx->stream>>>(net, g, ctx->pts, s_dev, mu_dev, static_cast<T>(w), ctx->part.as<T>(),
+                                                 jets_dev, ctx->bad.as<unsigned long long>(), ctx->term_spec,
+                                                 ctx->term_objective);
+    CK(cudaGetLastError());
+    dim3 rg((R1 + 127) / 128, static_cast<unsigned>(n_inst));
+    reduce_units_kernel<T><<<rg, 128, 0, ctx->stream>>>(ctx->part.as<T>(), static_cast<int>(n_per), R1, n_inst,
+                                                        dev_out);
     CK(cudaGetLastError());
     ctx->launches += 2;
 }

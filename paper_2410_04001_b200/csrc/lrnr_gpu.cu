@@ -49,6 +49,34 @@ void build_layout(Model& m) {
     m.packed.assign(o, 0.0);
 }
 
+small::Geom small_geom(const Model& m, int64_t n_inst, int64_t n_per) {
+    small::Geom g{};
+    g.n_total = n_inst * n_per;
+    g.n_per = std::max<int64_t>(1, n_per);
+    int a = 0, mm = 1;
+    for (int l = 0; l + 1 < m.L; ++l) {
+        g.aoff[l] = a;
+        a += m.M[l + 1];
+        mm = std::max(mm, m.M[l + 1]);
+    }
+    g.a_len = a;
+    g.mmax = mm;
+    g.rmax = m.rmax;
+    int blk = 0;
+    for (int l = 0; l + 1 < m.L; ++l) blk = std::max(blk, m.M[l + 1] * m.trow[l]);
+    g.blk = (blk + 7) & ~7;
+    const size_t elem = m.dtype == LRNR_F64 ? 8 : 4;
+    const size_t base = static_cast<size_t>(small::smem_elems(m.rtotal, g.a_len, g.mmax, g.rmax)) * elem;
+    g.stage = base + 2 * static_cast<size_t>(g.blk) * elem <= 200 * 1024 ? 1 : 0;
+    return g;
+}
+
+size_t small_smem_bytes(const Model& m, size_t elem) {
+    const small::Geom g = small_geom(m, 1, 1);
+    return static_cast<size_t>(small::smem_elems(m.rtotal, g.a_len, g.mmax, g.rmax)) * elem +
+           (g.stage ? 2 * static_cast<size_t>(g.blk) * elem : 0);
+}
+
 void release_model(Model& m) {
     m.dev.release();
     m.v2.dblocks.release();
@@ -454,9 +482,34 @@ bool dispatch_v2(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const d
 }
 
 // dispatch over (dtype, act, rmax, mode)
+// The small-batch latency kernel: LRNR_OPT_KERNEL 4 forces it; auto (0) takes
+// it for batches below one wave of the tile kernels.
+bool use_small(const lrnr_gpu_ctx* ctx, const Model& m) {
+    const size_t smem = small_smem_bytes(m, m.dtype == LRNR_F64 ? 8 : 4);
+    if (smem > 220 * 1024 || m.rmax > 1024) return false;
+    if (ctx->opt_kernel == 4) return true;
+    return ctx->opt_kernel == 0 && ctx->n_inst * ctx->n_per <= static_cast<int64_t>(ctx->num_sms) * 16;
+}
+
+template <int MODE>
+void dispatch_small(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
+                    double* dev_out, double* jets_dev) {
+    if (m.dtype == LRNR_F64) {
+        if (m.act == LRNR_ACT_TANH) launch_small<double, 0, MODE>(ctx, m, s_dev, mu_dev, w, dev_out, jets_dev);
+        else launch_small<double, 1, MODE>(ctx, m, s_dev, mu_dev, w, dev_out, jets_dev);
+    } else {
+        if (m.act == LRNR_ACT_TANH) launch_small<float, 0, MODE>(ctx, m, s_dev, mu_dev, w, dev_out, jets_dev);
+        else launch_small<float, 1, MODE>(ctx, m, s_dev, mu_dev, w, dev_out, jets_dev);
+    }
+}
+
 template <int MODE>
 void dispatch_pinn(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
                    double* dev_out, double* jets_dev) {
+    if (use_small(ctx, m)) {
+        dispatch_small<MODE>(ctx, m, s_dev, mu_dev, w, dev_out, jets_dev);
+        return;
+    }
     const int rm = m.rmax;
 #define LRNR_CASE(T, TPP, RM, ACT)                                                               \
     if (rm <= RM) {                                                                              \
@@ -668,6 +721,10 @@ double* run_resident(lrnr_gpu_ctx* ctx, const Model& m, double w, double* dev_ou
         return dev_out;
     }
     const double wt = w > 0.0 ? w : 1.0 / static_cast<double>(ctx->n_inst * ctx->n_per);
+    if (MODE == 0 && use_small(ctx, m)) {
+        dispatch_small<0>(ctx, m, ctx->s_dev.as<double>(), ctx->mu_dev.as<double>(), wt, dev_out, nullptr);
+        return dev_out;
+    }
     if (MODE == 0 && dispatch_tc(ctx, m, ctx->s_dev.as<double>(), ctx->mu_dev.as<double>(), wt, dev_out))
         return dev_out;
     if (MODE == 0 && dispatch_v2(ctx, m, ctx->s_dev.as<double>(), ctx->mu_dev.as<double>(), wt, dev_out))
@@ -1032,7 +1089,8 @@ void solve_epoch(lrnr_gpu_ctx* ctx, const Model& m, const SolveRun& r) {
     if (r.n_int > 0) {
         PointSwap keep(ctx, r.int_pts, r.n_int);
         if (r.objective == LRNR_OBJ_SQUARED) {
-            if (!dispatch_tc(ctx, m, sd, md, r.w_int, rows_int) && !dispatch_v2(ctx, m, sd, md, r.w_int, rows_int))
+            if (use_small(ctx, m)) dispatch_small<0>(ctx, m, sd, md, r.w_int, rows_int, nullptr);
+            else if (!dispatch_tc(ctx, m, sd, md, r.w_int, rows_int) && !dispatch_v2(ctx, m, sd, md, r.w_int, rows_int))
                 dispatch_pinn<0>(ctx, m, sd, md, r.w_int, rows_int, nullptr);
         } else {
             ctx->term_objective = 1;

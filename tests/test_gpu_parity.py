@@ -21,7 +21,7 @@ TOL32_LOSS = 1e-4
 
 # FP32 kernel choices (LRNR_OPT_KERNEL): auto = tcgen05 for the LRNR + FMA tile
 # for FastLRNR; forced tcgen05 (FastLRNR too); FMA tile; per-point streaming
-FP32_KERNELS = [pkg.KERNEL_AUTO, pkg.KERNEL_TC, pkg.KERNEL_FMA_TILE, pkg.KERNEL_STREAM]
+FP32_KERNELS = [pkg.KERNEL_AUTO, pkg.KERNEL_TC, pkg.KERNEL_FMA_TILE, pkg.KERNEL_STREAM, pkg.KERNEL_SMALL]
 
 
 @pytest.fixture
@@ -43,7 +43,9 @@ def lrnr_from_golden(g, prefix, act=pkg.ACT_TANH):
 # ----------------------------------------------------------------------------
 # config 0 / 1 (FP64) against the reference's own outputs
 # ----------------------------------------------------------------------------
-def test_c0_lrnr_fp64_matches_reference(gpu, golden):
+@pytest.mark.parametrize("kernel", [pkg.KERNEL_AUTO, pkg.KERNEL_SMALL, pkg.KERNEL_STREAM])
+def test_c0_lrnr_fp64_matches_reference(gpu, golden, opts, kernel):
+    opts(kernel)
     m = lrnr_from_golden(golden, "c0")
     gpu.set_lrnr(m, pkg.F64)
     gpu.set_points(golden["c0_pts"])
@@ -53,7 +55,9 @@ def test_c0_lrnr_fp64_matches_reference(gpu, golden):
     np.testing.assert_allclose(r["comps"], golden["c0_comps"], rtol=1e-12, atol=0)
 
 
-def test_c1_fast_fp64_matches_reference(gpu, golden):
+@pytest.mark.parametrize("kernel", [pkg.KERNEL_AUTO, pkg.KERNEL_SMALL, pkg.KERNEL_STREAM])
+def test_c1_fast_fp64_matches_reference(gpu, golden, opts, kernel):
+    opts(kernel)
     f = pkg.FastParams(golden["c0_ranks"], golden["c1_red_ranks"], golden["c1_fparams"], pkg.ACT_TANH)
     gpu.set_fast(f, pkg.F64)
     gpu.set_points(golden["c0_pts"])
@@ -65,7 +69,9 @@ def test_c1_fast_fp64_matches_reference(gpu, golden):
     assert 0.0 < rel < 1.0
 
 
-def test_c0_jets_match_reference(gpu, golden):
+@pytest.mark.parametrize("kernel", [pkg.KERNEL_AUTO, pkg.KERNEL_STREAM])
+def test_c0_jets_match_reference(gpu, golden, opts, kernel):
+    opts(kernel)
     m = lrnr_from_golden(golden, "c0")
     gpu.set_lrnr(m, pkg.F64)
     gpu.set_points(golden["c0_pts"][:256])
@@ -249,7 +255,7 @@ def test_bitwise_deterministic(gpu, golden):
     assert a["value"] == b["value"] and np.array_equal(a["grad_s"], b["grad_s"])
 
 
-@pytest.mark.parametrize("kernel", [pkg.KERNEL_TC, pkg.KERNEL_FMA_TILE])
+@pytest.mark.parametrize("kernel", [pkg.KERNEL_TC, pkg.KERNEL_FMA_TILE, pkg.KERNEL_SMALL])
 @pytest.mark.parametrize("n", [1, 127, 129, 1000])
 def test_c2_fp32_ragged_tiles_match_oracle(gpu, oracle, opts, kernel, n):
     """Partial point tiles (128-point TMEM tiles / 64-point FMA tiles) on the FP32 kernels."""
@@ -264,7 +270,7 @@ def test_c2_fp32_ragged_tiles_match_oracle(gpu, oracle, opts, kernel, n):
     assert normwise(got["grad_s"], want["grad_s"]) <= TOL32_NORM
 
 
-@pytest.mark.parametrize("kernel", [pkg.KERNEL_TC, pkg.KERNEL_FMA_TILE])
+@pytest.mark.parametrize("kernel", [pkg.KERNEL_TC, pkg.KERNEL_FMA_TILE, pkg.KERNEL_SMALL])
 def test_c2_fp32_multi_instance_matches_oracle(gpu, oracle, opts, kernel):
     """Several PDE instances (own s, mu, ragged point counts padded per instance)."""
     opts(kernel)
