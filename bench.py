@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--points", type=int, default=0, help="points per GPU (default: the config's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-solves", action="store_true", help="skip the fine_tune / fast_solve loop timings")
     ap.add_argument("--kernel", type=int, default=0,
                     help="LRNR_OPT_KERNEL: 0 auto (tcgen05 LRNR, FMA tile FastLRNR), 1 streaming, 2 tcgen05, 3 FMA tile")
     ap.add_argument("--fast-sincos", type=int, default=0, help="LRNR_OPT_FAST_SINCOS (SFU sin/cos)")
@@ -193,6 +194,51 @@ def cpu_baseline_sample(pkg, wl, seconds=10.0):
     return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": kind,
             "sample": f"first {n} of the {wl['n']} points, LRNR+FastLRNR residual+dL/ds, FP64"
                       + (", tanh (reference is tanh-only; identical shapes and FLOPs)" if use_ref else "")}, run
+
+
+def solve_loops(pkg, local, with_reference):
+    """The solve loops the model is trained / deployed with (training.cpp:428-607), on
+    BASELINE c2 shapes with tanh (the reference's activation): fast_solve of the FastLRNR
+    (12-point X grid, lambda 1e-2, 400 epochs) and fine_tune of the LRNR (1024 + 256 + 256
+    points re-sampled per epoch, 100 epochs), device ms/epoch; the reference's own loops
+    on the host cores beside them (bounded samples)."""
+    c = pkg.config2(n_points=0, act=pkg.ACT_TANH)
+    m, f = c["model"], c["fast"]
+    X = np.array([(2 * np.pi * i / 3.0, j / 2.0) for j in range(3) for i in range(4)])
+    ctx = pkg.GpuContext(local)
+    ctx.set_lrnr(m, pkg.F32)
+    ctx.set_fast(f, pkg.F32)
+    ctx.fast_solve(c["s"], c["mu"], X, 1e-2, 1e-2, 4)
+    t0 = time.perf_counter()
+    fs = ctx.fast_solve(c["s"], c["mu"], X, 1e-2, 1e-2, 400)
+    t_fs = (time.perf_counter() - t0) / 400
+    ctx.fine_tune(c["s"], c["mu"], 1e-2, 2)
+    t0 = time.perf_counter()
+    ft = ctx.fine_tune(c["s"], c["mu"], 1e-2, 100)
+    t_ft = (time.perf_counter() - t0) / 100
+    launches = ctx.launches
+    ctx.close()
+    out = {"fast_solve": {"ms_per_epoch": t_fs * 1e3, "epochs": 400, "best_loss": fs["best_loss"], "dtype": "f32",
+                          "workload": "c2 FastLRNR (tanh), 12-point X (4x3 grid), lambda_local 1e-2, lr 1e-2",
+                          "path": "lrnr_gpu_fast_solve (one CUDA graph per epoch)"},
+           "fine_tune": {"ms_per_epoch": t_ft * 1e3, "epochs": 100, "best_loss": ft["best_loss"], "dtype": "f32",
+                         "workload": "c2 LRNR (tanh), 1024 + 256 + 256 points re-sampled per epoch, lr 1e-2",
+                         "path": "lrnr_gpu_fine_tune"},
+           "gpu_launches": launches}
+    if with_reference:
+        from oracle.oracle import Reference, reference_available
+        if reference_available():
+            R = Reference()
+            th = os.cpu_count() or 1
+            t0 = time.perf_counter()
+            R.fast_solve(f.ranks, f.red_ranks, f.fparams, c["s"], c["mu"], X, 1e-2, 1e-2, 400, threads=th)
+            out["fast_solve"]["reference_ms_per_epoch"] = (time.perf_counter() - t0) / 400 * 1e3
+            t0 = time.perf_counter()
+            R.fine_tune(m.widths, m.ranks, m.params, c["s"], c["mu"], 1e-2, 5, 1024, 256, 256, 1234, threads=th)
+            out["fine_tune"]["reference_ms_per_epoch"] = (time.perf_counter() - t0) / 5 * 1e3
+            out["reference_cores"] = th
+            out["reference_note"] = "unmodified reference training::fast_solve / fine_tune, FP64, all host threads"
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -376,6 +422,13 @@ def run_ours(args):
         except Exception as e:  # reported, never fatal
             cpu = {"value": None, "error": str(e)}
 
+    solves = None
+    if rank == 0 and not args.no_solves:
+        try:
+            solves = solve_loops(pkg, local, world == 1 and not args.no_cpu_baseline)
+        except Exception as e:  # reported, never fatal
+            solves = {"error": str(e)}
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -385,7 +438,7 @@ def run_ours(args):
                            "l2": "flushed between timed steps (256 MiB write outside the step events)",
                            "kernel_option": args.kernel, "fast_sincos": args.fast_sincos},
                 "roofline": roofline, "kernels": per_kernel, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clk.summary()}
+                "gpu_launches": launches, "clocks": clk.summary(), "solve_loops": solves}
         print(json.dumps(line))
     ctx.close()
     if dist is not None:

@@ -186,6 +186,39 @@ int lrnr_gpu_fast_solve(lrnr_gpu_ctx* ctx, const double* s_init, const double* m
                         double lambda_local, double lr, int64_t epochs, double* out_s, double* out_best_loss,
                         int64_t* out_best_epoch, double* out_losses, int64_t* out_n_records, int* out_flags);
 
+/* ---- evaluation: l1_relative_error (pde.cpp:166-178) on the device ----
+ * u of `model` with coefficients s on the GridField grid x_i = 2 pi i / n_x,
+ * t_j = j / n_t (j = 0..n_t; t = 0 when n_t = 0), against ref_values
+ * ((n_t + 1) x n_x, row j = time): sum |u - ref| / sum |ref|. */
+int lrnr_gpu_l1_error(lrnr_gpu_ctx* ctx, int model, const double* s, const double* ref_values, int64_t n_x,
+                      int64_t n_t, double* out_l1);
+
+/* ---- checkpoint interop (proj/src/checkpoint.cpp) ----
+ * The reference's "LRNR" v1 file (named FP64 tensors + JSON meta), read and
+ * written by host C++ (no JSON library). Getters take NULL arrays to query the
+ * sizes first; flat layouts are those of lrnr_gpu_set_lrnr / _set_hyper /
+ * _set_fast. Files written here load with the reference's checkpoint_load and
+ * vice versa (tests/test_host.py). */
+typedef struct lrnr_ckpt lrnr_ckpt;
+const char* lrnr_ckpt_last_error(void);
+int lrnr_ckpt_create(lrnr_ckpt** out);
+int lrnr_ckpt_load(const char* path, lrnr_ckpt** out);
+int lrnr_ckpt_save(const lrnr_ckpt* c, const char* path);
+void lrnr_ckpt_free(lrnr_ckpt* c);
+int lrnr_ckpt_get_lrnr(const lrnr_ckpt* c, int* L, int64_t* widths, int64_t* ranks, int64_t* n_params, double* params);
+int lrnr_ckpt_put_lrnr(lrnr_ckpt* c, int L, const int64_t* widths, const int64_t* ranks, const double* params);
+int lrnr_ckpt_get_hyper(const lrnr_ckpt* c, int* K, int64_t* hw, int64_t* n_params, double* params, double* lo3,
+                        double* hi3);
+int lrnr_ckpt_put_hyper(lrnr_ckpt* c, int K, const int64_t* hw, const double* params, int L_split,
+                        const int64_t* split, const double* lo3, const double* hi3);
+int lrnr_ckpt_has_fast(const lrnr_ckpt* c);
+int lrnr_ckpt_get_fast(const lrnr_ckpt* c, int* L, int64_t* ranks, int64_t* red_ranks, int64_t* n_params,
+                       double* params);
+int lrnr_ckpt_put_fast(lrnr_ckpt* c, int L, const int64_t* ranks, const int64_t* red_ranks, int64_t m_in,
+                       int64_t m_out, const double* params);
+int lrnr_ckpt_get_sampling(const lrnr_ckpt* c, int64_t* n, double* xt);
+int lrnr_ckpt_put_sampling(lrnr_ckpt* c, int64_t n, const double* xt);
+
 /* Hypernetwork-coupled step (BASELINE config 3; the emit_hyper + emit_fast_jet
  * composition of autodiff.cpp:883-922): s_i = hyper(mu_i) on device, the model
  * gradient per instance, then the hypernetwork VJP summed over instances.

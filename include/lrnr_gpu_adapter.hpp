@@ -212,6 +212,15 @@ public:
         lb.total = lb.residual + lb.boundary;
         return lb;
     }
+    // pde::l1_relative_error (pde.cpp:166-178) of the bound LRNR (or FastLRNR)
+    // against a GridField, evaluated on the device.
+    double l1_relative_error(const Coefficients& s, const pde::GridField& ref, bool fast = false) {
+        const std::vector<double> sf = flatten(s);
+        double out = 0.0;
+        check(lrnr_gpu_l1_error(ctx_, fast ? LRNR_MODEL_FAST : LRNR_MODEL_LRNR, sf.data(), ref.values.data(),
+                                static_cast<int64_t>(ref.n_x), static_cast<int64_t>(ref.n_t), &out));
+        return out;
+    }
     std::vector<Jet> jet_forward(const std::vector<pde::Point>& pts, const Coefficients& s, bool fast = false) {
         set_points(pts, 1);
         const std::vector<double> sf = flatten(s);

@@ -446,6 +446,14 @@ class Reference:
         return dict(s=s, best_loss=bl.value, best_epoch=be.value, losses=losses[:nr.value], aborted=bool(fl.value & 1),
                     diverged=bool(fl.value & 2))
 
+    def l1_error(self, widths, ranks, P, s, values, n_x, n_t):
+        wv, rv = _i64(widths), _i64(ranks)
+        out = C.c_double(0.0)
+        self._rc(self.lib.ref_l1_error(C.c_int(len(rv)), _ptr(wv), _ptr(rv), _ptr(_f64(P)), _ptr(_f64(s)),
+                                       _ptr(_f64(values).reshape(-1)), C.c_int64(n_x), C.c_int64(n_t), C.byref(out)),
+                 "l1_error")
+        return out.value
+
     def lrnr_jets(self, widths, ranks, P, s, pts):
         wv, rv = _i64(widths), _i64(ranks)
         pts = _f64(pts).reshape(-1, 2)
@@ -559,3 +567,43 @@ class Reference:
                                          C.c_double(lambda_sparse), C.c_double(gamma), C.c_int(threads),
                                          C.c_int(chunk), C.byref(best), C.byref(be), _ptr(losses)), "meta_train")
         return best.value, be.value, losses
+
+
+REF_CKPT_SO = os.path.join(HERE, "_ref", "liblrnr_ref_ckpt.so")
+
+
+def reference_ckpt_available() -> bool:
+    return os.path.exists(REF_CKPT_SO)
+
+
+class ReferenceCheckpoint:
+    """The reference's own checkpoint writer / reader (oracle/ref_ckpt.cpp; build container only)."""
+
+    def __init__(self, path: str = REF_CKPT_SO):
+        self.lib = C.CDLL(path)
+        self.lib.ref_ckpt_error.restype = C.c_char_p
+
+    def _rc(self, rc, what):
+        if rc != 0:
+            raise OracleError(f"{what}: {self.lib.ref_ckpt_error().decode()}")
+
+    def write(self, path, widths, ranks, P, hw, H, lo, hi, X, fast=None):
+        wv, rv, hwv = _i64(widths), _i64(ranks), _i64(hw)
+        X = _f64(X).reshape(-1, 2)
+        if fast is not None:
+            fr, frh, F = _i64(fast[0]), _i64(fast[1]), _f64(fast[2])
+            Lf = len(fr)
+        else:
+            fr = frh = F = None
+            Lf = 0
+        self._rc(self.lib.ref_ckpt_write(str(path).encode(), C.c_int(len(rv)), _ptr(wv), _ptr(rv), _ptr(_f64(P)),
+                                         C.c_int(len(hwv) - 1), _ptr(hwv), _ptr(_f64(H)), _ptr(_f64(lo)),
+                                         _ptr(_f64(hi)), C.c_int(Lf), _ptr(fr), _ptr(frh), _ptr(F), _ptr(X),
+                                         C.c_int64(X.shape[0])), "ref_ckpt_write")
+
+    def read(self, path, n_lrnr, n_hyper):
+        P, H = np.zeros(n_lrnr + 1), np.zeros(n_hyper + 1)
+        npv, nhv = C.c_int64(0), C.c_int64(0)
+        self._rc(self.lib.ref_ckpt_read(str(path).encode(), _ptr(P), C.byref(npv), _ptr(H), C.byref(nhv)),
+                 "ref_ckpt_read")
+        return P[:npv.value], H[:nhv.value]

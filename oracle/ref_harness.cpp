@@ -698,6 +698,21 @@ int ref_fast_solve(int L, const int64_t* ranks, const int64_t* red, int64_t m_in
     });
 }
 
+// pde::l1_relative_error (pde.cpp:166-178) of lrnr_forward (model.cpp:255-270)
+// against a GridField ((n_t + 1) x n_x values).
+int ref_l1_error(int L, const int64_t* widths, const int64_t* ranks, const double* params, const double* s,
+                 const double* values, int64_t n_x, int64_t n_t, double* out) {
+    return guarded([&] {
+        LrnrParams p = unpack_lrnr(L, widths, ranks, params);
+        Coefficients c = unpack_s(p, s);
+        pde::GridField g;
+        g.n_x = static_cast<std::size_t>(n_x);
+        g.n_t = static_cast<std::size_t>(n_t);
+        g.values.assign(values, values + n_x * (n_t + 1));
+        *out = pde::l1_relative_error([&](double x, double t) { return lrnr_forward(x, t, p, c)[0]; }, g);
+    });
+}
+
 // ---- FastLRNR construction (reduction.cpp:10-31,111-283) ----
 // Constant hypernetwork (zero W, bias = s) so hyper_forward(mu) == s.
 int ref_build_fast(int L, const int64_t* widths, const int64_t* ranks, const double* params,

@@ -17,7 +17,10 @@ EXPORTS = (
     "lrnr_gpu_set_stream", "lrnr_gpu_set_option", "lrnr_gpu_launch_count", "lrnr_gpu_set_lrnr", "lrnr_gpu_set_fast",
     "lrnr_gpu_set_hyper", "lrnr_gpu_set_points", "lrnr_gpu_set_points_device", "lrnr_gpu_loss_grad_s",
     "lrnr_gpu_set_boundary", "lrnr_gpu_terms_grad", "lrnr_gpu_meta_terms_grad", "lrnr_gpu_fine_tune",
-    "lrnr_gpu_fast_solve", "lrnr_host_epoch_seed", "lrnr_host_sample_batch",
+    "lrnr_gpu_fast_solve", "lrnr_host_epoch_seed", "lrnr_host_sample_batch", "lrnr_gpu_l1_error",
+    "lrnr_ckpt_last_error", "lrnr_ckpt_create", "lrnr_ckpt_load", "lrnr_ckpt_save", "lrnr_ckpt_free",
+    "lrnr_ckpt_get_lrnr", "lrnr_ckpt_put_lrnr", "lrnr_ckpt_get_hyper", "lrnr_ckpt_put_hyper", "lrnr_ckpt_has_fast",
+    "lrnr_ckpt_get_fast", "lrnr_ckpt_put_fast", "lrnr_ckpt_get_sampling", "lrnr_ckpt_put_sampling",
     "lrnr_gpu_loss_grad_s_multi", "lrnr_gpu_hyper_loss_grad", "lrnr_gpu_meta_loss_grad", "lrnr_gpu_jets",
     "lrnr_gpu_loss", "lrnr_gpu_upload_coeffs", "lrnr_gpu_run", "lrnr_gpu_check", "lrnr_gpu_download",
     "lrnr_gpu_fma_peak",
@@ -69,6 +72,22 @@ def load() -> C.CDLL:
     lib.lrnr_host_epoch_seed.argtypes = [C.c_uint64, i64]
     lib.lrnr_host_epoch_seed.restype = C.c_uint64
     lib.lrnr_host_sample_batch.argtypes = [C.c_uint64, i64, i64, i64, dp, dp, dp]
+    lib.lrnr_gpu_l1_error.argtypes = [vp, ip, dp, dp, i64, i64, dp]
+    lib.lrnr_ckpt_last_error.restype = C.c_char_p
+    lib.lrnr_ckpt_create.argtypes = [C.POINTER(vp)]
+    lib.lrnr_ckpt_load.argtypes = [C.c_char_p, C.POINTER(vp)]
+    lib.lrnr_ckpt_save.argtypes = [vp, C.c_char_p]
+    lib.lrnr_ckpt_free.argtypes = [vp]
+    lib.lrnr_ckpt_free.restype = None
+    lib.lrnr_ckpt_get_lrnr.argtypes = [vp, C.POINTER(C.c_int), dp, dp, C.POINTER(i64), dp]
+    lib.lrnr_ckpt_put_lrnr.argtypes = [vp, ip, dp, dp, dp]
+    lib.lrnr_ckpt_get_hyper.argtypes = [vp, C.POINTER(C.c_int), dp, C.POINTER(i64), dp, dp, dp]
+    lib.lrnr_ckpt_put_hyper.argtypes = [vp, ip, dp, dp, ip, dp, dp, dp]
+    lib.lrnr_ckpt_has_fast.argtypes = [vp]
+    lib.lrnr_ckpt_get_fast.argtypes = [vp, C.POINTER(C.c_int), dp, dp, C.POINTER(i64), dp]
+    lib.lrnr_ckpt_put_fast.argtypes = [vp, ip, dp, dp, i64, i64, dp]
+    lib.lrnr_ckpt_get_sampling.argtypes = [vp, C.POINTER(i64), dp]
+    lib.lrnr_ckpt_put_sampling.argtypes = [vp, i64, dp]
     lib.lrnr_gpu_loss_grad_s_multi.argtypes = [vp, ip, dp, dp, C.c_double, dp, dp]
     lib.lrnr_gpu_hyper_loss_grad.argtypes = [vp, ip, dp, C.c_double, dp, dp, dp]
     lib.lrnr_gpu_meta_loss_grad.argtypes = [vp, dp, C.c_double, dp, dp]

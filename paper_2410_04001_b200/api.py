@@ -335,6 +335,13 @@ class GpuContext:
         return dict(s=s, best_loss=bl.value, best_epoch=be.value, losses=losses[:nr.value], aborted=bool(fl.value & 1),
                     diverged=bool(fl.value & 2))
 
+    def l1_error(self, model, s, ref_values, n_x, n_t):
+        """l1_relative_error (pde.cpp:166-178) of the model against a GridField ((n_t+1) x n_x)."""
+        v = C.c_double(0.0)
+        self._rc(self.lib.lrnr_gpu_l1_error(self.h, model, _p(_f64(s)), _p(_f64(ref_values).reshape(-1)), n_x, n_t,
+                                            C.byref(v)), "l1_error")
+        return v.value
+
     def jets(self, model, s):
         out = np.zeros((self.n_points, 4))
         self._rc(self.lib.lrnr_gpu_jets(self.h, model, _p(_f64(s)), _p(out)), "jets")
@@ -436,3 +443,86 @@ def fast_flops_per_point(ranks: Sequence[int], red: Sequence[int], m_in=2, m_out
     fwd = m_in * int(ranks[0]) + sum(int(red[l]) * (int(ranks[l]) + int(ranks[l + 1])) for l in range(L - 1)) + \
         int(ranks[-1]) * m_out
     return 2 * 2 * 4 * fwd
+
+
+# ---------------------------------------------------------------------------
+# checkpoint interop (lrnr_ckpt_*, proj/src/checkpoint.cpp format)
+# ---------------------------------------------------------------------------
+class Checkpoint:
+    """The reference's LRNR v1 checkpoint, read / written by the package's host C++."""
+
+    def __init__(self, path: str | None = None):
+        self.lib = _lib.load()
+        self.h = C.c_void_p()
+        if path is None:
+            rc = self.lib.lrnr_ckpt_create(C.byref(self.h))
+        else:
+            rc = self.lib.lrnr_ckpt_load(str(path).encode(), C.byref(self.h))
+        self._rc(rc)
+
+    def _rc(self, rc):
+        if rc != 0:
+            msg = self.lib.lrnr_ckpt_last_error().decode()
+            raise (ValueError if rc == 1 else LrnrGpuError)(f"checkpoint: {msg}")
+
+    def close(self):
+        if self.h:
+            self.lib.lrnr_ckpt_free(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def save(self, path):
+        self._rc(self.lib.lrnr_ckpt_save(self.h, str(path).encode()))
+
+    def lrnr(self, act=ACT_TANH) -> LrnrParams:
+        L, n = C.c_int(0), C.c_int64(0)
+        self._rc(self.lib.lrnr_ckpt_get_lrnr(self.h, C.byref(L), None, None, C.byref(n), None))
+        w, r, P = np.zeros(L.value + 1, np.int64), np.zeros(L.value, np.int64), np.zeros(n.value)
+        self._rc(self.lib.lrnr_ckpt_get_lrnr(self.h, C.byref(L), _p(w), _p(r), C.byref(n), _p(P)))
+        return LrnrParams(w, r, P, act)
+
+    def put_lrnr(self, m: LrnrParams):
+        w, r = _i64(m.widths), _i64(m.ranks)
+        self._rc(self.lib.lrnr_ckpt_put_lrnr(self.h, len(r), _p(w), _p(r), _p(_f64(m.params))))
+
+    def hyper(self) -> HyperParams:
+        K, n = C.c_int(0), C.c_int64(0)
+        self._rc(self.lib.lrnr_ckpt_get_hyper(self.h, C.byref(K), None, C.byref(n), None, None, None))
+        hw, H, lo, hi = np.zeros(K.value + 1, np.int64), np.zeros(n.value), np.zeros(3), np.zeros(3)
+        self._rc(self.lib.lrnr_ckpt_get_hyper(self.h, C.byref(K), _p(hw), C.byref(n), _p(H), _p(lo), _p(hi)))
+        return HyperParams(hw, H, lo, hi)
+
+    def put_hyper(self, h: HyperParams, split):
+        hw, sp = _i64(h.hw), _i64(split)
+        self._rc(self.lib.lrnr_ckpt_put_hyper(self.h, len(hw) - 1, _p(hw), _p(_f64(h.params)), len(sp), _p(sp),
+                                              _p(_f64(h.lo)), _p(_f64(h.hi))))
+
+    def has_fast(self) -> bool:
+        return bool(self.lib.lrnr_ckpt_has_fast(self.h))
+
+    def fast(self, act=ACT_TANH) -> FastParams:
+        L, n = C.c_int(0), C.c_int64(0)
+        self._rc(self.lib.lrnr_ckpt_get_fast(self.h, C.byref(L), None, None, C.byref(n), None))
+        r, rh, F = np.zeros(L.value, np.int64), np.zeros(L.value - 1, np.int64), np.zeros(n.value)
+        self._rc(self.lib.lrnr_ckpt_get_fast(self.h, C.byref(L), _p(r), _p(rh), C.byref(n), _p(F)))
+        return FastParams(r, rh, F, act)
+
+    def put_fast(self, f: FastParams):
+        r, rh = _i64(f.ranks), _i64(f.red_ranks)
+        self._rc(self.lib.lrnr_ckpt_put_fast(self.h, len(r), _p(r), _p(rh), 2, 1, _p(_f64(f.fparams))))
+
+    def sampling(self):
+        n = C.c_int64(0)
+        self._rc(self.lib.lrnr_ckpt_get_sampling(self.h, C.byref(n), None))
+        X = np.zeros((n.value, 2))
+        self._rc(self.lib.lrnr_ckpt_get_sampling(self.h, C.byref(n), _p(X)))
+        return X
+
+    def put_sampling(self, X):
+        X = _f64(X).reshape(-1, 2)
+        self._rc(self.lib.lrnr_ckpt_put_sampling(self.h, X.shape[0], _p(X)))

@@ -988,6 +988,40 @@ void meta_step(lrnr_gpu_ctx* ctx, Model& m, double w, double* out_grad, double* 
     download(ctx, gout, out_grad, static_cast<size_t>(n_lrnr + n_hyper));
 }
 
+// GridField points (pde.hpp:40-53): row j = time t_j = j / n_t (kTimeHorizon 1), x_i = 2 pi i / n_x
+__global__ void grid_points_kernel(int64_t n_x, int64_t n_t, double* __restrict__ xt) {
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n_x * (n_t + 1)) return;
+    const int64_t j = k / n_x, i = k % n_x;
+    xt[2 * k] = kTwoPi * static_cast<double>(i) / static_cast<double>(n_x);
+    xt[2 * k + 1] = n_t == 0 ? 0.0 : 1.0 * static_cast<double>(j) / static_cast<double>(n_t);
+}
+
+// out = {sum |u - ref|, sum |ref|}: per-thread strided sums, then a fixed-order tree
+__global__ void l1_reduce_kernel(const double* __restrict__ jets, const double* __restrict__ ref, int64_t n,
+                                 double* __restrict__ out) {
+    __shared__ double sn[1024], sd[1024];
+    double a = 0.0, b = 0.0;
+    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+        a += fabs(jets[4 * k] - ref[k]);
+        b += fabs(ref[k]);
+    }
+    sn[threadIdx.x] = a;
+    sd[threadIdx.x] = b;
+    __syncthreads();
+    for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+        if (static_cast<int>(threadIdx.x) < st) {
+            sn[threadIdx.x] += sn[threadIdx.x + st];
+            sd[threadIdx.x] += sd[threadIdx.x + st];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out[0] = sn[0];
+        out[1] = sd[0];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // solve loops on the device (training.cpp:428-607)
 // ---------------------------------------------------------------------------
@@ -1859,6 +1893,38 @@ int lrnr_gpu_fine_tune(lrnr_gpu_ctx* ctx, const double* s_init, const double* mu
             solve_epoch(ctx, m, r);
         }
         solve_results(ctx, m, out_s, out_best_loss, out_best_epoch, out_losses, out_n_records, out_flags);
+    });
+}
+
+int lrnr_gpu_l1_error(lrnr_gpu_ctx* ctx, int model, const double* s, const double* ref_values, int64_t n_x,
+                      int64_t n_t, double* out_l1) {
+    return guarded(ctx, [&] {
+        require(model == LRNR_MODEL_LRNR || model == LRNR_MODEL_FAST, "unknown model slot");
+        const Model& m = ctx->models[model];
+        if (!m.set) throw StateError("model not set");
+        require(s && ref_values && out_l1 && n_x > 0 && n_t >= 0, "bad arguments");
+        const int64_t n = n_x * (n_t + 1);
+        ctx->jets.ensure(static_cast<size_t>(4 * n) * sizeof(double));
+        ctx->meta_ws.ensure(static_cast<size_t>(2 * n + 2 * n) * sizeof(double) + 16);  // grid (x,t) + ref
+        double* grid = ctx->meta_ws.as<double>();
+        double* refd = grid + 2 * n;
+        grid_points_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(n_x, n_t, grid);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(refd, ref_values, static_cast<size_t>(n) * sizeof(double), cudaMemcpyHostToDevice,
+                           ctx->stream));
+        const double mu0[3] = {0.0, 0.0, 0.0};
+        const PointSwap keep(ctx, grid, n);
+        upload_coeffs_impl(ctx, s, mu0, 1, m.rtotal);
+        run_resident_stream<1>(ctx, m, 1.0, ctx->jets.as<double>());
+        double* red = ctx->out.as<double>();  // run_resident_stream sized it >= R1 >= 2
+        l1_reduce_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->jets.as<double>(), refd, n, red);
+        CK(cudaGetLastError());
+        ctx->launches += 2;
+        double h[2];
+        download(ctx, red, h, 2);
+        check_bad(ctx, m);
+        if (h[1] == 0.0) throw InvalidArg("l1_relative_error: reference is identically zero");
+        *out_l1 = h[0] / h[1];
     });
 }
 

@@ -23,7 +23,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
-from oracle.oracle import Reference  # noqa: E402
+from oracle.oracle import Reference, ReferenceCheckpoint  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
 TWO_PI = 6.283185307179586476925286766559
@@ -128,6 +128,20 @@ def main():
     m4r = R.meta_grad_reg(w4, r4, P4r, hw4, H4, lo3, hi3, pts4, mus4, 1e-2, 1.5, 1e-3, threads=4)
     g.update(c4_reg=np.array([1e-2, 1.5, 1e-3]), c4_reg_params=P4r, c4_reg_value=np.array([m4r["value"]]), c4_reg_comps=m4r["comps"],
              c4_reg_ortho=np.array([m4r["ortho"]]), c4_reg_grad=m4r["grad"])
+
+    # checkpoint interop: a file written by the reference's own checkpoint_save
+    # (put_lrnr / put_hyper / put_fast / put_sampling) from the c0 / c1 objects
+    hw0, H0 = R.make_hyper_params(r0, 2, 16, lo3, hi3, 4008, 0.01, 0.5)
+    ReferenceCheckpoint().write(os.path.join(OUT, "reference_checkpoint.lrnr"), w0, r0, P0, hw0, H0, lo3, hi3,
+                                np.array(xs), fast=(r0, f1["red_ranks"], f1["fparams"]))
+    g.update(ck_hw=hw0, ck_hparams=H0)
+    # l1_relative_error (pde.cpp:166-178) of the c0 LRNR against u = sin(x - 30 t)
+    # (the exact solution of mu = (30, 0, 0)) on a 64 x (16 + 1) GridField
+    nx, nt = 64, 16
+    xg = TWO_PI * np.arange(nx) / nx
+    tg = np.arange(nt + 1) / nt
+    field = np.sin(xg[None, :] - 30.0 * tg[:, None])
+    g.update(l1_field=field, l1_value=np.array([R.l1_error(w0, r0, P0, s0, field, nx, nt)]))
 
     path = os.path.join(OUT, "reference_golden.npz")
     np.savez_compressed(path, **g)

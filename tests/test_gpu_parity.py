@@ -601,3 +601,30 @@ def test_fine_tune_fp32_c2_shape_tracks_oracle(gpu, oracle):
                             act=pkg.ACT_SIN)
     np.testing.assert_allclose(r["losses"], want["losses"], rtol=1e-3, atol=0)
     assert normwise(r["s"], want["s"]) <= 1e-4
+
+
+# ----------------------------------------------------------------------------
+# evaluation and checkpoint-loaded models
+# ----------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", [pkg.F64, pkg.F32])
+def test_l1_relative_error_matches_reference(gpu, golden, dtype):
+    g = golden
+    gpu.set_lrnr(lrnr_from_golden(g, "c0"), dtype)
+    field = g["l1_field"]
+    got = gpu.l1_error(pkg.MODEL_LRNR, g["c0_s"], field, field.shape[1], field.shape[0] - 1)
+    tol = 1e-12 if dtype == pkg.F64 else 1e-5
+    assert abs(got - g["l1_value"][0]) <= tol * g["l1_value"][0]
+
+
+def test_model_from_reference_checkpoint_runs(gpu, golden):
+    """A model loaded from a reference-written checkpoint gives the reference's gradient."""
+    import os
+    g = golden
+    ck = pkg.Checkpoint(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_checkpoint.lrnr"))
+    gpu.set_lrnr(ck.lrnr(), pkg.F64)
+    gpu.set_fast(ck.fast(), pkg.F64)
+    gpu.set_points(g["c0_pts"])
+    r = gpu.loss_grad_s(pkg.MODEL_LRNR, g["c0_s"], g["c0_mu"])
+    assert floor_rel(r["grad_s"], g["c0_grad_s"]) <= TOL64
+    rf = gpu.loss_grad_s(pkg.MODEL_FAST, g["c0_s"], g["c0_mu"])
+    assert floor_rel(rf["grad_s"], g["c1_grad_s"]) <= TOL64

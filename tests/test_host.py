@@ -61,7 +61,7 @@ def test_flop_model_matches_survey():
 
 def test_abi_exports_every_declared_symbol():
     header = open(os.path.join(ROOT, "include", "lrnr_gpu.h")).read()
-    declared = set(re.findall(r"^\w[\w\s\*]*?\b(lrnr_(?:gpu|host)_\w+)\s*\(", header, re.M))
+    declared = set(re.findall(r"^\w[\w\s\*]*?\b(lrnr_(?:gpu|host|ckpt)_\w+)\s*\(", header, re.M))
     assert len(declared) >= 25
     lib = C.CDLL(_lib.LIB_PATH)
     for name in declared:
@@ -102,3 +102,68 @@ def test_dist_shard_ranges_cover_exactly():
             assert all(spans[k][1] == spans[k + 1][0] for k in range(world - 1))
             sizes = [b - a for a, b in spans]
             assert max(sizes) - min(sizes) <= 1
+
+
+# ----------------------------------------------------------------------------
+# checkpoint interop (proj/src/checkpoint.cpp format)
+# ----------------------------------------------------------------------------
+CKPT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_checkpoint.lrnr")
+
+
+def test_reads_reference_written_checkpoint(golden):
+    g = golden
+    ck = pkg.Checkpoint(CKPT)
+    m = ck.lrnr()
+    assert list(m.widths) == list(g["c0_widths"]) and list(m.ranks) == list(g["c0_ranks"])
+    assert np.array_equal(m.params, g["c0_params"])
+    h = ck.hyper()
+    assert list(h.hw) == list(g["ck_hw"]) and np.array_equal(h.params, g["ck_hparams"])
+    assert np.array_equal(h.lo, g["c3_lo"]) and np.array_equal(h.hi, g["c3_hi"])
+    assert ck.has_fast()
+    f = ck.fast()
+    assert list(f.red_ranks) == list(g["c1_red_ranks"]) and np.array_equal(f.fparams, g["c1_fparams"])
+    assert np.array_equal(ck.sampling(), g["c1_phase_x"])
+
+
+def test_checkpoint_round_trip(tmp_path, golden):
+    g = golden
+    src = pkg.Checkpoint(CKPT)
+    out = pkg.Checkpoint()
+    out.put_lrnr(src.lrnr())
+    out.put_hyper(src.hyper(), g["c0_ranks"])
+    out.put_fast(src.fast())
+    out.put_sampling(src.sampling())
+    path = tmp_path / "ours.lrnr"
+    out.save(path)
+    back = pkg.Checkpoint(path)
+    assert np.array_equal(back.lrnr().params, g["c0_params"])
+    assert np.array_equal(back.hyper().params, g["ck_hparams"])
+    assert np.array_equal(back.fast().fparams, g["c1_fparams"])
+    assert np.array_equal(back.sampling(), g["c1_phase_x"])
+
+
+def test_checkpoint_written_here_loads_in_the_reference(tmp_path, golden):
+    from oracle.oracle import ReferenceCheckpoint, reference_ckpt_available
+    if not reference_ckpt_available():
+        pytest.skip("reference checkpoint library not built (needs /root/reference and its json header)")
+    g = golden
+    out = pkg.Checkpoint()
+    m = pkg.LrnrParams(g["c0_widths"], g["c0_ranks"], g["c0_params"])
+    out.put_lrnr(m)
+    out.put_hyper(pkg.HyperParams(g["ck_hw"], g["ck_hparams"], g["c3_lo"], g["c3_hi"]), g["c0_ranks"])
+    out.put_sampling(g["c1_phase_x"])
+    path = tmp_path / "ours.lrnr"
+    out.save(path)
+    P, H = ReferenceCheckpoint().read(path, m.params.size, g["ck_hparams"].size)
+    assert np.array_equal(P, g["c0_params"]) and np.array_equal(H, g["ck_hparams"])
+
+
+def test_checkpoint_rejects_bad_files(tmp_path):
+    bad = tmp_path / "bad.lrnr"
+    bad.write_bytes(b"NOPE\x01\x00\x00\x00")
+    with pytest.raises(ValueError):
+        pkg.Checkpoint(bad)
+    trunc = tmp_path / "trunc.lrnr"
+    trunc.write_bytes(open(CKPT, "rb").read()[:1000])
+    with pytest.raises(ValueError):
+        pkg.Checkpoint(trunc)
