@@ -21,7 +21,8 @@
 #define LRNR_TILE_F32(X) \
     X(float, 64, 2, 16, 32, 1, false) X(float, 64, 2, 16, 32, 1, true) X(float, 64, 2, 16, 32, 0, false) \
     X(float, 64, 1, 8, 32, 1, false) X(float, 64, 1, 8, 32, 1, true) X(float, 64, 1, 8, 32, 0, false) \
-    X(float, 32, 2, 16, 32, 1, false) X(float, 32, 2, 16, 32, 1, true) X(float, 32, 2, 16, 32, 0, false)
+    X(float, 32, 2, 16, 32, 1, false) X(float, 32, 2, 16, 32, 1, true) X(float, 32, 2, 16, 32, 0, false) \
+    X(float, 32, 1, 8, 32, 1, false) X(float, 32, 1, 8, 32, 1, true) X(float, 32, 1, 8, 32, 0, false)
 #define LRNR_TILE_F32R64(X) \
     X(float, 32, 2, 16, 64, 1, false) X(float, 32, 2, 16, 64, 1, true) X(float, 32, 2, 16, 64, 0, false)
 #define LRNR_TILE_F64(X) X(double, 32, 1, 8, 32, 0, false) X(double, 32, 1, 8, 32, 1, false)

@@ -130,8 +130,8 @@ void build_v2(Model& m, bool meta) {
         v.P = 32;
         v.NG = 16;
         v.PT1 = 2;
-    } else if (maxM <= 32) {
-        v.P = 64;
+    } else if (maxM <= 32) {  // narrow (FastLRNR): one 32-neuron chunk per transition
+        v.P = m.tile_p == 32 ? 32 : 64;
         v.NG = 8;
         v.PT1 = 1;
     } else {
@@ -467,6 +467,9 @@ bool dispatch_v2(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const d
         V2CASE(float, 64, 1, 8, 32, 1, false)
         V2CASE(float, 64, 1, 8, 32, 1, true)
         V2CASE(float, 64, 1, 8, 32, 0, false)
+        V2CASE(float, 32, 1, 8, 32, 1, false)
+        V2CASE(float, 32, 1, 8, 32, 1, true)
+        V2CASE(float, 32, 1, 8, 32, 0, false)
         V2CASE(float, 32, 2, 16, 32, 1, false)
         V2CASE(float, 32, 2, 16, 32, 1, true)
         V2CASE(float, 32, 2, 16, 32, 0, false)

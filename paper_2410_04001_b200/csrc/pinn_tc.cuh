@@ -49,6 +49,17 @@ constexpr int ISSUER = TC_DEDICATED ? NWE : 0;
 constexpr int NT = 32 * (NWE + (TC_DEDICATED ? 1 : 0));
 constexpr int NG = KC / (NWE / 4);  // neurons (epilogue) / ranks (sums) per thread
 constexpr int TM_P1 = 0, TM_ZH = 128, TM_ZL = 256, TM_Y = 384;
+// Phase-2 products of YACC consecutive chunks accumulate in TMEM before the
+// epilogue reads them into the FP32 running sum (the tensor-core accumulator
+// truncates: 1 chunk = 12 MMAs keeps it at ~3e-6 on c2, 2 chunks ~6e-6, the
+// full K = 256 reached 1.2e-4). Halves the TMEM reads of Y (64 B/clk/SM).
+#ifndef TC_SPLITLD
+#define TC_SPLITLD 1
+#endif
+#ifndef TC_YACC
+#define TC_YACC 2
+#endif
+constexpr int YACC = TC_YACC;
 
 template <typename T = float>
 struct NetTC {
@@ -280,7 +291,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
     };
     // phase 2 (warp 0, converged): Y_c = Z_c B (fresh accumulator, A from TMEM),
     // B = factor tiles (rows rn) at float offset bo (hi) / bo + rn * KC (lo)
-    auto mma_p2 = [&](int bo, int rn) {
+    auto mma_p2 = [&](int bo, int rn, bool acc0) {
         const uint32_t id_p2 = umma::idesc_tf32(P, rn);
         const uint32_t lb = rn == 16 ? lb16 : lb32;
         const uint32_t bh0 = lb + (bo >> 2), bl0 = lb + ((bo + rn * KC) >> 2);
@@ -291,7 +302,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
 #pragma unroll
             for (int s = 0; s < KC / 8; ++s) {
                 const uint32_t azh = tbase + TM_ZH + c * KC + s * 8, azl = tbase + TM_ZL + c * KC + s * 8;
-                umma::mma_ts_w(d, azh, bh0 + s * sb, dhi, id_p2, s > 0 ? 1u : 0u);
+                umma::mma_ts_w(d, azh, bh0 + s * sb, dhi, id_p2, (s > 0 || acc0) ? 1u : 0u);
                 umma::mma_ts_w(d, azh, bl0 + s * sb, dhi, id_p2, 1);
                 umma::mma_ts_w(d, azl, bh0 + s * sb, dhi, id_p2, 1);
             }
@@ -354,7 +365,9 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                     wait_slot(qq);
                     mma_p1(static_cast<int>(qq % NBUF) * BUF, rk);
                 };
-                auto fwd_p2 = [&](int64_t qq) { mma_p2(static_cast<int>(qq % NBUF) * BUF + 2 * KC * rk + 32, rnn); };
+                auto fwd_p2 = [&](int64_t qq, int ch) {
+                    mma_p2(static_cast<int>(qq % NBUF) * BUF + 2 * KC * rk + 32, rnn, ch % YACC != 0);
+                };
                 if (warp == ISSUER) fwd_p1(q);
                 // pipeline per chunk ch: [P1(ch) | P2(ch-1)] on the tensor core while the
                 // epilogue of ch computes the activation jet; Z / Y are touched only after
@@ -369,13 +382,28 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                         if (ch == 0 && tid == 0) issue(q + NBUF - 1);
                         {
                             float a[4][NG];
+                            float* Ast = ascr + net.aoff[l] + static_cast<int64_t>(ch) * (P * KC * 4);
+#if TC_SPLITLD
+                            // two column halves: the second half's TMEM read overlaps the first half's math
+    #pragma unroll
+                            for (int c = 0; c < 4; ++c) umma::tmem_ld4(tlane + TM_P1 + c * KC + half * NG, a[c]);
+                            umma::tmem_ld_wait();
+    #pragma unroll
+                            for (int c = 0; c < 4; ++c) umma::tmem_ld4(tlane + TM_P1 + c * KC + half * NG + 4, a[c] + 4);
+#else
     #pragma unroll
                             for (int c = 0; c < 4; ++c) tld(tlane + TM_P1 + c * KC + half * NG, a[c]);
                             umma::tmem_ld_wait();
                             signal(&p1free);  // P1 may be overwritten by P1(ch+1)
-                            float* Ast = ascr + net.aoff[l] + static_cast<int64_t>(ch) * (P * KC * 4);
+#endif
     #pragma unroll
                             for (int n = 0; n < NG; ++n) {
+#if TC_SPLITLD
+                                if (n == NG / 2) {
+                                    umma::tmem_ld_wait();
+                                    signal(&p1free);
+                                }
+#endif
                                 const int k = half * NG + n;
                                 const float av = a[0][n] + bias[k], ax = a[1][n], at = a[2][n], aw = a[3][n];
                                 v2::st4(Ast + aidx(k, p), av, ax, at, aw);
@@ -390,7 +418,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                             if (ch > 0) {
                                 wait_mma2();  // P2(ch-1): Z free, its Y product ready
                                 if (tid == 0) issue(q + NBUF - 1);
-                                add_y(tlane + TM_Y + half * NG, ysum);
+                                if (ch % YACC == 0) add_y(tlane + TM_Y + half * NG, ysum);  // a group of YACC chunks is complete
                             }
                             TC_MARK(0);
     #pragma unroll
@@ -411,7 +439,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                         await(&p1free, phf);  // every chunk (keeps the phase count)
                         if (ch + 1 < net.nc[l]) fwd_p1(q + 1);
                         await(&zready, phz);
-                        fwd_p2(q);
+                        fwd_p2(q, ch);
                         if (lane == 0) TC_ISSUE_END();
                     }
                 }
@@ -502,7 +530,9 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                     wait_slot(qq);
                     mma_p1(static_cast<int>(qq % NBUF) * BUF, rkn);
                 };
-                auto bwd_p2 = [&](int64_t qq) { mma_p2(static_cast<int>(qq % NBUF) * BUF + 2 * KC * rkn, rnl); };
+                auto bwd_p2 = [&](int64_t qq, int ch) {
+                    mma_p2(static_cast<int>(qq % NBUF) * BUF + 2 * KC * rkn, rnl, ch % YACC != 0);
+                };
                 if (warp == ISSUER) bwd_p1(q);
                 for (int ch = 0; ch < net.nc[l]; ++ch, ++q) {
                     if (warp < NWE) {
@@ -522,12 +552,26 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                         if (ch == 0 && tid == 0) issue(q + NBUF - 1);
                         {
                             float dz[4][NG];
+#if TC_SPLITLD
+    #pragma unroll
+                            for (int c = 0; c < 4; ++c) umma::tmem_ld4(tlane + TM_P1 + c * KC + half * NG, dz[c]);
+                            umma::tmem_ld_wait();
+    #pragma unroll
+                            for (int c = 0; c < 4; ++c) umma::tmem_ld4(tlane + TM_P1 + c * KC + half * NG + 4, dz[c] + 4);
+#else
     #pragma unroll
                             for (int c = 0; c < 4; ++c) tld(tlane + TM_P1 + c * KC + half * NG, dz[c]);
                             umma::tmem_ld_wait();
                             signal(&p1free);
+#endif
     #pragma unroll
                             for (int n = 0; n < NG; ++n) {
+#if TC_SPLITLD
+                                if (n == NG / 2) {
+                                    umma::tmem_ld_wait();
+                                    signal(&p1free);
+                                }
+#endif
                                 const float av = a[0][n], ax = a[1][n], at = a[2][n], aw = a[3][n];
                                 const float g0 = dz[0][n], g1 = dz[1][n], g2 = dz[2][n], g3 = dz[3][n];
                                 float sg, d1, d2, d3;
@@ -541,7 +585,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                             if (ch > 0) {
                                 wait_mma2();  // P2(ch-1): G free, its T product ready
                                 if (tid == 0) issue(q + NBUF - 1);
-                                add_y(tlane + TM_Y + half * NG, tsum);
+                                if (ch % YACC == 0) add_y(tlane + TM_Y + half * NG, tsum);
                             }
                             TC_MARK(8);
     #pragma unroll
@@ -561,7 +605,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                         await(&p1free, phf);  // every chunk (keeps the phase count)
                         if (ch + 1 < net.nc[l]) bwd_p1(q + 1);
                         await(&zready, phz);
-                        bwd_p2(q);
+                        bwd_p2(q, ch);
                     }
                 }
                 // transition end: T -> dL/ds_l partials, ST = s_l (.) T (smem hi / lo)

@@ -9,8 +9,10 @@ ctx = pkg.GpuContext(0)
 st = torch.cuda.Stream(); torch.cuda.set_stream(st); ctx.set_stream(st.cuda_stream)
 ctx.set_fast(c['fast'], pkg.F32); ctx.set_points(c['pts']); ctx.upload_coeffs(c['s'], c['mu'])
 fl = pkg.fast_flops_per_point(c['fast'].ranks, c['fast'].red_ranks)
-for kern in (pkg.KERNEL_FMA_TILE, pkg.KERNEL_TC, pkg.KERNEL_STREAM):
+for kern, tp in ((pkg.KERNEL_FMA_TILE, 64), (pkg.KERNEL_FMA_TILE, 32), (pkg.KERNEL_TC, 64)):
     ctx.set_option(pkg.OPT_KERNEL, kern)
+    ctx.set_option(pkg.OPT_TILE_P, tp)
+    ctx.set_fast(c['fast'], pkg.F32)
     for _ in range(2): ctx.run(pkg.MODEL_FAST)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -20,5 +22,5 @@ for kern in (pkg.KERNEL_FMA_TILE, pkg.KERNEL_TC, pkg.KERNEL_STREAM):
     e1.record(st); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / K
     out = ctx.download(1 + c['model'].r_total)
-    print(f"kernel={kern} fast: {ms:.3f} ms  {fl*n/ms/1e9:.2f} TFLOP/s ({fl*n/ms/1e9/74.45*100:.1f}%)  loss={out[0]:.9e}")
+    print(f"kernel={kern} tile_p={tp} fast: {ms:.3f} ms  {fl*n/ms/1e9:.2f} TFLOP/s ({fl*n/ms/1e9/74.45*100:.1f}%)  loss={out[0]:.9e}")
 ctx.check()
