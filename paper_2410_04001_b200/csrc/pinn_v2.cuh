@@ -210,7 +210,8 @@ struct Tile {
     static_assert(RPMAX % (4 * JG) == 0, "RPMAX multiple of 32");
 
     // forward phase 1: Z = sigma-jet(SY U^T + b) for this thread's PT1 points x 4 neurons
-    template <int RL>
+    // KK: active neuron groups (k = ng + NG kk, kk < KK) of a narrow last chunk (warp-uniform)
+    template <int RL, int KK = 4>
     static __device__ __forceinline__ void fwd_phase1(const T* __restrict__ UT, const T* __restrict__ bb,
                                                       const T* __restrict__ SY, T* __restrict__ Zg, int ng,
                                                       int pg, T* __restrict__ Ast) {
@@ -220,7 +221,7 @@ struct Tile {
 #pragma unroll
             for (int c = 0; c < 4; ++c)
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) a1[i][c][kk] = T(0);
+                for (int kk = 0; kk < KK; ++kk) a1[i][c][kk] = T(0);
         const T* syb = SY + pg * PT1 * S::SS;
 #pragma unroll
         for (int j = 0; j < RL; ++j) {
@@ -233,7 +234,7 @@ struct Tile {
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) a1[i][c][kk] = fma(sy[c], ut[kk], a1[i][c][kk]);
+                    for (int kk = 0; kk < KK; ++kk) a1[i][c][kk] = fma(sy[c], ut[kk], a1[i][c][kk]);
             }
         }
         T bias[4];
@@ -241,7 +242,7 @@ struct Tile {
 #pragma unroll
         for (int i = 0; i < PT1; ++i)
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
+            for (int kk = 0; kk < KK; ++kk) {
                 const T av = a1[i][0][kk] + bias[kk], ax = a1[i][1][kk];
                 const T at = a1[i][2][kk], aw = a1[i][3][kk];
                 st4(Ast + ((pg * PT1 + i) * KC + ng + NG * kk) * 4, av, ax, at, aw);
@@ -252,7 +253,7 @@ struct Tile {
     }
 
     // backward phase 1: G = VJP(A, ST V^T), A reloaded from the forward sweep's store
-    template <int RN>
+    template <int RN, int KK = 4>
     static __device__ __forceinline__ void bwd_phase1(const T* __restrict__ Ast, const T* __restrict__ VT,
                                                       const T* __restrict__ ST, T* __restrict__ Zg, int ng,
                                                       int pg, T* __restrict__ Zz = nullptr) {
@@ -261,7 +262,7 @@ struct Tile {
 #pragma unroll
         for (int i = 0; i < PT1; ++i)
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
+            for (int kk = 0; kk < KK; ++kk) {
                 T a4[4];
                 ld4(Ast + ((pg * PT1 + i) * KC + ng + NG * kk) * 4, a4);
 #pragma unroll
@@ -272,7 +273,7 @@ struct Tile {
 #pragma unroll
             for (int c = 0; c < 4; ++c)
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) dz[i][c][kk] = T(0);
+                for (int kk = 0; kk < KK; ++kk) dz[i][c][kk] = T(0);
         const T* stb = ST + pg * PT1 * S::SS;
 #pragma unroll
         for (int j = 0; j < RN; ++j) {
@@ -285,13 +286,13 @@ struct Tile {
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) dz[i][c][kk] = fma(st[c], vt[kk], dz[i][c][kk]);
+                    for (int kk = 0; kk < KK; ++kk) dz[i][c][kk] = fma(st[c], vt[kk], dz[i][c][kk]);
             }
         }
 #pragma unroll
         for (int i = 0; i < PT1; ++i)
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
+            for (int kk = 0; kk < KK; ++kk) {
                 const T av = a1[i][0][kk], ax = a1[i][1][kk];
                 const T at = a1[i][2][kk], aw = a1[i][3][kk];
                 const T g0 = dz[i][0][kk], g1 = dz[i][1][kk], g2 = dz[i][2][kk], g3 = dz[i][3][kk];
@@ -365,14 +366,15 @@ struct Tile {
     }
 
     // phase 2: acc += Zg[p2] * Mat (Mat = KC x RN, row stride RN)
+    // kc: neurons of this chunk (< KC in a narrow last chunk; padded rows are zero)
     template <int RN>
     static __device__ __forceinline__ void phase2(const T* __restrict__ Zg, const T* __restrict__ Mat,
-                                                  T (&acc)[NJ][4][4], int p2, int jg) {
+                                                  T (&acc)[NJ][4][4], int p2, int jg, int kc) {
         constexpr int NJE = (RN + 4 * JG - 1) / (4 * JG);
         if (RN < 4 * JG && jg * 4 >= RN) return;
         const T* zb = Zg + p2 * S::ZS;
 #pragma unroll 16
-        for (int k = 0; k < KC; ++k) {
+        for (int k = 0; k < kc; ++k) {
             T z[4];
             ld4(zb + k * 4, z);
 #pragma unroll
@@ -519,11 +521,24 @@ pinn_tile_kernel(const NetV2<T> net, const RunGeom g, const double* __restrict__
                     const T* bb = UT + rl * KC;
                     const T* Vm = bb + KC;
                     T* Ast = ascr + net.aoff[l] + static_cast<int64_t>(ch) * (P * KC * 4);
-                    if (rl == 4) K::template fwd_phase1<4>(UT, bb, SY, Zg, ng, pg, Ast);
-                    else K::template fwd_phase1<RPMAX>(UT, bb, SY, Zg, ng, pg, Ast);
+                    const int kc = META ? KC : min(KC, net.M[l + 1] - ch * KC);
+                    const int kk = (kc + NG - 1) / NG;
+#define V2_FWD1(RLV)                                                                         \
+    switch (kk) {                                                                            \
+        case 1: K::template fwd_phase1<RLV, 1>(UT, bb, SY, Zg, ng, pg, Ast); break;          \
+        case 2: K::template fwd_phase1<RLV, 2>(UT, bb, SY, Zg, ng, pg, Ast); break;          \
+        case 3: K::template fwd_phase1<RLV, 3>(UT, bb, SY, Zg, ng, pg, Ast); break;          \
+        default: K::template fwd_phase1<RLV, 4>(UT, bb, SY, Zg, ng, pg, Ast); break;         \
+    }
+                    if (rl == 4) {
+                        V2_FWD1(4)
+                    } else {
+                        V2_FWD1(RPMAX)
+                    }
+#undef V2_FWD1
                     __syncthreads();
-                    if (rn == 4) K::template phase2<4>(Zg, Vm, yacc, p2, jg);
-                    else K::template phase2<RPMAX>(Zg, Vm, yacc, p2, jg);
+                    if (rn == 4) K::template phase2<4>(Zg, Vm, yacc, p2, jg, kc);
+                    else K::template phase2<RPMAX>(Zg, Vm, yacc, p2, jg, kc);
                     __syncthreads();
                 }
                 // y_{l+1} -> scratch, SY = s_{l+1} (.) y_{l+1}
@@ -644,11 +659,24 @@ pinn_tile_kernel(const NetV2<T> net, const RunGeom g, const double* __restrict__
                     const T* VT = acquire();
                     const T* Um = VT + rn * KC;
                     const T* Ast = ascr + net.aoff[l] + static_cast<int64_t>(ch) * (P * KC * 4);
-                    if (rn == 4) K::template bwd_phase1<4>(Ast, VT, ST, Zg, ng, pg, Zz);
-                    else K::template bwd_phase1<RPMAX>(Ast, VT, ST, Zg, ng, pg, Zz);
+                    const int kc = META ? KC : min(KC, net.M[l + 1] - ch * KC);
+                    const int kk = (kc + NG - 1) / NG;
+#define V2_BWD1(RNV)                                                                         \
+    switch (kk) {                                                                            \
+        case 1: K::template bwd_phase1<RNV, 1>(Ast, VT, ST, Zg, ng, pg, Zz); break;          \
+        case 2: K::template bwd_phase1<RNV, 2>(Ast, VT, ST, Zg, ng, pg, Zz); break;          \
+        case 3: K::template bwd_phase1<RNV, 3>(Ast, VT, ST, Zg, ng, pg, Zz); break;          \
+        default: K::template bwd_phase1<RNV, 4>(Ast, VT, ST, Zg, ng, pg, Zz); break;         \
+    }
+                    if (rn == 4) {
+                        V2_BWD1(4)
+                    } else {
+                        V2_BWD1(RPMAX)
+                    }
+#undef V2_BWD1
                     __syncthreads();
-                    if (rl == 4) K::template phase2<4>(Zg, Um, tacc, p2, jg);
-                    else K::template phase2<RPMAX>(Zg, Um, tacc, p2, jg);
+                    if (rl == 4) K::template phase2<4>(Zg, Um, tacc, p2, jg, kc);
+                    else K::template phase2<RPMAX>(Zg, Um, tacc, p2, jg, kc);
                     if constexpr (META) {
                         const int k0 = ch * KC;
                         const int M = net.M[l + 1];
