@@ -1,0 +1,50 @@
+"""Throughput of the non-headline BASELINE configs on one GPU (measurement record):
+c3 = hypernetwork -> FastLRNR per instance + hypernet VJP (1024 mu x 16,384 pts),
+c4 = meta step (U, V, b, theta gradients; 8 of the 64 mu x 1,048,576 pts per step).
+Device time with CUDA events around the host-buffer call (points resident)."""
+import json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import paper_2410_04001_b200 as pkg
+
+PEAK = 74.45
+out = {}
+# c3
+c = pkg.config3(n_inst=1024, pts_per_inst=16384)
+ctx = pkg.GpuContext(0)
+ctx.set_fast(c["fast"], pkg.F32)
+ctx.set_hyper(c["hyper"])
+ctx.set_points(c["pts"], n_inst=1024)
+ctx.hyper_loss_grad(pkg.MODEL_FAST, c["mus"])
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+K = 3
+for _ in range(K):
+    r = ctx.hyper_loss_grad(pkg.MODEL_FAST, c["mus"])
+dt = (time.perf_counter() - t0) / K
+n = 1024 * 16384
+fl = pkg.fast_flops_per_point(c["fast"].ranks, c["fast"].red_ranks)
+out["c3"] = {"ms_per_step": dt * 1e3, "point_evals_per_s": n / dt, "tflops": fl * n / dt / 1e12,
+             "frac_fp32_fma": fl * n / dt / 1e12 / PEAK, "flop_per_point": fl, "points": n,
+             "kernel": "FMA tile (FastLRNR) + FP64 hypernetwork fwd/VJP", "loss": r["value"]}
+ctx.close()
+# c4 (8 instances per step; the 64-instance step is 8x this)
+n_inst, per = 8, 1 << 20
+c = pkg.config4(n_inst=n_inst, pts_per_inst=per)
+ctx = pkg.GpuContext(0)
+ctx.set_lrnr(c["model"], pkg.F32)
+ctx.set_hyper(c["hyper"])
+ctx.set_points(c["pts"], n_inst=n_inst)
+ctx.meta_loss_grad(c["mus"], c["model"].params.size)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+r = ctx.meta_loss_grad(c["mus"], c["model"].params.size)
+dt = time.perf_counter() - t0
+n = n_inst * per
+fl = pkg.algorithmic_flops_per_point(c["model"].widths, c["model"].ranks, meta=True)
+out["c4"] = {"ms_per_step_8_of_64_instances": dt * 1e3, "point_evals_per_s": n / dt, "tflops": fl * n / dt / 1e12,
+             "frac_fp32_fma": fl * n / dt / 1e12 / PEAK, "flop_per_point": fl, "points": n,
+             "kernel": "FMA tile (META phase 3) + FP64 hypernetwork", "loss": r["value"]}
+ctx.close()
+print(json.dumps(out))
