@@ -16,6 +16,7 @@
 #include "pinn_kernels.cuh"
 #include "pinn_v2.cuh"
 #include "pinn_small.cuh"
+#include "pinn_solve.cuh"
 
 namespace lrnr_b200 {
 namespace detail {
@@ -187,7 +188,8 @@ struct lrnr_gpu_ctx {
     int tag = -1;
     int64_t launches = 0;
     int opt_fast_sincos = 0;  // LRNR_OPT_FAST_SINCOS
-    int opt_kernel = 0;       // LRNR_OPT_KERNEL: 0 auto, 1 streaming, 2 tensor core, 3 FMA tile
+    int opt_kernel = 0;       // LRNR_OPT_KERNEL: 0 auto, 1 streaming, 2 tensor core, 3 FMA tile, 4 small batch
+    int opt_solve = 0;        // LRNR_OPT_SOLVE: 0 auto (persistent fast solver when eligible), 1 graph path
 };
 
 namespace lrnr_b200 {

@@ -1028,7 +1028,7 @@ __global__ void l1_reduce_kernel(const double* __restrict__ jets, const double* 
 // ---------------------------------------------------------------------------
 // solve loops on the device (training.cpp:428-607)
 // ---------------------------------------------------------------------------
-struct SolveState {
+struct SolveState {  // same layout as solve::State (the persistent solver's)
     double best_loss;
     double initial;
     int64_t epoch, best_epoch, t;
@@ -1205,6 +1205,8 @@ void solve_results(lrnr_gpu_ctx* ctx, const Model& m, double* out_s, double* out
     if (out_flags) *out_flags = st.flags;
 }
 
+static_assert(sizeof(SolveState) == sizeof(solve::State), "solve state layouts must match");
+
 // Run the solve on a stream that can be captured (the legacy default stream cannot).
 struct SolveStream {
     lrnr_gpu_ctx* ctx;
@@ -1218,6 +1220,90 @@ struct SolveStream {
         ctx->stream = saved;
     }
 };
+
+// The persistent fast-phase solver (pinn_solve.cuh) when the FastLRNR and the
+// term set fit one CTA; returns false (nothing launched) otherwise.
+bool fast_solve_persistent(lrnr_gpu_ctx* ctx, const Model& m, const std::vector<double>& ip,
+                           const std::vector<double>& ic, const std::vector<double>& per, const double* s_init,
+                           const double* mu, double lambda_local, double lr, int64_t epochs) {
+    if (ctx->opt_solve != 0) return false;
+    const int n_int = static_cast<int>(ip.size() / 2), n_ic = static_cast<int>(ic.size()),
+              n_bc = static_cast<int>(per.size());
+    solve::Problem pb{};
+    pb.n_int = n_int;
+    pb.n_ic = n_ic;
+    pb.n_bc = n_bc;
+    pb.n_warps = n_int + n_ic + 2 * n_bc;
+    if (pb.n_warps < 1 || pb.n_warps > 32 || n_bc > 15 || m.r[0] > 4 || m.rtotal > 1024) return false;
+    for (int l = 0; l < m.L; ++l)
+        if (m.r[l] > 32) return false;
+    for (int l = 1; l < m.L; ++l)
+        if (m.M[l] > 32) return false;
+    int y = 0, a = 0, w = 0;
+    for (int l = 0; l < m.L; ++l) {
+        pb.yoff[l] = y;
+        y += m.r[l];
+    }
+    for (int l = 0; l + 1 < m.L; ++l) {
+        pb.aoff[l] = a;
+        a += m.M[l + 1];
+        pb.woff[l] = w;
+        pb.wrow[l] = m.trow[l] | 1;
+        w += m.M[l + 1] * pb.wrow[l];
+    }
+    pb.ylen = y;
+    pb.alen = a;
+    pb.wlen = (w + 3) & ~3;
+    pb.lr = lr;
+    pb.lambda_local = lambda_local;
+    pb.epochs = epochs;
+    const size_t elem = m.dtype == LRNR_F64 ? 8 : 4;
+    const size_t smem = solve::smem_bytes(pb, m.rtotal, elem);
+    if (smem > 220 * 1024) return false;
+    // terms: interior (x, t) pairs, then initial x, then periodic t
+    std::vector<double> terms(ip);
+    terms.insert(terms.end(), ic.begin(), ic.end());
+    terms.insert(terms.end(), per.begin(), per.end());
+    const int G = m.rtotal;
+    ctx->solve_pts[0].ensure(terms.size() * sizeof(double) + 16);
+    ctx->solve_s0.ensure(static_cast<size_t>(G) * sizeof(double) + 8);
+    ctx->solve_best.ensure(static_cast<size_t>(G) * sizeof(double) + 8);
+    ctx->solve_bt.ensure(static_cast<size_t>(2 * epochs) * sizeof(double));
+    ctx->solve_losses.ensure(static_cast<size_t>(epochs) * sizeof(double));
+    ctx->solve_state.ensure(sizeof(solve::State));
+    ctx->mu_dev.ensure(3 * sizeof(double) + 8);
+    std::vector<double> bt(static_cast<size_t>(2 * epochs));
+    for (int64_t t = 1; t <= epochs; ++t) {
+        bt[2 * (t - 1)] = 1.0 - std::pow(0.9, static_cast<double>(t));
+        bt[2 * (t - 1) + 1] = 1.0 - std::pow(0.999, static_cast<double>(t));
+    }
+    CK(cudaMemcpyAsync(ctx->solve_pts[0].p, terms.data(), terms.size() * sizeof(double), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CK(cudaMemcpyAsync(ctx->solve_s0.p, s_init, static_cast<size_t>(G) * sizeof(double), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CK(cudaMemcpyAsync(ctx->solve_bt.p, bt.data(), bt.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->mu_dev.p, mu, 3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    if (m.dtype == LRNR_F64) {
+        auto kern = m.act == LRNR_ACT_TANH ? solve::fast_solve_kernel<double, 0> : solve::fast_solve_kernel<double, 1>;
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        kern<<<1, 32 * pb.n_warps, smem, ctx->stream>>>(dev_net<double>(m), pb, ctx->solve_pts[0].as<double>(),
+                                                         ctx->mu_dev.as<double>(), ctx->solve_s0.as<double>(),
+                                                         ctx->solve_bt.as<double>(), ctx->solve_best.as<double>(),
+                                                         ctx->solve_losses.as<double>(),
+                                                         ctx->solve_state.as<solve::State>());
+    } else {
+        auto kern = m.act == LRNR_ACT_TANH ? solve::fast_solve_kernel<float, 0> : solve::fast_solve_kernel<float, 1>;
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        kern<<<1, 32 * pb.n_warps, smem, ctx->stream>>>(dev_net<float>(m), pb, ctx->solve_pts[0].as<double>(),
+                                                        ctx->mu_dev.as<double>(), ctx->solve_s0.as<double>(),
+                                                        ctx->solve_bt.as<double>(), ctx->solve_best.as<double>(),
+                                                        ctx->solve_losses.as<double>(),
+                                                        ctx->solve_state.as<solve::State>());
+    }
+    CK(cudaGetLastError());
+    ++ctx->launches;
+    return true;
+}
 
 }  // namespace
 
@@ -1269,6 +1355,7 @@ int lrnr_gpu_set_option(lrnr_gpu_ctx* ctx, int opt, int value) {
     return guarded(ctx, [&] {
         if (opt == LRNR_OPT_FAST_SINCOS) ctx->opt_fast_sincos = value;
         else if (opt == LRNR_OPT_KERNEL) ctx->opt_kernel = value;
+        else if (opt == LRNR_OPT_SOLVE) ctx->opt_solve = value;
         else if (opt == LRNR_OPT_TILE_P) {
             require(value == 0 || value == 32 || value == 64, "tile P must be 32 or 64 (0 = default)");
             for (auto& m : ctx->models) {
@@ -1769,6 +1856,10 @@ int lrnr_gpu_fast_solve(lrnr_gpu_ctx* ctx, const double* s_init, const double* m
         const int64_t n_int = static_cast<int64_t>(ip.size() / 2), n_ic = static_cast<int64_t>(ic.size()),
                       n_bc = static_cast<int64_t>(per.size());
         SolveStream ss(ctx);
+        if (fast_solve_persistent(ctx, m, ip, ic, per, s_init, mu, lambda_local, lr, epochs)) {
+            solve_results(ctx, m, out_s, out_best_loss, out_best_epoch, out_losses, out_n_records, out_flags);
+            return;
+        }
         const PointSwap restore(ctx, ctx->pts, ctx->n_per);  // keep the caller's point set
         ctx->n_inst = restore.n_inst;
         solve_setup(ctx, m, s_init, mu, epochs, n_ic + 2 * n_bc);

@@ -571,8 +571,19 @@ def test_fine_tune_fp64_matches_reference(gpu, golden):
     assert r["best_epoch"] == g["c0_ft_best"][1] and not r["aborted"]
 
 
+@pytest.fixture
+def solve_path(gpu):
+    def apply(path):
+        gpu.set_option(pkg.OPT_SOLVE, path)
+
+    yield apply
+    apply(0)
+
+
+@pytest.mark.parametrize("path", [0, 1])  # 0: persistent single-CTA solver, 1: graph path
 @pytest.mark.parametrize("tag", ["a", "b"])
-def test_fast_solve_fp64_matches_reference(gpu, golden, tag):
+def test_fast_solve_fp64_matches_reference(gpu, golden, solve_path, tag, path):
+    solve_path(path)
     g = golden
     lam, lr, ep = g[f"c1_fs{tag}_cfg"]
     gpu.set_fast(pkg.FastParams(g["c0_ranks"], g["c1_red_ranks"], g["c1_fparams"], pkg.ACT_TANH), pkg.F64)
@@ -582,13 +593,29 @@ def test_fast_solve_fp64_matches_reference(gpu, golden, tag):
     assert r["best_epoch"] == g[f"c1_fs{tag}_best"][1] and not r["diverged"]
 
 
-def test_fast_solve_nonfinite_start_aborts(gpu, golden):
+@pytest.mark.parametrize("path", [0, 1])
+def test_fast_solve_nonfinite_start_aborts(gpu, golden, solve_path, path):
+    solve_path(path)
     g = golden
     gpu.set_fast(pkg.FastParams(g["c0_ranks"], g["c1_red_ranks"], g["c1_fparams"], pkg.ACT_TANH), pkg.F64)
     s = g["c0_s"].copy()
     s[2] = np.nan
     r = gpu.fast_solve(s, g["c0_mu"], g["c1_phase_x"], 1e-2, 1e-2, 5)
     assert r["aborted"] and r["diverged"] and len(r["losses"]) == 0 and r["best_epoch"] == 0
+
+
+@pytest.mark.parametrize("path", [0, 1])
+def test_fast_solve_fp32_c2_tracks_oracle(gpu, oracle, solve_path, path):
+    """FP32 sin c2 FastLRNR: the device fast phase tracks the FP64 oracle loop."""
+    solve_path(path)
+    c = pkg.config2(n_points=0, act=pkg.ACT_SIN)
+    f = c["fast"]
+    X = np.array([(2 * np.pi * i / 3.0, j / 2.0) for j in range(3) for i in range(4)])
+    gpu.set_fast(f, pkg.F32)
+    r = gpu.fast_solve(c["s"], c["mu"], X, 1e-2, 1e-2, 30)
+    want = oracle.fast_solve(f.ranks, f.red_ranks, f.fparams, c["s"], c["mu"], X, 1e-2, 1e-2, 30, act=pkg.ACT_SIN)
+    np.testing.assert_allclose(r["losses"], want["losses"], rtol=1e-3, atol=0)
+    assert normwise(r["s"], want["s"]) <= 1e-4
 
 
 def test_fine_tune_fp32_c2_shape_tracks_oracle(gpu, oracle):
