@@ -423,7 +423,7 @@ def run_ours(args):
             cpu = {"value": None, "error": str(e)}
 
     solves = None
-    if rank == 0 and not args.no_solves:
+    if rank == 0 and world == 1 and not args.no_solves:  # per-GPU latency figures: N = 1 only
         try:
             solves = solve_loops(pkg, local, world == 1 and not args.no_cpu_baseline)
         except Exception as e:  # reported, never fatal
@@ -442,6 +442,7 @@ def run_ours(args):
         print(json.dumps(line))
     ctx.close()
     if dist is not None:
+        dist.barrier()
         dist.destroy_process_group()
     return 0
 

@@ -317,12 +317,15 @@ struct Tile {
                                                   const T* __restrict__ SY, const T* __restrict__ ST,
                                                   T* __restrict__ wg, int64_t oU, int64_t oV, int64_t ob, int k0,
                                                   int M, int rl_true, int rn_true, int tid) {
+        // thread (kq, jq) owns neurons kq + KQ a and ranks jq + JQ b (a, b < 4): the 8 kq
+        // lanes of a warp read 8 consecutive 16-B jets (all 32 banks, no conflicts)
         constexpr int KQ = KC / 4;
         constexpr int NU = KQ * (RL / 4), NV = KQ * (RN / 4);
         for (int idx = tid; idx < NU + NV; idx += NT) {
             const bool isU = idx < NU;
             const int e = isU ? idx : idx - NU;
             const int kq = e % KQ, jq = e / KQ;
+            const int JQ = (isU ? RL : RN) / 4;
             const T* A = isU ? Gs : Zs;
             const T* B = isU ? SY : ST;
             T acc[4][4], db[4];
@@ -337,8 +340,8 @@ struct Tile {
                 T g[4][4], y[4][4];
 #pragma unroll
                 for (int a = 0; a < 4; ++a) {
-                    ld4(A + p * S::ZS + (kq * 4 + a) * 4, g[a]);
-                    ld4(B + p * S::SS + (jq * 4 + a) * 4, y[a]);
+                    ld4(A + p * S::ZS + (kq + KQ * a) * 4, g[a]);
+                    ld4(B + p * S::SS + (jq + JQ * a) * 4, y[a]);
                 }
 #pragma unroll
                 for (int a = 0; a < 4; ++a) {
@@ -353,11 +356,11 @@ struct Tile {
             const int64_t base = isU ? oU : oV;
 #pragma unroll
             for (int a = 0; a < 4; ++a) {
-                const int k = k0 + kq * 4 + a;
+                const int k = k0 + kq + KQ * a;
                 if (k >= M) continue;
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
-                    const int j = jq * 4 + b;
+                    const int j = jq + JQ * b;
                     if (j < rtrue) wg[base + static_cast<int64_t>(k) * rtrue + j] += acc[a][b];
                 }
                 if (isU && jq == 0) wg[ob + k] += db[a];
