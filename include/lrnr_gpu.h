@@ -246,8 +246,17 @@ int lrnr_gpu_meta_loss_grad(lrnr_gpu_ctx* ctx, const double* mus, double w, doub
  *   + lambda_ortho * sum_l (||U_l^T U_l - I||_F^2 + ||V_l^T V_l - I||_F^2)
  *     (gram_ortho_penalty, autodiff.cpp:322-342; meta_train's grad() term)
  *     -> out_ortho.
- * out_value = interior + sparse + ortho (meta_train's `loss`), out_grad =
+ * plus the meta boundary terms when lrnr_gpu_set_meta_boundary set any -> out_comps[1].
+ * out_value = interior + boundary + sparse + ortho (meta_train's `loss`), out_grad =
  * bg.grad + ro.grad in ParamPacker (BasesBiasesAndHyper) order. */
+/* Meta-mode boundary points (PinnTermEmitter meta branch, training.cpp:307-327):
+ * per instance i, n_ic initial x's (initial_x[i * n_ic + k]) and n_bc periodic
+ * t's (periodic_t[i * n_bc + k]), evaluated with that instance's s = hyper(mu_i)
+ * by the following lrnr_gpu_meta_terms_grad calls (n_inst must match the
+ * interior points' instance count). Weights 1/(n_inst n_ic), 1/(n_inst n_bc)
+ * (safe_inv over the batch, training.cpp:364-366). Pass 0 counts to clear. */
+int lrnr_gpu_set_meta_boundary(lrnr_gpu_ctx* ctx, int64_t n_inst, const double* initial_x, int64_t n_ic,
+                               const double* periodic_t, int64_t n_bc);
 int lrnr_gpu_meta_terms_grad(lrnr_gpu_ctx* ctx, const double* mus, double w, double lambda_sparse, double gamma,
                              double lambda_ortho, double* out_value, double* out_comps, double* out_ortho,
                              double* out_grad);

@@ -140,6 +140,18 @@ public:
         return out;
     }
 
+    // meta_train's initial / periodic terms (meta mode): per instance i, its initial x's
+    // (initial_x[i * n_ic + k]) and periodic t's, evaluated with s = hyper(mu_i) by the
+    // following meta_gradient calls; empty vectors clear them.
+    void set_meta_boundary(std::size_t n_inst, const std::vector<double>& initial_x,
+                           const std::vector<double>& periodic_t) {
+        if (n_inst == 0 || initial_x.size() % n_inst || periodic_t.size() % n_inst)
+            throw std::invalid_argument("set_meta_boundary: points not grouped by instance");
+        check(lrnr_gpu_set_meta_boundary(ctx_, static_cast<int64_t>(n_inst), initial_x.data(),
+                                         static_cast<int64_t>(initial_x.size() / n_inst), periodic_t.data(),
+                                         static_cast<int64_t>(periodic_t.size() / n_inst)));
+    }
+
     // meta_train's step (training.cpp:368-389): interior terms + lambda_sparse
     // banded decay per term (comps[2]) + the lambda_ortho Gram term (returned in
     // *ortho, as meta_train's `ro`); value = bg.value + ro.value, grad = bg + ro.

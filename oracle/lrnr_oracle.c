@@ -834,8 +834,8 @@ static const double* any_fwd(const any_net* a, const double* s, double x, double
 }
 
 /* gA: scratch of g_len doubles whose first 4 entries are the output-jet seed */
-static void any_bwd(const any_net* a, const double* s, double* ws, double* gA, double* ds) {
-    if (a->kind == 0) lr_backward(&a->lr, s, ws, gA, ds, NULL);
+static void any_bwd(const any_net* a, const double* s, double* ws, double* gA, double* ds, double* dP) {
+    if (a->kind == 0) lr_backward(&a->lr, s, ws, gA, ds, dP);
     else fa_backward(&a->fa, s, ws, gA, ds);
 }
 
@@ -845,8 +845,10 @@ int orc_terms_grad(int model, int L, const int64_t* w, const int64_t* r, const i
                    int act, const double* s, const double* mu, const double* pts, int64_t n_int,
                    const double* ic_x, int64_t n_ic, const double* per_t, int64_t n_bc, double w_int,
                    double w_ic, double w_bc, int objective, const double* s_init, double lambda_local,
-                   int64_t chunk, double* out_value, double* out_comps, double* out_grad_s) {
+                   int64_t chunk, double* out_value, double* out_comps, double* out_grad_s,
+                   double* out_grad_params) {
     if (L < 1 || L > ORC_MAXL || chunk < 1 || (objective != 0 && objective != 1)) return 1;
+    if (out_grad_params && model != 0) return 1;
     any_net a;
     memset(&a, 0, sizeof(a));
     a.kind = model;
@@ -866,7 +868,8 @@ int orc_terms_grad(int model, int L, const int64_t* w, const int64_t* r, const i
     const int has_local = s_init != NULL && lambda_local > 0.0;
     const int64_t n_terms = n_int + n_ic + n_bc + (has_local ? 1 : 0);
     const int64_t n_chunks = (n_terms + chunk - 1) / chunk;
-    const int64_t G = a.r_total, stride = 5 + G; /* value, comps[4], grad */
+    const int64_t G = a.r_total, GP = out_grad_params ? a.lr.n_params : 0;
+    const int64_t stride = 5 + G + GP; /* value, comps[4], grad_s, grad_params */
     double* part = (double*)calloc((size_t)(n_chunks > 0 ? n_chunks : 1) * (size_t)stride, sizeof(double));
     int bad = 0;
 #pragma omp parallel
@@ -895,7 +898,7 @@ int orc_terms_grad(int model, int L, const int64_t* w, const int64_t* r, const i
                         gN = sgn0(N) * w_int;
                     }
                     cdr_vjp(u, mu, gN, g0);
-                    any_bwd(&a, s, ws0, g0, pc + 5);
+                    any_bwd(&a, s, ws0, g0, pc + 5, GP ? pc + 5 + G : NULL);
                     comp = 0;
                 } else if (idx < n_int + n_ic) {
                     const double x = ic_x[idx - n_int];
@@ -908,7 +911,7 @@ int orc_terms_grad(int model, int L, const int64_t* w, const int64_t* r, const i
                         term = w_ic * fabs(d);
                         g0[0] = sgn0(d) * w_ic;
                     }
-                    any_bwd(&a, s, ws0, g0, pc + 5);
+                    any_bwd(&a, s, ws0, g0, pc + 5, GP ? pc + 5 + G : NULL);
                     comp = 1;
                 } else if (idx < n_int + n_ic + n_bc) {
                     const double t = per_t[idx - n_int - n_ic];
@@ -925,8 +928,8 @@ int orc_terms_grad(int model, int L, const int64_t* w, const int64_t* r, const i
                     }
                     g0[0] = gd;
                     g1[0] = -gd;
-                    any_bwd(&a, s, ws0, g0, pc + 5);
-                    any_bwd(&a, s, ws1, g1, pc + 5);
+                    any_bwd(&a, s, ws0, g0, pc + 5, GP ? pc + 5 + G : NULL);
+                    any_bwd(&a, s, ws1, g1, pc + 5, GP ? pc + 5 + G : NULL);
                     comp = 1;
                 } else {
                     term = 0.0;
@@ -951,12 +954,13 @@ int orc_terms_grad(int model, int L, const int64_t* w, const int64_t* r, const i
         free(g0);
         free(g1);
     }
-    for (int64_t k = 0; k < 5 + G; ++k) {
+    for (int64_t k = 0; k < 5 + G + GP; ++k) {
         double acc = 0.0;
         for (int64_t c = 0; c < n_chunks; ++c) acc += part[c * stride + k];
         if (k == 0) *out_value = acc;
         else if (k < 5) out_comps[k - 1] = acc;
-        else out_grad_s[k - 5] = acc;
+        else if (k < 5 + G) out_grad_s[k - 5] = acc;
+        else out_grad_params[k - 5 - G] = acc;
     }
     free(part);
     return bad ? 2 : 0;
@@ -1441,11 +1445,11 @@ static int solve_loop(int model, int L, const int64_t* w, const int64_t* r, cons
                                    NULL);
             st = orc_terms_grad(model, L, w, r, rh, P, act, x, mu, pint, n_int, pic, n_ic, pper, n_bc,
                                 n_int ? 1.0 / (double)n_int : 0.0, n_ic ? 1.0 / (double)n_ic : 0.0,
-                                n_bc ? 1.0 / (double)n_bc : 0.0, 0, NULL, 0.0, chunk, &value, comps, g);
+                                n_bc ? 1.0 / (double)n_bc : 0.0, 0, NULL, 0.0, chunk, &value, comps, g, NULL);
         } else {
             st = orc_terms_grad(model, L, w, r, rh, P, act, x, mu, fx_int, fn_int, fx_ic, fn_ic, fx_bc, fn_bc, 1.0,
                                 1.0, 1.0, 1, lambda_local > 0.0 ? s_init : NULL, lambda_local, chunk, &value, comps,
-                                g);
+                                g, NULL);
         }
         if (st == 1) {
             rc = 1;

@@ -168,7 +168,7 @@ class Oracle:
         return out
 
     def terms_grad(self, model, dims, P, s, mu, pts=(), ic_x=(), per_t=(), w_int=None, w_ic=None, w_bc=None,
-                   objective=0, s_init=None, lambda_local=0.0, act=0, chunk=64):
+                   objective=0, s_init=None, lambda_local=0.0, act=0, chunk=64, params_grad=False):
         """Full solve-step term set (orc_terms_grad): model 0 = LRNR with dims = (widths, ranks),
         1 = FastLRNR with dims = (ranks, red_ranks); weights default to 1/n of each kind
         (training.cpp:364-366); objective 0 = squared, 1 = abs."""
@@ -188,15 +188,19 @@ class Oracle:
         comps = np.zeros(4)
         val = C.c_double(0.0)
         si = None if s_init is None else _f64(s_init)
+        gp = np.zeros(lrnr_param_count(dims[0], dims[1])) if params_grad else None
         rc = self.lib.orc_terms_grad(C.c_int(model), C.c_int(L), _ptr(wv), _ptr(rv), _ptr(rh), _ptr(_f64(P)),
                                      C.c_int(act), _ptr(_f64(s)), _ptr(_f64(mu)), _ptr(pts), C.c_int64(pts.shape[0]),
                                      _ptr(icx), C.c_int64(icx.shape[0]), _ptr(pt), C.c_int64(pt.shape[0]),
                                      C.c_double(w_int), C.c_double(w_ic), C.c_double(w_bc), C.c_int(objective),
                                      _ptr(si), C.c_double(lambda_local), C.c_int64(chunk), C.byref(val),
-                                     _ptr(comps), _ptr(gs))
+                                     _ptr(comps), _ptr(gs), _ptr(gp))
         if rc == 1:
             raise OracleError("orc_terms_grad: invalid arguments")
-        return dict(value=val.value, comps=comps, grad_s=gs, nonfinite=(rc == 2))
+        out = dict(value=val.value, comps=comps, grad_s=gs, nonfinite=(rc == 2))
+        if params_grad:
+            out["grad_params"] = gp
+        return out
 
     def meta_regs(self, widths, ranks, P, s_inst, n_per, w, lambda_sparse, gamma, lambda_ortho):
         """meta_train's regularizers for points grouped by instance (s_inst: n_inst x r_total):
@@ -510,6 +514,24 @@ class Reference:
                                         _ptr(_f64(mus).reshape(-1)), C.c_int64(n), C.c_double(w), C.c_int(threads),
                                         C.c_int(chunk), C.byref(val), _ptr(out)), "meta_grad")
         return dict(value=val.value, grad=out)
+
+    def meta_grad_full(self, widths, ranks, P, hw, H, lo, hi, pts, mus, ic_x, ic_mu, per_t, per_mu, lambda_sparse,
+                       gamma, lambda_ortho, threads=1, chunk=64):
+        """meta_train's full emitter: interior (+ sparse), initial, periodic (per-point mu), + ortho."""
+        wv, rv, hwv = _i64(widths), _i64(ranks), _i64(hw)
+        pts = _f64(pts).reshape(-1, 2)
+        out = np.zeros(lrnr_param_count(wv, rv) + hyper_param_count(hwv))
+        comps = np.zeros(4)
+        val, ortho = C.c_double(0.0), C.c_double(0.0)
+        icx, pt = _f64(ic_x).reshape(-1), _f64(per_t).reshape(-1)
+        self._rc(self.lib.ref_meta_grad_full(
+            C.c_int(len(rv)), _ptr(wv), _ptr(rv), _ptr(_f64(P)), C.c_int(len(hwv) - 1), _ptr(hwv), _ptr(_f64(H)),
+            _ptr(_f64(lo)), _ptr(_f64(hi)), _ptr(pts), _ptr(_f64(mus).reshape(-1)), C.c_int64(pts.shape[0]),
+            _ptr(icx), _ptr(_f64(ic_mu).reshape(-1)), C.c_int64(icx.shape[0]), _ptr(pt),
+            _ptr(_f64(per_mu).reshape(-1)), C.c_int64(pt.shape[0]), C.c_double(lambda_sparse), C.c_double(gamma),
+            C.c_double(lambda_ortho), C.c_int(threads), C.c_int(chunk), C.byref(val), _ptr(comps), C.byref(ortho),
+            _ptr(out)), "meta_grad_full")
+        return dict(value=val.value, comps=comps, ortho=ortho.value, grad=out)
 
     def meta_grad_reg(self, widths, ranks, P, hw, H, lo, hi, pts, mus, lambda_sparse, gamma, lambda_ortho, w=None,
                       threads=1, chunk=64):

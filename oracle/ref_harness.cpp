@@ -713,6 +713,86 @@ int ref_l1_error(int L, const int64_t* widths, const int64_t* ranks, const doubl
     });
 }
 
+// meta_train's full PinnTermEmitter (meta mode, training.cpp:283-327): interior terms
+// (+ lambda_sparse banded decay), initial and periodic terms, each point with its
+// own mu through the hypernetwork, weights 1/n per kind; plus the ortho grad().
+int ref_meta_grad_full(int L, const int64_t* widths, const int64_t* ranks, const double* params, int K,
+                       const int64_t* hw, const double* hparams, const double* lo, const double* hi,
+                       const double* pts, const double* mus, int64_t n, const double* ic_x, const double* ic_mu,
+                       int64_t n_ic, const double* per_t, const double* per_mu, int64_t n_bc, double lambda_sparse,
+                       double gamma, double lambda_ortho, int threads, int chunk, double* out_value,
+                       double* out_comps, double* out_ortho, double* out_grad) {
+    return guarded([&] {
+        LrnrParams p = unpack_lrnr(L, widths, ranks, params);
+        HyperParams h = unpack_hyper(K, hw, hparams, L, ranks, lo, hi);
+        Trainables at{&p, &h, nullptr};
+        const double wi = n ? 1.0 / static_cast<double>(n) : 0.0;
+        const double wc = n_ic ? 1.0 / static_cast<double>(n_ic) : 0.0;
+        const double wb = n_bc ? 1.0 / static_cast<double>(n_bc) : 0.0;
+        training::EmitFn emit = [&](TapeBindings& ctx, const training::ExtraBindings&, std::size_t idx,
+                                    double* comps) -> NodeId {
+            Tape& tp = ctx.tape;
+            const std::size_t ni = static_cast<std::size_t>(n), nc = static_cast<std::size_t>(n_ic);
+            if (idx < ni) {
+                const PdeParams m = mu_of(mus + 3 * idx);
+                const std::vector<NodeId> s_nodes = emit_hyper(tp, m, ctx.hyper);
+                const NodeId jet = emit_lrnr_jet(tp, pts[2 * idx], pts[2 * idx + 1], ctx.lrnr, s_nodes);
+                const NodeId term = tp.scale(tp.square(tp.residual_cdr(jet, m)), wi);
+                comps[0] += tp.value(term);
+                if (lambda_sparse > 0.0) {
+                    std::vector<NodeId> ids{term};
+                    std::vector<double> ws{1.0};
+                    for (const NodeId sn : s_nodes) {
+                        ids.push_back(tp.banded_decay_penalty(sn, gamma));
+                        ws.push_back(lambda_sparse * wi);
+                    }
+                    const NodeId tot = tp.weighted_sum(ids, ws);
+                    comps[2] += tp.value(tot) - tp.value(term);
+                    return tot;
+                }
+                return term;
+            }
+            if (idx < ni + nc) {
+                const std::size_t j = idx - ni;
+                const std::vector<NodeId> s_nodes = emit_hyper(tp, mu_of(ic_mu + 3 * j), ctx.hyper);
+                const double x = ic_x[j];
+                const NodeId jet = emit_lrnr_jet(tp, x, 0.0, ctx.lrnr, s_nodes);
+                const NodeId term = tp.scale(tp.square(tp.sub_const(tp.pick_value(jet, 0), std::sin(x))), wc);
+                comps[1] += tp.value(term);
+                return term;
+            }
+            const std::size_t j = idx - ni - nc;
+            const std::vector<NodeId> s_nodes = emit_hyper(tp, mu_of(per_mu + 3 * j), ctx.hyper);
+            const double t = per_t[j];
+            const NodeId j0 = emit_lrnr_jet(tp, 0.0, t, ctx.lrnr, s_nodes);
+            const NodeId j1 = emit_lrnr_jet(tp, pde::kTwoPi, t, ctx.lrnr, s_nodes);
+            const NodeId term = tp.scale(tp.square(tp.sub(tp.pick_value(j0, 0), tp.pick_value(j1, 0))), wb);
+            comps[1] += tp.value(term);
+            return term;
+        };
+        training::BatchGradResult bg = training::run_batch_gradient(
+            at, ParamSelector::BasesBiasesAndHyper, nullptr, emit, static_cast<std::size_t>(n + n_ic + n_bc),
+            par_of(threads, chunk));
+        GradResult ro = grad(
+            [&](TapeBindings& ctx) {
+                std::vector<NodeId> ids;
+                std::vector<double> ws;
+                for (std::size_t l = 0; l < ctx.at.lrnr->depth(); ++l) {
+                    ids.push_back(ctx.tape.gram_ortho_penalty(ctx.lrnr.u_slots[l]));
+                    ws.push_back(lambda_ortho);
+                    ids.push_back(ctx.tape.gram_ortho_penalty(ctx.lrnr.v_slots[l]));
+                    ws.push_back(lambda_ortho);
+                }
+                return ctx.tape.weighted_sum(ids, ws);
+            },
+            at, ParamSelector::BasesBiasesAndHyper);
+        *out_value = bg.value + ro.value;
+        for (int k = 0; k < 4; ++k) out_comps[k] = bg.comps[k];
+        *out_ortho = ro.value;
+        for (std::size_t i = 0; i < bg.grad.size(); ++i) out_grad[i] = bg.grad[i] + ro.grad[i];
+    });
+}
+
 // ---- FastLRNR construction (reduction.cpp:10-31,111-283) ----
 // Constant hypernetwork (zero W, bias = s) so hyper_forward(mu) == s.
 int ref_build_fast(int L, const int64_t* widths, const int64_t* ranks, const double* params,

@@ -16,7 +16,7 @@ EXPORTS = (
     "lrnr_gpu_create", "lrnr_gpu_destroy", "lrnr_gpu_last_error", "lrnr_gpu_last_layer_tag",
     "lrnr_gpu_set_stream", "lrnr_gpu_set_option", "lrnr_gpu_launch_count", "lrnr_gpu_set_lrnr", "lrnr_gpu_set_fast",
     "lrnr_gpu_set_hyper", "lrnr_gpu_set_points", "lrnr_gpu_set_points_device", "lrnr_gpu_loss_grad_s",
-    "lrnr_gpu_set_boundary", "lrnr_gpu_terms_grad", "lrnr_gpu_meta_terms_grad", "lrnr_gpu_fine_tune",
+    "lrnr_gpu_set_boundary", "lrnr_gpu_terms_grad", "lrnr_gpu_meta_terms_grad", "lrnr_gpu_set_meta_boundary", "lrnr_gpu_fine_tune",
     "lrnr_gpu_fast_solve", "lrnr_host_epoch_seed", "lrnr_host_sample_batch", "lrnr_gpu_l1_error",
     "lrnr_ckpt_last_error", "lrnr_ckpt_create", "lrnr_ckpt_load", "lrnr_ckpt_save", "lrnr_ckpt_free",
     "lrnr_ckpt_get_lrnr", "lrnr_ckpt_put_lrnr", "lrnr_ckpt_get_hyper", "lrnr_ckpt_put_hyper", "lrnr_ckpt_has_fast",
@@ -91,6 +91,7 @@ def load() -> C.CDLL:
     lib.lrnr_gpu_loss_grad_s_multi.argtypes = [vp, ip, dp, dp, C.c_double, dp, dp]
     lib.lrnr_gpu_hyper_loss_grad.argtypes = [vp, ip, dp, C.c_double, dp, dp, dp]
     lib.lrnr_gpu_meta_loss_grad.argtypes = [vp, dp, C.c_double, dp, dp]
+    lib.lrnr_gpu_set_meta_boundary.argtypes = [vp, i64, dp, i64, dp, i64]
     lib.lrnr_gpu_meta_terms_grad.argtypes = [vp, dp, C.c_double, C.c_double, C.c_double, C.c_double, dp, dp, dp, dp]
     lib.lrnr_gpu_jets.argtypes = [vp, ip, dp, dp]
     lib.lrnr_gpu_loss.argtypes = [vp, ip, dp, dp, C.c_double, dp]

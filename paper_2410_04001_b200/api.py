@@ -306,6 +306,14 @@ class GpuContext:
                  "meta_loss_grad")
         return dict(value=v.value, grad=g)
 
+    def set_meta_boundary(self, n_inst, initial_x=(), periodic_t=()):
+        """Meta boundary points per instance: initial_x (n_inst x n_ic), periodic_t (n_inst x n_bc)."""
+        ic = _f64(initial_x).reshape(n_inst, -1) if len(initial_x) else np.zeros((n_inst, 0))
+        pt = _f64(periodic_t).reshape(n_inst, -1) if len(periodic_t) else np.zeros((n_inst, 0))
+        ic, pt = np.ascontiguousarray(ic), np.ascontiguousarray(pt)
+        self._rc(self.lib.lrnr_gpu_set_meta_boundary(self.h, n_inst, _p(ic), ic.shape[1], _p(pt), pt.shape[1]),
+                 "set_meta_boundary")
+
     def meta_terms_grad(self, mus, n_lrnr_params, lambda_sparse=0.0, gamma=1.5, lambda_ortho=0.0, w=0.0):
         """meta_train's step: interior terms + sparse (banded decay) + ortho (Gram) regularizers."""
         g = np.zeros(n_lrnr_params + self.hyper_n)

@@ -160,6 +160,10 @@ struct lrnr_gpu_ctx {
     // nullptr + objective 0 = the interior squared residual
     const lrnr_b200::TermSpec* term_spec = nullptr;
     int term_objective = 0;
+    int accumulate_wg = 0;  // META factor-gradient reduction adds onto its output (boundary pass)
+    // meta boundary points, grouped by instance: [inst][initial (x, 0) | periodic pairs]
+    lrnr_b200::detail::DevBuf mb_pts, mb_sinx, mb_rows, mb_sum;
+    int64_t mb_ic = 0, mb_bc = 0, mb_inst = 0;
     // boundary points (lrnr_gpu_set_boundary): [initial (x, 0)] [periodic (0, t), (2pi, t)] pairs
     lrnr_b200::detail::DevBuf bnd_pts, bnd_x, bnd_spec, bnd_jets;
     int64_t n_ic = 0, n_bc = 0;
@@ -347,11 +351,12 @@ void launch_v2(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
     }
     kern<<<grid, NT, smem, ctx->stream>>>(net, g, ctx->pts, s_dev, mu_dev, static_cast<T>(w),
                                                ctx->scratch.as<T>(), ctx->part.as<T>(),
-                                               ctx->bad.as<unsigned long long>(), ctx->ascratch.as<T>(), wg);
+                                               ctx->bad.as<unsigned long long>(), ctx->ascratch.as<T>(), wg,
+                                               ctx->term_spec, ctx->term_objective);
     CK(cudaGetLastError());
     if (META) {
         reduce_rows_kernel<T><<<static_cast<unsigned>((n_params + 255) / 256), 256, 0, ctx->stream>>>(
-            wg, grid, net.wg_stride, n_params, wg_out);
+            wg, grid, net.wg_stride, n_params, wg_out, ctx->accumulate_wg);
         CK(cudaGetLastError());
         ctx->launches += 1;
     }

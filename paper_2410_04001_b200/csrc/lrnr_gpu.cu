@@ -569,6 +569,30 @@ __global__ void boundary_spec_kernel(const double* __restrict__ jets, const doub
     }
 }
 
+// The same for boundary points grouped by instance (meta mode: each instance's
+// points use its own s = hyper(mu_i)): nb = n_ic + 2 n_bc points per instance.
+__global__ void boundary_spec_multi_kernel(const double* __restrict__ jets, const double* __restrict__ sin_x,
+                                           int64_t n_inst, int64_t n_ic, int64_t n_bc, double w_ic, double w_bc,
+                                           TermSpec* __restrict__ spec) {
+    const int64_t nb = n_ic + 2 * n_bc;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n_inst * nb) return;
+    const int64_t inst = i / nb, loc = i % nb, base = inst * nb;
+    if (loc < n_ic) {
+        spec[i] = TermSpec{sin_x[inst * n_ic + loc], w_ic, w_ic, 2, 0};
+    } else {
+        const int64_t j = loc - n_ic, first = base + n_ic + (j & ~int64_t(1));
+        if ((j & 1) == 0) spec[i] = TermSpec{jets[4 * (first + 1)], w_bc, w_bc, 2, 0};
+        else spec[i] = TermSpec{jets[4 * first], 0.0, w_bc, 2, 0};
+    }
+}
+
+__global__ void add_rows_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
+                                double* __restrict__ c) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) c[i] = a[i] + b[i];
+}
+
 // Temporarily point the context's point set at another device array (one instance).
 struct PointSwap {
     lrnr_gpu_ctx* ctx;
@@ -883,7 +907,8 @@ __global__ void gram_grad_kernel(const double* __restrict__ A, int rows, int r, 
 
 struct MetaReg {
     double lambda_sparse = 0.0, gamma = 1.5, lambda_ortho = 0.0;
-    double sparse = 0.0, ortho = 0.0;  // outputs
+    bool boundary = false;  // include the meta boundary points (lrnr_gpu_set_meta_boundary)
+    double sparse = 0.0, ortho = 0.0, boundary_value = 0.0;  // outputs
 };
 
 // Meta step: per-instance s from the hypernetwork (already in ctx->s_dev),
@@ -908,17 +933,64 @@ void meta_step(lrnr_gpu_ctx* ctx, Model& m, double w, double* out_grad, double* 
     if (ctx->n_per == 0) {
         CK(cudaMemsetAsync(rows, 0, static_cast<size_t>(ctx->n_inst * R1) * sizeof(double), ctx->stream));
         CK(cudaMemsetAsync(gout, 0, static_cast<size_t>(n_lrnr) * sizeof(double), ctx->stream));
-    } else {
-        const double* sd = ctx->s_dev.as<double>();
-        const double* md = ctx->mu_dev.as<double>();
+    }
+    const double* sd = ctx->s_dev.as<double>();
+    const double* md = ctx->mu_dev.as<double>();
+    auto launch_meta = [&](double wt, double* rows_out) {
         const int RP = v.RPMAX;
-        if (m.dtype == LRNR_F32 && m.act == LRNR_ACT_SIN && RP == 64) launch_v2<float, 32, 1, 8, 64, 1, false, true>(ctx, m, sd, md, w, rows, gout);
-        else if (m.dtype == LRNR_F32 && m.act == LRNR_ACT_SIN && RP == 32) launch_v2<float, 32, 1, 8, 32, 1, false, true>(ctx, m, sd, md, w, rows, gout);
-        else if (m.dtype == LRNR_F32 && m.act == LRNR_ACT_TANH && RP == 64) launch_v2<float, 32, 1, 8, 64, 0, false, true>(ctx, m, sd, md, w, rows, gout);
-        else if (m.dtype == LRNR_F32 && m.act == LRNR_ACT_TANH && RP == 32) launch_v2<float, 32, 1, 8, 32, 0, false, true>(ctx, m, sd, md, w, rows, gout);
-        else if (m.dtype == LRNR_F64 && m.act == LRNR_ACT_TANH && RP == 32) launch_v2<double, 32, 1, 8, 32, 0, false, true>(ctx, m, sd, md, w, rows, gout);
-        else if (m.dtype == LRNR_F64 && m.act == LRNR_ACT_SIN && RP == 32) launch_v2<double, 32, 1, 8, 32, 1, false, true>(ctx, m, sd, md, w, rows, gout);
+        if (m.dtype == LRNR_F32 && m.act == LRNR_ACT_SIN && RP == 64) launch_v2<float, 32, 1, 8, 64, 1, false, true>(ctx, m, sd, md, wt, rows_out, gout);
+        else if (m.dtype == LRNR_F32 && m.act == LRNR_ACT_SIN && RP == 32) launch_v2<float, 32, 1, 8, 32, 1, false, true>(ctx, m, sd, md, wt, rows_out, gout);
+        else if (m.dtype == LRNR_F32 && m.act == LRNR_ACT_TANH && RP == 64) launch_v2<float, 32, 1, 8, 64, 0, false, true>(ctx, m, sd, md, wt, rows_out, gout);
+        else if (m.dtype == LRNR_F32 && m.act == LRNR_ACT_TANH && RP == 32) launch_v2<float, 32, 1, 8, 32, 0, false, true>(ctx, m, sd, md, wt, rows_out, gout);
+        else if (m.dtype == LRNR_F64 && m.act == LRNR_ACT_TANH && RP == 32) launch_v2<double, 32, 1, 8, 32, 0, false, true>(ctx, m, sd, md, wt, rows_out, gout);
+        else if (m.dtype == LRNR_F64 && m.act == LRNR_ACT_SIN && RP == 32) launch_v2<double, 32, 1, 8, 32, 1, false, true>(ctx, m, sd, md, wt, rows_out, gout);
         else throw InvalidArg("meta path: unsupported dtype / rank combination");
+    };
+    if (ctx->n_per > 0) launch_meta(w, rows);
+    // boundary terms (PinnTermEmitter meta mode, training.cpp:307-327): a forward pass for u,
+    // per-point specs, then the seeded META pass adding its factor gradients onto gout
+    double* hrows = rows;  // the per-instance dL/ds rows the hypernetwork backward consumes
+    const int64_t nbp = ctx->mb_ic + 2 * ctx->mb_bc;
+    const bool with_bnd = reg && reg->boundary && nbp > 0;
+    if (with_bnd) {
+        require(ctx->mb_inst == ctx->n_inst, "meta boundary points were set for another instance count");
+        const int64_t n_inst = ctx->n_inst, nb_all = n_inst * nbp;
+        ctx->mb_rows.ensure(static_cast<size_t>(n_inst * R1) * sizeof(double));
+        ctx->mb_sum.ensure(static_cast<size_t>(n_inst * R1) * sizeof(double));
+        ctx->bnd_jets.ensure(static_cast<size_t>(4 * nb_all) * sizeof(double) + 16);
+        ctx->bnd_spec.ensure(static_cast<size_t>(nb_all) * sizeof(TermSpec) + 16);
+        const double* save_pts = ctx->pts;
+        const int64_t save_per = ctx->n_per;
+        ctx->pts = ctx->mb_pts.as<double>();
+        ctx->n_per = nbp;
+        try {
+            dispatch_small<1>(ctx, m, sd, md, 1.0, ctx->mb_rows.as<double>(), ctx->bnd_jets.as<double>());
+            const double wc = ctx->mb_ic ? 1.0 / static_cast<double>(n_inst * ctx->mb_ic) : 0.0;
+            const double wb = ctx->mb_bc ? 1.0 / static_cast<double>(n_inst * ctx->mb_bc) : 0.0;
+            boundary_spec_multi_kernel<<<static_cast<unsigned>((nb_all + 127) / 128), 128, 0, ctx->stream>>>(
+                ctx->bnd_jets.as<double>(), ctx->mb_sinx.as<double>(), n_inst, ctx->mb_ic, ctx->mb_bc, wc, wb,
+                ctx->bnd_spec.as<TermSpec>());
+            CK(cudaGetLastError());
+            ++ctx->launches;
+            ctx->term_spec = ctx->bnd_spec.as<TermSpec>();
+            ctx->accumulate_wg = ctx->n_per > 0 && save_per > 0 ? 1 : 0;
+            launch_meta(1.0, ctx->mb_rows.as<double>());
+        } catch (...) {
+            ctx->pts = save_pts;
+            ctx->n_per = save_per;
+            ctx->term_spec = nullptr;
+            ctx->accumulate_wg = 0;
+            throw;
+        }
+        ctx->pts = save_pts;
+        ctx->n_per = save_per;
+        ctx->term_spec = nullptr;
+        ctx->accumulate_wg = 0;
+        hrows = ctx->mb_sum.as<double>();
+        add_rows_kernel<<<static_cast<unsigned>((n_inst * R1 + 255) / 256), 256, 0, ctx->stream>>>(
+            rows, ctx->mb_rows.as<double>(), n_inst * R1, hrows);
+        CK(cudaGetLastError());
+        ++ctx->launches;
     }
     const double c_sparse = reg ? reg->lambda_sparse * w * static_cast<double>(ctx->n_per) : 0.0;
     if (c_sparse > 0.0) {
@@ -927,11 +999,11 @@ void meta_step(lrnr_gpu_ctx* ctx, Model& m, double w, double* out_grad, double* 
         for (int l = 0; l <= m.L; ++l) lay.off[l] = m.soff[l];
         ctx->meta_ws.ensure(static_cast<size_t>(ctx->n_inst) * sizeof(double) + 8);
         banded_decay_kernel<<<static_cast<unsigned>((ctx->n_inst + 127) / 128), 128, 0, ctx->stream>>>(
-            ctx->s_dev.as<double>(), ctx->n_inst, m.rtotal, lay, reg->gamma, c_sparse, rows, R1, ctx->meta_ws.as<double>());
+            ctx->s_dev.as<double>(), ctx->n_inst, m.rtotal, lay, reg->gamma, c_sparse, hrows, R1, ctx->meta_ws.as<double>());
         CK(cudaGetLastError());
         ++ctx->launches;
     }
-    hyper_backward_resident(ctx, rows, R1, gout + n_lrnr);
+    hyper_backward_resident(ctx, hrows, R1, gout + n_lrnr);
     std::vector<double> gram_e;
     std::vector<std::pair<int, int>> gram_shape;
     if (reg && reg->lambda_ortho > 0.0) {
@@ -972,6 +1044,12 @@ void meta_step(lrnr_gpu_ctx* ctx, Model& m, double w, double* out_grad, double* 
     double val = 0.0;
     for (int64_t i = 0; i < ctx->n_inst; ++i) val += h[static_cast<size_t>(i * R1)];
     *out_value = val;
+    if (with_bnd) {
+        download(ctx, ctx->mb_rows.as<double>(), h.data(), h.size());
+        double bv = 0.0;
+        for (int64_t i = 0; i < ctx->n_inst; ++i) bv += h[static_cast<size_t>(i * R1)];
+        reg->boundary_value = bv;
+    }
     if (c_sparse > 0.0) {
         std::vector<double> pen(static_cast<size_t>(ctx->n_inst));
         download(ctx, ctx->meta_ws.as<double>(), pen.data(), pen.size());
@@ -1784,6 +1862,43 @@ int lrnr_gpu_meta_loss_grad(lrnr_gpu_ctx* ctx, const double* mus, double w, doub
     });
 }
 
+int lrnr_gpu_set_meta_boundary(lrnr_gpu_ctx* ctx, int64_t n_inst, const double* initial_x, int64_t n_ic,
+                               const double* periodic_t, int64_t n_bc) {
+    return guarded(ctx, [&] {
+        require(n_inst >= 0 && n_ic >= 0 && n_bc >= 0, "bad boundary counts");
+        require((initial_x || n_ic == 0) && (periodic_t || n_bc == 0), "null boundary points");
+        const int64_t nb = n_ic + 2 * n_bc;
+        std::vector<double> xt(static_cast<size_t>(2 * nb * n_inst)), sx(static_cast<size_t>(n_ic * n_inst));
+        for (int64_t q = 0; q < n_inst; ++q) {
+            double* p = xt.data() + 2 * nb * q;
+            for (int64_t i = 0; i < n_ic; ++i) {
+                const double x = initial_x[q * n_ic + i];
+                p[2 * i] = x;
+                p[2 * i + 1] = 0.0;
+                sx[static_cast<size_t>(q * n_ic + i)] = std::sin(x);
+            }
+            for (int64_t j = 0; j < n_bc; ++j) {
+                const double t = periodic_t[q * n_bc + j];
+                double* r = p + 2 * (n_ic + 2 * j);
+                r[0] = 0.0;
+                r[1] = t;
+                r[2] = kTwoPi;
+                r[3] = t;
+            }
+        }
+        ctx->mb_pts.ensure(xt.size() * sizeof(double) + 16);
+        ctx->mb_sinx.ensure(sx.size() * sizeof(double) + 16);
+        if (!xt.empty()) CK(cudaMemcpyAsync(ctx->mb_pts.p, xt.data(), xt.size() * sizeof(double),
+                                            cudaMemcpyHostToDevice, ctx->stream));
+        if (!sx.empty()) CK(cudaMemcpyAsync(ctx->mb_sinx.p, sx.data(), sx.size() * sizeof(double),
+                                            cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->mb_inst = n_inst;
+        ctx->mb_ic = n_ic;
+        ctx->mb_bc = n_bc;
+    });
+}
+
 int lrnr_gpu_meta_terms_grad(lrnr_gpu_ctx* ctx, const double* mus, double w, double lambda_sparse, double gamma,
                              double lambda_ortho, double* out_value, double* out_comps4, double* out_ortho,
                              double* out_grad) {
@@ -1803,17 +1918,18 @@ int lrnr_gpu_meta_terms_grad(lrnr_gpu_ctx* ctx, const double* mus, double w, dou
         reg.lambda_sparse = lambda_sparse;
         reg.gamma = gamma;
         reg.lambda_ortho = lambda_ortho;
+        reg.boundary = true;
         double interior = 0.0;
         meta_step(ctx, m, wt, out_grad, &interior, &reg);
         if (!std::isfinite(reg.sparse) || !std::isfinite(reg.ortho)) throw NonFinite(-1);
         if (out_comps4) {
             out_comps4[0] = interior;
-            out_comps4[1] = 0.0;
+            out_comps4[1] = reg.boundary_value;
             out_comps4[2] = reg.sparse;
             out_comps4[3] = 0.0;
         }
         if (out_ortho) *out_ortho = reg.ortho;
-        if (out_value) *out_value = interior + reg.sparse + reg.ortho;
+        if (out_value) *out_value = interior + reg.boundary_value + reg.sparse + reg.ortho;
     });
 }
 

@@ -501,12 +501,12 @@ __global__ void reduce_units_kernel(const T* __restrict__ part, int units_per_in
 // out[i] = sum_r rows[r][i] in double, rows in fixed order (per-CTA partials).
 template <typename T>
 __global__ void reduce_rows_kernel(const T* __restrict__ rows, int n_rows, int64_t stride, int64_t n,
-                                   double* __restrict__ out) {
+                                   double* __restrict__ out, int accumulate = 0) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double s = 0.0;
     for (int r = 0; r < n_rows; ++r) s += double(rows[r * stride + i]);
-    out[i] = s;
+    out[i] = accumulate ? out[i] + s : s;
 }
 
 }  // namespace lrnr_b200

@@ -405,7 +405,8 @@ __global__ void __launch_bounds__(JG * P, (META ? 1 : tile_min_blocks<T, P>()))
 pinn_tile_kernel(const NetV2<T> net, const RunGeom g, const double* __restrict__ pts,
                  const double* __restrict__ svec, const double* __restrict__ mus, const T w,
                  T* __restrict__ scratch, T* __restrict__ part, unsigned long long* __restrict__ bad,
-                 T* __restrict__ ascratch, T* __restrict__ wgrad = nullptr) {
+                 T* __restrict__ ascratch, T* __restrict__ wgrad = nullptr,
+                 const TermSpec* __restrict__ spec = nullptr, const int objective = 0) {
     using K = Tile<T, P, PT1, NG, RPMAX, ACT, FAST, META>;
     using S = typename K::S;
     constexpr int NT = K::NT;
@@ -584,10 +585,32 @@ pinn_tile_kernel(const NetV2<T> net, const RunGeom g, const double* __restrict__
                     }
                     u[0] += net.ulast[rL];
                     const T N = u[2] + mu0 * u[1] - mu1 * u[3] - mu2 * u[0] * (T(1) - u[0]);
-                    const T term = valid ? w * (N * N) : T(0);
+                    // per-point term kind (TermSpec, pinn_kernels.cuh): interior w N^2 / w |N|,
+                    // value terms w (u - c)^2 / w |u - c| (boundary terms)
+                    int kind = objective;
+                    T tw = w, sw = w, tgt = T(0);
+                    if (spec != nullptr && valid) {
+                        const TermSpec sp = spec[gp];
+                        kind = sp.kind;
+                        tgt = T(sp.target);
+                        tw = T(sp.w_term);
+                        sw = T(sp.w_seed);
+                    }
+                    const T dv = u[0] - tgt;
+                    T term = kind == 0 ? tw * (N * N) : (kind == 1 ? tw * fabs(N) : (kind == 2 ? tw * (dv * dv) : tw * fabs(dv)));
+                    term = valid ? term : T(0);
                     if (valid && !isfinite(term)) atomicMin(bad, static_cast<unsigned long long>(gp));
-                    const T gN = valid ? T(2) * N * w : T(0);
-                    const T gu[4] = {gN * (-mu2 * (T(1) - T(2) * u[0])), gN * mu0, gN, -gN * mu1};
+                    T gu[4];
+                    if (kind <= 1) {
+                        const T gN = valid ? (kind == 0 ? T(2) * N * sw : sgn0(N) * sw) : T(0);
+                        gu[0] = gN * (-mu2 * (T(1) - T(2) * u[0]));
+                        gu[1] = gN * mu0;
+                        gu[2] = gN;
+                        gu[3] = -gN * mu1;
+                    } else {
+                        gu[0] = valid ? (kind == 2 ? T(2) * dv * sw : sgn0(dv) * sw) : T(0);
+                        gu[1] = gu[2] = gu[3] = T(0);
+                    }
                     red[P * RPMAX + p] = term;
                     if constexpr (META) red[P * RPMAX + P + p] = gu[0];
                     for (int j = 0; j < rpL; ++j) {

@@ -129,6 +129,17 @@ def main():
     g.update(c4_reg=np.array([1e-2, 1.5, 1e-3]), c4_reg_params=P4r, c4_reg_value=np.array([m4r["value"]]), c4_reg_comps=m4r["comps"],
              c4_reg_ortho=np.array([m4r["ortho"]]), c4_reg_grad=m4r["grad"])
 
+    # meta_train's full emitter: + initial / periodic terms (per-point mu through the
+    # hypernetwork, training.cpp:307-327); 6 initial + 5 periodic points per instance
+    bb = R.sample_collocation(4009, 0, 12, 10)
+    mu_a, mu_b = mus4[0], mus4[-1]
+    ic_mu = np.array([mu_a] * 6 + [mu_b] * 6)
+    per_mu = np.array([mu_a] * 5 + [mu_b] * 5)
+    m4f = R.meta_grad_full(w4, r4, P4r, hw4, H4, lo3, hi3, pts4, mus4, bb["initial_x"], ic_mu, bb["periodic_t"],
+                           per_mu, 1e-2, 1.5, 1e-3, threads=4)
+    g.update(c4_full_ic_x=bb["initial_x"], c4_full_per_t=bb["periodic_t"], c4_full_value=np.array([m4f["value"]]),
+             c4_full_comps=m4f["comps"], c4_full_ortho=np.array([m4f["ortho"]]), c4_full_grad=m4f["grad"])
+
     # checkpoint interop: a file written by the reference's own checkpoint_save
     # (put_lrnr / put_hyper / put_fast / put_sampling) from the c0 / c1 objects
     hw0, H0 = R.make_hyper_params(r0, 2, 16, lo3, hi3, 4008, 0.01, 0.5)

@@ -432,6 +432,26 @@ def test_meta_regularizers_c4_shape_fp32_match_oracle(gpu, oracle, act):
     assert normwise(got["grad"][nP:], want[nP:]) <= TOL32_NORM
 
 
+@pytest.mark.parametrize("dtype", [pkg.F64, pkg.F32])
+def test_meta_full_emitter_matches_reference(gpu, golden, dtype):
+    """meta_train's full step: interior (+ sparse), initial and periodic terms per instance, + ortho."""
+    g = golden
+    lam_sp, gamma, lam_o = g["c4_reg"]
+    m = pkg.LrnrParams(g["c4_widths"], g["c4_ranks"], g["c4_reg_params"], pkg.ACT_TANH)
+    gpu.set_lrnr(m, dtype)
+    gpu.set_hyper(pkg.HyperParams(g["c4_hw"], g["c4_hparams"], g["c3_lo"], g["c3_hi"]))
+    gpu.set_points(g["c4_pts"], n_inst=2)
+    gpu.set_meta_boundary(2, g["c4_full_ic_x"], g["c4_full_per_t"])
+    try:
+        r = gpu.meta_terms_grad(np.array([g["c4_mus"][0], g["c4_mus"][-1]]), m.params.size, lam_sp, gamma, lam_o)
+    finally:
+        gpu.set_meta_boundary(0)
+    tol_v, tol_g = (1e-12, 1e-10) if dtype == pkg.F64 else (TOL32_LOSS, TOL32_NORM)
+    assert abs(r["value"] - g["c4_full_value"][0]) <= tol_v * g["c4_full_value"][0]
+    np.testing.assert_allclose(r["comps"], g["c4_full_comps"], rtol=tol_v, atol=1e-14)
+    assert normwise(r["grad"], g["c4_full_grad"]) <= tol_g
+
+
 def test_cpp_adapter_drop_in_against_reference():
     """include/lrnr_gpu_adapter.hpp compiled against the reference's own headers and
     objects (oracle/_ref/adapter_test): same fine-tune / FastLRNR gradient as
