@@ -352,6 +352,16 @@ def run_ours(args):
     value = world * n / (ms_per_step * 1e-3)
     ctx.check()
 
+    # the paper's approximation metric: FastLRNR dL/ds against the full LRNR's on the same points
+    approx = None
+    if len(outs) == 2:
+        g_l, g_f = outs[0].double().cpu().numpy(), outs[1].double().cpu().numpy()
+        approx = {"grad_s_rel_l2": float(np.linalg.norm(g_f[1:] - g_l[1:]) / np.linalg.norm(g_l[1:])),
+                  "loss_rel": float(abs(g_f[0] - g_l[0]) / abs(g_l[0])),
+                  "cosine": float(np.dot(g_f[1:], g_l[1:]) / (np.linalg.norm(g_f[1:]) * np.linalg.norm(g_l[1:]))),
+                  "what": "FastLRNR vs full-LRNR residual loss and dL/ds on the step's points (EIM r_hat "
+                          f"{list(map(int, wl['models'][1][1].red_ranks))})"}
+
     # roofline of the dominant kernel (the LRNR sweep): algorithmic FLOPs / its event time
     peak_meas = ctx.fma_peak_tflops(wl["dtype"])
     nominal = NOMINAL_FP32_TFLOPS if wl["dtype"] == pkg.F32 else NOMINAL_FP64_TFLOPS
@@ -438,7 +448,8 @@ def run_ours(args):
                            "l2": "flushed between timed steps (256 MiB write outside the step events)",
                            "kernel_option": args.kernel, "fast_sincos": args.fast_sincos},
                 "roofline": roofline, "kernels": per_kernel, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clk.summary(), "solve_loops": solves}
+                "gpu_launches": launches, "clocks": clk.summary(), "solve_loops": solves,
+                "fast_vs_lrnr": approx}
         print(json.dumps(line))
     ctx.close()
     if dist is not None:
