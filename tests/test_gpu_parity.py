@@ -675,3 +675,20 @@ def test_model_from_reference_checkpoint_runs(gpu, golden):
     assert floor_rel(r["grad_s"], g["c0_grad_s"]) <= TOL64
     rf = gpu.loss_grad_s(pkg.MODEL_FAST, g["c0_s"], g["c0_mu"])
     assert floor_rel(rf["grad_s"], g["c1_grad_s"]) <= TOL64
+
+
+@pytest.mark.parametrize("kernel", FP32_KERNELS)
+@pytest.mark.parametrize("act", [pkg.ACT_SIN, pkg.ACT_TANH])
+def test_unaligned_shapes_fp32_match_oracle(gpu, oracle, opts, kernel, act):
+    """Width 100 (not a multiple of the 32-neuron chunk), ranks 2 / 10 / 1 (padded MMA K / N,
+    rank classes): every FP32 kernel against the FP64 oracle."""
+    opts(kernel)
+    m, s = pkg.make_baseline_model([2, 100, 100, 100, 1], [2, 10, 10, 1], 2410, act)
+    pts = pkg.sample_collocation(4001, 700)
+    mu = np.array([5.0, 0.01, 1.0])
+    gpu.set_lrnr(m, pkg.F32)
+    gpu.set_points(pts)
+    got = gpu.loss_grad_s(pkg.MODEL_LRNR, s, mu)
+    want = oracle.lrnr_grad(m.widths, m.ranks, m.params, s, mu, pts, act=act)
+    assert abs(got["value"] - want["value"]) <= TOL32_LOSS * abs(want["value"])
+    assert normwise(got["grad_s"], want["grad_s"]) <= TOL32_NORM
