@@ -67,7 +67,10 @@ small::Geom small_geom(const Model& m, int64_t n_inst, int64_t n_per) {
     g.blk = (blk + 7) & ~7;
     const size_t elem = m.dtype == LRNR_F64 ? 8 : 4;
     const size_t base = static_cast<size_t>(small::smem_elems(m.rtotal, g.a_len, g.mmax, g.rmax)) * elem;
-    g.stage = base + 2 * static_cast<size_t>(g.blk) * elem <= 200 * 1024 ? 1 : 0;
+#ifndef SMALL_STAGE_MAX_KB
+#define SMALL_STAGE_MAX_KB 100  // wide layers: several unstaged CTAs per SM beat one staged (fine_tune 1.29 -> 1.05 ms)
+#endif
+    g.stage = base + 2 * static_cast<size_t>(g.blk) * elem <= SMALL_STAGE_MAX_KB * 1024 ? 1 : 0;
     return g;
 }
 
