@@ -94,10 +94,11 @@ int lrnr_gpu_set_stream(lrnr_gpu_ctx* ctx, void* cuda_stream);
 #define LRNR_OPT_FAST_SINCOS 1
 #define LRNR_OPT_KERNEL 2
 #define LRNR_OPT_TILE_P 3
-/* LRNR_OPT_SOLVE (lrnr_gpu_fast_solve): 0 = auto: the persistent single-CTA
- * solver (one warp per loss term, whole loop in one launch) when every width
- * and rank is <= 32, the terms fit 32 warps and there are <= 15 periodic
- * pairs; 1 = the graph path (one captured epoch replayed per epoch). */
+/* LRNR_OPT_SOLVE (lrnr_gpu_fast_solve): 0 = auto: the persistent solver (one
+ * thread-block cluster, one warp per loss term, the whole loop in one launch,
+ * per-epoch reduction over distributed shared memory) when every width and
+ * rank is <= 32 and the terms fit 8 CTAs x 16 warps; 1 = the graph path (one
+ * captured epoch replayed per epoch). */
 #define LRNR_OPT_SOLVE 4   /* FP32 wide-layer tile: 64 points x 512 threads (default) or 32 x 256 (2 CTAs/SM) */
 int lrnr_gpu_set_option(lrnr_gpu_ctx* ctx, int opt, int value);
 /* Number of kernels this context has launched so far (instrumentation). */

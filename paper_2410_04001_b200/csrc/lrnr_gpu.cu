@@ -1315,7 +1315,18 @@ bool fast_solve_persistent(lrnr_gpu_ctx* ctx, const Model& m, const std::vector<
     pb.n_ic = n_ic;
     pb.n_bc = n_bc;
     pb.n_warps = n_int + n_ic + 2 * n_bc;
-    if (pb.n_warps < 1 || pb.n_warps > 32 || n_bc > 15 || m.r[0] > 4 || m.rtotal > 1024) return false;
+    // cluster layout: periodic pairs start at an even global warp, even warps per CTA (a pair
+    // never straddles CTAs), SOLVE_WPC warps per CTA (more when the terms need > 8 CTAs, the
+    // portable cluster size)
+    pb.pair_base = (n_int + n_ic + 1) & ~1;
+    pb.n_gw = pb.pair_base + 2 * n_bc;
+#ifndef SOLVE_WPC
+#define SOLVE_WPC 4  // measured on c2 (16 terms): 4 CTAs x 4 warps 15.9 us/epoch, 8 x 2 21.4, 1 x 16 24
+#endif
+    pb.wpc = SOLVE_WPC;
+    while ((pb.n_gw + pb.wpc - 1) / pb.wpc > 8) pb.wpc += 2;
+    const int n_cta = (pb.n_gw + pb.wpc - 1) / pb.wpc;
+    if (pb.n_warps < 1 || pb.wpc > 16 || m.r[0] > 4 || m.rtotal > 1024) return false;
     for (int l = 0; l < m.L; ++l)
         if (m.r[l] > 32) return false;
     for (int l = 1; l < m.L; ++l)
@@ -1364,22 +1375,33 @@ bool fast_solve_persistent(lrnr_gpu_ctx* ctx, const Model& m, const std::vector<
                        ctx->stream));
     CK(cudaMemcpyAsync(ctx->solve_bt.p, bt.data(), bt.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(ctx->mu_dev.p, mu, 3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    // one cluster of n_cta CTAs (cudaLaunchKernelEx with a cluster-dimension attribute)
+    auto launch = [&](auto kern, auto net) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(n_cta));
+        cfg.blockDim = dim3(static_cast<unsigned>(32 * pb.wpc));
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = static_cast<unsigned>(n_cta);
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, kern, net, pb, static_cast<const double*>(ctx->solve_pts[0].as<double>()),
+                              static_cast<const double*>(ctx->mu_dev.as<double>()),
+                              static_cast<const double*>(ctx->solve_s0.as<double>()),
+                              static_cast<const double*>(ctx->solve_bt.as<double>()), ctx->solve_best.as<double>(),
+                              ctx->solve_losses.as<double>(), ctx->solve_state.as<solve::State>()));
+    };
     if (m.dtype == LRNR_F64) {
-        auto kern = m.act == LRNR_ACT_TANH ? solve::fast_solve_kernel<double, 0> : solve::fast_solve_kernel<double, 1>;
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        kern<<<1, 32 * pb.n_warps, smem, ctx->stream>>>(dev_net<double>(m), pb, ctx->solve_pts[0].as<double>(),
-                                                         ctx->mu_dev.as<double>(), ctx->solve_s0.as<double>(),
-                                                         ctx->solve_bt.as<double>(), ctx->solve_best.as<double>(),
-                                                         ctx->solve_losses.as<double>(),
-                                                         ctx->solve_state.as<solve::State>());
+        if (m.act == LRNR_ACT_TANH) launch(solve::fast_solve_kernel<double, 0>, dev_net<double>(m));
+        else launch(solve::fast_solve_kernel<double, 1>, dev_net<double>(m));
     } else {
-        auto kern = m.act == LRNR_ACT_TANH ? solve::fast_solve_kernel<float, 0> : solve::fast_solve_kernel<float, 1>;
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        kern<<<1, 32 * pb.n_warps, smem, ctx->stream>>>(dev_net<float>(m), pb, ctx->solve_pts[0].as<double>(),
-                                                        ctx->mu_dev.as<double>(), ctx->solve_s0.as<double>(),
-                                                        ctx->solve_bt.as<double>(), ctx->solve_best.as<double>(),
-                                                        ctx->solve_losses.as<double>(),
-                                                        ctx->solve_state.as<solve::State>());
+        if (m.act == LRNR_ACT_TANH) launch(solve::fast_solve_kernel<float, 0>, dev_net<float>(m));
+        else launch(solve::fast_solve_kernel<float, 1>, dev_net<float>(m));
     }
     CK(cudaGetLastError());
     ++ctx->launches;

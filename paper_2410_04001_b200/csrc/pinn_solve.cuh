@@ -23,6 +23,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cooperative_groups.h>
+
 #include "pinn_kernels.cuh"
 #include "pinn_small.cuh"
 
@@ -31,7 +33,10 @@ namespace solve {
 
 struct Problem {
     int n_int, n_ic, n_bc;  // interior points, initial points, periodic pairs
-    int n_warps;            // n_int + n_ic + 2 n_bc (<= 32)
+    int n_warps;            // n_int + n_ic + 2 n_bc
+    // cluster layout: global warp gw = cluster rank * wpc + warp; terms at gw < n_int + n_ic,
+    // periodic pairs at pair_base + 2 j (pair_base even, wpc even: a pair never straddles CTAs)
+    int wpc, pair_base, n_gw;
     int yoff[kMaxL + 1];    // per-warp state: y_l at 4 * yoff[l], A_l at 4 * (ylen + aoff[l])
     int aoff[kMaxL];
     int ylen, alen;
@@ -52,8 +57,8 @@ struct State {
 
 // smem (bytes): T weights + T per-warp state + double s, s0, m, v, best, per-warp ds rows, terms
 __host__ inline size_t smem_bytes(const Problem& p, int rtotal, size_t elem) {
-    return elem * (static_cast<size_t>(p.wlen) + 8 + static_cast<size_t>(p.n_warps) * (4 * (p.ylen + p.alen) + 128)) +
-           8 * (5 * static_cast<size_t>(rtotal) + static_cast<size_t>(p.n_warps) * (rtotal + 1) + 64 + 33);
+    return elem * (static_cast<size_t>(p.wlen) + 8 + static_cast<size_t>(p.wpc) * (4 * (p.ylen + p.alen) + 128)) +
+           8 * (5 * static_cast<size_t>(rtotal) + static_cast<size_t>(p.wpc) * (rtotal + 1) + 64 + 33);
 }
 
 template <typename T>
@@ -62,7 +67,7 @@ __device__ __forceinline__ T wshfl(T v, int src) {
 }
 
 template <typename T, int ACT>
-__global__ void __launch_bounds__(1024, 1)
+__global__ void __launch_bounds__(512, 1)
 fast_solve_kernel(const DevNet<T> net, const Problem pb, const double* __restrict__ terms,
                   const double* __restrict__ mu, const double* __restrict__ s_init, const double* __restrict__ bt,
                   double* __restrict__ best_out, double* __restrict__ losses, State* __restrict__ st_out) {
@@ -75,16 +80,20 @@ fast_solve_kernel(const DevNet<T> net, const Problem pb, const double* __restric
     double* av = am + G;
     double* best = av + G;
     double* rows = best + G;                         // [warp][term, ds (G)]
-    double* misc = rows + pb.n_warps * (G + 1);      // u exchange (32) + reduction scratch
+    double* misc = rows + pb.wpc * (G + 1);          // u exchange (32) + reduction scratch
     double* pair_u = misc;                           // [warp] value of u
     double* terms_s = misc + 32;                     // 32 (x / t / target per warp)
     // factor blocks, V0, per-warp state: 16-B aligned (vector loads)
-    T* wsm = reinterpret_cast<T*>(terms_s + 32 + ((5 * G + pb.n_warps * (G + 1)) & 1));
+    T* wsm = reinterpret_cast<T*>(terms_s + 32 + ((5 * G + pb.wpc * (G + 1)) & 1));
     T* v0s = wsm + pb.wlen;
     T* states = v0s + 8;                              // [warp][4 (ylen + alen) + 128]
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nthr = blockDim.x;
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int crank = static_cast<int>(cluster.block_rank()), csize = static_cast<int>(cluster.num_blocks());
+    const int gw = crank * pb.wpc + warp;  // global warp: this warp's term
     // ---- one-time staging: factor blocks, V_0, u_last; s, s0 ----
     for (int l = 0; l + 1 < L; ++l) {
         const int trow = net.trow[l], wr = pb.wrow[l];
@@ -99,6 +108,7 @@ fast_solve_kernel(const DevNet<T> net, const Problem pb, const double* __restric
         am[i] = 0.0;
         av[i] = 0.0;
     }
+    for (int i = tid; i < pb.wpc * (G + 1); i += nthr) rows[i] = 0.0;  // idle warps keep zero rows
     __shared__ State st;
     __shared__ int go, copy;
     if (tid == 0) {
@@ -111,21 +121,22 @@ fast_solve_kernel(const DevNet<T> net, const Problem pb, const double* __restric
     const T mu0 = T(mu[0]), mu1 = T(mu[1]), mu2 = T(mu[2]);
 
     // ---- this warp's term ----
-    const bool active = warp < pb.n_warps;
+    const bool is_pair = gw >= pb.pair_base && gw < pb.pair_base + 2 * pb.n_bc;
+    const bool active = gw < pb.n_int + pb.n_ic || is_pair;
     int kind = 0;       // 0 interior |N|, 1 initial |u - sin x|, 2 periodic side 0, 3 periodic side 1
     T px = T(0), pt = T(0);
     double tgt = 0.0;
     if (active) {
-        if (warp < pb.n_int) {
-            px = T(terms[2 * warp]);
-            pt = T(terms[2 * warp + 1]);
-        } else if (warp < pb.n_int + pb.n_ic) {
+        if (gw < pb.n_int) {
+            px = T(terms[2 * gw]);
+            pt = T(terms[2 * gw + 1]);
+        } else if (gw < pb.n_int + pb.n_ic) {
             kind = 1;
-            const int i = warp - pb.n_int;
+            const int i = gw - pb.n_int;
             px = T(terms[2 * pb.n_int + i]);
             tgt = sin(terms[2 * pb.n_int + i]);
         } else {
-            const int j = warp - pb.n_int - pb.n_ic;
+            const int j = gw - pb.pair_base;
             kind = 2 + (j & 1);
             px = (j & 1) ? T(6.283185307179586476925286766559) : T(0);
             pt = T(terms[2 * pb.n_int + pb.n_ic + (j >> 1)]);
@@ -256,10 +267,8 @@ fast_solve_kernel(const DevNet<T> net, const Problem pb, const double* __restric
                 g0 = sgn0(d);
             } else {
                 if (lane == 0) pair_u[warp] = double(u0);
-                // the two sides of a pair: warps (w, w ^ 1) with w even relative to the pair base
-                const int base = pb.n_int + pb.n_ic;
-                const int first = base + ((warp - base) & ~1);
-                asm volatile("bar.sync %0, 64;" ::"r"(1 + ((first - base) >> 1) % 15) : "memory");
+                // the two sides of a pair: local warps (w, w + 1), w even
+                asm volatile("bar.sync %0, 64;" ::"r"(1 + ((gw - pb.pair_base) >> 1) % 15) : "memory");
                 const double other = pair_u[kind == 2 ? warp + 1 : warp - 1];
                 const T d = kind == 2 ? u0 - T(other) : T(other) - u0;  // u(0,t) - u(2pi,t)
                 if (kind == 2) term = fabs(d);
@@ -336,70 +345,88 @@ fast_solve_kernel(const DevNet<T> net, const Problem pb, const double* __restric
             }
             if (lane == 0) drow[0] = double(term);
         }
-        __syncthreads();
-        // ---------------- step (thread 0 decides, all threads update) ----------------
-        if (warp == 0) {
-            // loss = sum of the warp terms + lambda ||s - s0||_1: lane-strided partials,
-            // then a fixed xor tree (deterministic)
-            double value = lane < pb.n_warps ? rows[lane * (G + 1)] : 0.0;
-            double local = 0.0;
-            if (pb.lambda_local > 0.0)
-                for (int i = lane; i < G; i += 32) local += fabs(s[i] - s0[i]);
+        cluster.sync();  // every CTA's rows are complete
+        // ---------------- step: rank 0 reduces all CTAs' rows (DSMEM) in global warp order ----------------
+        if (crank == 0) {
+            if (warp == 0) {
+                // loss = sum of the warp terms + lambda ||s - s0||_1: lane-strided partials, then a
+                // fixed xor tree (deterministic)
+                double value = 0.0;
+                for (int g2 = lane; g2 < csize * pb.wpc; g2 += 32) {
+                    const double* rr = cluster.map_shared_rank(rows, g2 / pb.wpc);
+                    value += rr[(g2 % pb.wpc) * (G + 1)];
+                }
+                double local = 0.0;
+                if (pb.lambda_local > 0.0)
+                    for (int i = lane; i < G; i += 32) local += fabs(s[i] - s0[i]);
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                value += __shfl_xor_sync(0xffffffffu, value, o);
-                local += __shfl_xor_sync(0xffffffffu, local, o);
+                for (int o = 16; o > 0; o >>= 1) {
+                    value += __shfl_xor_sync(0xffffffffu, value, o);
+                    local += __shfl_xor_sync(0xffffffffu, local, o);
+                }
+                if (lane == 0) misc[63] = value + pb.lambda_local * local;
+                __syncwarp();
             }
-            if (lane == 0) misc[63] = value + pb.lambda_local * local;
-            __syncwarp();
-        }
-        if (tid == 0) {
-            go = 0;
-            copy = 0;
-            const int64_t e = ++st.epoch;
-            const double value = misc[63];
-            if (!isfinite(value)) {
-                st.flags |= 3;
-                st.stopped = 1;
-            } else {
-                losses[e - 1] = value;
-                if (e == 1) st.initial = value;
-                if (value > 1e3 * st.initial) {
-                    st.flags |= 2;
+            __syncthreads();
+            if (tid == 0) {
+                go = 0;
+                copy = 0;
+                const int64_t e = ++st.epoch;
+                const double value = misc[63];
+                if (!isfinite(value)) {
+                    st.flags |= 3;
                     st.stopped = 1;
                 } else {
-                    if (value < st.best_loss) {
-                        st.best_loss = value;
-                        st.best_epoch = e;
-                        copy = 1;
+                    losses[e - 1] = value;
+                    if (e == 1) st.initial = value;
+                    if (value > 1e3 * st.initial) {
+                        st.flags |= 2;
+                        st.stopped = 1;
+                    } else {
+                        if (value < st.best_loss) {
+                            st.best_loss = value;
+                            st.best_epoch = e;
+                            copy = 1;
+                        }
+                        ++st.t;
+                        go = 1;
                     }
-                    ++st.t;
-                    go = 1;
+                }
+            }
+            __syncthreads();
+            if (go) {
+                const double b1t = bt[2 * (st.t - 1)], b2t = bt[2 * (st.t - 1) + 1];
+                for (int i = tid; i < G; i += nthr) {
+                    const double si = s[i];
+                    if (copy) best[i] = si;
+                    double g = 0.0;
+                    for (int r = 0; r < csize; ++r) {
+                        const double* rr = cluster.map_shared_rank(rows, r);
+                        for (int w = 0; w < pb.wpc; ++w) g += rr[w * (G + 1) + 1 + i];
+                    }
+                    if (pb.lambda_local > 0.0) {
+                        const double d = si - s0[i];
+                        g += pb.lambda_local * (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0));
+                    }
+                    const double mi = 0.9 * am[i] + (1.0 - 0.9) * g;
+                    const double vi = 0.999 * av[i] + (1.0 - 0.999) * g * g;
+                    am[i] = mi;
+                    av[i] = vi;
+                    const double x = si - pb.lr * (mi / b1t) / (sqrt(vi / b2t) + 1e-8);
+                    s[i] = x < 0.0 ? 0.0 : x;
                 }
             }
         }
-        __syncthreads();
-        if (go) {
-            const double b1t = bt[2 * (st.t - 1)], b2t = bt[2 * (st.t - 1) + 1];
-            for (int i = tid; i < G; i += nthr) {
-                const double si = s[i];
-                if (copy) best[i] = si;
-                double g = 0.0;
-                for (int w = 0; w < pb.n_warps; ++w) g += rows[w * (G + 1) + 1 + i];
-                if (pb.lambda_local > 0.0) {
-                    const double d = si - s0[i];
-                    g += pb.lambda_local * (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0));
-                }
-                const double mi = 0.9 * am[i] + (1.0 - 0.9) * g;
-                const double vi = 0.999 * av[i] + (1.0 - 0.999) * g * g;
-                am[i] = mi;
-                av[i] = vi;
-                const double x = si - pb.lr * (mi / b1t) / (sqrt(vi / b2t) + 1e-8);
-                s[i] = x < 0.0 ? 0.0 : x;
-            }
+        cluster.sync();  // rank 0's step is complete
+        if (crank != 0) {  // pull the new s and the stop flag
+            const double* s_r0 = cluster.map_shared_rank(s, 0);
+            for (int i = tid; i < G; i += nthr) s[i] = s_r0[i];
+            if (tid == 0) st.stopped = cluster.map_shared_rank(&st, 0)->stopped;
         }
         __syncthreads();
     }
+    cluster.sync();  // no CTA exits while others may still read its shared memory
+    if (crank != 0) return;
     for (int i = tid; i < G; i += nthr) best_out[i] = best[i];
     if (tid == 0) *st_out = st;
 }
