@@ -793,6 +793,25 @@ int ref_meta_grad_full(int L, const int64_t* widths, const int64_t* ranks, const
     });
 }
 
+// The reference's own step-time benchmark (training.cpp:613-799): per width, the
+// median fine-tune step and fast step seconds (BenchmarkConfig defaults unless given).
+int ref_benchmark_step_time(const int64_t* widths, int64_t n_widths, int64_t reps, int64_t warmup, int threads,
+                            double* out_tune_s, double* out_fast_s) {
+    return guarded([&] {
+        training::BenchmarkConfig cfg;
+        cfg.reps = static_cast<std::size_t>(reps);
+        cfg.warmup = static_cast<std::size_t>(warmup);
+        cfg.par = par_of(threads, 64);
+        std::vector<std::size_t> w;
+        for (int64_t i = 0; i < n_widths; ++i) w.push_back(static_cast<std::size_t>(widths[i]));
+        const auto rows = training::benchmark_step_time(w, cfg);
+        for (std::size_t i = 0; i < rows.size(); ++i) {
+            out_tune_s[i] = rows[i].t_lrnr_s;
+            out_fast_s[i] = rows[i].t_fast_s;
+        }
+    });
+}
+
 // ---- FastLRNR construction (reduction.cpp:10-31,111-283) ----
 // Constant hypernetwork (zero W, bias = s) so hyper_forward(mu) == s.
 int ref_build_fast(int L, const int64_t* widths, const int64_t* ranks, const double* params,
