@@ -71,14 +71,19 @@ extern "C" {
 typedef struct lrnr_gpu_ctx lrnr_gpu_ctx;
 
 /* ---- context ---- */
+/* One context = one device + one stream + resident parameters: the role of the
+ * reference's per-thread Tape and its bindings (autodiff.hpp:36-170, TapeBindings
+ * autodiff.hpp:244, make_bindings autodiff.cpp:979-1018). */
 int lrnr_gpu_create(int device, lrnr_gpu_ctx** out);
 int lrnr_gpu_destroy(lrnr_gpu_ctx* ctx);
 const char* lrnr_gpu_last_error(const lrnr_gpu_ctx* ctx);
 /* layer tag of the last LRNR_ENONFINITE (NonFiniteError::layer_tag semantics:
  * l+1 for LRNR layer l, 0 for the FastLRNR input factor, -1 otherwise). */
+/* NonFiniteError::layer_tag of the last LRNR_ENONFINITE (autodiff.hpp:28-34). */
 int lrnr_gpu_last_layer_tag(const lrnr_gpu_ctx* ctx);
 /* Use a caller-owned cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
  * NULL restores the context's own stream. */
+/* Stream for all work of the context (no reference counterpart: the reference is synchronous). */
 int lrnr_gpu_set_stream(lrnr_gpu_ctx* ctx, void* cuda_stream);
 /* Options.  LRNR_OPT_FAST_SINCOS (FP32 sin networks): 1 = sin/cos from the SFU
  * approximations after a Cody-Waite reduction (~4e-7 absolute), 0 = polynomial
@@ -102,6 +107,7 @@ int lrnr_gpu_set_stream(lrnr_gpu_ctx* ctx, void* cuda_stream);
 #define LRNR_OPT_SOLVE 4   /* FP32 wide-layer tile: 64 points x 512 threads (default) or 32 x 256 (2 CTAs/SM) */
 int lrnr_gpu_set_option(lrnr_gpu_ctx* ctx, int opt, int value);
 /* Number of kernels this context has launched so far (instrumentation). */
+/* Kernels launched so far (instrumentation; no reference counterpart). */
 int64_t lrnr_gpu_launch_count(const lrnr_gpu_ctx* ctx);
 
 /* ---- model upload (replaces the Tape bindings, autodiff.cpp:826-868) ---- */
@@ -207,22 +213,34 @@ int lrnr_gpu_l1_error(lrnr_gpu_ctx* ctx, int model, const double* s, const doubl
  * vice versa (tests/test_host.py). */
 typedef struct lrnr_ckpt lrnr_ckpt;
 const char* lrnr_ckpt_last_error(void);
+/* An empty Checkpoint (checkpoint.hpp). */
 int lrnr_ckpt_create(lrnr_ckpt** out);
+/* checkpoint_load (checkpoint.cpp:127-161). */
 int lrnr_ckpt_load(const char* path, lrnr_ckpt** out);
+/* checkpoint_save (checkpoint.cpp:103-125). */
 int lrnr_ckpt_save(const lrnr_ckpt* c, const char* path);
 void lrnr_ckpt_free(lrnr_ckpt* c);
+/* get_lrnr (checkpoint.cpp:174-186). */
 int lrnr_ckpt_get_lrnr(const lrnr_ckpt* c, int* L, int64_t* widths, int64_t* ranks, int64_t* n_params, double* params);
+/* put_lrnr (checkpoint.cpp:163-172). */
 int lrnr_ckpt_put_lrnr(lrnr_ckpt* c, int L, const int64_t* widths, const int64_t* ranks, const double* params);
+/* get_hyper (checkpoint.cpp:201-215). */
 int lrnr_ckpt_get_hyper(const lrnr_ckpt* c, int* K, int64_t* hw, int64_t* n_params, double* params, double* lo3,
                         double* hi3);
+/* put_hyper (checkpoint.cpp:188-199). */
 int lrnr_ckpt_put_hyper(lrnr_ckpt* c, int K, const int64_t* hw, const double* params, int L_split,
                         const int64_t* split, const double* lo3, const double* hi3);
+/* has_fast (checkpoint.cpp:231). */
 int lrnr_ckpt_has_fast(const lrnr_ckpt* c);
+/* get_fast (checkpoint.cpp:233-248). */
 int lrnr_ckpt_get_fast(const lrnr_ckpt* c, int* L, int64_t* ranks, int64_t* red_ranks, int64_t* n_params,
                        double* params);
+/* put_fast (checkpoint.cpp:217-229). */
 int lrnr_ckpt_put_fast(lrnr_ckpt* c, int L, const int64_t* ranks, const int64_t* red_ranks, int64_t m_in,
                        int64_t m_out, const double* params);
+/* get_sampling (checkpoint.cpp:282-288). */
 int lrnr_ckpt_get_sampling(const lrnr_ckpt* c, int64_t* n, double* xt);
+/* put_sampling (checkpoint.cpp:276-280). */
 int lrnr_ckpt_put_sampling(lrnr_ckpt* c, int64_t n, const double* xt);
 
 /* Hypernetwork-coupled step (BASELINE config 3; the emit_hyper + emit_fast_jet
@@ -279,6 +297,8 @@ int lrnr_gpu_loss(lrnr_gpu_ctx* ctx, int model, const double* s, const double* m
  * lrnr_gpu_check: synchronize and map a recorded non-finite term to
  * LRNR_ENONFINITE (+ layer tag). */
 int lrnr_gpu_upload_coeffs(lrnr_gpu_ctx* ctx, const double* s, const double* mu, int64_t n_inst);
+/* lrnr_gpu_run / _check / _download: run_batch_gradient (training.cpp:191-263) over resident
+ * points and coefficients without host synchronization (multi-GPU steps, benchmarks). */
 int lrnr_gpu_run(lrnr_gpu_ctx* ctx, int model, double w, double* dev_out);
 int lrnr_gpu_check(lrnr_gpu_ctx* ctx);
 /* Copy the context's result buffer (n_inst x (1 + r_total) doubles) to host. */
@@ -286,11 +306,15 @@ int lrnr_gpu_download(lrnr_gpu_ctx* ctx, double* host_out, int64_t n_doubles);
 
 /* Achievable FMA-pipe rate of this device (dtype LRNR_F32 / LRNR_F64), TFLOP/s,
  * from a full-chip independent-chain FMA kernel; the roofline denominator. */
+/* FP32 / FP64 FMA-chain microbenchmark: the roofline denominator (measurement aid; no reference
+ * counterpart). */
 int lrnr_gpu_fma_peak(lrnr_gpu_ctx* ctx, int dtype, double* out_tflops);
 
 /* ---- host-side setup (no GPU needed; reference reduction.cpp / model.cpp) ---- */
 /* BASELINE config generator: make_lrnr_params(orthonormal,
  * bias 0) from Rng(seed), then b <- 0.1*normal(), s <- U[0,1] sorted descending. */
+/* make_lrnr_params (model.cpp:454-504) + the BASELINE init recipe (b = 0.1 normal, s = U[0,1]
+ * sorted descending), bit-identical streams (rng.hpp:13-44). */
 int lrnr_host_make_baseline_model(int depth, const int64_t* widths, const int64_t* ranks,
                                   uint64_t seed, double* out_params, double* out_s);
 /* make_hyper_params (model.cpp:480-504) from a fresh Rng(seed). */
