@@ -1443,7 +1443,8 @@ int lrnr_gpu_destroy(lrnr_gpu_ctx* ctx) {
                       &ctx->bnd_x, &ctx->bnd_spec, &ctx->bnd_jets, &ctx->solve_rows, &ctx->solve_state, &ctx->solve_m,
                       &ctx->solve_v, &ctx->solve_best, &ctx->solve_s0, &ctx->solve_bt, &ctx->solve_losses,
                       &ctx->solve_pts[0], &ctx->solve_pts[1], &ctx->solve_bnd[0], &ctx->solve_bnd[1],
-                      &ctx->solve_sinx[0], &ctx->solve_sinx[1]})
+                      &ctx->solve_sinx[0], &ctx->solve_sinx[1], &ctx->mb_pts, &ctx->mb_sinx, &ctx->mb_rows,
+                      &ctx->mb_sum})
         b->release();
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;

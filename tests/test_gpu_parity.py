@@ -692,3 +692,32 @@ def test_unaligned_shapes_fp32_match_oracle(gpu, oracle, opts, kernel, act):
     want = oracle.lrnr_grad(m.widths, m.ranks, m.params, s, mu, pts, act=act)
     assert abs(got["value"] - want["value"]) <= TOL32_LOSS * abs(want["value"])
     assert normwise(got["grad_s"], want["grad_s"]) <= TOL32_NORM
+
+
+def test_context_lifecycle_does_not_leak(golden):
+    """create -> every feature -> destroy, repeated: device memory returns to its baseline."""
+    import torch
+    g = golden
+    m = lrnr_from_golden(g, "c0")
+    f = pkg.FastParams(g["c0_ranks"], g["c1_red_ranks"], g["c1_fparams"], pkg.ACT_TANH)
+
+    def cycle():
+        ctx = pkg.GpuContext(0)
+        ctx.set_lrnr(m, pkg.F64)
+        ctx.set_fast(f, pkg.F64)
+        ctx.set_points(g["c0_pts"][:512])
+        ctx.loss_grad_s(pkg.MODEL_LRNR, g["c0_s"], g["c0_mu"])
+        ctx.set_boundary(g["c0_full_ic_x"][:8], g["c0_full_per_t"][:8])
+        ctx.terms_grad(pkg.MODEL_LRNR, g["c0_s"], g["c0_mu"])
+        ctx.fast_solve(g["c0_s"], g["c0_mu"], g["c1_phase_x"], 1e-2, 1e-2, 3)
+        ctx.fine_tune(g["c0_s"], g["c0_mu"], 1e-2, 2, 64, 16, 16)
+        ctx.close()
+
+    cycle()
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(5):
+        cycle()
+    torch.cuda.synchronize()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 < 8 << 20, f"{(free0 - free1) / 2**20:.1f} MiB not returned"
