@@ -111,25 +111,36 @@ __device__ __forceinline__ void put_split(float* sm, int c, int p, int j, float 
 // CTA 0 / thread 32 into a global array (see scripts/tc_timing.py).
 #ifdef LRNR_TC_TIMING
 __device__ unsigned long long g_tc_timing[16];
-#define TC_T0() long long _tt = clock64();
+// accumulated in shared memory (a few cycles per mark) and flushed once at the end
+#define TC_T0()                                                \
+    __shared__ unsigned long long _tc_acc[16];                 \
+    if (threadIdx.x < 16) _tc_acc[threadIdx.x] = 0;            \
+    __syncthreads();                                           \
+    long long _tt = clock64();
 #define TC_ISSUE_BEGIN() const long long _ti = clock64();
-#define TC_ISSUE_END()                                                                            \
-    do {                                                                                          \
-        if (blockIdx.x == 0) atomicAdd(&g_tc_timing[15], static_cast<unsigned long long>(clock64() - _ti)); \
+#define TC_ISSUE_END()                                                                    \
+    do {                                                                                  \
+        if (blockIdx.x == 0) _tc_acc[15] += static_cast<unsigned long long>(clock64() - _ti); \
     } while (0)
 #define TC_MARK(i)                                                         \
     do {                                                                   \
         if (blockIdx.x == 0 && threadIdx.x == 32) {                        \
             const long long _n = clock64();                                \
-            g_tc_timing[i] += static_cast<unsigned long long>(_n - _tt);  \
+            _tc_acc[i] += static_cast<unsigned long long>(_n - _tt);       \
             _tt = _n;                                                      \
         }                                                                  \
+    } while (0)
+#define TC_FLUSH()                                                          \
+    do {                                                                    \
+        __syncthreads();                                                    \
+        if (blockIdx.x == 0 && threadIdx.x < 16) g_tc_timing[threadIdx.x] += _tc_acc[threadIdx.x]; \
     } while (0)
 #else
 #define TC_T0()
 #define TC_ISSUE_BEGIN()
 #define TC_ISSUE_END()
 #define TC_MARK(i)
+#define TC_FLUSH()
 #endif
 
 // acc[1 + off + j] += sum_p red[p][j] for j < r, fixed order: NRG groups of
@@ -442,6 +453,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                         fwd_p2(q, ch);
                         if (lane == 0) TC_ISSUE_END();
                     }
+                    TC_MARK(5);
                 }
                 // transition end: Y -> y_{l+1} (scratch), SY = s (.) y (smem hi / lo)
                 TC_MARK(0);
@@ -649,6 +661,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
         }
         __syncthreads();
     }
+    TC_FLUSH();
     umma::fence_before();
     __syncthreads();
     if (warp == 0) umma::tmem_dealloc<512>(tbase);

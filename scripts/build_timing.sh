@@ -9,4 +9,4 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler
     --expt-relaxed-constexpr -diag-suppress 177 -DLRNR_TC_TIMING "$@" \
     -c paper_2410_04001_b200/csrc/lrnr_gpu.cu -o build/lrnr_gpu_timing.o
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o scripts/liblrnr_gpu_timing.so build/lrnr_gpu_timing.o \
-    build/inst_*.o build/host_setup.cpp.o -cudart static
+    build/inst_*.o build/*.cpp.o -cudart static

@@ -18,7 +18,7 @@ lib.lrnr_dev_tc_timing(out)
 ctx.loss_grad_s(pkg.MODEL_LRNR, c['s'], c['mu'])
 lib.lrnr_dev_tc_timing(out)
 names = ["fwd: wait P2(ch-1) + add_y", "fwd: P1/P2 issue -> chunk top", "fwd: wait mma1 (P1)", "fwd: epilogue act jet + A store",
-         "fwd: Z split/st + sync", "fwd: trans-end wait P2", "fwd: trans end Y->SY", "output layer",
+         "fwd: Z split/st + sync", "fwd: issuer block (skip) + trans-end wait P2", "fwd: trans end Y->SY", "output layer",
          "bwd: wait P2(ch-1) + add_t", "bwd: chunk top + A loads", "bwd: wait mma1 (P1)", "bwd: epilogue VJP",
          "bwd: G split/st + sync", "bwd: trans-end wait P2", "bwd: trans end + ds reduce", "-"]
 tot = sum(out[:15])
