@@ -340,6 +340,49 @@ int lrnr_host_build_fast(int depth, const int64_t* widths, const int64_t* ranks,
                          int64_t r_hat, int64_t* out_red, int64_t* out_indices,
                          double* out_fparams, int* out_exhausted);
 
+/* The points harvest_snapshots evaluates (reduction.cpp:111-148 with
+ * SamplingSetX::uniform_grid, reduction.cpp:10-25): n_mu x (nx*nt) x (1+n_perturb)
+ * (x, t) pairs in column order (mu, point, perturbation); the perturbations
+ * use the reference's Rng stream bit-identically. */
+int lrnr_host_harvest_points(int64_t n_mu, int64_t nx, int64_t nt, int64_t n_perturb, double sigma,
+                             uint64_t seed, double* out_xt);
+/* reduction::eim_greedy (reduction.cpp:150-238) on one m x n_cols row-major
+ * snapshot matrix: out_idx (r_hat, -1 padded), out_xi (m x r_hat row-major,
+ * zero padded), out_count = the basis size, out_exhausted. */
+int lrnr_host_eim_greedy(int64_t m, int64_t n_cols, const double* snapshots, int64_t r_hat, int64_t* out_idx,
+                         double* out_xi, int64_t* out_count, int* out_exhausted);
+/* reduction::build_fastparams (reduction.cpp:240-283) from given EIM bases:
+ * red (L-1), indices ((L-1) x r_hat), xi (per inner layer M_l x r_hat
+ * row-major, concatenated) -> out_fparams (the lrnr_host_build_fast layout). */
+int lrnr_host_build_fastparams(int depth, const int64_t* widths, const int64_t* ranks, const double* params,
+                               int act, int64_t r_hat, const int64_t* red, const int64_t* indices,
+                               const double* xi, double* out_fparams);
+
+/* ---- FastLRNR construction on the device ---------
+ * lrnr_gpu_eim_greedy replaces reduction::eim_greedy (reduction.cpp:150-238):
+ * the residual sweep over all snapshot columns runs on the device, one thread
+ * per column, in the reference's FP64 operation order (the x86-64-v3 build
+ * contracts a*b+c to FMA; so does this), so indices and basis columns are
+ * bit-identical to lrnr_host_eim_greedy on the same snapshots. Same outputs.
+ * lrnr_gpu_build_fast replaces harvest_snapshots + eim_greedy +
+ * build_fastparams (reduction.cpp:111-283; lrnr_host_build_fast's signature
+ * plus ctx): the hidden-state harvest is a device forward pass (activation
+ * values may differ from libm in the last ulp), every inner layer's greedy
+ * sweep runs concurrently on the device, and the O(r_hat^2 r) assembly of the
+ * reduced matrices runs on the host.
+ * lrnr_gpu_harvest_snapshots is reduction::harvest_snapshots alone: the inner
+ * layers' M_l x n_cols snapshot blocks (row-major, concatenated) to the host. */
+int lrnr_gpu_harvest_snapshots(lrnr_gpu_ctx* ctx, int depth, const int64_t* widths, const int64_t* ranks,
+                               const double* params, int act, const double* s, int64_t n_mu, int64_t nx,
+                               int64_t nt, int64_t n_perturb, double sigma, uint64_t seed,
+                               double* out_snapshots);
+int lrnr_gpu_eim_greedy(lrnr_gpu_ctx* ctx, int64_t m, int64_t n_cols, const double* snapshots, int64_t r_hat,
+                        int64_t* out_idx, double* out_xi, int64_t* out_count, int* out_exhausted);
+int lrnr_gpu_build_fast(lrnr_gpu_ctx* ctx, int depth, const int64_t* widths, const int64_t* ranks,
+                        const double* params, int act, const double* s, int64_t n_mu, int64_t nx, int64_t nt,
+                        int64_t n_perturb, double sigma, uint64_t seed, int64_t r_hat, int64_t* out_red,
+                        int64_t* out_indices, double* out_fparams, int* out_exhausted);
+
 #ifdef __cplusplus
 }
 #endif

@@ -566,6 +566,18 @@ class Reference:
         F = F[:fast_param_count(rv, red)]
         return dict(red_ranks=red, indices=idx.reshape(L - 1, r_hat), fparams=F, exhausted=exh)
 
+    def eim_greedy(self, S, r_hat):
+        """reduction::eim_greedy itself on an M x n_cols snapshot matrix."""
+        S = _f64(S)
+        m, n = S.shape
+        idx = np.zeros(r_hat, np.int64)
+        xi = np.zeros((m, r_hat))
+        cnt, ex = C.c_int64(0), C.c_int(0)
+        self._rc(self.lib.ref_eim_greedy(C.c_int64(m), C.c_int64(n), _ptr(S), C.c_int64(r_hat), _ptr(idx), _ptr(xi),
+                                         C.byref(cnt), C.byref(ex)), "eim_greedy")
+        k = cnt.value
+        return dict(indices=idx[:k].copy(), xi=xi[:, :k].copy(), exhausted=bool(ex.value))
+
     def identity_fast(self, widths, ranks, P):
         wv, rv = _i64(widths), _i64(ranks)
         red = wv[1:-1].copy()

@@ -856,6 +856,26 @@ int ref_build_fast(int L, const int64_t* widths, const int64_t* ranks, const dou
     });
 }
 
+// reduction::eim_greedy (reduction.cpp:150-238) on a given M x n_cols row-major
+// snapshot matrix: the pin for lrnr_host_eim_greedy / lrnr_gpu_eim_greedy.
+int ref_eim_greedy(int64_t m, int64_t n_cols, const double* snaps, int64_t r_hat, int64_t* out_idx,
+                   double* out_xi, int64_t* out_count, int* out_exhausted) {
+    return guarded([&] {
+        DenseMatrix S(static_cast<std::size_t>(m), static_cast<std::size_t>(n_cols));
+        for (std::size_t i = 0; i < S.data.size(); ++i) S.data[i] = snaps[i];
+        const reduction::EimBasis e = reduction::eim_greedy(S, static_cast<std::size_t>(r_hat));
+        const int64_t k = static_cast<int64_t>(e.dim());
+        for (int64_t q = 0; q < r_hat; ++q)
+            out_idx[q] = q < k ? static_cast<int64_t>(e.indices[static_cast<std::size_t>(q)]) : -1;
+        for (int64_t i = 0; i < m; ++i)
+            for (int64_t q = 0; q < r_hat; ++q)
+                out_xi[i * r_hat + q] =
+                    q < k ? e.xi.at(static_cast<std::size_t>(i), static_cast<std::size_t>(q)) : 0.0;
+        *out_count = k;
+        *out_exhausted = e.exhausted ? 1 : 0;
+    });
+}
+
 // Identity reduction (reduction.cpp:285-296) -> FastParams.
 int ref_identity_fast(int L, const int64_t* widths, const int64_t* ranks, const double* params,
                       double* out_fparams) {

@@ -148,29 +148,91 @@ def sample_collocation(seed, n_interior, lo=(0.0, 0.0, 0.0), hi=(0.0, 0.0, 0.0),
     return (xt, mu[:3 * n_interior].reshape(n_interior, 3)) if with_mu else xt
 
 
-def build_fast(model: LrnrParams, s, nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777, r_hat=10) -> FastParams:
-    """harvest_snapshots + eim_greedy + build_fastparams (reduction.cpp:111-283)."""
-    lib = _lib.load()
+def _fast_buffers(model: LrnrParams, r_hat):
     L = model.depth
-    S = _f64(s).reshape(-1, model.r_total)
-    red = np.zeros(L - 1, np.int64)
-    idx = np.zeros((L - 1) * r_hat, np.int64)
     nF = 2 * int(model.ranks[0])
     for l in range(L - 1):
         nF += r_hat * int(model.ranks[l]) + r_hat + r_hat * int(model.ranks[l + 1])
     nF += int(model.ranks[-1]) + 1
-    F = np.zeros(nF)
-    exh = np.zeros(L - 1, np.int32)
-    rc = lib.lrnr_host_build_fast(L, _p(model.widths), _p(model.ranks), _p(_f64(model.params)), model.act, _p(S),
-                                  S.shape[0], nx, nt, n_perturb, C.c_double(sigma), C.c_uint64(seed), r_hat,
-                                  _p(red), _p(idx), _p(F), exh.ctypes.data_as(C.c_void_p))
-    if rc != 0:
-        raise ValueError("build_fast: reduction failed (shape error or singular interpolation block)")
+    return np.zeros(L - 1, np.int64), np.zeros((L - 1) * r_hat, np.int64), np.zeros(nF), np.zeros(L - 1, np.int32)
+
+
+def _fast_result(model: LrnrParams, r_hat, red, idx, F, exh) -> FastParams:
+    L = model.depth
     used = 2 * int(model.ranks[0])
     for l in range(L - 1):
         used += int(red[l]) * (int(model.ranks[l]) + 1 + int(model.ranks[l + 1]))
     used += int(model.ranks[-1]) + 1
     return FastParams(model.ranks.copy(), red, F[:used], model.act, idx.reshape(L - 1, r_hat), exh)
+
+
+def build_fast(model: LrnrParams, s, nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777, r_hat=10) -> FastParams:
+    """harvest_snapshots + eim_greedy + build_fastparams (reduction.cpp:111-283), on the host.
+    GpuContext.build_fast is the device path."""
+    lib = _lib.load()
+    S = _f64(s).reshape(-1, model.r_total)
+    red, idx, F, exh = _fast_buffers(model, r_hat)
+    rc = lib.lrnr_host_build_fast(model.depth, _p(model.widths), _p(model.ranks), _p(_f64(model.params)), model.act,
+                                  _p(S), S.shape[0], nx, nt, n_perturb, C.c_double(sigma), C.c_uint64(seed), r_hat,
+                                  _p(red), _p(idx), _p(F), exh.ctypes.data_as(C.c_void_p))
+    if rc != 0:
+        raise ValueError("build_fast: reduction failed (shape error or singular interpolation block)")
+    return _fast_result(model, r_hat, red, idx, F, exh)
+
+
+def harvest_points(n_mu=1, nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777):
+    """The (x, t) columns harvest_snapshots evaluates (reduction.cpp:111-148), (n_mu*nx*nt*(1+n_perturb), 2)."""
+    n = n_mu * nx * nt * (1 + n_perturb)
+    out = np.zeros(2 * n)
+    rc = _lib.load().lrnr_host_harvest_points(n_mu, nx, nt, n_perturb, C.c_double(sigma), C.c_uint64(seed), _p(out))
+    if rc != 0:
+        raise ValueError("harvest_points: bad arguments")
+    return out.reshape(n, 2)
+
+
+def _eim_call(fn, lead, S, r_hat, what):
+    S = _f64(S)
+    if S.ndim != 2:
+        raise ValueError(what + ": snapshots must be a 2-D (M x n_cols) array")
+    m, n = S.shape
+    idx = np.zeros(max(r_hat, 1), np.int64)
+    xi = np.zeros((m, max(r_hat, 1)))
+    cnt, ex = C.c_int64(0), C.c_int(0)
+    rc = fn(*lead, m, n, _p(S), r_hat, _p(idx), _p(xi), C.byref(cnt), C.byref(ex))
+    return rc, dict(indices=idx[:cnt.value].copy(), xi=xi[:, :cnt.value].copy(), exhausted=bool(ex.value))
+
+
+def eim_greedy(S, r_hat):
+    """reduction::eim_greedy (reduction.cpp:150-238) on the host: dict(indices, xi (M x r), exhausted)."""
+    rc, out = _eim_call(_lib.load().lrnr_host_eim_greedy, (), S, r_hat, "eim_greedy")
+    if rc != 0:
+        raise ValueError("eim_greedy: bad snapshots/budget or singular interpolation block")
+    return out
+
+
+def build_fastparams(model: LrnrParams, bases, r_hat=None) -> FastParams:
+    """reduction::build_fastparams (reduction.cpp:240-283) from per-inner-layer EIM bases
+    (dicts with 'indices' and 'xi', as eim_greedy returns)."""
+    L = model.depth
+    if len(bases) != L - 1:
+        raise ValueError("build_fastparams: one basis per inner layer")
+    r_hat = r_hat or max(len(b["indices"]) for b in bases)
+    red, idx, F, exh = _fast_buffers(model, r_hat)
+    xi = []
+    for l, b in enumerate(bases):
+        k = len(b["indices"])
+        red[l] = k
+        idx[l * r_hat:l * r_hat + k] = b["indices"]
+        idx[l * r_hat + k:(l + 1) * r_hat] = -1
+        x = np.zeros((int(model.widths[l + 1]), r_hat))
+        x[:, :k] = _f64(b["xi"])[:, :k]
+        xi.append(x.reshape(-1))
+        exh[l] = int(b.get("exhausted", False))
+    rc = _lib.load().lrnr_host_build_fastparams(L, _p(model.widths), _p(model.ranks), _p(_f64(model.params)),
+                                                model.act, r_hat, _p(red), _p(idx), _p(np.concatenate(xi)), _p(F))
+    if rc != 0:
+        raise ValueError("build_fastparams: bad bases or singular interpolation block")
+    return _fast_result(model, r_hat, red, idx, F, exh)
 
 
 # ---------------------------------------------------------------------------
@@ -342,6 +404,38 @@ class GpuContext:
         self._rc(fn(self.h, *args, _p(s), C.byref(bl), C.byref(be), _p(losses), C.byref(nr), C.byref(fl)), "solve")
         return dict(s=s, best_loss=bl.value, best_epoch=be.value, losses=losses[:nr.value], aborted=bool(fl.value & 1),
                     diverged=bool(fl.value & 2))
+
+    def eim_greedy(self, S, r_hat):
+        """reduction::eim_greedy (reduction.cpp:150-238) on the device; bit-identical to eim_greedy()."""
+        rc, out = _eim_call(self.lib.lrnr_gpu_eim_greedy, (self.h,), S, r_hat, "eim_greedy")
+        self._rc(rc, "eim_greedy")
+        return out
+
+    def harvest_snapshots(self, model: LrnrParams, s, nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777):
+        """reduction::harvest_snapshots (reduction.cpp:111-148) on the device: one M_l x n_cols array per inner layer."""
+        S = _f64(s).reshape(-1, model.r_total)
+        n = S.shape[0] * nx * nt * (1 + n_perturb)
+        rows = [int(w) for w in model.widths[1:-1]]
+        out = np.zeros(sum(rows) * n)
+        self._rc(self.lib.lrnr_gpu_harvest_snapshots(self.h, model.depth, _p(model.widths), _p(model.ranks),
+                                                     _p(_f64(model.params)), model.act, _p(S), S.shape[0], nx, nt,
+                                                     n_perturb, C.c_double(sigma), C.c_uint64(seed), _p(out)),
+                 "harvest_snapshots")
+        blocks, o = [], 0
+        for m in rows:
+            blocks.append(out[o:o + m * n].reshape(m, n))
+            o += m * n
+        return blocks
+
+    def build_fast(self, model: LrnrParams, s, nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777, r_hat=10) -> FastParams:
+        """harvest_snapshots + eim_greedy on the device, build_fastparams on the host (reduction.cpp:111-283)."""
+        S = _f64(s).reshape(-1, model.r_total)
+        red, idx, F, exh = _fast_buffers(model, r_hat)
+        self._rc(self.lib.lrnr_gpu_build_fast(self.h, model.depth, _p(model.widths), _p(model.ranks),
+                                              _p(_f64(model.params)), model.act, _p(S), S.shape[0], nx, nt, n_perturb,
+                                              C.c_double(sigma), C.c_uint64(seed), r_hat, _p(red), _p(idx), _p(F),
+                                              exh.ctypes.data_as(C.c_void_p)), "build_fast")
+        return _fast_result(model, r_hat, red, idx, F, exh)
 
     def l1_error(self, model, s, ref_values, n_x, n_t):
         """l1_relative_error (pde.cpp:166-178) of the model against a GridField ((n_t+1) x n_x)."""

@@ -167,6 +167,8 @@ struct lrnr_gpu_ctx {
     // boundary points (lrnr_gpu_set_boundary): [initial (x, 0)] [periodic (0, t), (2pi, t)] pairs
     lrnr_b200::detail::DevBuf bnd_pts, bnd_x, bnd_spec, bnd_jets;
     int64_t n_ic = 0, n_bc = 0;
+    // FastLRNR construction (eim.cu): snapshots + inputs, greedy-loop state
+    lrnr_b200::detail::DevBuf eim_snaps, eim_state;
     // solve loops (lrnr_gpu_fine_tune / lrnr_gpu_fast_solve)
     lrnr_b200::detail::DevBuf solve_rows, solve_state, solve_m, solve_v, solve_best, solve_s0, solve_bt, solve_losses,
         solve_pts[2], solve_bnd[2], solve_sinx[2];
@@ -364,6 +366,38 @@ void launch_v2(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
     reduce_units_kernel<T><<<rg, 128, 0, ctx->stream>>>(ctx->part.as<T>(), g.units_per_inst, R1, n_inst, dev_out);
     CK(cudaGetLastError());
     ctx->launches += 2;
+}
+
+// Every C-ABI entry point runs its body through guarded(): C++ exceptions become
+// LRNR_E* codes plus ctx->err (lrnr_gpu_last_error).
+template <class F>
+int guarded(lrnr_gpu_ctx* ctx, F&& f) {
+    if (!ctx) return LRNR_EINVAL;
+    try {
+        CK(cudaSetDevice(ctx->device));
+        f();
+        ctx->err.clear();
+        return LRNR_OK;
+    } catch (const NonFinite& e) {
+        ctx->err = e.what();
+        ctx->tag = e.tag;
+        return LRNR_ENONFINITE;
+    } catch (const InvalidArg& e) {
+        ctx->err = e.what();
+        return LRNR_EINVAL;
+    } catch (const StateError& e) {
+        ctx->err = e.what();
+        return LRNR_ESTATE;
+    } catch (const std::bad_alloc&) {
+        ctx->err = "device allocation failed";
+        return LRNR_ENOMEM;
+    } catch (const CudaError& e) {
+        ctx->err = e.what();
+        return LRNR_ECUDA;
+    } catch (const std::exception& e) {
+        ctx->err = e.what();
+        return LRNR_EINVAL;
+    }
 }
 
 }  // namespace detail

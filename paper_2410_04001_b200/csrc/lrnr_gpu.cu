@@ -345,35 +345,6 @@ void build_tc(Model& m) {
 
 namespace {
 
-template <class F>
-int guarded(lrnr_gpu_ctx* ctx, F&& f) {
-    if (!ctx) return LRNR_EINVAL;
-    try {
-        CK(cudaSetDevice(ctx->device));
-        f();
-        ctx->err.clear();
-        return LRNR_OK;
-    } catch (const NonFinite& e) {
-        ctx->err = e.what();
-        ctx->tag = e.tag;
-        return LRNR_ENONFINITE;
-    } catch (const InvalidArg& e) {
-        ctx->err = e.what();
-        return LRNR_EINVAL;
-    } catch (const StateError& e) {
-        ctx->err = e.what();
-        return LRNR_ESTATE;
-    } catch (const std::bad_alloc&) {
-        ctx->err = "device allocation failed";
-        return LRNR_ENOMEM;
-    } catch (const CudaError& e) {
-        ctx->err = e.what();
-        return LRNR_ECUDA;
-    } catch (const std::exception& e) {
-        ctx->err = e.what();
-        return LRNR_EINVAL;
-    }
-}
 
 // ---------------------------------------------------------------------------
 // launch planning
@@ -1444,7 +1415,7 @@ int lrnr_gpu_destroy(lrnr_gpu_ctx* ctx) {
                       &ctx->solve_v, &ctx->solve_best, &ctx->solve_s0, &ctx->solve_bt, &ctx->solve_losses,
                       &ctx->solve_pts[0], &ctx->solve_pts[1], &ctx->solve_bnd[0], &ctx->solve_bnd[1],
                       &ctx->solve_sinx[0], &ctx->solve_sinx[1], &ctx->mb_pts, &ctx->mb_sinx, &ctx->mb_rows,
-                      &ctx->mb_sum})
+                      &ctx->mb_sum, &ctx->eim_snaps, &ctx->eim_state})
         b->release();
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;

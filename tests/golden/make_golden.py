@@ -154,6 +154,22 @@ def main():
     field = np.sin(xg[None, :] - 30.0 * tg[:, None])
     g.update(l1_field=field, l1_value=np.array([R.l1_error(w0, r0, P0, s0, field, nx, nt)]))
 
+    # reduction::eim_greedy on fixed snapshot matrices (stored: the GPU box must
+    # not recompute them with its own libm): hidden-state-like tanh features, a
+    # rank-5 set that exhausts the budget, duplicated columns (argmax ties) and
+    # the 64-row / r_hat = 64 maximum of the device path
+    rng = np.random.default_rng(2410)
+    Xa = rng.uniform(-1.0, 1.0, (2, 972))
+    Sa = np.tanh(rng.normal(0, 1, (32, 16)) @ np.tanh(rng.normal(0, 1.5, (16, 2)) @ Xa + rng.normal(0, 0.3, (16, 1))))
+    Sb = rng.normal(0, 1, (16, 5)) @ rng.normal(0, 1, (5, 300))
+    base = rng.normal(0, 1, (8, 20))
+    Sc = np.repeat(base, 2, axis=1)
+    Sd = np.tanh(rng.normal(0, 1, (64, 600)))
+    for tag, S, r in (("a", Sa, 32), ("b", Sb, 12), ("c", Sc, 6), ("d", Sd, 64)):
+        e = R.eim_greedy(S, r)
+        g.update({f"eim_{tag}_S": S, f"eim_{tag}_idx": e["indices"], f"eim_{tag}_xi": e["xi"],
+                  f"eim_{tag}_exh": np.array([int(e["exhausted"])]), f"eim_{tag}_rhat": np.array([r])})
+
     path = os.path.join(OUT, "reference_golden.npz")
     np.savez_compressed(path, **g)
     print("wrote", path, os.path.getsize(path), "bytes;", len(g), "arrays")

@@ -43,6 +43,58 @@ def test_eim_reduction_bit_exact_c2(golden):
     assert np.array_equal(f.fparams, golden["c2_fparams"])
 
 
+EIM_TAGS = ["a", "b", "c", "d"]
+
+
+@pytest.mark.parametrize("tag", EIM_TAGS)
+def test_host_eim_greedy_bit_exact(golden, tag):
+    """lrnr_host_eim_greedy == reduction::eim_greedy bit-for-bit (indices, basis columns,
+    exhaustion) on the golden snapshot sets: tanh features, rank-deficient (exhausts the
+    budget), duplicated columns (argmax ties), 64 rows with r_hat = 64."""
+    e = pkg.eim_greedy(golden[f"eim_{tag}_S"], int(golden[f"eim_{tag}_rhat"][0]))
+    assert np.array_equal(e["indices"], golden[f"eim_{tag}_idx"])
+    assert np.array_equal(e["xi"], golden[f"eim_{tag}_xi"])
+    assert e["exhausted"] == bool(golden[f"eim_{tag}_exh"][0])
+
+
+def test_eim_greedy_rejects_bad_input():
+    with pytest.raises(ValueError):
+        pkg.eim_greedy(np.ones((4, 3)), 0)
+    with pytest.raises(ValueError):
+        pkg.eim_greedy(np.zeros((4, 0)), 2)
+    with pytest.raises(ValueError):
+        pkg.eim_greedy(np.zeros((4, 3)), 2)  # all-zero snapshots: no basis vector selected
+
+
+def numpy_hidden_states(m, s, pts):
+    """hidden_states (model.cpp:407-428) for many points at once, FP64 numpy."""
+    offs, _ = m.offsets()
+    P, z, so, out = m.params, pts.T, 0, []
+    for l in range(m.depth - 1):
+        w0, w1, r = int(m.widths[l]), int(m.widths[l + 1]), int(m.ranks[l])
+        oU, oV, ob = offs[l]
+        U, V, b = P[oU:oU + w1 * r].reshape(w1, r), P[oV:oV + w0 * r].reshape(w0, r), P[ob:ob + w1]
+        y = (V.T @ z) * s[so:so + r, None]
+        z = np.tanh(U @ y + b[:, None])
+        out.append(z)
+        so += r
+    return out
+
+
+def test_harvest_points_and_build_fastparams_compose(golden):
+    """harvest_points -> hidden states -> eim_greedy per layer -> build_fastparams reproduces
+    build_fast (and so the reference's c1 reduction): the pieces the device path uses."""
+    m = pkg.LrnrParams(golden["c0_widths"], golden["c0_ranks"], golden["c0_params"], pkg.ACT_TANH)
+    X = pkg.harvest_points(1, 4, 3, 8, 0.05, 777)
+    assert X.shape == (108, 2)
+    assert np.all((X[:, 0] >= 0) & (X[:, 0] <= 2 * np.pi) & (X[:, 1] >= 0) & (X[:, 1] <= 1))
+    assert np.array_equal(X[::9, 0], np.tile(2 * np.pi * np.arange(4) / 3, 3))
+    bases = [pkg.eim_greedy(S, 10) for S in numpy_hidden_states(m, golden["c0_s"], X)]
+    f = pkg.build_fastparams(m, bases, r_hat=10)
+    assert np.array_equal(f.indices, golden["c1_indices"])
+    assert np.allclose(f.fparams, golden["c1_fparams"], rtol=1e-9, atol=1e-12)
+
+
 def test_eim_rejects_bad_shapes():
     m = pkg.LrnrParams(np.array([2, 4, 1]), np.array([3, 1]), np.zeros(64))
     with pytest.raises(ValueError):
