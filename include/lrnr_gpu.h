@@ -340,12 +340,14 @@ int lrnr_host_build_fast(int depth, const int64_t* widths, const int64_t* ranks,
                          int64_t r_hat, int64_t* out_red, int64_t* out_indices,
                          double* out_fparams, int* out_exhausted);
 
-/* The points harvest_snapshots evaluates (reduction.cpp:111-148 with
- * SamplingSetX::uniform_grid, reduction.cpp:10-25): n_mu x (nx*nt) x (1+n_perturb)
- * (x, t) pairs in column order (mu, point, perturbation); the perturbations
- * use the reference's Rng stream bit-identically. */
-int lrnr_host_harvest_points(int64_t n_mu, int64_t nx, int64_t nt, int64_t n_perturb, double sigma,
-                             uint64_t seed, double* out_xt);
+/* SamplingSetX::uniform_grid (reduction.cpp:10-25): nx * nt (x, t) pairs, x fastest. */
+int lrnr_host_uniform_grid(int64_t nx, int64_t nt, double* out_xt);
+/* The columns harvest_snapshots evaluates (reduction.cpp:111-148): for each of
+ * n_mu coefficient vectors and each of the n_sampling points, the point then
+ * n_perturb Gaussian perturbations (sigma * extent, clamped), from the
+ * reference's Rng stream bit-identically: n_mu * n_sampling * (1+n_perturb) pairs. */
+int lrnr_host_harvest_points(const double* sampling_xt, int64_t n_sampling, int64_t n_mu, int64_t n_perturb,
+                             double sigma, uint64_t seed, double* out_xt);
 /* reduction::eim_greedy (reduction.cpp:150-238) on one m x n_cols row-major
  * snapshot matrix: out_idx (r_hat, -1 padded), out_xi (m x r_hat row-major,
  * zero padded), out_count = the basis size, out_exhausted. */
@@ -370,12 +372,13 @@ int lrnr_host_build_fastparams(int depth, const int64_t* widths, const int64_t* 
  * values may differ from libm in the last ulp), every inner layer's greedy
  * sweep runs concurrently on the device, and the O(r_hat^2 r) assembly of the
  * reduced matrices runs on the host.
- * lrnr_gpu_harvest_snapshots is reduction::harvest_snapshots alone: the inner
- * layers' M_l x n_cols snapshot blocks (row-major, concatenated) to the host. */
+ * lrnr_gpu_harvest_snapshots is reduction::harvest_snapshots alone, for any
+ * SamplingSetX (sampling_xt, n_sampling points): the inner layers' M_l x n_cols
+ * snapshot blocks (row-major, concatenated) to the host. */
 int lrnr_gpu_harvest_snapshots(lrnr_gpu_ctx* ctx, int depth, const int64_t* widths, const int64_t* ranks,
-                               const double* params, int act, const double* s, int64_t n_mu, int64_t nx,
-                               int64_t nt, int64_t n_perturb, double sigma, uint64_t seed,
-                               double* out_snapshots);
+                               const double* params, int act, const double* s, int64_t n_mu,
+                               const double* sampling_xt, int64_t n_sampling, int64_t n_perturb, double sigma,
+                               uint64_t seed, double* out_snapshots);
 int lrnr_gpu_eim_greedy(lrnr_gpu_ctx* ctx, int64_t m, int64_t n_cols, const double* snapshots, int64_t r_hat,
                         int64_t* out_idx, double* out_xi, int64_t* out_count, int* out_exhausted);
 int lrnr_gpu_build_fast(lrnr_gpu_ctx* ctx, int depth, const int64_t* widths, const int64_t* ranks,

@@ -248,6 +248,80 @@ public:
         return out;
     }
 
+    // ---- FastLRNR construction (reduction.cpp:111-238) on the device ----
+    // reduction::harvest_snapshots: s(mu) from the reference's own hyper_forward
+    // (host), the perturbation stream from the reference's Rng (host,
+    // bit-identical), the hidden states on the device (bit-identical for tanh).
+    reduction::SnapshotSet harvest_snapshots(const LrnrParams& p, const HyperParams& theta,
+                                             const reduction::SamplingSetX& sampling, std::size_t n_perturb,
+                                             double sigma_factor, const std::vector<PdeParams>& mu_grid,
+                                             std::uint64_t seed, int act = LRNR_ACT_TANH) {
+        std::vector<double> flat, s, X;
+        for (std::size_t l = 0; l < p.depth(); ++l) {
+            flat.insert(flat.end(), p.u[l].data.begin(), p.u[l].data.end());
+            flat.insert(flat.end(), p.v[l].data.begin(), p.v[l].data.end());
+            flat.insert(flat.end(), p.b[l].data.begin(), p.b[l].data.end());
+        }
+        for (const PdeParams& mu : mu_grid) {
+            const std::vector<double> c = flatten(hyper_forward(mu, theta));
+            s.insert(s.end(), c.begin(), c.end());
+        }
+        for (const pde::Point& q : sampling.points) {
+            X.push_back(q.x);
+            X.push_back(q.t);
+        }
+        const std::vector<int64_t> w(p.widths.begin(), p.widths.end()), r(p.ranks.begin(), p.ranks.end());
+        const int64_t n_x = static_cast<int64_t>(sampling.points.size()), n_mu = static_cast<int64_t>(mu_grid.size());
+        const int64_t n_cols = n_mu * n_x * static_cast<int64_t>(1 + n_perturb);
+        std::size_t rows = 0;
+        for (std::size_t l = 0; l + 1 < p.depth(); ++l) rows += p.widths[l + 1];
+        std::vector<double> out(rows * static_cast<std::size_t>(n_cols)), pts(2 * static_cast<std::size_t>(n_cols));
+        check(lrnr_gpu_harvest_snapshots(ctx_, static_cast<int>(p.depth()), w.data(), r.data(), flat.data(), act,
+                                         s.data(), n_mu, X.data(), n_x, static_cast<int64_t>(n_perturb), sigma_factor,
+                                         seed, out.data()));
+        if (lrnr_host_harvest_points(X.data(), n_x, n_mu, static_cast<int64_t>(n_perturb), sigma_factor, seed,
+                                     pts.data()) != LRNR_OK)
+            throw std::invalid_argument("harvest_snapshots: bad sampling set");
+        reduction::SnapshotSet set;
+        std::size_t o = 0;
+        for (std::size_t l = 0; l + 1 < p.depth(); ++l) {
+            DenseMatrix m(p.widths[l + 1], static_cast<std::size_t>(n_cols));
+            std::copy(out.begin() + static_cast<std::ptrdiff_t>(o), out.begin() + static_cast<std::ptrdiff_t>(o + m.data.size()),
+                      m.data.begin());
+            o += m.data.size();
+            set.layers.push_back(std::move(m));
+        }
+        std::size_t col = 0;
+        for (std::size_t mi = 0; mi < mu_grid.size(); ++mi)
+            for (std::size_t pi = 0; pi < sampling.points.size(); ++pi)
+                for (std::size_t k = 0; k <= n_perturb; ++k, ++col)
+                    set.tags.push_back({mi, pi, k, pde::Point{pts[2 * col], pts[2 * col + 1]}, mu_grid[mi]});
+        return set;
+    }
+    // reduction::eim_greedy: the greedy sweeps on the device, bit-identical indices
+    // and basis columns; the block LU is refactored with the reference's lu_factor.
+    reduction::EimBasis eim_greedy(const DenseMatrix& snapshots, std::size_t r_hat) {
+        const int64_t m = static_cast<int64_t>(snapshots.rows), rh = static_cast<int64_t>(r_hat);
+        std::vector<int64_t> idx(r_hat > 0 ? r_hat : 1);
+        std::vector<double> xi(snapshots.rows * (r_hat > 0 ? r_hat : 1));
+        int64_t count = 0;
+        int exhausted = 0;
+        check(lrnr_gpu_eim_greedy(ctx_, m, static_cast<int64_t>(snapshots.cols), snapshots.data.data(), rh, idx.data(),
+                                  xi.data(), &count, &exhausted));
+        reduction::EimBasis b;
+        b.xi = DenseMatrix(snapshots.rows, static_cast<std::size_t>(count));
+        for (int64_t i = 0; i < m; ++i)
+            for (int64_t k = 0; k < count; ++k)
+                b.xi.at(static_cast<std::size_t>(i), static_cast<std::size_t>(k)) = xi[i * rh + k];
+        for (int64_t k = 0; k < count; ++k) b.indices.push_back(static_cast<std::size_t>(idx[k]));
+        b.exhausted = exhausted != 0;
+        DenseMatrix block(b.indices.size(), b.indices.size());
+        for (std::size_t i = 0; i < b.indices.size(); ++i)
+            for (std::size_t j = 0; j < b.indices.size(); ++j) block.at(i, j) = b.xi.at(b.indices[i], j);
+        b.block_lu = lu_factor(block);
+        return b;
+    }
+
     lrnr_gpu_ctx* handle() { return ctx_; }
 
 private:

@@ -25,7 +25,7 @@ EXPORTS = (
     "lrnr_gpu_loss", "lrnr_gpu_upload_coeffs", "lrnr_gpu_run", "lrnr_gpu_check", "lrnr_gpu_download",
     "lrnr_gpu_fma_peak",
     "lrnr_host_make_baseline_model", "lrnr_host_make_hyper_params", "lrnr_host_sample_collocation",
-    "lrnr_host_build_fast", "lrnr_host_harvest_points", "lrnr_host_eim_greedy", "lrnr_host_build_fastparams",
+    "lrnr_host_build_fast", "lrnr_host_harvest_points", "lrnr_host_uniform_grid", "lrnr_host_eim_greedy", "lrnr_host_build_fastparams",
     "lrnr_gpu_eim_greedy", "lrnr_gpu_build_fast", "lrnr_gpu_harvest_snapshots",
 )
 
@@ -106,11 +106,12 @@ def load() -> C.CDLL:
     lib.lrnr_host_sample_collocation.argtypes = [C.c_uint64, i64, dp, dp, ip, dp, dp]
     lib.lrnr_host_build_fast.argtypes = [ip, dp, dp, dp, ip, dp, i64, i64, i64, i64, C.c_double, C.c_uint64, i64,
                                          dp, dp, dp, dp]
-    lib.lrnr_host_harvest_points.argtypes = [i64, i64, i64, i64, C.c_double, C.c_uint64, dp]
+    lib.lrnr_host_uniform_grid.argtypes = [i64, i64, dp]
+    lib.lrnr_host_harvest_points.argtypes = [dp, i64, i64, i64, C.c_double, C.c_uint64, dp]
     lib.lrnr_host_eim_greedy.argtypes = [i64, i64, dp, i64, dp, dp, dp, dp]
     lib.lrnr_host_build_fastparams.argtypes = [ip, dp, dp, dp, ip, i64, dp, dp, dp, dp]
     lib.lrnr_gpu_eim_greedy.argtypes = [vp, i64, i64, dp, i64, dp, dp, dp, dp]
-    lib.lrnr_gpu_harvest_snapshots.argtypes = [vp, ip, dp, dp, dp, ip, dp, i64, i64, i64, i64, C.c_double,
+    lib.lrnr_gpu_harvest_snapshots.argtypes = [vp, ip, dp, dp, dp, ip, dp, i64, dp, i64, i64, C.c_double,
                                                C.c_uint64, dp]
     lib.lrnr_gpu_build_fast.argtypes = [vp, ip, dp, dp, dp, ip, dp, i64, i64, i64, i64, C.c_double, C.c_uint64, i64,
                                         dp, dp, dp, dp]

@@ -180,11 +180,22 @@ def build_fast(model: LrnrParams, s, nx=4, nt=3, n_perturb=8, sigma=0.05, seed=7
     return _fast_result(model, r_hat, red, idx, F, exh)
 
 
-def harvest_points(n_mu=1, nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777):
-    """The (x, t) columns harvest_snapshots evaluates (reduction.cpp:111-148), (n_mu*nx*nt*(1+n_perturb), 2)."""
-    n = n_mu * nx * nt * (1 + n_perturb)
+def uniform_grid(nx=4, nt=3):
+    """SamplingSetX::uniform_grid (reduction.cpp:10-25): (nx*nt, 2) points, x fastest."""
+    out = np.zeros(2 * nx * nt)
+    if _lib.load().lrnr_host_uniform_grid(nx, nt, _p(out)) != 0:
+        raise ValueError("uniform_grid: bad sizes")
+    return out.reshape(-1, 2)
+
+
+def harvest_points(n_mu=1, nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777, X=None):
+    """The (x, t) columns harvest_snapshots evaluates (reduction.cpp:111-148) for the sampling
+    set X (default: uniform_grid(nx, nt)), (n_mu * len(X) * (1 + n_perturb), 2)."""
+    X = uniform_grid(nx, nt) if X is None else _f64(X).reshape(-1, 2)
+    n = n_mu * X.shape[0] * (1 + n_perturb)
     out = np.zeros(2 * n)
-    rc = _lib.load().lrnr_host_harvest_points(n_mu, nx, nt, n_perturb, C.c_double(sigma), C.c_uint64(seed), _p(out))
+    rc = _lib.load().lrnr_host_harvest_points(_p(X), X.shape[0], n_mu, n_perturb, C.c_double(sigma),
+                                              C.c_uint64(seed), _p(out))
     if rc != 0:
         raise ValueError("harvest_points: bad arguments")
     return out.reshape(n, 2)
@@ -411,15 +422,18 @@ class GpuContext:
         self._rc(rc, "eim_greedy")
         return out
 
-    def harvest_snapshots(self, model: LrnrParams, s, nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777):
-        """reduction::harvest_snapshots (reduction.cpp:111-148) on the device: one M_l x n_cols array per inner layer."""
+    def harvest_snapshots(self, model: LrnrParams, s, nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777, X=None):
+        """reduction::harvest_snapshots (reduction.cpp:111-148) on the device for the sampling set X
+        (default uniform_grid(nx, nt)): one M_l x n_cols array per inner layer."""
         S = _f64(s).reshape(-1, model.r_total)
-        n = S.shape[0] * nx * nt * (1 + n_perturb)
+        X = uniform_grid(nx, nt) if X is None else _f64(X).reshape(-1, 2)
+        n = S.shape[0] * X.shape[0] * (1 + n_perturb)
         rows = [int(w) for w in model.widths[1:-1]]
         out = np.zeros(sum(rows) * n)
         self._rc(self.lib.lrnr_gpu_harvest_snapshots(self.h, model.depth, _p(model.widths), _p(model.ranks),
-                                                     _p(_f64(model.params)), model.act, _p(S), S.shape[0], nx, nt,
-                                                     n_perturb, C.c_double(sigma), C.c_uint64(seed), _p(out)),
+                                                     _p(_f64(model.params)), model.act, _p(S), S.shape[0], _p(X),
+                                                     X.shape[0], n_perturb, C.c_double(sigma), C.c_uint64(seed),
+                                                     _p(out)),
                  "harvest_snapshots")
         blocks, o = [], 0
         for m in rows:

@@ -584,7 +584,7 @@ struct Harvest {
 // harvest_snapshots (reduction.cpp:111-148): points from the reference's Rng
 // stream on the host (bit-identical, one upload), hidden states on the device.
 Harvest harvest_device(lrnr_gpu_ctx* ctx, int L, const int64_t* widths, const int64_t* ranks, const double* params,
-                       int act, const double* s, int64_t n_mu, int64_t nx, int64_t nt, int64_t n_perturb,
+                       int act, const double* s, int64_t n_mu, const double* X, int64_t n_x, int64_t n_perturb,
                        double sigma, uint64_t seed) {
     require(widths && ranks && params && s, "null argument");
     require(L >= 2 && L <= EIM_MAX_LAYERS, "build_fastparams: need at least two layers");
@@ -595,11 +595,11 @@ Harvest harvest_device(lrnr_gpu_ctx* ctx, int L, const int64_t* widths, const in
         require(ranks[l] <= std::min(widths[l], widths[l + 1]), "LrnrParams: rank exceeds min(M_l, M_{l-1})");
         require(ranks[l] <= EIM_RMAX, "harvest_snapshots: device path supports ranks <= 64");
     }
-    require(n_mu >= 1 && nx >= 1 && nt >= 1 && n_perturb >= 0, "harvest_snapshots: bad sizes");
+    require(X != nullptr && n_mu >= 1 && n_x >= 1 && n_perturb >= 0, "harvest_snapshots: bad sizes");
     require(sigma > 0.0 || n_perturb == 0, "harvest_snapshots: sigma must be positive");
-    const int64_t per_mu = nx * nt * (1 + n_perturb), n_cols = n_mu * per_mu;
+    const int64_t per_mu = n_x * (1 + n_perturb), n_cols = n_mu * per_mu;
     std::vector<double> pts(static_cast<size_t>(2 * n_cols));
-    require(lrnr_host_harvest_points(n_mu, nx, nt, n_perturb, sigma, seed, pts.data()) == LRNR_OK,
+    require(lrnr_host_harvest_points(X, n_x, n_mu, n_perturb, sigma, seed, pts.data()) == LRNR_OK,
             "harvest_snapshots: point generation failed");
     HarvestNet net{};
     net.L = L;
@@ -669,11 +669,13 @@ int lrnr_gpu_eim_greedy(lrnr_gpu_ctx* ctx, int64_t m, int64_t n_cols, const doub
 }
 
 int lrnr_gpu_harvest_snapshots(lrnr_gpu_ctx* ctx, int L, const int64_t* widths, const int64_t* ranks,
-                               const double* params, int act, const double* s, int64_t n_mu, int64_t nx, int64_t nt,
-                               int64_t n_perturb, double sigma, uint64_t seed, double* out_snapshots) {
+                               const double* params, int act, const double* s, int64_t n_mu,
+                               const double* sampling_xt, int64_t n_sampling, int64_t n_perturb, double sigma,
+                               uint64_t seed, double* out_snapshots) {
     return guarded(ctx, [&] {
         require(out_snapshots != nullptr, "null argument");
-        const Harvest h = harvest_device(ctx, L, widths, ranks, params, act, s, n_mu, nx, nt, n_perturb, sigma, seed);
+        const Harvest h = harvest_device(ctx, L, widths, ranks, params, act, s, n_mu, sampling_xt, n_sampling,
+                                         n_perturb, sigma, seed);
         CK(cudaMemcpyAsync(out_snapshots, h.snaps, static_cast<size_t>(h.rows) * h.n_cols * sizeof(double),
                            cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
@@ -688,7 +690,11 @@ int lrnr_gpu_build_fast(lrnr_gpu_ctx* ctx, int L, const int64_t* widths, const i
         require(out_red && out_indices && out_fparams && out_exhausted, "null argument");
         require(r_hat >= 1, "eim_greedy: budget must be positive");
         require(r_hat <= EIM_RMAX, "eim_greedy: device path supports r_hat <= 64");
-        const Harvest h = harvest_device(ctx, L, widths, ranks, params, act, s, n_mu, nx, nt, n_perturb, sigma, seed);
+        require(nx >= 1 && nt >= 1, "uniform_grid: bad sizes");
+        std::vector<double> X(static_cast<size_t>(2 * nx * nt));
+        require(lrnr_host_uniform_grid(nx, nt, X.data()) == LRNR_OK, "uniform_grid: bad sizes");
+        const Harvest h =
+            harvest_device(ctx, L, widths, ranks, params, act, s, n_mu, X.data(), nx * nt, n_perturb, sigma, seed);
         EimLayers layers{};
         layers.n = L - 1;
         const double* S = h.snaps;

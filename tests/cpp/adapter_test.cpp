@@ -90,6 +90,44 @@ int main() {
     const double egf = floor_rel(gotf.grad, reff.grad);
     std::printf("FastLRNR gradient: value rel err %.3e, dL/ds floor-rel err %.3e\n", evf, egf);
 
+    // FastLRNR construction on the device == the reference's, bit for bit: c2 widths
+    // (deep layers exhaust the budget), a mu grid through a hypernetwork
+    bool eim_ok = true;
+    {
+        Rng rng2(2411);
+        LrnrParams p2 = make_lrnr_params({2, 256, 256, 256, 256, 256, 256, 1}, {2, 32, 32, 32, 32, 32, 1}, rng2,
+                                         true, 0.5);
+        HyperParams th = make_hyper_params(p2.ranks, 2, 16, ParamDomain{{1.0, 0.0, 0.0}, {40.0, 0.1, 10.0}}, rng2,
+                                           0.01, 0.5);
+        const std::vector<PdeParams> grid{{5.0, 0.01, 1.0}, {20.0, 0.05, 3.0}, {35.0, 0.09, 8.0}};
+        auto X2 = reduction::SamplingSetX::uniform_grid(4, 3);
+        auto ref_snaps = reduction::harvest_snapshots(p2, th, X2, 8, 0.05, grid, 99);
+        auto dev_snaps = eng.harvest_snapshots(p2, th, X2, 8, 0.05, grid, 99);
+        std::size_t snap_diff = 0;
+        for (std::size_t l = 0; l < ref_snaps.layers.size(); ++l)
+            for (std::size_t i = 0; i < ref_snaps.layers[l].data.size(); ++i)
+                snap_diff += ref_snaps.layers[l].data[i] != dev_snaps.layers[l].data[i];
+        for (std::size_t c = 0; c < ref_snaps.tags.size(); ++c)
+            snap_diff += ref_snaps.tags[c].point.x != dev_snaps.tags[c].point.x ||
+                         ref_snaps.tags[c].point.t != dev_snaps.tags[c].point.t;
+        std::vector<reduction::EimBasis> rb, db;
+        std::size_t basis_diff = 0;
+        for (std::size_t l = 0; l + 1 < p2.depth(); ++l) {
+            rb.push_back(reduction::eim_greedy(ref_snaps.layers[l], 32));
+            db.push_back(eng.eim_greedy(ref_snaps.layers[l], 32));
+            basis_diff += rb[l].indices != db[l].indices || rb[l].xi.data != db[l].xi.data ||
+                          rb[l].exhausted != db[l].exhausted;
+        }
+        FastParams fr = reduction::build_fastparams(p2, rb), fd = reduction::build_fastparams(p2, db);
+        std::size_t fast_diff = 0;
+        for (std::size_t l = 0; l + 1 < p2.depth(); ++l)
+            fast_diff += fr.u_hat[l].data != fd.u_hat[l].data || fr.v_hat[l].data != fd.v_hat[l].data ||
+                         fr.b_hat[l].data != fd.b_hat[l].data;
+        std::printf("FastLRNR construction: %zu snapshot / %zu basis / %zu factor mismatches (%zu columns)\n",
+                    snap_diff, basis_diff, fast_diff, ref_snaps.tags.size());
+        eim_ok = snap_diff == 0 && basis_diff == 0 && fast_diff == 0;
+    }
+
     // full fine-tune batch: interior + initial + periodic terms (PinnTermEmitter,
     // training.cpp:286-327) with the fine_tune weights 1/n per kind
     pde::CollocationBatch fb = pde::sample_collocation(4007, 1024, 256, 256, ParamDomain{}, false);
@@ -225,7 +263,7 @@ int main() {
     std::printf("NonFiniteError mapped: %s\n", threw ? "yes" : "NO");
     const bool ok = ev <= 1e-12 && eg <= 1e-10 && evf <= 1e-12 && egf <= 1e-10 && evb <= 1e-12 && ecb <= 1e-12 &&
                     egb <= 1e-10 && evp <= 1e-12 && egp <= 1e-10 && sft && eft <= 1e-10 && sfs && efs <= 1e-10 &&
-                    efs_s <= 1e-10 && threw;
+                    efs_s <= 1e-10 && threw && eim_ok;
     std::printf("%s\n", ok ? "ADAPTER PARITY OK" : "ADAPTER PARITY FAILED");
     return ok ? 0 : 1;
 }
