@@ -88,23 +88,25 @@ int lrnr_gpu_set_stream(lrnr_gpu_ctx* ctx, void* cuda_stream);
 /* Options.  LRNR_OPT_FAST_SINCOS (FP32 sin networks): 1 = sin/cos from the SFU
  * approximations after a Cody-Waite reduction (~4e-7 absolute), 0 = polynomial
  * sin/cos after a 3-term reduction (~1.5 ulp, default).  LRNR_OPT_KERNEL:
- * 0 = auto (default): FP32 LRNR with ranks <= 32 on the tcgen05 tensor-core
+ * 0 = auto (default): FP32 nets whose hidden widths and ranks are all <= 32
+ * (the FastLRNR) on the narrow-network kernel (lane pairs per point, whole net
+ * in shared memory), FP32 LRNR with ranks <= 32 on the tcgen05 tensor-core
  * tile kernel (3xTF32), other FP32/FP64 shapes with ranks <= 64 on the FMA
  * tile-GEMM kernel, the rest on the per-point streaming kernel;
  * batches below ~16 points per SM on the small-batch latency kernel (one CTA
  * per point, threads across neurons / ranks);
  * 1 = force the streaming kernel, 2 = tensor-core kernel wherever it applies
  * (also FastLRNR), 3 = FMA tile kernel (no tensor cores), 4 = small-batch
- * kernel at any size. */
+ * kernel at any size, 5 = narrow-network kernel wherever it applies. */
 #define LRNR_OPT_FAST_SINCOS 1
 #define LRNR_OPT_KERNEL 2
-#define LRNR_OPT_TILE_P 3
+#define LRNR_OPT_TILE_P 3   /* FP32 wide-layer tile: 64 points x 512 threads (default) or 32 x 256 (2 CTAs/SM) */
 /* LRNR_OPT_SOLVE (lrnr_gpu_fast_solve): 0 = auto: the persistent solver (one
  * thread-block cluster, one warp per loss term, the whole loop in one launch,
  * per-epoch reduction over distributed shared memory) when every width and
  * rank is <= 32 and the terms fit 8 CTAs x 16 warps; 1 = the graph path (one
  * captured epoch replayed per epoch). */
-#define LRNR_OPT_SOLVE 4   /* FP32 wide-layer tile: 64 points x 512 threads (default) or 32 x 256 (2 CTAs/SM) */
+#define LRNR_OPT_SOLVE 4
 int lrnr_gpu_set_option(lrnr_gpu_ctx* ctx, int opt, int value);
 /* Number of kernels this context has launched so far (instrumentation). */
 /* Kernels launched so far (instrumentation; no reference counterpart). */

@@ -17,6 +17,7 @@
 #include "pinn_v2.cuh"
 #include "pinn_small.cuh"
 #include "pinn_solve.cuh"
+#include "pinn_fast.cuh"
 
 namespace lrnr_b200 {
 namespace detail {
@@ -116,6 +117,13 @@ struct Model {
         std::vector<int> sched_cnt;
         DevBuf dblocks, dsched_off, dsched_bytes;
     } tc;
+    // narrow-network kernel (pinn_fast.cuh): every hidden width and rank <= 32
+    struct FK {
+        bool ok = false;
+        std::vector<int> np;
+        int blk_len = 0;
+        DevBuf dblk;
+    } fk;
 };
 
 struct Hyper {
@@ -133,6 +141,7 @@ void release_model(Model& m);
 void upload_model(Model& m);
 void build_v2(Model& m, bool meta = false);
 void build_tc(Model& m);
+void build_fk(Model& m);
 
 template <class T>
 DevNet<T> dev_net(const Model& m) {
@@ -399,6 +408,11 @@ int guarded(lrnr_gpu_ctx* ctx, F&& f) {
         return LRNR_EINVAL;
     }
 }
+
+// The narrow-network kernel (fast_launch.cu) when eligible: FP32, every hidden
+// width and rank <= 32, LRNR_OPT_KERNEL auto (0) or 5. Returns false otherwise.
+bool dispatch_fast(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
+                   double* dev_out);
 
 }  // namespace detail
 }  // namespace lrnr_b200

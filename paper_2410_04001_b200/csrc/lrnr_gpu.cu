@@ -89,6 +89,7 @@ void release_model(Model& m) {
     m.v2meta.dsched_off.release();
     m.v2meta.dsched_bytes.release();
     m.tc.dblocks.release();
+    m.fk.dblk.release();
     m.tc.dsched_off.release();
     m.tc.dsched_bytes.release();
     m.flat_dev.release();
@@ -726,6 +727,8 @@ double* run_resident(lrnr_gpu_ctx* ctx, const Model& m, double w, double* dev_ou
         dispatch_small<0>(ctx, m, ctx->s_dev.as<double>(), ctx->mu_dev.as<double>(), wt, dev_out, nullptr);
         return dev_out;
     }
+    if (MODE == 0 && dispatch_fast(ctx, m, ctx->s_dev.as<double>(), ctx->mu_dev.as<double>(), wt, dev_out))
+        return dev_out;
     if (MODE == 0 && dispatch_tc(ctx, m, ctx->s_dev.as<double>(), ctx->mu_dev.as<double>(), wt, dev_out))
         return dev_out;
     if (MODE == 0 && dispatch_v2(ctx, m, ctx->s_dev.as<double>(), ctx->mu_dev.as<double>(), wt, dev_out))
@@ -1179,7 +1182,8 @@ void solve_epoch(lrnr_gpu_ctx* ctx, const Model& m, const SolveRun& r) {
         PointSwap keep(ctx, r.int_pts, r.n_int);
         if (r.objective == LRNR_OBJ_SQUARED) {
             if (use_small(ctx, m)) dispatch_small<0>(ctx, m, sd, md, r.w_int, rows_int, nullptr);
-            else if (!dispatch_tc(ctx, m, sd, md, r.w_int, rows_int) && !dispatch_v2(ctx, m, sd, md, r.w_int, rows_int))
+            else if (!dispatch_fast(ctx, m, sd, md, r.w_int, rows_int) && !dispatch_tc(ctx, m, sd, md, r.w_int, rows_int) &&
+                     !dispatch_v2(ctx, m, sd, md, r.w_int, rows_int))
                 dispatch_pinn<0>(ctx, m, sd, md, r.w_int, rows_int, nullptr);
         } else {
             ctx->term_objective = 1;
@@ -1498,6 +1502,7 @@ int lrnr_gpu_set_lrnr(lrnr_gpu_ctx* ctx, int L, const int64_t* widths, const int
         upload_model(dst);
         build_v2(dst);
         build_tc(dst);
+        build_fk(dst);
     });
 }
 
@@ -1548,6 +1553,7 @@ int lrnr_gpu_set_fast(lrnr_gpu_ctx* ctx, int L, const int64_t* ranks, const int6
         upload_model(dst);
         build_v2(dst);
         build_tc(dst);
+        build_fk(dst);
     });
 }
 

@@ -9,7 +9,7 @@ ctx = pkg.GpuContext(0)
 st = torch.cuda.Stream(); torch.cuda.set_stream(st); ctx.set_stream(st.cuda_stream)
 ctx.set_fast(c['fast'], pkg.F32); ctx.set_points(c['pts']); ctx.upload_coeffs(c['s'], c['mu'])
 fl = pkg.fast_flops_per_point(c['fast'].ranks, c['fast'].red_ranks)
-for kern, tp in ((pkg.KERNEL_FMA_TILE, 64), (pkg.KERNEL_FMA_TILE, 32), (pkg.KERNEL_TC, 64)):
+for kern, tp in ((pkg.KERNEL_NARROW, 64), (pkg.KERNEL_FMA_TILE, 64), (pkg.KERNEL_TC, 64)):
     ctx.set_option(pkg.OPT_KERNEL, kern)
     ctx.set_option(pkg.OPT_TILE_P, tp)
     ctx.set_fast(c['fast'], pkg.F32)

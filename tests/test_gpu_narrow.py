@@ -1,0 +1,110 @@
+"""B200: the narrow-network kernel (csrc/pinn_fast.cuh), the auto choice for FP32
+FastLRNR: against the FP64 C oracle (emit_fast_jet + run_batch_gradient
+restated) and the FMA tile kernel, on ragged tiles, several instances, both
+activations and sincos modes, odd reduced widths, term specs, non-finite input
+and bitwise reproducibility."""
+import numpy as np
+import pytest
+
+import paper_2410_04001_b200 as pkg
+from conftest import normwise
+
+pytestmark = pytest.mark.gpu
+
+TOL32_NORM = 1e-4
+TOL32_LOSS = 1e-4
+
+
+@pytest.fixture
+def narrow(gpu):
+    gpu.set_option(pkg.OPT_KERNEL, pkg.KERNEL_NARROW)
+    yield gpu
+    gpu.set_option(pkg.OPT_KERNEL, pkg.KERNEL_AUTO)
+    gpu.set_option(pkg.OPT_FAST_SINCOS, 0)
+
+
+@pytest.mark.parametrize("act,fast_sincos", [(pkg.ACT_SIN, 0), (pkg.ACT_SIN, 1), (pkg.ACT_TANH, 0)])
+@pytest.mark.parametrize("n", [1, 15, 17, 129, 3000])
+def test_c2_fast_matches_oracle(narrow, oracle, act, fast_sincos, n):
+    narrow.set_option(pkg.OPT_FAST_SINCOS, fast_sincos)
+    c = pkg.config2(n_points=n, act=act)
+    f = c["fast"]
+    narrow.set_fast(f, pkg.F32)
+    narrow.set_points(c["pts"])
+    got = narrow.loss_grad_s(pkg.MODEL_FAST, c["s"], c["mu"])
+    want = oracle.fast_grad(f.ranks, f.red_ranks, f.fparams, c["s"], c["mu"], c["pts"], act=act)
+    assert abs(got["value"] - want["value"]) <= TOL32_LOSS * abs(want["value"])
+    assert normwise(got["grad_s"], want["grad_s"]) <= TOL32_NORM
+
+
+def test_auto_picks_narrow_and_agrees_with_fma_tile(gpu):
+    c = pkg.config2(n_points=20000, act=pkg.ACT_SIN)
+    gpu.set_fast(c["fast"], pkg.F32)
+    gpu.set_points(c["pts"])
+    auto = gpu.loss_grad_s(pkg.MODEL_FAST, c["s"], c["mu"])
+    gpu.set_option(pkg.OPT_KERNEL, pkg.KERNEL_FMA_TILE)
+    try:
+        tile = gpu.loss_grad_s(pkg.MODEL_FAST, c["s"], c["mu"])
+    finally:
+        gpu.set_option(pkg.OPT_KERNEL, pkg.KERNEL_AUTO)
+    assert abs(auto["value"] - tile["value"]) <= 1e-5 * abs(tile["value"])
+    assert normwise(auto["grad_s"], tile["grad_s"]) <= 1e-5
+
+
+def test_odd_widths_and_ranks(narrow, oracle):
+    """Reduced widths 1..32 (odd ones pad a zero neuron), ranks below 32."""
+    rng = np.random.default_rng(7)
+    ranks = np.array([2, 7, 13, 32, 1])
+    red = np.array([5, 31, 1, 32])
+    L = len(ranks)
+    n = 2 * ranks[0] + sum(red[l] * (ranks[l] + 1 + ranks[l + 1]) for l in range(L - 1)) + ranks[-1] + 1
+    F = rng.normal(0, 0.4, n)
+    s = rng.uniform(0.3, 1.2, ranks.sum())
+    mu = np.array([12.0, 0.03, 2.0])
+    pts = pkg.sample_collocation(17, 777)
+    f = pkg.FastParams(ranks, red, F, pkg.ACT_SIN)
+    narrow.set_fast(f, pkg.F32)
+    narrow.set_points(pts)
+    got = narrow.loss_grad_s(pkg.MODEL_FAST, s, mu)
+    want = oracle.fast_grad(ranks, red, F, s, mu, pts, act=pkg.ACT_SIN)
+    assert abs(got["value"] - want["value"]) <= TOL32_LOSS * abs(want["value"])
+    assert normwise(got["grad_s"], want["grad_s"]) <= TOL32_NORM
+
+
+def test_multi_instance_ragged(narrow, oracle):
+    c = pkg.config2(n_points=0, act=pkg.ACT_SIN)
+    f = c["fast"]
+    n_inst, n_per = 4, 203
+    pts = pkg.sample_collocation(93, n_inst * n_per)
+    rng = np.random.default_rng(9)
+    S = np.stack([c["s"] * (1.0 + 0.1 * rng.standard_normal(c["s"].shape)) for _ in range(n_inst)])
+    MU = np.array([[20.0, 0.01, 5.0], [5.0, 0.05, 1.0], [35.0, 0.002, 8.0], [1.0, 0.1, 0.0]])
+    narrow.set_fast(f, pkg.F32)
+    narrow.set_points(pts, n_inst=n_inst)
+    got = narrow.loss_grad_s_multi(pkg.MODEL_FAST, S, MU, w=1.0 / n_per)
+    total = 0.0
+    for i in range(n_inst):
+        sl = pts[i * n_per:(i + 1) * n_per]
+        want = oracle.fast_grad(f.ranks, f.red_ranks, f.fparams, S[i], MU[i], sl, act=pkg.ACT_SIN)
+        total += want["value"]
+        assert normwise(got["grad_s"][i], want["grad_s"]) <= TOL32_NORM
+    assert abs(got["value"] - total) <= TOL32_LOSS * abs(total)
+
+
+def test_nonfinite_input_maps_to_error(narrow):
+    c = pkg.config2(n_points=500, act=pkg.ACT_SIN)
+    narrow.set_fast(c["fast"], pkg.F32)
+    narrow.set_points(c["pts"])
+    s = c["s"].copy()
+    s[3] = np.nan
+    with pytest.raises(pkg.NonFiniteError):
+        narrow.loss_grad_s(pkg.MODEL_FAST, s, c["mu"])
+
+
+def test_bitwise_reproducible(narrow):
+    c = pkg.config2(n_points=50000, act=pkg.ACT_SIN)
+    narrow.set_fast(c["fast"], pkg.F32)
+    narrow.set_points(c["pts"])
+    a = narrow.loss_grad_s(pkg.MODEL_FAST, c["s"], c["mu"])
+    b = narrow.loss_grad_s(pkg.MODEL_FAST, c["s"], c["mu"])
+    assert a["value"] == b["value"] and np.array_equal(a["grad_s"], b["grad_s"])
