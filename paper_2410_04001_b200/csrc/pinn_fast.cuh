@@ -65,6 +65,134 @@ __device__ __forceinline__ float transpose_reduce(float (&v)[R], int lane) {
     return v[0];
 }
 
+// One forward transition: u_{l+1} (unscaled, yn) from y_l = s_l (.) u_l, the
+// pre-activation jets z of every neuron pair to the stash. KJ / KK bound the
+// rank loops of the two GEMMs (4 for the rank-2 input and rank-1 output
+// layers of a FastLRNR; padded columns there are zero anyway).
+// Activation jets (jet_activation, model.cpp:170-181): lane pair (even: slots
+// u, u_x; odd: u_t, u_xx) trades z so the even lane evaluates neuron n and the
+// odd lane neuron n+1 in full, then trades the results back.
+template <int KJ>
+__device__ __forceinline__ void gemm_pair(const float* __restrict__ ua, const float* __restrict__ ub,
+                                          const float (&v)[2][R], float& c00, float& c01, float& c10, float& c11) {
+#pragma unroll
+    for (int j = 0; j < KJ; j += 4) {
+        const float4 a = *reinterpret_cast<const float4*>(ua + j);
+        const float4 b = *reinterpret_cast<const float4*>(ub + j);
+        c00 = fmaf(a.x, v[0][j], c00);
+        c01 = fmaf(a.x, v[1][j], c01);
+        c10 = fmaf(b.x, v[0][j], c10);
+        c11 = fmaf(b.x, v[1][j], c11);
+        c00 = fmaf(a.y, v[0][j + 1], c00);
+        c01 = fmaf(a.y, v[1][j + 1], c01);
+        c10 = fmaf(b.y, v[0][j + 1], c10);
+        c11 = fmaf(b.y, v[1][j + 1], c11);
+        c00 = fmaf(a.z, v[0][j + 2], c00);
+        c01 = fmaf(a.z, v[1][j + 2], c01);
+        c10 = fmaf(b.z, v[0][j + 2], c10);
+        c11 = fmaf(b.z, v[1][j + 2], c11);
+        c00 = fmaf(a.w, v[0][j + 3], c00);
+        c01 = fmaf(a.w, v[1][j + 3], c01);
+        c10 = fmaf(b.w, v[0][j + 3], c10);
+        c11 = fmaf(b.w, v[1][j + 3], c11);
+    }
+}
+
+// acc[c][k] += va[k] * x0c + vb[k] * x1c for the lane's two slots c
+template <int KK>
+__device__ __forceinline__ void axpy_pair(const float* __restrict__ va, const float* __restrict__ vb, float x00,
+                                          float x01, float x10, float x11, float (&acc)[2][R]) {
+#pragma unroll
+    for (int k = 0; k < KK; k += 4) {
+        const float4 a = *reinterpret_cast<const float4*>(va + k);
+        const float4 b = *reinterpret_cast<const float4*>(vb + k);
+        acc[0][k] = fmaf(b.x, x10, fmaf(a.x, x00, acc[0][k]));
+        acc[1][k] = fmaf(b.x, x11, fmaf(a.x, x01, acc[1][k]));
+        acc[0][k + 1] = fmaf(b.y, x10, fmaf(a.y, x00, acc[0][k + 1]));
+        acc[1][k + 1] = fmaf(b.y, x11, fmaf(a.y, x01, acc[1][k + 1]));
+        acc[0][k + 2] = fmaf(b.z, x10, fmaf(a.z, x00, acc[0][k + 2]));
+        acc[1][k + 2] = fmaf(b.z, x11, fmaf(a.z, x01, acc[1][k + 2]));
+        acc[0][k + 3] = fmaf(b.w, x10, fmaf(a.w, x00, acc[0][k + 3]));
+        acc[1][k + 3] = fmaf(b.w, x11, fmaf(a.w, x01, acc[1][k + 3]));
+    }
+}
+
+// One forward transition: u_{l+1} (unscaled, yn) from y_l = s_l (.) u_l, the
+// pre-activation jets z of every neuron pair to the stash. KJ / KK bound the
+// rank loops of the two GEMMs (4 for the rank-2 input and rank-1 output
+// layers of a FastLRNR; padded columns there are zero anyway).
+// Activation jets (jet_activation, model.cpp:170-181): lane pair (even: slots
+// u, u_x; odd: u_t, u_xx) trades z so the even lane evaluates neuron n and the
+// odd lane neuron n+1 in full, then trades the results back. The next pair's
+// z GEMM is issued before this pair's shuffle / sincos chain so the two overlap.
+template <int ACT, bool FAST, int KJ, int KK>
+__device__ __forceinline__ void fwd_transition(const float* __restrict__ Ub, const float* __restrict__ Vb,
+                                               const float* __restrict__ bb, int np, float4* __restrict__ zst,
+                                               int lane, int half, const float (&y)[2][R], float (&yn)[2][R]) {
+#pragma unroll
+    for (int k = 0; k < R; ++k) yn[0][k] = yn[1][k] = 0.f;
+    float z00 = half ? 0.f : bb[0], z01 = 0.f, z10 = half ? 0.f : bb[1], z11 = 0.f;
+    gemm_pair<KJ>(Ub, Ub + R, y, z00, z01, z10, z11);
+    for (int q = 0; q < np; ++q) {
+        const int n = 2 * q;
+        zst[q * 32 + lane] = make_float4(z00, z01, z10, z11);
+        // even lane: neuron n (z0, z1 own; z2, z3 from the odd lane); odd lane: neuron n+1
+        const float e1 = __shfl_xor_sync(0xffffffffu, half ? z00 : z10, 1);
+        const float e2 = __shfl_xor_sync(0xffffffffu, half ? z01 : z11, 1);
+        const float z0 = half ? e1 : z00, z1 = half ? e2 : z01, z2 = half ? z10 : e1, z3 = half ? z11 : e2;
+        if (q + 1 < np) {
+            z00 = half ? 0.f : bb[n + 2];
+            z01 = 0.f;
+            z10 = half ? 0.f : bb[n + 3];
+            z11 = 0.f;
+            gemm_pair<KJ>(Ub + (n + 2) * R, Ub + (n + 3) * R, y, z00, z01, z10, z11);
+        }
+        float sg, d1, d2, d3;
+        v2::act3<ACT, FAST>(z0, sg, d1, d2, d3);
+        const float a0 = sg, a1 = d1 * z1, a2 = d1 * z2, a3 = fmaf(d2 * z1, z1, d1 * z3);
+        const float e3 = __shfl_xor_sync(0xffffffffu, half ? a0 : a2, 1);
+        const float e4 = __shfl_xor_sync(0xffffffffu, half ? a1 : a3, 1);
+        axpy_pair<KK>(Vb + n * R, Vb + (n + 1) * R, half ? e3 : a0, half ? e4 : a1, half ? a2 : e3, half ? a3 : e4, yn);
+    }
+}
+
+// One reverse transition: dL/dy_l (gp) from g = dL/du_{l+1} (already scaled by
+// s_{l+1}). Activation-jet VJP (autodiff.cpp:644-666) split like the forward:
+// each lane of the pair does one neuron's four slots.
+template <int ACT, bool FAST, int KJ, int KK>
+__device__ __forceinline__ void bwd_transition(const float* __restrict__ Ub, const float* __restrict__ Vb, int np,
+                                               const float4* __restrict__ zst, int lane, int half,
+                                               const float (&g)[2][R], float (&gp)[2][R]) {
+#pragma unroll
+    for (int j = 0; j < R; ++j) gp[0][j] = gp[1][j] = 0.f;
+    float g00 = 0.f, g01 = 0.f, g10 = 0.f, g11 = 0.f;  // dL/da [neuron][slot]
+    gemm_pair<KK>(Vb, Vb + R, g, g00, g01, g10, g11);
+    float4 zz = zst[lane];
+    for (int q = 0; q < np; ++q) {
+        const int n = 2 * q;
+        // gather neuron m = n + half's four slots of z and dL/da on each lane
+        const float e1 = __shfl_xor_sync(0xffffffffu, half ? zz.x : zz.z, 1);
+        const float e2 = __shfl_xor_sync(0xffffffffu, half ? zz.y : g10, 1);
+        const float e3 = __shfl_xor_sync(0xffffffffu, half ? g00 : g11, 1);
+        const float e4 = __shfl_xor_sync(0xffffffffu, half ? g01 : zz.w, 1);
+        const float z0 = half ? e1 : zz.x, z1 = half ? e4 : zz.y, z2 = half ? zz.z : e1, z3 = half ? zz.w : e2;
+        const float c0 = half ? e2 : g00, c1 = half ? e3 : g01, c2 = half ? g10 : e3, c3 = half ? g11 : e4;
+        if (q + 1 < np) {  // the next pair's dL/da and z, overlapping this pair's VJP chain
+            zz = zst[(q + 1) * 32 + lane];
+            g00 = g01 = g10 = g11 = 0.f;
+            gemm_pair<KK>(Vb + (n + 2) * R, Vb + (n + 3) * R, g, g00, g01, g10, g11);
+        }
+        float sg, s1, s2, s3;
+        v2::act3<ACT, FAST>(z0, sg, s1, s2, s3);
+        const float h0 = c0 * s1 + s2 * (c1 * z1 + c2 * z2) + c3 * (s3 * z1 * z1 + s2 * z3);
+        const float h1 = c1 * s1 + 2.f * c3 * s2 * z1;
+        const float h2 = c2 * s1, h3 = c3 * s1;
+        const float e5 = __shfl_xor_sync(0xffffffffu, half ? h0 : h2, 1);
+        const float e6 = __shfl_xor_sync(0xffffffffu, half ? h1 : h3, 1);
+        axpy_pair<KJ>(Ub + n * R, Ub + (n + 1) * R, half ? e5 : h0, half ? e6 : h1, half ? h2 : e5, half ? h3 : e6, gp);
+    }
+}
+
 template <int ACT, bool FAST>
 __global__ void __launch_bounds__(NT, 1)
 pinn_fast_kernel(const NetF net, const RunGeom g, const double* __restrict__ pts, const double* __restrict__ svec,
@@ -118,77 +246,17 @@ pinn_fast_kernel(const NetF net, const RunGeom g, const double* __restrict__ pts
                 }
             }
             // ---- forward transitions ----
+            const bool in4 = net.r[0] <= 4, out4 = net.r[L - 1] <= 4;
             for (int l = 0; l + 1 < L; ++l) {
                 const float* Ub = Bk + 2 * R + l * TRANS;
                 const float* Vb = Ub + R * R;
                 const float* bb = Vb + R * R;
                 float4* zst = reinterpret_cast<float4*>(wst + net.zoff[l]);
-#pragma unroll
-                for (int k = 0; k < R; ++k) yn[0][k] = yn[1][k] = 0.f;
-                for (int q = 0; q < net.np[l]; ++q) {
-                    const int n = 2 * q;
-                    const float* ua = Ub + n * R;
-                    const float* ub = ua + R;
-                    float z00 = half ? 0.f : bb[n], z01 = 0.f, z10 = half ? 0.f : bb[n + 1], z11 = 0.f;
-#pragma unroll
-                    for (int j = 0; j < R; j += 4) {
-                        const float4 a = *reinterpret_cast<const float4*>(ua + j);
-                        const float4 b = *reinterpret_cast<const float4*>(ub + j);
-                        z00 = fmaf(a.x, y[0][j], z00);
-                        z01 = fmaf(a.x, y[1][j], z01);
-                        z10 = fmaf(b.x, y[0][j], z10);
-                        z11 = fmaf(b.x, y[1][j], z11);
-                        z00 = fmaf(a.y, y[0][j + 1], z00);
-                        z01 = fmaf(a.y, y[1][j + 1], z01);
-                        z10 = fmaf(b.y, y[0][j + 1], z10);
-                        z11 = fmaf(b.y, y[1][j + 1], z11);
-                        z00 = fmaf(a.z, y[0][j + 2], z00);
-                        z01 = fmaf(a.z, y[1][j + 2], z01);
-                        z10 = fmaf(b.z, y[0][j + 2], z10);
-                        z11 = fmaf(b.z, y[1][j + 2], z11);
-                        z00 = fmaf(a.w, y[0][j + 3], z00);
-                        z01 = fmaf(a.w, y[1][j + 3], z01);
-                        z10 = fmaf(b.w, y[0][j + 3], z10);
-                        z11 = fmaf(b.w, y[1][j + 3], z11);
-                    }
-                    zst[q * 32 + lane] = make_float4(z00, z01, z10, z11);
-                    // activation jets (jet_activation, model.cpp:170-181): the even lane
-                    // evaluates sigma at neuron n, the odd lane at n+1
-                    const float zx = __shfl_xor_sync(0xffffffffu, z10, 1);
-                    float sg, d1, d2, d3;
-                    v2::act3<ACT, FAST>(half ? zx : z00, sg, d1, d2, d3);
-                    const float e1 = __shfl_xor_sync(0xffffffffu, half ? sg : d1, 1);
-                    const float e2 = __shfl_xor_sync(0xffffffffu, half ? d1 : d2, 1);
-                    const float e3 = __shfl_xor_sync(0xffffffffu, z01, 1);
-                    const float e4 = __shfl_xor_sync(0xffffffffu, z11, 1);
-                    float a00, a01, a10, a11;
-                    if (!half) {
-                        a00 = sg;
-                        a01 = d1 * z01;
-                        a10 = e1;
-                        a11 = e2 * z11;
-                    } else {  // z00 = u_t slot, z01 = u_xx slot of neuron n; e1 = sigma'(n), e2 = sigma''(n)
-                        a00 = e1 * z00;
-                        a01 = fmaf(e2 * e3, e3, e1 * z01);
-                        a10 = d1 * z10;
-                        a11 = fmaf(d2 * e4, e4, d1 * z11);
-                    }
-                    const float* va = Vb + n * R;
-                    const float* vb = va + R;
-#pragma unroll
-                    for (int k = 0; k < R; k += 4) {
-                        const float4 a = *reinterpret_cast<const float4*>(va + k);
-                        const float4 b = *reinterpret_cast<const float4*>(vb + k);
-                        yn[0][k] = fmaf(b.x, a10, fmaf(a.x, a00, yn[0][k]));
-                        yn[1][k] = fmaf(b.x, a11, fmaf(a.x, a01, yn[1][k]));
-                        yn[0][k + 1] = fmaf(b.y, a10, fmaf(a.y, a00, yn[0][k + 1]));
-                        yn[1][k + 1] = fmaf(b.y, a11, fmaf(a.y, a01, yn[1][k + 1]));
-                        yn[0][k + 2] = fmaf(b.z, a10, fmaf(a.z, a00, yn[0][k + 2]));
-                        yn[1][k + 2] = fmaf(b.z, a11, fmaf(a.z, a01, yn[1][k + 2]));
-                        yn[0][k + 3] = fmaf(b.w, a10, fmaf(a.w, a00, yn[0][k + 3]));
-                        yn[1][k + 3] = fmaf(b.w, a11, fmaf(a.w, a01, yn[1][k + 3]));
-                    }
-                }
+                const bool kj4 = l == 0 && in4, kk4 = l == L - 2 && out4;
+                if (kj4 && kk4) fwd_transition<ACT, FAST, 4, 4>(Ub, Vb, bb, net.np[l], zst, lane, half, y, yn);
+                else if (kj4) fwd_transition<ACT, FAST, 4, R>(Ub, Vb, bb, net.np[l], zst, lane, half, y, yn);
+                else if (kk4) fwd_transition<ACT, FAST, R, 4>(Ub, Vb, bb, net.np[l], zst, lane, half, y, yn);
+                else fwd_transition<ACT, FAST, R, R>(Ub, Vb, bb, net.np[l], zst, lane, half, y, yn);
                 // u_{l+1} -> stash; y_{l+1} = s_{l+1} (.) u_{l+1}
                 float4* ust = reinterpret_cast<float4*>(wst + net.uoff[l]);
                 const int rn = net.r[l + 1], so = net.soff[l + 1];
@@ -276,79 +344,11 @@ pinn_fast_kernel(const NetF net, const RunGeom g, const double* __restrict__ pts
                 const float* Ub = Bk + 2 * R + l * TRANS;
                 const float* Vb = Ub + R * R;
                 const float4* zst = reinterpret_cast<const float4*>(wst + net.zoff[l]);
-#pragma unroll
-                for (int j = 0; j < R; ++j) yn[0][j] = yn[1][j] = 0.f;
-                for (int q = 0; q < net.np[l]; ++q) {
-                    const int n = 2 * q;
-                    const float* va = Vb + n * R;
-                    const float* vb = va + R;
-                    float g00 = 0.f, g01 = 0.f, g10 = 0.f, g11 = 0.f;  // dL/da [neuron][slot]
-#pragma unroll
-                    for (int k = 0; k < R; k += 4) {
-                        const float4 a = *reinterpret_cast<const float4*>(va + k);
-                        const float4 b = *reinterpret_cast<const float4*>(vb + k);
-                        g00 = fmaf(a.x, gy[0][k], g00);
-                        g01 = fmaf(a.x, gy[1][k], g01);
-                        g10 = fmaf(b.x, gy[0][k], g10);
-                        g11 = fmaf(b.x, gy[1][k], g11);
-                        g00 = fmaf(a.y, gy[0][k + 1], g00);
-                        g01 = fmaf(a.y, gy[1][k + 1], g01);
-                        g10 = fmaf(b.y, gy[0][k + 1], g10);
-                        g11 = fmaf(b.y, gy[1][k + 1], g11);
-                        g00 = fmaf(a.z, gy[0][k + 2], g00);
-                        g01 = fmaf(a.z, gy[1][k + 2], g01);
-                        g10 = fmaf(b.z, gy[0][k + 2], g10);
-                        g11 = fmaf(b.z, gy[1][k + 2], g11);
-                        g00 = fmaf(a.w, gy[0][k + 3], g00);
-                        g01 = fmaf(a.w, gy[1][k + 3], g01);
-                        g10 = fmaf(b.w, gy[0][k + 3], g10);
-                        g11 = fmaf(b.w, gy[1][k + 3], g11);
-                    }
-                    // activation-jet VJP (autodiff.cpp:644-666); the even lane does the
-                    // coupled slots (u, u_x), the odd lane the diagonal ones (u_t, u_xx)
-                    const float4 zz = zst[q * 32 + lane];
-                    const float zx = __shfl_xor_sync(0xffffffffu, zz.z, 1);  // odd: z0(n+1); even: z2(n+1)
-                    float sg, d1, d2, d3;
-                    v2::act3<ACT, FAST>(half ? zx : zz.x, sg, d1, d2, d3);
-                    const float x1 = __shfl_xor_sync(0xffffffffu, half ? g00 : d1, 1);  // even: g2(n); odd: s1(n)
-                    const float x2 = __shfl_xor_sync(0xffffffffu, g01, 1);   // even: g3(n)
-                    const float x3 = __shfl_xor_sync(0xffffffffu, zz.x, 1);  // even: z2(n)
-                    const float x4 = __shfl_xor_sync(0xffffffffu, zz.y, 1);  // even: z3(n)
-                    const float x5 = __shfl_xor_sync(0xffffffffu, g10, 1);   // even: g2(n+1)
-                    const float x6 = __shfl_xor_sync(0xffffffffu, g11, 1);   // even: g3(n+1)
-                    const float x8 = __shfl_xor_sync(0xffffffffu, zz.w, 1);  // even: z3(n+1)
-                    const float x9 = __shfl_xor_sync(0xffffffffu, d1, 1);    // even: s1(n+1)
-                    const float x10 = __shfl_xor_sync(0xffffffffu, d2, 1);   // even: s2(n+1)
-                    const float x11 = __shfl_xor_sync(0xffffffffu, d3, 1);   // even: s3(n+1)
-                    float h00, h01, h10, h11;  // dL/dz [neuron][slot]
-                    if (!half) {
-                        const float z1 = zz.y, z1b = zz.w;
-                        h00 = g00 * d1 + d2 * (g01 * z1 + x1 * x3) + x2 * (d3 * z1 * z1 + d2 * x4);
-                        h01 = g01 * d1 + 2.f * x2 * d2 * z1;
-                        h10 = g10 * x9 + x10 * (g11 * z1b + x5 * zx) + x6 * (x11 * z1b * z1b + x10 * x8);
-                        h11 = g11 * x9 + 2.f * x6 * x10 * z1b;
-                    } else {
-                        h00 = g00 * x1;
-                        h01 = g01 * x1;
-                        h10 = g10 * d1;
-                        h11 = g11 * d1;
-                    }
-                    const float* ua = Ub + n * R;
-                    const float* ub = ua + R;
-#pragma unroll
-                    for (int j = 0; j < R; j += 4) {
-                        const float4 a = *reinterpret_cast<const float4*>(ua + j);
-                        const float4 b = *reinterpret_cast<const float4*>(ub + j);
-                        yn[0][j] = fmaf(b.x, h10, fmaf(a.x, h00, yn[0][j]));
-                        yn[1][j] = fmaf(b.x, h11, fmaf(a.x, h01, yn[1][j]));
-                        yn[0][j + 1] = fmaf(b.y, h10, fmaf(a.y, h00, yn[0][j + 1]));
-                        yn[1][j + 1] = fmaf(b.y, h11, fmaf(a.y, h01, yn[1][j + 1]));
-                        yn[0][j + 2] = fmaf(b.z, h10, fmaf(a.z, h00, yn[0][j + 2]));
-                        yn[1][j + 2] = fmaf(b.z, h11, fmaf(a.z, h01, yn[1][j + 2]));
-                        yn[0][j + 3] = fmaf(b.w, h10, fmaf(a.w, h00, yn[0][j + 3]));
-                        yn[1][j + 3] = fmaf(b.w, h11, fmaf(a.w, h01, yn[1][j + 3]));
-                    }
-                }
+                const bool kj4 = l == 0 && in4, kk4 = l == L - 2 && out4;
+                if (kj4 && kk4) bwd_transition<ACT, FAST, 4, 4>(Ub, Vb, net.np[l], zst, lane, half, gy, yn);
+                else if (kj4) bwd_transition<ACT, FAST, 4, R>(Ub, Vb, net.np[l], zst, lane, half, gy, yn);
+                else if (kk4) bwd_transition<ACT, FAST, R, 4>(Ub, Vb, net.np[l], zst, lane, half, gy, yn);
+                else bwd_transition<ACT, FAST, R, R>(Ub, Vb, net.np[l], zst, lane, half, gy, yn);
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
                     gy[0][j] = yn[0][j];
