@@ -27,7 +27,7 @@ n = 1024 * 16384
 fl = pkg.fast_flops_per_point(c["fast"].ranks, c["fast"].red_ranks)
 out["c3"] = {"ms_per_step": dt * 1e3, "point_evals_per_s": n / dt, "tflops": fl * n / dt / 1e12,
              "frac_fp32_fma": fl * n / dt / 1e12 / PEAK, "flop_per_point": fl, "points": n,
-             "kernel": "FMA tile (FastLRNR) + FP64 hypernetwork fwd/VJP", "loss": r["value"]}
+             "kernel": "narrow-network kernel (FastLRNR, auto) + FP64 hypernetwork fwd/VJP", "loss": r["value"]}
 ctx.close()
 # c4 (8 instances per step; the 64-instance step is 8x this)
 n_inst, per = 8, 1 << 20
