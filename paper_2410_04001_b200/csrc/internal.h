@@ -414,5 +414,55 @@ int guarded(lrnr_gpu_ctx* ctx, F&& f) {
 bool dispatch_fast(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
                    double* dev_out);
 
+// ---- shared between lrnr_gpu.cu (definitions), solve.cu and meta.cu ----
+constexpr double kTwoPi = 6.283185307179586476925286766559;  // pde.hpp:21
+
+// Temporarily point the context's point set at another device array (one instance).
+struct PointSwap {
+    lrnr_gpu_ctx* ctx;
+    const double* pts;
+    int64_t n_inst, n_per;
+    PointSwap(lrnr_gpu_ctx* c, const double* p, int64_t n) : ctx(c), pts(c->pts), n_inst(c->n_inst), n_per(c->n_per) {
+        c->pts = p;
+        c->n_inst = 1;
+        c->n_per = n;
+    }
+    ~PointSwap() {
+        ctx->pts = pts;
+        ctx->n_inst = n_inst;
+        ctx->n_per = n_per;
+        ctx->term_spec = nullptr;
+        ctx->term_objective = 0;
+    }
+};
+
+bool use_small(const lrnr_gpu_ctx* ctx, const Model& m);
+template <int MODE>
+void dispatch_small(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
+                    double* dev_out, double* jets_dev);
+template <int MODE>
+void dispatch_pinn(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
+                   double* dev_out, double* jets_dev);
+bool dispatch_tc(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
+                 double* dev_out);
+bool dispatch_v2(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
+                 double* dev_out);
+// boundary terms: per-point TermSpecs from a forward pass's jets (training.cpp:307-327, 533-549)
+__global__ void boundary_spec_kernel(const double* __restrict__ jets, const double* __restrict__ sin_x,
+                                     int64_t n_ic, int64_t n_bc, double w_ic, double w_bc, int abs_obj,
+                                     TermSpec* __restrict__ spec);
+__global__ void boundary_spec_multi_kernel(const double* __restrict__ jets, const double* __restrict__ sin_x,
+                                           int64_t n_inst, int64_t n_ic, int64_t n_bc, double w_ic, double w_bc,
+                                           TermSpec* __restrict__ spec);
+__global__ void add_rows_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
+                                double* __restrict__ c);
+void check_bad(lrnr_gpu_ctx* ctx, const Model& m);
+void reset_bad(lrnr_gpu_ctx* ctx);
+const Model& need_model(lrnr_gpu_ctx* ctx, int model);
+void upload_coeffs_impl(lrnr_gpu_ctx* ctx, const double* s, const double* mu, int64_t n_inst, int rtotal);
+void download(lrnr_gpu_ctx* ctx, const double* dev, double* host, size_t n);
+void hyper_forward_resident(lrnr_gpu_ctx* ctx, int rtotal);
+void hyper_backward_resident(lrnr_gpu_ctx* ctx, const double* dev_rows, int R1, double* dev_grad);
+
 }  // namespace detail
 }  // namespace lrnr_b200

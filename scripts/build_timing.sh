@@ -8,5 +8,6 @@ cd "$(dirname "$0")/.."
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude \
     --expt-relaxed-constexpr -diag-suppress 177 -DLRNR_TC_TIMING "$@" \
     -c paper_2410_04001_b200/csrc/lrnr_gpu.cu -o build/lrnr_gpu_timing.o
+others=$(ls build/*.cu.o | grep -v '/lrnr_gpu.cu.o$')
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o scripts/liblrnr_gpu_timing.so build/lrnr_gpu_timing.o \
-    build/inst_*.o build/*.cpp.o -cudart static
+    $others build/*.cpp.o -cudart static
