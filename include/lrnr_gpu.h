@@ -107,6 +107,12 @@ int lrnr_gpu_set_stream(lrnr_gpu_ctx* ctx, void* cuda_stream);
  * rank is <= 32 and the terms fit 8 CTAs x 16 warps; 1 = the graph path (one
  * captured epoch replayed per epoch). */
 #define LRNR_OPT_SOLVE 4
+/* LRNR_OPT_META_PREC (meta step, lrnr_gpu_meta_loss_grad / lrnr_gpu_meta_terms_grad,
+ * FP32 LRNR): 0 = FP32 throughout on the FMA tile kernel (default); 1 = BF16
+ * tensor-core operands with FP32 accumulation and FP32 activation / residual /
+ * reduction math (tcgen05 meta kernel; BASELINE config 4's "BF16/TF32 inputs
+ * with FP32 accumulate"); widths (2, ..., 1), ranks <= 64. */
+#define LRNR_OPT_META_PREC 5
 int lrnr_gpu_set_option(lrnr_gpu_ctx* ctx, int opt, int value);
 /* Number of kernels this context has launched so far (instrumentation). */
 /* Kernels launched so far (instrumentation; no reference counterpart). */

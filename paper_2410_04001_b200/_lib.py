@@ -33,7 +33,7 @@ LRNR_OK, LRNR_EINVAL, LRNR_ENONFINITE, LRNR_ECUDA, LRNR_ENOMEM, LRNR_ESTATE = ra
 ACT_TANH, ACT_SIN = 0, 1
 F64, F32 = 0, 1
 MODEL_LRNR, MODEL_FAST = 0, 1
-OPT_FAST_SINCOS, OPT_KERNEL, OPT_TILE_P, OPT_SOLVE = 1, 2, 3, 4
+OPT_FAST_SINCOS, OPT_KERNEL, OPT_TILE_P, OPT_SOLVE, OPT_META_PREC = 1, 2, 3, 4, 5
 # LRNR_OPT_KERNEL values
 KERNEL_AUTO, KERNEL_STREAM, KERNEL_TC, KERNEL_FMA_TILE, KERNEL_SMALL, KERNEL_NARROW = 0, 1, 2, 3, 4, 5
 # lrnr_gpu_terms_grad objectives

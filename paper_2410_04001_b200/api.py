@@ -17,7 +17,7 @@ import numpy as np
 from . import _lib
 from ._lib import ACT_SIN, ACT_TANH, F32, F64, MODEL_FAST, MODEL_LRNR  # noqa: F401
 from ._lib import (  # noqa: F401
-    KERNEL_AUTO, KERNEL_FMA_TILE, KERNEL_NARROW, KERNEL_SMALL, KERNEL_STREAM, KERNEL_TC, OBJ_ABS, OBJ_SQUARED, OPT_FAST_SINCOS, OPT_KERNEL, OPT_SOLVE,
+    KERNEL_AUTO, KERNEL_FMA_TILE, KERNEL_NARROW, KERNEL_SMALL, KERNEL_STREAM, KERNEL_TC, OBJ_ABS, OBJ_SQUARED, OPT_FAST_SINCOS, OPT_KERNEL, OPT_META_PREC, OPT_SOLVE,
     OPT_TILE_P,
 )
 

@@ -117,6 +117,16 @@ struct Model {
         std::vector<int> sched_cnt;
         DevBuf dblocks, dsched_off, dsched_bytes;
     } tc;
+    // meta tensor-core kernel (pinn_meta_tc.cuh): bf16 factor blocks, schedule,
+    // per-CTA partial layout and the ParamPacker map
+    struct MTC {
+        bool ok = false;
+        std::vector<int> rp, nc, yoff, qdb;
+        std::vector<int64_t> gbase;
+        int64_t ystride = 0, qbase = 0, wg_stride = 0, n_params = 0;
+        int QS = 0, qdUL = 0, qdbL = 0, qdV0 = 0, sched_len = 0;
+        DevBuf dblocks, dsched_off, dsched_bytes, dmap, wg, sum;
+    } mtc;
     // narrow-network kernel (pinn_fast.cuh): every hidden width and rank <= 32
     struct FK {
         bool ok = false;
@@ -142,6 +152,11 @@ void upload_model(Model& m);
 void build_v2(Model& m, bool meta = false);
 void build_tc(Model& m);
 void build_fk(Model& m);
+bool mtc_eligible(const Model& m);
+void build_mtc(Model& m);
+template <int ACT>
+void launch_meta_tc(lrnr_gpu_ctx* ctx, Model& m, const double* s_dev, const double* mu_dev, double w, double* dev_out,
+                    double* wg_out);
 
 template <class T>
 DevNet<T> dev_net(const Model& m) {
@@ -205,6 +220,7 @@ struct lrnr_gpu_ctx {
     int opt_fast_sincos = 0;  // LRNR_OPT_FAST_SINCOS
     int opt_kernel = 0;       // LRNR_OPT_KERNEL: 0 auto, 1 streaming, 2 tensor core, 3 FMA tile, 4 small batch
     int opt_solve = 0;        // LRNR_OPT_SOLVE: 0 auto (persistent fast solver when eligible), 1 graph path
+    int opt_meta_prec = 0;    // LRNR_OPT_META_PREC: 0 FP32 FMA tile kernel, 1 BF16 tensor-core operands
 };
 
 namespace lrnr_b200 {

@@ -95,6 +95,8 @@ void release_model(Model& m) {
     m.tc.dsched_off.release();
     m.tc.dsched_bytes.release();
     m.flat_dev.release();
+    for (DevBuf* b : {&m.mtc.dblocks, &m.mtc.dsched_off, &m.mtc.dsched_bytes, &m.mtc.dmap, &m.mtc.wg, &m.mtc.sum})
+        b->release();
 }
 
 void upload_model(Model& m) {
@@ -912,6 +914,10 @@ int lrnr_gpu_set_option(lrnr_gpu_ctx* ctx, int opt, int value) {
         if (opt == LRNR_OPT_FAST_SINCOS) ctx->opt_fast_sincos = value;
         else if (opt == LRNR_OPT_KERNEL) ctx->opt_kernel = value;
         else if (opt == LRNR_OPT_SOLVE) ctx->opt_solve = value;
+        else if (opt == LRNR_OPT_META_PREC) {
+            require(value == 0 || value == 1, "meta precision must be 0 (FP32) or 1 (BF16 tensor-core operands)");
+            ctx->opt_meta_prec = value;
+        }
         else if (opt == LRNR_OPT_TILE_P) {
             require(value == 0 || value == 32 || value == 64, "tile P must be 32 or 64 (0 = default)");
             for (auto& m : ctx->models) {
