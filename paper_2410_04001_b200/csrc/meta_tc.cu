@@ -246,3 +246,12 @@ template void launch_meta_tc<1>(lrnr_gpu_ctx*, Model&, const double*, const doub
 
 }  // namespace detail
 }  // namespace lrnr_b200
+
+#ifdef MTC_TIMING
+// dev aid: read and reset the meta kernel's per-phase cycle counters (CTA 0)
+extern "C" int lrnr_mtc_timing(unsigned long long* out) {
+    if (cudaMemcpyFromSymbol(out, lrnr_b200::mtc::g_mtc_timing, 32 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+    static const unsigned long long zero[32] = {};
+    return cudaMemcpyToSymbol(lrnr_b200::mtc::g_mtc_timing, zero, sizeof(zero)) != cudaSuccess;
+}
+#endif

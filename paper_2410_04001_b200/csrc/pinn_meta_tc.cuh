@@ -111,6 +111,68 @@ __device__ __forceinline__ void mma(uint32_t d, uint32_t a_lo, uint32_t a_hi, ui
         "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc)
         : "memory");
 }
+__device__ __forceinline__ uint32_t elect_one() {
+    uint32_t pred;
+    asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(pred));
+    return pred;
+}
+// One MMA (single-thread form, used by the issuing lane) and the warp-collective
+// (elected-lane) form.
+#ifndef MTC_ELECT_ASM
+#define MTC_ELECT_ASM 1
+#endif
+__device__ __forceinline__ void mma1(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// single-thread MMA from 32-bit descriptor low words (start >> 4 | LBO >> 4 << 16)
+// with compile-time high words (SBO, version): keeps only 32-bit values live
+template <uint32_t HA, uint32_t HB>
+__device__ __forceinline__ void mma_lo(uint32_t d, uint32_t alo, uint32_t blo, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b64 da, db;\n\t"
+        "mov.b64 da, {%1, %5};\n\t"
+        "mov.b64 db, {%2, %6};\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %3, p;\n\t}" ::"r"(d),
+        "r"(alo), "r"(blo), "r"(idesc), "r"(acc), "n"(HA), "n"(HB)
+        : "memory");
+}
+__device__ __forceinline__ void commit1(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(umma::smem_addr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mma64(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+#if MTC_ELECT_ASM
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+#else
+    if (elect_one())
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+            "l"(a), "l"(b), "r"(idesc), "r"(acc)
+            : "memory");
+#endif
+}
+// timing knobs (dev aid; results are wrong when set): bit 0 skips the dU / dV
+// MMAs, bit 1 the partial-gradient reductions, bit 2 the activation math
+#ifndef MTC_SKIP
+#define MTC_SKIP 0
+#endif
+__device__ __forceinline__ void commit(uint64_t* bar) {
+    if (elect_one())
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         umma::smem_addr(bar))
+                     : "memory");
+}
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
@@ -128,6 +190,18 @@ __device__ __forceinline__ void red4(float* p, float a, float b, float c, float 
 }
 __device__ __forceinline__ void red1(float* p, float a) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(a) : "memory");
+}
+#ifndef MTC_UWAIT
+#define MTC_UWAIT 0
+#endif
+__device__ __forceinline__ uint32_t try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(umma::smem_addr(bar)), "r"(parity), "n"(UMMA_WAIT_HINT_NS)
+        : "memory");
+    return ok;
 }
 // named barrier over the 16 epilogue warps
 __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NWE * 32) : "memory"); }
@@ -166,6 +240,21 @@ __device__ __forceinline__ float wsum(float v) {
     return v;
 }
 
+// Per-phase cycle counters of CTA 0 (dev aid, -DMTC_TIMING): epilogue warp 0 and
+// the MMA warp accumulate clock64 deltas per site; read g_mtc_timing[32].
+#ifdef MTC_TIMING
+__device__ unsigned long long g_mtc_timing[32];
+#define MT(slot, ...)                                                                     \
+    do {                                                                                  \
+        const long long _t0 = clock64();                                                  \
+        __VA_ARGS__;                                                                      \
+        if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == ISSUER * 32))          \
+            atomicAdd(&g_mtc_timing[slot], static_cast<unsigned long long>(clock64() - _t0)); \
+    } while (0)
+#else
+#define MT(slot, ...) __VA_ARGS__
+#endif
+
 template <int ACT>
 __device__ __forceinline__ void act3(float a, float& sg, float& d1, float& d2, float& d3) {
     v2::act3<ACT, true, float>(a, sg, d1, d2, d3);  // sin: SFU after a Cody-Waite reduction (~1e-6)
@@ -183,7 +272,10 @@ meta_tc_kernel(const MetaNet net, const RunGeom g, const double* __restrict__ pt
     __shared__ uint32_t tmem_base;
     float* acc4 = reinterpret_cast<float*>(sm + OFF_ACC);
 
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31;
+    // warp index through a shuffle: provably warp-uniform, so the MMA warp's
+    // descriptor arithmetic stays on the uniform datapath (no R2UR per MMA)
+    const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
     const int quarter = warp & 3, grp = warp >> 2;
     const int p = quarter * 32 + lane;  // epilogue: the point (TMEM lane) of this thread
     const int L = net.L;
@@ -217,7 +309,9 @@ meta_tc_kernel(const MetaNet net, const RunGeom g, const double* __restrict__ pt
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
-    const uint32_t tbase = tmem_base;
+    // all 512 columns are allocated, so the TMEM base address is 0 (lane 0, column 0)
+    const uint32_t tbase = 0;
+    if (tid == 0 && tmem_base != 0) __trap();
 
     int64_t total_tiles = 0;
     for (int64_t u = blockIdx.x; u < g.n_units; u += gridDim.x) {
@@ -228,10 +322,20 @@ meta_tc_kernel(const MetaNet net, const RunGeom g, const double* __restrict__ pt
     const int64_t total_chunks = total_tiles * net.sched_len;
 
     auto wait = [](uint64_t* bar, uint32_t parity) {
+#if MTC_UWAIT
+        // warp-uniform wait: the loop exit is __all_sync-voted, so code after it
+        // stays provably convergent (uniform datapath for the MMA warp)
+        while (!__all_sync(0xffffffffu, try_wait(bar, parity))) {
+        }
+#else
         umma::mbar_wait(bar, parity);
+#endif
         umma::fence_after();
     };
 
+#ifdef MTC_TIMING
+    const long long t_start = clock64();
+#endif
     // =========================== TMA producer ===========================
     if (warp == PRODUCER) {
         if (lane == 0) {
@@ -247,123 +351,132 @@ meta_tc_kernel(const MetaNet net, const RunGeom g, const double* __restrict__ pt
         __syncwarp();
     }
     // =========================== MMA issuer ===========================
+    // One thread (lane 0) issues every MMA: in a single-thread region ptxas keeps
+    // the descriptors on the uniform datapath (UIADD3 + UTCHMMA per MMA); the
+    // warp-collective elected form cost ~165 cycles per MMA (R2UR.BROADCAST chains).
     else if (warp == ISSUER) {
-        const uint32_t HK = umma::desc_hi(128);   // SBO 128 B (K-major tiles, ring tiles)
-        const uint32_t HM = umma::desc_hi(2048);  // SBO 2048 B (MN-major SY / ST / G / Z)
-        int64_t qc = 0, rc = 0, pe = 0;  // chunk counter, reverse-chunk counter, p1empty completions consumed
+      if (lane == 0) {
+        const uint32_t sbase = umma::smem_addr(sm) >> 4;
+        constexpr uint32_t HK = (128u >> 4) | (1u << 14);   // SBO 128 B (K-major tiles, ring tiles)
+        constexpr uint32_t HM = (2048u >> 4) | (1u << 14);  // SBO 2048 B (MN-major SY / ST / G / Z)
+        // descriptor low word: start address >> 4 | LBO >> 4 << 16
+        auto lo = [&](uint32_t off, uint32_t lbo) -> uint32_t { return sbase + (off >> 4) + ((lbo >> 4) << 16); };
+        uint32_t qc = 0, rc = 0, pe = 0;  // chunk counter, reverse-chunk counter, p1empty completions consumed
         uint32_t tcount = 0;
-        auto drain_p1empty = [&](int64_t upto) {  // consume p1empty completions of chunks <= upto, in order
-            for (; pe <= upto; ++pe) wait(&p1empty[pe & 1], static_cast<uint32_t>((pe >> 1) & 1));
+        auto drain_p1empty = [&](uint32_t end) {  // consume p1empty completions of chunks < end, in order
+            for (; pe < end; ++pe) MT(18, wait(&p1empty[pe & 1], static_cast<uint32_t>((pe >> 1) & 1)));
         };
-        auto ring = [&](int64_t q) { return sm + OFF_RING + static_cast<int>(q % NBUF) * BLKS; };
-        auto wait_full = [&](int64_t q) {
-            wait(&full[q % NBUF], static_cast<uint32_t>((q / NBUF) & 1));
-        };
-        auto commit = [&](uint64_t* bar) { umma::mma_commit_w(bar); };
+        auto ring = [&](uint32_t q) { return static_cast<uint32_t>(OFF_RING + static_cast<int>(q % NBUF) * BLKS); };
+        auto wait_full = [&](uint32_t q) { MT(17, wait(&full[q % NBUF], static_cast<uint32_t>((q / NBUF) & 1))); };
         for (int64_t t = 0; t < total_tiles; ++t) {
             // ---------------- forward ----------------
             for (int l = 0; l + 1 < L; ++l) {
-                wait(&sready, tcount & 1);  // SY_l in shared memory
+                MT(16, wait(&sready, tcount & 1));  // SY_l in shared memory
                 const int RL = net.rp[l], RN = net.rp[l + 1], n = net.nc[l];
                 const uint32_t id1 = idesc_bf16(P, KC, 0, 0), id2 = idesc_bf16(P, RN, 0, 0);
-                auto p1 = [&](int64_t q) {
+                auto p1 = [&](uint32_t q) {
                     wait_full(q);
-                    const unsigned char* b = ring(q);
+                    const uint32_t a0 = lo(OFF_SY, 2048), b0 = lo(ring(q), 256);
                     const uint32_t d0 = tbase + TM_P1 + static_cast<uint32_t>(q & 1) * 64;
+                    const int nk = RL / 16;
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        for (int k = 0; k < RL / 16; ++k)
-                            mma(d0 + c * 16, umma::desc_lo(sm + OFF_SY + c * SLOT + k * 4096, 2048), HK,
-                                umma::desc_lo(b + k * 512, 256), HK, id1, k > 0);
-                    commit(&p1full[q & 1]);
+                    for (int k = 0; k < RP / 16; ++k)
+                        if (k < nk)
+#pragma unroll
+                            for (int c = 0; c < 4; ++c)
+                                mma_lo<HK, HK>(d0 + c * 16, a0 + ((c * SLOT + k * 4096) >> 4), b0 + ((k * 512) >> 4), id1, k > 0);
+                    commit1(&p1full[q & 1]);
                 };
-                const int64_t q0 = qc;
-                p1(q0);
+                const uint32_t q0 = qc;
+                MT(21, p1(q0));
                 for (int ch = 0; ch < n; ++ch) {
-                    const int64_t q = q0 + ch;
+                    const uint32_t q = q0 + ch;
                     if (ch + 1 < n) {
-                        drain_p1empty(q - 1);
-                        p1(q + 1);
+                        drain_p1empty(q);
+                        MT(21, p1(q + 1));
                     }
-                    wait(&zgfull[q & 1], static_cast<uint32_t>((q >> 1) & 1));
-                    const unsigned char* zb = sm + OFF_ZG + static_cast<int>(q & 1) * ZGBUF;
-                    const unsigned char* vb = ring(q) + RL * 32 + 64;
+                    MT(19, wait(&zgfull[q & 1], static_cast<uint32_t>((q >> 1) & 1)));
+                    const uint32_t a0 = lo(OFF_ZG + static_cast<uint32_t>(q & 1) * ZGBUF, 2048);
+                    const uint32_t b0 = lo(ring(q) + RL * 32 + 64, (RN / 8) * 128);
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        mma(tbase + TM_Y + c * 64, umma::desc_lo(zb + c * ZSLOT, 2048), HK,
-                            umma::desc_lo(vb, (RN / 8) * 128), HK, id2, ch > 0);
-                    commit(&zgfree[q & 1]);
-                    commit(&slotfree[q % NBUF]);
+                    for (int c = 0; c < 4; ++c) mma_lo<HK, HK>(tbase + TM_Y + c * 64, a0 + ((c * ZSLOT) >> 4), b0, id2, ch > 0);
+                    commit1(&zgfree[q & 1]);
+                    commit1(&slotfree[q % NBUF]);
                 }
-                commit(&tdone);
-                drain_p1empty(q0 + n - 1);
+                commit1(&tdone);
+                drain_p1empty(q0 + n);
                 qc += n;
                 ++tcount;
             }
             // ---------------- reverse ----------------
             for (int l = L - 2; l >= 0; --l) {
-                wait(&sready, tcount & 1);  // ST_{l+1} and SY_l in shared memory
+                MT(16, wait(&sready, tcount & 1));  // ST_{l+1} and SY_l in shared memory
                 const int RL = net.rp[l], RN = net.rp[l + 1], n = net.nc[l];
                 const uint32_t id1 = idesc_bf16(P, KC, 0, 0), id2 = idesc_bf16(P, RL, 0, 0);
                 const uint32_t id3 = idesc_bf16(64, KC, 1, 1);
-                auto p1 = [&](int64_t q) {
+                auto p1 = [&](uint32_t q) {
                     wait_full(q);
-                    const unsigned char* b = ring(q);
+                    const uint32_t ay = lo(OFF_SY, 2048), at = lo(OFF_ST, 2048), bu = lo(ring(q), 256),
+                                   bv = lo(ring(q) + RL * 32 + 64, 256);
+                    const int nkl = RL / 16, nkn = RN / 16;
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        for (int k = 0; k < RL / 16; ++k)
-                            mma(tbase + TM_P1 + c * 16, umma::desc_lo(sm + OFF_SY + c * SLOT + k * 4096, 2048), HK,
-                                umma::desc_lo(b + k * 512, 256), HK, id1, k > 0);
+                    for (int k = 0; k < RP / 16; ++k)
+                        if (k < nkl)
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        for (int k = 0; k < RN / 16; ++k)
-                            mma(tbase + TM_DZ + c * 16, umma::desc_lo(sm + OFF_ST + c * SLOT + k * 4096, 2048), HK,
-                                umma::desc_lo(b + RL * 32 + 64 + k * 512, 256), HK, id1, k > 0);
-                    commit(&p1full[q & 1]);
+                            for (int c = 0; c < 4; ++c)
+                                mma_lo<HK, HK>(tbase + TM_P1 + c * 16, ay + ((c * SLOT + k * 4096) >> 4), bu + ((k * 512) >> 4),
+                                               id1, k > 0);
+#pragma unroll
+                    for (int k = 0; k < RP / 16; ++k)
+                        if (k < nkn)
+#pragma unroll
+                            for (int c = 0; c < 4; ++c)
+                                mma_lo<HK, HK>(tbase + TM_DZ + c * 16, at + ((c * SLOT + k * 4096) >> 4), bv + ((k * 512) >> 4),
+                                               id1, k > 0);
+                    commit1(&p1full[q & 1]);
                 };
-                const int64_t q0 = qc;
-                p1(q0);
+                const uint32_t q0 = qc;
+                MT(22, p1(q0));
                 for (int ch = 0; ch < n; ++ch) {
-                    const int64_t q = q0 + ch;
+                    const uint32_t q = q0 + ch;
                     if (ch + 1 < n) {
-                        drain_p1empty(q);
-                        p1(q + 1);
+                        drain_p1empty(q + 1);
+                        MT(22, p1(q + 1));
                     }
-                    wait(&zgfull[q & 1], static_cast<uint32_t>((q >> 1) & 1));
-                    if (rc >= 2) wait(&dfree[rc & 1], static_cast<uint32_t>(((rc - 2) >> 1) & 1));
-                    const unsigned char* zb = sm + OFF_ZG + static_cast<int>(q & 1) * ZGBUF;
-                    const unsigned char* gb = zb + 4 * ZSLOT;
-                    const unsigned char* ut = ring(q) + RL * 32 + 64 + RN * 32;
+                    MT(19, wait(&zgfull[q & 1], static_cast<uint32_t>((q >> 1) & 1)));
+                    if (rc >= 2) MT(20, wait(&dfree[rc & 1], static_cast<uint32_t>(((rc - 2) >> 1) & 1)));
+                    const uint32_t zo = OFF_ZG + static_cast<uint32_t>(q & 1) * ZGBUF, go = zo + 4 * ZSLOT;
                     // T += G U
+                    const uint32_t ag = lo(go, 2048), but = lo(ring(q) + RL * 32 + 64 + RN * 32, (RL / 8) * 128);
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        mma(tbase + TM_Y + c * 64, umma::desc_lo(gb + c * ZSLOT, 2048), HK,
-                            umma::desc_lo(ut, (RL / 8) * 128), HK, id2, ch > 0);
-                    // dU_l^T = SY^T G (lanes 0-15), dV_{l+1}^T = ST^T Z (lanes 16-31)
+                    for (int c = 0; c < 4; ++c) mma_lo<HK, HK>(tbase + TM_Y + c * 64, ag + ((c * ZSLOT) >> 4), but, id2, ch > 0);
+                    // dU_l^T = SY^T G (lanes 0-15), dV_{l+1}^T = ST^T Z (lanes 16-31), interleaved
                     const uint32_t dd = tbase + TM_D + static_cast<uint32_t>(rc & 1) * 16;
+                    const uint32_t my = lo(OFF_SY, 128), mg = lo(go, 128), mt = lo(OFF_ST, 128), mz = lo(zo, 128);
+                    if (!(MTC_SKIP & 1)) {
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
+                        for (int c = 0; c < 4; ++c)
 #pragma unroll
-                        for (int k = 0; k < P / 16; ++k)
-                            mma(dd, umma::desc_lo(sm + OFF_SY + c * SLOT + k * 256, 128), HM,
-                                umma::desc_lo(gb + c * ZSLOT + k * 256, 128), HM, id3, (c | k) != 0);
-#pragma unroll
-                    for (int c = 0; c < 4; ++c)
-#pragma unroll
-                        for (int k = 0; k < P / 16; ++k)
-                            mma(dd + (16u << 16), umma::desc_lo(sm + OFF_ST + c * SLOT + k * 256, 128), HM,
-                                umma::desc_lo(zb + c * ZSLOT + k * 256, 128), HM, id3, (c | k) != 0);
-                    commit(&zgfree[q & 1]);
-                    commit(&dready[rc & 1]);
-                    commit(&slotfree[q % NBUF]);
+                            for (int k = 0; k < P / 16; ++k) {
+                                mma_lo<HM, HM>(dd, my + ((c * SLOT + k * 256) >> 4), mg + ((c * ZSLOT + k * 256) >> 4), id3,
+                                               (c | k) != 0);
+                                mma_lo<HM, HM>(dd + (16u << 16), mt + ((c * SLOT + k * 256) >> 4),
+                                               mz + ((c * ZSLOT + k * 256) >> 4), id3, (c | k) != 0);
+                            }
+                    }
+                    commit1(&zgfree[q & 1]);
+                    commit1(&dready[rc & 1]);
+                    commit1(&slotfree[q % NBUF]);
                     ++rc;
                 }
-                commit(&tdone);
-                drain_p1empty(q0 + n - 1);
+                commit1(&tdone);
+                drain_p1empty(q0 + n);
                 qc += n;
                 ++tcount;
             }
         }
+      }
+      __syncwarp();  // converge the MMA warp before the CTA barrier at the end
     }
     // =========================== epilogue warps ===========================
     else {
@@ -403,14 +516,14 @@ meta_tc_kernel(const MetaNet net, const RunGeom g, const double* __restrict__ pt
         };
         // flush reverse chunk rr (transition l, chunk ch): dU_l^T / dV_{l+1}^T columns 4 grp .. 4 grp + 3
         auto flush = [&](int64_t rr, int l, int ch) {
-            wait(&dready[rr & 1], static_cast<uint32_t>((rr >> 1) & 1));
+            MT(8, wait(&dready[rr & 1], static_cast<uint32_t>((rr >> 1) & 1)));
             float v[4];
             umma::tmem_ld4(tl + TM_D + static_cast<uint32_t>(rr & 1) * 16 + 4 * grp, v);
             umma::tmem_ld_wait();
             signal(&dfree[rr & 1]);
             const int row = 16 * quarter + (lane & 15);
             const bool isV = lane >= 16;
-            if (row < (isV ? net.r[l + 1] : net.r[l]))
+            if (!(MTC_SKIP & 2) && row < (isV ? net.r[l + 1] : net.r[l]))
                 red4(wg + net.gbase[l] + static_cast<int64_t>(ch) * 2048 + (isV ? 1024 : 0) + row * 16 + 4 * grp, v[0],
                      v[1], v[2], v[3]);
         };
@@ -466,12 +579,14 @@ meta_tc_kernel(const MetaNet net, const RunGeom g, const double* __restrict__ pt
                 for (int l = 0; l + 1 < L; ++l) {
                     const int RL = net.rp[l], n = net.nc[l];
                     for (int ch = 0; ch < n; ++ch, ++qc) {
-                        wait(&p1full[qc & 1], static_cast<uint32_t>((qc >> 1) & 1));
-                        float a[4][4];
+                        MT(0, wait(&p1full[qc & 1], static_cast<uint32_t>((qc >> 1) & 1)));
+                        float a[4][4] = {};
+                        if (!(MTC_SKIP & 8)) {
 #pragma unroll
-                        for (int c = 0; c < 4; ++c)
-                            umma::tmem_ld4(tl + TM_P1 + static_cast<uint32_t>(qc & 1) * 64 + c * 16 + 4 * grp, a[c]);
-                        umma::tmem_ld_wait();
+                            for (int c = 0; c < 4; ++c)
+                                umma::tmem_ld4(tl + TM_P1 + static_cast<uint32_t>(qc & 1) * 64 + c * 16 + 4 * grp, a[c]);
+                            umma::tmem_ld_wait();
+                        }
                         signal(&p1empty[qc & 1]);
                         wait(&full[qc % NBUF], static_cast<uint32_t>((qc / NBUF) & 1));
                         const float4 bias = *reinterpret_cast<const float4*>(
@@ -487,15 +602,16 @@ meta_tc_kernel(const MetaNet net, const RunGeom g, const double* __restrict__ pt
                             a[2][k] = d1 * at;
                             a[3][k] = d2 * ax * ax + d1 * aw;
                         }
-                        if (qc >= 2) wait(&zgfree[qc & 1], static_cast<uint32_t>(((qc - 2) >> 1) & 1));
+                        if (qc >= 2) MT(1, wait(&zgfree[qc & 1], static_cast<uint32_t>(((qc - 2) >> 1) & 1)));
                         unsigned char* zb = sm + OFF_ZG + static_cast<int>(qc & 1) * ZGBUF + toff(p, 4 * grp, P) * 2;
+                        if (!(MTC_SKIP & 16))
 #pragma unroll
                         for (int c = 0; c < 4; ++c)
                             sts64(zb + c * ZSLOT, pack_bf16(a[c][0], a[c][1]), pack_bf16(a[c][2], a[c][3]));
                         umma::fence_async_smem();
                         signal(&zgfull[qc & 1]);
                     }
-                    wait(&tdone, tcount & 1);
+                    MT(2, wait(&tdone, tcount & 1));
                     ++tcount;
                     // transition end: Y -> y_{l+1} scratch + SY_{l+1}, or the output layer
                     const int RN = net.rp[l + 1];
@@ -619,14 +735,16 @@ meta_tc_kernel(const MetaNet net, const RunGeom g, const double* __restrict__ pt
                     const int RL = net.rp[l], n = net.nc[l];
                     const int Mn = net.M[l + 1];
                     for (int ch = 0; ch < n; ++ch, ++qc, ++rc) {
-                        wait(&p1full[qc & 1], static_cast<uint32_t>((qc >> 1) & 1));
-                        float a[4][4], dz[4][4];
+                        MT(4, wait(&p1full[qc & 1], static_cast<uint32_t>((qc >> 1) & 1)));
+                        float a[4][4] = {}, dz[4][4] = {};
+                        if (!(MTC_SKIP & 8)) {
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            umma::tmem_ld4(tl + TM_P1 + c * 16 + 4 * grp, a[c]);
-                            umma::tmem_ld4(tl + TM_DZ + c * 16 + 4 * grp, dz[c]);
+                            for (int c = 0; c < 4; ++c) {
+                                umma::tmem_ld4(tl + TM_P1 + c * 16 + 4 * grp, a[c]);
+                                umma::tmem_ld4(tl + TM_DZ + c * 16 + 4 * grp, dz[c]);
+                            }
+                            umma::tmem_ld_wait();
                         }
-                        umma::tmem_ld_wait();
                         signal(&p1empty[qc & 1]);
                         wait(&full[qc % NBUF], static_cast<uint32_t>((qc / NBUF) & 1));
                         const float4 bias = *reinterpret_cast<const float4*>(
@@ -638,7 +756,11 @@ meta_tc_kernel(const MetaNet net, const RunGeom g, const double* __restrict__ pt
                             const float av = a[0][k] + bb[k], ax = a[1][k], at = a[2][k], aw = a[3][k];
                             const float g0 = dz[0][k], g1 = dz[1][k], g2 = dz[2][k], g3 = dz[3][k];
                             float sg, d1, d2, d3;
-                            act3<ACT>(av, sg, d1, d2, d3);
+                            if (MTC_SKIP & 4) {
+                                sg = av; d1 = ax; d2 = at; d3 = aw;
+                            } else {
+                                act3<ACT>(av, sg, d1, d2, d3);
+                            }
                             dz[0][k] = g0 * d1 + g1 * d2 * ax + g2 * d2 * at + g3 * (d3 * ax * ax + d2 * aw);
                             dz[1][k] = g1 * d1 + g3 * 2.f * d2 * ax;
                             dz[2][k] = g2 * d1;
@@ -649,8 +771,9 @@ meta_tc_kernel(const MetaNet net, const RunGeom g, const double* __restrict__ pt
                             a[2][k] = d1 * at;
                             a[3][k] = d2 * ax * ax + d1 * aw;
                         }
-                        if (qc >= 2) wait(&zgfree[qc & 1], static_cast<uint32_t>(((qc - 2) >> 1) & 1));
+                        if (qc >= 2) MT(5, wait(&zgfree[qc & 1], static_cast<uint32_t>(((qc - 2) >> 1) & 1)));
                         unsigned char* zb = sm + OFF_ZG + static_cast<int>(qc & 1) * ZGBUF + toff(p, 4 * grp, P) * 2;
+                        if (!(MTC_SKIP & 16))
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
                             sts64(zb + c * ZSLOT, pack_bf16(a[c][0], a[c][1]), pack_bf16(a[c][2], a[c][3]));
@@ -663,10 +786,10 @@ meta_tc_kernel(const MetaNet net, const RunGeom g, const double* __restrict__ pt
                         const float dbs = treduce<4>(gv, lane, idx);
                         const int k = ch * KC + 4 * grp + idx;
                         if ((lane & 7) == 0 && k < Mn) red1(wq + net.qdb[l] + k, dbs);
-                        if (ch > 0) flush(rc - 1, l, ch - 1);
+                        if (ch > 0) MT(6, flush(rc - 1, l, ch - 1));
                     }
-                    flush(rc - 1, l, n - 1);
-                    wait(&tdone, tcount & 1);
+                    MT(6, flush(rc - 1, l, n - 1));
+                    MT(7, wait(&tdone, tcount & 1));
                     ++tcount;
                     // transition end: T -> dL/ds_l, ST_l (or dV_0), SY_{l-1}
                     if (16 * grp < RL) {
@@ -728,6 +851,10 @@ meta_tc_kernel(const MetaNet net, const RunGeom g, const double* __restrict__ pt
             epi_sync();
         }
     }
+#ifdef MTC_TIMING
+    if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == ISSUER * 32))
+        atomicAdd(&g_mtc_timing[threadIdx.x == 0 ? 15 : 31], static_cast<unsigned long long>(clock64() - t_start));
+#endif
     umma::fence_before();
     __syncthreads();
     if (warp == 0) umma::tmem_dealloc<512>(tbase);
