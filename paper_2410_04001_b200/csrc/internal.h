@@ -127,6 +127,15 @@ struct Model {
         int QS = 0, qdUL = 0, qdbL = 0, qdV0 = 0, sched_len = 0;
         DevBuf dblocks, dsched_off, dsched_bytes, dmap, wg, sum;
     } mtc;
+    // meta tensor-core kernel v2 (pinn_meta_tc2.cuh): neurons on TMEM lanes, 128-neuron chunks
+    struct MTC2 {
+        bool ok = false;
+        std::vector<int> rp, nc, qdb, coff;
+        std::vector<int64_t> yoff, gbase;
+        int64_t ystride = 0, qbase = 0, wg_stride = 0, n_params = 0;
+        int QS = 0, qdUL = 0, qdbL = 0, qdV0 = 0;
+        DevBuf dblocks, dblk_off, dblk_bytes, dmap, wg, sum;
+    } mtc2;
     // narrow-network kernel (pinn_fast.cuh): every hidden width and rank <= 32
     struct FK {
         bool ok = false;
@@ -157,6 +166,10 @@ void build_mtc(Model& m);
 template <int ACT>
 void launch_meta_tc(lrnr_gpu_ctx* ctx, Model& m, const double* s_dev, const double* mu_dev, double w, double* dev_out,
                     double* wg_out);
+void build_mtc2(Model& m);
+template <int ACT>
+void launch_meta_tc2(lrnr_gpu_ctx* ctx, Model& m, const double* s_dev, const double* mu_dev, double w, double* dev_out,
+                     double* wg_out);
 
 template <class T>
 DevNet<T> dev_net(const Model& m) {

@@ -95,7 +95,8 @@ void release_model(Model& m) {
     m.tc.dsched_off.release();
     m.tc.dsched_bytes.release();
     m.flat_dev.release();
-    for (DevBuf* b : {&m.mtc.dblocks, &m.mtc.dsched_off, &m.mtc.dsched_bytes, &m.mtc.dmap, &m.mtc.wg, &m.mtc.sum})
+    for (DevBuf* b : {&m.mtc.dblocks, &m.mtc.dsched_off, &m.mtc.dsched_bytes, &m.mtc.dmap, &m.mtc.wg, &m.mtc.sum,
+                      &m.mtc2.dblocks, &m.mtc2.dblk_off, &m.mtc2.dblk_bytes, &m.mtc2.dmap, &m.mtc2.wg, &m.mtc2.sum})
         b->release();
 }
 
@@ -915,7 +916,7 @@ int lrnr_gpu_set_option(lrnr_gpu_ctx* ctx, int opt, int value) {
         else if (opt == LRNR_OPT_KERNEL) ctx->opt_kernel = value;
         else if (opt == LRNR_OPT_SOLVE) ctx->opt_solve = value;
         else if (opt == LRNR_OPT_META_PREC) {
-            require(value == 0 || value == 1, "meta precision must be 0 (FP32) or 1 (BF16 tensor-core operands)");
+            require(value >= 0 && value <= 2, "meta precision must be 0 (FP32) or 1 / 2 (BF16 tensor-core operands)");
             ctx->opt_meta_prec = value;
         }
         else if (opt == LRNR_OPT_TILE_P) {

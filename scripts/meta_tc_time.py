@@ -17,16 +17,16 @@ ctx.set_lrnr(m, pkg.F32)
 ctx.set_hyper(h)
 ctx.set_points(c["pts"], n_inst=n_inst)
 out = {}
-for prec in ([1, 0] if with_fp32 else [1]):
+for prec in ([1, 2, 0] if with_fp32 else [1, 2]):
     ctx.set_option(pkg.OPT_META_PREC, prec)
     r = ctx.meta_loss_grad(c["mus"], m.params.size)
     torch.cuda.synchronize()
-    K = 3 if prec == 1 else 1
+    K = 3 if prec else 1
     t0 = time.perf_counter()
     for _ in range(K):
         r = ctx.meta_loss_grad(c["mus"], m.params.size)
     dt = (time.perf_counter() - t0) / K
     n = n_inst * per
-    out["bf16_tc" if prec else "fp32_fma"] = dict(ms=dt * 1e3, point_evals_per_s=n / dt, tflops=fl * n / dt / 1e12,
+    out[{1: "bf16_tc_v2", 2: "bf16_tc_v1", 0: "fp32_fma"}[prec]] = dict(ms=dt * 1e3, point_evals_per_s=n / dt, tflops=fl * n / dt / 1e12,
                                                  loss=r["value"], gnorm=float(np.linalg.norm(r["grad"])))
 print(json.dumps(out))
