@@ -141,6 +141,42 @@ __device__ __forceinline__ void mma_lo(uint32_t d, uint32_t alo, uint32_t blo, u
         "r"(alo), "r"(blo), "r"(idesc), "r"(acc), "n"(HA), "n"(HB)
         : "memory");
 }
+// 8 MMAs into one accumulator in a single asm block (one warp-uniformity region
+// for ptxas instead of one per MMA): descriptor low words advance by AST / BST
+// (16-byte units) per MMA; the first MMA accumulates iff acc0 != 0.
+template <uint32_t HA, uint32_t HB, uint32_t AST, uint32_t BST>
+__device__ __forceinline__ void mma_x8(uint32_t d, uint32_t alo, uint32_t blo, uint32_t idesc, uint32_t acc0) {
+#define MTC_MMA8_STEP(I)                                                    \
+    "add.u32 al, %1, " #I "*%7;\n\t"                                        \
+    "add.u32 bl, %2, " #I "*%8;\n\t"                                        \
+    "mov.b64 da, {al, %5};\n\t"                                             \
+    "mov.b64 db, {bl, %6};\n\t"                                             \
+    "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %3, " #I "_P;\n\t"
+    asm volatile(
+        "{\n\t.reg .pred p0, pt;\n\t.reg .b32 al, bl;\n\t.reg .b64 da, db;\n\t"
+        "setp.ne.b32 p0, %4, 0;\n\t"
+        "setp.eq.b32 pt, 0, 0;\n\t"
+        "mov.b64 da, {%1, %5};\n\t"
+        "mov.b64 db, {%2, %6};\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %3, p0;\n\t"
+        "add.u32 al, %1, %7;\n\tadd.u32 bl, %2, %8;\n\tmov.b64 da, {al, %5};\n\tmov.b64 db, {bl, %6};\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %3, pt;\n\t"
+        "add.u32 al, al, %7;\n\tadd.u32 bl, bl, %8;\n\tmov.b64 da, {al, %5};\n\tmov.b64 db, {bl, %6};\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %3, pt;\n\t"
+        "add.u32 al, al, %7;\n\tadd.u32 bl, bl, %8;\n\tmov.b64 da, {al, %5};\n\tmov.b64 db, {bl, %6};\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %3, pt;\n\t"
+        "add.u32 al, al, %7;\n\tadd.u32 bl, bl, %8;\n\tmov.b64 da, {al, %5};\n\tmov.b64 db, {bl, %6};\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %3, pt;\n\t"
+        "add.u32 al, al, %7;\n\tadd.u32 bl, bl, %8;\n\tmov.b64 da, {al, %5};\n\tmov.b64 db, {bl, %6};\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %3, pt;\n\t"
+        "add.u32 al, al, %7;\n\tadd.u32 bl, bl, %8;\n\tmov.b64 da, {al, %5};\n\tmov.b64 db, {bl, %6};\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %3, pt;\n\t"
+        "add.u32 al, al, %7;\n\tadd.u32 bl, bl, %8;\n\tmov.b64 da, {al, %5};\n\tmov.b64 db, {bl, %6};\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %3, pt;\n\t}" ::"r"(d),
+        "r"(alo), "r"(blo), "r"(idesc), "r"(acc0), "n"(HA), "n"(HB), "n"(AST), "n"(BST)
+        : "memory");
+#undef MTC_MMA8_STEP
+}
 __device__ __forceinline__ void commit1(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(umma::smem_addr(bar))
                  : "memory");
@@ -249,7 +285,7 @@ __device__ unsigned long long g_mtc_timing[32];
         const long long _t0 = clock64();                                                  \
         __VA_ARGS__;                                                                      \
         if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == ISSUER * 32))          \
-            atomicAdd(&g_mtc_timing[slot], static_cast<unsigned long long>(clock64() - _t0)); \
+            atomicAdd(&::lrnr_b200::mtc::g_mtc_timing[slot], static_cast<unsigned long long>(clock64() - _t0)); \
     } while (0)
 #else
 #define MT(slot, ...) __VA_ARGS__

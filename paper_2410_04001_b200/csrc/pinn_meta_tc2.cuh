@@ -35,6 +35,7 @@ using mtc::commit1;
 using mtc::epi_sync;
 using mtc::idesc_bf16;
 using mtc::mma_lo;
+using mtc::mma_x8;
 using mtc::pack_bf16;
 using mtc::red1;
 using mtc::red4;
@@ -61,7 +62,8 @@ constexpr int OFF_G = OFF_Z + ZT;
 constexpr int OFF_RING = OFF_G + ZT;
 constexpr int OFF_ACC = OFF_RING + NBUF * BLKS;
 constexpr int MAX_R1 = 512;
-constexpr int SMEM_BYTES = OFF_ACC + 4 * MAX_R1 * 4;
+constexpr int OFF_S = OFF_ACC + 4 * MAX_R1 * 4;  // the unit's s vector (fp32)
+constexpr int SMEM_BYTES = OFF_S + MAX_R1 * 4;
 constexpr uint32_t TM_P1 = 0, TM_DZ = 128, TM_Y = 256, TM_DU = 384, TM_DV = 448;
 constexpr uint32_t HK = (128u >> 4) | (1u << 14);   // SBO 128 B
 constexpr uint32_t HM = (2048u >> 4) | (1u << 14);  // SBO 2048 B
@@ -92,6 +94,9 @@ struct MetaNet2 {
     int64_t wg_stride;
 };
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 // byte offset of (row, col) in a [col grp][row grp][8 rows][8 cols] bf16 tile with `rows` rows
 __device__ __forceinline__ uint32_t tb(int row, int col, int rows) {
     return static_cast<uint32_t>((((col >> 3) * (rows >> 3) + (row >> 3)) * 64 + (row & 7) * 8 + (col & 7)) * 2);
@@ -108,6 +113,7 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
         dfree, tdone, sready;
     __shared__ uint32_t tmem_base;
     float* acc4 = reinterpret_cast<float*>(sm + OFF_ACC);
+    float* ssm = reinterpret_cast<float*>(sm + OFF_S);
 
     const int tid = threadIdx.x, lane = tid & 31;
     const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
@@ -157,6 +163,9 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
         umma::fence_after();
     };
 
+#ifdef MTC_TIMING
+    const long long t_start = clock64();
+#endif
     // =========================== TMA producer ===========================
     if (warp == PRODUCER) {
         if (lane == 0) {
@@ -184,92 +193,60 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
             auto lo = [&](uint32_t off, uint32_t lbo) -> uint32_t { return sbase + (off >> 4) + ((lbo >> 4) << 16); };
             uint32_t s = 0, pe = 0, qc = 0, rc = 0, tcount = 0;
             auto drain = [&](uint32_t end) {  // consume p1empty completions of steps < end, in order
-                for (; pe < end; ++pe) wait(&p1empty[pe & 1], (pe >> 1) & 1);
+                for (; pe < end; ++pe) MT(18, wait(&p1empty[pe & 1], (pe >> 1) & 1));
             };
             auto ringoff = [&](uint32_t q) { return static_cast<uint32_t>(OFF_RING + static_cast<int>(q % NBUF) * BLKS); };
             for (int64_t t = 0; t < total_tiles; ++t) {
                 // ---------------- forward ----------------
+                // step i of the transition (chunk i / 2, half i % 2): P1(i), then P2(i - 1)
                 for (int l = 0; l + 1 < L; ++l) {
-                    wait(&sready, tcount & 1);
+                    MT(16, wait(&sready, tcount & 1));
                     const int RL = net.rp[l], RN = net.rp[l + 1], n = net.nc[l];
                     const uint32_t id1 = idesc_bf16(128, ROWS, 0, 0), id2 = idesc_bf16(128, RN, 1, 1);
-                    bool pend = false;
-                    uint32_t ps = 0, pq = 0;
-                    int ph = 0, pch = 0;
-                    auto p2 = [&]() {  // P2 of the pending step: Y^T of half ph += Z V_c
-                        wait(&zgfull[ps & 1], (ps >> 1) & 1);
-                        const uint32_t az = lo(OFF_Z, 128), bv = lo(ringoff(pq) + RL * 256 + 512, 128);
-                        const uint32_t d = tbase + TM_Y + ph * 64;
-#pragma unroll
-                        for (int k = 0; k < KC / 16; ++k)
-                            mma_lo<HM, HM>(d, az + ((k * 256) >> 4), bv + ((k * 256) >> 4), id2, (pch > 0 || k > 0) ? 1u : 0u);
-                        commit1(&zgfree[ps & 1]);
-                        if (ph == 1) commit1(&slotfree[pq % NBUF]);
-                    };
-                    for (int ch = 0; ch < n; ++ch, ++qc) {
-                        wait(&full[qc % NBUF], (qc / NBUF) & 1);
-                        for (int h = 0; h < 2; ++h, ++s) {
-                            drain(s >= 1 ? s - 1 : 0);  // P1 buffer s & 1 was read by step s - 2
-                            const uint32_t au = lo(ringoff(qc), 2048), by = lo(OFF_SY + h * SYH, 2048);
-                            const uint32_t d = tbase + TM_P1 + (s & 1) * 128;
+                    const uint32_t s0 = s, q0 = qc;
+                    for (int i = 0; i <= 2 * n; ++i) {
+                        if (i < 2 * n) {
+                            const uint32_t si = s0 + i, qi = q0 + (i >> 1);
+                            if ((i & 1) == 0) MT(17, wait(&full[qi % NBUF], (qi / NBUF) & 1));
+                            drain(si >= 1 ? si - 1 : 0);  // P1 buffer si & 1 was read by step si - 2
+                            const uint32_t au = lo(ringoff(qi), 2048), by = lo(OFF_SY + (i & 1) * SYH, 2048);
+                            const uint32_t d = tbase + TM_P1 + (si & 1) * 128;
                             const int nk = RL / 16;
 #pragma unroll
                             for (int k = 0; k < RP / 16; ++k)
                                 if (k < nk) mma_lo<HK, HK>(d, au + ((k * 4096) >> 4), by + ((k * 4096) >> 4), id1, k > 0);
-                            commit1(&p1full[s & 1]);
-                            if (pend) p2();
-                            pend = true;
-                            ps = s;
-                            pq = qc;
-                            ph = h;
-                            pch = ch;
+                            commit1(&p1full[si & 1]);
+                        }
+                        if (i > 0) {
+                            const int j = i - 1;
+                            const uint32_t sj = s0 + j, qj = q0 + (j >> 1);
+                            MT(19, wait(&zgfull[sj & 1], (sj >> 1) & 1));
+                            const uint32_t az = lo(OFF_Z, 128), bv = lo(ringoff(qj) + RL * 256 + 512, 128);
+                            mma_x8<HM, HM, 16, 16>(tbase + TM_Y + (j & 1) * 64, az, bv, id2, j >= 2 ? 1u : 0u);
+                            commit1(&zgfree[sj & 1]);
+                            if (j & 1) commit1(&slotfree[qj % NBUF]);
                         }
                     }
-                    // the last pending P2, then the transition is complete
-                    p2();
+                    s += 2 * n;
+                    qc += n;
                     commit1(&tdone);
                     drain(s);
                     ++tcount;
                 }
                 // ---------------- reverse ----------------
                 for (int l = L - 2; l >= 0; --l) {
-                    wait(&sready, tcount & 1);
+                    MT(16, wait(&sready, tcount & 1));
                     const int RL = net.rp[l], RN = net.rp[l + 1], n = net.nc[l];
                     const uint32_t id1 = idesc_bf16(128, ROWS, 0, 0), id2 = idesc_bf16(128, RL, 1, 1);
                     const uint32_t idu = idesc_bf16(128, RL, 0, 1), idv = idesc_bf16(128, RN, 0, 1);
-                    bool pend = false;
-                    uint32_t ps = 0, pq = 0;
-                    int ph = 0, pch = 0;
-                    auto p2 = [&]() {  // P2r, dU, dV of the pending step
-                        wait(&zgfull[ps & 1], (ps >> 1) & 1);
-                        const uint32_t ag = lo(OFF_G, 128), bu = lo(ringoff(pq), 128);
-                        const uint32_t d = tbase + TM_Y + (ph & 1) * 64;
-#pragma unroll
-                        for (int k = 0; k < KC / 16; ++k)
-                            mma_lo<HM, HM>(d, ag + ((k * 256) >> 4), bu + ((k * 256) >> 4), id2, (pch > 0 || k > 0) ? 1u : 0u);
-                        if ((ph & 1) == 0 && rc >= 1) wait(&dfree, (rc - 1) & 1);  // D free: previous chunk flushed
-                        const uint32_t gk = lo(OFF_G, 2048), zk = lo(OFF_Z, 2048);
-                        const uint32_t sy = lo(OFF_SY + (ph & 1) * SYH, 128), st = lo(OFF_ST + (ph & 1) * SYH, 128);
-#pragma unroll
-                        for (int k = 0; k < ROWS / 16; ++k) {
-                            mma_lo<HK, HM>(tbase + TM_DU, gk + ((k * 4096) >> 4), sy + ((k * 256) >> 4), idu,
-                                           ((ph & 1) | k) != 0 ? 1u : 0u);
-                            mma_lo<HK, HM>(tbase + TM_DV, zk + ((k * 4096) >> 4), st + ((k * 256) >> 4), idv,
-                                           ((ph & 1) | k) != 0 ? 1u : 0u);
-                        }
-                        commit1(&zgfree[ps & 1]);
-                        if ((ph & 1) == 1) {
-                            commit1(&dready);
-                            commit1(&slotfree[pq % NBUF]);
-                            ++rc;
-                        }
-                    };
-                    for (int ch = 0; ch < n; ++ch, ++qc) {
-                        wait(&full[qc % NBUF], (qc / NBUF) & 1);
-                        for (int h = 0; h < 2; ++h, ++s) {
-                            drain(s);  // the single P1r region was read by step s - 1
-                            const uint32_t au = lo(ringoff(qc), 2048), by = lo(OFF_SY + h * SYH, 2048);
-                            const uint32_t av = lo(ringoff(qc) + RL * 256 + 512, 2048), bt = lo(OFF_ST + h * SYH, 2048);
+                    const uint32_t s0 = s, q0 = qc, r0 = rc;
+                    for (int i = 0; i <= 2 * n; ++i) {
+                        if (i < 2 * n) {
+                            const uint32_t si = s0 + i, qi = q0 + (i >> 1);
+                            if ((i & 1) == 0) MT(17, wait(&full[qi % NBUF], (qi / NBUF) & 1));
+                            drain(si);  // the single P1r region was read by step si - 1
+                            const uint32_t au = lo(ringoff(qi), 2048), by = lo(OFF_SY + (i & 1) * SYH, 2048);
+                            const uint32_t av = lo(ringoff(qi) + RL * 256 + 512, 2048), bt = lo(OFF_ST + (i & 1) * SYH, 2048);
                             const int nkl = RL / 16, nkn = RN / 16;
 #pragma unroll
                             for (int k = 0; k < RP / 16; ++k)
@@ -279,16 +256,31 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                             for (int k = 0; k < RP / 16; ++k)
                                 if (k < nkn)
                                     mma_lo<HK, HK>(tbase + TM_DZ, av + ((k * 4096) >> 4), bt + ((k * 4096) >> 4), id1, k > 0);
-                            commit1(&p1full[s & 1]);
-                            if (pend) p2();
-                            pend = true;
-                            ps = s;
-                            pq = qc;
-                            ph = h;
-                            pch = ch;
+                            commit1(&p1full[si & 1]);
+                        }
+                        if (i > 0) {
+                            const int j = i - 1, hj = j & 1;
+                            const uint32_t sj = s0 + j, qj = q0 + (j >> 1), rj = r0 + (j >> 1);
+                            MT(19, wait(&zgfull[sj & 1], (sj >> 1) & 1));
+                            // T += G U_c
+                            mma_x8<HM, HM, 16, 16>(tbase + TM_Y + hj * 64, lo(OFF_G, 128), lo(ringoff(qj), 128), id2,
+                                                   j >= 2 ? 1u : 0u);
+                            if (hj == 0 && rj >= 1) MT(20, wait(&dfree, (rj - 1) & 1));  // D free: previous chunk flushed
+                            // dU_c += G^T SY_l, dV_c += Z^T ST_{l+1} (accumulated over both halves)
+                            mma_x8<HK, HM, 256, 16>(tbase + TM_DU, lo(OFF_G, 2048), lo(OFF_SY + hj * SYH, 128), idu,
+                                                    hj ? 1u : 0u);
+                            mma_x8<HK, HM, 256, 16>(tbase + TM_DV, lo(OFF_Z, 2048), lo(OFF_ST + hj * SYH, 128), idv,
+                                                    hj ? 1u : 0u);
+                            commit1(&zgfree[sj & 1]);
+                            if (hj) {
+                                commit1(&dready);
+                                commit1(&slotfree[qj % NBUF]);
+                            }
                         }
                     }
-                    p2();
+                    s += 2 * n;
+                    qc += n;
+                    rc += n;
                     commit1(&tdone);
                     drain(s);
                     ++tcount;
@@ -309,24 +301,41 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
             __syncwarp();
             if (lane == 0) umma::mbar_arrive(bar);
         };
+#ifdef MTC_TIMING
+        long long tmark = clock64();
+        auto mark = [&](int slot) {
+            const long long t = clock64();
+            if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&mtc::g_mtc_timing[slot], static_cast<unsigned long long>(t - tmark));
+            tmark = t;
+        };
+#else
+        auto mark = [](int) {};
+#endif
         auto st16 = [&](int off, float v0, float v1, float v2, float v3, float v4, float v5, float v6, float v7) {
             sts128(sm + off, pack_bf16(v0, v1), pack_bf16(v2, v3), pack_bf16(v4, v5), pack_bf16(v6, v7));
         };
         // SY_l of both halves (bf16) from the y_l scratch: this thread's row, ranks 16 grp ..
-        auto build_sy = [&](int l, const double* sv) {
+        auto build_sy = [&](int l) {
             const int RL = net.rp[l];
             if (16 * grp >= RL) return;
-            const double* sl = sv + net.soff[l];
+            const float* sl = ssm + net.soff[l];
             const int rt = net.r[l];
             float sj[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) sj[i] = 16 * grp + i < rt ? static_cast<float>(sl[16 * grp + i]) : 0.f;
+            for (int i = 0; i < 16; ++i) sj[i] = 16 * grp + i < rt ? sl[16 * grp + i] : 0.f;
+            float4 yv[2][4];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    yv[h][i] = reinterpret_cast<const float4*>(scr + net.yoff[l] + static_cast<int64_t>(h * ROWS + row) * RL +
+                                                               16 * grp)[i];
+#pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const float* yp = scr + net.yoff[l] + static_cast<int64_t>(h * ROWS + row) * RL + 16 * grp;
                 float y[16];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const float4 v = reinterpret_cast<const float4*>(yp)[i];
+                    const float4 v = yv[h][i];
                     y[4 * i] = v.x * sj[4 * i];
                     y[4 * i + 1] = v.y * sj[4 * i + 1];
                     y[4 * i + 2] = v.z * sj[4 * i + 2];
@@ -341,7 +350,7 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
         // flush the dU / dV chunk of reverse chunk rr (transition l, chunk ch): this thread's
         // neuron, ranks 16 grp .. 16 grp + 15
         auto flush = [&](uint32_t rr, int l, int ch) {
-            wait(&dready, rr & 1);
+            MT(8, wait(&dready, rr & 1));
             float du[16], dv[16];
             umma::tmem_ld16(tl + TM_DU + 16 * grp, du);
             umma::tmem_ld16(tl + TM_DV + 16 * grp, dv);
@@ -364,6 +373,8 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
             const int t_hi = min(g.tiles_per_inst, t_lo + g.tiles_per_unit);
             const double* sv = svec + inst * net.rtotal;
             const float mu0 = float(mus[3 * inst]), mu1 = float(mus[3 * inst + 1]), mu2 = float(mus[3 * inst + 2]);
+            for (int k = tid; k < net.rtotal; k += NWE * 32) ssm[k] = static_cast<float>(sv[k]);
+            epi_sync();
 
             for (int tile = t_lo; tile < t_hi; ++tile) {
                 // ---------------- input layer: y_0 = V_0^T z_0, per jet row ----------------
@@ -398,13 +409,14 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                 }
                 umma::fence_async_smem();
                 signal(&sready);
+                mark(9);
 
                 // ---------------- forward transitions ----------------
                 for (int l = 0; l + 1 < L; ++l) {
                     const int RL = net.rp[l], n = net.nc[l];
                     for (int ch = 0; ch < n; ++ch, ++qc) {
                         for (int h = 0; h < 2; ++h, ++s) {
-                            wait(&p1full[s & 1], (s >> 1) & 1);
+                            MT(0, wait(&p1full[s & 1], (s >> 1) & 1));
                             float a[32];
                             const uint32_t src = tl + TM_P1 + (s & 1) * 128 + 32 * grp;
                             {
@@ -427,7 +439,7 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                                 zp[2 * p] = pack_bf16(sg, d1 * ax);
                                 zp[2 * p + 1] = pack_bf16(d1 * at, d2 * ax * ax + d1 * aw);
                             }
-                            if (s >= 1) wait(&zgfree[(s - 1) & 1], ((s - 1) >> 1) & 1);
+                            if (s >= 1) MT(1, wait(&zgfree[(s - 1) & 1], ((s - 1) >> 1) & 1));
 #pragma unroll
                             for (int i = 0; i < 4; ++i)
                                 sts128(sm + OFF_Z + tb(kn, 32 * grp + 8 * i, KC), zp[4 * i], zp[4 * i + 1], zp[4 * i + 2],
@@ -436,14 +448,33 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                             signal(&zgfull[s & 1]);
                         }
                     }
-                    wait(&tdone, tcount & 1);
+                    mark(10);
+                    MT(2, wait(&tdone, tcount & 1));
                     ++tcount;
+                    mark(3);
                     const int RN = net.rp[l + 1];
                     if (l + 2 < L) {
                         // transition end: Y^T -> y_{l+1} scratch, SY_{l+1}
+                        // SY_{l+1} first (the next transition's MMAs need it), the y scratch after
+                        // sready (Y^T stays in TMEM until this warp's first store of that transition)
                         if (16 * grp < RN) {
-                            const double* sl = sv + net.soff[l + 1];
+                            const float* sl = ssm + net.soff[l + 1];
                             const int rt = net.r[l + 1];
+                            for (int h = 0; h < 2; ++h) {
+                                float y[16];
+                                umma::tmem_ld16(tl + TM_Y + h * 64 + 16 * grp, y);
+                                umma::tmem_ld_wait();
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) y[i] *= 16 * grp + i < rt ? sl[16 * grp + i] : 0.f;
+#pragma unroll
+                                for (int e = 0; e < 2; ++e)
+                                    st16(OFF_SY + h * SYH + tb(row, 16 * grp + 8 * e, ROWS), y[8 * e], y[8 * e + 1],
+                                         y[8 * e + 2], y[8 * e + 3], y[8 * e + 4], y[8 * e + 5], y[8 * e + 6], y[8 * e + 7]);
+                            }
+                        }
+                        umma::fence_async_smem();
+                        signal(&sready);
+                        if (16 * grp < RN)
                             for (int h = 0; h < 2; ++h) {
                                 float y[16];
                                 umma::tmem_ld16(tl + TM_Y + h * 64 + 16 * grp, y);
@@ -452,19 +483,12 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
 #pragma unroll
                                 for (int i = 0; i < 4; ++i)
                                     reinterpret_cast<float4*>(yp)[i] = make_float4(y[4 * i], y[4 * i + 1], y[4 * i + 2], y[4 * i + 3]);
-#pragma unroll
-                                for (int i = 0; i < 16; ++i) y[i] *= 16 * grp + i < rt ? static_cast<float>(sl[16 * grp + i]) : 0.f;
-#pragma unroll
-                                for (int e = 0; e < 2; ++e)
-                                    st16(OFF_SY + h * SYH + tb(row, 16 * grp + 8 * e, ROWS), y[8 * e], y[8 * e + 1],
-                                         y[8 * e + 2], y[8 * e + 3], y[8 * e + 4], y[8 * e + 5], y[8 * e + 6], y[8 * e + 7]);
                             }
-                        }
                     } else {
                         // ---------------- output layer (M_L = 1) + residual, per jet row ----------------
                         if (grp == 0) {
                             const int rL = net.r[L - 1];
-                            const double* sL = sv + net.soff[L - 1];
+                            const float* sL = ssm + net.soff[L - 1];
                             for (int h = 0; h < 2; ++h) {
                                 float y[16];
                                 umma::tmem_ld16(tl + TM_Y + h * 64, y);
@@ -533,19 +557,28 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                                          st[8 * e + 3], st[8 * e + 4], st[8 * e + 5], st[8 * e + 6], st[8 * e + 7]);
                             }
                         }
-                        build_sy(L - 2, sv);
+                        build_sy(L - 2);
+                        umma::fence_async_smem();
+                        signal(&sready);
                     }
-                    umma::fence_async_smem();
-                    signal(&sready);
+                    mark(l + 2 < L ? 11 : 12);
                 }
 
                 // ---------------- reverse transitions ----------------
                 for (int l = L - 2; l >= 0; --l) {
                     const int RL = net.rp[l], n = net.nc[l];
                     const int Mn = net.M[l + 1];
+                    // the transition end reads y_l (dL/ds) and y_{l-1} (SY rebuild) back from the
+                    // scratch: pull this thread's lines into L2 now, so those loads do not pay HBM latency
+                    if (16 * grp < RL)
+                        for (int h = 0; h < 2; ++h)
+                            prefetch_l2(scr + net.yoff[l] + static_cast<int64_t>(h * ROWS + row) * RL + 16 * grp);
+                    if (l > 0 && 16 * grp < net.rp[l - 1])
+                        for (int h = 0; h < 2; ++h)
+                            prefetch_l2(scr + net.yoff[l - 1] + static_cast<int64_t>(h * ROWS + row) * net.rp[l - 1] + 16 * grp);
                     for (int ch = 0; ch < n; ++ch, ++qc) {
                         for (int h = 0; h < 2; ++h, ++s) {
-                            wait(&p1full[s & 1], (s >> 1) & 1);
+                            MT(4, wait(&p1full[s & 1], (s >> 1) & 1));
                             wait(&full[qc % NBUF], (qc / NBUF) & 1);
                             const float bias =
                                 reinterpret_cast<const float*>(sm + OFF_RING + (qc % NBUF) * BLKS + RL * 256)[kn];
@@ -573,7 +606,7 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                                     gz[16 + o + 1] = pack_bf16(d1 * at, d2 * ax * ax + d1 * aw);
                                 }
                             }
-                            if (s >= 1) wait(&zgfree[(s - 1) & 1], ((s - 1) >> 1) & 1);
+                            if (s >= 1) MT(5, wait(&zgfree[(s - 1) & 1], ((s - 1) >> 1) & 1));
 #pragma unroll
                             for (int i = 0; i < 4; ++i) {
                                 sts128(sm + OFF_G + tb(kn, 32 * grp + 8 * i, KC), gz[4 * i], gz[4 * i + 1], gz[4 * i + 2],
@@ -586,45 +619,68 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                             // db_l: this warp's 8 points of this neuron (one writer per (warp, neuron))
                             const int k = ch * KC + kn;
                             if (k < Mn) red1(wq + net.qdb[l] + k, dbs);
-                            if (h == 0 && ch > 0) flush(rc++, l, ch - 1);
+                            if (h == 0 && ch > 0) MT(6, flush(rc++, l, ch - 1));
                         }
                     }
-                    flush(rc++, l, n - 1);
-                    wait(&tdone, tcount & 1);
+                    MT(6, flush(rc++, l, n - 1));
+                    mark(13);
+                    MT(7, wait(&tdone, tcount & 1));
                     ++tcount;
-                    // transition end: T^T -> dL/ds_l, ST_l (or dV_0), SY_{l-1}
-                    if (16 * grp < RL) {
-                        const double* sl = sv + net.soff[l];
-                        const int rt = net.r[l];
-                        float sj[16];
+                    mark(3);
+                    // transition end: ST_l = s_l (.) T_l and SY_{l-1} first (the next transition's
+                    // MMAs need them), then dL/ds_l (and dV_0) after sready: T^T stays in TMEM
+                    // until every warp has stored its first G / Z of the next transition
+                    const float* sl = ssm + net.soff[l];
+                    const int rt = net.r[l];
+                    if (l > 0) {
+                        if (16 * grp < RL) {
+                            float sj[16];
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) sj[i] = 16 * grp + i < rt ? static_cast<float>(sl[16 * grp + i]) : 0.f;
-                        float cd[16];
+                            for (int i = 0; i < 16; ++i) sj[i] = 16 * grp + i < rt ? sl[16 * grp + i] : 0.f;
+                            for (int h = 0; h < 2; ++h) {
+                                float tv[16];
+                                umma::tmem_ld16(tl + TM_Y + h * 64 + 16 * grp, tv);
+                                umma::tmem_ld_wait();
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) cd[i] = 0.f;
-                        float dv0[2] = {0.f, 0.f}, dv1[2] = {0.f, 0.f};
-                        for (int h = 0; h < 2; ++h) {
-                            float tv[16];
-                            umma::tmem_ld16(tl + TM_Y + h * 64 + 16 * grp, tv);
-                            umma::tmem_ld_wait();
-                            const float* yp = scr + net.yoff[l] + static_cast<int64_t>(h * ROWS + row) * RL + 16 * grp;
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                const float4 y4 = reinterpret_cast<const float4*>(yp)[i];
-                                cd[4 * i] = fmaf(tv[4 * i], y4.x, cd[4 * i]);
-                                cd[4 * i + 1] = fmaf(tv[4 * i + 1], y4.y, cd[4 * i + 1]);
-                                cd[4 * i + 2] = fmaf(tv[4 * i + 2], y4.z, cd[4 * i + 2]);
-                                cd[4 * i + 3] = fmaf(tv[4 * i + 3], y4.w, cd[4 * i + 3]);
-                            }
-#pragma unroll
-                            for (int i = 0; i < 16; ++i) tv[i] *= sj[i];
-                            if (l > 0) {
+                                for (int i = 0; i < 16; ++i) tv[i] *= sj[i];
 #pragma unroll
                                 for (int e = 0; e < 2; ++e)
                                     st16(OFF_ST + h * SYH + tb(row, 16 * grp + 8 * e, ROWS), tv[8 * e], tv[8 * e + 1],
                                          tv[8 * e + 2], tv[8 * e + 3], tv[8 * e + 4], tv[8 * e + 5], tv[8 * e + 6],
                                          tv[8 * e + 7]);
-                            } else if (grp == 0) {
+                            }
+                        }
+                        build_sy(l - 1);
+                        umma::fence_async_smem();
+                        signal(&sready);
+                    }
+                    mark(14);
+                    if (16 * grp < RL) {
+                        float cd[16];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) cd[i] = 0.f;
+                        float dv0[2] = {0.f, 0.f}, dv1[2] = {0.f, 0.f};
+                        float4 yv[2][4];  // both halves' y_l, loaded before use
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+#pragma unroll
+                            for (int i = 0; i < 4; ++i)
+                                yv[h][i] = reinterpret_cast<const float4*>(
+                                    scr + net.yoff[l] + static_cast<int64_t>(h * ROWS + row) * RL + 16 * grp)[i];
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            float tv[16];
+                            umma::tmem_ld16(tl + TM_Y + h * 64 + 16 * grp, tv);
+                            umma::tmem_ld_wait();
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const float4 y4 = yv[h][i];
+                                cd[4 * i] = fmaf(tv[4 * i], y4.x, cd[4 * i]);
+                                cd[4 * i + 1] = fmaf(tv[4 * i + 1], y4.y, cd[4 * i + 1]);
+                                cd[4 * i + 2] = fmaf(tv[4 * i + 2], y4.z, cd[4 * i + 2]);
+                                cd[4 * i + 3] = fmaf(tv[4 * i + 3], y4.w, cd[4 * i + 3]);
+                            }
+                            if (l == 0 && grp == 0) {
                                 // dV_0[i][j] = sum over jet rows of z0[row][i] st_0[row][j],
                                 // z0 rows: (x, t), (1, 0), (0, 1), (0, 0)
                                 const int64_t pi = static_cast<int64_t>(tile) * PT + h * PH + pl;
@@ -635,8 +691,9 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                                 const float zi1 = slot == 0 ? t : (slot == 2 ? 1.f : 0.f);
 #pragma unroll
                                 for (int j = 0; j < 2; ++j) {
-                                    dv0[j] = fmaf(zi0, tv[j], dv0[j]);
-                                    dv1[j] = fmaf(zi1, tv[j], dv1[j]);
+                                    const float st0 = j < rt ? sl[j] * tv[j] : 0.f;
+                                    dv0[j] = fmaf(zi0, st0, dv0[j]);
+                                    dv1[j] = fmaf(zi1, st0, dv1[j]);
                                 }
                             }
                         }
@@ -654,11 +711,7 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                             }
                         }
                     }
-                    if (l > 0) {
-                        build_sy(l - 1, sv);
-                        umma::fence_async_smem();
-                        signal(&sready);
-                    }
+                    mark(25);
                 }
             }
             // unit end: [loss, dL/ds] row = sum of the 4 quarter copies (fixed order)
@@ -670,6 +723,10 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
             epi_sync();
         }
     }
+#ifdef MTC_TIMING
+    if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == ISSUER * 32))
+        atomicAdd(&mtc::g_mtc_timing[threadIdx.x == 0 ? 15 : 31], static_cast<unsigned long long>(clock64() - t_start));
+#endif
     umma::fence_before();
     __syncthreads();
     if (warp == 0) umma::tmem_dealloc<512>(tbase);
