@@ -241,6 +241,46 @@ def solve_loops(pkg, local, with_reference):
     return out
 
 
+def meta_step(pkg, local, n_inst=4, per=1 << 20):
+    """BASELINE config 4's meta step (widths 2-512x8-1, ranks (2,64x7,1), hypernetwork
+    3-64-64-451, sin): U, V, b and hypernetwork gradients through the tcgen05 meta kernel
+    (LRNR_OPT_META_PREC = 1: BF16 operands, FP32 accumulation), on a bounded sample of
+    n_inst of the 64 instances x 1,048,576 points; device time of the whole step (meta
+    kernel + reductions + hypernetwork VJP) with CUDA events, points resident."""
+    import torch
+    c = pkg.config4(n_inst=n_inst, pts_per_inst=per)
+    m, h = c["model"], c["hyper"]
+    fl = pkg.algorithmic_flops_per_point(m.widths, m.ranks, meta=True)
+    ctx = pkg.GpuContext(local)
+    ctx.set_option(pkg.OPT_META_PREC, 1)
+    ctx.set_lrnr(m, pkg.F32)
+    ctx.set_hyper(h)
+    ctx.set_points(c["pts"], n_inst=n_inst)
+    stream = torch.cuda.current_stream(local)
+    ctx.set_stream(stream.cuda_stream)
+    ctx.meta_loss_grad(c["mus"], m.params.size)
+    reps = 3
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(local)
+    e0.record(stream)
+    for _ in range(reps):
+        r = ctx.meta_loss_grad(c["mus"], m.params.size)
+    e1.record(stream)
+    torch.cuda.synchronize(local)
+    ms = e0.elapsed_time(e1) / reps
+    ctx.close()
+    n = n_inst * per
+    tf = fl * n / (ms * 1e-3) / 1e12
+    peak = measured_peak("bf16_tflops_sustained", 1400.0)
+    return {"workload": f"c4 meta step: {n_inst} of the 64 mu instances x {per} points, 2-512x8-1, r (2,64x7,1), "
+                        "hypernet 3-64-64-451, sin; grads U, V, b, theta (498,121)",
+            "kernel": "meta_tc2_kernel (tcgen05 kind::f16, BF16 operands, FP32 accumulate)",
+            "ms_per_step": ms, "point_evals_per_s": n / ms * 1e3, "flop_per_point": fl, "tflops": tf,
+            "tensor_roofline": {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
+                                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS bf16, 4 s)"},
+            "full_step_64_instances_ms_extrapolated": ms * 64 / n_inst, "loss": r["value"]}
+
+
 # ---------------------------------------------------------------------------
 # reference arm
 # ---------------------------------------------------------------------------
@@ -439,6 +479,13 @@ def run_ours(args):
         except Exception as e:  # reported, never fatal
             solves = {"error": str(e)}
 
+    meta = None
+    if rank == 0 and world == 1 and not args.no_solves:
+        try:
+            meta = meta_step(pkg, local)
+        except Exception as e:  # reported, never fatal
+            meta = {"error": str(e)}
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -449,7 +496,7 @@ def run_ours(args):
                            "kernel_option": args.kernel, "fast_sincos": args.fast_sincos},
                 "roofline": roofline, "kernels": per_kernel, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk.summary(), "solve_loops": solves,
-                "fast_vs_lrnr": approx}
+                "fast_vs_lrnr": approx, "meta_c4": meta}
         print(json.dumps(line))
     ctx.close()
     if dist is not None:

@@ -1,6 +1,6 @@
 """Throughput of the non-headline BASELINE configs on one GPU (measurement record):
 c3 = hypernetwork -> FastLRNR per instance + hypernet VJP (1024 mu x 16,384 pts),
-c4 = meta step (U, V, b, theta gradients; 8 of the 64 mu x 1,048,576 pts per step).
+c4 = meta step (U, V, b, theta gradients; 64 mu x 1,048,576 pts per step on the BF16 tensor-core kernel, 2 of them on the FP32 FMA path).
 Device time with CUDA events around the host-buffer call (points resident)."""
 import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -29,22 +29,28 @@ out["c3"] = {"ms_per_step": dt * 1e3, "point_evals_per_s": n / dt, "tflops": fl 
              "frac_fp32_fma": fl * n / dt / 1e12 / PEAK, "flop_per_point": fl, "points": n,
              "kernel": "narrow-network kernel (FastLRNR, auto) + FP64 hypernetwork fwd/VJP", "loss": r["value"]}
 ctx.close()
-# c4 (8 instances per step; the 64-instance step is 8x this)
-n_inst, per = 8, 1 << 20
-c = pkg.config4(n_inst=n_inst, pts_per_inst=per)
-ctx = pkg.GpuContext(0)
-ctx.set_lrnr(c["model"], pkg.F32)
-ctx.set_hyper(c["hyper"])
-ctx.set_points(c["pts"], n_inst=n_inst)
-ctx.meta_loss_grad(c["mus"], c["model"].params.size)
-torch.cuda.synchronize()
-t0 = time.perf_counter()
-r = ctx.meta_loss_grad(c["mus"], c["model"].params.size)
-dt = time.perf_counter() - t0
-n = n_inst * per
-fl = pkg.algorithmic_flops_per_point(c["model"].widths, c["model"].ranks, meta=True)
-out["c4"] = {"ms_per_step_8_of_64_instances": dt * 1e3, "point_evals_per_s": n / dt, "tflops": fl * n / dt / 1e12,
-             "frac_fp32_fma": fl * n / dt / 1e12 / PEAK, "flop_per_point": fl, "points": n,
-             "kernel": "FMA tile (META phase 3) + FP64 hypernetwork", "loss": r["value"]}
-ctx.close()
+# c4: the full meta step (64 instances x 1,048,576 points) on the tcgen05 meta kernel
+# (BF16 operands, FP32 accumulate), and 2 of the 64 instances on the FP32 FMA tile kernel
+for prec, n_inst in ((1, 64), (0, 2)):
+    per = 1 << 20
+    c = pkg.config4(n_inst=n_inst, pts_per_inst=per)
+    ctx = pkg.GpuContext(0)
+    ctx.set_option(pkg.OPT_META_PREC, prec)
+    ctx.set_lrnr(c["model"], pkg.F32)
+    ctx.set_hyper(c["hyper"])
+    ctx.set_points(c["pts"], n_inst=n_inst)
+    ctx.meta_loss_grad(c["mus"], c["model"].params.size)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = ctx.meta_loss_grad(c["mus"], c["model"].params.size)
+    dt = time.perf_counter() - t0
+    n = n_inst * per
+    fl = pkg.algorithmic_flops_per_point(c["model"].widths, c["model"].ranks, meta=True)
+    key = "c4_bf16_tc" if prec else "c4_fp32_fma"
+    out[key] = {"instances": n_inst, "ms_per_step": dt * 1e3, "point_evals_per_s": n / dt, "tflops": fl * n / dt / 1e12,
+                "frac_fp32_fma": fl * n / dt / 1e12 / PEAK, "frac_bf16_sustained": fl * n / dt / 1e12 / 1398.4,
+                "flop_per_point": fl, "points": n, "loss": r["value"],
+                "kernel": "meta_tc2_kernel (tcgen05, BF16 operands, FP32 accumulate) + FP64 hypernetwork" if prec else
+                "FMA tile (META phase 3, FP32) + FP64 hypernetwork"}
+    ctx.close()
 print(json.dumps(out))
