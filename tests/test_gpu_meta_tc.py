@@ -133,9 +133,12 @@ def test_meta_tc_full_emitter_with_boundary_and_regularizers(bf16):
     bf16.set_hyper(h)
     bf16.set_points(c["pts"], n_inst=n_inst)
     bf16.set_meta_boundary(n_inst, rng.uniform(0, 2 * np.pi, 2 * 32), rng.uniform(0, 1, 2 * 16))
-    a = bf16.meta_terms_grad(c["mus"], m.params.size, 1e-3, 1.5, 1e-4)
-    bf16.set_option(pkg.OPT_META_PREC, 0)
-    ref = bf16.meta_terms_grad(c["mus"], m.params.size, 1e-3, 1.5, 1e-4)
+    try:
+        a = bf16.meta_terms_grad(c["mus"], m.params.size, 1e-3, 1.5, 1e-4)
+        bf16.set_option(pkg.OPT_META_PREC, 0)
+        ref = bf16.meta_terms_grad(c["mus"], m.params.size, 1e-3, 1.5, 1e-4)
+    finally:
+        bf16.set_meta_boundary(n_inst)  # the context is shared by the session: drop the boundary points
     print(f"full emitter vs FP32: loss rel {abs(a['value'] - ref['value']) / abs(ref['value']):.2e} "
           f"grad norm {normwise(a['grad'], ref['grad']):.2e}")
     assert abs(a["value"] - ref["value"]) <= TOL_BF16_LOSS * abs(ref["value"])
