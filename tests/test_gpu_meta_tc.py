@@ -155,3 +155,28 @@ def test_meta_tc_rejects_ineligible_models(bf16):
     bf16.set_points(c["pts"], n_inst=1)
     with pytest.raises(ValueError):
         bf16.meta_loss_grad(c["mus"], m.params.size)
+
+
+@pytest.mark.parametrize("widths,ranks", [([2, 100, 150, 72, 1], [2, 10, 40, 1]),
+                                          ([2, 200, 130, 1], [2, 64, 1])])
+def test_meta_tc_ragged_widths_and_ranks(bf16, oracle, widths, ranks):
+    """Hidden widths that are not multiples of the 128-neuron chunk and ranks that are not
+    multiples of 16 (zero-padded on the device), several instances, ragged point counts."""
+    n_inst, per = 3, 150
+    m, _ = pkg.make_baseline_model(widths, ranks, 77, pkg.ACT_SIN)
+    h = pkg.make_hyper_params(ranks, 2, 64, 78, pkg.api.C3_LO, pkg.api.C3_HI, 0.01, 0.5)
+    _, mus = pkg.sample_collocation(79, n_inst, pkg.api.C3_LO, pkg.api.C3_HI, with_mu=True)
+    pts = np.concatenate([pkg.sample_collocation(80 + i, per) for i in range(n_inst)])
+    c = dict(model=m, hyper=h, mus=mus, pts=pts)
+    bf16.set_lrnr(m, pkg.F32)
+    bf16.set_hyper(h)
+    bf16.set_points(pts, n_inst=n_inst)
+    got = bf16.meta_loss_grad(mus, m.params.size)
+    nP = m.params.size
+    val, want = bf16_model_meta(oracle, c, n_inst, per, pkg.ACT_SIN)
+    assert abs(got["value"] - val) <= TOL_EMU * abs(val)
+    assert normwise(got["grad"], want) <= TOL_EMU
+    assert normwise(got["grad"][nP:], want[nP:]) <= TOL_EMU_HYPER
+    val, want = oracle_meta(oracle, c, n_inst, per, pkg.ACT_SIN)
+    assert abs(got["value"] - val) <= TOL_BF16_LOSS * abs(val)
+    assert normwise(got["grad"], want) <= TOL_BF16_NORM
