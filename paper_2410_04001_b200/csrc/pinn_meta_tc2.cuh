@@ -357,6 +357,7 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
             umma::tmem_ld_wait();
             signal(&dfree);
             float* base = wg + net.gbase[l] + static_cast<int64_t>(ch) * 16384 + kn * 64 + 16 * grp;
+            if (MTC_SKIP & 2) return;
             if (16 * grp < net.rp[l])
 #pragma unroll
                 for (int i = 0; i < 4; ++i) red4(base + 4 * i, du[4 * i], du[4 * i + 1], du[4 * i + 2], du[4 * i + 3]);
