@@ -32,7 +32,6 @@ namespace mtc2 {
 
 using mtc::act3;
 using mtc::commit1;
-using mtc::epi_sync;
 using mtc::idesc_bf16;
 using mtc::mma_lo;
 using mtc::mma_x8;
@@ -48,7 +47,13 @@ constexpr int ROWS = 4 * PH;      // jet rows per half (MMA N of P1, M of P2)
 constexpr int PT = 2 * PH;        // points per tile
 constexpr int KC = 128;           // neurons per chunk
 constexpr int RP = 64;            // max padded rank
-constexpr int NWE = 16;
+#ifndef MTC2_NWE
+#define MTC2_NWE 16
+#endif
+constexpr int NWE = MTC2_NWE;     // epilogue warps (32 + 2 would exceed 1024 threads per CTA)
+constexpr int NGRP = NWE / 4;     // warps per TMEM lane quarter
+constexpr int CW = ROWS / NGRP;   // P1 columns (jet rows) per warp per half-step: 32 or 16
+constexpr int RW = 64 / NGRP;     // ranks per warp at the transition ends: 16 or 8
 constexpr int ISSUER = NWE, PRODUCER = NWE + 1;
 constexpr int NT = 32 * (NWE + 2);
 constexpr int NBUF = 2;
@@ -96,6 +101,12 @@ struct MetaNet2 {
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NWE * 32) : "memory"); }
+// RW consecutive TMEM columns of this warp's lanes
+__device__ __forceinline__ void tld_rw(uint32_t taddr, float (&v)[RW]) {
+    if constexpr (RW == 16) umma::tmem_ld16(taddr, *reinterpret_cast<float(*)[16]>(v));
+    else umma::tmem_ld8(taddr, *reinterpret_cast<float(*)[8]>(v));
 }
 // byte offset of (row, col) in a [col grp][row grp][8 rows][8 cols] bf16 tile with `rows` rows
 __device__ __forceinline__ uint32_t tb(int row, int col, int rows) {
@@ -314,27 +325,27 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
         auto st16 = [&](int off, float v0, float v1, float v2, float v3, float v4, float v5, float v6, float v7) {
             sts128(sm + off, pack_bf16(v0, v1), pack_bf16(v2, v3), pack_bf16(v4, v5), pack_bf16(v6, v7));
         };
-        // SY_l of both halves (bf16) from the y_l scratch: this thread's row, ranks 16 grp ..
+        // SY_l of both halves (bf16) from the y_l scratch: this thread's row, ranks RW grp ..
         auto build_sy = [&](int l) {
             const int RL = net.rp[l];
-            if (16 * grp >= RL) return;
+            if (RW * grp >= RL) return;
             const float* sl = ssm + net.soff[l];
             const int rt = net.r[l];
-            float sj[16];
+            float sj[RW];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) sj[i] = 16 * grp + i < rt ? sl[16 * grp + i] : 0.f;
-            float4 yv[2][4];
+            for (int i = 0; i < RW; ++i) sj[i] = RW * grp + i < rt ? sl[RW * grp + i] : 0.f;
+            float4 yv[2][RW / 4];
 #pragma unroll
             for (int h = 0; h < 2; ++h)
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
+                for (int i = 0; i < RW / 4; ++i)
                     yv[h][i] = reinterpret_cast<const float4*>(scr + net.yoff[l] + static_cast<int64_t>(h * ROWS + row) * RL +
-                                                               16 * grp)[i];
+                                                               RW * grp)[i];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                float y[16];
+                float y[RW];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
+                for (int i = 0; i < RW / 4; ++i) {
                     const float4 v = yv[h][i];
                     y[4 * i] = v.x * sj[4 * i];
                     y[4 * i + 1] = v.y * sj[4 * i + 1];
@@ -342,28 +353,28 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                     y[4 * i + 3] = v.w * sj[4 * i + 3];
                 }
 #pragma unroll
-                for (int e = 0; e < 2; ++e)
-                    st16(OFF_SY + h * SYH + tb(row, 16 * grp + 8 * e, ROWS), y[8 * e], y[8 * e + 1], y[8 * e + 2],
+                for (int e = 0; e < RW / 8; ++e)
+                    st16(OFF_SY + h * SYH + tb(row, RW * grp + 8 * e, ROWS), y[8 * e], y[8 * e + 1], y[8 * e + 2],
                          y[8 * e + 3], y[8 * e + 4], y[8 * e + 5], y[8 * e + 6], y[8 * e + 7]);
             }
         };
         // flush the dU / dV chunk of reverse chunk rr (transition l, chunk ch): this thread's
-        // neuron, ranks 16 grp .. 16 grp + 15
+        // neuron, ranks RW grp .. RW grp + RW - 1
         auto flush = [&](uint32_t rr, int l, int ch) {
             MT(8, wait(&dready, rr & 1));
-            float du[16], dv[16];
-            umma::tmem_ld16(tl + TM_DU + 16 * grp, du);
-            umma::tmem_ld16(tl + TM_DV + 16 * grp, dv);
+            float du[RW], dv[RW];
+            tld_rw(tl + TM_DU + RW * grp, du);
+            tld_rw(tl + TM_DV + RW * grp, dv);
             umma::tmem_ld_wait();
             signal(&dfree);
-            float* base = wg + net.gbase[l] + static_cast<int64_t>(ch) * 16384 + kn * 64 + 16 * grp;
+            float* base = wg + net.gbase[l] + static_cast<int64_t>(ch) * 16384 + kn * 64 + RW * grp;
             if (MTC_SKIP & 2) return;
-            if (16 * grp < net.rp[l])
+            if (RW * grp < net.rp[l])
 #pragma unroll
-                for (int i = 0; i < 4; ++i) red4(base + 4 * i, du[4 * i], du[4 * i + 1], du[4 * i + 2], du[4 * i + 3]);
-            if (16 * grp < net.rp[l + 1])
+                for (int i = 0; i < RW / 4; ++i) red4(base + 4 * i, du[4 * i], du[4 * i + 1], du[4 * i + 2], du[4 * i + 3]);
+            if (RW * grp < net.rp[l + 1])
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
+                for (int i = 0; i < RW / 4; ++i)
                     red4(base + 8192 + 4 * i, dv[4 * i], dv[4 * i + 1], dv[4 * i + 2], dv[4 * i + 3]);
         };
 
@@ -418,22 +429,19 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                     for (int ch = 0; ch < n; ++ch, ++qc) {
                         for (int h = 0; h < 2; ++h, ++s) {
                             MT(0, wait(&p1full[s & 1], (s >> 1) & 1));
-                            float a[32];
-                            const uint32_t src = tl + TM_P1 + (s & 1) * 128 + 32 * grp;
-                            {
-                                float (&a0)[16] = *reinterpret_cast<float(*)[16]>(a);
-                                float (&a1)[16] = *reinterpret_cast<float(*)[16]>(a + 16);
-                                umma::tmem_ld16(src, a0);
-                                umma::tmem_ld16(src + 16, a1);
-                            }
+                            float a[CW];
+                            const uint32_t src = tl + TM_P1 + (s & 1) * 128 + CW * grp;
+#pragma unroll
+                            for (int i = 0; i < CW / 16; ++i)
+                                umma::tmem_ld16(src + 16 * i, *reinterpret_cast<float(*)[16]>(a + 16 * i));
                             umma::tmem_ld_wait();
                             signal(&p1empty[s & 1]);
                             wait(&full[qc % NBUF], (qc / NBUF) & 1);
                             const float bias =
                                 reinterpret_cast<const float*>(sm + OFF_RING + (qc % NBUF) * BLKS + RL * 256)[kn];
-                            uint32_t zp[16];
+                            uint32_t zp[CW / 2];
 #pragma unroll
-                            for (int p = 0; p < 8; ++p) {
+                            for (int p = 0; p < CW / 4; ++p) {
                                 const float av = a[4 * p] + bias, ax = a[4 * p + 1], at = a[4 * p + 2], aw = a[4 * p + 3];
                                 float sg, d1, d2, d3;
                                 act3<ACT>(av, sg, d1, d2, d3);
@@ -442,8 +450,8 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                             }
                             if (s >= 1) MT(1, wait(&zgfree[(s - 1) & 1], ((s - 1) >> 1) & 1));
 #pragma unroll
-                            for (int i = 0; i < 4; ++i)
-                                sts128(sm + OFF_Z + tb(kn, 32 * grp + 8 * i, KC), zp[4 * i], zp[4 * i + 1], zp[4 * i + 2],
+                            for (int i = 0; i < CW / 8; ++i)
+                                sts128(sm + OFF_Z + tb(kn, CW * grp + 8 * i, KC), zp[4 * i], zp[4 * i + 1], zp[4 * i + 2],
                                        zp[4 * i + 3]);
                             umma::fence_async_smem();
                             signal(&zgfull[s & 1]);
@@ -458,31 +466,31 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                         // transition end: Y^T -> y_{l+1} scratch, SY_{l+1}
                         // SY_{l+1} first (the next transition's MMAs need it), the y scratch after
                         // sready (Y^T stays in TMEM until this warp's first store of that transition)
-                        if (16 * grp < RN) {
+                        if (RW * grp < RN) {
                             const float* sl = ssm + net.soff[l + 1];
                             const int rt = net.r[l + 1];
                             for (int h = 0; h < 2; ++h) {
-                                float y[16];
-                                umma::tmem_ld16(tl + TM_Y + h * 64 + 16 * grp, y);
+                                float y[RW];
+                                tld_rw(tl + TM_Y + h * 64 + RW * grp, y);
                                 umma::tmem_ld_wait();
 #pragma unroll
-                                for (int i = 0; i < 16; ++i) y[i] *= 16 * grp + i < rt ? sl[16 * grp + i] : 0.f;
+                                for (int i = 0; i < RW; ++i) y[i] *= RW * grp + i < rt ? sl[RW * grp + i] : 0.f;
 #pragma unroll
-                                for (int e = 0; e < 2; ++e)
-                                    st16(OFF_SY + h * SYH + tb(row, 16 * grp + 8 * e, ROWS), y[8 * e], y[8 * e + 1],
+                                for (int e = 0; e < RW / 8; ++e)
+                                    st16(OFF_SY + h * SYH + tb(row, RW * grp + 8 * e, ROWS), y[8 * e], y[8 * e + 1],
                                          y[8 * e + 2], y[8 * e + 3], y[8 * e + 4], y[8 * e + 5], y[8 * e + 6], y[8 * e + 7]);
                             }
                         }
                         umma::fence_async_smem();
                         signal(&sready);
-                        if (16 * grp < RN)
+                        if (RW * grp < RN)
                             for (int h = 0; h < 2; ++h) {
-                                float y[16];
-                                umma::tmem_ld16(tl + TM_Y + h * 64 + 16 * grp, y);
+                                float y[RW];
+                                tld_rw(tl + TM_Y + h * 64 + RW * grp, y);
                                 umma::tmem_ld_wait();
-                                float* yp = scr + net.yoff[l + 1] + static_cast<int64_t>(h * ROWS + row) * RN + 16 * grp;
+                                float* yp = scr + net.yoff[l + 1] + static_cast<int64_t>(h * ROWS + row) * RN + RW * grp;
 #pragma unroll
-                                for (int i = 0; i < 4; ++i)
+                                for (int i = 0; i < RW / 4; ++i)
                                     reinterpret_cast<float4*>(yp)[i] = make_float4(y[4 * i], y[4 * i + 1], y[4 * i + 2], y[4 * i + 3]);
                             }
                     } else {
@@ -571,27 +579,27 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                     const int Mn = net.M[l + 1];
                     // the transition end reads y_l (dL/ds) and y_{l-1} (SY rebuild) back from the
                     // scratch: pull this thread's lines into L2 now, so those loads do not pay HBM latency
-                    if (16 * grp < RL)
+                    if (RW * grp < RL)
                         for (int h = 0; h < 2; ++h)
-                            prefetch_l2(scr + net.yoff[l] + static_cast<int64_t>(h * ROWS + row) * RL + 16 * grp);
-                    if (l > 0 && 16 * grp < net.rp[l - 1])
+                            prefetch_l2(scr + net.yoff[l] + static_cast<int64_t>(h * ROWS + row) * RL + RW * grp);
+                    if (l > 0 && RW * grp < net.rp[l - 1])
                         for (int h = 0; h < 2; ++h)
-                            prefetch_l2(scr + net.yoff[l - 1] + static_cast<int64_t>(h * ROWS + row) * net.rp[l - 1] + 16 * grp);
+                            prefetch_l2(scr + net.yoff[l - 1] + static_cast<int64_t>(h * ROWS + row) * net.rp[l - 1] + RW * grp);
                     for (int ch = 0; ch < n; ++ch, ++qc) {
                         for (int h = 0; h < 2; ++h, ++s) {
                             MT(4, wait(&p1full[s & 1], (s >> 1) & 1));
                             wait(&full[qc % NBUF], (qc / NBUF) & 1);
                             const float bias =
                                 reinterpret_cast<const float*>(sm + OFF_RING + (qc % NBUF) * BLKS + RL * 256)[kn];
-                            uint32_t gz[32];  // packed bf16: G (16 words) then Z (16 words), 8 points
+                            uint32_t gz[CW];  // packed bf16: G (CW / 2 words) then Z (CW / 2 words)
                             float dbs = 0.f;
 #pragma unroll
-                            for (int pass = 0; pass < 2; ++pass) {
+                            for (int pass = 0; pass < CW / 16; ++pass) {
                                 float a[16], dz[16];
-                                umma::tmem_ld16(tl + TM_P1 + 32 * grp + 16 * pass, a);
-                                umma::tmem_ld16(tl + TM_DZ + 32 * grp + 16 * pass, dz);
+                                umma::tmem_ld16(tl + TM_P1 + CW * grp + 16 * pass, a);
+                                umma::tmem_ld16(tl + TM_DZ + CW * grp + 16 * pass, dz);
                                 umma::tmem_ld_wait();
-                                if (pass == 1) signal(&p1empty[s & 1]);
+                                if (pass == CW / 16 - 1) signal(&p1empty[s & 1]);
 #pragma unroll
                                 for (int p = 0; p < 4; ++p) {
                                     const float av = a[4 * p] + bias, ax = a[4 * p + 1], at = a[4 * p + 2], aw = a[4 * p + 3];
@@ -603,21 +611,21 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                                     const int o = 2 * (4 * pass + p);
                                     gz[o] = pack_bf16(gv, g1 * d1 + g3 * 2.f * d2 * ax);
                                     gz[o + 1] = pack_bf16(g2 * d1, g3 * d1);
-                                    gz[16 + o] = pack_bf16(sg, d1 * ax);
-                                    gz[16 + o + 1] = pack_bf16(d1 * at, d2 * ax * ax + d1 * aw);
+                                    gz[CW / 2 + o] = pack_bf16(sg, d1 * ax);
+                                    gz[CW / 2 + o + 1] = pack_bf16(d1 * at, d2 * ax * ax + d1 * aw);
                                 }
                             }
                             if (s >= 1) MT(5, wait(&zgfree[(s - 1) & 1], ((s - 1) >> 1) & 1));
 #pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                sts128(sm + OFF_G + tb(kn, 32 * grp + 8 * i, KC), gz[4 * i], gz[4 * i + 1], gz[4 * i + 2],
+                            for (int i = 0; i < CW / 8; ++i) {
+                                sts128(sm + OFF_G + tb(kn, CW * grp + 8 * i, KC), gz[4 * i], gz[4 * i + 1], gz[4 * i + 2],
                                        gz[4 * i + 3]);
-                                sts128(sm + OFF_Z + tb(kn, 32 * grp + 8 * i, KC), gz[16 + 4 * i], gz[16 + 4 * i + 1],
-                                       gz[16 + 4 * i + 2], gz[16 + 4 * i + 3]);
+                                sts128(sm + OFF_Z + tb(kn, CW * grp + 8 * i, KC), gz[CW / 2 + 4 * i], gz[CW / 2 + 4 * i + 1],
+                                       gz[CW / 2 + 4 * i + 2], gz[CW / 2 + 4 * i + 3]);
                             }
                             umma::fence_async_smem();
                             signal(&zgfull[s & 1]);
-                            // db_l: this warp's 8 points of this neuron (one writer per (warp, neuron))
+                            // db_l: this warp's points of this neuron (one writer per (warp, neuron))
                             const int k = ch * KC + kn;
                             if (k < Mn) red1(wq + net.qdb[l] + k, dbs);
                             if (h == 0 && ch > 0) MT(6, flush(rc++, l, ch - 1));
@@ -634,19 +642,19 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                     const float* sl = ssm + net.soff[l];
                     const int rt = net.r[l];
                     if (l > 0) {
-                        if (16 * grp < RL) {
-                            float sj[16];
+                        if (RW * grp < RL) {
+                            float sj[RW];
 #pragma unroll
-                            for (int i = 0; i < 16; ++i) sj[i] = 16 * grp + i < rt ? sl[16 * grp + i] : 0.f;
+                            for (int i = 0; i < RW; ++i) sj[i] = RW * grp + i < rt ? sl[RW * grp + i] : 0.f;
                             for (int h = 0; h < 2; ++h) {
-                                float tv[16];
-                                umma::tmem_ld16(tl + TM_Y + h * 64 + 16 * grp, tv);
+                                float tv[RW];
+                                tld_rw(tl + TM_Y + h * 64 + RW * grp, tv);
                                 umma::tmem_ld_wait();
 #pragma unroll
-                                for (int i = 0; i < 16; ++i) tv[i] *= sj[i];
+                                for (int i = 0; i < RW; ++i) tv[i] *= sj[i];
 #pragma unroll
-                                for (int e = 0; e < 2; ++e)
-                                    st16(OFF_ST + h * SYH + tb(row, 16 * grp + 8 * e, ROWS), tv[8 * e], tv[8 * e + 1],
+                                for (int e = 0; e < RW / 8; ++e)
+                                    st16(OFF_ST + h * SYH + tb(row, RW * grp + 8 * e, ROWS), tv[8 * e], tv[8 * e + 1],
                                          tv[8 * e + 2], tv[8 * e + 3], tv[8 * e + 4], tv[8 * e + 5], tv[8 * e + 6],
                                          tv[8 * e + 7]);
                             }
@@ -656,25 +664,25 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                         signal(&sready);
                     }
                     mark(14);
-                    if (16 * grp < RL) {
-                        float cd[16];
+                    if (RW * grp < RL) {
+                        float cd[RW];
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) cd[i] = 0.f;
+                        for (int i = 0; i < RW; ++i) cd[i] = 0.f;
                         float dv0[2] = {0.f, 0.f}, dv1[2] = {0.f, 0.f};
-                        float4 yv[2][4];  // both halves' y_l, loaded before use
+                        float4 yv[2][RW / 4];  // both halves' y_l, loaded before use
 #pragma unroll
                         for (int h = 0; h < 2; ++h)
 #pragma unroll
-                            for (int i = 0; i < 4; ++i)
+                            for (int i = 0; i < RW / 4; ++i)
                                 yv[h][i] = reinterpret_cast<const float4*>(
-                                    scr + net.yoff[l] + static_cast<int64_t>(h * ROWS + row) * RL + 16 * grp)[i];
+                                    scr + net.yoff[l] + static_cast<int64_t>(h * ROWS + row) * RL + RW * grp)[i];
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
-                            float tv[16];
-                            umma::tmem_ld16(tl + TM_Y + h * 64 + 16 * grp, tv);
+                            float tv[RW];
+                            tld_rw(tl + TM_Y + h * 64 + RW * grp, tv);
                             umma::tmem_ld_wait();
 #pragma unroll
-                            for (int i = 0; i < 4; ++i) {
+                            for (int i = 0; i < RW / 4; ++i) {
                                 const float4 y4 = yv[h][i];
                                 cd[4 * i] = fmaf(tv[4 * i], y4.x, cd[4 * i]);
                                 cd[4 * i + 1] = fmaf(tv[4 * i + 1], y4.y, cd[4 * i + 1]);
@@ -699,9 +707,9 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                             }
                         }
                         int idx;
-                        const float cs = treduce<16>(cd, lane, idx);
-                        const int j = 16 * grp + idx;
-                        if ((lane & 1) == 0 && j < rt) acc4[quarter * MAX_R1 + 1 + net.soff[l] + j] += cs;
+                        const float cs = treduce<RW>(cd, lane, idx);
+                        const int j = RW * grp + idx;
+                        if ((lane & (32 / RW - 1)) == 0 && j < rt) acc4[quarter * MAX_R1 + 1 + net.soff[l] + j] += cs;
                         if (l == 0 && grp == 0) {
                             for (int jj = 0; jj < rt && jj < 2; ++jj) {
                                 const float v0 = wsum(dv0[jj]), v1 = wsum(dv1[jj]);
