@@ -52,7 +52,7 @@ constexpr int TM_P1 = 0, TM_ZH = 128, TM_ZL = 256, TM_Y = 384;
 // Phase-2 products of YACC consecutive chunks accumulate in TMEM before the
 // epilogue reads them into the FP32 running sum (the tensor-core accumulator
 // truncates: 1 chunk = 12 MMAs keeps it at ~3e-6 on c2, 2 chunks ~6e-6, the
-// full K = 256 reached 1.2e-4). Halves the TMEM reads of Y (64 B/clk/SM).
+// full K = 256 reached 1.2e-4). Halves the TMEM load round trips of Y.
 #ifndef TC_SPLITLD
 #define TC_SPLITLD 1
 #endif
