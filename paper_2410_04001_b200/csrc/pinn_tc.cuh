@@ -623,10 +623,19 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                 // transition end: T -> dL/ds_l partials, ST = s_l (.) T (smem hi / lo)
                 TC_MARK(8);
                 if (warp < NWE) {
-                    wait_mma2();
-                    TC_MARK(13);
                     const double* sl = sv + net.soff[l];
                     const int rtrue = net.r[l];
+                    // this thread's y_l (scratch, usually an L2 / HBM round trip): all loads issued
+                    // together and before the wait for the last phase-2 product
+                    float4 yv[NG];
+#pragma unroll
+                    for (int n = 0; n < NG; ++n) {
+                        const int j = half * NG + n;
+                        yv[n] = j < rtrue ? *reinterpret_cast<const float4*>(scr + net.yoff[l] + (p * rtrue + j) * 4)
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                    wait_mma2();
+                    TC_MARK(13);
                     float (&tt)[4][NG] = tsum;
                     add_y(tlane + TM_Y + half * NG, tt);
 #pragma unroll
@@ -636,8 +645,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                             float cd = 0.f, sj = 0.f;
                             if (j < rtrue) {
                                 sj = float(sl[j]);
-                                float y4[4];
-                                v2::ld4(scr + net.yoff[l] + (p * rtrue + j) * 4, y4);
+                                const float y4[4] = {yv[n].x, yv[n].y, yv[n].z, yv[n].w};
 #pragma unroll
                                 for (int c = 0; c < 4; ++c) cd = fmaf(tt[c][n], y4[c], cd);
                             }
