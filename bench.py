@@ -241,44 +241,66 @@ def solve_loops(pkg, local, with_reference):
     return out
 
 
-def meta_step(pkg, local, n_inst=4, per=1 << 20):
+def meta_step(pkg, local, rank=0, world=1, dist=None, n_inst=4, per=1 << 20):
     """BASELINE config 4's meta step (widths 2-512x8-1, ranks (2,64x7,1), hypernetwork
     3-64-64-451, sin): U, V, b and hypernetwork gradients through the tcgen05 meta kernel
-    (LRNR_OPT_META_PREC = 1: BF16 operands, FP32 accumulation), on a bounded sample of
-    n_inst of the 64 instances x 1,048,576 points; device time of the whole step (meta
-    kernel + reductions + hypernetwork VJP) with CUDA events, points resident."""
+    (LRNR_OPT_META_PREC = 1: BF16 operands, FP32 accumulation). Each rank owns n_inst whole
+    instances of the 64 (instances 4 rank .. 4 rank + 3, weak scaling) x 1,048,576 points;
+    one step = the rank's meta gradient + the sum over ranks of the 498,121-entry gradient
+    (NCCL all-reduce). Device time with CUDA events, max over ranks, points resident."""
     import torch
-    c = pkg.config4(n_inst=n_inst, pts_per_inst=per)
-    m, h = c["model"], c["hyper"]
+    m, _ = pkg.make_baseline_model(pkg.api.C4_WIDTHS, pkg.api.C4_RANKS, 2412, pkg.ACT_SIN)
+    h = pkg.make_hyper_params(pkg.api.C4_RANKS, 2, 64, 4005, pkg.api.C3_LO, pkg.api.C3_HI, 0.01, 0.5)
+    _, mus_all = pkg.sample_collocation(4006, max(64, n_inst * world), pkg.api.C3_LO, pkg.api.C3_HI, with_mu=True)
+    first = n_inst * rank
+    mus = np.ascontiguousarray(mus_all[first:first + n_inst])
+    pts = np.concatenate([pkg.sample_collocation(6000 + i, per) for i in range(first, first + n_inst)])
     fl = pkg.algorithmic_flops_per_point(m.widths, m.ranks, meta=True)
     ctx = pkg.GpuContext(local)
     ctx.set_option(pkg.OPT_META_PREC, 1)
     ctx.set_lrnr(m, pkg.F32)
     ctx.set_hyper(h)
-    ctx.set_points(c["pts"], n_inst=n_inst)
+    ctx.set_points(pts, n_inst=n_inst)
     stream = torch.cuda.current_stream(local)
     ctx.set_stream(stream.cuda_stream)
-    ctx.meta_loss_grad(c["mus"], m.params.size)
+
+    def step():
+        r = ctx.meta_loss_grad(mus, m.params.size)
+        if dist is not None:
+            g = torch.from_numpy(np.concatenate([[r["value"]], r["grad"]])).cuda(local)
+            dist.all_reduce(g)
+            return g
+        return None
+
+    step()
     reps = 3
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist is not None:
+        dist.barrier()
     torch.cuda.synchronize(local)
     e0.record(stream)
     for _ in range(reps):
-        r = ctx.meta_loss_grad(c["mus"], m.params.size)
+        step()
     e1.record(stream)
     torch.cuda.synchronize(local)
     ms = e0.elapsed_time(e1) / reps
+    if dist is not None:
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
     ctx.close()
-    n = n_inst * per
+    n = n_inst * per * world
     tf = fl * n / (ms * 1e-3) / 1e12
-    peak = measured_peak("bf16_tflops_sustained", 1400.0)
-    return {"workload": f"c4 meta step: {n_inst} of the 64 mu instances x {per} points, 2-512x8-1, r (2,64x7,1), "
-                        "hypernet 3-64-64-451, sin; grads U, V, b, theta (498,121)",
+    peak = measured_peak("bf16_tflops_sustained", 1400.0) * world
+    return {"workload": f"c4 meta step: {n_inst} mu instances per GPU x {per} points (instances 0..{n_inst * world - 1} "
+                        "of the 64), 2-512x8-1, r (2,64x7,1), hypernet 3-64-64-451, sin; grads U, V, b, theta (498,121)",
             "kernel": "meta_tc2_kernel (tcgen05 kind::f16, BF16 operands, FP32 accumulate)",
+            "n_gpus": world, "scaling": "weak", "collective": "NCCL all-reduce of [loss, gradient] (498,122 doubles)"
+            if world > 1 else None,
             "ms_per_step": ms, "point_evals_per_s": n / ms * 1e3, "flop_per_point": fl, "tflops": tf,
             "tensor_roofline": {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
-                                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS bf16, 4 s)"},
-            "full_step_64_instances_ms_extrapolated": ms * 64 / n_inst, "loss": r["value"]}
+                                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS bf16, 4 s) x GPUs"},
+            "full_step_64_instances_ms_extrapolated": ms * 64 / (n_inst * world)}
 
 
 # ---------------------------------------------------------------------------
@@ -480,9 +502,9 @@ def run_ours(args):
             solves = {"error": str(e)}
 
     meta = None
-    if rank == 0 and world == 1 and not args.no_solves:
+    if not args.no_solves and world <= 16:  # all ranks: instances sharded, gradient all-reduced
         try:
-            meta = meta_step(pkg, local)
+            meta = meta_step(pkg, local, rank, world, dist)
         except Exception as e:  # reported, never fatal
             meta = {"error": str(e)}
 

@@ -4,7 +4,8 @@ Each rank computes its shard's [loss, dL/ds] rows (points sharded for config 2,
 whole instances for config 3) with the FP64 oracle standing in for the device
 sweep, then the rows are summed with the same all-reduce helper bench.py uses
 (NCCL on the GPU box).  The result must equal the single-process sweep over
-all points / instances."""
+all points / instances.  Config 4 (meta step): whole instances per rank, the
+packed [U, V, b, theta] gradient summed."""
 import os
 import socket
 import sys
@@ -21,6 +22,20 @@ def _free_port():
     p = s.getsockname()[1]
     s.close()
     return p
+
+
+def meta_grads(O, g, a, b):
+    """Sum over instances a..b-1 of 4 (24 golden c4 points each) of the meta gradient."""
+    nP = g["c4_params"].size
+    out = np.zeros(nP + g["c4_hparams"].size)
+    for i in range(a, b):
+        mu = g["c4_mus"][24 * i]
+        s_i = O.hyper_forward(g["c4_hw"], g["c4_hparams"], g["c3_lo"], g["c3_hi"], mu)
+        r = O.lrnr_grad(g["c4_widths"], g["c4_ranks"], g["c4_params"], s_i, mu, g["c4_pts"][24 * i:24 * (i + 1)],
+                        w=1.0 / 96, params_grad=True)
+        out[:nP] += r["grad_params"]
+        O.hyper_vjp(g["c4_hw"], g["c4_hparams"], g["c3_lo"], g["c3_hi"], mu, r["grad_s"], out=out[nP:])
+    return out
 
 
 def _worker(rank, world, port, q):
@@ -56,8 +71,12 @@ def _worker(rank, world, port, q):
         O.hyper_vjp(hw, H, lo3, hi3, mus[i], ri["grad_s"], out=ght)
     th = torch.tensor(ght)
     allreduce_sum_(th)
+    # config-4 style: meta gradient (U, V, b then theta, ParamPacker order), instances sharded
+    mg = meta_grads(O, g, *shard_instances(4, world, rank))
+    tm = torch.tensor(mg)
+    allreduce_sum_(tm)
     if rank == 0:
-        q.put((row.numpy(), th.numpy()))
+        q.put((row.numpy(), th.numpy(), tm.numpy()))
     dist.destroy_process_group()
 
 
@@ -72,7 +91,7 @@ def test_two_rank_gloo_sharding_equals_single_process(oracle, golden):
     procs = [ctx.Process(target=_worker, args=(k, 2, port, q)) for k in range(2)]
     for p in procs:
         p.start()
-    row, th = q.get(timeout=240)
+    row, th, tm = q.get(timeout=240)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -89,3 +108,5 @@ def test_two_rank_gloo_sharding_equals_single_process(oracle, golden):
                               w=1.0 / (len(mus) * len(sub)))
         oracle.hyper_vjp(g["c3_hw"], g["c3_hparams"], g["c3_lo"], g["c3_hi"], mus[i], ri["grad_s"], out=ref)
     np.testing.assert_allclose(th, ref, rtol=1e-11, atol=1e-14 * np.abs(ref).max())
+    ref4 = meta_grads(oracle, g, 0, 4)
+    np.testing.assert_allclose(tm, ref4, rtol=1e-11, atol=1e-14 * np.abs(ref4).max())
