@@ -10,6 +10,27 @@ import paper_2410_04001_b200 as pkg
 
 PEAK = 74.45
 out = {}
+# c0 / c1 (FP64, 4096 points): one gradient call each, device time over 200 calls
+# (launch-latency bound at this size; FP64 FMA peak = half the FP32 one)
+c = pkg.config1()
+ctx = pkg.GpuContext(0)
+ctx.set_lrnr(c["model"], pkg.F64)
+ctx.set_fast(c["fast"], pkg.F64)
+ctx.set_points(c["pts"])
+for key, model, fl in (("c0", pkg.MODEL_LRNR, pkg.algorithmic_flops_per_point(c["model"].widths, c["model"].ranks)),
+                       ("c1", pkg.MODEL_FAST, pkg.fast_flops_per_point(c["fast"].ranks, c["fast"].red_ranks))):
+    for _ in range(5):
+        ctx.loss_grad_s(model, c["s"], c["mu"])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(200):
+        r = ctx.loss_grad_s(model, c["s"], c["mu"])
+    dt = (time.perf_counter() - t0) / 200
+    n = len(c["pts"])
+    out[key] = {"us_per_call": dt * 1e6, "point_evals_per_s": n / dt, "tflops": fl * n / dt / 1e12,
+                "frac_fp64_fma": fl * n / dt / 1e12 / (PEAK / 2), "flop_per_point": fl, "points": n,
+                "loss": r["value"], "path": "lrnr_gpu_loss_grad_s (host buffers in / out), FP64"}
+ctx.close()
 # c3
 c = pkg.config3(n_inst=1024, pts_per_inst=16384)
 ctx = pkg.GpuContext(0)
