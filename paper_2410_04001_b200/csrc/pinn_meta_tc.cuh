@@ -98,29 +98,7 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int amaj, int bm
            (static_cast<uint32_t>(bmaj) << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
            (static_cast<uint32_t>(M >> 4) << 24);
 }
-// warp-collective MMA issue (elected lane), A and B descriptors with their own high words
-__device__ __forceinline__ void mma(uint32_t d, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo, uint32_t b_hi,
-                                    uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\t.reg .b64 da, db;\n\t"
-        "mov.b64 da, {%1, %2};\n\t"
-        "mov.b64 db, {%3, %4};\n\t"
-        "setp.ne.b32 p, %6, 0;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, p;\n\t}" ::"r"(d),
-        "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc)
-        : "memory");
-}
-__device__ __forceinline__ uint32_t elect_one() {
-    uint32_t pred;
-    asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(pred));
-    return pred;
-}
-// One MMA (single-thread form, used by the issuing lane) and the warp-collective
-// (elected-lane) form.
-#ifndef MTC_ELECT_ASM
-#define MTC_ELECT_ASM 1
-#endif
+// One MMA, issued by the single MMA thread.
 __device__ __forceinline__ void mma1(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -146,12 +124,6 @@ __device__ __forceinline__ void mma_lo(uint32_t d, uint32_t alo, uint32_t blo, u
 // (16-byte units) per MMA; the first MMA accumulates iff acc0 != 0.
 template <uint32_t HA, uint32_t HB, uint32_t AST, uint32_t BST>
 __device__ __forceinline__ void mma_x8(uint32_t d, uint32_t alo, uint32_t blo, uint32_t idesc, uint32_t acc0) {
-#define MTC_MMA8_STEP(I)                                                    \
-    "add.u32 al, %1, " #I "*%7;\n\t"                                        \
-    "add.u32 bl, %2, " #I "*%8;\n\t"                                        \
-    "mov.b64 da, {al, %5};\n\t"                                             \
-    "mov.b64 db, {bl, %6};\n\t"                                             \
-    "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %3, " #I "_P;\n\t"
     asm volatile(
         "{\n\t.reg .pred p0, pt;\n\t.reg .b32 al, bl;\n\t.reg .b64 da, db;\n\t"
         "setp.ne.b32 p0, %4, 0;\n\t"
@@ -175,40 +147,16 @@ __device__ __forceinline__ void mma_x8(uint32_t d, uint32_t alo, uint32_t blo, u
         "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %3, pt;\n\t}" ::"r"(d),
         "r"(alo), "r"(blo), "r"(idesc), "r"(acc0), "n"(HA), "n"(HB), "n"(AST), "n"(BST)
         : "memory");
-#undef MTC_MMA8_STEP
 }
 __device__ __forceinline__ void commit1(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(umma::smem_addr(bar))
                  : "memory");
-}
-__device__ __forceinline__ void mma64(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-#if MTC_ELECT_ASM
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc)
-        : "memory");
-#else
-    if (elect_one())
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-            "l"(a), "l"(b), "r"(idesc), "r"(acc)
-            : "memory");
-#endif
 }
 // timing knobs (dev aid; results are wrong when set): bit 0 skips the dU / dV
 // MMAs, bit 1 the partial-gradient reductions, bit 2 the activation math
 #ifndef MTC_SKIP
 #define MTC_SKIP 0
 #endif
-__device__ __forceinline__ void commit(uint64_t* bar) {
-    if (elect_one())
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                         umma::smem_addr(bar))
-                     : "memory");
-}
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
@@ -226,18 +174,6 @@ __device__ __forceinline__ void red4(float* p, float a, float b, float c, float 
 }
 __device__ __forceinline__ void red1(float* p, float a) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(a) : "memory");
-}
-#ifndef MTC_UWAIT
-#define MTC_UWAIT 0
-#endif
-__device__ __forceinline__ uint32_t try_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(umma::smem_addr(bar)), "r"(parity), "n"(UMMA_WAIT_HINT_NS)
-        : "memory");
-    return ok;
 }
 // named barrier over the 16 epilogue warps
 __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NWE * 32) : "memory"); }
@@ -358,14 +294,7 @@ meta_tc_kernel(const MetaNet net, const RunGeom g, const double* __restrict__ pt
     const int64_t total_chunks = total_tiles * net.sched_len;
 
     auto wait = [](uint64_t* bar, uint32_t parity) {
-#if MTC_UWAIT
-        // warp-uniform wait: the loop exit is __all_sync-voted, so code after it
-        // stays provably convergent (uniform datapath for the MMA warp)
-        while (!__all_sync(0xffffffffu, try_wait(bar, parity))) {
-        }
-#else
         umma::mbar_wait(bar, parity);
-#endif
         umma::fence_after();
     };
 
