@@ -577,15 +577,19 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                 for (int l = L - 2; l >= 0; --l) {
                     const int RL = net.rp[l], n = net.nc[l];
                     const int Mn = net.M[l + 1];
-                    // the transition end reads y_l (dL/ds) and y_{l-1} (SY rebuild) back from the
-                    // scratch: pull this thread's lines into L2 now, so those loads do not pay HBM latency
-                    if (RW * grp < RL)
-                        for (int h = 0; h < 2; ++h)
-                            prefetch_l2(scr + net.yoff[l] + static_cast<int64_t>(h * ROWS + row) * RL + RW * grp);
-                    if (l > 0 && RW * grp < net.rp[l - 1])
-                        for (int h = 0; h < 2; ++h)
-                            prefetch_l2(scr + net.yoff[l - 1] + static_cast<int64_t>(h * ROWS + row) * net.rp[l - 1] + RW * grp);
                     for (int ch = 0; ch < n; ++ch, ++qc) {
+                        // the transition end reads y_l (dL/ds) and y_{l-1} (SY rebuild) back from the
+                        // scratch: pull this thread's lines into L2 one chunk ahead (earlier, the
+                        // partial-gradient reduction stream evicts them again)
+                        if (ch == n - 1) {
+                            if (RW * grp < RL)
+                                for (int h = 0; h < 2; ++h)
+                                    prefetch_l2(scr + net.yoff[l] + static_cast<int64_t>(h * ROWS + row) * RL + RW * grp);
+                            if (l > 0 && RW * grp < net.rp[l - 1])
+                                for (int h = 0; h < 2; ++h)
+                                    prefetch_l2(scr + net.yoff[l - 1] +
+                                                static_cast<int64_t>(h * ROWS + row) * net.rp[l - 1] + RW * grp);
+                        }
                         for (int h = 0; h < 2; ++h, ++s) {
                             MT(4, wait(&p1full[s & 1], (s >> 1) & 1));
                             wait(&full[qc % NBUF], (qc / NBUF) & 1);
@@ -631,7 +635,6 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                             if (h == 0 && ch > 0) MT(6, flush(rc++, l, ch - 1));
                         }
                     }
-                    MT(6, flush(rc++, l, n - 1));
                     mark(13);
                     MT(7, wait(&tdone, tcount & 1));
                     ++tcount;
@@ -663,6 +666,9 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                         umma::fence_async_smem();
                         signal(&sready);
                     }
+                    // the last chunk's dU / dV after the next transition is released: its
+                    // reductions would otherwise queue ahead of the y_{l-1} loads above
+                    MT(6, flush(rc++, l, n - 1));
                     mark(14);
                     if (RW * grp < RL) {
                         float cd[RW];
