@@ -45,8 +45,18 @@ constexpr int RP = 32;    // max padded rank
 constexpr int NWE = TC_NWE;  // epilogue warps: lane quarter = warp % 4, neuron / rank group of NG = warp / 4
 // the MMA issuer (its issue blocks while the MMA queue drains, so a dedicated
 // warp keeps the epilogue warps free); warp 0 (also an epilogue warp) otherwise
-constexpr int ISSUER = TC_DEDICATED ? NWE : 0;
-constexpr int NT = 32 * (NWE + (TC_DEDICATED ? 1 : 0));
+// TC_SPLIT_ISSUE: MMA issue is latency-bound (~57 cycles per MMA from one warp),
+// so it is spread over warps that issue concurrently: 0 = one warp for both
+// phases; 1 = phase-1 and phase-2 MMAs from two warps; 2 = four warps, each
+// phase's 4 jet slots split between two (independent TMEM accumulators; measured
+// slower: 27.1 vs 23.8 ms on c2).
+#ifndef TC_SPLIT_ISSUE
+#define TC_SPLIT_ISSUE 1
+#endif
+constexpr int NISS = (TC_DEDICATED && TC_SPLIT_ISSUE == 2) ? 2 : 1;  // issuer warps per phase
+constexpr int ISSUER = TC_DEDICATED ? NWE : 0;                       // first phase-1 issuer
+constexpr int ISSUER2 = (TC_DEDICATED && TC_SPLIT_ISSUE) ? NWE + NISS : ISSUER;  // first phase-2 issuer
+constexpr int NT = 32 * (NWE + (TC_DEDICATED ? (TC_SPLIT_ISSUE ? 2 * NISS : 1) : 0));
 constexpr int NG = KC / (NWE / 4);  // neurons (epilogue) / ranks (sums) per thread
 constexpr int TM_P1 = 0, TM_ZH = 128, TM_ZL = 256, TM_Y = 384;
 // Phase-2 products of YACC consecutive chunks accumulate in TMEM before the
@@ -218,8 +228,8 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
     if (warp == 0) umma::tmem_alloc<512>(&tmem_base);
     if (tid == 0) {
         for (int i = 0; i < NBUF; ++i) umma::mbar_init(&wbar[i], 1);
-        umma::mbar_init(&mbar1, 1);
-        umma::mbar_init(&mbar2, 1);
+        umma::mbar_init(&mbar1, NISS);  // one commit per issuing warp
+        umma::mbar_init(&mbar2, NISS);
         umma::mbar_init(&p1free, NWE);
         umma::mbar_init(&zready, NWE);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -285,9 +295,13 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
     const uint32_t lb16 = umma::desc_lo(sm + OFF_B0, (16 / 8) * 128);   // factor tiles with 16 rows
     // phase 1 (warp 0, converged): P1_c = S_c B (3xTF32), S = SY / ST from smem,
     // B = factor tiles at float offset bo (hi) / bo + KC * rk (lo) of the ring slot
+    // the jet slots this warp issues (all 4, or 2 when each phase has two issuer warps)
+    const int cis = NISS == 1 ? 0 : ((warp - (warp >= ISSUER2 ? ISSUER2 : ISSUER)) & 1) * 2;
+    const int cie = NISS == 1 ? 4 : cis + 2;
     auto mma_p1 = [&](int bo, int rk) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
+            if (c < cis || c >= cie) continue;
             const uint32_t d = tbase + TM_P1 + c * KC;
             const uint32_t ah0 = lsy + ((2 * c) * SY_TILE >> 2), al0 = lsy + ((2 * c + 1) * SY_TILE >> 2);
             const uint32_t bh0 = lb32 + (bo >> 2), bl0 = lb32 + ((bo + KC * rk) >> 2);
@@ -309,6 +323,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
         const uint32_t sb = 2 * (rn / 8) * 32 >> 2;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
+            if (c < cis || c >= cie) continue;
             const uint32_t d = tbase + TM_Y + c * 32;
 #pragma unroll
             for (int s = 0; s < KC / 8; ++s) {
@@ -379,7 +394,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                 auto fwd_p2 = [&](int64_t qq, int ch) {
                     mma_p2(static_cast<int>(qq % NBUF) * BUF + 2 * KC * rk + 32, rnn, ch % YACC != 0);
                 };
-                if (warp == ISSUER) fwd_p1(q);
+                if (warp >= ISSUER && warp < ISSUER + NISS) fwd_p1(q);
                 // pipeline per chunk ch: [P1(ch) | P2(ch-1)] on the tensor core while the
                 // epilogue of ch computes the activation jet; Z / Y are touched only after
                 // P2(ch-1) completes.  P1(ch+1) is issued ahead of P2(ch).
@@ -445,13 +460,19 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                         }
                     }
                     TC_MARK(4);
-                    if (warp == ISSUER) {
+                    if (warp >= ISSUER && warp < ISSUER + NISS) {
                         TC_ISSUE_BEGIN();
                         await(&p1free, phf);  // every chunk (keeps the phase count)
                         if (ch + 1 < net.nc[l]) fwd_p1(q + 1);
+                        if (ISSUER2 == ISSUER) {
+                            await(&zready, phz);
+                            fwd_p2(q, ch);
+                        }
+                        if (lane == 0 && warp == ISSUER) TC_ISSUE_END();
+                    }
+                    if (ISSUER2 != ISSUER && warp >= ISSUER2 && warp < ISSUER2 + NISS) {
                         await(&zready, phz);
                         fwd_p2(q, ch);
-                        if (lane == 0) TC_ISSUE_END();
                     }
                     TC_MARK(5);
                 }
@@ -545,7 +566,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                 auto bwd_p2 = [&](int64_t qq, int ch) {
                     mma_p2(static_cast<int>(qq % NBUF) * BUF + 2 * KC * rkn, rnl, ch % YACC != 0);
                 };
-                if (warp == ISSUER) bwd_p1(q);
+                if (warp >= ISSUER && warp < ISSUER + NISS) bwd_p1(q);
                 for (int ch = 0; ch < net.nc[l]; ++ch, ++q) {
                     if (warp < NWE) {
                         // stored pre-activations of this chunk (in flight during the MMAs)
@@ -613,9 +634,15 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                         }
                     }
                     TC_MARK(12);
-                    if (warp == ISSUER) {
+                    if (warp >= ISSUER && warp < ISSUER + NISS) {
                         await(&p1free, phf);  // every chunk (keeps the phase count)
                         if (ch + 1 < net.nc[l]) bwd_p1(q + 1);
+                        if (ISSUER2 == ISSUER) {
+                            await(&zready, phz);
+                            bwd_p2(q, ch);
+                        }
+                    }
+                    if (ISSUER2 != ISSUER && warp >= ISSUER2 && warp < ISSUER2 + NISS) {
                         await(&zready, phz);
                         bwd_p2(q, ch);
                     }
