@@ -53,10 +53,12 @@ constexpr int NWE = TC_NWE;  // epilogue warps: lane quarter = warp % 4, neuron 
 #ifndef TC_SPLIT_ISSUE
 #define TC_SPLIT_ISSUE 1
 #endif
-constexpr int NISS = (TC_DEDICATED && TC_SPLIT_ISSUE == 2) ? 2 : 1;  // issuer warps per phase
-constexpr int ISSUER = TC_DEDICATED ? NWE : 0;                       // first phase-1 issuer
+// (3 = one phase-1 issuer, phase 2 split over two warps: 23.8 vs 23.5 ms, slower too)
+constexpr int NISS = (TC_DEDICATED && TC_SPLIT_ISSUE == 2) ? 2 : 1;   // phase-1 issuer warps
+constexpr int NISS2 = (TC_DEDICATED && TC_SPLIT_ISSUE >= 2) ? 2 : 1;  // phase-2 issuer warps
+constexpr int ISSUER = TC_DEDICATED ? NWE : 0;                        // first phase-1 issuer
 constexpr int ISSUER2 = (TC_DEDICATED && TC_SPLIT_ISSUE) ? NWE + NISS : ISSUER;  // first phase-2 issuer
-constexpr int NT = 32 * (NWE + (TC_DEDICATED ? (TC_SPLIT_ISSUE ? 2 * NISS : 1) : 0));
+constexpr int NT = 32 * (NWE + (TC_DEDICATED ? (TC_SPLIT_ISSUE ? NISS + NISS2 : 1) : 0));
 constexpr int NG = KC / (NWE / 4);  // neurons (epilogue) / ranks (sums) per thread
 constexpr int TM_P1 = 0, TM_ZH = 128, TM_ZL = 256, TM_Y = 384;
 // Phase-2 products of YACC consecutive chunks accumulate in TMEM before the
@@ -229,7 +231,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
     if (tid == 0) {
         for (int i = 0; i < NBUF; ++i) umma::mbar_init(&wbar[i], 1);
         umma::mbar_init(&mbar1, NISS);  // one commit per issuing warp
-        umma::mbar_init(&mbar2, NISS);
+        umma::mbar_init(&mbar2, NISS2);
         umma::mbar_init(&p1free, NWE);
         umma::mbar_init(&zready, NWE);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -296,8 +298,9 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
     // phase 1 (warp 0, converged): P1_c = S_c B (3xTF32), S = SY / ST from smem,
     // B = factor tiles at float offset bo (hi) / bo + KC * rk (lo) of the ring slot
     // the jet slots this warp issues (all 4, or 2 when each phase has two issuer warps)
-    const int cis = NISS == 1 ? 0 : ((warp - (warp >= ISSUER2 ? ISSUER2 : ISSUER)) & 1) * 2;
-    const int cie = NISS == 1 ? 4 : cis + 2;
+    const bool p2w = ISSUER2 != ISSUER && warp >= ISSUER2;
+    const int cis = (p2w ? NISS2 : NISS) == 1 ? 0 : ((warp - (p2w ? ISSUER2 : ISSUER)) & 1) * 2;
+    const int cie = (p2w ? NISS2 : NISS) == 1 ? 4 : cis + 2;
     auto mma_p1 = [&](int bo, int rk) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -470,7 +473,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                         }
                         if (lane == 0 && warp == ISSUER) TC_ISSUE_END();
                     }
-                    if (ISSUER2 != ISSUER && warp >= ISSUER2 && warp < ISSUER2 + NISS) {
+                    if (ISSUER2 != ISSUER && warp >= ISSUER2 && warp < ISSUER2 + NISS2) {
                         await(&zready, phz);
                         fwd_p2(q, ch);
                     }
@@ -642,7 +645,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                             bwd_p2(q, ch);
                         }
                     }
-                    if (ISSUER2 != ISSUER && warp >= ISSUER2 && warp < ISSUER2 + NISS) {
+                    if (ISSUER2 != ISSUER && warp >= ISSUER2 && warp < ISSUER2 + NISS2) {
                         await(&zready, phz);
                         bwd_p2(q, ch);
                     }
