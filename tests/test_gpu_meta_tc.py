@@ -180,3 +180,22 @@ def test_meta_tc_ragged_widths_and_ranks(bf16, oracle, widths, ranks):
     val, want = oracle_meta(oracle, c, n_inst, per, pkg.ACT_SIN)
     assert abs(got["value"] - val) <= TOL_BF16_LOSS * abs(val)
     assert normwise(got["grad"], want) <= TOL_BF16_NORM
+
+
+def test_meta_tc_nonfinite_layer_tag(bf16):
+    """A non-finite factor raises the reference's NonFiniteError with the FP32 path's layer tag."""
+    c = pkg.config4(n_inst=2, pts_per_inst=64)
+    m, h = c["model"], c["hyper"]
+    P = m.params.copy()
+    o = m.widths[1] * m.ranks[0] + m.widths[0] * m.ranks[0] + m.widths[1]
+    P[o] = np.inf  # U_1[0, 0]
+    bad = pkg.LrnrParams(m.widths, m.ranks, P, m.act)
+    bf16.set_lrnr(bad, pkg.F32)
+    bf16.set_hyper(h)
+    bf16.set_points(c["pts"], n_inst=2)
+    with pytest.raises(pkg.NonFiniteError) as e_bf16:
+        bf16.meta_loss_grad(c["mus"], m.params.size)
+    bf16.set_option(pkg.OPT_META_PREC, 0)
+    with pytest.raises(pkg.NonFiniteError) as e_fp32:
+        bf16.meta_loss_grad(c["mus"], m.params.size)
+    assert e_bf16.value.layer_tag == e_fp32.value.layer_tag
