@@ -60,6 +60,20 @@ constexpr int ISSUER = TC_DEDICATED ? NWE : 0;                        // first p
 constexpr int ISSUER2 = (TC_DEDICATED && TC_SPLIT_ISSUE) ? NWE + NISS : ISSUER;  // first phase-2 issuer
 constexpr int NT = 32 * (NWE + (TC_DEDICATED ? (TC_SPLIT_ISSUE ? NISS + NISS2 : 1) : 0));
 constexpr int NG = KC / (NWE / 4);  // neurons (epilogue) / ranks (sums) per thread
+// TC_LANE_ISSUE: the issuing warp's lane 0 issues its MMAs as a single thread
+// (0 = warp-collective, elect.sync inside every MMA: 23.55 ms on c2 vs 25.9 for 1)
+#ifndef TC_LANE_ISSUE
+#define TC_LANE_ISSUE 0
+#endif
+#if TC_LANE_ISSUE
+#define TC_MMA_SS umma::mma_ss_1
+#define TC_MMA_TS umma::mma_ts_1
+#define TC_COMMIT umma::mma_commit_1
+#else
+#define TC_MMA_SS umma::mma_ss_w
+#define TC_MMA_TS umma::mma_ts_w
+#define TC_COMMIT umma::mma_commit_w
+#endif
 constexpr int TM_P1 = 0, TM_ZH = 128, TM_ZL = 256, TM_Y = 384;
 // Phase-2 products of YACC consecutive chunks accumulate in TMEM before the
 // epilogue reads them into the FP32 running sum (the tensor-core accumulator
@@ -302,6 +316,9 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
     const int cis = (p2w ? NISS2 : NISS) == 1 ? 0 : ((warp - (p2w ? ISSUER2 : ISSUER)) & 1) * 2;
     const int cie = (p2w ? NISS2 : NISS) == 1 ? 4 : cis + 2;
     auto mma_p1 = [&](int bo, int rk) {
+#if TC_LANE_ISSUE
+        if (lane == 0) {
+#endif
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             if (c < cis || c >= cie) continue;
@@ -310,12 +327,16 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
             const uint32_t bh0 = lb32 + (bo >> 2), bl0 = lb32 + ((bo + KC * rk) >> 2);
             for (int s = 0; s < rk / 8; ++s) {
                 const uint32_t sa = s * (2 * (P / 8) * 32 >> 2), sb = s * (2 * (KC / 8) * 32 >> 2);
-                umma::mma_ss_w(d, ah0 + sa, bh0 + sb, dhi, id_p1, s > 0);
-                umma::mma_ss_w(d, ah0 + sa, bl0 + sb, dhi, id_p1, 1);
-                umma::mma_ss_w(d, al0 + sa, bh0 + sb, dhi, id_p1, 1);
+                TC_MMA_SS(d, ah0 + sa, bh0 + sb, dhi, id_p1, s > 0);
+                TC_MMA_SS(d, ah0 + sa, bl0 + sb, dhi, id_p1, 1);
+                TC_MMA_SS(d, al0 + sa, bh0 + sb, dhi, id_p1, 1);
             }
         }
-        umma::mma_commit_w(&mbar1);
+        TC_COMMIT(&mbar1);
+#if TC_LANE_ISSUE
+        }
+        __syncwarp();
+#endif
     };
     // phase 2 (warp 0, converged): Y_c = Z_c B (fresh accumulator, A from TMEM),
     // B = factor tiles (rows rn) at float offset bo (hi) / bo + rn * KC (lo)
@@ -324,6 +345,9 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
         const uint32_t lb = rn == 16 ? lb16 : lb32;
         const uint32_t bh0 = lb + (bo >> 2), bl0 = lb + ((bo + rn * KC) >> 2);
         const uint32_t sb = 2 * (rn / 8) * 32 >> 2;
+#if TC_LANE_ISSUE
+        if (lane == 0) {
+#endif
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             if (c < cis || c >= cie) continue;
@@ -331,12 +355,16 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
 #pragma unroll
             for (int s = 0; s < KC / 8; ++s) {
                 const uint32_t azh = tbase + TM_ZH + c * KC + s * 8, azl = tbase + TM_ZL + c * KC + s * 8;
-                umma::mma_ts_w(d, azh, bh0 + s * sb, dhi, id_p2, (s > 0 || acc0) ? 1u : 0u);
-                umma::mma_ts_w(d, azh, bl0 + s * sb, dhi, id_p2, 1);
-                umma::mma_ts_w(d, azl, bh0 + s * sb, dhi, id_p2, 1);
+                TC_MMA_TS(d, azh, bh0 + s * sb, dhi, id_p2, (s > 0 || acc0) ? 1u : 0u);
+                TC_MMA_TS(d, azh, bl0 + s * sb, dhi, id_p2, 1);
+                TC_MMA_TS(d, azl, bh0 + s * sb, dhi, id_p2, 1);
             }
         }
-        umma::mma_commit_w(&mbar2);
+        TC_COMMIT(&mbar2);
+#if TC_LANE_ISSUE
+        }
+        __syncwarp();
+#endif
     };
     auto wait_slot = [&](int64_t qq) {
         umma::mbar_wait(&wbar[qq % NBUF], static_cast<uint32_t>((qq / NBUF) & 1));
