@@ -119,12 +119,26 @@ constexpr int BUF = 4 * KC * RP + KC + 32;    // factor chunk (max): 4 canonical
 constexpr int NBUF = TC_NBUF;                 // factor-chunk ring (NBUF - 1 chunks in flight)
 constexpr int OFF_B0 = OFF_SY + 8 * SY_TILE;
 constexpr int OFF_RED = OFF_B0 + NBUF * BUF;  // [P][RP] + P (loss) + [16][RP] partials
-constexpr int OFF_ACC = OFF_RED + P * RP + P + 16 * RP;  // partials: up to 16 groups
+constexpr int RPS = RP + 1;                   // red[] point stride (odd: conflict-free column writes)
+constexpr int OFF_ACC = OFF_RED + P * RPS + P + 16 * RP;  // partials: up to 16 groups
 constexpr int SMEM_FLOATS = OFF_ACC + 1024;
 
 __device__ __forceinline__ float* sy_tile(float* sm, int c, int lo) { return sm + OFF_SY + (2 * c + lo) * SY_TILE; }
 
 // write an fp32 value split into the hi / lo canonical tiles of slot c at (row p, k j)
+// four consecutive k (j0 % 4 == 0) of row p as one 16-byte store per tile: a
+// quarter-warp's 8 rows then fill one 128-byte core matrix (no bank conflicts; the
+// scalar form hits each bank 4 times per warp)
+__device__ __forceinline__ void put_split4(float* sm, int c, int p, int j0, float v0, float v1, float v2, float v3) {
+    float h[4], l[4];
+    umma::split_tf32(v0, h[0], l[0]);
+    umma::split_tf32(v1, h[1], l[1]);
+    umma::split_tf32(v2, h[2], l[2]);
+    umma::split_tf32(v3, h[3], l[3]);
+    const int o = umma::kmaj_off(p, j0, P);
+    *reinterpret_cast<float4*>(sy_tile(sm, c, 0) + o) = make_float4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<float4*>(sy_tile(sm, c, 1) + o) = make_float4(l[0], l[1], l[2], l[3]);
+}
 __device__ __forceinline__ void put_split(float* sm, int c, int p, int j, float v) {
     float h, l;
     umma::split_tf32(v, h, l);
@@ -173,13 +187,13 @@ __device__ unsigned long long g_tc_timing[16];
 // P / NRG points in parallel (one thread per (group, rank)), then the partials.
 constexpr int NRG = NWE;
 __device__ __forceinline__ void reduce_points(float* red, float* acc, int off, int r, int tid) {
-    float* part = red + P * RP + P;
+    float* part = red + P * RPS + P;
     if (tid < NRG * RP) {
         const int j = tid % RP, g = tid / RP;
         float s = 0.f;
         if (j < r)
 #pragma unroll
-            for (int i = 0; i < P / NRG; ++i) s += red[((P / NRG) * g + i) * RP + j];
+            for (int i = 0; i < P / NRG; ++i) s += red[((P / NRG) * g + i) * RPS + j];
         part[g * RP + j] = s;
     }
     __syncthreads();
@@ -517,14 +531,22 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                     float (&y)[4][NG] = ysum;
                     add_y(tlane + TM_Y + half * NG, y);
 #pragma unroll
-                    for (int n = 0; n < NG; ++n) {
-                        const int j = half * NG + n;
-                        if (j < net.rk[l + 1]) {
-                            const float sj = j < rtrue ? float(sl[j]) : 0.f;
-                            if (j < rtrue)
-                                v2::st4(scr + net.yoff[l + 1] + (p * rtrue + j) * 4, y[0][n], y[1][n], y[2][n], y[3][n]);
+                    for (int n4 = 0; n4 < NG / 4; ++n4) {
+                        const int j0 = half * NG + 4 * n4;
+                        if (j0 < net.rk[l + 1]) {  // rk is a multiple of 8: a group of 4 is all in or all out
+                            float sj[4];
 #pragma unroll
-                            for (int c = 0; c < 4; ++c) put_split(sm, c, p, j, sj * y[c][n]);
+                            for (int i = 0; i < 4; ++i) {
+                                const int j = j0 + i, n = 4 * n4 + i;
+                                sj[i] = j < rtrue ? float(sl[j]) : 0.f;
+                                if (j < rtrue)
+                                    v2::st4(scr + net.yoff[l + 1] + (p * rtrue + j) * 4, y[0][n], y[1][n], y[2][n],
+                                            y[3][n]);
+                            }
+#pragma unroll
+                            for (int c = 0; c < 4; ++c)
+                                put_split4(sm, c, p, j0, sj[0] * y[c][4 * n4], sj[1] * y[c][4 * n4 + 1],
+                                           sj[2] * y[c][4 * n4 + 2], sj[3] * y[c][4 * n4 + 3]);
                         }
                     }
                 }
@@ -553,7 +575,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                     if (valid && !isfinite(term)) atomicMin(bad, static_cast<unsigned long long>(gp));
                     const float gN = valid ? 2.f * N * w : 0.f;
                     const float gu[4] = {gN * (-mu2 * (1.f - 2.f * u[0])), gN * mu0, gN, -gN * mu1};
-                    red[P * RP + p] = term;
+                    red[P * RPS + p] = term;
                     for (int j = 0; j < net.rk[L - 1]; ++j) {
                         const float uj = j < rL ? net.ulast[j] : 0.f;
                         const float sj = j < rL ? float(sL[j]) : 0.f;
@@ -564,7 +586,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
 #pragma unroll
                             for (int c = 0; c < 4; ++c) cd = fmaf(uj * gu[c], y4[c], cd);
                         }
-                        red[p * RP + j] = cd;
+                        red[p * RPS + j] = cd;
 #pragma unroll
                         for (int c = 0; c < 4; ++c) put_split(sm, c, p, j, sj * uj * gu[c]);
                     }
@@ -574,7 +596,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                 reduce_points(red, acc, net.soff[L - 1], rL, tid);
                 if (tid == NT - 1) {
                     float sacc = 0.f;
-                    for (int pp = 0; pp < P; ++pp) sacc += red[P * RP + pp];
+                    for (int pp = 0; pp < P; ++pp) sacc += red[P * RPS + pp];
                     acc[0] += sacc;
                 }
                 __syncthreads();
@@ -697,19 +719,27 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                     float (&tt)[4][NG] = tsum;
                     add_y(tlane + TM_Y + half * NG, tt);
 #pragma unroll
-                    for (int n = 0; n < NG; ++n) {
-                        const int j = half * NG + n;
-                        if (j < net.rk[l]) {
-                            float cd = 0.f, sj = 0.f;
-                            if (j < rtrue) {
-                                sj = float(sl[j]);
-                                const float y4[4] = {yv[n].x, yv[n].y, yv[n].z, yv[n].w};
+                    for (int n4 = 0; n4 < NG / 4; ++n4) {
+                        const int j0 = half * NG + 4 * n4;
+                        if (j0 < net.rk[l]) {  // rk is a multiple of 8
+                            float sj[4];
 #pragma unroll
-                                for (int c = 0; c < 4; ++c) cd = fmaf(tt[c][n], y4[c], cd);
+                            for (int i = 0; i < 4; ++i) {
+                                const int j = j0 + i, n = 4 * n4 + i;
+                                float cd = 0.f;
+                                sj[i] = 0.f;
+                                if (j < rtrue) {
+                                    sj[i] = float(sl[j]);
+                                    const float y4[4] = {yv[n].x, yv[n].y, yv[n].z, yv[n].w};
+#pragma unroll
+                                    for (int c = 0; c < 4; ++c) cd = fmaf(tt[c][n], y4[c], cd);
+                                }
+                                red[p * RPS + j] = cd;
                             }
-                            red[p * RP + j] = cd;
 #pragma unroll
-                            for (int c = 0; c < 4; ++c) put_split(sm, c, p, j, sj * tt[c][n]);
+                            for (int c = 0; c < 4; ++c)
+                                put_split4(sm, c, p, j0, sj[0] * tt[c][4 * n4], sj[1] * tt[c][4 * n4 + 1],
+                                           sj[2] * tt[c][4 * n4 + 2], sj[3] * tt[c][4 * n4 + 3]);
                         }
                     }
                 }
