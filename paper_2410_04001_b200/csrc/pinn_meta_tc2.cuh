@@ -54,8 +54,13 @@ constexpr int NWE = MTC2_NWE;     // epilogue warps (32 + 2 would exceed 1024 th
 constexpr int NGRP = NWE / 4;     // warps per TMEM lane quarter
 constexpr int CW = ROWS / NGRP;   // P1 columns (jet rows) per warp per half-step: 32 or 16
 constexpr int RW = 64 / NGRP;     // ranks per warp at the transition ends: 16 or 8
-constexpr int ISSUER = NWE, PRODUCER = NWE + 1;
-constexpr int NT = 32 * (NWE + 2);
+// MTC2_SPLIT: the pre-activation MMAs (P1 / P1r) and the rank-side + factor-gradient MMAs
+// (P2 / P2r, dU, dV) come from two issuer warps (issue is latency-bound)
+#ifndef MTC2_SPLIT
+#define MTC2_SPLIT 1
+#endif
+constexpr int ISSUER = NWE, PRODUCER = NWE + 1, ISSUER2 = MTC2_SPLIT ? NWE + 2 : NWE;
+constexpr int NT = 32 * (NWE + 2 + (MTC2_SPLIT ? 1 : 0));
 constexpr int NBUF = 2;
 constexpr int SYH = ROWS * RP * 2;              // one half tile of SY / ST: 16 KB
 constexpr int ZT = ROWS * KC * 2;               // Z or G tile: 32 KB
@@ -198,7 +203,8 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
         __syncwarp();
     }
     // =========================== MMA issuer (one thread) ===========================
-    else if (warp == ISSUER) {
+    else if (warp == ISSUER || warp == ISSUER2) {
+        const bool do1 = warp == ISSUER, do2 = warp == ISSUER2;  // P1 side / P2 side (both without the split)
         if (lane == 0) {
             const uint32_t sbase = umma::smem_addr(sm) >> 4;
             auto lo = [&](uint32_t off, uint32_t lbo) -> uint32_t { return sbase + (off >> 4) + ((lbo >> 4) << 16); };
@@ -211,12 +217,12 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                 // ---------------- forward ----------------
                 // step i of the transition (chunk i / 2, half i % 2): P1(i), then P2(i - 1)
                 for (int l = 0; l + 1 < L; ++l) {
-                    MT(16, wait(&sready, tcount & 1));
+                    if (do1) MT(16, wait(&sready, tcount & 1));
                     const int RL = net.rp[l], RN = net.rp[l + 1], n = net.nc[l];
                     const uint32_t id1 = idesc_bf16(128, ROWS, 0, 0), id2 = idesc_bf16(128, RN, 1, 1);
                     const uint32_t s0 = s, q0 = qc;
                     for (int i = 0; i <= 2 * n; ++i) {
-                        if (i < 2 * n) {
+                        if (do1 && i < 2 * n) {
                             const uint32_t si = s0 + i, qi = q0 + (i >> 1);
                             if ((i & 1) == 0) MT(17, wait(&full[qi % NBUF], (qi / NBUF) & 1));
                             drain(si >= 1 ? si - 1 : 0);  // P1 buffer si & 1 was read by step si - 2
@@ -228,7 +234,7 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                                 if (k < nk) mma_lo<HK, HK>(d, au + ((k * 4096) >> 4), by + ((k * 4096) >> 4), id1, k > 0);
                             commit1(&p1full[si & 1]);
                         }
-                        if (i > 0) {
+                        if (do2 && i > 0) {
                             const int j = i - 1;
                             const uint32_t sj = s0 + j, qj = q0 + (j >> 1);
                             MT(19, wait(&zgfull[sj & 1], (sj >> 1) & 1));
@@ -240,19 +246,19 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                     }
                     s += 2 * n;
                     qc += n;
-                    commit1(&tdone);
-                    drain(s);
+                    if (do2) commit1(&tdone);
+                    if (do1) drain(s);
                     ++tcount;
                 }
                 // ---------------- reverse ----------------
                 for (int l = L - 2; l >= 0; --l) {
-                    MT(16, wait(&sready, tcount & 1));
+                    if (do1) MT(16, wait(&sready, tcount & 1));
                     const int RL = net.rp[l], RN = net.rp[l + 1], n = net.nc[l];
                     const uint32_t id1 = idesc_bf16(128, ROWS, 0, 0), id2 = idesc_bf16(128, RL, 1, 1);
                     const uint32_t idu = idesc_bf16(128, RL, 0, 1), idv = idesc_bf16(128, RN, 0, 1);
                     const uint32_t s0 = s, q0 = qc, r0 = rc;
                     for (int i = 0; i <= 2 * n; ++i) {
-                        if (i < 2 * n) {
+                        if (do1 && i < 2 * n) {
                             const uint32_t si = s0 + i, qi = q0 + (i >> 1);
                             if ((i & 1) == 0) MT(17, wait(&full[qi % NBUF], (qi / NBUF) & 1));
                             drain(si);  // the single P1r region was read by step si - 1
@@ -269,7 +275,7 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                                     mma_lo<HK, HK>(tbase + TM_DZ, av + ((k * 4096) >> 4), bt + ((k * 4096) >> 4), id1, k > 0);
                             commit1(&p1full[si & 1]);
                         }
-                        if (i > 0) {
+                        if (do2 && i > 0) {
                             const int j = i - 1, hj = j & 1;
                             const uint32_t sj = s0 + j, qj = q0 + (j >> 1), rj = r0 + (j >> 1);
                             MT(19, wait(&zgfull[sj & 1], (sj >> 1) & 1));
@@ -292,8 +298,8 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                     s += 2 * n;
                     qc += n;
                     rc += n;
-                    commit1(&tdone);
-                    drain(s);
+                    if (do2) commit1(&tdone);
+                    if (do1) drain(s);
                     ++tcount;
                 }
             }
