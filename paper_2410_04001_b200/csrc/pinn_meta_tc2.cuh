@@ -57,10 +57,13 @@ constexpr int RW = 64 / NGRP;     // ranks per warp at the transition ends: 16 o
 // MTC2_SPLIT: the pre-activation MMAs (P1 / P1r) and the rank-side + factor-gradient MMAs
 // (P2 / P2r, dU, dV) come from two issuer warps (issue is latency-bound)
 #ifndef MTC2_SPLIT
-#define MTC2_SPLIT 1
+#define MTC2_SPLIT 2
 #endif
+// (2: a third warp issues dU / dV, so zgfree and tdone take one commit from each of two warps)
 constexpr int ISSUER = NWE, PRODUCER = NWE + 1, ISSUER2 = MTC2_SPLIT ? NWE + 2 : NWE;
-constexpr int NT = 32 * (NWE + 2 + (MTC2_SPLIT ? 1 : 0));
+constexpr int ISSUER3 = MTC2_SPLIT == 2 ? NWE + 3 : ISSUER2;
+constexpr int NCOM = MTC2_SPLIT == 2 ? 2 : 1;  // commits per zgfree / tdone phase
+constexpr int NT = 32 * (NWE + 2 + (MTC2_SPLIT ? 1 : 0) + (MTC2_SPLIT == 2 ? 1 : 0));
 constexpr int NBUF = 2;
 constexpr int SYH = ROWS * RP * 2;              // one half tile of SY / ST: 16 KB
 constexpr int ZT = ROWS * KC * 2;               // Z or G tile: 32 KB
@@ -152,11 +155,11 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
             umma::mbar_init(&p1full[i], 1);
             umma::mbar_init(&p1empty[i], NWE);
             umma::mbar_init(&zgfull[i], NWE);
-            umma::mbar_init(&zgfree[i], 1);
+            umma::mbar_init(&zgfree[i], NCOM);
         }
         umma::mbar_init(&dready, 1);
         umma::mbar_init(&dfree, NWE);
-        umma::mbar_init(&tdone, 1);
+        umma::mbar_init(&tdone, NCOM);
         umma::mbar_init(&sready, NWE);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -203,8 +206,9 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
         __syncwarp();
     }
     // =========================== MMA issuer (one thread) ===========================
-    else if (warp == ISSUER || warp == ISSUER2) {
-        const bool do1 = warp == ISSUER, do2 = warp == ISSUER2;  // P1 side / P2 side (both without the split)
+    else if (warp == ISSUER || warp == ISSUER2 || warp == ISSUER3) {
+        // P1 side / P2 side / dU-dV side (one warp may take several)
+        const bool do1 = warp == ISSUER, do2 = warp == ISSUER2, do3 = warp == ISSUER3;
         if (lane == 0) {
             const uint32_t sbase = umma::smem_addr(sm) >> 4;
             auto lo = [&](uint32_t off, uint32_t lbo) -> uint32_t { return sbase + (off >> 4) + ((lbo >> 4) << 16); };
@@ -243,10 +247,15 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                             commit1(&zgfree[sj & 1]);
                             if (j & 1) commit1(&slotfree[qj % NBUF]);
                         }
+                        if (NCOM == 2 && do3 && i > 0) {  // the dU-dV warp's (empty) share of zgfree
+                            const uint32_t sj = s0 + i - 1;
+                            wait(&zgfull[sj & 1], (sj >> 1) & 1);
+                            commit1(&zgfree[sj & 1]);
+                        }
                     }
                     s += 2 * n;
                     qc += n;
-                    if (do2) commit1(&tdone);
+                    if (do2 || (NCOM == 2 && do3)) commit1(&tdone);
                     if (do1) drain(s);
                     ++tcount;
                 }
@@ -275,30 +284,32 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                                     mma_lo<HK, HK>(tbase + TM_DZ, av + ((k * 4096) >> 4), bt + ((k * 4096) >> 4), id1, k > 0);
                             commit1(&p1full[si & 1]);
                         }
-                        if (do2 && i > 0) {
+                        if ((do2 || do3) && i > 0) {
                             const int j = i - 1, hj = j & 1;
                             const uint32_t sj = s0 + j, qj = q0 + (j >> 1), rj = r0 + (j >> 1);
                             MT(19, wait(&zgfull[sj & 1], (sj >> 1) & 1));
-                            // T += G U_c
-                            mma_x8<HM, HM, 16, 16>(tbase + TM_Y + hj * 64, lo(OFF_G, 128), lo(ringoff(qj), 128), id2,
-                                                   j >= 2 ? 1u : 0u);
-                            if (hj == 0 && rj >= 1) MT(20, wait(&dfree, (rj - 1) & 1));  // D free: previous chunk flushed
-                            // dU_c += G^T SY_l, dV_c += Z^T ST_{l+1} (accumulated over both halves)
-                            mma_x8<HK, HM, 256, 16>(tbase + TM_DU, lo(OFF_G, 2048), lo(OFF_SY + hj * SYH, 128), idu,
-                                                    hj ? 1u : 0u);
-                            mma_x8<HK, HM, 256, 16>(tbase + TM_DV, lo(OFF_Z, 2048), lo(OFF_ST + hj * SYH, 128), idv,
-                                                    hj ? 1u : 0u);
+                            if (do2)  // T += G U_c
+                                mma_x8<HM, HM, 16, 16>(tbase + TM_Y + hj * 64, lo(OFF_G, 128), lo(ringoff(qj), 128), id2,
+                                                       j >= 2 ? 1u : 0u);
+                            if (do3) {
+                                if (hj == 0 && rj >= 1) MT(20, wait(&dfree, (rj - 1) & 1));  // D free: previous chunk flushed
+                                // dU_c += G^T SY_l, dV_c += Z^T ST_{l+1} (accumulated over both halves)
+                                mma_x8<HK, HM, 256, 16>(tbase + TM_DU, lo(OFF_G, 2048), lo(OFF_SY + hj * SYH, 128), idu,
+                                                        hj ? 1u : 0u);
+                                mma_x8<HK, HM, 256, 16>(tbase + TM_DV, lo(OFF_Z, 2048), lo(OFF_ST + hj * SYH, 128), idv,
+                                                        hj ? 1u : 0u);
+                            }
                             commit1(&zgfree[sj & 1]);
                             if (hj) {
-                                commit1(&dready);
-                                commit1(&slotfree[qj % NBUF]);
+                                if (do3) commit1(&dready);
+                                if (do2) commit1(&slotfree[qj % NBUF]);
                             }
                         }
                     }
                     s += 2 * n;
                     qc += n;
                     rc += n;
-                    if (do2) commit1(&tdone);
+                    if (do2 || (NCOM == 2 && do3)) commit1(&tdone);
                     if (do1) drain(s);
                     ++tcount;
                 }
