@@ -60,6 +60,12 @@ constexpr int ISSUER = TC_DEDICATED ? NWE : 0;                        // first p
 constexpr int ISSUER2 = (TC_DEDICATED && TC_SPLIT_ISSUE) ? NWE + NISS : ISSUER;  // first phase-2 issuer
 constexpr int NT = 32 * (NWE + (TC_DEDICATED ? (TC_SPLIT_ISSUE ? NISS + NISS2 : 1) : 0));
 constexpr int NG = KC / (NWE / 4);  // neurons (epilogue) / ranks (sums) per thread
+// TC_STASH_HINT: streaming (evict-first) stores / loads for the pre-activation stash,
+// which is read back once, half a tile later (measured slower: 26.9 vs 23.3 ms -- part of
+// the stash is still hit in L2)
+#ifndef TC_STASH_HINT
+#define TC_STASH_HINT 0
+#endif
 // TC_LANE_ISSUE: the issuing warp's lane 0 issues its MMAs as a single thread
 // (0 = warp-collective, elect.sync inside every MMA: 23.55 ms on c2 vs 25.9 for 1)
 #ifndef TC_LANE_ISSUE
@@ -477,7 +483,11 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
 #endif
                                 const int k = half * NG + n;
                                 const float av = a[0][n] + bias[k], ax = a[1][n], at = a[2][n], aw = a[3][n];
+#if TC_STASH_HINT
+                                __stcs(reinterpret_cast<float4*>(Ast + aidx(k, p)), make_float4(av, ax, at, aw));
+#else
                                 v2::st4(Ast + aidx(k, p), av, ax, at, aw);
+#endif
                                 float sg, d1, d2, d3;
                                 act3f<ACT, FAST>(av, sg, d1, d2, d3);
                                 a[0][n] = sg;
@@ -628,7 +638,17 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
     #pragma unroll
                         for (int n = 0; n < NG; ++n) {
                             float a4[4];
+#if TC_STASH_HINT
+                            {
+                                const float4 q4 = __ldcs(reinterpret_cast<const float4*>(Ast + aidx(half * NG + n, p)));
+                                a4[0] = q4.x;
+                                a4[1] = q4.y;
+                                a4[2] = q4.z;
+                                a4[3] = q4.w;
+                            }
+#else
                             v2::ld4(Ast + aidx(half * NG + n, p), a4);
+#endif
     #pragma unroll
                             for (int c = 0; c < 4; ++c) a[c][n] = a4[c];
                         }
