@@ -94,16 +94,13 @@ void launch_fast(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const d
     g.n_units = static_cast<int64_t>(g.units_per_inst) * n_inst;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(grid_max, g.n_units)));
     ctx->ascratch.ensure(static_cast<size_t>(grid) * NW * net.wstride * sizeof(float) + 64);
-    ctx->part.ensure(static_cast<size_t>(g.n_units) * R1 * sizeof(float));
+    ensure_part<float>(ctx, n_inst, g.units_per_inst, R1);
     kern<<<grid, NT, smem, ctx->stream>>>(net, g, ctx->pts, s_dev, mu_dev, static_cast<float>(w),
                                           ctx->ascratch.as<float>(), ctx->part.as<float>(),
                                           ctx->bad.as<unsigned long long>(), ctx->term_spec, ctx->term_objective);
     CK(cudaGetLastError());
-    dim3 rg((R1 + 127) / 128, static_cast<unsigned>(n_inst));
-    reduce_units_kernel<float><<<rg, 128, 0, ctx->stream>>>(ctx->part.as<float>(), g.units_per_inst, R1, n_inst,
-                                                            dev_out);
-    CK(cudaGetLastError());
-    ctx->launches += 2;
+    reduce_units<float>(ctx, n_inst, g.units_per_inst, R1, dev_out);
+    ctx->launches += 1;
 }
 
 }  // namespace

@@ -224,6 +224,7 @@ struct lrnr_gpu_ctx {
     int64_t coeff_inst = 0;
     int coeff_rtotal = 0;
     // workspaces
+    lrnr_b200::detail::DevBuf unit_ctr;  // dynamic unit claims of the tensor-core sweep
     lrnr_b200::detail::DevBuf scratch, ascratch, part, out, bad, acts, G, hgrad, jets, meta_ws, gram_ws;
     int64_t out_rows = 0;
     int out_R1 = 0;
@@ -243,6 +244,46 @@ struct Plan {
     int grid;
     size_t smem;
 };
+
+// ---------------------------------------------------------------------------
+// per-unit partials: ctx->part holds [n_inst][units_per_inst][R1] values (one
+// writer per unit); reduce_units sums them in a fixed order into dev_out
+// [n_inst][R1] (double).  More than 2 UNIT_GROUP units per instance (e.g. the
+// single-tile units of the dynamically scheduled tensor-core sweep) go through
+// a group level first: one thread per column summing thousands of units
+// serially cost 0.6 ms at 4096 units.
+// ---------------------------------------------------------------------------
+constexpr int UNIT_GROUP = 64;
+
+template <class T>
+inline size_t part_bytes(int64_t n_inst, int units_per_inst, int R1) {
+    return (static_cast<size_t>(n_inst) * units_per_inst * R1 * sizeof(T) + 15) / 16 * 16;
+}
+
+template <class T>
+inline void ensure_part(lrnr_gpu_ctx* ctx, int64_t n_inst, int units_per_inst, int R1) {
+    const size_t groups = units_per_inst > 2 * UNIT_GROUP ? (units_per_inst + UNIT_GROUP - 1) / UNIT_GROUP : 0;
+    ctx->part.ensure(part_bytes<T>(n_inst, units_per_inst, R1) + groups * n_inst * R1 * sizeof(double));
+}
+
+template <class T>
+inline void reduce_units(lrnr_gpu_ctx* ctx, int64_t n_inst, int units_per_inst, int R1, double* dev_out) {
+    const dim3 rg((R1 + 127) / 128, static_cast<unsigned>(n_inst));
+    if (units_per_inst <= 2 * UNIT_GROUP) {
+        reduce_units_kernel<T><<<rg, 128, 0, ctx->stream>>>(ctx->part.as<T>(), units_per_inst, R1, n_inst, dev_out);
+        CK(cudaGetLastError());
+        ctx->launches += 1;
+        return;
+    }
+    const int ngroups = (units_per_inst + UNIT_GROUP - 1) / UNIT_GROUP;
+    double* grp = reinterpret_cast<double*>(ctx->part.as<char>() + part_bytes<T>(n_inst, units_per_inst, R1));
+    reduce_unit_groups_kernel<T><<<dim3(ngroups, static_cast<unsigned>(n_inst)), 128, 0, ctx->stream>>>(
+        ctx->part.as<T>(), units_per_inst, R1, UNIT_GROUP, grp);
+    CK(cudaGetLastError());
+    reduce_units_kernel<double><<<rg, 128, 0, ctx->stream>>>(grp, ngroups, R1, n_inst, dev_out);
+    CK(cudaGetLastError());
+    ctx->launches += 2;
+}
 
 template <class T, int TPP, int RMAX, int ACT, int MODE>
 Plan plan_for(lrnr_gpu_ctx* ctx, const Model& m, int64_t n_inst, int64_t n_per) {
@@ -277,16 +318,14 @@ void launch_pinn(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const d
     Plan p = plan_for<T, TPP, RMAX, ACT, MODE>(ctx, m, n_inst, n_per);
     const int R1 = 1 + m.rtotal;
     ctx->scratch.ensure(static_cast<size_t>(p.grid) * p.g.P * 4 * m.rtotal * sizeof(T));
-    ctx->part.ensure(static_cast<size_t>(p.g.n_units) * R1 * sizeof(T));
+    ensure_part<T>(ctx, n_inst, p.g.units_per_inst, R1);
     DevNet<T> net = dev_net<T>(m);
     pinn_kernel<T, TPP, RMAX, ACT, MODE><<<p.grid, kThreads, p.smem, ctx->stream>>>(
         net, p.g, ctx->pts, s_dev, mu_dev, static_cast<T>(w), ctx->scratch.as<T>(), ctx->part.as<T>(),
         jets_dev, ctx->bad.as<unsigned long long>(), ctx->term_spec, ctx->term_objective);
     CK(cudaGetLastError());
-    dim3 rg((R1 + 127) / 128, static_cast<unsigned>(n_inst));
-    reduce_units_kernel<T><<<rg, 128, 0, ctx->stream>>>(ctx->part.as<T>(), p.g.units_per_inst, R1, n_inst, dev_out);
-    CK(cudaGetLastError());
-    ctx->launches += 2;
+    reduce_units<T>(ctx, n_inst, p.g.units_per_inst, R1, dev_out);
+    ctx->launches += 1;
 }
 
 // ---- small-batch latency kernel (pinn_small.cuh): one CTA per point ----
@@ -306,17 +345,14 @@ void launch_small(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const 
     occ = std::max(occ, 1);
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g.n_total, int64_t(ctx->num_sms) * occ)));
     const int R1 = 1 + m.rtotal;
-    ctx->part.ensure(static_cast<size_t>(g.n_total) * R1 * sizeof(T));
+    ensure_part<T>(ctx, n_inst, static_cast<int>(n_per), R1);
     DevNet<T> net = dev_net<T>(m);
     kern<<<grid, small::NT, smem, ctx->stream>>>(net, g, ctx->pts, s_dev, mu_dev, static_cast<T>(w), ctx->part.as<T>(),
                                                  jets_dev, ctx->bad.as<unsigned long long>(), ctx->term_spec,
                                                  ctx->term_objective);
     CK(cudaGetLastError());
-    dim3 rg((R1 + 127) / 128, static_cast<unsigned>(n_inst));
-    reduce_units_kernel<T><<<rg, 128, 0, ctx->stream>>>(ctx->part.as<T>(), static_cast<int>(n_per), R1, n_inst,
-                                                        dev_out);
-    CK(cudaGetLastError());
-    ctx->launches += 2;
+    reduce_units<T>(ctx, n_inst, static_cast<int>(n_per), R1, dev_out);
+    ctx->launches += 1;
 }
 
 // ---- kernel v2 (tile GEMM) ----
@@ -349,7 +385,7 @@ void launch_v2(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
     const auto& v = META ? m.v2meta : m.v2;
     ctx->scratch.ensure(static_cast<size_t>(grid) * v.ystride * sizeof(T) + 64);
     ctx->ascratch.ensure(static_cast<size_t>(grid) * v.astride * sizeof(T) + 64);
-    ctx->part.ensure(static_cast<size_t>(g.n_units) * R1 * sizeof(T));
+    ensure_part<T>(ctx, n_inst, g.units_per_inst, R1);
     v2::NetV2<T> net{};
     net.L = m.L;
     for (int l = 0; l <= m.L; ++l) net.M[l] = m.M[l];
@@ -400,10 +436,8 @@ void launch_v2(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
         CK(cudaGetLastError());
         ctx->launches += 1;
     }
-    dim3 rg((R1 + 127) / 128, static_cast<unsigned>(n_inst));
-    reduce_units_kernel<T><<<rg, 128, 0, ctx->stream>>>(ctx->part.as<T>(), g.units_per_inst, R1, n_inst, dev_out);
-    CK(cudaGetLastError());
-    ctx->launches += 2;
+    reduce_units<T>(ctx, n_inst, g.units_per_inst, R1, dev_out);
+    ctx->launches += 1;
 }
 
 // Every C-ABI entry point runs its body through guarded(): C++ exceptions become

@@ -365,6 +365,8 @@ void launch_tc(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
     if (R1 > 1024) throw InvalidArg("tensor-core path supports r_total < 1024");
     const size_t smem = static_cast<size_t>(tc::SMEM_FLOATS) * sizeof(float);
     auto kern = tc::pinn_tc_kernel<ACT, FAST>;
+    ctx->unit_ctr.ensure(sizeof(unsigned long long));
+    CK(cudaMemsetAsync(ctx->unit_ctr.p, 0xff, sizeof(unsigned long long), ctx->stream));
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     RunGeom g{};
     g.P = tc::P;
@@ -372,7 +374,12 @@ void launch_tc(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
     g.tiles_per_inst = static_cast<int>((n_per + tc::P - 1) / tc::P);
     const int64_t total_tiles = static_cast<int64_t>(g.tiles_per_inst) * n_inst;
     const int64_t max_grid = ctx->num_sms;  // one CTA per SM: it owns all 512 TMEM columns
+#if TC_DYN_SCHED
+    // units are claimed dynamically: one tile each up to 64 per CTA
+    int64_t tpu = (total_tiles + max_grid * 64 - 1) / (max_grid * 64);
+#else
     int64_t tpu = (total_tiles + max_grid * 4 - 1) / (max_grid * 4);
+#endif
     tpu = std::max<int64_t>(1, std::min<int64_t>(tpu, g.tiles_per_inst));
     g.tiles_per_unit = static_cast<int>(tpu);
     g.units_per_inst = static_cast<int>((g.tiles_per_inst + tpu - 1) / tpu);
@@ -380,7 +387,7 @@ void launch_tc(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_grid, g.n_units)));
     ctx->scratch.ensure(static_cast<size_t>(grid) * v.ystride * sizeof(float) + 64);
     ctx->ascratch.ensure(static_cast<size_t>(grid) * v.astride * sizeof(float) + 64);
-    ctx->part.ensure(static_cast<size_t>(g.n_units) * R1 * sizeof(float));
+    ensure_part<float>(ctx, n_inst, g.units_per_inst, R1);
     tc::NetTC<> net{};
     net.L = m.L;
     for (int l = 0; l <= m.L; ++l) {
@@ -407,12 +414,11 @@ void launch_tc(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
     net.ulast = base + m.off_ulast;
     kern<<<grid, tc::NT, smem, ctx->stream>>>(net, g, ctx->pts, s_dev, mu_dev, static_cast<float>(w),
                                               ctx->scratch.as<float>(), ctx->ascratch.as<float>(),
-                                              ctx->part.as<float>(), ctx->bad.as<unsigned long long>());
+                                              ctx->part.as<float>(), ctx->bad.as<unsigned long long>(),
+                                              ctx->unit_ctr.as<unsigned long long>());
     CK(cudaGetLastError());
-    dim3 rg((R1 + 127) / 128, static_cast<unsigned>(n_inst));
-    reduce_units_kernel<float><<<rg, 128, 0, ctx->stream>>>(ctx->part.as<float>(), g.units_per_inst, R1, n_inst, dev_out);
-    CK(cudaGetLastError());
-    ctx->launches += 2;
+    reduce_units<float>(ctx, n_inst, g.units_per_inst, R1, dev_out);
+    ctx->launches += 1;
 }
 
 bool dispatch_tc(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,

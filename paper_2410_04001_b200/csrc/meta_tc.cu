@@ -195,7 +195,7 @@ void launch_meta_tc(lrnr_gpu_ctx* ctx, Model& m, const double* s_dev, const doub
     g.n_units = static_cast<int64_t>(g.units_per_inst) * n_inst;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_grid, g.n_units)));
     ctx->scratch.ensure(static_cast<size_t>(grid) * v.ystride * sizeof(float) + 64);
-    ctx->part.ensure(static_cast<size_t>(g.n_units) * R1 * sizeof(float));
+    ensure_part<float>(ctx, n_inst, g.units_per_inst, R1);
     m.mtc.wg.ensure(static_cast<size_t>(grid) * v.wg_stride * sizeof(float));
     m.mtc.sum.ensure(static_cast<size_t>(v.wg_stride) * sizeof(double));
     float* wg = m.mtc.wg.as<float>();
@@ -238,10 +238,8 @@ void launch_meta_tc(lrnr_gpu_ctx* ctx, Model& m, const double* s_dev, const doub
     mtc_permute_kernel<<<static_cast<unsigned>((v.n_params + 255) / 256), 256, 0, ctx->stream>>>(
         m.mtc.sum.as<double>(), v.dmap.as<int>(), v.n_params, v.qbase, v.QS, wg_out, ctx->accumulate_wg);
     CK(cudaGetLastError());
-    dim3 rg((R1 + 127) / 128, static_cast<unsigned>(n_inst));
-    reduce_units_kernel<float><<<rg, 128, 0, ctx->stream>>>(ctx->part.as<float>(), g.units_per_inst, R1, n_inst, dev_out);
-    CK(cudaGetLastError());
-    ctx->launches += 4;
+    reduce_units<float>(ctx, n_inst, g.units_per_inst, R1, dev_out);
+    ctx->launches += 3;
 }
 
 // ---------------------------------------------------------------------------
@@ -368,7 +366,7 @@ void launch_meta_tc2(lrnr_gpu_ctx* ctx, Model& m, const double* s_dev, const dou
     g.n_units = static_cast<int64_t>(g.units_per_inst) * n_inst;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_grid, g.n_units)));
     ctx->scratch.ensure(static_cast<size_t>(grid) * v.ystride * sizeof(float) + 64);
-    ctx->part.ensure(static_cast<size_t>(g.n_units) * R1 * sizeof(float));
+    ensure_part<float>(ctx, n_inst, g.units_per_inst, R1);
     m.mtc2.wg.ensure(static_cast<size_t>(grid) * v.wg_stride * sizeof(float));
     m.mtc2.sum.ensure(static_cast<size_t>(v.wg_stride) * sizeof(double));
     float* wg = m.mtc2.wg.as<float>();
@@ -411,10 +409,8 @@ void launch_meta_tc2(lrnr_gpu_ctx* ctx, Model& m, const double* s_dev, const dou
     mtc_permute_kernel<<<static_cast<unsigned>((v.n_params + 255) / 256), 256, 0, ctx->stream>>>(
         m.mtc2.sum.as<double>(), v.dmap.as<int>(), v.n_params, v.qbase, v.QS, wg_out, ctx->accumulate_wg, mtc2::NWE);
     CK(cudaGetLastError());
-    dim3 rg((R1 + 127) / 128, static_cast<unsigned>(n_inst));
-    reduce_units_kernel<float><<<rg, 128, 0, ctx->stream>>>(ctx->part.as<float>(), g.units_per_inst, R1, n_inst, dev_out);
-    CK(cudaGetLastError());
-    ctx->launches += 4;
+    reduce_units<float>(ctx, n_inst, g.units_per_inst, R1, dev_out);
+    ctx->launches += 3;
 }
 
 template void launch_meta_tc2<0>(lrnr_gpu_ctx*, Model&, const double*, const double*, double, double*, double*);

@@ -498,6 +498,23 @@ __global__ void reduce_units_kernel(const T* __restrict__ part, int units_per_in
     out[inst * R1 + k] = s;
 }
 
+// First level of a two-level fixed-order unit reduction (many units, e.g. the
+// dynamically claimed single-tile units of the tensor-core sweep): group g of
+// instance inst sums units [g G, (g + 1) G) into out2[inst][g][k] in double.
+template <typename T>
+__global__ void reduce_unit_groups_kernel(const T* __restrict__ part, int units_per_inst, int R1, int G,
+                                          double* __restrict__ out2) {
+    const int g = blockIdx.x, ngroups = gridDim.x;
+    const int64_t inst = blockIdx.y;
+    const int u0 = g * G, u1 = min(units_per_inst, u0 + G);
+    const T* p = part + (inst * units_per_inst + u0) * static_cast<int64_t>(R1);
+    for (int k = threadIdx.x; k < R1; k += blockDim.x) {
+        double s = 0.0;
+        for (int u = 0; u < u1 - u0; ++u) s += double(p[static_cast<int64_t>(u) * R1 + k]);
+        out2[(inst * ngroups + g) * R1 + k] = s;
+    }
+}
+
 // out[i] = sum_r rows[r][i] in double, rows in fixed order (per-CTA partials).
 template <typename T>
 __global__ void reduce_rows_kernel(const T* __restrict__ rows, int n_rows, int64_t stride, int64_t n,

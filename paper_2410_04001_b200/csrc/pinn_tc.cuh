@@ -60,6 +60,11 @@ constexpr int ISSUER = TC_DEDICATED ? NWE : 0;                        // first p
 constexpr int ISSUER2 = (TC_DEDICATED && TC_SPLIT_ISSUE) ? NWE + NISS : ISSUER;  // first phase-2 issuer
 constexpr int NT = 32 * (NWE + (TC_DEDICATED ? (TC_SPLIT_ISSUE ? NISS + NISS2 : 1) : 0));
 constexpr int NG = KC / (NWE / 4);  // neurons (epilogue) / ranks (sums) per thread
+// TC_DYN_SCHED: units after each CTA's first are claimed from a global counter (SMs run at
+// slightly different speeds: per-CTA times on a static split spread by up to 5 %)
+#ifndef TC_DYN_SCHED
+#define TC_DYN_SCHED 1
+#endif
 // TC_STASH_HINT: streaming (evict-first) stores / loads for the pre-activation stash,
 // which is read back once, half a tile later (measured slower: 26.9 vs 23.3 ms -- part of
 // the stash is still hit in L2)
@@ -242,7 +247,8 @@ template <int ACT, bool FAST>
 __global__ void __launch_bounds__(NT, 1)
 pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pts, const double* __restrict__ svec,
                const double* __restrict__ mus, const float w, float* __restrict__ scratch,
-               float* __restrict__ ascratch, float* __restrict__ part, unsigned long long* __restrict__ bad) {
+               float* __restrict__ ascratch, float* __restrict__ part, unsigned long long* __restrict__ bad,
+               unsigned long long* __restrict__ unit_ctr) {
     extern __shared__ __align__(128) float sm[];
     float* red = sm + OFF_RED;
     float* acc = sm + OFF_ACC;
@@ -250,6 +256,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
     __shared__ __align__(8) uint64_t mbar1, mbar2;
     __shared__ __align__(8) uint64_t p1free, zready;  // epilogue -> issuer (one arrive per epilogue warp)
     __shared__ uint32_t tmem_base;
+    __shared__ int64_t next_unit;
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -260,6 +267,10 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
     float* scr = scratch + static_cast<int64_t>(blockIdx.x) * net.ystride;
     float* ascr = ascratch + static_cast<int64_t>(blockIdx.x) * net.astride;
 
+#ifdef TC_CTA_TIMES
+    unsigned long long _t_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t_start));
+#endif
     for (int k = tid; k < R1; k += NT) acc[k] = 0.f;
     if (warp == 0) umma::tmem_alloc<512>(&tmem_base);
     if (tid == 0) {
@@ -290,6 +301,14 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
     };
 
     // ---- factor-chunk pipeline (TMA bulk copies) ----
+#if TC_DYN_SCHED
+    // every tile runs the same chunk schedule, so the ring is refilled without knowing the
+    // CTA's tile count; the NBUF - 1 copies in flight past the last chunk are drained at exit
+    const int64_t total_chunks = INT64_MAX;
+#ifdef TC_CTA_TIMES
+    int64_t total_tiles = 0;
+#endif
+#else
     int64_t total_tiles = 0;
     for (int64_t u = blockIdx.x; u < g.n_units; u += gridDim.x) {
         const int seg = static_cast<int>(u % g.units_per_inst);
@@ -297,6 +316,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
         total_tiles += min(g.tiles_per_inst, t_lo + g.tiles_per_unit) - t_lo;
     }
     const int64_t total_chunks = total_tiles * net.sched_len;
+#endif
     int64_t q = 0;
     auto issue = [&](int64_t qq) {
         if (qq < total_chunks) {
@@ -391,7 +411,17 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
         umma::fence_after();
     };
 
+#if TC_DYN_SCHED
+    // claims: the counter starts at all-ones (memset 0xff), so the first claim returns unit gridDim.x
+    unsigned long long claim = 0;
+    if (tid == 0) claim = atomicAdd(unit_ctr, 1ull) + 1ull + gridDim.x;
+    for (int64_t unit = blockIdx.x; unit < g.n_units;) {
+#else
     for (int64_t unit = blockIdx.x; unit < g.n_units; unit += gridDim.x) {
+#endif
+#if defined(TC_CTA_TIMES) && TC_DYN_SCHED
+        ++total_tiles;
+#endif
         const int64_t inst = unit / g.units_per_inst;
         const int seg = static_cast<int>(unit % g.units_per_inst);
         const int t_lo = seg * g.tiles_per_unit;
@@ -775,12 +805,34 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
             part[unit * R1 + k] = acc[k];
             acc[k] = 0.f;
         }
+#if TC_DYN_SCHED
+        if (tid == 0) {
+            next_unit = static_cast<int64_t>(claim);
+            if (claim < static_cast<unsigned long long>(g.n_units)) claim = atomicAdd(unit_ctr, 1ull) + 1ull + gridDim.x;
+        }
         __syncthreads();
+        unit = next_unit;
+#else
+        __syncthreads();
+#endif
     }
+#if TC_DYN_SCHED
+    if (tid == 0)
+        for (int64_t qq = q; qq < q + NBUF - 1; ++qq) wait_slot(qq);  // prefetches past the last chunk
+#endif
     TC_FLUSH();
     umma::fence_before();
     __syncthreads();
     if (warp == 0) umma::tmem_dealloc<512>(tbase);
+#ifdef TC_CTA_TIMES
+    if (tid == 0) {
+        unsigned long long _t_end;
+        unsigned _smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t_end));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(_smid));
+        printf("CTA %d %u %llu %llu %lld\n", blockIdx.x, _smid, _t_start, _t_end, (long long)total_tiles);
+    }
+#endif
 }
 
 }  // namespace tc
