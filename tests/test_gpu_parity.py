@@ -295,6 +295,31 @@ def test_c2_fp32_multi_instance_matches_oracle(gpu, oracle, opts, kernel):
     assert abs(got["value"] - total) <= TOL32_LOSS * abs(total)
 
 
+def test_c2_fp32_tc_dynamic_claims_deterministic(gpu, opts):
+    """The tensor-core sweep claims single-tile units from a global counter and reduces the
+    per-unit rows in two fixed-order levels (> 128 units per instance): 5 instances x 40000
+    points (1565 units on 148 CTAs) are bitwise reproducible across runs, whatever CTA ran
+    each unit, and agree per instance with the statically scheduled FMA tile kernel."""
+    c = pkg.config2(n_points=0, act=pkg.ACT_SIN, with_fast=False)
+    m = c["model"]
+    n_inst, n_per = 5, 40000
+    pts = pkg.sample_collocation(93, n_inst * n_per)
+    rng = np.random.default_rng(9)
+    S = np.stack([c["s"] * (1.0 + 0.1 * rng.standard_normal(c["s"].shape)) for _ in range(n_inst)])
+    MU = np.tile(c["mu"], (n_inst, 1))
+    gpu.set_lrnr(m, pkg.F32)
+    gpu.set_points(pts, n_inst=n_inst)
+    opts(pkg.KERNEL_TC)
+    runs = [gpu.loss_grad_s_multi(pkg.MODEL_LRNR, S, MU, w=1.0 / n_per) for _ in range(3)]
+    for r in runs[1:]:
+        assert r["value"] == runs[0]["value"] and np.array_equal(r["grad_s"], runs[0]["grad_s"])
+    opts(pkg.KERNEL_FMA_TILE)
+    ref = gpu.loss_grad_s_multi(pkg.MODEL_LRNR, S, MU, w=1.0 / n_per)
+    assert abs(runs[0]["value"] - ref["value"]) <= TOL32_LOSS * abs(ref["value"])
+    for i in range(n_inst):
+        assert normwise(runs[0]["grad_s"][i], ref["grad_s"][i]) <= TOL32_NORM
+
+
 def test_c2_fp32_tc_nonfinite_tag(gpu, golden, opts):
     """The tensor-core path reports the reference's NonFiniteError layer tag."""
     opts(pkg.KERNEL_TC)
