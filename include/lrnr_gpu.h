@@ -55,6 +55,7 @@ extern "C" {
 #define LRNR_ECUDA 3       /* CUDA runtime failure                                        */
 #define LRNR_ENOMEM 4      /* device allocation failure                                   */
 #define LRNR_ESTATE 5      /* call order error (e.g. no model / points set)               */
+#define LRNR_ENCCL 6       /* NCCL failure (communicator init / all-reduce)               */
 
 /* activation (ActivationKind, model.hpp:18; sin is this build's extension) */
 #define LRNR_ACT_TANH 0
@@ -317,6 +318,64 @@ int lrnr_gpu_download(lrnr_gpu_ctx* ctx, double* host_out, int64_t n_doubles);
 /* FP32 / FP64 FMA-chain microbenchmark: the roofline denominator (measurement aid; no reference
  * counterpart). */
 int lrnr_gpu_fma_peak(lrnr_gpu_ctx* ctx, int dtype, double* out_tflops);
+
+/* ---- multi-GPU: an NCCL communicator per context ----
+ * The reference's only parallelism is run_batch_gradient's thread pool with a
+ * fixed-order chunk combine (training.cpp:243-259). Here one process drives
+ * one GPU through one context, each rank holds a shard of the points (or of
+ * the PDE-parameter instances), and a context with a communicator attached
+ * sums its results over the ranks with ncclAllReduce on the context stream,
+ * after its own fixed-order reduction:
+ *   lrnr_gpu_run / _loss_grad_s / _loss_grad_s_multi / _terms_grad / _loss /
+ *   _loss_tune / _loss_fast / _loss_meta: value, comps and dL/ds rows summed
+ *     (points sharded; the instance list is the same on every rank);
+ *   lrnr_gpu_hyper_loss_grad: value and dL/dtheta summed, per-instance dL/ds
+ *     rows stay local (instances sharded);
+ *   lrnr_gpu_meta_loss_grad / _meta_terms_grad: value, comps and the packed
+ *     bases + hypernetwork gradient summed (the Gram penalty, which depends on
+ *     the bases only, is added once).
+ * Default weights (w <= 0) become 1/n over every rank's terms. Every rank must
+ * make the same sequence of calls (each may involve a collective). The solve
+ * loops, jets, values and l1_error stay per-rank.
+ * libnccl is loaded at run time (dlopen "libnccl.so.2"), so inside a process
+ * that already mapped NCCL (PyTorch) that library is shared. */
+/* ncclGetUniqueId into out_id (id_bytes >= 128). */
+int lrnr_gpu_comm_unique_id(void* out_id, size_t id_bytes);
+/* ncclCommInitRank(nranks, id, rank) on the context's device; the context owns it. */
+int lrnr_gpu_comm_init(lrnr_gpu_ctx* ctx, int nranks, int rank, const void* id, size_t id_bytes);
+/* Attach a caller-owned ncclComm_t (NULL detaches; the caller destroys it). */
+int lrnr_gpu_set_comm(lrnr_gpu_ctx* ctx, void* nccl_comm);
+/* Size and rank of the attached communicator (1, 0 without one). */
+int lrnr_gpu_comm_info(const lrnr_gpu_ctx* ctx, int* nranks, int* rank);
+/* In-place sum over the ranks of n device doubles on the context stream (e.g. a
+ * caller's own lrnr_gpu_run output buffers). */
+int lrnr_gpu_allreduce(lrnr_gpu_ctx* ctx, double* dev, int64_t n);
+
+/* ---- plain losses and values, forward only (training.cpp:76-189, model.cpp:260-292) ----
+ * out3 = LossBreakdown {total, residual, boundary} (training.hpp:82-86). Boundary
+ * terms need u only and run the value-only (1-slot) forward; interior terms the
+ * 4-slot jets. A non-finite total -> LRNR_ENONFINITE with layer tag -1, as the
+ * reference's NonFiniteError(-1).
+ * lrnr_gpu_values: lrnr_forward / fast_forward (u only) of `model` at n host
+ *   (x, t) pairs with coefficients s (r_total) -> out_u (n).
+ * lrnr_gpu_loss_tune: loss_tune (training.cpp:139-163): mean N^2 over the
+ *   resident points (single instance) + mean (u(x,0) - sin x)^2 over the
+ *   initial x + mean (u(0,t) - u(2pi,t))^2 over the periodic t of
+ *   lrnr_gpu_set_boundary. model = LRNR_MODEL_FAST evaluates the same terms on
+ *   the FastLRNR.
+ * lrnr_gpu_loss_fast: loss_fast (training.cpp:165-189): SUMS of |N| at the
+ *   interior points of the sampling set X (n_x (x, t) pairs, classified as
+ *   classify_point, reduction.cpp:27-31), |u(x,0) - sin x| at its initial and
+ *   |u(0,t) - u(2pi,t)| at its periodic points.
+ * lrnr_gpu_loss_meta: loss_meta (training.cpp:109-137): per-instance mu
+ *   (mus n_inst x 3) through the hypernetwork, s_i = hyper_forward(mu_i): mean
+ *   N^2 over the resident points (n_inst groups) + the means over the meta
+ *   boundary points of lrnr_gpu_set_meta_boundary. */
+int lrnr_gpu_values(lrnr_gpu_ctx* ctx, int model, const double* s, const double* xt, int64_t n, double* out_u);
+int lrnr_gpu_loss_tune(lrnr_gpu_ctx* ctx, int model, const double* s, const double* mu, double* out3);
+int lrnr_gpu_loss_fast(lrnr_gpu_ctx* ctx, int model, const double* s, const double* mu, const double* X, int64_t n_x,
+                       double* out3);
+int lrnr_gpu_loss_meta(lrnr_gpu_ctx* ctx, const double* mus, double* out3);
 
 /* ---- host-side setup (no GPU needed; reference reduction.cpp / model.cpp) ---- */
 /* BASELINE config generator: make_lrnr_params(orthonormal,

@@ -209,20 +209,83 @@ public:
         return out;
     }
 
-    // ---- forward only: loss_tune (training.cpp:139-163), jet_forward (model.cpp:357-405) ----
-    training::LossBreakdown loss_tune(const Coefficients& s, const PdeParams& mu, const pde::CollocationBatch& batch) {
+    // ---- forward only: loss_tune / loss_fast / loss_meta (training.cpp:109-189),
+    //      lrnr_forward / fast_forward (model.cpp:260-292), jet_forward (model.cpp:357-405) ----
+    training::LossBreakdown loss_tune(const Coefficients& s, const PdeParams& mu, const pde::CollocationBatch& batch,
+                                      bool fast = false) {
         set_points(batch.interior, 1);
         set_boundary(batch.initial_x, batch.periodic_t);
-        training::LossBreakdown lb;
-        try {
-            const training::BatchGradResult r = terms(LRNR_MODEL_LRNR, s, mu, LRNR_OBJ_SQUARED, 0.0, nullptr, 0.0);
-            lb.residual = r.comps[0];
-            lb.boundary = r.comps[1];
-        } catch (const NonFiniteError&) {
-            throw NonFiniteError(-1);  // loss_tune's own check (training.cpp:161)
+        const std::vector<double> sf = flatten(s);
+        const double m[3] = {mu.mu1, mu.mu2, mu.mu3};
+        double o[3];
+        check(lrnr_gpu_loss_tune(ctx_, fast ? LRNR_MODEL_FAST : LRNR_MODEL_LRNR, sf.data(), m, o));
+        return breakdown(o);
+    }
+    training::LossBreakdown loss_fast(const Coefficients& s, const PdeParams& mu,
+                                      const reduction::SamplingSetX& sampling) {
+        std::vector<double> xt;
+        for (const pde::Point& p : sampling.points) {
+            xt.push_back(p.x);
+            xt.push_back(p.t);
         }
-        lb.total = lb.residual + lb.boundary;
-        return lb;
+        const std::vector<double> sf = flatten(s);
+        const double m[3] = {mu.mu1, mu.mu2, mu.mu3};
+        double o[3];
+        check(lrnr_gpu_loss_fast(ctx_, LRNR_MODEL_FAST, sf.data(), m, xt.data(),
+                                 static_cast<int64_t>(sampling.points.size()), o));
+        return breakdown(o);
+    }
+    // loss_meta: every sample carries its own mu (sample_collocation(with_mu), pde.cpp:20-49),
+    // so each term kind runs as one instance per sample through the hypernetwork.
+    training::LossBreakdown loss_meta(const pde::CollocationBatch& batch) {
+        if (batch.interior_mu.size() != batch.interior.size() || batch.initial_mu.size() != batch.initial_x.size() ||
+            batch.periodic_mu.size() != batch.periodic_t.size())
+            throw std::invalid_argument("loss_meta: batch lacks per-sample mu");
+        auto mus_of = [](const std::vector<PdeParams>& v) {
+            std::vector<double> m;
+            for (const PdeParams& q : v) {
+                m.push_back(q.mu1);
+                m.push_back(q.mu2);
+                m.push_back(q.mu3);
+            }
+            return m;
+        };
+        double o[3] = {0.0, 0.0, 0.0}, part[3];
+        check(lrnr_gpu_set_meta_boundary(ctx_, 0, nullptr, 0, nullptr, 0));
+        if (!batch.interior.empty()) {
+            set_points(batch.interior, batch.interior.size());
+            const std::vector<double> m = mus_of(batch.interior_mu);
+            check(lrnr_gpu_loss_meta(ctx_, m.data(), part));
+            o[1] += part[1];
+        }
+        auto boundary_kind = [&](const std::vector<double>& v, const std::vector<PdeParams>& mus, bool initial) {
+            if (v.empty()) return;
+            const int64_t n = static_cast<int64_t>(v.size());
+            check(lrnr_gpu_set_points(ctx_, nullptr, n, 0));
+            check(lrnr_gpu_set_meta_boundary(ctx_, n, initial ? v.data() : nullptr, initial ? 1 : 0,
+                                             initial ? nullptr : v.data(), initial ? 0 : 1));
+            const std::vector<double> m = mus_of(mus);
+            check(lrnr_gpu_loss_meta(ctx_, m.data(), part));
+            o[2] += part[2];
+        };
+        boundary_kind(batch.initial_x, batch.initial_mu, true);
+        boundary_kind(batch.periodic_t, batch.periodic_mu, false);
+        check(lrnr_gpu_set_meta_boundary(ctx_, 0, nullptr, 0, nullptr, 0));
+        o[0] = o[1] + o[2];
+        if (!std::isfinite(o[0])) throw NonFiniteError(-1);
+        return breakdown(o);
+    }
+    // lrnr_forward / fast_forward: u at each point (value-only forward on the device)
+    std::vector<double> forward_values(const std::vector<pde::Point>& pts, const Coefficients& s, bool fast = false) {
+        std::vector<double> xt, u(pts.size());
+        for (const pde::Point& p : pts) {
+            xt.push_back(p.x);
+            xt.push_back(p.t);
+        }
+        const std::vector<double> sf = flatten(s);
+        check(lrnr_gpu_values(ctx_, fast ? LRNR_MODEL_FAST : LRNR_MODEL_LRNR, sf.data(), xt.data(),
+                              static_cast<int64_t>(pts.size()), u.data()));
+        return u;
     }
     // pde::l1_relative_error (pde.cpp:166-178) of the bound LRNR (or FastLRNR)
     // against a GridField, evaluated on the device.
@@ -331,6 +394,13 @@ private:
         if (rc == LRNR_ENONFINITE) throw NonFiniteError(lrnr_gpu_last_layer_tag(ctx_));
         if (rc == LRNR_EINVAL) throw std::invalid_argument(msg);
         throw std::runtime_error("lrnr_gpu: " + msg);
+    }
+    static training::LossBreakdown breakdown(const double* o) {
+        training::LossBreakdown lb;
+        lb.total = o[0];
+        lb.residual = o[1];
+        lb.boundary = o[2];
+        return lb;
     }
     static std::vector<double> flatten(const Coefficients& s) {
         std::vector<double> f;

@@ -486,6 +486,40 @@ class Reference:
                  "loss_tune")
         return out
 
+    def values(self, model, widths, ranks, P, red, F, s, pts):
+        """lrnr_forward (model 0) / fast_forward (model 1): u at the points."""
+        wv, rv = _i64(widths if widths is not None else [0]), _i64(ranks)
+        hv = _i64(red if red is not None else [0])
+        pts = _f64(pts).reshape(-1, 2)
+        out = np.zeros(pts.shape[0])
+        self._rc(self.lib.ref_values(C.c_int(model), C.c_int(len(rv)), _ptr(wv), _ptr(rv),
+                                     _ptr(_f64(P if P is not None else [0.0])), _ptr(hv),
+                                     _ptr(_f64(F if F is not None else [0.0])), _ptr(_f64(s)), _ptr(pts),
+                                     C.c_int64(pts.shape[0]), _ptr(out)), "values")
+        return out
+
+    def loss_fast(self, ranks, red, F, s, mu, X):
+        rv, hv = _i64(ranks), _i64(red)
+        X = _f64(X).reshape(-1, 2)
+        out = np.zeros(3)
+        self._rc(self.lib.ref_loss_fast(C.c_int(len(rv)), _ptr(rv), _ptr(hv), _ptr(_f64(F)), _ptr(_f64(s)),
+                                        _ptr(_f64(mu)), _ptr(X), C.c_int64(X.shape[0]), _ptr(out)), "loss_fast")
+        return out
+
+    def loss_meta(self, widths, ranks, P, hw, H, lo, hi, pts, mus, ic_x=(), ic_mu=(), per_t=(), per_mu=()):
+        wv, rv, hwv = _i64(widths), _i64(ranks), _i64(hw)
+        pts = _f64(pts).reshape(-1, 2)
+        mus = _f64(mus).reshape(-1)
+        icx, icm = _f64(list(ic_x) + [0.0]), _f64(np.append(_f64(ic_mu).reshape(-1), 0.0))
+        pt, pm = _f64(list(per_t) + [0.0]), _f64(np.append(_f64(per_mu).reshape(-1), 0.0))
+        out = np.zeros(3)
+        self._rc(self.lib.ref_loss_meta(C.c_int(len(rv)), _ptr(wv), _ptr(rv), _ptr(_f64(P)), C.c_int(len(hwv) - 1),
+                                        _ptr(hwv), _ptr(_f64(H)), _ptr(_f64(lo)), _ptr(_f64(hi)), _ptr(pts),
+                                        _ptr(mus), C.c_int64(pts.shape[0]), _ptr(icx), _ptr(icm),
+                                        C.c_int64(len(ic_x)), _ptr(pt), _ptr(pm), C.c_int64(len(per_t)), _ptr(out)),
+                 "loss_meta")
+        return out
+
     def hyper_forward(self, hw, H, split, lo, hi, mu):
         hwv, sp = _i64(hw), _i64(split)
         out = np.zeros(int(hwv[-1]))

@@ -933,4 +933,66 @@ int ref_meta_train(int L, const int64_t* widths, const int64_t* ranks, int hyper
     });
 }
 
+// ---- plain losses and values (training.cpp:109-189, model.cpp:260-292) ----
+
+// lrnr_forward (model = 0) / fast_forward (model = 1): u at n points.
+int ref_values(int model, int L, const int64_t* widths, const int64_t* ranks, const double* params,
+               const int64_t* red, const double* fparams, const double* s, const double* pts, int64_t n,
+               double* out_u) {
+    return guarded([&] {
+        if (model == 0) {
+            LrnrParams p = unpack_lrnr(L, widths, ranks, params);
+            Coefficients c = unpack_s(p, s);
+            for (int64_t i = 0; i < n; ++i) out_u[i] = lrnr_forward(pts[2 * i], pts[2 * i + 1], p, c)[0];
+        } else {
+            FastParams f = unpack_fast(L, ranks, red, 2, 1, fparams);
+            Coefficients c = unpack_s_ranks(f.ranks, s);
+            for (int64_t i = 0; i < n; ++i) out_u[i] = fast_forward(pts[2 * i], pts[2 * i + 1], f, c)[0];
+        }
+    });
+}
+
+// training::loss_fast over the sampling set X (n_x points).
+int ref_loss_fast(int L, const int64_t* ranks, const int64_t* red, const double* fparams, const double* s,
+                  const double* mu, const double* X, int64_t n_x, double* out3) {
+    return guarded([&] {
+        FastParams f = unpack_fast(L, ranks, red, 2, 1, fparams);
+        Coefficients c = unpack_s_ranks(f.ranks, s);
+        reduction::SamplingSetX sx;
+        for (int64_t i = 0; i < n_x; ++i) sx.points.push_back({X[2 * i], X[2 * i + 1]});
+        training::LossBreakdown lb = training::loss_fast(c, mu_of(mu), f, sx);
+        out3[0] = lb.total;
+        out3[1] = lb.residual;
+        out3[2] = lb.boundary;
+    });
+}
+
+// training::loss_meta: interior points with per-point mu, initial x / periodic t with per-point mu.
+int ref_loss_meta(int L, const int64_t* widths, const int64_t* ranks, const double* params, int K,
+                  const int64_t* hw, const double* hparams, const double* lo, const double* hi,
+                  const double* pts, const double* mus, int64_t n, const double* ic_x, const double* ic_mu,
+                  int64_t n_ic, const double* per_t, const double* per_mu, int64_t n_per, double* out3) {
+    return guarded([&] {
+        LrnrParams p = unpack_lrnr(L, widths, ranks, params);
+        HyperParams h = unpack_hyper(K, hw, hparams, L, ranks, lo, hi);
+        pde::CollocationBatch b;
+        for (int64_t i = 0; i < n; ++i) {
+            b.interior.push_back({pts[2 * i], pts[2 * i + 1]});
+            b.interior_mu.push_back(mu_of(mus + 3 * i));
+        }
+        for (int64_t i = 0; i < n_ic; ++i) {
+            b.initial_x.push_back(ic_x[i]);
+            b.initial_mu.push_back(mu_of(ic_mu + 3 * i));
+        }
+        for (int64_t i = 0; i < n_per; ++i) {
+            b.periodic_t.push_back(per_t[i]);
+            b.periodic_mu.push_back(mu_of(per_mu + 3 * i));
+        }
+        training::LossBreakdown lb = training::loss_meta(p, h, b);
+        out3[0] = lb.total;
+        out3[1] = lb.residual;
+        out3[2] = lb.boundary;
+    });
+}
+
 }  // extern "C"

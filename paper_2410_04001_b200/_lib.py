@@ -27,9 +27,11 @@ EXPORTS = (
     "lrnr_host_make_baseline_model", "lrnr_host_make_hyper_params", "lrnr_host_sample_collocation",
     "lrnr_host_build_fast", "lrnr_host_harvest_points", "lrnr_host_uniform_grid", "lrnr_host_eim_greedy", "lrnr_host_build_fastparams",
     "lrnr_gpu_eim_greedy", "lrnr_gpu_build_fast", "lrnr_gpu_harvest_snapshots",
+    "lrnr_gpu_comm_unique_id", "lrnr_gpu_comm_init", "lrnr_gpu_set_comm", "lrnr_gpu_comm_info", "lrnr_gpu_allreduce",
+    "lrnr_gpu_values", "lrnr_gpu_loss_tune", "lrnr_gpu_loss_fast", "lrnr_gpu_loss_meta",
 )
 
-LRNR_OK, LRNR_EINVAL, LRNR_ENONFINITE, LRNR_ECUDA, LRNR_ENOMEM, LRNR_ESTATE = range(6)
+LRNR_OK, LRNR_EINVAL, LRNR_ENONFINITE, LRNR_ECUDA, LRNR_ENOMEM, LRNR_ESTATE, LRNR_ENCCL = range(7)
 ACT_TANH, ACT_SIN = 0, 1
 F64, F32 = 0, 1
 MODEL_LRNR, MODEL_FAST = 0, 1
@@ -115,5 +117,14 @@ def load() -> C.CDLL:
                                                C.c_uint64, dp]
     lib.lrnr_gpu_build_fast.argtypes = [vp, ip, dp, dp, dp, ip, dp, i64, i64, i64, i64, C.c_double, C.c_uint64, i64,
                                         dp, dp, dp, dp]
+    lib.lrnr_gpu_comm_unique_id.argtypes = [vp, C.c_size_t]
+    lib.lrnr_gpu_comm_init.argtypes = [vp, ip, ip, vp, C.c_size_t]
+    lib.lrnr_gpu_set_comm.argtypes = [vp, vp]
+    lib.lrnr_gpu_comm_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    lib.lrnr_gpu_allreduce.argtypes = [vp, vp, i64]
+    lib.lrnr_gpu_values.argtypes = [vp, ip, dp, dp, i64, dp]
+    lib.lrnr_gpu_loss_tune.argtypes = [vp, ip, dp, dp, dp]
+    lib.lrnr_gpu_loss_fast.argtypes = [vp, ip, dp, dp, dp, i64, dp]
+    lib.lrnr_gpu_loss_meta.argtypes = [vp, dp, dp]
     _lib = lib
     return lib

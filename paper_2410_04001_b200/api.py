@@ -469,6 +469,60 @@ class GpuContext:
                  "loss")
         return v.value
 
+    # --- plain losses / values, forward only (training.cpp:76-189, model.cpp:260-292) ---
+    def values(self, model, s, xt):
+        """u only (lrnr_forward / fast_forward) at (n, 2) points, on the value-only kernel."""
+        xt = _f64(xt).reshape(-1, 2)
+        out = np.zeros(xt.shape[0])
+        self._rc(self.lib.lrnr_gpu_values(self.h, model, _p(_f64(s)), _p(xt), xt.shape[0], _p(out)), "values")
+        return out
+
+    def loss_tune(self, model, s, mu):
+        """loss_tune: LossBreakdown dict(total, residual, boundary) over the resident interior points and the
+        boundary points of set_boundary."""
+        o = np.zeros(3)
+        self._rc(self.lib.lrnr_gpu_loss_tune(self.h, model, _p(_f64(s)), _p(_f64(mu)), _p(o)), "loss_tune")
+        return dict(total=o[0], residual=o[1], boundary=o[2])
+
+    def loss_fast(self, model, s, mu, X):
+        """loss_fast: l1 sums over the classified sampling set X ((n, 2) points)."""
+        X = _f64(X).reshape(-1, 2)
+        o = np.zeros(3)
+        self._rc(self.lib.lrnr_gpu_loss_fast(self.h, model, _p(_f64(s)), _p(_f64(mu)), _p(X), X.shape[0], _p(o)),
+                 "loss_fast")
+        return dict(total=o[0], residual=o[1], boundary=o[2])
+
+    def loss_meta(self, mus):
+        """loss_meta: per-instance mu through the hypernetwork; resident points + meta boundary points."""
+        o = np.zeros(3)
+        self._rc(self.lib.lrnr_gpu_loss_meta(self.h, _p(_f64(mus)), _p(o)), "loss_meta")
+        return dict(total=o[0], residual=o[1], boundary=o[2])
+
+    # --- NCCL communicator (multi-GPU, one process per GPU) ---
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        rc = _lib.load().lrnr_gpu_comm_unique_id(C.cast(buf, C.c_void_p), 128)
+        if rc != 0:
+            raise LrnrGpuError(f"lrnr_gpu_comm_unique_id failed with code {rc} (libnccl.so.2 not loadable?)")
+        return buf.raw
+
+    def comm_init(self, nranks: int, rank: int, uid: bytes):
+        """ncclCommInitRank on this context's device; results are then summed over the ranks."""
+        buf = C.create_string_buffer(bytes(uid), 128)
+        self._rc(self.lib.lrnr_gpu_comm_init(self.h, nranks, rank, C.cast(buf, C.c_void_p), 128), "comm_init")
+
+    def set_comm(self, nccl_comm_ptr: int | None):
+        self._rc(self.lib.lrnr_gpu_set_comm(self.h, C.c_void_p(nccl_comm_ptr or 0)), "set_comm")
+
+    def comm_info(self):
+        n, r = C.c_int(0), C.c_int(0)
+        self._rc(self.lib.lrnr_gpu_comm_info(self.h, C.byref(n), C.byref(r)), "comm_info")
+        return n.value, r.value
+
+    def allreduce(self, dev_ptr: int, n: int):
+        self._rc(self.lib.lrnr_gpu_allreduce(self.h, C.c_void_p(dev_ptr), n), "allreduce")
+
     def set_option(self, opt: int, value: int):
         self._rc(self.lib.lrnr_gpu_set_option(self.h, opt, value), "set_option")
 

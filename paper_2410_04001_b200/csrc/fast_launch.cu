@@ -97,7 +97,7 @@ void launch_fast(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const d
     ensure_part<float>(ctx, n_inst, g.units_per_inst, R1);
     kern<<<grid, NT, smem, ctx->stream>>>(net, g, ctx->pts, s_dev, mu_dev, static_cast<float>(w),
                                           ctx->ascratch.as<float>(), ctx->part.as<float>(),
-                                          ctx->bad.as<unsigned long long>(), ctx->term_spec, ctx->term_objective);
+                                          bad_word(ctx, m), ctx->term_spec, ctx->term_objective);
     CK(cudaGetLastError());
     reduce_units<float>(ctx, n_inst, g.units_per_inst, R1, dev_out);
     ctx->launches += 1;

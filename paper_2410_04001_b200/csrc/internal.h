@@ -31,6 +31,9 @@ struct InvalidArg : std::runtime_error {
 struct StateError : std::runtime_error {
     explicit StateError(const std::string& m) : std::runtime_error(m) {}
 };
+struct NcclError : std::runtime_error {
+    explicit NcclError(const std::string& m) : std::runtime_error(m) {}
+};
 struct NonFinite : std::runtime_error {
     int tag;
     NonFinite(int t) : std::runtime_error("non-finite value in recorded computation, layer tag " + std::to_string(t)), tag(t) {}
@@ -235,10 +238,22 @@ struct lrnr_gpu_ctx {
     int opt_kernel = 0;       // LRNR_OPT_KERNEL: 0 auto, 1 streaming, 2 tensor core, 3 FMA tile, 4 small batch
     int opt_solve = 0;        // LRNR_OPT_SOLVE: 0 auto (persistent fast solver when eligible), 1 graph path
     int opt_meta_prec = 0;    // LRNR_OPT_META_PREC: 0 FP32 FMA tile kernel, 1 BF16 tensor-core operands
+    // NCCL communicator (comm.cu): results of the gradient calls are summed over its ranks
+    void* comm = nullptr;     // ncclComm_t
+    bool comm_owned = false;  // created by lrnr_gpu_comm_init (destroyed with the context)
+    int comm_nranks = 1, comm_rank = 0;
+    int64_t comm_gen = 0;     // bumped by set_points / set_boundary / set_comm (global-count cache key)
+    int64_t gcount_gen = -1;
+    std::vector<std::pair<int64_t, int64_t>> gcount;  // (local count, global count) for comm_gen
+    lrnr_b200::detail::DevBuf comm_ws;
 };
 
 namespace lrnr_b200 {
 namespace detail {
+// non-finite flag of a model slot (declared here for the launch templates below)
+unsigned long long* bad_word(lrnr_gpu_ctx* ctx, const Model& m);
+void reset_bad(lrnr_gpu_ctx* ctx, const Model& m);
+
 struct Plan {
     RunGeom g;
     int grid;
@@ -322,7 +337,7 @@ void launch_pinn(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const d
     DevNet<T> net = dev_net<T>(m);
     pinn_kernel<T, TPP, RMAX, ACT, MODE><<<p.grid, kThreads, p.smem, ctx->stream>>>(
         net, p.g, ctx->pts, s_dev, mu_dev, static_cast<T>(w), ctx->scratch.as<T>(), ctx->part.as<T>(),
-        jets_dev, ctx->bad.as<unsigned long long>(), ctx->term_spec, ctx->term_objective);
+        jets_dev, bad_word(ctx, m), ctx->term_spec, ctx->term_objective);
     CK(cudaGetLastError());
     reduce_units<T>(ctx, n_inst, p.g.units_per_inst, R1, dev_out);
     ctx->launches += 1;
@@ -348,7 +363,7 @@ void launch_small(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const 
     ensure_part<T>(ctx, n_inst, static_cast<int>(n_per), R1);
     DevNet<T> net = dev_net<T>(m);
     kern<<<grid, small::NT, smem, ctx->stream>>>(net, g, ctx->pts, s_dev, mu_dev, static_cast<T>(w), ctx->part.as<T>(),
-                                                 jets_dev, ctx->bad.as<unsigned long long>(), ctx->term_spec,
+                                                 jets_dev, bad_word(ctx, m), ctx->term_spec,
                                                  ctx->term_objective);
     CK(cudaGetLastError());
     reduce_units<T>(ctx, n_inst, static_cast<int>(n_per), R1, dev_out);
@@ -427,7 +442,7 @@ void launch_v2(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
     }
     kern<<<grid, NT, smem, ctx->stream>>>(net, g, ctx->pts, s_dev, mu_dev, static_cast<T>(w),
                                                ctx->scratch.as<T>(), ctx->part.as<T>(),
-                                               ctx->bad.as<unsigned long long>(), ctx->ascratch.as<T>(), wg,
+                                               bad_word(ctx, m), ctx->ascratch.as<T>(), wg,
                                                ctx->term_spec, ctx->term_objective);
     CK(cudaGetLastError());
     if (META) {
@@ -466,6 +481,9 @@ int guarded(lrnr_gpu_ctx* ctx, F&& f) {
     } catch (const CudaError& e) {
         ctx->err = e.what();
         return LRNR_ECUDA;
+    } catch (const NcclError& e) {
+        ctx->err = e.what();
+        return LRNR_ENCCL;
     } catch (const std::exception& e) {
         ctx->err = e.what();
         return LRNR_EINVAL;
@@ -520,7 +538,24 @@ __global__ void boundary_spec_multi_kernel(const double* __restrict__ jets, cons
 __global__ void add_rows_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
                                 double* __restrict__ c);
 void check_bad(lrnr_gpu_ctx* ctx, const Model& m);
-void reset_bad(lrnr_gpu_ctx* ctx);
+// non-finite flag of a model slot: the first bad point index (atomicMin), ULLONG_MAX when clean;
+// one word per model slot, reset when it is read (check_bad) or by a run that owns the step
+// ---- communicator (comm.cu) ----
+bool comm_active(const lrnr_gpu_ctx* ctx);
+// in-place sum over the communicator's ranks of n doubles (device), on ctx->stream; no-op without one
+void comm_allreduce(lrnr_gpu_ctx* ctx, double* dev, size_t n);
+// the same for host doubles (staged through ctx->comm_ws, synchronous)
+void comm_allreduce_host(lrnr_gpu_ctx* ctx, double* host, size_t n);
+// the sum over ranks of a local term count (cached per point-set generation); local without a communicator
+int64_t comm_global_count(lrnr_gpu_ctx* ctx, int64_t local);
+void comm_release(lrnr_gpu_ctx* ctx);
+// forward-only sweep of the streaming kernel over the current point set (lrnr_gpu.cu)
+template <int MODE>
+double* run_resident_stream(lrnr_gpu_ctx* ctx, const Model& m, double w, double* jets_dev);
+// value-only forward (pinn_value.cuh, losses.cu): u at n_total points, n_per consecutive points per
+// instance row of s_dev (n_inst x r_total); out_u on the device
+void launch_values(lrnr_gpu_ctx* ctx, const Model& m, const double* pts, int64_t n_per, int64_t n_total,
+                   const double* s_dev, double* out_u);
 const Model& need_model(lrnr_gpu_ctx* ctx, int model);
 void upload_coeffs_impl(lrnr_gpu_ctx* ctx, const double* s, const double* mu, int64_t n_inst, int rtotal);
 void download(lrnr_gpu_ctx* ctx, const double* dev, double* host, size_t n);

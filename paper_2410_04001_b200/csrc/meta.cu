@@ -85,8 +85,7 @@ void meta_step(lrnr_gpu_ctx* ctx, Model& m, double w, double* out_grad, double* 
     double* gout = ctx->hgrad.as<double>();
     ctx->out_rows = ctx->n_inst;
     ctx->out_R1 = R1;
-    ctx->bad.ensure(sizeof(unsigned long long));
-    reset_bad(ctx);
+    reset_bad(ctx, m);
     if (ctx->n_per == 0) {
         CK(cudaMemsetAsync(rows, 0, static_cast<size_t>(ctx->n_inst * R1) * sizeof(double), ctx->stream));
         CK(cudaMemsetAsync(gout, 0, static_cast<size_t>(n_lrnr) * sizeof(double), ctx->stream));
@@ -121,6 +120,9 @@ void meta_step(lrnr_gpu_ctx* ctx, Model& m, double w, double* out_grad, double* 
     double* hrows = rows;  // the per-instance dL/ds rows the hypernetwork backward consumes
     const int64_t nbp = ctx->mb_ic + 2 * ctx->mb_bc;
     const bool with_bnd = reg && reg->boundary && nbp > 0;
+    // 1/(instances x points) of each boundary kind over every rank (safe_inv, training.cpp:364-366)
+    const int64_t n_ic_all = reg && reg->boundary ? comm_global_count(ctx, ctx->mb_inst * ctx->mb_ic) : 0;
+    const int64_t n_bc_all = reg && reg->boundary ? comm_global_count(ctx, ctx->mb_inst * ctx->mb_bc) : 0;
     if (with_bnd) {
         require(ctx->mb_inst == ctx->n_inst, "meta boundary points were set for another instance count");
         const int64_t n_inst = ctx->n_inst, nb_all = n_inst * nbp;
@@ -134,8 +136,8 @@ void meta_step(lrnr_gpu_ctx* ctx, Model& m, double w, double* out_grad, double* 
         ctx->n_per = nbp;
         try {
             dispatch_small<1>(ctx, m, sd, md, 1.0, ctx->mb_rows.as<double>(), ctx->bnd_jets.as<double>());
-            const double wc = ctx->mb_ic ? 1.0 / static_cast<double>(n_inst * ctx->mb_ic) : 0.0;
-            const double wb = ctx->mb_bc ? 1.0 / static_cast<double>(n_inst * ctx->mb_bc) : 0.0;
+            const double wc = n_ic_all ? 1.0 / static_cast<double>(n_ic_all) : 0.0;
+            const double wb = n_bc_all ? 1.0 / static_cast<double>(n_bc_all) : 0.0;
             boundary_spec_multi_kernel<<<static_cast<unsigned>((nb_all + 127) / 128), 128, 0, ctx->stream>>>(
                 ctx->bnd_jets.as<double>(), ctx->mb_sinx.as<double>(), n_inst, ctx->mb_ic, ctx->mb_bc, wc, wb,
                 ctx->bnd_spec.as<TermSpec>());
@@ -194,10 +196,13 @@ void meta_step(lrnr_gpu_ctx* ctx, Model& m, double w, double* out_grad, double* 
                 const int rw = rows_uv[which];
                 const double* A = m.flat_dev.as<double>() + off;
                 gram_e_kernel<<<(r * r + 127) / 128, 128, 0, ctx->stream>>>(A, rw, r, E + eo);
-                gram_grad_kernel<<<static_cast<unsigned>((static_cast<int64_t>(rw) * r + 127) / 128), 128, 0,
-                                   ctx->stream>>>(A, rw, r, E + eo, 4.0 * reg->lambda_ortho, gout + off);
+                if (ctx->comm_rank == 0) {  // rank-independent term: added once before the all-reduce
+                    gram_grad_kernel<<<static_cast<unsigned>((static_cast<int64_t>(rw) * r + 127) / 128), 128, 0,
+                                       ctx->stream>>>(A, rw, r, E + eo, 4.0 * reg->lambda_ortho, gout + off);
+                    ++ctx->launches;
+                }
                 CK(cudaGetLastError());
-                ctx->launches += 2;
+                ++ctx->launches;
                 gram_shape.emplace_back(r, static_cast<int>(eo));
                 eo += static_cast<size_t>(r) * r;
                 off += static_cast<int64_t>(rw) * r;
@@ -207,24 +212,27 @@ void meta_step(lrnr_gpu_ctx* ctx, Model& m, double w, double* out_grad, double* 
         gram_e.resize(eo);
         download(ctx, E, gram_e.data(), eo);
     }
+    // instances (or points) are sharded over the ranks: the bases / hypernetwork gradient is summed
+    comm_allreduce(ctx, gout, static_cast<size_t>(n_lrnr + n_hyper));
     std::vector<double> h(static_cast<size_t>(ctx->n_inst * R1));
     download(ctx, rows, h.data(), h.size());
     check_bad(ctx, m);
-    double val = 0.0;
-    for (int64_t i = 0; i < ctx->n_inst; ++i) val += h[static_cast<size_t>(i * R1)];
-    *out_value = val;
+    double sums[3] = {0.0, 0.0, 0.0};  // interior, boundary, sparse
+    for (int64_t i = 0; i < ctx->n_inst; ++i) sums[0] += h[static_cast<size_t>(i * R1)];
     if (with_bnd) {
         download(ctx, ctx->mb_rows.as<double>(), h.data(), h.size());
-        double bv = 0.0;
-        for (int64_t i = 0; i < ctx->n_inst; ++i) bv += h[static_cast<size_t>(i * R1)];
-        reg->boundary_value = bv;
+        for (int64_t i = 0; i < ctx->n_inst; ++i) sums[1] += h[static_cast<size_t>(i * R1)];
     }
     if (c_sparse > 0.0) {
         std::vector<double> pen(static_cast<size_t>(ctx->n_inst));
         download(ctx, ctx->meta_ws.as<double>(), pen.data(), pen.size());
-        double sp = 0.0;
-        for (int64_t i = 0; i < ctx->n_inst; ++i) sp += c_sparse * pen[static_cast<size_t>(i)];
-        reg->sparse = sp;
+        for (int64_t i = 0; i < ctx->n_inst; ++i) sums[2] += c_sparse * pen[static_cast<size_t>(i)];
+    }
+    comm_allreduce_host(ctx, sums, 3);
+    *out_value = sums[0];
+    if (reg) {
+        reg->boundary_value = sums[1];
+        reg->sparse = sums[2];
     }
     if (!gram_shape.empty()) {
         double ro = 0.0;  // weighted_sum over (U_0, V_0, U_1, V_1, ...), each lambda * ||E||_F^2
@@ -253,7 +261,7 @@ int lrnr_gpu_meta_loss_grad(lrnr_gpu_ctx* ctx, const double* mus, double w, doub
                            ctx->stream));
         ctx->coeff_inst = n;
         hyper_forward_resident(ctx, m.rtotal);
-        const double wt = w > 0.0 ? w : 1.0 / static_cast<double>(std::max<int64_t>(1, n * ctx->n_per));
+        const double wt = w > 0.0 ? w : 1.0 / static_cast<double>(std::max<int64_t>(1, comm_global_count(ctx, n * ctx->n_per)));
         double value = 0.0;
         meta_step(ctx, m, wt, out_grad, &value);
         if (out_value) *out_value = value;
@@ -294,6 +302,7 @@ int lrnr_gpu_set_meta_boundary(lrnr_gpu_ctx* ctx, int64_t n_inst, const double* 
         ctx->mb_inst = n_inst;
         ctx->mb_ic = n_ic;
         ctx->mb_bc = n_bc;
+        ++ctx->comm_gen;
     });
 }
 
@@ -311,7 +320,7 @@ int lrnr_gpu_meta_terms_grad(lrnr_gpu_ctx* ctx, const double* mus, double w, dou
                            ctx->stream));
         ctx->coeff_inst = n;
         hyper_forward_resident(ctx, m.rtotal);
-        const double wt = w > 0.0 ? w : 1.0 / static_cast<double>(std::max<int64_t>(1, n * ctx->n_per));
+        const double wt = w > 0.0 ? w : 1.0 / static_cast<double>(std::max<int64_t>(1, comm_global_count(ctx, n * ctx->n_per)));
         MetaReg reg;
         reg.lambda_sparse = lambda_sparse;
         reg.gamma = gamma;

@@ -229,7 +229,7 @@ void launch_meta_tc(lrnr_gpu_ctx* ctx, Model& m, const double* s_dev, const doub
     net.wg_stride = v.wg_stride;
     kern<<<grid, mtc::NT, mtc::SMEM_BYTES, ctx->stream>>>(net, g, ctx->pts, s_dev, mu_dev, static_cast<float>(w),
                                                            ctx->scratch.as<float>(), ctx->part.as<float>(), wg,
-                                                           ctx->bad.as<unsigned long long>(), ctx->term_spec,
+                                                           bad_word(ctx, m), ctx->term_spec,
                                                            ctx->term_objective);
     CK(cudaGetLastError());
     reduce_rows_kernel<float><<<static_cast<unsigned>((v.wg_stride + 255) / 256), 256, 0, ctx->stream>>>(
@@ -400,7 +400,7 @@ void launch_meta_tc2(lrnr_gpu_ctx* ctx, Model& m, const double* s_dev, const dou
     net.wg_stride = v.wg_stride;
     kern<<<grid, mtc2::NT, mtc2::SMEM_BYTES, ctx->stream>>>(net, g, ctx->pts, s_dev, mu_dev, static_cast<float>(w),
                                                              ctx->scratch.as<float>(), ctx->part.as<float>(), wg,
-                                                             ctx->bad.as<unsigned long long>(), ctx->term_spec,
+                                                             bad_word(ctx, m), ctx->term_spec,
                                                              ctx->term_objective);
     CK(cudaGetLastError());
     reduce_rows_kernel<float><<<static_cast<unsigned>((v.wg_stride + 255) / 256), 256, 0, ctx->stream>>>(

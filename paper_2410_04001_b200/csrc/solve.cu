@@ -112,7 +112,7 @@ void solve_epoch(lrnr_gpu_ctx* ctx, const Model& m, const SolveRun& r) {
     double* rows_bnd = rows_int + R1;
     double* sd = ctx->s_dev.as<double>();
     const double* md = ctx->mu_dev.as<double>();
-    reset_bad(ctx);
+    reset_bad(ctx, m);
     if (r.n_int > 0) {
         PointSwap keep(ctx, r.int_pts, r.n_int);
         if (r.objective == LRNR_OBJ_SQUARED) {
@@ -138,7 +138,7 @@ void solve_epoch(lrnr_gpu_ctx* ctx, const Model& m, const SolveRun& r) {
         dispatch_pinn<0>(ctx, m, sd, md, 1.0, rows_bnd, nullptr);
     }
     solve_step_kernel<<<1, 256, 0, ctx->stream>>>(
-        rows_int, rows_bnd, ctx->bad.as<unsigned long long>(), m.rtotal, sd, ctx->solve_s0.as<double>(),
+        rows_int, rows_bnd, bad_word(ctx, m), m.rtotal, sd, ctx->solve_s0.as<double>(),
         r.lambda_local, ctx->solve_m.as<double>(), ctx->solve_v.as<double>(), ctx->solve_best.as<double>(),
         ctx->solve_state.as<SolveState>(), ctx->solve_bt.as<double>(), r.lr, r.fast,
         ctx->solve_losses.as<double>(), r.epochs);
@@ -160,7 +160,7 @@ void solve_setup(lrnr_gpu_ctx* ctx, const Model& m, const double* s_init, const 
     ctx->solve_losses.ensure(static_cast<size_t>(epochs) * sizeof(double));
     ctx->bnd_spec.ensure(static_cast<size_t>(nb) * sizeof(TermSpec) + 16);
     ctx->bnd_jets.ensure(static_cast<size_t>(4 * nb) * sizeof(double) + 16);
-    ctx->bad.ensure(sizeof(unsigned long long));
+    bad_word(ctx, m);  // allocated before any graph capture
     std::vector<double> bt(static_cast<size_t>(2 * epochs));
     for (int64_t t = 1; t <= epochs; ++t) {
         bt[2 * (t - 1)] = 1.0 - std::pow(0.9, static_cast<double>(t));

@@ -58,3 +58,13 @@ def floor_rel(got, want, floor=1e-3):
 def normwise(got, want):
     got, want = np.asarray(got, float), np.asarray(want, float)
     return float(np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-300))
+
+
+@pytest.fixture(scope="session")
+def reference():
+    """The unmodified reference compiled in place (oracle/_ref, built by oracle/Makefile in the build
+    container; the .so travels to the GPU box). Missing -> the test FAILS: it is the strongest pin."""
+    from oracle.oracle import Reference, reference_available
+
+    assert reference_available(), "oracle/_ref/liblrnr_ref.so missing: run __graft_entry__.build() with /root/reference"
+    return Reference()

@@ -251,6 +251,32 @@ int main() {
             efs_s = std::max(efs_s, std::fabs(gfs.coeffs.s[l][i] - rfs.coeffs.s[l][i]));
     std::printf("fast_solve loop (200 epochs): losses max rel err %.3e, best s max abs err %.3e\n", efs, efs_s);
 
+    // forward-only losses: loss_tune / loss_fast / loss_meta (training.cpp:109-189) and u only
+    eng.bind(p, LRNR_F64);
+    const training::LossBreakdown rlt = training::loss_tune(s, mu, p, fb), glt = eng.loss_tune(s, mu, fb);
+    const double elt = std::max(std::fabs(glt.total - rlt.total) / rlt.total,
+                                std::fabs(glt.boundary - rlt.boundary) / rlt.boundary);
+    eng.bind(f, LRNR_F64);
+    auto X7 = reduction::SamplingSetX::uniform_grid(7, 5);
+    const training::LossBreakdown rlf = training::loss_fast(s, mu, f, X7), glf = eng.loss_fast(s, mu, X7);
+    const double elf = std::max(std::fabs(glf.total - rlf.total) / rlf.total,
+                                std::fabs(glf.boundary - rlf.boundary) / rlf.boundary);
+    HyperParams hm = make_hyper_params(p.ranks, 2, 16, ParamDomain::d1(), rng, 0.01, 0.5);
+    pde::CollocationBatch mb = pde::sample_collocation(4011, 300, 40, 30, ParamDomain::d1(), true);
+    eng.bind(hm);
+    const training::LossBreakdown rlm = training::loss_meta(p, hm, mb), glm = eng.loss_meta(mb);
+    const double elm = std::max({std::fabs(glm.total - rlm.total) / rlm.total,
+                                 std::fabs(glm.residual - rlm.residual) / rlm.residual,
+                                 std::fabs(glm.boundary - rlm.boundary) / rlm.boundary});
+    std::vector<double> uv = eng.forward_values(fb.interior, s);
+    double euv = 0.0;
+    for (std::size_t i = 0; i < fb.interior.size(); ++i) {
+        const double r = lrnr_forward(fb.interior[i].x, fb.interior[i].t, p, s)[0];
+        euv = std::max(euv, std::fabs(uv[i] - r) / std::max(std::fabs(r), 1e-3));
+    }
+    std::printf("plain losses: loss_tune %.3e, loss_fast %.3e, loss_meta %.3e, lrnr_forward %.3e\n", elt, elf, elm,
+                euv);
+
     // NonFiniteError surfaces as the reference's exception type
     Coefficients bad = s;
     bad.s[1][0] = std::nan("");
@@ -263,7 +289,8 @@ int main() {
     std::printf("NonFiniteError mapped: %s\n", threw ? "yes" : "NO");
     const bool ok = ev <= 1e-12 && eg <= 1e-10 && evf <= 1e-12 && egf <= 1e-10 && evb <= 1e-12 && ecb <= 1e-12 &&
                     egb <= 1e-10 && evp <= 1e-12 && egp <= 1e-10 && sft && eft <= 1e-10 && sfs && efs <= 1e-10 &&
-                    efs_s <= 1e-10 && threw && eim_ok;
+                    efs_s <= 1e-10 && threw && eim_ok && elt <= 1e-12 && elf <= 1e-12 && elm <= 1e-12 &&
+                    euv <= 1e-12;
     std::printf("%s\n", ok ? "ADAPTER PARITY OK" : "ADAPTER PARITY FAILED");
     return ok ? 0 : 1;
 }

@@ -110,3 +110,90 @@ def test_two_rank_gloo_sharding_equals_single_process(oracle, golden):
     np.testing.assert_allclose(th, ref, rtol=1e-11, atol=1e-14 * np.abs(ref).max())
     ref4 = meta_grads(oracle, g, 0, 4)
     np.testing.assert_allclose(tm, ref4, rtol=1e-11, atol=1e-14 * np.abs(ref4).max())
+
+
+# ---------------------------------------------------------------------------
+# the product path: 2 ranks over gloo, each driving its own context on cuda:0
+# ---------------------------------------------------------------------------
+def _gpu_case():
+    import paper_2410_04001_b200 as pkg
+
+    c2 = pkg.config2(n_points=6000)
+    c3 = pkg.config3(n_inst=6, pts_per_inst=300)
+    c4 = pkg.config4(n_inst=4, pts_per_inst=96)
+    return pkg, c2, c3, c4
+
+
+def _gpu_rows(pkg, c2, c3, c4, rank, world):
+    """One rank's share through the C ABI: c2 points, c3 / c4 whole instances; global weights."""
+    from paper_2410_04001_b200.dist import shard_instances, shard_range
+
+    ctx = pkg.GpuContext(0)
+    try:
+        n = len(c2["pts"])
+        lo, hi = shard_range(n, world, rank)
+        ctx.set_lrnr(c2["model"], pkg.F32)
+        ctx.set_fast(c2["fast"], pkg.F32)
+        ctx.set_points(c2["pts"][lo:hi])
+        r = ctx.loss_grad_s(pkg.MODEL_LRNR, c2["s"], c2["mu"], w=1.0 / n)
+        rf = ctx.loss_grad_s(pkg.MODEL_FAST, c2["s"], c2["mu"], w=1.0 / n)
+        a, b = shard_instances(c3["n_inst"], world, rank)
+        per = len(c3["pts"]) // c3["n_inst"]
+        ctx.set_fast(c3["fast"], pkg.F32)
+        ctx.set_hyper(c3["hyper"])
+        ctx.set_points(c3["pts"][a * per:b * per], n_inst=b - a)
+        h = ctx.hyper_loss_grad(pkg.MODEL_FAST, c3["mus"][a:b], w=1.0 / len(c3["pts"]))
+        a4, b4 = shard_instances(c4["n_inst"], world, rank)
+        per4 = len(c4["pts"]) // c4["n_inst"]
+        ctx.set_option(pkg.OPT_META_PREC, 1)
+        ctx.set_lrnr(c4["model"], pkg.F32)
+        ctx.set_hyper(c4["hyper"])
+        ctx.set_points(c4["pts"][a4 * per4:b4 * per4], n_inst=b4 - a4)
+        g4 = ctx.meta_loss_grad(c4["mus"][a4:b4], c4["model"].params.size, w=1.0 / len(c4["pts"]))
+        return (np.concatenate([[r["value"]], r["grad_s"]]), np.concatenate([[rf["value"]], rf["grad_s"]]),
+                np.concatenate([[h["value"]], h["grad_theta"]]), np.concatenate([[g4["value"]], g4["grad"]]))
+    finally:
+        ctx.close()
+
+
+def _gpu_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    from paper_2410_04001_b200.dist import allreduce_sum_
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    pkg, c2, c3, c4 = _gpu_case()
+    out = [allreduce_sum_(torch.from_numpy(x.copy())).numpy() for x in _gpu_rows(pkg, c2, c3, c4, rank, world)]
+    if rank == 0:
+        q.put(out)
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+def test_two_rank_product_path_equals_single_context():
+    """Two processes on one GPU (their kernels never wait on each other), each running its shard
+    through the product C ABI; the rows summed over gloo equal one context over everything."""
+    pytest.importorskip("torch")
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(k, 2, port, q)) for k in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=540)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    pkg, c2, c3, c4 = _gpu_case()
+    want = _gpu_rows(pkg, c2, c3, c4, 0, 1)
+    for name, g, w, tol in zip(("c2 LRNR", "c2 FastLRNR", "c3 theta", "c4 meta"), got, want,
+                               (1e-6, 1e-6, 1e-6, 1e-5)):
+        err = np.linalg.norm(g - w) / np.linalg.norm(w)
+        assert err <= tol, (name, err)
