@@ -407,6 +407,12 @@ int lrnr_host_build_fast(int depth, const int64_t* widths, const int64_t* ranks,
                          int64_t r_hat, int64_t* out_red, int64_t* out_indices,
                          double* out_fparams, int* out_exhausted);
 
+/* hyper_forward (model.cpp:294-318) for n_mu parameter vectors mus (n_mu x 3) -> out_s
+ * (n_mu x hw[K]); bit-identical to the reference build (the mu-grid snapshot recipe of
+ * harvest_snapshots evaluates it, reduction.cpp:111-148). */
+int lrnr_host_hyper_forward(int n_layers, const int64_t* hw, const double* hparams, const double* box_lo,
+                            const double* box_hi, int64_t n_mu, const double* mus, double* out_s);
+
 /* SamplingSetX::uniform_grid (reduction.cpp:10-25): nx * nt (x, t) pairs, x fastest. */
 int lrnr_host_uniform_grid(int64_t nx, int64_t nt, double* out_xt);
 /* The columns harvest_snapshots evaluates (reduction.cpp:111-148): for each of

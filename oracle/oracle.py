@@ -600,6 +600,24 @@ class Reference:
         F = F[:fast_param_count(rv, red)]
         return dict(red_ranks=red, indices=idx.reshape(L - 1, r_hat), fparams=F, exhausted=exh)
 
+    def build_fast_hyper(self, widths, ranks, P, hw, H, lo, hi, mus, nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777,
+                         r_hat=32):
+        """harvest_snapshots through the hypernetwork over the mu grid `mus`, eim_greedy, build_fastparams."""
+        wv, rv, hwv = _i64(widths), _i64(ranks), _i64(hw)
+        mus = _f64(mus).reshape(-1, 3)
+        L = len(rv)
+        red = np.zeros(L - 1, np.int64)
+        idx = np.full((L - 1) * r_hat, -1, np.int64)
+        F = np.zeros(fast_param_count(rv, [r_hat] * (L - 1)))
+        exh = np.zeros(L - 1, np.int32)
+        self._rc(self.lib.ref_build_fast_hyper(
+            C.c_int(L), _ptr(wv), _ptr(rv), _ptr(_f64(P)), C.c_int(len(hwv) - 1), _ptr(hwv), _ptr(_f64(H)),
+            _ptr(_f64(lo)), _ptr(_f64(hi)), _ptr(mus), C.c_int64(mus.shape[0]), C.c_int64(nx), C.c_int64(nt),
+            C.c_int64(n_perturb), C.c_double(sigma), C.c_uint64(seed), C.c_int64(r_hat), _ptr(red), _ptr(idx), _ptr(F),
+            exh.ctypes.data_as(C.c_void_p)), "build_fast_hyper")
+        F = F[:fast_param_count(rv, red)]
+        return dict(red_ranks=red, indices=idx.reshape(L - 1, r_hat), fparams=F, exhausted=exh)
+
     def eim_greedy(self, S, r_hat):
         """reduction::eim_greedy itself on an M x n_cols snapshot matrix."""
         S = _f64(S)

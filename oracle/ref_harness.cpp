@@ -814,13 +814,40 @@ int ref_benchmark_step_time(const int64_t* widths, int64_t n_widths, int64_t rep
 
 // ---- FastLRNR construction (reduction.cpp:10-31,111-283) ----
 // Constant hypernetwork (zero W, bias = s) so hyper_forward(mu) == s.
+static void build_fast_from(const LrnrParams& p, const HyperParams& h, const std::vector<PdeParams>& grid,
+                            int64_t nx, int64_t nt, int64_t n_perturb, double sigma, uint64_t seed, int64_t r_hat,
+                            int64_t* out_red, int64_t* out_indices, double* out_fparams, int* out_exhausted) {
+    reduction::SamplingSetX X = reduction::SamplingSetX::uniform_grid(
+        static_cast<std::size_t>(nx), static_cast<std::size_t>(nt));
+    reduction::SnapshotSet snaps = reduction::harvest_snapshots(
+        p, h, X, static_cast<std::size_t>(n_perturb), sigma, grid, seed);
+    std::vector<reduction::EimBasis> bases;
+    for (std::size_t l = 0; l + 1 < p.depth(); ++l) {
+        bases.push_back(reduction::eim_greedy(snaps.layers[l], static_cast<std::size_t>(r_hat)));
+        out_exhausted[l] = bases.back().exhausted ? 1 : 0;
+        out_red[l] = static_cast<int64_t>(bases.back().dim());
+        for (std::size_t k = 0; k < bases.back().indices.size(); ++k)
+            out_indices[l * r_hat + static_cast<int64_t>(k)] = static_cast<int64_t>(bases.back().indices[k]);
+    }
+    FastParams f = reduction::build_fastparams(p, bases);
+    std::size_t o = 0;
+    for (double v : f.v_in.data) out_fparams[o++] = v;
+    for (std::size_t l = 0; l + 1 < p.depth(); ++l) {
+        for (double v : f.u_hat[l].data) out_fparams[o++] = v;
+        for (double v : f.b_hat[l].data) out_fparams[o++] = v;
+        for (double v : f.v_hat[l].data) out_fparams[o++] = v;
+    }
+    for (double v : f.u_out.data) out_fparams[o++] = v;
+    for (double v : f.b_out.data) out_fparams[o++] = v;
+}
+
 int ref_build_fast(int L, const int64_t* widths, const int64_t* ranks, const double* params,
                    const double* s, int64_t nx, int64_t nt, int64_t n_perturb, double sigma,
                    uint64_t seed, int64_t r_hat, const double* mu, int64_t* out_red,
                    int64_t* out_indices, double* out_fparams, int* out_exhausted) {
     return guarded([&] {
         LrnrParams p = unpack_lrnr(L, widths, ranks, params);
-        HyperParams h;
+        HyperParams h;  // constant hypernetwork: hyper_forward(mu) == s
         std::size_t r_total = 0;
         for (auto r : p.ranks) r_total += r;
         h.w.emplace_back(r_total, 3);
@@ -829,30 +856,25 @@ int ref_build_fast(int L, const int64_t* widths, const int64_t* ranks, const dou
         h.b.push_back(std::move(b));
         h.split = p.ranks;
         h.box = ParamDomain::d1();
-        reduction::SamplingSetX X = reduction::SamplingSetX::uniform_grid(
-            static_cast<std::size_t>(nx), static_cast<std::size_t>(nt));
-        std::vector<PdeParams> grid{mu_of(mu)};
-        reduction::SnapshotSet snaps = reduction::harvest_snapshots(
-            p, h, X, static_cast<std::size_t>(n_perturb), sigma, grid, seed);
-        std::vector<reduction::EimBasis> bases;
-        for (std::size_t l = 0; l + 1 < p.depth(); ++l) {
-            bases.push_back(reduction::eim_greedy(snaps.layers[l], static_cast<std::size_t>(r_hat)));
-            out_exhausted[l] = bases.back().exhausted ? 1 : 0;
-            out_red[l] = static_cast<int64_t>(bases.back().dim());
-            for (std::size_t k = 0; k < bases.back().indices.size(); ++k)
-                out_indices[l * r_hat + static_cast<int64_t>(k)] =
-                    static_cast<int64_t>(bases.back().indices[k]);
-        }
-        FastParams f = reduction::build_fastparams(p, bases);
-        std::size_t o = 0;
-        for (double v : f.v_in.data) out_fparams[o++] = v;
-        for (std::size_t l = 0; l + 1 < p.depth(); ++l) {
-            for (double v : f.u_hat[l].data) out_fparams[o++] = v;
-            for (double v : f.b_hat[l].data) out_fparams[o++] = v;
-            for (double v : f.v_hat[l].data) out_fparams[o++] = v;
-        }
-        for (double v : f.u_out.data) out_fparams[o++] = v;
-        for (double v : f.b_out.data) out_fparams[o++] = v;
+        build_fast_from(p, h, {mu_of(mu)}, nx, nt, n_perturb, sigma, seed, r_hat, out_red, out_indices, out_fparams,
+                        out_exhausted);
+    });
+}
+
+// The reduction recipe through a real hypernetwork over a mu grid (harvest_snapshots with
+// mu_grid, reduction.cpp:111-148; cli build_reduction).
+int ref_build_fast_hyper(int L, const int64_t* widths, const int64_t* ranks, const double* params, int K,
+                         const int64_t* hw, const double* hparams, const double* lo, const double* hi,
+                         const double* mus, int64_t n_mu, int64_t nx, int64_t nt, int64_t n_perturb, double sigma,
+                         uint64_t seed, int64_t r_hat, int64_t* out_red, int64_t* out_indices, double* out_fparams,
+                         int* out_exhausted) {
+    return guarded([&] {
+        LrnrParams p = unpack_lrnr(L, widths, ranks, params);
+        HyperParams h = unpack_hyper(K, hw, hparams, L, ranks, lo, hi);
+        std::vector<PdeParams> grid;
+        for (int64_t i = 0; i < n_mu; ++i) grid.push_back(mu_of(mus + 3 * i));
+        build_fast_from(p, h, grid, nx, nt, n_perturb, sigma, seed, r_hat, out_red, out_indices, out_fparams,
+                        out_exhausted);
     });
 }
 

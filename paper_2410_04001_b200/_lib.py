@@ -28,7 +28,7 @@ EXPORTS = (
     "lrnr_host_build_fast", "lrnr_host_harvest_points", "lrnr_host_uniform_grid", "lrnr_host_eim_greedy", "lrnr_host_build_fastparams",
     "lrnr_gpu_eim_greedy", "lrnr_gpu_build_fast", "lrnr_gpu_harvest_snapshots",
     "lrnr_gpu_comm_unique_id", "lrnr_gpu_comm_init", "lrnr_gpu_set_comm", "lrnr_gpu_comm_info", "lrnr_gpu_allreduce",
-    "lrnr_gpu_values", "lrnr_gpu_loss_tune", "lrnr_gpu_loss_fast", "lrnr_gpu_loss_meta",
+    "lrnr_gpu_values", "lrnr_gpu_loss_tune", "lrnr_gpu_loss_fast", "lrnr_gpu_loss_meta", "lrnr_host_hyper_forward",
 )
 
 LRNR_OK, LRNR_EINVAL, LRNR_ENONFINITE, LRNR_ECUDA, LRNR_ENOMEM, LRNR_ESTATE, LRNR_ENCCL = range(7)
@@ -117,6 +117,7 @@ def load() -> C.CDLL:
                                                C.c_uint64, dp]
     lib.lrnr_gpu_build_fast.argtypes = [vp, ip, dp, dp, dp, ip, dp, i64, i64, i64, i64, C.c_double, C.c_uint64, i64,
                                         dp, dp, dp, dp]
+    lib.lrnr_host_hyper_forward.argtypes = [ip, dp, dp, dp, dp, i64, dp, dp]
     lib.lrnr_gpu_comm_unique_id.argtypes = [vp, C.c_size_t]
     lib.lrnr_gpu_comm_init.argtypes = [vp, ip, ip, vp, C.c_size_t]
     lib.lrnr_gpu_set_comm.argtypes = [vp, vp]

@@ -136,6 +136,19 @@ def make_hyper_params(split, hidden_depth, hidden_width, seed, lo, hi, out_w_sca
     return HyperParams(hw, H, _f64(lo), _f64(hi))
 
 
+def hyper_forward(h: HyperParams, mus):
+    """hyper_forward (model.cpp:294-318) on the host for each row of mus (n, 3) -> (n, r_total); the same
+    roundings as the reference build (host C++, lrnr_host_hyper_forward)."""
+    mus = _f64(mus).reshape(-1, 3)
+    hw = _i64(h.hw)
+    out = np.zeros((mus.shape[0], int(hw[-1])))
+    rc = _lib.load().lrnr_host_hyper_forward(len(hw) - 1, _p(hw), _p(_f64(h.params)), _p(_f64(h.lo)), _p(_f64(h.hi)),
+                                             mus.shape[0], _p(mus), _p(out))
+    if rc != 0:
+        raise ValueError("hyper_forward: bad shapes")
+    return out
+
+
 def sample_collocation(seed, n_interior, lo=(0.0, 0.0, 0.0), hi=(0.0, 0.0, 0.0), with_mu=False):
     lib = _lib.load()
     xt = np.zeros(2 * n_interior + 2)
@@ -500,7 +513,16 @@ class GpuContext:
 
     # --- NCCL communicator (multi-GPU, one process per GPU) ---
     @staticmethod
+    def _map_nccl():
+        """The library dlopens libnccl.so.2 by soname: map torch's NCCL first so both share one."""
+        try:
+            import torch  # noqa: F401  (libtorch_cuda links the NCCL torch.distributed uses)
+        except ImportError:
+            pass
+
+    @staticmethod
     def comm_unique_id() -> bytes:
+        GpuContext._map_nccl()
         buf = C.create_string_buffer(128)
         rc = _lib.load().lrnr_gpu_comm_unique_id(C.cast(buf, C.c_void_p), 128)
         if rc != 0:
@@ -509,10 +531,12 @@ class GpuContext:
 
     def comm_init(self, nranks: int, rank: int, uid: bytes):
         """ncclCommInitRank on this context's device; results are then summed over the ranks."""
+        self._map_nccl()
         buf = C.create_string_buffer(bytes(uid), 128)
         self._rc(self.lib.lrnr_gpu_comm_init(self.h, nranks, rank, C.cast(buf, C.c_void_p), 128), "comm_init")
 
     def set_comm(self, nccl_comm_ptr: int | None):
+        self._map_nccl()
         self._rc(self.lib.lrnr_gpu_set_comm(self.h, C.c_void_p(nccl_comm_ptr or 0)), "set_comm")
 
     def comm_info(self):
@@ -570,20 +594,35 @@ def config1(n_points=4096):
     return c
 
 
+# The FastLRNR of the c2 / c3 base network: snapshots harvested over a mu grid (the 8 corners of the
+# c3 parameter box) through the c3 hypernetwork, as harvest_snapshots does with a mu_grid
+# (reduction.cpp:111-148; the cli's build_reduction).  At one fixed s the reference recipe exhausts
+# its 108 snapshot columns at the 1e-12 residual floor before the budget (r_hat 16-29 on c2); over
+# the grid's 8 x 108 columns the greedy EIM reaches the budget of 32.
+C2_FAST_MU_GRID = np.array([(a, b, c) for a in (C3_LO[0], C3_HI[0]) for b in (C3_LO[1], C3_HI[1])
+                            for c in (C3_LO[2], C3_HI[2])])
+
+
+def c3_hyper():
+    """c3 hypernetwork 3-64-64-163 (tanh, Xavier-uniform hidden layers) on the c2 base network."""
+    return make_hyper_params(C2_RANKS, 2, 64, 4003, C3_LO, C3_HI, 0.01, 0.5)
+
+
 def config2(n_points=1 << 20, act=ACT_SIN, with_fast=True):
-    """c2: LRNR 2-256x6-1, r (2,32x5,1), FP32, sin, mu=(20,0.01,5); FastLRNR rhat=32."""
+    """c2: LRNR 2-256x6-1, r (2,32x5,1), FP32, sin, mu=(20,0.01,5); FastLRNR r_hat 32 (mu-grid snapshots)."""
     m, s = make_baseline_model(C2_WIDTHS, C2_RANKS, 2411, act)
     pts = sample_collocation(4002, n_points)
     out = dict(model=m, s=s, pts=pts, mu=np.array([20.0, 0.01, 5.0]), dtype=F32)
     if with_fast:
-        out["fast"] = build_fast(m, s, nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777, r_hat=32)
+        S = hyper_forward(c3_hyper(), C2_FAST_MU_GRID)
+        out["fast"] = build_fast(m, S, nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777, r_hat=32)
     return out
 
 
 def config3(n_inst=1024, pts_per_inst=16384, act=ACT_SIN):
     """c3: 1024 mu ~ U[1,40]xU[0,0.1]xU[0,10]; hypernet 3-64-64-163 on the c2 base; FastLRNR."""
     c = config2(n_points=0, act=act, with_fast=True)
-    hyper = make_hyper_params(C2_RANKS, 2, 64, 4003, C3_LO, C3_HI, 0.01, 0.5)
+    hyper = c3_hyper()
     _, mus = sample_collocation(4004, n_inst, C3_LO, C3_HI, with_mu=True)
     pts = np.concatenate([sample_collocation(5000 + i, pts_per_inst) for i in range(n_inst)]) if pts_per_inst else \
         np.zeros((0, 2))

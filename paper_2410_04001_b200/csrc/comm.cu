@@ -5,10 +5,13 @@
 // fixed-order chunk combine (training.cpp:243-259): every rank reduces its own
 // points in a fixed order first, then the ranks' partials are summed.
 //
-// libnccl is resolved at run time (dlopen "libnccl.so.2"): inside a PyTorch
-// process that is the NCCL torch already mapped (same soname), in a plain C++
-// caller the system one.  The library therefore has no link-time NCCL
-// dependency, and a context without a communicator never touches NCCL.
+// libnccl is resolved at run time (dlopen "libnccl.so.2", RTLD_LOCAL): inside a
+// PyTorch process that is the NCCL torch already mapped (same soname; the
+// Python binding imports torch before the first communicator call), in a plain
+// C++ caller the system one.  RTLD_LOCAL keeps it out of the global symbol
+// scope, so a torch imported later still binds its own (newer) NCCL.  The
+// library has no link-time NCCL dependency, and a context without a
+// communicator never touches NCCL.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -44,7 +47,7 @@ NcclApi& nccl() {
     api.tried = true;
     const char* names[] = {"libnccl.so.2", "libnccl.so"};
     for (const char* n : names) {
-        api.handle = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+        api.handle = dlopen(n, RTLD_NOW | RTLD_LOCAL);
         if (api.handle) break;
     }
     if (!api.handle) {

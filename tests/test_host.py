@@ -219,3 +219,36 @@ def test_checkpoint_rejects_bad_files(tmp_path):
     trunc.write_bytes(open(CKPT, "rb").read()[:1000])
     with pytest.raises(ValueError):
         pkg.Checkpoint(trunc)
+
+
+@pytest.fixture(scope="module")
+def golden_r2():
+    return dict(np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_golden_r2.npz")))
+
+
+def test_host_hyper_forward_bit_exact(golden_r2):
+    """hyper_forward (model.cpp:294-318) of the c3 hypernetwork on the mu grid, bit for bit."""
+    h = pkg.c3_hyper()
+    assert np.array_equal(h.params, golden_r2["c3_hparams"])
+    S = pkg.hyper_forward(h, golden_r2["mu_grid"])
+    assert np.array_equal(S, golden_r2["grid_s"])
+
+
+def test_mu_grid_fast_construction_bit_exact(golden_r2):
+    """The c2 FastLRNR from snapshots over the mu grid (harvest_snapshots with mu_grid, eim_greedy,
+    build_fastparams; reduction.cpp:111-283): indices and reduced matrices equal the reference's, and
+    the budget of 32 is reached in every inner layer (tanh, the reference's activation)."""
+    m, _ = pkg.make_baseline_model(pkg.api.C2_WIDTHS, pkg.api.C2_RANKS, 2411, pkg.ACT_TANH)
+    f = pkg.build_fast(m, golden_r2["grid_s"], nx=4, nt=3, n_perturb=8, sigma=0.05, seed=777, r_hat=32)
+    assert list(f.red_ranks) == list(golden_r2["c2grid_red"]) == [32] * 6
+    assert np.array_equal(f.indices, golden_r2["c2grid_idx"])
+    assert np.array_equal(f.fparams, golden_r2["c2grid_fparams"])
+    c = pkg.config2(n_points=0, act=pkg.ACT_TANH)  # the bench's / tests' c2 builder uses this recipe
+    assert np.array_equal(c["fast"].fparams, golden_r2["c2grid_fparams"])
+
+
+def test_hyper_forward_rejects_bad_shapes():
+    h = pkg.c3_hyper()
+    bad = pkg.HyperParams(np.array([2, 64, 163]), h.params[:10], h.lo, h.hi)
+    with pytest.raises(ValueError):
+        pkg.hyper_forward(bad, [[1.0, 0.0, 0.0]])
