@@ -33,7 +33,10 @@ def test_c2_fast_matches_oracle(narrow, oracle, act, fast_sincos, n):
     narrow.set_points(c["pts"])
     got = narrow.loss_grad_s(pkg.MODEL_FAST, c["s"], c["mu"])
     want = oracle.fast_grad(f.ranks, f.red_ranks, f.fparams, c["s"], c["mu"], c["pts"], act=act)
-    assert abs(got["value"] - want["value"]) <= TOL32_LOSS * abs(want["value"])
+    # the SFU sin/cos mode (~4e-7 absolute) is the approximate option: 1e-3 on the loss of a few points,
+    # whose residual cancels to ~1e-3 of its terms; the accurate default keeps 1e-4
+    tol_loss = 1e-3 if fast_sincos else TOL32_LOSS
+    assert abs(got["value"] - want["value"]) <= tol_loss * abs(want["value"])
     assert normwise(got["grad_s"], want["grad_s"]) <= TOL32_NORM
 
 
