@@ -90,6 +90,14 @@ __device__ __forceinline__ double ref_dot(double acc, const double* a, int sa, c
 // follow that build one for one (constants are fdlibm's), so harvested
 // snapshots are bit-identical to the CPU's and the greedy selection downstream
 // cannot diverge on near-ties. Domain used by tanh: finite x > -38.8.
+//
+// The algorithm and constants of glibc_expm1 / glibc_tanh below are those of
+// fdlibm's s_expm1.c / s_tanh.c, which carry this notice:
+//   Copyright (C) 1993 by Sun Microsystems, Inc. All rights reserved.
+//   Developed at SunPro, a Sun Microsystems, Inc. business.
+//   Permission to use, copy, modify, and distribute this
+//   software is freely granted, provided that this notice
+//   is preserved.
 __device__ __forceinline__ double scale2k(double y, int k) {
     return __hiloint2double(__double2hiint(y) + (k << 20), __double2loint(y));
 }

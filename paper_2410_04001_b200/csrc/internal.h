@@ -120,16 +120,6 @@ struct Model {
         std::vector<int> sched_cnt;
         DevBuf dblocks, dsched_off, dsched_bytes;
     } tc;
-    // meta tensor-core kernel (pinn_meta_tc.cuh): bf16 factor blocks, schedule,
-    // per-CTA partial layout and the ParamPacker map
-    struct MTC {
-        bool ok = false;
-        std::vector<int> rp, nc, yoff, qdb;
-        std::vector<int64_t> gbase;
-        int64_t ystride = 0, qbase = 0, wg_stride = 0, n_params = 0;
-        int QS = 0, qdUL = 0, qdbL = 0, qdV0 = 0, sched_len = 0;
-        DevBuf dblocks, dsched_off, dsched_bytes, dmap, wg, sum;
-    } mtc;
     // meta tensor-core kernel v2 (pinn_meta_tc2.cuh): neurons on TMEM lanes, 128-neuron chunks
     struct MTC2 {
         bool ok = false;
@@ -165,10 +155,6 @@ void build_v2(Model& m, bool meta = false);
 void build_tc(Model& m);
 void build_fk(Model& m);
 bool mtc_eligible(const Model& m);
-void build_mtc(Model& m);
-template <int ACT>
-void launch_meta_tc(lrnr_gpu_ctx* ctx, Model& m, const double* s_dev, const double* mu_dev, double w, double* dev_out,
-                    double* wg_out);
 void build_mtc2(Model& m);
 template <int ACT>
 void launch_meta_tc2(lrnr_gpu_ctx* ctx, Model& m, const double* s_dev, const double* mu_dev, double w, double* dev_out,

@@ -19,7 +19,6 @@
 
 #include "hyper_kernels.cuh"
 #include "internal.h"
-#include "meta_kernels.cuh"
 #include "instances.h"
 #include "pinn_tc.cuh"
 
@@ -95,8 +94,7 @@ void release_model(Model& m) {
     m.tc.dsched_off.release();
     m.tc.dsched_bytes.release();
     m.flat_dev.release();
-    for (DevBuf* b : {&m.mtc.dblocks, &m.mtc.dsched_off, &m.mtc.dsched_bytes, &m.mtc.dmap, &m.mtc.wg, &m.mtc.sum,
-                      &m.mtc2.dblocks, &m.mtc2.dblk_off, &m.mtc2.dblk_bytes, &m.mtc2.dmap, &m.mtc2.wg, &m.mtc2.sum})
+    for (DevBuf* b : {&m.mtc2.dblocks, &m.mtc2.dblk_off, &m.mtc2.dblk_bytes, &m.mtc2.dmap, &m.mtc2.wg, &m.mtc2.sum})
         b->release();
 }
 
@@ -374,12 +372,8 @@ void launch_tc(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
     g.tiles_per_inst = static_cast<int>((n_per + tc::P - 1) / tc::P);
     const int64_t total_tiles = static_cast<int64_t>(g.tiles_per_inst) * n_inst;
     const int64_t max_grid = ctx->num_sms;  // one CTA per SM: it owns all 512 TMEM columns
-#if TC_DYN_SCHED
     // units are claimed dynamically: one tile each up to 64 per CTA
     int64_t tpu = (total_tiles + max_grid * 64 - 1) / (max_grid * 64);
-#else
-    int64_t tpu = (total_tiles + max_grid * 4 - 1) / (max_grid * 4);
-#endif
     tpu = std::max<int64_t>(1, std::min<int64_t>(tpu, g.tiles_per_inst));
     g.tiles_per_unit = static_cast<int>(tpu);
     g.units_per_inst = static_cast<int>((g.tiles_per_inst + tpu - 1) / tpu);
@@ -939,7 +933,7 @@ int lrnr_gpu_set_option(lrnr_gpu_ctx* ctx, int opt, int value) {
         else if (opt == LRNR_OPT_KERNEL) ctx->opt_kernel = value;
         else if (opt == LRNR_OPT_SOLVE) ctx->opt_solve = value;
         else if (opt == LRNR_OPT_META_PREC) {
-            require(value >= 0 && value <= 2, "meta precision must be 0 (FP32) or 1 / 2 (BF16 tensor-core operands)");
+            require(value == 0 || value == 1, "meta precision must be 0 (FP32) or 1 (BF16 tensor-core operands)");
             ctx->opt_meta_prec = value;
         }
         else if (opt == LRNR_OPT_TILE_P) {

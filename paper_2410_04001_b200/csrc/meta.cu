@@ -96,14 +96,8 @@ void meta_step(lrnr_gpu_ctx* ctx, Model& m, double w, double* out_grad, double* 
         const int RP = v.RPMAX;
         if (ctx->opt_meta_prec != 0) {
             require(mtc_eligible(m), "BF16 meta path: needs an FP32 LRNR with widths (2, ..., 1), ranks <= 64, r_total < 512");
-            // 1: v2 kernel (neurons on TMEM lanes, default); 2: v1 kernel (points on TMEM lanes)
-            if (ctx->opt_meta_prec == 2) {
-                if (m.act == LRNR_ACT_SIN) launch_meta_tc<1>(ctx, m, sd, md, wt, rows_out, gout);
-                else launch_meta_tc<0>(ctx, m, sd, md, wt, rows_out, gout);
-            } else {
-                if (m.act == LRNR_ACT_SIN) launch_meta_tc2<1>(ctx, m, sd, md, wt, rows_out, gout);
-                else launch_meta_tc2<0>(ctx, m, sd, md, wt, rows_out, gout);
-            }
+            if (m.act == LRNR_ACT_SIN) launch_meta_tc2<1>(ctx, m, sd, md, wt, rows_out, gout);
+            else launch_meta_tc2<0>(ctx, m, sd, md, wt, rows_out, gout);
             return;
         }
         if (m.dtype == LRNR_F32 && m.act == LRNR_ACT_SIN && RP == 64) launch_v2<float, 32, 1, 8, 64, 1, false, true>(ctx, m, sd, md, wt, rows_out, gout);

@@ -1,4 +1,4 @@
-// Host side of the meta tensor-core kernel (pinn_meta_tc.cuh): bf16 factor
+// Host side of the meta tensor-core kernel (pinn_meta_tc2.cuh): bf16 factor
 // blocks + per-tile schedule, the launch, and the fixed-order reduction of the
 // per-CTA partial gradients into ParamPacker order (autodiff.cpp:926-946).
 #include <cuda_bf16.h>
@@ -7,7 +7,6 @@
 #include <vector>
 
 #include "internal.h"
-#include "pinn_meta_tc.cuh"
 #include "pinn_meta_tc2.cuh"
 
 namespace lrnr_b200 {
@@ -46,206 +45,6 @@ bool mtc_eligible(const Model& m) {
     return 1 + m.rtotal <= mtc::MAX_R1;
 }
 
-void build_mtc(Model& m) {
-    auto& v = m.mtc;
-    v = Model::MTC{};
-    if (!mtc_eligible(m)) return;
-    const int L = m.L;
-    v.rp.assign(L, 0);
-    v.nc.assign(L, 0);
-    v.yoff.assign(L, 0);
-    for (int l = 0; l < L; ++l) v.rp[l] = pad16(m.r[l]);
-    int64_t yo = 0;
-    for (int l = 0; l + 1 < L; ++l) {
-        v.nc[l] = (m.M[l + 1] + mtc::KC - 1) / mtc::KC;
-        v.yoff[l] = static_cast<int>(yo);
-        yo += static_cast<int64_t>(mtc::P) * v.rp[l] * 4;
-    }
-    v.ystride = yo;
-    // factor blocks (bytes)
-    std::vector<unsigned char> blob;
-    std::vector<std::vector<int64_t>> foff(L), boff(L);
-    std::vector<int> fbytes(L), bbytes(L);
-    auto put = [&](size_t base, int elem, float x) {
-        const __nv_bfloat16 h = __float2bfloat16(x);
-        std::memcpy(blob.data() + base + 2 * static_cast<size_t>(elem), &h, 2);
-    };
-    for (int l = 0; l + 1 < L; ++l) {
-        const int rl = m.r[l], rn = m.r[l + 1], RL = v.rp[l], RN = v.rp[l + 1], M = m.M[l + 1];
-        const double* rows = m.packed.data() + m.off_trans[l];
-        auto U = [&](int k, int j) { return (k < M && j < rl) ? rows[static_cast<size_t>(k) * m.trow[l] + j] : 0.0; };
-        auto V = [&](int k, int j) { return (k < M && j < rn) ? rows[static_cast<size_t>(k) * m.trow[l] + rl + j] : 0.0; };
-        auto B = [&](int k) { return k < M ? rows[static_cast<size_t>(k) * m.trow[l] + rl + rn] : 0.0; };
-        fbytes[l] = 32 * (RL + RN) + 64;
-        bbytes[l] = 32 * (2 * RL + RN) + 64;
-        for (int c = 0; c < v.nc[l]; ++c) {
-            const int k0 = c * mtc::KC;
-            // forward: UB (N 16 neurons x K RL) | bias | VB (N RN x K 16)
-            size_t o = blob.size();
-            foff[l].push_back(static_cast<int64_t>(o));
-            blob.resize(o + fbytes[l], 0);
-            for (int n = 0; n < mtc::KC; ++n)
-                for (int j = 0; j < RL; ++j) put(o, toff_h(n, j, mtc::KC), static_cast<float>(U(k0 + n, j)));
-            for (int n = 0; n < mtc::KC; ++n) {
-                const float b = static_cast<float>(B(k0 + n));
-                std::memcpy(blob.data() + o + 32 * RL + 4 * n, &b, 4);
-            }
-            for (int j = 0; j < RN; ++j)
-                for (int n = 0; n < mtc::KC; ++n)
-                    put(o + 32 * RL + 64, toff_h(j, n, RN), static_cast<float>(V(k0 + n, j)));
-            // reverse: UB | bias | VB' (N 16 neurons x K RN) | UT (N RL x K 16)
-            o = blob.size();
-            boff[l].push_back(static_cast<int64_t>(o));
-            blob.resize(o + bbytes[l], 0);
-            for (int n = 0; n < mtc::KC; ++n)
-                for (int j = 0; j < RL; ++j) put(o, toff_h(n, j, mtc::KC), static_cast<float>(U(k0 + n, j)));
-            for (int n = 0; n < mtc::KC; ++n) {
-                const float b = static_cast<float>(B(k0 + n));
-                std::memcpy(blob.data() + o + 32 * RL + 4 * n, &b, 4);
-            }
-            for (int n = 0; n < mtc::KC; ++n)
-                for (int j = 0; j < RN; ++j)
-                    put(o + 32 * RL + 64, toff_h(n, j, mtc::KC), static_cast<float>(V(k0 + n, j)));
-            for (int j = 0; j < RL; ++j)
-                for (int n = 0; n < mtc::KC; ++n)
-                    put(o + 32 * RL + 64 + 32 * RN, toff_h(j, n, RL), static_cast<float>(U(k0 + n, j)));
-        }
-    }
-    std::vector<int64_t> soff;
-    std::vector<int> sbytes;
-    for (int l = 0; l + 1 < L; ++l)
-        for (int c = 0; c < v.nc[l]; ++c) {
-            soff.push_back(foff[l][c]);
-            sbytes.push_back(fbytes[l]);
-        }
-    for (int l = L - 2; l >= 0; --l)
-        for (int c = 0; c < v.nc[l]; ++c) {
-            soff.push_back(boff[l][c]);
-            sbytes.push_back(bbytes[l]);
-        }
-    v.sched_len = static_cast<int>(soff.size());
-    v.dblocks.ensure(std::max<size_t>(blob.size(), 16));
-    CK(cudaMemcpy(v.dblocks.p, blob.data(), blob.size(), cudaMemcpyHostToDevice));
-    v.dsched_off.ensure(soff.size() * sizeof(int64_t));
-    v.dsched_bytes.ensure(sbytes.size() * sizeof(int));
-    CK(cudaMemcpy(v.dsched_off.p, soff.data(), soff.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(v.dsched_bytes.p, sbytes.data(), sbytes.size() * sizeof(int), cudaMemcpyHostToDevice));
-    // per-CTA partial layout
-    int64_t go = 0;
-    v.gbase.assign(L, 0);
-    for (int l = 0; l + 1 < L; ++l) {
-        v.gbase[l] = go;
-        go += static_cast<int64_t>(v.nc[l]) * 2048;
-    }
-    v.qbase = go;
-    int qo = 0;
-    v.qdb.assign(L, 0);
-    for (int l = 0; l + 1 < L; ++l) {
-        v.qdb[l] = qo;
-        qo += v.nc[l] * mtc::KC;
-    }
-    v.qdUL = qo;
-    qo += m.r[L - 1];
-    v.qdbL = qo;
-    qo += 1;
-    v.qdV0 = qo;
-    qo += 2 * m.r[0];
-    v.QS = (qo + 31) & ~31;
-    v.wg_stride = (v.qbase + 4 * static_cast<int64_t>(v.QS) + 63) & ~int64_t(63);
-    // ParamPacker index -> partial entry (>= 0) or -(quarter offset + 1)
-    std::vector<int> map;
-    for (int l = 0; l < L; ++l) {
-        const int Mo = m.M[l + 1], Mi = m.M[l], r = m.r[l];
-        for (int k = 0; k < Mo; ++k)
-            for (int j = 0; j < r; ++j)
-                map.push_back(l + 1 < L ? static_cast<int>(v.gbase[l] + (k / 16) * 2048 + j * 16 + k % 16)
-                                        : -(v.qdUL + j) - 1);
-        for (int i = 0; i < Mi; ++i)
-            for (int j = 0; j < r; ++j)
-                map.push_back(l == 0 ? -(v.qdV0 + i * r + j) - 1
-                                     : static_cast<int>(v.gbase[l - 1] + (i / 16) * 2048 + 1024 + j * 16 + i % 16));
-        for (int k = 0; k < Mo; ++k) map.push_back(l + 1 < L ? -(v.qdb[l] + k) - 1 : -v.qdbL - 1);
-    }
-    v.n_params = static_cast<int64_t>(map.size());
-    v.dmap.ensure(map.size() * sizeof(int));
-    CK(cudaMemcpy(v.dmap.p, map.data(), map.size() * sizeof(int), cudaMemcpyHostToDevice));
-    v.ok = true;
-}
-
-template <int ACT>
-void launch_meta_tc(lrnr_gpu_ctx* ctx, Model& m, const double* s_dev, const double* mu_dev, double w, double* dev_out,
-                    double* wg_out) {
-    if (!m.mtc.ok) build_mtc(m);
-    const auto& v = m.mtc;
-    if (!v.ok) throw InvalidArg("meta tensor-core kernel: needs an FP32 LRNR with widths (2, ..., 1), ranks <= 64");
-    const int64_t n_inst = ctx->n_inst, n_per = ctx->n_per;
-    const int R1 = 1 + m.rtotal;
-    auto kern = mtc::meta_tc_kernel<ACT>;
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, mtc::SMEM_BYTES));
-    RunGeom g{};
-    g.P = mtc::P;
-    g.n_per_inst = n_per;
-    g.tiles_per_inst = static_cast<int>((n_per + mtc::P - 1) / mtc::P);
-    const int64_t total_tiles = static_cast<int64_t>(g.tiles_per_inst) * n_inst;
-    const int64_t max_grid = ctx->num_sms;
-    int64_t tpu = (total_tiles + max_grid * 4 - 1) / (max_grid * 4);
-    tpu = std::max<int64_t>(1, std::min<int64_t>(tpu, g.tiles_per_inst));
-    g.tiles_per_unit = static_cast<int>(tpu);
-    g.units_per_inst = static_cast<int>((g.tiles_per_inst + tpu - 1) / tpu);
-    g.n_units = static_cast<int64_t>(g.units_per_inst) * n_inst;
-    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_grid, g.n_units)));
-    ctx->scratch.ensure(static_cast<size_t>(grid) * v.ystride * sizeof(float) + 64);
-    ensure_part<float>(ctx, n_inst, g.units_per_inst, R1);
-    m.mtc.wg.ensure(static_cast<size_t>(grid) * v.wg_stride * sizeof(float));
-    m.mtc.sum.ensure(static_cast<size_t>(v.wg_stride) * sizeof(double));
-    float* wg = m.mtc.wg.as<float>();
-    CK(cudaMemsetAsync(wg, 0, static_cast<size_t>(grid) * v.wg_stride * sizeof(float), ctx->stream));
-    mtc::MetaNet net{};
-    net.L = m.L;
-    for (int l = 0; l <= m.L; ++l) net.M[l] = m.M[l];
-    for (int l = 0; l < m.L; ++l) {
-        net.r[l] = m.r[l];
-        net.rp[l] = v.rp[l];
-        net.nc[l] = v.nc[l];
-        net.yoff[l] = v.yoff[l];
-        net.gbase[l] = v.gbase[l];
-        net.qdb[l] = v.qdb[l];
-    }
-    for (int l = 0; l <= m.L; ++l) net.soff[l] = m.soff[l];
-    net.ystride = v.ystride;
-    net.rtotal = m.rtotal;
-    net.blocks = v.dblocks.as<unsigned char>();
-    net.sched_off = v.dsched_off.as<int64_t>();
-    net.sched_bytes = v.dsched_bytes.as<int>();
-    net.sched_len = v.sched_len;
-    const float* base = m.dev.as<float>();
-    net.V0 = base + m.off_V0;
-    net.ulast = base + m.off_ulast;
-    net.qbase = v.qbase;
-    net.QS = v.QS;
-    net.qdUL = v.qdUL;
-    net.qdbL = v.qdbL;
-    net.qdV0 = v.qdV0;
-    net.wg_stride = v.wg_stride;
-    kern<<<grid, mtc::NT, mtc::SMEM_BYTES, ctx->stream>>>(net, g, ctx->pts, s_dev, mu_dev, static_cast<float>(w),
-                                                           ctx->scratch.as<float>(), ctx->part.as<float>(), wg,
-                                                           bad_word(ctx, m), ctx->term_spec,
-                                                           ctx->term_objective);
-    CK(cudaGetLastError());
-    reduce_rows_kernel<float><<<static_cast<unsigned>((v.wg_stride + 255) / 256), 256, 0, ctx->stream>>>(
-        wg, grid, v.wg_stride, v.wg_stride, m.mtc.sum.as<double>(), 0);
-    CK(cudaGetLastError());
-    mtc_permute_kernel<<<static_cast<unsigned>((v.n_params + 255) / 256), 256, 0, ctx->stream>>>(
-        m.mtc.sum.as<double>(), v.dmap.as<int>(), v.n_params, v.qbase, v.QS, wg_out, ctx->accumulate_wg);
-    CK(cudaGetLastError());
-    reduce_units<float>(ctx, n_inst, g.units_per_inst, R1, dev_out);
-    ctx->launches += 3;
-}
-
-// ---------------------------------------------------------------------------
-// v2 (pinn_meta_tc2.cuh): factor blocks per (transition, 128-neuron chunk), shared
-// by the forward and reverse sweeps: [U_c | b_c | V_c], U_c / V_c as
-// [rank grp][neuron grp][8 neurons][8 ranks] bf16, b_c fp32
 void build_mtc2(Model& m) {
     auto& v = m.mtc2;
     v = Model::MTC2{};
@@ -416,8 +215,6 @@ void launch_meta_tc2(lrnr_gpu_ctx* ctx, Model& m, const double* s_dev, const dou
 template void launch_meta_tc2<0>(lrnr_gpu_ctx*, Model&, const double*, const double*, double, double*, double*);
 template void launch_meta_tc2<1>(lrnr_gpu_ctx*, Model&, const double*, const double*, double, double*, double*);
 
-template void launch_meta_tc<0>(lrnr_gpu_ctx*, Model&, const double*, const double*, double, double*, double*);
-template void launch_meta_tc<1>(lrnr_gpu_ctx*, Model&, const double*, const double*, double, double*, double*);
 
 }  // namespace detail
 }  // namespace lrnr_b200

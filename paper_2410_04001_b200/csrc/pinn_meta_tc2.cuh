@@ -1,6 +1,6 @@
 // Meta step on tcgen05, v2: neurons on the TMEM lanes.
 //
-// Same math and outputs as pinn_meta_tc.cuh (BF16 tensor-core operands, FP32
+// Same math and outputs as the retired first meta kernel (BF16 tensor-core operands, FP32
 // accumulation, FP32 activation / residual / reduction math; BASELINE config 4),
 // with the GEMM roles transposed so that every MMA is wide:
 //   * a tile is 64 collocation points = 2 halves of 32 points; a half is 128 jet
@@ -25,7 +25,7 @@
 // TMEM: P1 [0,256) (forward: 2 buffers; reverse: A^T | DZ^T) | Y/T per half [256,384) | dU [384,448) | dV [448,512).
 #pragma once
 
-#include "pinn_meta_tc.cuh"
+#include "meta_common.cuh"
 
 namespace lrnr_b200 {
 namespace mtc2 {

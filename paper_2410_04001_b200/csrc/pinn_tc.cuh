@@ -17,10 +17,9 @@
 // 3xTF32: x = hi + lo with hi = tf32(x); a*b ~ a_hi b_hi + a_hi b_lo + a_lo b_hi
 // (fp32 accumulate), giving ~fp32 accuracy (the dropped lo*lo term is 2^-22).
 // TMEM (512 columns): P1_c 4x32 | Z hi 4x32 | Z lo 4x32 | Y/T 4x32.
-// Shared memory: SY/ST hi/lo for 4 slots (128 KB) + double-buffered factor
-// chunks (2 x 16 KB).  Phases are serialized within a CTA (one CTA per SM owns
-// the whole TMEM); MMA issue is a single thread, completion via tcgen05.commit
-// -> mbarrier.
+// Shared memory: SY/ST hi/lo for 4 slots (128 KB) + a 3-slot factor-chunk ring.
+// One CTA per SM owns the whole TMEM; two issuer warps issue the phase-1 and
+// phase-2 MMAs warp-collectively, completion via tcgen05.commit -> mbarrier.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -39,60 +38,25 @@ constexpr int RP = 32;    // max padded rank
 #ifndef TC_NWE
 #define TC_NWE 16
 #endif
-#ifndef TC_DEDICATED
-#define TC_DEDICATED 1
-#endif
 constexpr int NWE = TC_NWE;  // epilogue warps: lane quarter = warp % 4, neuron / rank group of NG = warp / 4
-// the MMA issuer (its issue blocks while the MMA queue drains, so a dedicated
-// warp keeps the epilogue warps free); warp 0 (also an epilogue warp) otherwise
-// TC_SPLIT_ISSUE: MMA issue is latency-bound (~57 cycles per MMA from one warp),
-// so it is spread over warps that issue concurrently: 0 = one warp for both
-// phases; 1 = phase-1 and phase-2 MMAs from two warps; 2 = four warps, each
-// phase's 4 jet slots split between two (independent TMEM accumulators; measured
-// slower: 27.1 vs 23.8 ms on c2).
-#ifndef TC_SPLIT_ISSUE
-#define TC_SPLIT_ISSUE 1
-#endif
-// (3 = one phase-1 issuer, phase 2 split over two warps: 23.8 vs 23.5 ms, slower too)
-constexpr int NISS = (TC_DEDICATED && TC_SPLIT_ISSUE == 2) ? 2 : 1;   // phase-1 issuer warps
-constexpr int NISS2 = (TC_DEDICATED && TC_SPLIT_ISSUE >= 2) ? 2 : 1;  // phase-2 issuer warps
-constexpr int ISSUER = TC_DEDICATED ? NWE : 0;                        // first phase-1 issuer
-constexpr int ISSUER2 = (TC_DEDICATED && TC_SPLIT_ISSUE) ? NWE + NISS : ISSUER;  // first phase-2 issuer
-constexpr int NT = 32 * (NWE + (TC_DEDICATED ? (TC_SPLIT_ISSUE ? NISS + NISS2 : 1) : 0));
+// Two dedicated MMA issuer warps after the epilogue warps: MMA issue is
+// latency-bound (~57 cycles per MMA from one warp), so the phase-1 and phase-2
+// MMAs are issued concurrently by warps ISSUER and ISSUER2 (one issuer: 24.40 ms
+// on c2; two: 23.51 ms; four, with each phase's jet slots split: 27.1 ms).
+constexpr int ISSUER = NWE;       // phase-1 issuer
+constexpr int ISSUER2 = NWE + 1;  // phase-2 issuer
+constexpr int NT = 32 * (NWE + 2);
 constexpr int NG = KC / (NWE / 4);  // neurons (epilogue) / ranks (sums) per thread
-// TC_DYN_SCHED: units after each CTA's first are claimed from a global counter (SMs run at
-// slightly different speeds: per-CTA times on a static split spread by up to 5 %)
-#ifndef TC_DYN_SCHED
-#define TC_DYN_SCHED 1
-#endif
-// TC_STASH_HINT: streaming (evict-first) stores / loads for the pre-activation stash,
-// which is read back once, half a tile later (measured slower: 26.9 vs 23.3 ms -- part of
-// the stash is still hit in L2)
-#ifndef TC_STASH_HINT
-#define TC_STASH_HINT 0
-#endif
-// TC_LANE_ISSUE: the issuing warp's lane 0 issues its MMAs as a single thread
-// (0 = warp-collective, elect.sync inside every MMA: 23.55 ms on c2 vs 25.9 for 1)
-#ifndef TC_LANE_ISSUE
-#define TC_LANE_ISSUE 0
-#endif
-#if TC_LANE_ISSUE
-#define TC_MMA_SS umma::mma_ss_1
-#define TC_MMA_TS umma::mma_ts_1
-#define TC_COMMIT umma::mma_commit_1
-#else
+// Units (single tiles) after each CTA's first are claimed from a global counter:
+// SMs run at slightly different speeds (a static split spread by up to 5 %).
 #define TC_MMA_SS umma::mma_ss_w
 #define TC_MMA_TS umma::mma_ts_w
 #define TC_COMMIT umma::mma_commit_w
-#endif
 constexpr int TM_P1 = 0, TM_ZH = 128, TM_ZL = 256, TM_Y = 384;
 // Phase-2 products of YACC consecutive chunks accumulate in TMEM before the
 // epilogue reads them into the FP32 running sum (the tensor-core accumulator
 // truncates: 1 chunk = 12 MMAs keeps it at ~3e-6 on c2, 2 chunks ~6e-6, the
 // full K = 256 reached 1.2e-4). Halves the TMEM load round trips of Y.
-#ifndef TC_SPLITLD
-#define TC_SPLITLD 1
-#endif
 #ifndef TC_YACC
 #define TC_YACC 2
 #endif
@@ -275,8 +239,8 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
     if (warp == 0) umma::tmem_alloc<512>(&tmem_base);
     if (tid == 0) {
         for (int i = 0; i < NBUF; ++i) umma::mbar_init(&wbar[i], 1);
-        umma::mbar_init(&mbar1, NISS);  // one commit per issuing warp
-        umma::mbar_init(&mbar2, NISS2);
+        umma::mbar_init(&mbar1, 1);
+        umma::mbar_init(&mbar2, 1);
         umma::mbar_init(&p1free, NWE);
         umma::mbar_init(&zready, NWE);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -301,21 +265,11 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
     };
 
     // ---- factor-chunk pipeline (TMA bulk copies) ----
-#if TC_DYN_SCHED
     // every tile runs the same chunk schedule, so the ring is refilled without knowing the
     // CTA's tile count; the NBUF - 1 copies in flight past the last chunk are drained at exit
     const int64_t total_chunks = INT64_MAX;
 #ifdef TC_CTA_TIMES
     int64_t total_tiles = 0;
-#endif
-#else
-    int64_t total_tiles = 0;
-    for (int64_t u = blockIdx.x; u < g.n_units; u += gridDim.x) {
-        const int seg = static_cast<int>(u % g.units_per_inst);
-        const int t_lo = seg * g.tiles_per_unit;
-        total_tiles += min(g.tiles_per_inst, t_lo + g.tiles_per_unit) - t_lo;
-    }
-    const int64_t total_chunks = total_tiles * net.sched_len;
 #endif
     int64_t q = 0;
     auto issue = [&](int64_t qq) {
@@ -349,19 +303,11 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
     const uint32_t lsy = umma::desc_lo(sm + OFF_SY, (P / 8) * 128);     // SY / ST tiles (rows = P)
     const uint32_t lb32 = umma::desc_lo(sm + OFF_B0, (KC / 8) * 128);   // factor tiles with 32 rows
     const uint32_t lb16 = umma::desc_lo(sm + OFF_B0, (16 / 8) * 128);   // factor tiles with 16 rows
-    // phase 1 (warp 0, converged): P1_c = S_c B (3xTF32), S = SY / ST from smem,
+    // phase 1 (issuer warp, converged): P1_c = S_c B (3xTF32), S = SY / ST from smem,
     // B = factor tiles at float offset bo (hi) / bo + KC * rk (lo) of the ring slot
-    // the jet slots this warp issues (all 4, or 2 when each phase has two issuer warps)
-    const bool p2w = ISSUER2 != ISSUER && warp >= ISSUER2;
-    const int cis = (p2w ? NISS2 : NISS) == 1 ? 0 : ((warp - (p2w ? ISSUER2 : ISSUER)) & 1) * 2;
-    const int cie = (p2w ? NISS2 : NISS) == 1 ? 4 : cis + 2;
     auto mma_p1 = [&](int bo, int rk) {
-#if TC_LANE_ISSUE
-        if (lane == 0) {
-#endif
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            if (c < cis || c >= cie) continue;
             const uint32_t d = tbase + TM_P1 + c * KC;
             const uint32_t ah0 = lsy + ((2 * c) * SY_TILE >> 2), al0 = lsy + ((2 * c + 1) * SY_TILE >> 2);
             const uint32_t bh0 = lb32 + (bo >> 2), bl0 = lb32 + ((bo + KC * rk) >> 2);
@@ -373,24 +319,16 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
             }
         }
         TC_COMMIT(&mbar1);
-#if TC_LANE_ISSUE
-        }
-        __syncwarp();
-#endif
     };
-    // phase 2 (warp 0, converged): Y_c = Z_c B (fresh accumulator, A from TMEM),
+    // phase 2 (issuer warp 2, converged): Y_c = Z_c B (fresh accumulator, A from TMEM),
     // B = factor tiles (rows rn) at float offset bo (hi) / bo + rn * KC (lo)
     auto mma_p2 = [&](int bo, int rn, bool acc0) {
         const uint32_t id_p2 = umma::idesc_tf32(P, rn);
         const uint32_t lb = rn == 16 ? lb16 : lb32;
         const uint32_t bh0 = lb + (bo >> 2), bl0 = lb + ((bo + rn * KC) >> 2);
         const uint32_t sb = 2 * (rn / 8) * 32 >> 2;
-#if TC_LANE_ISSUE
-        if (lane == 0) {
-#endif
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            if (c < cis || c >= cie) continue;
             const uint32_t d = tbase + TM_Y + c * 32;
 #pragma unroll
             for (int s = 0; s < KC / 8; ++s) {
@@ -401,25 +339,17 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
             }
         }
         TC_COMMIT(&mbar2);
-#if TC_LANE_ISSUE
-        }
-        __syncwarp();
-#endif
     };
     auto wait_slot = [&](int64_t qq) {
         umma::mbar_wait(&wbar[qq % NBUF], static_cast<uint32_t>((qq / NBUF) & 1));
         umma::fence_after();
     };
 
-#if TC_DYN_SCHED
     // claims: the counter starts at all-ones (memset 0xff), so the first claim returns unit gridDim.x
     unsigned long long claim = 0;
     if (tid == 0) claim = atomicAdd(unit_ctr, 1ull) + 1ull + gridDim.x;
     for (int64_t unit = blockIdx.x; unit < g.n_units;) {
-#else
-    for (int64_t unit = blockIdx.x; unit < g.n_units; unit += gridDim.x) {
-#endif
-#if defined(TC_CTA_TIMES) && TC_DYN_SCHED
+#ifdef TC_CTA_TIMES
         ++total_tiles;
 #endif
         const int64_t inst = unit / g.units_per_inst;
@@ -475,7 +405,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                 auto fwd_p2 = [&](int64_t qq, int ch) {
                     mma_p2(static_cast<int>(qq % NBUF) * BUF + 2 * KC * rk + 32, rnn, ch % YACC != 0);
                 };
-                if (warp >= ISSUER && warp < ISSUER + NISS) fwd_p1(q);
+                if (warp == ISSUER) fwd_p1(q);
                 // pipeline per chunk ch: [P1(ch) | P2(ch-1)] on the tensor core while the
                 // epilogue of ch computes the activation jet; Z / Y are touched only after
                 // P2(ch-1) completes.  P1(ch+1) is issued ahead of P2(ch).
@@ -490,34 +420,21 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                         {
                             float a[4][NG];
                             float* Ast = ascr + net.aoff[l] + static_cast<int64_t>(ch) * (P * KC * 4);
-#if TC_SPLITLD
                             // two column halves: the second half's TMEM read overlaps the first half's math
     #pragma unroll
                             for (int c = 0; c < 4; ++c) umma::tmem_ld4(tlane + TM_P1 + c * KC + half * NG, a[c]);
                             umma::tmem_ld_wait();
     #pragma unroll
                             for (int c = 0; c < 4; ++c) umma::tmem_ld4(tlane + TM_P1 + c * KC + half * NG + 4, a[c] + 4);
-#else
-    #pragma unroll
-                            for (int c = 0; c < 4; ++c) tld(tlane + TM_P1 + c * KC + half * NG, a[c]);
-                            umma::tmem_ld_wait();
-                            signal(&p1free);  // P1 may be overwritten by P1(ch+1)
-#endif
     #pragma unroll
                             for (int n = 0; n < NG; ++n) {
-#if TC_SPLITLD
                                 if (n == NG / 2) {
                                     umma::tmem_ld_wait();
-                                    signal(&p1free);
+                                    signal(&p1free);  // P1 may be overwritten by P1(ch+1)
                                 }
-#endif
                                 const int k = half * NG + n;
                                 const float av = a[0][n] + bias[k], ax = a[1][n], at = a[2][n], aw = a[3][n];
-#if TC_STASH_HINT
-                                __stcs(reinterpret_cast<float4*>(Ast + aidx(k, p)), make_float4(av, ax, at, aw));
-#else
                                 v2::st4(Ast + aidx(k, p), av, ax, at, aw);
-#endif
                                 float sg, d1, d2, d3;
                                 act3f<ACT, FAST>(av, sg, d1, d2, d3);
                                 a[0][n] = sg;
@@ -545,17 +462,13 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                         }
                     }
                     TC_MARK(4);
-                    if (warp >= ISSUER && warp < ISSUER + NISS) {
+                    if (warp == ISSUER) {
                         TC_ISSUE_BEGIN();
                         await(&p1free, phf);  // every chunk (keeps the phase count)
                         if (ch + 1 < net.nc[l]) fwd_p1(q + 1);
-                        if (ISSUER2 == ISSUER) {
-                            await(&zready, phz);
-                            fwd_p2(q, ch);
-                        }
-                        if (lane == 0 && warp == ISSUER) TC_ISSUE_END();
+                        if (lane == 0) TC_ISSUE_END();
                     }
-                    if (ISSUER2 != ISSUER && warp >= ISSUER2 && warp < ISSUER2 + NISS2) {
+                    if (warp == ISSUER2) {
                         await(&zready, phz);
                         fwd_p2(q, ch);
                     }
@@ -659,7 +572,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                 auto bwd_p2 = [&](int64_t qq, int ch) {
                     mma_p2(static_cast<int>(qq % NBUF) * BUF + 2 * KC * rkn, rnl, ch % YACC != 0);
                 };
-                if (warp >= ISSUER && warp < ISSUER + NISS) bwd_p1(q);
+                if (warp == ISSUER) bwd_p1(q);
                 for (int ch = 0; ch < net.nc[l]; ++ch, ++q) {
                     if (warp < NWE) {
                         // stored pre-activations of this chunk (in flight during the MMAs)
@@ -668,17 +581,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
     #pragma unroll
                         for (int n = 0; n < NG; ++n) {
                             float a4[4];
-#if TC_STASH_HINT
-                            {
-                                const float4 q4 = __ldcs(reinterpret_cast<const float4*>(Ast + aidx(half * NG + n, p)));
-                                a4[0] = q4.x;
-                                a4[1] = q4.y;
-                                a4[2] = q4.z;
-                                a4[3] = q4.w;
-                            }
-#else
                             v2::ld4(Ast + aidx(half * NG + n, p), a4);
-#endif
     #pragma unroll
                             for (int c = 0; c < 4; ++c) a[c][n] = a4[c];
                         }
@@ -688,26 +591,17 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                         if (ch == 0 && tid == 0) issue(q + NBUF - 1);
                         {
                             float dz[4][NG];
-#if TC_SPLITLD
     #pragma unroll
                             for (int c = 0; c < 4; ++c) umma::tmem_ld4(tlane + TM_P1 + c * KC + half * NG, dz[c]);
                             umma::tmem_ld_wait();
     #pragma unroll
                             for (int c = 0; c < 4; ++c) umma::tmem_ld4(tlane + TM_P1 + c * KC + half * NG + 4, dz[c] + 4);
-#else
-    #pragma unroll
-                            for (int c = 0; c < 4; ++c) tld(tlane + TM_P1 + c * KC + half * NG, dz[c]);
-                            umma::tmem_ld_wait();
-                            signal(&p1free);
-#endif
     #pragma unroll
                             for (int n = 0; n < NG; ++n) {
-#if TC_SPLITLD
                                 if (n == NG / 2) {
                                     umma::tmem_ld_wait();
                                     signal(&p1free);
                                 }
-#endif
                                 const float av = a[0][n], ax = a[1][n], at = a[2][n], aw = a[3][n];
                                 const float g0 = dz[0][n], g1 = dz[1][n], g2 = dz[2][n], g3 = dz[3][n];
                                 float sg, d1, d2, d3;
@@ -737,15 +631,11 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                         }
                     }
                     TC_MARK(12);
-                    if (warp >= ISSUER && warp < ISSUER + NISS) {
+                    if (warp == ISSUER) {
                         await(&p1free, phf);  // every chunk (keeps the phase count)
                         if (ch + 1 < net.nc[l]) bwd_p1(q + 1);
-                        if (ISSUER2 == ISSUER) {
-                            await(&zready, phz);
-                            bwd_p2(q, ch);
-                        }
                     }
-                    if (ISSUER2 != ISSUER && warp >= ISSUER2 && warp < ISSUER2 + NISS2) {
+                    if (warp == ISSUER2) {
                         await(&zready, phz);
                         bwd_p2(q, ch);
                     }
@@ -805,21 +695,15 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
             part[unit * R1 + k] = acc[k];
             acc[k] = 0.f;
         }
-#if TC_DYN_SCHED
         if (tid == 0) {
             next_unit = static_cast<int64_t>(claim);
             if (claim < static_cast<unsigned long long>(g.n_units)) claim = atomicAdd(unit_ctr, 1ull) + 1ull + gridDim.x;
         }
         __syncthreads();
         unit = next_unit;
-#else
-        __syncthreads();
-#endif
     }
-#if TC_DYN_SCHED
     if (tid == 0)
         for (int64_t qq = q; qq < q + NBUF - 1; ++qq) wait_slot(qq);  // prefetches past the last chunk
-#endif
     TC_FLUSH();
     umma::fence_before();
     __syncthreads();
