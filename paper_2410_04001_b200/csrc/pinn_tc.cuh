@@ -198,6 +198,21 @@ __device__ __forceinline__ void add_y(uint32_t taddr, float (&acc)[4][NG]) {
         for (int n = 0; n < NG; ++n) acc[c][n] += v[c][n];
 }
 
+// P1 columns of this thread (4 slots x NG neurons) in two column halves: the first
+// half is waited for here, the second is in flight while the first half's math runs
+// (the caller waits before touching column NG / 2)
+__device__ __forceinline__ void ld_p1_halves(uint32_t taddr, float (&v)[4][NG]) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int h = 0; h < NG / 2; h += 4) umma::tmem_ld4(taddr + c * KC + h, v[c] + h);
+    umma::tmem_ld_wait();
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int h = NG / 2; h < NG; h += 4) umma::tmem_ld4(taddr + c * KC + h, v[c] + h);
+}
+
 // stored pre-activation A of (neuron k, point p) inside its chunk: [k][p][4]
 // (a warp's 32 points are one contiguous 512-B segment)
 __device__ __forceinline__ int aidx(int k, int p) { return (k * P + p) * 4; }
@@ -421,11 +436,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                             float a[4][NG];
                             float* Ast = ascr + net.aoff[l] + static_cast<int64_t>(ch) * (P * KC * 4);
                             // two column halves: the second half's TMEM read overlaps the first half's math
-    #pragma unroll
-                            for (int c = 0; c < 4; ++c) umma::tmem_ld4(tlane + TM_P1 + c * KC + half * NG, a[c]);
-                            umma::tmem_ld_wait();
-    #pragma unroll
-                            for (int c = 0; c < 4; ++c) umma::tmem_ld4(tlane + TM_P1 + c * KC + half * NG + 4, a[c] + 4);
+                            ld_p1_halves(tlane + TM_P1 + half * NG, a);
     #pragma unroll
                             for (int n = 0; n < NG; ++n) {
                                 if (n == NG / 2) {
@@ -591,11 +602,7 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                         if (ch == 0 && tid == 0) issue(q + NBUF - 1);
                         {
                             float dz[4][NG];
-    #pragma unroll
-                            for (int c = 0; c < 4; ++c) umma::tmem_ld4(tlane + TM_P1 + c * KC + half * NG, dz[c]);
-                            umma::tmem_ld_wait();
-    #pragma unroll
-                            for (int c = 0; c < 4; ++c) umma::tmem_ld4(tlane + TM_P1 + c * KC + half * NG + 4, dz[c] + 4);
+                            ld_p1_halves(tlane + TM_P1 + half * NG, dz);
     #pragma unroll
                             for (int n = 0; n < NG; ++n) {
                                 if (n == NG / 2) {

@@ -9,4 +9,4 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler
     --expt-relaxed-constexpr "$@" -c paper_2410_04001_b200/csrc/lrnr_gpu.cu -o build/lrnr_gpu_$name.o
 others=$(ls build/*.cu.o | grep -v '/lrnr_gpu.cu.o$')
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o scripts/liblrnr_gpu_$name.so build/lrnr_gpu_$name.o \
-    $others build/*.cpp.o -cudart static
+    $others build/*.cpp.o -cudart static -ldl

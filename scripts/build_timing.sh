@@ -10,4 +10,4 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler
     -c paper_2410_04001_b200/csrc/lrnr_gpu.cu -o build/lrnr_gpu_timing.o
 others=$(ls build/*.cu.o | grep -v '/lrnr_gpu.cu.o$')
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o scripts/liblrnr_gpu_timing.so build/lrnr_gpu_timing.o \
-    $others build/*.cpp.o -cudart static
+    $others build/*.cpp.o -cudart static -ldl
