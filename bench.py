@@ -260,11 +260,20 @@ class Env:
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         if self.world != args.gpus:
             raise SystemExit(f"bench.py: WORLD_SIZE {self.world} != --gpus {args.gpus}")
+        # LRNR_BENCH_GLOO=1 (tests only): ranks share one GPU, so no NCCL communicator can exist;
+        # the process group is gloo and the contexts get none (their rows are not summed). It
+        # exercises the launch / sharding / timing orchestration of the N-rank run on one GPU.
+        self.gloo = os.environ.get("LRNR_BENCH_GLOO") == "1"
+        if self.gloo:
+            self.local %= torch.cuda.device_count()
         torch.cuda.set_device(self.local)
         self.dist = None
         if self.world > 1:
             import torch.distributed as dist
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if self.gloo:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
             self.dist = dist
         self.stream = torch.cuda.Stream()
         torch.cuda.set_stream(self.stream)
@@ -275,7 +284,7 @@ class Env:
             self.dist.barrier()
 
     def max_over_ranks(self, vals):
-        t = self.torch.tensor(vals, dtype=self.torch.float64, device="cuda")
+        t = self.torch.tensor(vals, dtype=self.torch.float64, device="cpu" if self.gloo else "cuda")
         if self.dist is not None:
             self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return [float(x) for x in t]
@@ -284,7 +293,7 @@ class Env:
         import paper_2410_04001_b200 as pkg
         ctx = pkg.GpuContext(self.local)
         ctx.set_stream(self.stream.cuda_stream)
-        if comm and self.world > 1:
+        if comm and self.world > 1 and not self.gloo:
             from paper_2410_04001_b200.dist import attach_nccl
             attach_nccl(ctx)
         return ctx

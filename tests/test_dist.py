@@ -197,3 +197,25 @@ def test_two_rank_product_path_equals_single_context():
                                (1e-6, 1e-6, 1e-6, 1e-5)):
         err = np.linalg.norm(g - w) / np.linalg.norm(w)
         assert err <= tol, (name, err)
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(900)
+def test_bench_two_ranks_orchestration_on_one_gpu(tmp_path):
+    """bench.py --gpus 2 re-launches itself under torch.distributed.run with 2 ranks (here both on
+    cuda:0, gloo process group, no NCCL communicator -- LRNR_BENCH_GLOO), shards c2 / c3, times with
+    max over ranks and prints one line with n_gpus 2 from rank 0."""
+    import json
+    import subprocess
+
+    env = dict(os.environ, LRNR_BENCH_GLOO="1")
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "1",
+           "--configs", "c0,c3", "--no-solves", "--no-cpu-baseline", "--no-e2e", "--points", "65536"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=800, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["c2_strong"]["n_gpus"] == 2
+    assert d["configs"]["c3"]["n_gpus"] == 2 and d["configs"]["c3"]["instances_per_gpu"] == 512
+    assert d["configs"]["c0"]["n_gpus"] == 1 and d["configs"]["c0"]["value"] > 0
