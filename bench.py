@@ -298,15 +298,17 @@ class Env:
             attach_nccl(ctx)
         return ctx
 
-    def time_steps(self, step, steps, warmup, flush=True, extra_events=0):
+    def time_steps(self, step, steps, warmup, flush=True, extra_events=0, single_rank=False):
         """W untimed steps, then K steps bracketed by barrier + synchronize, CUDA events on the
         launching stream per step (L2 flushed between steps outside the events); max over ranks.
-        step(evs) may record extra events (per-kernel splits) into evs."""
+        step(evs) may record extra events (per-kernel splits) into evs.  single_rank: a section
+        only one rank runs (no collectives: the other ranks are not there)."""
         torch = self.torch
+        barrier = (lambda: None) if single_rank else self.barrier
         for _ in range(warmup):
             step(None)
         torch.cuda.synchronize()
-        self.barrier()
+        barrier()
         torch.cuda.synchronize()
         evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2 + 2 * extra_events)] for _ in range(steps)]
         for k in range(steps):
@@ -316,10 +318,10 @@ class Env:
             step(evs[k][2:])
             evs[k][1].record(self.stream)
         torch.cuda.synchronize()
-        self.barrier()
+        barrier()
         total = sum(e[0].elapsed_time(e[1]) for e in evs)
         splits = [sum(e[2 + 2 * i].elapsed_time(e[3 + 2 * i]) for e in evs) for i in range(extra_events)]
-        vals = self.max_over_ranks([total] + splits)
+        vals = [total] + splits if single_rank else self.max_over_ranks([total] + splits)
         return vals[0] / steps, [v / steps for v in vals[1:]]
 
 
@@ -511,7 +513,7 @@ def single_gpu_fp64(env, pkg, args, key):
         timing = f"stream launch per call (graph capture failed: {e})"
     l0 = ctx.launches
     step = (lambda evs: graph.replay()) if graph is not None else (lambda evs: ctx.run(model, w, out.data_ptr()))
-    ms, _ = env.time_steps(step, max(args.steps, 20), args.warmup)
+    ms, _ = env.time_steps(step, max(args.steps, 20), args.warmup, single_rank=True)  # rank 0 only
     launches_per_call = ctx.launches - l0 if graph is None else None
     ctx.check()
     value = n / (ms * 1e-3)

@@ -200,7 +200,7 @@ def test_two_rank_product_path_equals_single_context():
 
 
 @pytest.mark.gpu
-@pytest.mark.timeout(900)
+@pytest.mark.timeout(480)
 def test_bench_two_ranks_orchestration_on_one_gpu(tmp_path):
     """bench.py --gpus 2 re-launches itself under torch.distributed.run with 2 ranks (here both on
     cuda:0, gloo process group, no NCCL communicator -- LRNR_BENCH_GLOO), shards c2 / c3, times with
@@ -211,7 +211,7 @@ def test_bench_two_ranks_orchestration_on_one_gpu(tmp_path):
     env = dict(os.environ, LRNR_BENCH_GLOO="1")
     cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "1",
            "--configs", "c0,c3", "--no-solves", "--no-cpu-baseline", "--no-e2e", "--points", "65536"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=800, env=env, cwd=ROOT)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=420, env=env, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, r.stdout[-2000:]
