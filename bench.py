@@ -95,13 +95,14 @@ def measured_peak(key, fallback):
         return fallback, "fallback (B200_PROFILING.md)"
 
 
-def traffic_per_launch(kernel):
-    """DRAM bytes (read + write) per launch of a kernel from the committed ncu --set full captures
-    (profiles/traffic.json, written from the .ncu-rep by scripts/ncu_summary.py)."""
+def traffic_per_launch(kernel, points):
+    """DRAM bytes (read + write) per launch of a kernel from the committed ncu --set full capture
+    (profiles/traffic.json), scaled to this launch's points when the profiled launch had fewer."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            d = json.load(f)
-        return d.get("kernels", {}).get(kernel, {}).get("dram_bytes_per_launch")
+            k = json.load(f).get("kernels", {}).get(kernel, {})
+        b = k.get("dram_bytes_per_launch")
+        return None if b is None else b * points / k.get("points", points)
     except Exception:
         return None
 
@@ -395,7 +396,7 @@ def headline(env, pkg, args, ctx):
     lrnr_on_tc = args.kernel in (pkg.KERNEL_AUTO, pkg.KERNEL_TC)
     if lrnr_on_tc:
         roofline = {"bound": "tensor", "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
-                    "frac": achieved / tc_peak, "traffic": traffic_per_launch("pinn_tc_kernel"),
+                    "frac": achieved / tc_peak, "traffic": traffic_per_launch("pinn_tc_kernel", n),
                     "kernel": "pinn_tc_kernel (tcgen05 kind::tf32, 3xTF32 split = FP32-accurate products)",
                     "flop_per_point": flops[0], "points_per_launch": n,
                     "peak_source": f"{bf16_src} {bf16:.1f} TFLOP/s (bf16 dense, burst) / 2 (tf32) / 3 (3 products "
@@ -415,6 +416,7 @@ def headline(env, pkg, args, ctx):
             "kernel": ("pinn_tc_kernel (tcgen05 3xTF32)" if model == pkg.MODEL_LRNR else
                        "pinn_fast_kernel (narrow network, FP32 FMA)")}
     per_kernel["fast"]["roofline"] = {"bound": "fp32-fma", "peak": fp32_peak,
+                                      "traffic": traffic_per_launch("pinn_fast_kernel", n),
                                       "frac": per_kernel["fast"]["tflops"] / fp32_peak}
 
     # end to end through the public host-buffer C ABI: H2D of the step's points from pinned
@@ -601,7 +603,7 @@ def config_c3(env, pkg, args):
             "roofline": {"bound": "fp32-fma", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
                          "flop_per_point": fl, "points_per_launch": (b - a) * PER, "peak_source": src,
                          "kernel": "pinn_fast_kernel (narrow network, FP32 FMA) + FP64 hypernetwork fwd / VJP",
-                         "traffic": traffic_per_launch("pinn_fast_kernel")},
+                         "traffic": traffic_per_launch("pinn_fast_kernel", (b - a) * PER)},
             "gpu_launches": launches,
             "l2": "inputs (268 MB of points) larger than L2; no flush"}
     if not args.no_e2e:
@@ -682,7 +684,7 @@ def config_c4(env, pkg, args):
                          "flop_per_point": fl, "points_per_launch": (b - a) * PER,
                          "peak_source": f"{src} x {env.world} GPU(s) (the kernel runs for seconds under the power cap)",
                          "kernel": "meta_tc2_kernel (tcgen05 kind::f16, BF16 operands, FP32 accumulate)",
-                         "traffic": traffic_per_launch("meta_tc2_kernel")},
+                         "traffic": traffic_per_launch("meta_tc2_kernel", (b - a) * PER)},
             "gpu_launches": launches,
             "l2": "inputs (1 GB of points) larger than L2; no flush"}
     if not args.no_e2e:
