@@ -1,6 +1,5 @@
 // Tensor-core (tcgen05 / TMEM) tile kernel for the fused LRNR / FastLRNR
 // residual + reverse-to-s sweep, FP32-grade accuracy via 3xTF32.
-// (Round 2: 16-neuron chunks with double-buffered P1 and Z in TMEM, see TM_P1.)
 //
 // Same math as the FMA tile kernel (pinn_v2.cuh); the two tile GEMMs of every
 // chunk run on the 5th-generation tensor cores:
@@ -34,10 +33,7 @@ namespace lrnr_b200 {
 namespace tc {
 
 constexpr int P = 128;    // points per tile (MMA M)
-#ifndef TC_KC
-#define TC_KC 16
-#endif
-constexpr int KC = TC_KC;  // neurons per chunk (phase-1 N, phase-2 K)
+constexpr int KC = 32;    // neurons per chunk (phase-1 N, phase-2 K)
 constexpr int RP = 32;    // max padded rank
 #ifndef TC_NWE
 #define TC_NWE 16
@@ -50,30 +46,19 @@ constexpr int NWE = TC_NWE;  // epilogue warps: lane quarter = warp % 4, neuron 
 constexpr int ISSUER = NWE;       // phase-1 issuer
 constexpr int ISSUER2 = NWE + 1;  // phase-2 issuer
 constexpr int NT = 32 * (NWE + 2);
-constexpr int NG = KC / (NWE / 4);   // neurons per thread in a chunk's epilogue
-constexpr int NGR = RP / (NWE / 4);  // ranks per thread at the transition ends (Y / T sums)
+constexpr int NG = KC / (NWE / 4);  // neurons (epilogue) / ranks (sums) per thread
 // Units (single tiles) after each CTA's first are claimed from a global counter:
 // SMs run at slightly different speeds (a static split spread by up to 5 %).
 #define TC_MMA_SS umma::mma_ss_w
 #define TC_MMA_TS umma::mma_ts_w
 #define TC_COMMIT umma::mma_commit_w
-// TMEM (512 columns): two P1 buffers [4 slots x KC], two Z / G buffers [hi 4 x KC | lo 4 x KC]
-// and the Y / T accumulators [4 slots x RP]. Chunk q uses buffer q & 1 of P1 and Z, so the
-// epilogue of chunk q never waits for the phase-2 MMAs of chunk q - 1, and phase 1 of chunk
-// q + 1 runs while the epilogue of chunk q does its math.
-constexpr int TM_P1 = 0;       // + buffer * 4 * KC
-constexpr int TM_Z = 8 * KC;   // + buffer * 8 * KC (hi), + 4 * KC (lo)
-constexpr int TM_Y = 24 * KC;
-static_assert(TM_Y + 4 * RP <= 512, "TMEM budget");
+constexpr int TM_P1 = 0, TM_ZH = 128, TM_ZL = 256, TM_Y = 384;
 // Phase-2 products of YACC consecutive chunks accumulate in TMEM before the
 // epilogue reads them into the FP32 running sum (the tensor-core accumulator
 // truncates: 1 chunk = 12 MMAs keeps it at ~3e-6 on c2, 2 chunks ~6e-6, the
 // full K = 256 reached 1.2e-4). Halves the TMEM load round trips of Y.
-#ifndef TC_DEV_1X
-#define TC_DEV_1X 0
-#endif
 #ifndef TC_YACC
-#define TC_YACC (64 / TC_KC)
+#define TC_YACC 2
 #endif
 constexpr int YACC = TC_YACC;
 
@@ -104,9 +89,9 @@ constexpr int SY_TILE = P * RP;               // one canonical K-major tile (row
 constexpr int OFF_SY = 0;                     // [c][hi/lo] tiles: 8 x 4096 floats = 128 KB
 constexpr int BUF = 4 * KC * RP + KC + 32;    // factor chunk (max): 4 canonical 32x32 tiles + bias
 #ifndef TC_NBUF
-#define TC_NBUF 4
+#define TC_NBUF 3
 #endif
-constexpr int NBUF = TC_NBUF;                 // factor-chunk ring (slot of chunk q refilled once P2(q) is done)
+constexpr int NBUF = TC_NBUF;                 // factor-chunk ring (NBUF - 1 chunks in flight)
 constexpr int OFF_B0 = OFF_SY + 8 * SY_TILE;
 constexpr int OFF_RED = OFF_B0 + NBUF * BUF;  // [P][RP] + P (loss) + [16][RP] partials
 constexpr int RPS = RP + 1;                   // red[] point stride (odd: conflict-free column writes)
@@ -195,33 +180,37 @@ __device__ __forceinline__ void reduce_points(float* red, float* acc, int off, i
     }
 }
 
-__device__ __forceinline__ void tld(uint32_t taddr, float (&v)[4]) { umma::tmem_ld4(taddr, v); }
-__device__ __forceinline__ void tst(uint32_t taddr, const float (&v)[4]) { umma::tmem_st4(taddr, v); }
 __device__ __forceinline__ void tld(uint32_t taddr, float (&v)[8]) { umma::tmem_ld8(taddr, v); }
 __device__ __forceinline__ void tld(uint32_t taddr, float (&v)[16]) { umma::tmem_ld16(taddr, v); }
 __device__ __forceinline__ void tst(uint32_t taddr, const float (&v)[8]) { umma::tmem_st8(taddr, v); }
 __device__ __forceinline__ void tst(uint32_t taddr, const float (&v)[16]) { umma::tmem_st16(taddr, v); }
 
-// acc[c][n] += TMEM[taddr + c * 32 + n] (a completed group of phase-2 products),
+// acc[c][n] += TMEM[taddr + c * 32 + n] (the previous chunk's phase-2 product),
 // one load batch, one wait
-__device__ __forceinline__ void add_y(uint32_t taddr, float (&acc)[4][NGR]) {
-    float v[4][NGR];
+__device__ __forceinline__ void add_y(uint32_t taddr, float (&acc)[4][NG]) {
+    float v[4][NG];
 #pragma unroll
     for (int c = 0; c < 4; ++c) tld(taddr + c * 32, v[c]);
     umma::tmem_ld_wait();
 #pragma unroll
     for (int c = 0; c < 4; ++c)
 #pragma unroll
-        for (int n = 0; n < NGR; ++n) acc[c][n] += v[c][n];
+        for (int n = 0; n < NG; ++n) acc[c][n] += v[c][n];
 }
 
-// P1 columns of this thread (4 slots x NG neurons of the chunk), one batch, one wait
-__device__ __forceinline__ void ld_p1(uint32_t taddr, float (&v)[4][NG]) {
+// P1 columns of this thread (4 slots x NG neurons) in two column halves: the first
+// half is waited for here, the second is in flight while the first half's math runs
+// (the caller waits before touching column NG / 2)
+__device__ __forceinline__ void ld_p1_halves(uint32_t taddr, float (&v)[4][NG]) {
 #pragma unroll
     for (int c = 0; c < 4; ++c)
 #pragma unroll
-        for (int h = 0; h < NG; h += 4) umma::tmem_ld4(taddr + c * KC + h, v[c] + h);
+        for (int h = 0; h < NG / 2; h += 4) umma::tmem_ld4(taddr + c * KC + h, v[c] + h);
     umma::tmem_ld_wait();
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int h = NG / 2; h < NG; h += 4) umma::tmem_ld4(taddr + c * KC + h, v[c] + h);
 }
 
 // stored pre-activation A of (neuron k, point p) inside its chunk: [k][p][4]
@@ -243,16 +232,14 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
     float* red = sm + OFF_RED;
     float* acc = sm + OFF_ACC;
     __shared__ __align__(8) uint64_t wbar[NBUF];
-    // per buffer parity b = q & 1 of chunk q: P1 / P2 complete (tcgen05.commit), P1 read / Z
-    // written (one arrival per epilogue warp).  A waiter never lags a barrier by two phases:
-    // chunk q + 2 reuses barrier b only after the waits of chunk q are done.
-    __shared__ __align__(8) uint64_t mbar1[2], mbar2[2], p1free[2], zready[2];
+    __shared__ __align__(8) uint64_t mbar1, mbar2;
+    __shared__ __align__(8) uint64_t p1free, zready;  // epilogue -> issuer (one arrive per epilogue warp)
     __shared__ uint32_t tmem_base;
     __shared__ int64_t next_unit;
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const int quarter = warp & 3, half = warp >> 2;  // half: neuron / rank group (NG / NGR) of the warp
+    const int quarter = warp & 3, half = warp >> 2;  // half: neuron / rank group of NG
     const int p = quarter * 32 + lane;  // the point (TMEM lane) this thread serves in epilogues
     const int R1 = 1 + net.rtotal;
     const int L = net.L;
@@ -262,18 +249,15 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
 #ifdef TC_CTA_TIMES
     unsigned long long _t_start;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t_start));
-    int64_t total_tiles = 0;
 #endif
     for (int k = tid; k < R1; k += NT) acc[k] = 0.f;
     if (warp == 0) umma::tmem_alloc<512>(&tmem_base);
     if (tid == 0) {
         for (int i = 0; i < NBUF; ++i) umma::mbar_init(&wbar[i], 1);
-        for (int b = 0; b < 2; ++b) {
-            umma::mbar_init(&mbar1[b], 1);
-            umma::mbar_init(&mbar2[b], 1);
-            umma::mbar_init(&p1free[b], NWE);
-            umma::mbar_init(&zready[b], NWE);
-        }
+        umma::mbar_init(&mbar1, 1);
+        umma::mbar_init(&mbar2, 1);
+        umma::mbar_init(&p1free, NWE);
+        umma::mbar_init(&zready, NWE);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     umma::fence_before();
@@ -281,68 +265,79 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
     umma::fence_after();
     const uint32_t tbase = tmem_base;
     const uint32_t tlane = tbase + (static_cast<uint32_t>(quarter * 32) << 16);
-    // epilogue warp -> issuer hand-off (after its warp-collective tcgen05 ld / st waits)
+    uint32_t ph1 = 0, ph2 = 0;  // mbarrier phase counters (epilogue warps)
+    uint32_t phf = 0, phz = 0;  // p1free / zready phase counters (issuer warp)
+    // epilogue warp -> issuer handshakes (after warp-collective tcgen05 ld / st waits)
     auto signal = [&](uint64_t* bar) {
         umma::fence_before();
         __syncwarp();
         if (lane == 0) umma::mbar_arrive(bar);
     };
-    // wait for chunk k's phase of a per-parity barrier pair
-    auto wait_chunk = [&](uint64_t* bars, int64_t k) {
-        umma::mbar_wait(&bars[k & 1], static_cast<uint32_t>((k >> 1) & 1));
+    auto await = [&](uint64_t* bar, uint32_t& ph) {
+        umma::mbar_wait(bar, ph & 1);
+        ++ph;
         umma::fence_after();
     };
 
     // ---- factor-chunk pipeline (TMA bulk copies) ----
-    // every tile runs the same chunk schedule, so the ring is refilled without knowing the CTA's
-    // tile count; the chunks prefetched past the last one are drained at exit
+    // every tile runs the same chunk schedule, so the ring is refilled without knowing the
+    // CTA's tile count; the NBUF - 1 copies in flight past the last chunk are drained at exit
+    const int64_t total_chunks = INT64_MAX;
+#ifdef TC_CTA_TIMES
+    int64_t total_tiles = 0;
+#endif
+    int64_t q = 0;
     auto issue = [&](int64_t qq) {
-        const int e = static_cast<int>(qq % net.sched_len);
-        const int b = static_cast<int>(qq % NBUF);
-        v2::fence_proxy_async();
-        v2::mbar_expect_tx(&wbar[b], static_cast<uint32_t>(net.sched_bytes[e]));
-        v2::bulk_g2s(sm + OFF_B0 + b * BUF, net.blocks + net.sched_off[e], static_cast<uint32_t>(net.sched_bytes[e]),
-                     &wbar[b]);
+        if (qq < total_chunks) {
+            const int e = static_cast<int>(qq % net.sched_len);
+            const int b = static_cast<int>(qq % NBUF);
+            v2::fence_proxy_async();
+            v2::mbar_expect_tx(&wbar[b], static_cast<uint32_t>(net.sched_bytes[e]));
+            v2::bulk_g2s(sm + OFF_B0 + b * BUF, net.blocks + net.sched_off[e], static_cast<uint32_t>(net.sched_bytes[e]),
+                         &wbar[b]);
+        }
     };
-    if (tid == 0)
-        for (int i = 0; i < NBUF; ++i) issue(i);
-    auto wait_slot = [&](int64_t qq) {
-        umma::mbar_wait(&wbar[qq % NBUF], static_cast<uint32_t>((qq / NBUF) & 1));
+    if (tid == 0) {
+        for (int i = 0; i + 1 < NBUF; ++i) issue(i);
+    }
+    TC_T0();
+    auto wait_mma1 = [&]() {
+        umma::mbar_wait(&mbar1, ph1 & 1);
+        ++ph1;
         umma::fence_after();
     };
-    auto slot = [&](int64_t qq) { return static_cast<int>(qq % NBUF) * BUF; };
-    TC_T0();
+    auto wait_mma2 = [&]() {
+        umma::mbar_wait(&mbar2, ph2 & 1);
+        ++ph2;
+        umma::fence_after();
+    };
     const uint32_t id_p1 = umma::idesc_tf32(P, KC);
     // descriptor low words (start >> 4 | LBO >> 4 << 16); advancing the start by
     // a float offset f adds f >> 2.  Common high word: SBO = 128 B, version 1.
     const uint32_t dhi = umma::desc_hi(128);
-    const uint32_t lsy = umma::desc_lo(sm + OFF_SY, (P / 8) * 128);    // SY / ST tiles (rows = P)
-    const uint32_t lbk = umma::desc_lo(sm + OFF_B0, (KC / 8) * 128);   // factor tiles with KC rows
-    const uint32_t lb16 = umma::desc_lo(sm + OFF_B0, (16 / 8) * 128);  // factor tiles with 16 / 32 rows
-    const uint32_t lb32 = umma::desc_lo(sm + OFF_B0, (32 / 8) * 128);
-    // phase 1 (issuer warp, converged): P1[b] = S B (3xTF32), S = SY / ST from smem,
+    const uint32_t lsy = umma::desc_lo(sm + OFF_SY, (P / 8) * 128);     // SY / ST tiles (rows = P)
+    const uint32_t lb32 = umma::desc_lo(sm + OFF_B0, (KC / 8) * 128);   // factor tiles with 32 rows
+    const uint32_t lb16 = umma::desc_lo(sm + OFF_B0, (16 / 8) * 128);   // factor tiles with 16 rows
+    // phase 1 (issuer warp, converged): P1_c = S_c B (3xTF32), S = SY / ST from smem,
     // B = factor tiles at float offset bo (hi) / bo + KC * rk (lo) of the ring slot
-    auto mma_p1 = [&](int bo, int rk, int b) {
+    auto mma_p1 = [&](int bo, int rk) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            const uint32_t d = tbase + TM_P1 + b * 4 * KC + c * KC;
+            const uint32_t d = tbase + TM_P1 + c * KC;
             const uint32_t ah0 = lsy + ((2 * c) * SY_TILE >> 2), al0 = lsy + ((2 * c + 1) * SY_TILE >> 2);
-            const uint32_t bh0 = lbk + (bo >> 2), bl0 = lbk + ((bo + KC * rk) >> 2);
+            const uint32_t bh0 = lb32 + (bo >> 2), bl0 = lb32 + ((bo + KC * rk) >> 2);
             for (int s = 0; s < rk / 8; ++s) {
                 const uint32_t sa = s * (2 * (P / 8) * 32 >> 2), sb = s * (2 * (KC / 8) * 32 >> 2);
                 TC_MMA_SS(d, ah0 + sa, bh0 + sb, dhi, id_p1, s > 0);
-#if !(TC_DEV_1X & 1)  // timing knob (dev aid, results wrong when set): hi * hi only
                 TC_MMA_SS(d, ah0 + sa, bl0 + sb, dhi, id_p1, 1);
                 TC_MMA_SS(d, al0 + sa, bh0 + sb, dhi, id_p1, 1);
-#endif
             }
         }
-        TC_COMMIT(&mbar1[b]);
+        TC_COMMIT(&mbar1);
     };
-    // phase 2 (issuer warp 2, converged): Y += Z[b] B (A from TMEM; a fresh accumulator
-    // at the start of every YACC-chunk group), B = factor tiles (rows rn) at float offset
-    // bo (hi) / bo + rn * KC (lo)
-    auto mma_p2 = [&](int bo, int rn, bool acc0, int b) {
+    // phase 2 (issuer warp 2, converged): Y_c = Z_c B (fresh accumulator, A from TMEM),
+    // B = factor tiles (rows rn) at float offset bo (hi) / bo + rn * KC (lo)
+    auto mma_p2 = [&](int bo, int rn, bool acc0) {
         const uint32_t id_p2 = umma::idesc_tf32(P, rn);
         const uint32_t lb = rn == 16 ? lb16 : lb32;
         const uint32_t bh0 = lb + (bo >> 2), bl0 = lb + ((bo + rn * KC) >> 2);
@@ -352,62 +347,19 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
             const uint32_t d = tbase + TM_Y + c * 32;
 #pragma unroll
             for (int s = 0; s < KC / 8; ++s) {
-                const uint32_t azh = tbase + TM_Z + b * 8 * KC + c * KC + s * 8, azl = azh + 4 * KC;
+                const uint32_t azh = tbase + TM_ZH + c * KC + s * 8, azl = tbase + TM_ZL + c * KC + s * 8;
                 TC_MMA_TS(d, azh, bh0 + s * sb, dhi, id_p2, (s > 0 || acc0) ? 1u : 0u);
-#if !(TC_DEV_1X & 2)
                 TC_MMA_TS(d, azh, bl0 + s * sb, dhi, id_p2, 1);
                 TC_MMA_TS(d, azl, bh0 + s * sb, dhi, id_p2, 1);
-#endif
             }
         }
-        TC_COMMIT(&mbar2[b]);
+        TC_COMMIT(&mbar2);
     };
-    // the issuers' side of one transition: phase 1 of chunk qq once the epilogue has read
-    // P1(qq - 2) out of the same buffer and the factor block has landed; phase 2 of chunk qq
-    // once the epilogue has written Z(qq)
-    auto issue_transition = [&](int64_t q0, int nc, int rk1, int bo2, int rn2) {
-        if (warp == ISSUER) {
-            for (int ch = 0; ch < nc; ++ch) {
-                const int64_t qq = q0 + ch;
-                if (qq >= 2) wait_chunk(p1free, qq - 2);
-                wait_slot(qq);
-                mma_p1(slot(qq), rk1, static_cast<int>(qq & 1));
-            }
-        } else if (warp == ISSUER2) {
-            for (int ch = 0; ch < nc; ++ch) {
-                const int64_t qq = q0 + ch;
-                wait_chunk(zready, qq);
-                mma_p2(slot(qq) + bo2, rn2, ch % YACC != 0, static_cast<int>(qq & 1));
-            }
-        }
-    };
-    // the epilogue's wait before writing Z(qq): buffer qq & 1 was last read by P2(qq - 2); at the
-    // start of a new YACC group the previous group's Y / T sum is read first (P2(qq - 1) done).
-    // Then the ring slot of chunk qq - 2 (P1 and P2 done) is refilled with chunk qq - 2 + NBUF.
-    auto before_z = [&](int64_t qq, int ch, float (&sum)[4][NGR]) {
-        if (ch % YACC == 0 && ch > 0) {
-            wait_chunk(mbar2, qq - 1);
-            add_y(tlane + TM_Y + half * NGR, sum);
-        } else if (qq >= 2) {
-            wait_chunk(mbar2, qq - 2);
-        }
-        if (tid == 0 && qq >= 2) issue(qq - 2 + NBUF);
-    };
-    auto store_z = [&](int64_t qq, float (&z)[4][NG]) {
-        const int b = static_cast<int>(qq & 1);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            float hi[NG], lo[NG];
-#pragma unroll
-            for (int n = 0; n < NG; ++n) umma::split_tf32(z[c][n], hi[n], lo[n]);
-            tst(tlane + TM_Z + b * 8 * KC + c * KC + half * NG, hi);
-            tst(tlane + TM_Z + b * 8 * KC + 4 * KC + c * KC + half * NG, lo);
-        }
-        umma::tmem_st_wait();
-        signal(&zready[b]);
+    auto wait_slot = [&](int64_t qq) {
+        umma::mbar_wait(&wbar[qq % NBUF], static_cast<uint32_t>((qq / NBUF) & 1));
+        umma::fence_after();
     };
 
-    int64_t q = 0;  // chunk counter over the CTA's lifetime (ring slot, TMEM buffer, barrier phases)
     // claims: the counter starts at all-ones (memset 0xff), so the first claim returns unit gridDim.x
     unsigned long long claim = 0;
     if (tid == 0) claim = atomicAdd(unit_ctr, 1ull) + 1ull + gridDim.x;
@@ -451,59 +403,100 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
 
             // ---------------- forward transitions ----------------
             for (int l = 0; l + 1 < L; ++l) {
-                const int rk = net.rk[l], rnn = net.rn[l + 1], nc = net.nc[l];
-                // Y = sum over YACC-chunk groups of fresh tensor-core accumulations, summed here in
-                // FP32 (the tensor-core accumulator truncates; ~64 neurons per group keeps that
-                // bias at the FP32 level)
-                float ysum[4][NGR];
+                const int rk = net.rk[l], rnn = net.rn[l + 1];
+                // Y = sum over chunks of fresh per-chunk tensor-core products, summed
+                // here in FP32 (the tensor-core accumulator truncates; one K = 32
+                // chunk per accumulator keeps that bias at the FP32 level)
+                float ysum[4][NG];
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
 #pragma unroll
-                    for (int n = 0; n < NGR; ++n) ysum[c][n] = 0.f;
+                    for (int n = 0; n < NG; ++n) ysum[c][n] = 0.f;
                 // factor block of chunk qq: UT_H | UT_L (KC x rk, rows KC) | bias (KC, padded 32) | VT_H | VT_L (rnn x KC)
-                issue_transition(q, nc, rk, 2 * KC * rk + 32, rnn);
-                if (warp < NWE) {
-                    for (int ch = 0; ch < nc; ++ch) {
-                        const int64_t qq = q + ch;
-                        const float* bias = sm + OFF_B0 + slot(qq) + 2 * KC * rk;
-                        float* Ast = ascr + net.aoff[l] + static_cast<int64_t>(ch) * (P * KC * 4);
+                auto fwd_p1 = [&](int64_t qq) {
+                    wait_slot(qq);
+                    mma_p1(static_cast<int>(qq % NBUF) * BUF, rk);
+                };
+                auto fwd_p2 = [&](int64_t qq, int ch) {
+                    mma_p2(static_cast<int>(qq % NBUF) * BUF + 2 * KC * rk + 32, rnn, ch % YACC != 0);
+                };
+                if (warp == ISSUER) fwd_p1(q);
+                // pipeline per chunk ch: [P1(ch) | P2(ch-1)] on the tensor core while the
+                // epilogue of ch computes the activation jet; Z / Y are touched only after
+                // P2(ch-1) completes.  P1(ch+1) is issued ahead of P2(ch).
+                for (int ch = 0; ch < net.nc[l]; ++ch, ++q) {
+                    const float* bias = sm + OFF_B0 + static_cast<int>(q % NBUF) * BUF + 2 * KC * rk;
+                    if (warp < NWE) {
                         TC_MARK(1);
-                        wait_chunk(mbar1, qq);
+                        wait_mma1();
                         TC_MARK(2);
-                        float a[4][NG];
-                        ld_p1(tlane + TM_P1 + static_cast<int>(qq & 1) * 4 * KC + half * NG, a);
-                        signal(&p1free[qq & 1]);  // P1(qq + 2) may now overwrite the buffer
-#pragma unroll
-                        for (int n = 0; n < NG; ++n) {
-                            const int k = half * NG + n;
-                            const float av = a[0][n] + bias[k], ax = a[1][n], at = a[2][n], aw = a[3][n];
-                            v2::st4(Ast + aidx(k, p), av, ax, at, aw);
-                            float sg, d1, d2, d3;
-                            act3f<ACT, FAST>(av, sg, d1, d2, d3);
-                            a[0][n] = sg;
-                            a[1][n] = d1 * ax;
-                            a[2][n] = d1 * at;
-                            a[3][n] = d2 * ax * ax + d1 * aw;
+                        // ring slot of chunk q-1 is free once P2(q-1) is complete
+                        if (ch == 0 && tid == 0) issue(q + NBUF - 1);
+                        {
+                            float a[4][NG];
+                            float* Ast = ascr + net.aoff[l] + static_cast<int64_t>(ch) * (P * KC * 4);
+                            // two column halves: the second half's TMEM read overlaps the first half's math
+                            ld_p1_halves(tlane + TM_P1 + half * NG, a);
+    #pragma unroll
+                            for (int n = 0; n < NG; ++n) {
+                                if (n == NG / 2) {
+                                    umma::tmem_ld_wait();
+                                    signal(&p1free);  // P1 may be overwritten by P1(ch+1)
+                                }
+                                const int k = half * NG + n;
+                                const float av = a[0][n] + bias[k], ax = a[1][n], at = a[2][n], aw = a[3][n];
+                                v2::st4(Ast + aidx(k, p), av, ax, at, aw);
+                                float sg, d1, d2, d3;
+                                act3f<ACT, FAST>(av, sg, d1, d2, d3);
+                                a[0][n] = sg;
+                                a[1][n] = d1 * ax;
+                                a[2][n] = d1 * at;
+                                a[3][n] = d2 * ax * ax + d1 * aw;
+                            }
+                            TC_MARK(3);
+                            if (ch > 0) {
+                                wait_mma2();  // P2(ch-1): Z free, its Y product ready
+                                if (tid == 0) issue(q + NBUF - 1);
+                                if (ch % YACC == 0) add_y(tlane + TM_Y + half * NG, ysum);  // a group of YACC chunks is complete
+                            }
+                            TC_MARK(0);
+    #pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                float hi[NG], lo[NG];
+    #pragma unroll
+                                for (int n = 0; n < NG; ++n) umma::split_tf32(a[c][n], hi[n], lo[n]);
+                                tst(tlane + TM_ZH + c * KC + half * NG, hi);
+                                tst(tlane + TM_ZL + c * KC + half * NG, lo);
+                            }
+                            umma::tmem_st_wait();
+                            signal(&zready);
                         }
-                        TC_MARK(3);
-                        before_z(qq, ch, ysum);
-                        TC_MARK(0);
-                        store_z(qq, a);
-                        TC_MARK(4);
                     }
+                    TC_MARK(4);
+                    if (warp == ISSUER) {
+                        TC_ISSUE_BEGIN();
+                        await(&p1free, phf);  // every chunk (keeps the phase count)
+                        if (ch + 1 < net.nc[l]) fwd_p1(q + 1);
+                        if (lane == 0) TC_ISSUE_END();
+                    }
+                    if (warp == ISSUER2) {
+                        await(&zready, phz);
+                        fwd_p2(q, ch);
+                    }
+                    TC_MARK(5);
                 }
-                q += nc;
                 // transition end: Y -> y_{l+1} (scratch), SY = s (.) y (smem hi / lo)
+                TC_MARK(0);
                 if (warp < NWE) {
-                    wait_chunk(mbar2, q - 1);  // the transition's last phase-2 product (in order: all)
+                    wait_mma2();
                     TC_MARK(5);
                     const double* sl = sv + net.soff[l + 1];
                     const int rtrue = net.r[l + 1];
-                    float (&y)[4][NGR] = ysum;
-                    add_y(tlane + TM_Y + half * NGR, y);
+                    float (&y)[4][NG] = ysum;
+                    add_y(tlane + TM_Y + half * NG, y);
 #pragma unroll
-                    for (int n4 = 0; n4 < NGR / 4; ++n4) {
-                        const int j0 = half * NGR + 4 * n4;
+                    for (int n4 = 0; n4 < NG / 4; ++n4) {
+                        const int j0 = half * NG + 4 * n4;
                         if (j0 < net.rk[l + 1]) {  // rk is a multiple of 8: a group of 4 is all in or all out
                             float sj[4];
 #pragma unroll
@@ -524,7 +517,6 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                 umma::fence_async_smem();
                 umma::fence_before();
                 __syncthreads();
-                umma::fence_after();
             }
 
             TC_MARK(6);
@@ -577,72 +569,105 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
             TC_MARK(7);
             // ---------------- reverse transitions ----------------
             for (int l = L - 2; l >= 0; --l) {
-                const int rkn = net.rk[l + 1], rnl = net.rn[l], nc = net.nc[l];
-                float tsum[4][NGR];
+                const int rkn = net.rk[l + 1], rnl = net.rn[l];
+                float tsum[4][NG];
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
 #pragma unroll
-                    for (int n = 0; n < NGR; ++n) tsum[c][n] = 0.f;
+                    for (int n = 0; n < NG; ++n) tsum[c][n] = 0.f;
                 // factor block of chunk qq: V_H | V_L (KC x rkn, rows KC) | UT_H | UT_L (rnl x KC)
-                issue_transition(q, nc, rkn, 2 * KC * rkn, rnl);
-                if (warp < NWE) {
-                    for (int ch = 0; ch < nc; ++ch) {
-                        const int64_t qq = q + ch;
+                auto bwd_p1 = [&](int64_t qq) {
+                    wait_slot(qq);
+                    mma_p1(static_cast<int>(qq % NBUF) * BUF, rkn);
+                };
+                auto bwd_p2 = [&](int64_t qq, int ch) {
+                    mma_p2(static_cast<int>(qq % NBUF) * BUF + 2 * KC * rkn, rnl, ch % YACC != 0);
+                };
+                if (warp == ISSUER) bwd_p1(q);
+                for (int ch = 0; ch < net.nc[l]; ++ch, ++q) {
+                    if (warp < NWE) {
                         // stored pre-activations of this chunk (in flight during the MMAs)
                         const float* Ast = ascr + net.aoff[l] + static_cast<int64_t>(ch) * (P * KC * 4);
                         float a[4][NG];
-#pragma unroll
+    #pragma unroll
                         for (int n = 0; n < NG; ++n) {
                             float a4[4];
                             v2::ld4(Ast + aidx(half * NG + n, p), a4);
-#pragma unroll
+    #pragma unroll
                             for (int c = 0; c < 4; ++c) a[c][n] = a4[c];
                         }
                         TC_MARK(9);
-                        wait_chunk(mbar1, qq);
+                        wait_mma1();
                         TC_MARK(10);
-                        float dz[4][NG];
-                        ld_p1(tlane + TM_P1 + static_cast<int>(qq & 1) * 4 * KC + half * NG, dz);
-                        signal(&p1free[qq & 1]);
-#pragma unroll
-                        for (int n = 0; n < NG; ++n) {
-                            const float av = a[0][n], ax = a[1][n], at = a[2][n], aw = a[3][n];
-                            const float g0 = dz[0][n], g1 = dz[1][n], g2 = dz[2][n], g3 = dz[3][n];
-                            float sg, d1, d2, d3;
-                            act3f<ACT, FAST>(av, sg, d1, d2, d3);
-                            dz[0][n] = g0 * d1 + g1 * d2 * ax + g2 * d2 * at + g3 * (d3 * ax * ax + d2 * aw);
-                            dz[1][n] = g1 * d1 + g3 * 2.f * d2 * ax;
-                            dz[2][n] = g2 * d1;
-                            dz[3][n] = g3 * d1;
+                        if (ch == 0 && tid == 0) issue(q + NBUF - 1);
+                        {
+                            float dz[4][NG];
+                            ld_p1_halves(tlane + TM_P1 + half * NG, dz);
+    #pragma unroll
+                            for (int n = 0; n < NG; ++n) {
+                                if (n == NG / 2) {
+                                    umma::tmem_ld_wait();
+                                    signal(&p1free);
+                                }
+                                const float av = a[0][n], ax = a[1][n], at = a[2][n], aw = a[3][n];
+                                const float g0 = dz[0][n], g1 = dz[1][n], g2 = dz[2][n], g3 = dz[3][n];
+                                float sg, d1, d2, d3;
+                                act3f<ACT, FAST>(av, sg, d1, d2, d3);
+                                dz[0][n] = g0 * d1 + g1 * d2 * ax + g2 * d2 * at + g3 * (d3 * ax * ax + d2 * aw);
+                                dz[1][n] = g1 * d1 + g3 * 2.f * d2 * ax;
+                                dz[2][n] = g2 * d1;
+                                dz[3][n] = g3 * d1;
+                            }
+                            TC_MARK(11);
+                            if (ch > 0) {
+                                wait_mma2();  // P2(ch-1): G free, its T product ready
+                                if (tid == 0) issue(q + NBUF - 1);
+                                if (ch % YACC == 0) add_y(tlane + TM_Y + half * NG, tsum);
+                            }
+                            TC_MARK(8);
+    #pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                float hi[NG], lo[NG];
+    #pragma unroll
+                                for (int n = 0; n < NG; ++n) umma::split_tf32(dz[c][n], hi[n], lo[n]);
+                                tst(tlane + TM_ZH + c * KC + half * NG, hi);
+                                tst(tlane + TM_ZL + c * KC + half * NG, lo);
+                            }
+                            umma::tmem_st_wait();
+                            signal(&zready);
                         }
-                        TC_MARK(11);
-                        before_z(qq, ch, tsum);
-                        TC_MARK(8);
-                        store_z(qq, dz);
-                        TC_MARK(12);
+                    }
+                    TC_MARK(12);
+                    if (warp == ISSUER) {
+                        await(&p1free, phf);  // every chunk (keeps the phase count)
+                        if (ch + 1 < net.nc[l]) bwd_p1(q + 1);
+                    }
+                    if (warp == ISSUER2) {
+                        await(&zready, phz);
+                        bwd_p2(q, ch);
                     }
                 }
-                q += nc;
                 // transition end: T -> dL/ds_l partials, ST = s_l (.) T (smem hi / lo)
+                TC_MARK(8);
                 if (warp < NWE) {
                     const double* sl = sv + net.soff[l];
                     const int rtrue = net.r[l];
                     // this thread's y_l (scratch, usually an L2 / HBM round trip): all loads issued
                     // together and before the wait for the last phase-2 product
-                    float4 yv[NGR];
+                    float4 yv[NG];
 #pragma unroll
-                    for (int n = 0; n < NGR; ++n) {
-                        const int j = half * NGR + n;
+                    for (int n = 0; n < NG; ++n) {
+                        const int j = half * NG + n;
                         yv[n] = j < rtrue ? *reinterpret_cast<const float4*>(scr + net.yoff[l] + (p * rtrue + j) * 4)
                                           : make_float4(0.f, 0.f, 0.f, 0.f);
                     }
-                    wait_chunk(mbar2, q - 1);
+                    wait_mma2();
                     TC_MARK(13);
-                    float (&tt)[4][NGR] = tsum;
-                    add_y(tlane + TM_Y + half * NGR, tt);
+                    float (&tt)[4][NG] = tsum;
+                    add_y(tlane + TM_Y + half * NG, tt);
 #pragma unroll
-                    for (int n4 = 0; n4 < NGR / 4; ++n4) {
-                        const int j0 = half * NGR + 4 * n4;
+                    for (int n4 = 0; n4 < NG / 4; ++n4) {
+                        const int j0 = half * NG + 4 * n4;
                         if (j0 < net.rk[l]) {  // rk is a multiple of 8
                             float sj[4];
 #pragma unroll
@@ -668,7 +693,6 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
                 umma::fence_async_smem();
                 umma::fence_before();
                 __syncthreads();
-                umma::fence_after();
                 reduce_points(red, acc, net.soff[l], net.r[l], tid);
                 __syncthreads();
                 TC_MARK(14);
@@ -685,9 +709,8 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
         __syncthreads();
         unit = next_unit;
     }
-    // the ring copies in flight past the last chunk (chunks q .. q + NBUF - 3)
     if (tid == 0)
-        for (int64_t qq = q; qq < q + NBUF - 2; ++qq) wait_slot(qq);
+        for (int64_t qq = q; qq < q + NBUF - 1; ++qq) wait_slot(qq);  // prefetches past the last chunk
     TC_FLUSH();
     umma::fence_before();
     __syncthreads();
