@@ -112,10 +112,9 @@ struct Model {
     struct TC {
         bool ok = false;
         std::vector<int> rk, rn, nc, yoff;
-        std::vector<int64_t> aoff;
-        int64_t astride = 0;
+        std::vector<float> isU, isV, muU, muV;
         int ystride = 0;
-        std::vector<float> blocks;
+        std::vector<unsigned char> blocks;  // fp16 hi / lo factor tiles + FP32 biases
         std::vector<int64_t> sched_off;
         std::vector<int> sched_cnt;
         DevBuf dblocks, dsched_off, dsched_bytes;

@@ -6,6 +6,7 @@
 // solve.cu, the meta step in meta.cu, the FastLRNR construction in eim.cu and
 // the narrow-network kernel's host side in fast_launch.cu.
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <climits>
@@ -233,25 +234,16 @@ void build_v2(Model& m, bool meta) {
     v.ok = true;
 }
 
-// tf32 round-to-nearest (ties away), as cvt.rna.tf32.f32
-static float tf32_rna(float x) {
-    uint32_t u;
-    std::memcpy(&u, &x, 4);
-    if ((u & 0x7F800000u) != 0x7F800000u) u = (u + 0x1000u) & 0xFFFFE000u;
-    float r;
-    std::memcpy(&r, &u, 4);
-    return r;
-}
-
-// Tensor-core layout (pinn_tc.cuh): per transition l and chunk of 32 neurons,
-//   forward block  [U_H | U_L (B: N = 32 neurons x K = rk_l, K-major canonical) |
-//                   bias (32) | VT_H | VT_L (B: N = rn_{l+1} x K = 32 neurons)]
-//   backward block [V_H | V_L (N = 32 neurons x K = rk_{l+1}) | UT_H | UT_L (N = rn_l x K = 32)]
-// hi = tf32(x), lo = x - hi (3xTF32).
+// Tensor-core layout (pinn_tc.cuh), FP16 two-term split of FP32 factors: x S = hi + lo,
+// hi = fp16(x S), lo = fp16(x S - hi), S = 2^e per matrix (max |x| S < 2^15).  Per
+// transition l and chunk of 32 neurons (16-bit K-major canonical tiles, hi then lo):
+//   forward block [UT (N = 32 neurons x K = rk_l) | bias (32 floats) | V (N = rn_{l+1} x K = 32)]
+//   reverse block [UT | bias | VT (N = 32 neurons x K = rk_{l+1}) | U (N = rn_l x K = 32)]
+// plus, per layer, 1 / S and the max row 2-norm of U_l and V_l (the kernel's Z / G bounds).
 void build_tc(Model& m) {
     auto& v = m.tc;
     v = Model::TC{};
-    if (m.dtype != LRNR_F32) return;
+    if (m.dtype != LRNR_F32 || m.L < 2) return;
     const int L = m.L;
     const int KC = tc::KC;
     for (int l = 0; l < L; ++l)
@@ -259,65 +251,102 @@ void build_tc(Model& m) {
     v.rk.resize(L);
     v.rn.resize(L);
     for (int l = 0; l < L; ++l) {
-        v.rk[l] = (m.r[l] + 7) & ~7;
+        v.rk[l] = (m.r[l] + 15) & ~15;
         v.rn[l] = m.r[l] <= 16 ? 16 : 32;
     }
     v.nc.assign(L, 0);
     v.yoff.assign(L, 0);
-    v.aoff.assign(L, 0);
+    v.isU.assign(L, 1.f);
+    v.isV.assign(L, 1.f);
+    v.muU.assign(L, 0.f);
+    v.muV.assign(L, 0.f);
     int yo = 0;
     for (int l = 0; l < L; ++l) {
         v.yoff[l] = yo;
         yo += tc::P * m.r[l] * 4;
     }
     v.ystride = yo;
-    int64_t ao = 0;
-    for (int l = 0; l + 1 < L; ++l) {
-        v.nc[l] = (m.M[l + 1] + KC - 1) / KC;
-        v.aoff[l] = ao;
-        ao += static_cast<int64_t>(v.nc[l]) * tc::P * KC * 4;
-    }
-    v.astride = ao;
+    for (int l = 0; l + 1 < L; ++l) v.nc[l] = (m.M[l + 1] + KC - 1) / KC;
     std::vector<std::vector<int64_t>> foff(L), boff(L);
     std::vector<int> fcnt(L), bcnt(L);
-    auto put = [](float* hi, float* lo, int off, double x) {
-        const float f = static_cast<float>(x);
-        const float h = tf32_rna(f);
-        hi[off] = h;
-        lo[off] = f - h;
+    // fp16 hi / lo of x * S at byte offset o of the hi tile (lo tile at hi + lo_off)
+    auto put = [](unsigned char* hi, int lo_off, int o, double x, float S) {
+        const float f = static_cast<float>(x) * S;
+        const __half hh = __float2half_rn(f);
+        const __half ll = __float2half_rn(f - __half2float(hh));
+        std::memcpy(hi + o, &hh, 2);
+        std::memcpy(hi + lo_off + o, &ll, 2);
+    };
+    auto pow2_for = [](double amax) {  // S = 2^e with amax * S < 2^15
+        if (!(amax > 0.0) || !std::isfinite(amax)) return 1.f;
+        int e;
+        std::frexp(amax, &e);  // amax < 2^e
+        return static_cast<float>(std::ldexp(1.0, 14 - e));
     };
     for (int l = 0; l + 1 < L; ++l) {
         const int rl = m.r[l], rn = m.r[l + 1], M = m.M[l + 1];
         const int rkl = v.rk[l], rkn = v.rk[l + 1], rnl = v.rn[l], rnn = v.rn[l + 1];
         const double* rows = m.packed.data() + m.off_trans[l];
-        auto U = [&](int k, int j) { return (k < M && j < rl) ? rows[static_cast<size_t>(k) * m.trow[l] + j] : 0.0; };
-        auto V = [&](int k, int j) { return (k < M && j < rn) ? rows[static_cast<size_t>(k) * m.trow[l] + rl + j] : 0.0; };
+        auto U = [&](int k, int j) {
+            return (k < M && j < rl) ? static_cast<double>(static_cast<float>(rows[static_cast<size_t>(k) * m.trow[l] + j]))
+                                     : 0.0;
+        };
+        auto V = [&](int k, int j) {
+            return (k < M && j < rn)
+                       ? static_cast<double>(static_cast<float>(rows[static_cast<size_t>(k) * m.trow[l] + rl + j]))
+                       : 0.0;
+        };
         auto B = [&](int k) { return k < M ? rows[static_cast<size_t>(k) * m.trow[l] + rl + rn] : 0.0; };
-        const int nf = 2 * KC * rkl + 32 + 2 * rnn * KC;
-        const int nb = 2 * KC * rkn + 2 * rnl * KC;
+        double umax = 0.0, vmax = 0.0, un = 0.0, vn = 0.0;
+        for (int k = 0; k < M; ++k) {
+            double su = 0.0, svv = 0.0;
+            for (int j = 0; j < rl; ++j) {
+                umax = std::max(umax, std::fabs(U(k, j)));
+                su += U(k, j) * U(k, j);
+            }
+            for (int j = 0; j < rn; ++j) {
+                vmax = std::max(vmax, std::fabs(V(k, j)));
+                svv += V(k, j) * V(k, j);
+            }
+            un = std::max(un, su);
+            vn = std::max(vn, svv);
+        }
+        const float SU = pow2_for(umax), SV = pow2_for(vmax);
+        v.isU[l] = 1.f / SU;
+        v.isV[l] = 1.f / SV;
+        // bounds are used as upper bounds: round the norms up a little
+        v.muU[l] = static_cast<float>(std::sqrt(un) * (1.0 + 1e-6));
+        v.muV[l] = static_cast<float>(std::sqrt(vn) * (1.0 + 1e-6));
+        const int ut = 4 * KC * rkl;                 // UT hi + lo bytes
+        const int nf = ut + 4 * KC + 4 * rnn * KC;   // forward block bytes
+        const int nb = ut + 4 * KC + 4 * KC * rkn + 4 * rnl * KC;
         fcnt[l] = nf;
         bcnt[l] = nb;
         for (int c = 0; c < v.nc[l]; ++c) {
             const int k0 = c * KC;
-            size_t o = v.blocks.size();
-            foff[l].push_back(static_cast<int64_t>(o));
-            v.blocks.resize(o + nf, 0.f);
-            float* f = v.blocks.data() + o;
-            float *UH = f, *UL = f + KC * rkl, *bias = UL + KC * rkl, *VTH = bias + 32, *VTL = VTH + rnn * KC;
-            for (int n = 0; n < KC; ++n)
-                for (int j = 0; j < rkl; ++j) put(UH, UL, umma::kmaj_off(n, j, KC), U(k0 + n, j));
-            for (int n = 0; n < KC; ++n) bias[n] = static_cast<float>(B(k0 + n));
-            for (int j = 0; j < rnn; ++j)
-                for (int n = 0; n < KC; ++n) put(VTH, VTL, umma::kmaj_off(j, n, rnn), V(k0 + n, j));
-            o = v.blocks.size();
-            boff[l].push_back(static_cast<int64_t>(o));
-            v.blocks.resize(o + nb, 0.f);
-            float* bb = v.blocks.data() + o;
-            float *VH = bb, *VL = bb + KC * rkn, *UTH = VL + KC * rkn, *UTL = UTH + rnl * KC;
-            for (int n = 0; n < KC; ++n)
-                for (int j = 0; j < rkn; ++j) put(VH, VL, umma::kmaj_off(n, j, KC), V(k0 + n, j));
-            for (int j = 0; j < rnl; ++j)
-                for (int n = 0; n < KC; ++n) put(UTH, UTL, umma::kmaj_off(j, n, rnl), U(k0 + n, j));
+            for (int dir = 0; dir < 2; ++dir) {
+                size_t o = v.blocks.size();
+                (dir == 0 ? foff : boff)[l].push_back(static_cast<int64_t>(o));
+                v.blocks.resize(o + (dir == 0 ? nf : nb), 0);
+                unsigned char* f = v.blocks.data() + o;
+                for (int n = 0; n < KC; ++n)
+                    for (int j = 0; j < rkl; ++j) put(f, 2 * KC * rkl, umma::kmaj16_off(n, j, KC), U(k0 + n, j), SU);
+                float* bias = reinterpret_cast<float*>(f + ut);
+                for (int n = 0; n < KC; ++n) bias[n] = static_cast<float>(B(k0 + n));
+                unsigned char* g = f + ut + 4 * KC;
+                if (dir == 0) {
+                    for (int j = 0; j < rnn; ++j)
+                        for (int n = 0; n < KC; ++n)
+                            put(g, 2 * rnn * KC, umma::kmaj16_off(j, n, rnn), V(k0 + n, j), SV);
+                } else {
+                    for (int n = 0; n < KC; ++n)
+                        for (int j = 0; j < rkn; ++j) put(g, 2 * KC * rkn, umma::kmaj16_off(n, j, KC), V(k0 + n, j), SV);
+                    unsigned char* uu = g + 4 * KC * rkn;
+                    for (int j = 0; j < rnl; ++j)
+                        for (int n = 0; n < KC; ++n)
+                            put(uu, 2 * rnl * KC, umma::kmaj16_off(j, n, rnl), U(k0 + n, j), SU);
+                }
+            }
         }
     }
     for (int l = 0; l + 1 < L; ++l)
@@ -330,16 +359,14 @@ void build_tc(Model& m) {
             v.sched_off.push_back(boff[l][c]);
             v.sched_cnt.push_back(bcnt[l]);
         }
-    v.dblocks.ensure(std::max<size_t>(v.blocks.size(), 8) * 4);
-    if (!v.blocks.empty()) CK(cudaMemcpy(v.dblocks.p, v.blocks.data(), v.blocks.size() * 4, cudaMemcpyHostToDevice));
+    v.dblocks.ensure(std::max<size_t>(v.blocks.size(), 16));
+    if (!v.blocks.empty()) CK(cudaMemcpy(v.dblocks.p, v.blocks.data(), v.blocks.size(), cudaMemcpyHostToDevice));
     const size_t ns = std::max<size_t>(v.sched_off.size(), 1);
-    std::vector<int> bytes(v.sched_cnt.size());
-    for (size_t i = 0; i < bytes.size(); ++i) bytes[i] = v.sched_cnt[i] * 4;
     v.dsched_off.ensure(ns * sizeof(int64_t));
     v.dsched_bytes.ensure(ns * sizeof(int));
     if (!v.sched_off.empty()) {
         CK(cudaMemcpy(v.dsched_off.p, v.sched_off.data(), v.sched_off.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(v.dsched_bytes.p, bytes.data(), bytes.size() * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(v.dsched_bytes.p, v.sched_cnt.data(), v.sched_cnt.size() * sizeof(int), cudaMemcpyHostToDevice));
     }
     v.ok = true;
 }
@@ -361,7 +388,7 @@ void launch_tc(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
     const int64_t n_inst = ctx->n_inst, n_per = ctx->n_per;
     const int R1 = 1 + m.rtotal;
     if (R1 > 1024) throw InvalidArg("tensor-core path supports r_total < 1024");
-    const size_t smem = static_cast<size_t>(tc::SMEM_FLOATS) * sizeof(float);
+    const size_t smem = static_cast<size_t>(tc::SMEM_BYTES);
     auto kern = tc::pinn_tc_kernel<ACT, FAST>;
     ctx->unit_ctr.ensure(sizeof(unsigned long long));
     CK(cudaMemsetAsync(ctx->unit_ctr.p, 0xff, sizeof(unsigned long long), ctx->stream));
@@ -380,9 +407,8 @@ void launch_tc(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
     g.n_units = static_cast<int64_t>(g.units_per_inst) * n_inst;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_grid, g.n_units)));
     ctx->scratch.ensure(static_cast<size_t>(grid) * v.ystride * sizeof(float) + 64);
-    ctx->ascratch.ensure(static_cast<size_t>(grid) * v.astride * sizeof(float) + 64);
     ensure_part<float>(ctx, n_inst, g.units_per_inst, R1);
-    tc::NetTC<> net{};
+    tc::NetTC net{};
     net.L = m.L;
     for (int l = 0; l <= m.L; ++l) {
         net.M[l] = m.M[l];
@@ -394,12 +420,15 @@ void launch_tc(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
         net.rn[l] = v.rn[l];
         net.nc[l] = v.nc[l];
         net.yoff[l] = v.yoff[l];
-        net.aoff[l] = v.aoff[l];
+        net.isU[l] = v.isU[l];
+        net.isV[l] = v.isV[l];
+        net.muU[l] = v.muU[l];
+        net.muV[l] = v.muV[l];
     }
+    net.c3 = ACT == 1 ? 1.f : 2.f;
     net.ystride = v.ystride;
-    net.astride = v.astride;
     net.rtotal = m.rtotal;
-    net.blocks = v.dblocks.as<float>();
+    net.blocks = v.dblocks.as<unsigned char>();
     net.sched_off = v.dsched_off.as<int64_t>();
     net.sched_bytes = v.dsched_bytes.as<int>();
     net.sched_len = static_cast<int>(v.sched_off.size());
@@ -407,8 +436,7 @@ void launch_tc(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
     net.V0 = base + m.off_V0;
     net.ulast = base + m.off_ulast;
     kern<<<grid, tc::NT, smem, ctx->stream>>>(net, g, ctx->pts, s_dev, mu_dev, static_cast<float>(w),
-                                              ctx->scratch.as<float>(), ctx->ascratch.as<float>(),
-                                              ctx->part.as<float>(), bad_word(ctx, m),
+                                              ctx->scratch.as<float>(), ctx->part.as<float>(), bad_word(ctx, m),
                                               ctx->unit_ctr.as<unsigned long long>());
     CK(cudaGetLastError());
     reduce_units<float>(ctx, n_inst, g.units_per_inst, R1, dev_out);

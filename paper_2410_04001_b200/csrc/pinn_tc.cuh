@@ -1,25 +1,32 @@
 // Tensor-core (tcgen05 / TMEM) tile kernel for the fused LRNR / FastLRNR
-// residual + reverse-to-s sweep, FP32-grade accuracy via 3xTF32.
+// residual + reverse-to-s sweep, FP32-grade accuracy from an FP16 two-term split.
 //
-// Same math as the FMA tile kernel (pinn_v2.cuh); the two tile GEMMs of every
-// chunk run on the 5th-generation tensor cores:
-//   * a CTA owns P = 128 collocation points = the MMA M dimension (TMEM lane =
-//     point); the 4 jet slots (u, u_x, u_t, u_xx) are 4 independent MMAs, so
-//     the epilogue thread that owns a point sees all 4 slots of every neuron
-//     (the activation jet and its VJP mix slots) without shuffles;
-//   * phase 1 (K = rank):   P1_c = SY_c U^T  (forward)  |  P1_c = ST_c V^T (reverse)
-//     A operand SY_c / ST_c from shared memory, B operand = factor chunk (TMA bulk);
-//   * epilogue (CUDA cores): tcgen05.ld P1 -> (+b) activation jet / its VJP with
-//     the pre-activation A reloaded from the forward's store -> 3xTF32 split ->
-//     tcgen05.st into TMEM (Z_c hi / lo);
-//   * phase 2 (K = KC neurons): Y_c += Z_c V (forward) | T_c += G_c U (reverse),
-//     A operand from TMEM, accumulated in TMEM over the chunks of the transition.
-// 3xTF32: x = hi + lo with hi = tf32(x); a*b ~ a_hi b_hi + a_hi b_lo + a_lo b_hi
-// (fp32 accumulate), giving ~fp32 accuracy (the dropped lo*lo term is 2^-22).
-// TMEM (512 columns): P1_c 4x32 | Z hi 4x32 | Z lo 4x32 | Y/T 4x32.
-// Shared memory: SY/ST hi/lo for 4 slots (128 KB) + a 3-slot factor-chunk ring.
-// One CTA per SM owns the whole TMEM; two issuer warps issue the phase-1 and
-// phase-2 MMAs warp-collectively, completion via tcgen05.commit -> mbarrier.
+// Same math as the FMA tile kernel (pinn_v2.cuh; reference: jet_affine_factored /
+// jet_activation, proj/src/model.cpp:85-223, and their VJPs, proj/src/autodiff.cpp:473-563).
+// A CTA owns P = 128 collocation points = the MMA M dimension (TMEM lane = point); the
+// 4 jet slots (u, u_x, u_t, u_xx) are 4 independent MMAs, so the epilogue thread that
+// owns a point sees all 4 slots of each of its neurons without shuffles.  Per chunk of
+// KC = 32 neurons of transition l:
+//   forward   P1  A_c  = SY_c U^T          SS: A = SY (smem), B = U^T chunk (ring)  -> TMEM (2 buffers)
+//             epilogue: A -> (+b) sigma-jet Z_c -> TMEM (fp16 hi | lo)
+//             P2  Y_c += Z_c V             TS: A = Z (TMEM),  B = V chunk           -> TMEM
+//   reverse   P1r A_c  = SY_c U^T (recomputed from SY_l in smem, no stash in HBM)
+//             P1d DZ_c = ST_c V^T          SS: A = ST (smem)
+//             epilogue: G_c = VJP(A, DZ) -> TMEM (fp16 hi | lo)
+//             P2r T_c += G_c U             TS: A = G (TMEM)
+// FP16 two-term split: every operand x is scaled by a power of two S (per point and jet
+// slot for SY / ST / Z / G, per matrix for the factors), hi = fp16(x S), lo =
+// fp16(x S - hi), and a*b ~ hi*hi + hi*lo + lo*hi with FP32 accumulation; the products
+// are unscaled exactly in the epilogue (2^-22 relative, scripts/umma_f16_test.cu).  SY /
+// ST rows are scaled by their exact 2-norm; Z / G rows by a Cauchy-Schwarz bound from
+// the SY / ST row norms and the factors' row norms (|sigma^(k)| <= 1 for sin, <= 2 for
+// tanh), so no per-chunk reduction is needed.  FP16 operands halve the shared-memory
+// bytes of the SS MMAs (which are shared-memory bound at N = 32: 42 cycles for
+// tf32 K8 vs 42 for f16 K16, scripts/umma_issue_tf32.cu) and let SY_l stay resident
+// for the reverse recompute.
+// TMEM (512 columns): forward P1 x2 | Z | Y;  reverse A | DZ | G | T.
+// Warp roles: 16 epilogue warps; warp 16 issues P1-type MMAs; warp 17 issues P2-type
+// MMAs and the factor-chunk TMA bulk copies (4-slot ring).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -33,110 +40,71 @@ namespace lrnr_b200 {
 namespace tc {
 
 constexpr int P = 128;    // points per tile (MMA M)
-constexpr int KC = 32;    // neurons per chunk (phase-1 N, phase-2 K)
+constexpr int KC = 32;    // neurons per chunk (N of the P1-type MMAs, K of the P2-type)
 constexpr int RP = 32;    // max padded rank
-#ifndef TC_NWE
-#define TC_NWE 16
-#endif
-constexpr int NWE = TC_NWE;  // epilogue warps: lane quarter = warp % 4, neuron / rank group of NG = warp / 4
-// Two dedicated MMA issuer warps after the epilogue warps: MMA issue is
-// latency-bound (~57 cycles per MMA from one warp), so the phase-1 and phase-2
-// MMAs are issued concurrently by warps ISSUER and ISSUER2 (one issuer: 24.40 ms
-// on c2; two: 23.51 ms; four, with each phase's jet slots split: 27.1 ms).
-constexpr int ISSUER = NWE;       // phase-1 issuer
-constexpr int ISSUER2 = NWE + 1;  // phase-2 issuer
+constexpr int NWE = 16;   // epilogue warps: lane quarter = warp % 4, neuron / rank group h = warp / 4
+constexpr int ISSUER = NWE;       // P1-type MMAs
+constexpr int ISSUER2 = NWE + 1;  // P2-type MMAs + TMA producer
 constexpr int NT = 32 * (NWE + 2);
-constexpr int NG = KC / (NWE / 4);  // neurons (epilogue) / ranks (sums) per thread
-// Units (single tiles) after each CTA's first are claimed from a global counter:
-// SMs run at slightly different speeds (a static split spread by up to 5 %).
-#define TC_MMA_SS umma::mma_ss_w
-#define TC_MMA_TS umma::mma_ts_w
-#define TC_COMMIT umma::mma_commit_w
-constexpr int TM_P1 = 0, TM_ZH = 128, TM_ZL = 256, TM_Y = 384;
-// Phase-2 products of YACC consecutive chunks accumulate in TMEM before the
-// epilogue reads them into the FP32 running sum (the tensor-core accumulator
-// truncates: 1 chunk = 12 MMAs keeps it at ~3e-6 on c2, 2 chunks ~6e-6, the
-// full K = 256 reached 1.2e-4). Halves the TMEM load round trips of Y.
-#ifndef TC_YACC
-#define TC_YACC 2
-#endif
-constexpr int YACC = TC_YACC;
+constexpr int NG = 8;             // neurons / ranks per epilogue thread
+// TMEM columns
+constexpr int TM_R = 0;     // forward: P1 buffers at 0 / 128 (chunk parity); reverse: A at 0, DZ at 128
+constexpr int TM_Z = 256;   // Z / G: per slot 32 columns = fp16 hi (16 columns) | lo (16 columns)
+constexpr int TM_Y = 384;   // Y / T: per slot 32 fp32 columns
+// Phase-2 products of YACC consecutive chunks accumulate in TMEM before the epilogue
+// adds them to its FP32 running sum (a long tensor-core accumulation loses precision:
+// K = 256 in one accumulator reached 1.2e-4 with 3xTF32).
+constexpr int YACC = 2;
 
-template <typename T = float>
+// shared memory (bytes)
+constexpr int OPD_HALF = P * RP * 2;           // one fp16 tile of a jet slot (128 rows x 32 K)
+constexpr int OPD_SLOT = 2 * OPD_HALF;         // hi | lo
+constexpr int OFF_X = 0;                       // SY (forward) / ST (reverse): P1-type A operand
+constexpr int OFF_W = OFF_X + 4 * OPD_SLOT;    // reverse: SY_l for the recomputed pre-activations
+constexpr int BUF = 3 * (4 * KC * RP) + 4 * KC;  // largest chunk block: three fp16 hi / lo 32 x 32 tiles + bias
+constexpr int NBUF = 4;
+constexpr int OFF_B0 = OFF_W + 4 * OPD_SLOT;
+constexpr int OFF_RED = OFF_B0 + NBUF * BUF;   // floats: [P][RPS] + P (loss) + [NWE][RP] partials
+constexpr int RPS = RP + 1;                    // odd point stride: conflict-free column writes
+constexpr int OFF_XCH = OFF_RED + (P * RPS + P + NWE * RP) * 4;  // floats [4 groups][P][8]
+constexpr int OFF_ACC = OFF_XCH + 4 * P * 8 * 4;
+constexpr int SMEM_BYTES = OFF_ACC + 1024 * 4;
+static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
+static_assert(BUF % 16 == 0 && OFF_B0 % 1024 == 0, "alignment");
+
 struct NetTC {
     int L;
     int M[kMaxL + 1];
     int r[kMaxL];
-    int rk[kMaxL];         // padded rank as MMA K (multiple of 8, <= 32)
+    int rk[kMaxL];         // padded rank as MMA K (multiple of 16, <= 32)
     int rn[kMaxL];         // padded rank as MMA N (16 or 32)
     int nc[kMaxL];
     int soff[kMaxL + 1];
     int yoff[kMaxL];       // y_l in per-CTA scratch: [p][j (r_l)][4]
     int ystride;
-    int64_t aoff[kMaxL];   // A in per-CTA scratch: [chunk][KC][p][4]
-    int64_t astride;
+    float isU[kMaxL];      // 1 / (power-of-two scale of U_l) and of V_l
+    float isV[kMaxL];
+    float muU[kMaxL];      // max row 2-norm of U_l / V_l (bounds of the pre-activation jets)
+    float muV[kMaxL];
+    float c3;              // max |sigma'''| (1 sin, 2 tanh)
     int rtotal;
-    const float* blocks;
-    const int64_t* sched_off;
+    const unsigned char* blocks;
+    const int64_t* sched_off;  // bytes
     const int* sched_bytes;
     int sched_len;
     const float* V0;       // 2 x r[0]
     const float* ulast;    // r[L-1] then b_{L-1}[0]
 };
 
-// smem layout (floats)
-constexpr int SY_TILE = P * RP;               // one canonical K-major tile (rows = 128, K = 32)
-constexpr int OFF_SY = 0;                     // [c][hi/lo] tiles: 8 x 4096 floats = 128 KB
-constexpr int BUF = 4 * KC * RP + KC + 32;    // factor chunk (max): 4 canonical 32x32 tiles + bias
-#ifndef TC_NBUF
-#define TC_NBUF 3
-#endif
-constexpr int NBUF = TC_NBUF;                 // factor-chunk ring (NBUF - 1 chunks in flight)
-constexpr int OFF_B0 = OFF_SY + 8 * SY_TILE;
-constexpr int OFF_RED = OFF_B0 + NBUF * BUF;  // [P][RP] + P (loss) + [16][RP] partials
-constexpr int RPS = RP + 1;                   // red[] point stride (odd: conflict-free column writes)
-constexpr int OFF_ACC = OFF_RED + P * RPS + P + 16 * RP;  // partials: up to 16 groups
-constexpr int SMEM_FLOATS = OFF_ACC + 1024;
-
-__device__ __forceinline__ float* sy_tile(float* sm, int c, int lo) { return sm + OFF_SY + (2 * c + lo) * SY_TILE; }
-
-// write an fp32 value split into the hi / lo canonical tiles of slot c at (row p, k j)
-// four consecutive k (j0 % 4 == 0) of row p as one 16-byte store per tile: a
-// quarter-warp's 8 rows then fill one 128-byte core matrix (no bank conflicts; the
-// scalar form hits each bank 4 times per warp)
-__device__ __forceinline__ void put_split4(float* sm, int c, int p, int j0, float v0, float v1, float v2, float v3) {
-    float h[4], l[4];
-    umma::split_tf32(v0, h[0], l[0]);
-    umma::split_tf32(v1, h[1], l[1]);
-    umma::split_tf32(v2, h[2], l[2]);
-    umma::split_tf32(v3, h[3], l[3]);
-    const int o = umma::kmaj_off(p, j0, P);
-    *reinterpret_cast<float4*>(sy_tile(sm, c, 0) + o) = make_float4(h[0], h[1], h[2], h[3]);
-    *reinterpret_cast<float4*>(sy_tile(sm, c, 1) + o) = make_float4(l[0], l[1], l[2], l[3]);
-}
-__device__ __forceinline__ void put_split(float* sm, int c, int p, int j, float v) {
-    float h, l;
-    umma::split_tf32(v, h, l);
-    const int o = umma::kmaj_off(p, j, P);
-    sy_tile(sm, c, 0)[o] = h;
-    sy_tile(sm, c, 1)[o] = l;
-}
-
 // Optional phase timing (dev aid): -DLRNR_TC_TIMING records clock64 deltas of
 // CTA 0 / thread 32 into a global array (see scripts/tc_timing.py).
 #ifdef LRNR_TC_TIMING
 __device__ unsigned long long g_tc_timing[16];
-// accumulated in shared memory (a few cycles per mark) and flushed once at the end
 #define TC_T0()                                                \
     __shared__ unsigned long long _tc_acc[16];                 \
     if (threadIdx.x < 16) _tc_acc[threadIdx.x] = 0;            \
     __syncthreads();                                           \
     long long _tt = clock64();
-#define TC_ISSUE_BEGIN() const long long _ti = clock64();
-#define TC_ISSUE_END()                                                                    \
-    do {                                                                                  \
-        if (blockIdx.x == 0) _tc_acc[15] += static_cast<unsigned long long>(clock64() - _ti); \
-    } while (0)
 #define TC_MARK(i)                                                         \
     do {                                                                   \
         if (blockIdx.x == 0 && threadIdx.x == 32) {                        \
@@ -152,112 +120,113 @@ __device__ unsigned long long g_tc_timing[16];
     } while (0)
 #else
 #define TC_T0()
-#define TC_ISSUE_BEGIN()
-#define TC_ISSUE_END()
 #define TC_MARK(i)
 #define TC_FLUSH()
 #endif
 
-// acc[1 + off + j] += sum_p red[p][j] for j < r, fixed order: NRG groups of
-// P / NRG points in parallel (one thread per (group, rank)), then the partials.
-constexpr int NRG = NWE;
+// acc[1 + off + j] += sum_p red[p][j] for j < r, fixed order: NWE groups of P / NWE
+// points in parallel (one thread per (group, rank)), then the partials.
 __device__ __forceinline__ void reduce_points(float* red, float* acc, int off, int r, int tid) {
     float* part = red + P * RPS + P;
-    if (tid < NRG * RP) {
+    if (tid < NWE * RP) {
         const int j = tid % RP, g = tid / RP;
         float s = 0.f;
         if (j < r)
 #pragma unroll
-            for (int i = 0; i < P / NRG; ++i) s += red[((P / NRG) * g + i) * RPS + j];
+            for (int i = 0; i < P / NWE; ++i) s += red[((P / NWE) * g + i) * RPS + j];
         part[g * RP + j] = s;
     }
     __syncthreads();
     if (tid < r) {
         float s = 0.f;
 #pragma unroll
-        for (int g = 0; g < NRG; ++g) s += part[g * RP + tid];
+        for (int g = 0; g < NWE; ++g) s += part[g * RP + tid];
         acc[1 + off + tid] += s;
     }
 }
 
-__device__ __forceinline__ void tld(uint32_t taddr, float (&v)[8]) { umma::tmem_ld8(taddr, v); }
-__device__ __forceinline__ void tld(uint32_t taddr, float (&v)[16]) { umma::tmem_ld16(taddr, v); }
-__device__ __forceinline__ void tst(uint32_t taddr, const float (&v)[8]) { umma::tmem_st8(taddr, v); }
-__device__ __forceinline__ void tst(uint32_t taddr, const float (&v)[16]) { umma::tmem_st16(taddr, v); }
-
-// acc[c][n] += TMEM[taddr + c * 32 + n] (the previous chunk's phase-2 product),
-// one load batch, one wait
-__device__ __forceinline__ void add_y(uint32_t taddr, float (&acc)[4][NG]) {
+// acc[c][n] += iv[c] * TMEM[taddr + c * 32 + n] (YACC chunks of phase-2 products, unscaled)
+__device__ __forceinline__ void add_acc(uint32_t taddr, const float (&iv)[4], float (&acc)[4][NG]) {
     float v[4][NG];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) tld(taddr + c * 32, v[c]);
+    for (int c = 0; c < 4; ++c) umma::tmem_ld8(taddr + c * 32, v[c]);
     umma::tmem_ld_wait();
 #pragma unroll
     for (int c = 0; c < 4; ++c)
 #pragma unroll
-        for (int n = 0; n < NG; ++n) acc[c][n] += v[c][n];
+        for (int n = 0; n < NG; ++n) acc[c][n] = fmaf(v[c][n], iv[c], acc[c][n]);
 }
 
-// P1 columns of this thread (4 slots x NG neurons) in two column halves: the first
-// half is waited for here, the second is in flight while the first half's math runs
-// (the caller waits before touching column NG / 2)
-__device__ __forceinline__ void ld_p1_halves(uint32_t taddr, float (&v)[4][NG]) {
+// Write this thread's 8 values (K block h = ranks 8h..8h+7) of point p of the four jet
+// slots into an operand buffer (fp16 hi / lo tiles) after scaling slot c by 2^e[c]:
+// a quarter-warp's 8 points fill one 128-byte core matrix (conflict-free 16-B stores).
+__device__ __forceinline__ void put_rows(unsigned char* buf, int p, int h, const float (&v)[4][NG], const int (&e)[4]) {
+    const int o = umma::kmaj16_off(p, 8 * h, P);
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
+    for (int c = 0; c < 4; ++c) {
+        const float s = umma::exp2i(e[c]);
+        uint32_t hw[4], lw[4];
 #pragma unroll
-        for (int h = 0; h < NG / 2; h += 4) umma::tmem_ld4(taddr + c * KC + h, v[c] + h);
-    umma::tmem_ld_wait();
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int h = NG / 2; h < NG; h += 4) umma::tmem_ld4(taddr + c * KC + h, v[c] + h);
+        for (int i = 0; i < 4; ++i) umma::split16x2(v[c][2 * i] * s, v[c][2 * i + 1] * s, hw[i], lw[i]);
+        *reinterpret_cast<uint4*>(buf + c * OPD_SLOT + o) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(buf + c * OPD_SLOT + OPD_HALF + o) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
 }
 
-// stored pre-activation A of (neuron k, point p) inside its chunk: [k][p][4]
-// (a warp's 32 points are one contiguous 512-B segment)
-__device__ __forceinline__ int aidx(int k, int p) { return (k * P + p) * 4; }
+// named barrier over the 16 epilogue warps (the issuer warps keep running)
+__device__ __forceinline__ void named_bar_epi() { asm volatile("bar.sync 1, %0;" ::"n"(NWE * 32) : "memory"); }
 
 template <int ACT, bool FAST>
 __device__ __forceinline__ void act3f(float a, float& sg, float& d1, float& d2, float& d3) {
     v2::act3<ACT, FAST>(a, sg, d1, d2, d3);
 }
 
+// Per-point scales of one transition (exponents / unscale factors), all 4 jet slots.
+struct FwdScales {
+    float ia[4];   // P1 unscale: 2^-eSY * isU
+    int ez[4];     // Z scale exponents
+    float iy[4];   // Y unscale: 2^-ez * isV
+};
+struct RevScales {
+    float ia[4];   // recomputed A unscale
+    float id[4];   // DZ unscale: 2^-eST * isV
+    int eg[4];     // G scale exponents
+    float it[4];   // T unscale: 2^-eg * isU
+};
+
 template <int ACT, bool FAST>
 __global__ void __launch_bounds__(NT, 1)
-pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pts, const double* __restrict__ svec,
-               const double* __restrict__ mus, const float w, float* __restrict__ scratch,
-               float* __restrict__ ascratch, float* __restrict__ part, unsigned long long* __restrict__ bad,
-               unsigned long long* __restrict__ unit_ctr) {
-    extern __shared__ __align__(128) float sm[];
-    float* red = sm + OFF_RED;
-    float* acc = sm + OFF_ACC;
-    __shared__ __align__(8) uint64_t wbar[NBUF];
-    __shared__ __align__(8) uint64_t mbar1, mbar2;
-    __shared__ __align__(8) uint64_t p1free, zready;  // epilogue -> issuer (one arrive per epilogue warp)
+pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts, const double* __restrict__ svec,
+               const double* __restrict__ mus, const float w, float* __restrict__ scratch, float* __restrict__ part,
+               unsigned long long* __restrict__ bad, unsigned long long* __restrict__ unit_ctr) {
+    extern __shared__ __align__(1024) unsigned char smb[];
+    float* red = reinterpret_cast<float*>(smb + OFF_RED);
+    float* xch = reinterpret_cast<float*>(smb + OFF_XCH);
+    float* acc = reinterpret_cast<float*>(smb + OFF_ACC);
+    unsigned char* X = smb + OFF_X;
+    unsigned char* W = smb + OFF_W;
+    __shared__ __align__(8) uint64_t wbar[NBUF];           // ring slot filled (TMA)
+    __shared__ __align__(8) uint64_t p1full[2];  // forward P1 buffers written (tcgen05.commit)
+    __shared__ __align__(8) uint64_t rfull;      // reverse A / DZ written
+    __shared__ __align__(8) uint64_t zfree;      // P2 done: Z / G free, Y / T product ready
     __shared__ uint32_t tmem_base;
     __shared__ int64_t next_unit;
 
     const int tid = threadIdx.x;
-    const int warp = tid >> 5, lane = tid & 31;
-    const int quarter = warp & 3, half = warp >> 2;  // half: neuron / rank group of NG
-    const int p = quarter * 32 + lane;  // the point (TMEM lane) this thread serves in epilogues
+    const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
+    const int quarter = warp & 3, h = warp >> 2;  // h: neuron / rank group (epilogue warps)
+    const int p = quarter * 32 + lane;            // the point (TMEM lane) this thread serves
     const int R1 = 1 + net.rtotal;
     const int L = net.L;
     float* scr = scratch + static_cast<int64_t>(blockIdx.x) * net.ystride;
-    float* ascr = ascratch + static_cast<int64_t>(blockIdx.x) * net.astride;
 
-#ifdef TC_CTA_TIMES
-    unsigned long long _t_start;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t_start));
-#endif
     for (int k = tid; k < R1; k += NT) acc[k] = 0.f;
     if (warp == 0) umma::tmem_alloc<512>(&tmem_base);
     if (tid == 0) {
         for (int i = 0; i < NBUF; ++i) umma::mbar_init(&wbar[i], 1);
-        umma::mbar_init(&mbar1, 1);
-        umma::mbar_init(&mbar2, 1);
-        umma::mbar_init(&p1free, NWE);
-        umma::mbar_init(&zready, NWE);
+        for (int i = 0; i < 2; ++i) umma::mbar_init(&p1full[i], 1);
+        umma::mbar_init(&rfull, 1);
+        umma::mbar_init(&zfree, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     umma::fence_before();
@@ -265,108 +234,154 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
     umma::fence_after();
     const uint32_t tbase = tmem_base;
     const uint32_t tlane = tbase + (static_cast<uint32_t>(quarter * 32) << 16);
-    uint32_t ph1 = 0, ph2 = 0;  // mbarrier phase counters (epilogue warps)
-    uint32_t phf = 0, phz = 0;  // p1free / zready phase counters (issuer warp)
-    // epilogue warp -> issuer handshakes (after warp-collective tcgen05 ld / st waits)
-    auto signal = [&](uint64_t* bar) {
+
+    auto wait = [&](uint64_t* bar, uint32_t parity) {
+        umma::mbar_wait(bar, parity);
+        umma::fence_after();
+    };
+    // epilogue -> issuer hand-offs are hardware named barriers (the 16 epilogue warps
+    // arrive, the issuer warp syncs: it blocks without spinning; at most one generation
+    // of each is outstanding): Z / G written, forward P1 buffer 0 / 1 read, reverse A / DZ read
+    // (barrier 1 is the epilogue-only barrier)
+    constexpr int BAR_ZFULL = 2, BAR_P1FREE = 3, BAR_RFREE = 5, BAR_N = NWE * 32 + 32;
+    auto signal = [&](int id) {
         umma::fence_before();
         __syncwarp();
-        if (lane == 0) umma::mbar_arrive(bar);
+        asm volatile("bar.arrive %0, %1;" ::"r"(id), "n"(BAR_N) : "memory");
     };
-    auto await = [&](uint64_t* bar, uint32_t& ph) {
-        umma::mbar_wait(bar, ph & 1);
-        ++ph;
+    auto await = [&](int id) {
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(BAR_N) : "memory");
         umma::fence_after();
     };
 
-    // ---- factor-chunk pipeline (TMA bulk copies) ----
-    // every tile runs the same chunk schedule, so the ring is refilled without knowing the
-    // CTA's tile count; the NBUF - 1 copies in flight past the last chunk are drained at exit
-    const int64_t total_chunks = INT64_MAX;
-#ifdef TC_CTA_TIMES
-    int64_t total_tiles = 0;
-#endif
-    int64_t q = 0;
-    auto issue = [&](int64_t qq) {
-        if (qq < total_chunks) {
-            const int e = static_cast<int>(qq % net.sched_len);
-            const int b = static_cast<int>(qq % NBUF);
-            v2::fence_proxy_async();
-            v2::mbar_expect_tx(&wbar[b], static_cast<uint32_t>(net.sched_bytes[e]));
-            v2::bulk_g2s(sm + OFF_B0 + b * BUF, net.blocks + net.sched_off[e], static_cast<uint32_t>(net.sched_bytes[e]),
-                         &wbar[b]);
-        }
+    // ---- factor-chunk ring (TMA bulk copies, issued by ISSUER2's elected lane) ----
+    // every tile runs the same chunk schedule; the copies in flight past the last chunk
+    // are drained at exit
+    auto tma = [&](int64_t qq) {
+        const int e = static_cast<int>(qq % net.sched_len);
+        const int b = static_cast<int>(qq % NBUF);
+        v2::fence_proxy_async();
+        v2::mbar_expect_tx(&wbar[b], static_cast<uint32_t>(net.sched_bytes[e]));
+        v2::bulk_g2s(smb + OFF_B0 + b * BUF, net.blocks + net.sched_off[e], static_cast<uint32_t>(net.sched_bytes[e]),
+                     &wbar[b]);
     };
-    if (tid == 0) {
-        for (int i = 0; i + 1 < NBUF; ++i) issue(i);
-    }
-    TC_T0();
-    auto wait_mma1 = [&]() {
-        umma::mbar_wait(&mbar1, ph1 & 1);
-        ++ph1;
-        umma::fence_after();
-    };
-    auto wait_mma2 = [&]() {
-        umma::mbar_wait(&mbar2, ph2 & 1);
-        ++ph2;
-        umma::fence_after();
-    };
-    const uint32_t id_p1 = umma::idesc_tf32(P, KC);
-    // descriptor low words (start >> 4 | LBO >> 4 << 16); advancing the start by
-    // a float offset f adds f >> 2.  Common high word: SBO = 128 B, version 1.
+    const bool producer = warp == ISSUER2 && lane == 0;
+    if (producer)
+        for (int i = 0; i < NBUF; ++i) tma(i);
+    auto wait_slot = [&](int64_t qq) { wait(&wbar[qq % NBUF], static_cast<uint32_t>((qq / NBUF) & 1)); };
+    auto slot = [&](int64_t qq) { return smb + OFF_B0 + static_cast<int>(qq % NBUF) * BUF; };
+
+    // descriptor words: high word SBO = 128 B, version 1; low words start >> 4 | LBO >> 4 << 16
     const uint32_t dhi = umma::desc_hi(128);
-    const uint32_t lsy = umma::desc_lo(sm + OFF_SY, (P / 8) * 128);     // SY / ST tiles (rows = P)
-    const uint32_t lb32 = umma::desc_lo(sm + OFF_B0, (KC / 8) * 128);   // factor tiles with 32 rows
-    const uint32_t lb16 = umma::desc_lo(sm + OFF_B0, (16 / 8) * 128);   // factor tiles with 16 rows
-    // phase 1 (issuer warp, converged): P1_c = S_c B (3xTF32), S = SY / ST from smem,
-    // B = factor tiles at float offset bo (hi) / bo + KC * rk (lo) of the ring slot
-    auto mma_p1 = [&](int bo, int rk) {
+    auto dlo = [&](const unsigned char* ptr, int rows) { return umma::desc_lo(ptr, (rows / 8) * 128); };
+    const uint32_t idP1 = umma::idesc_f16(P, KC);
+    // P1-type MMAs (SS) into d: A = operand buffer (4 slots), B = fp16 hi / lo tile of
+    // 32 neuron rows at bsrc; K = rk (multiple of 16).  One elected lane issues.
+    auto mma_p1 = [&](uint32_t d, const unsigned char* abuf, const unsigned char* bsrc, int rk) {
+        const uint32_t bh = dlo(bsrc, KC), bl = dlo(bsrc + 2 * KC * rk, KC);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            const uint32_t d = tbase + TM_P1 + c * KC;
-            const uint32_t ah0 = lsy + ((2 * c) * SY_TILE >> 2), al0 = lsy + ((2 * c + 1) * SY_TILE >> 2);
-            const uint32_t bh0 = lb32 + (bo >> 2), bl0 = lb32 + ((bo + KC * rk) >> 2);
-            for (int s = 0; s < rk / 8; ++s) {
-                const uint32_t sa = s * (2 * (P / 8) * 32 >> 2), sb = s * (2 * (KC / 8) * 32 >> 2);
-                TC_MMA_SS(d, ah0 + sa, bh0 + sb, dhi, id_p1, s > 0);
-                TC_MMA_SS(d, ah0 + sa, bl0 + sb, dhi, id_p1, 1);
-                TC_MMA_SS(d, al0 + sa, bh0 + sb, dhi, id_p1, 1);
+            const uint32_t ah = dlo(abuf + c * OPD_SLOT, P), al = dlo(abuf + c * OPD_SLOT + OPD_HALF, P);
+            for (int s = 0; s < rk / 16; ++s) {
+                const uint32_t sa = s * 2 * P, sb = s * 2 * KC;  // 16-B units per K step of 16
+                umma::mma16_ss(d + c * 32, ah + sa, bh + sb, dhi, idP1, s > 0);
+                umma::mma16_ss(d + c * 32, ah + sa, bl + sb, dhi, idP1, 1);
+                umma::mma16_ss(d + c * 32, al + sa, bh + sb, dhi, idP1, 1);
             }
         }
-        TC_COMMIT(&mbar1);
     };
-    // phase 2 (issuer warp 2, converged): Y_c = Z_c B (fresh accumulator, A from TMEM),
-    // B = factor tiles (rows rn) at float offset bo (hi) / bo + rn * KC (lo)
-    auto mma_p2 = [&](int bo, int rn, bool acc0) {
-        const uint32_t id_p2 = umma::idesc_tf32(P, rn);
-        const uint32_t lb = rn == 16 ? lb16 : lb32;
-        const uint32_t bh0 = lb + (bo >> 2), bl0 = lb + ((bo + rn * KC) >> 2);
-        const uint32_t sb = 2 * (rn / 8) * 32 >> 2;
+    // P2-type MMAs (TS): D = TM_Y, A = Z / G in TMEM, B = fp16 hi / lo tile of rn rows x KC at bsrc
+    auto mma_p2 = [&](const unsigned char* bsrc, int rn, bool acc0) {
+        const uint32_t id2 = umma::idesc_f16(P, rn);
+        const uint32_t bh = dlo(bsrc, rn), bl = dlo(bsrc + 2 * rn * KC, rn);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            const uint32_t d = tbase + TM_Y + c * 32;
+            const uint32_t d = tbase + TM_Y + c * 32, az = tbase + TM_Z + c * 32;
 #pragma unroll
-            for (int s = 0; s < KC / 8; ++s) {
-                const uint32_t azh = tbase + TM_ZH + c * KC + s * 8, azl = tbase + TM_ZL + c * KC + s * 8;
-                TC_MMA_TS(d, azh, bh0 + s * sb, dhi, id_p2, (s > 0 || acc0) ? 1u : 0u);
-                TC_MMA_TS(d, azh, bl0 + s * sb, dhi, id_p2, 1);
-                TC_MMA_TS(d, azl, bh0 + s * sb, dhi, id_p2, 1);
+            for (int s = 0; s < KC / 16; ++s) {
+                const uint32_t sb = s * 2 * rn;
+                umma::mma16_ts(d, az + 8 * s, bh + sb, dhi, id2, (s > 0 || acc0) ? 1u : 0u);
+                umma::mma16_ts(d, az + 8 * s, bl + sb, dhi, id2, 1);
+                umma::mma16_ts(d, az + 16 + 8 * s, bh + sb, dhi, id2, 1);
             }
         }
-        TC_COMMIT(&mbar2);
-    };
-    auto wait_slot = [&](int64_t qq) {
-        umma::mbar_wait(&wbar[qq % NBUF], static_cast<uint32_t>((qq / NBUF) & 1));
-        umma::fence_after();
     };
 
+    int64_t q = 0;      // global chunk counter (ring schedule)
+    uint32_t fq = 0;    // forward chunks (P1 buffer uses)
+    uint32_t rq = 0;    // reverse chunks
+    uint32_t zw = 0;    // epilogue: zfree completions consumed
+
+    // ISSUER2 per chunk: wait for Z / G, refill the previous chunk's ring slot (Z / G of
+    // chunk qq are written only after P2(qq - 1), the slot's last reader, completed),
+    // then issue the phase-2 MMAs
+    auto issue_p2 = [&](int64_t qq, const unsigned char* bsrc, int rn, bool acc0) {
+        await(BAR_ZFULL);
+        if (lane == 0 && qq >= 1) tma(qq - 1 + NBUF);
+        if (umma::elect_one()) {
+            mma_p2(bsrc, rn, acc0);
+            umma::mma_commit_1(&zfree);
+        }
+        __syncwarp();
+    };
+    // ISSUER: forward P1 of chunk qq into buffer fq & 1
+    auto issue_fwd_p1 = [&](int64_t qq, uint32_t fqq, int rk) {
+        wait_slot(qq);
+        const uint32_t b = fqq & 1, k = fqq >> 1;
+        if (k >= 1) await(BAR_P1FREE + b);
+        if (umma::elect_one()) {
+            mma_p1(tbase + TM_R + 128 * b, X, slot(qq), rk);
+            umma::mma_commit_1(&p1full[b]);
+        }
+        __syncwarp();
+    };
+    // ISSUER: reverse A (recomputed) and DZ of chunk qq
+    auto issue_rev_p1 = [&](int64_t qq, uint32_t rqq, int rkl, int rkn) {
+        wait_slot(qq);
+        if (rqq >= 1) await(BAR_RFREE);
+        if (umma::elect_one()) {
+            const unsigned char* b = slot(qq);
+            mma_p1(tbase + TM_R, W, b, rkl);                               // A = SY_l U^T
+            mma_p1(tbase + TM_R + 128, X, b + 4 * KC * rkl + 4 * KC, rkn);  // DZ = ST_{l+1} V^T
+            umma::mma_commit_1(&rfull);
+        }
+        __syncwarp();
+    };
+
+    // Reverse scales of transition lr from the exchanged squared row norms of ST_{lr+1}
+    // (nst) and SY_lr (nsy); writes this thread's K block of ST_{lr+1} into X and of
+    // SY_lr into W.  G bound (|sigma'|, |sigma''| <= 1, |sigma'''| <= c3, |DZ_c| <= |ST_c| muV,
+    // |A_c| <= |SY_c| muU): |G0| <= B0 + B1 bx + B2 bt + B3 (c3 bx^2 + bw), |G1| <= B1 + 2 B3 bx.
+    auto rev_scales = [&](RevScales& r, float (&nst)[4], float (&nsy)[4], int lr, const float (&st)[4][NG],
+                          const float (&sy)[4][NG]) {
+        int est[4], esy[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            nst[c] = sqrtf(nst[c]);
+            nsy[c] = sqrtf(nsy[c]);
+            est[c] = umma::pow2_exp(nst[c]);
+            esy[c] = umma::pow2_exp(nsy[c]);
+            r.id[c] = umma::exp2i(-est[c]) * net.isV[lr];
+            r.ia[c] = umma::exp2i(-esy[c]) * net.isU[lr];
+        }
+        if (NG * h < net.rk[lr + 1]) put_rows(X, p, h, st, est);
+        if (NG * h < net.rk[lr]) put_rows(W, p, h, sy, esy);
+        const float mu = net.muU[lr], mv = net.muV[lr];
+        const float bx = nsy[1] * mu, bt = nsy[2] * mu, bw = nsy[3] * mu;
+        const float B0 = nst[0] * mv, B1 = nst[1] * mv, B2 = nst[2] * mv, B3 = nst[3] * mv;
+        r.eg[0] = umma::pow2_exp(B0 + B1 * bx + B2 * bt + B3 * fmaf(net.c3 * bx, bx, bw));
+        r.eg[1] = umma::pow2_exp(fmaf(2.f * B3, bx, B1));
+        r.eg[2] = umma::pow2_exp(B2);
+        r.eg[3] = umma::pow2_exp(B3);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) r.it[c] = umma::exp2i(-r.eg[c]) * net.isU[lr];
+    };
+
+    TC_T0();
     // claims: the counter starts at all-ones (memset 0xff), so the first claim returns unit gridDim.x
     unsigned long long claim = 0;
     if (tid == 0) claim = atomicAdd(unit_ctr, 1ull) + 1ull + gridDim.x;
     for (int64_t unit = blockIdx.x; unit < g.n_units;) {
-#ifdef TC_CTA_TIMES
-        ++total_tiles;
-#endif
         const int64_t inst = unit / g.units_per_inst;
         const int seg = static_cast<int>(unit % g.units_per_inst);
         const int t_lo = seg * g.tiles_per_unit;
@@ -378,324 +393,430 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
             const int64_t pi = static_cast<int64_t>(tile) * P + p;
             const bool valid = pi < g.n_per_inst;
             const int64_t gp = inst * g.n_per_inst + pi;
-            // ---------------- input layer: y_0 = V_0^T z_0 ----------------
-            if (half == 0) {
-                const float x = valid ? float(pts[2 * gp]) : 0.f;
-                const float t = valid ? float(pts[2 * gp + 1]) : 0.f;
-                const int r0 = net.r[0];
-                for (int j = 0; j < net.rk[0]; ++j) {
-                    float y4[4] = {0.f, 0.f, 0.f, 0.f};
-                    float sj = 0.f;
-                    if (j < r0) {
-                        const float v0 = net.V0[j], v1 = net.V0[r0 + j];
-                        y4[0] = v0 * x + v1 * t;
-                        y4[1] = v0;
-                        y4[2] = v1;
-                        sj = float(sv[j]);
-                        v2::st4(scr + net.yoff[0] + (p * r0 + j) * 4, y4[0], y4[1], y4[2], y4[3]);
-                    }
+            FwdScales fs;
+            // ---------------- input layer: y_0 = V_0^T z_0, SY_0 = s_0 (.) y_0 ----------------
+            {
+                float sy[4][NG];
+                if (warp < NWE) {
+                    const float x = valid ? float(pts[2 * gp]) : 0.f;
+                    const float t = valid ? float(pts[2 * gp + 1]) : 0.f;
+                    const int r0 = net.r[0];
+                    float ss[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) put_split(sm, c, p, j, sj * y4[c]);
+                    for (int n = 0; n < NG; ++n) {
+                        const int j = NG * h + n;
+                        float y4[4] = {0.f, 0.f, 0.f, 0.f};
+                        float sj = 0.f;
+                        if (j < r0) {
+                            const float v0 = net.V0[j], v1 = net.V0[r0 + j];
+                            y4[0] = v0 * x + v1 * t;
+                            y4[1] = v0;
+                            y4[2] = v1;
+                            sj = float(sv[j]);
+                            v2::st4(scr + net.yoff[0] + (p * r0 + j) * 4, y4[0], y4[1], y4[2], y4[3]);
+                        }
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            sy[c][n] = sj * y4[c];
+                            ss[c] = fmaf(sy[c][n], sy[c][n], ss[c]);
+                        }
+                    }
+                    *reinterpret_cast<float4*>(xch + (h * P + p) * 8) = make_float4(ss[0], ss[1], ss[2], ss[3]);
                 }
+                __syncthreads();
+                if (warp < NWE) {
+                    float nr[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int hh = 0; hh < 4; ++hh) {
+                        const float4 v = *reinterpret_cast<const float4*>(xch + (hh * P + p) * 8);
+                        nr[0] += v.x;
+                        nr[1] += v.y;
+                        nr[2] += v.z;
+                        nr[3] += v.w;
+                    }
+                    int e[4];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        nr[c] = sqrtf(nr[c]);
+                        e[c] = umma::pow2_exp(nr[c]);
+                        fs.ia[c] = umma::exp2i(-e[c]) * net.isU[0];
+                    }
+                    if (NG * h < net.rk[0]) put_rows(X, p, h, sy, e);
+                    const float bx = nr[1] * net.muU[0], bt = nr[2] * net.muU[0], bw = nr[3] * net.muU[0];
+                    fs.ez[0] = umma::pow2_exp(1.f);
+                    fs.ez[1] = umma::pow2_exp(bx);
+                    fs.ez[2] = umma::pow2_exp(bt);
+                    fs.ez[3] = umma::pow2_exp(fmaf(bx, bx, bw));
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) fs.iy[c] = umma::exp2i(-fs.ez[c]) * net.isV[0];
+                }
+                umma::fence_async_smem();
+                __syncthreads();
             }
-            umma::fence_async_smem();
-            __syncthreads();
 
             // ---------------- forward transitions ----------------
+            RevScales rs;
             for (int l = 0; l + 1 < L; ++l) {
-                const int rk = net.rk[l], rnn = net.rn[l + 1];
-                // Y = sum over chunks of fresh per-chunk tensor-core products, summed
-                // here in FP32 (the tensor-core accumulator truncates; one K = 32
-                // chunk per accumulator keeps that bias at the FP32 level)
+                const int rk = net.rk[l], rnn = net.rn[l + 1], nc = net.nc[l];
+                const int fbias = 4 * KC * rk, fv = fbias + 4 * KC;  // byte offsets in the forward block
                 float ysum[4][NG];
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
 #pragma unroll
                     for (int n = 0; n < NG; ++n) ysum[c][n] = 0.f;
-                // factor block of chunk qq: UT_H | UT_L (KC x rk, rows KC) | bias (KC, padded 32) | VT_H | VT_L (rnn x KC)
-                auto fwd_p1 = [&](int64_t qq) {
-                    wait_slot(qq);
-                    mma_p1(static_cast<int>(qq % NBUF) * BUF, rk);
-                };
-                auto fwd_p2 = [&](int64_t qq, int ch) {
-                    mma_p2(static_cast<int>(qq % NBUF) * BUF + 2 * KC * rk + 32, rnn, ch % YACC != 0);
-                };
-                if (warp == ISSUER) fwd_p1(q);
-                // pipeline per chunk ch: [P1(ch) | P2(ch-1)] on the tensor core while the
-                // epilogue of ch computes the activation jet; Z / Y are touched only after
-                // P2(ch-1) completes.  P1(ch+1) is issued ahead of P2(ch).
-                for (int ch = 0; ch < net.nc[l]; ++ch, ++q) {
-                    const float* bias = sm + OFF_B0 + static_cast<int>(q % NBUF) * BUF + 2 * KC * rk;
-                    if (warp < NWE) {
+                if (warp == ISSUER) issue_fwd_p1(q, fq, rk);
+                for (int ch = 0; ch < nc; ++ch, ++q, ++fq) {
+                    if (warp == ISSUER) {
+                        if (ch + 1 < nc) issue_fwd_p1(q + 1, fq + 1, rk);
+                    } else if (warp == ISSUER2) {
+                        issue_p2(q, slot(q) + fv, rnn, ch % YACC != 0);
+                    } else {
                         TC_MARK(1);
-                        wait_mma1();
+                        const uint32_t b = fq & 1;
+                        wait(&p1full[b], (fq >> 1) & 1);
                         TC_MARK(2);
-                        // ring slot of chunk q-1 is free once P2(q-1) is complete
-                        if (ch == 0 && tid == 0) issue(q + NBUF - 1);
-                        {
-                            float a[4][NG];
-                            float* Ast = ascr + net.aoff[l] + static_cast<int64_t>(ch) * (P * KC * 4);
-                            // two column halves: the second half's TMEM read overlaps the first half's math
-                            ld_p1_halves(tlane + TM_P1 + half * NG, a);
-    #pragma unroll
-                            for (int n = 0; n < NG; ++n) {
-                                if (n == NG / 2) {
-                                    umma::tmem_ld_wait();
-                                    signal(&p1free);  // P1 may be overwritten by P1(ch+1)
-                                }
-                                const int k = half * NG + n;
-                                const float av = a[0][n] + bias[k], ax = a[1][n], at = a[2][n], aw = a[3][n];
-                                v2::st4(Ast + aidx(k, p), av, ax, at, aw);
+                        const float* bias = reinterpret_cast<const float*>(slot(q) + fbias);
+                        float a[4][NG];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) umma::tmem_ld8(tlane + TM_R + 128 * b + c * 32 + NG * h, a[c]);
+                        umma::tmem_ld_wait();
+                        signal(BAR_P1FREE + b);  // the buffer may take P1(q + 2)
+                        uint32_t zh[4][NG / 2], zl[4][NG / 2];
+#pragma unroll
+                        for (int n = 0; n < NG; n += 2) {
+                            float z[2][4];
+#pragma unroll
+                            for (int i = 0; i < 2; ++i) {
+                                const int k = NG * h + n + i;
+                                const float av = fmaf(a[0][n + i], fs.ia[0], bias[k]);
+                                const float ax = a[1][n + i] * fs.ia[1], at = a[2][n + i] * fs.ia[2];
+                                const float aw = a[3][n + i] * fs.ia[3];
                                 float sg, d1, d2, d3;
                                 act3f<ACT, FAST>(av, sg, d1, d2, d3);
-                                a[0][n] = sg;
-                                a[1][n] = d1 * ax;
-                                a[2][n] = d1 * at;
-                                a[3][n] = d2 * ax * ax + d1 * aw;
+                                z[i][0] = sg;
+                                z[i][1] = d1 * ax;
+                                z[i][2] = d1 * at;
+                                z[i][3] = fmaf(d2 * ax, ax, d1 * aw);
                             }
-                            TC_MARK(3);
-                            if (ch > 0) {
-                                wait_mma2();  // P2(ch-1): Z free, its Y product ready
-                                if (tid == 0) issue(q + NBUF - 1);
-                                if (ch % YACC == 0) add_y(tlane + TM_Y + half * NG, ysum);  // a group of YACC chunks is complete
-                            }
-                            TC_MARK(0);
-    #pragma unroll
+#pragma unroll
                             for (int c = 0; c < 4; ++c) {
-                                float hi[NG], lo[NG];
-    #pragma unroll
-                                for (int n = 0; n < NG; ++n) umma::split_tf32(a[c][n], hi[n], lo[n]);
-                                tst(tlane + TM_ZH + c * KC + half * NG, hi);
-                                tst(tlane + TM_ZL + c * KC + half * NG, lo);
+                                const float s = umma::exp2i(fs.ez[c]);
+                                umma::split16x2(z[0][c] * s, z[1][c] * s, zh[c][n / 2], zl[c][n / 2]);
                             }
-                            umma::tmem_st_wait();
-                            signal(&zready);
                         }
+                        TC_MARK(3);
+                        if (ch > 0) {
+                            wait(&zfree, zw & 1);  // P2(q - 1): Z free, its Y product ready
+                            ++zw;
+                            if (ch % YACC == 0) add_acc(tlane + TM_Y + NG * h, fs.iy, ysum);
+                        }
+                        TC_MARK(0);
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const uint32_t zc = tlane + TM_Z + c * 32 + (NG / 2) * h;
+                            umma::tmem_st4u(zc, zh[c][0], zh[c][1], zh[c][2], zh[c][3]);
+                            umma::tmem_st4u(zc + 16, zl[c][0], zl[c][1], zl[c][2], zl[c][3]);
+                        }
+                        umma::tmem_st_wait();
+                        signal(BAR_ZFULL);
+                        TC_MARK(4);
                     }
-                    TC_MARK(4);
-                    if (warp == ISSUER) {
-                        TC_ISSUE_BEGIN();
-                        await(&p1free, phf);  // every chunk (keeps the phase count)
-                        if (ch + 1 < net.nc[l]) fwd_p1(q + 1);
-                        if (lane == 0) TC_ISSUE_END();
-                    }
-                    if (warp == ISSUER2) {
-                        await(&zready, phz);
-                        fwd_p2(q, ch);
-                    }
-                    TC_MARK(5);
                 }
-                // transition end: Y -> y_{l+1} (scratch), SY = s (.) y (smem hi / lo)
-                TC_MARK(0);
+                // transition end: Y -> y_{l+1} (scratch), then SY_{l+1} or the output layer
+                const bool last = l + 2 == L;
+                const double* sl = sv + net.soff[l + 1];
+                const int rtrue = net.r[l + 1];
                 if (warp < NWE) {
-                    wait_mma2();
-                    TC_MARK(5);
-                    const double* sl = sv + net.soff[l + 1];
-                    const int rtrue = net.r[l + 1];
-                    float (&y)[4][NG] = ysum;
-                    add_y(tlane + TM_Y + half * NG, y);
+                    wait(&zfree, zw & 1);
+                    ++zw;
+                    add_acc(tlane + TM_Y + NG * h, fs.iy, ysum);
+                    TC_MARK(13);
+                    float pr[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                    for (int n4 = 0; n4 < NG / 4; ++n4) {
-                        const int j0 = half * NG + 4 * n4;
-                        if (j0 < net.rk[l + 1]) {  // rk is a multiple of 8: a group of 4 is all in or all out
-                            float sj[4];
+                    for (int n = 0; n < NG; ++n) {
+                        const int j = NG * h + n;
+                        float sj = 0.f;
+                        if (j < rtrue) {
+                            v2::st4(scr + net.yoff[l + 1] + (p * rtrue + j) * 4, ysum[0][n], ysum[1][n], ysum[2][n],
+                                    ysum[3][n]);
+                            sj = float(sl[j]);
+                            if (last) sj *= net.ulast[j];
+                        }
 #pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                const int j = j0 + i, n = 4 * n4 + i;
-                                sj[i] = j < rtrue ? float(sl[j]) : 0.f;
-                                if (j < rtrue)
-                                    v2::st4(scr + net.yoff[l + 1] + (p * rtrue + j) * 4, y[0][n], y[1][n], y[2][n],
-                                            y[3][n]);
+                        for (int c = 0; c < 4; ++c) {
+                            const float v = sj * ysum[c][n];
+                            pr[c] = last ? pr[c] + v : fmaf(v, v, pr[c]);
+                            if (!last) ysum[c][n] = v;  // SY_{l+1}
+                        }
+                    }
+                    *reinterpret_cast<float4*>(xch + (h * P + p) * 8) = make_float4(pr[0], pr[1], pr[2], pr[3]);
+                }
+                TC_MARK(5);
+                __syncthreads();
+                if (warp < NWE) {
+                    float nr[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int hh = 0; hh < 4; ++hh) {
+                        const float4 v = *reinterpret_cast<const float4*>(xch + (hh * P + p) * 8);
+                        nr[0] += v.x;
+                        nr[1] += v.y;
+                        nr[2] += v.z;
+                        nr[3] += v.w;
+                    }
+                    if (!last) {
+                        int e[4];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            nr[c] = sqrtf(nr[c]);
+                            e[c] = umma::pow2_exp(nr[c]);
+                            fs.ia[c] = umma::exp2i(-e[c]) * net.isU[l + 1];
+                        }
+                        if (NG * h < net.rk[l + 1]) put_rows(X, p, h, ysum, e);
+                        const float mu = net.muU[l + 1];
+                        const float bx = nr[1] * mu, bt = nr[2] * mu, bw = nr[3] * mu;
+                        fs.ez[0] = umma::pow2_exp(1.f);
+                        fs.ez[1] = umma::pow2_exp(bx);
+                        fs.ez[2] = umma::pow2_exp(bt);
+                        fs.ez[3] = umma::pow2_exp(fmaf(bx, bx, bw));
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) fs.iy[c] = umma::exp2i(-fs.ez[c]) * net.isV[l + 1];
+                    } else {
+                        // ---------------- output layer (M_L = 1) + residual ----------------
+                        float u[4] = {nr[0] + net.ulast[rtrue], nr[1], nr[2], nr[3]};
+                        const float N = u[2] + mu0 * u[1] - mu1 * u[3] - mu2 * u[0] * (1.f - u[0]);
+                        const float term = valid ? w * (N * N) : 0.f;
+                        if (h == 0) {
+                            if (valid && !isfinite(term)) atomicMin(bad, static_cast<unsigned long long>(gp));
+                            red[P * RPS + p] = term;
+                        }
+                        const float gN = valid ? 2.f * N * w : 0.f;
+                        const float gu[4] = {gN * (-mu2 * (1.f - 2.f * u[0])), gN * mu0, gN, -gN * mu1};
+                        // ST_{L-1} (own ranks) and the dL/ds_{L-1} partials; y_{L-1} is ysum
+                        float st[4][NG];
+                        float ss[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                        for (int n = 0; n < NG; ++n) {
+                            const int j = NG * h + n;
+                            const float uj = j < rtrue ? net.ulast[j] : 0.f;
+                            const float sj = j < rtrue ? float(sl[j]) : 0.f;
+                            float cd = 0.f;
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                cd = fmaf(uj * gu[c], ysum[c][n], cd);
+                                st[c][n] = sj * uj * gu[c];
+                                ss[c] = fmaf(st[c][n], st[c][n], ss[c]);
+                            }
+                            if (j < RP) red[p * RPS + j] = cd;
+                        }
+                        // SY_{L-2} from y_{L-2} (the first reverse transition recomputes A_{L-2})
+                        const int lr = L - 2, rr = net.r[lr];
+                        const double* sr = sv + net.soff[lr];
+                        float sy[4][NG];
+                        float ssy[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                        for (int n = 0; n < NG; ++n) {
+                            const int j = NG * h + n;
+                            float y4[4] = {0.f, 0.f, 0.f, 0.f};
+                            float sj = 0.f;
+                            if (j < rr) {
+                                v2::ld4(scr + net.yoff[lr] + (p * rr + j) * 4, y4);
+                                sj = float(sr[j]);
                             }
 #pragma unroll
-                            for (int c = 0; c < 4; ++c)
-                                put_split4(sm, c, p, j0, sj[0] * y[c][4 * n4], sj[1] * y[c][4 * n4 + 1],
-                                           sj[2] * y[c][4 * n4 + 2], sj[3] * y[c][4 * n4 + 3]);
+                            for (int c = 0; c < 4; ++c) {
+                                sy[c][n] = sj * y4[c];
+                                ssy[c] = fmaf(sy[c][n], sy[c][n], ssy[c]);
+                            }
                         }
+                        named_bar_epi();  // every epilogue thread has read the u partials
+                        *reinterpret_cast<float4*>(xch + (h * P + p) * 8) = make_float4(ss[0], ss[1], ss[2], ss[3]);
+                        *reinterpret_cast<float4*>(xch + (h * P + p) * 8 + 4) = make_float4(ssy[0], ssy[1], ssy[2], ssy[3]);
+                        named_bar_epi();
+                        float nst[4] = {0.f, 0.f, 0.f, 0.f}, nsy[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                        for (int hh = 0; hh < 4; ++hh) {
+                            const float4 v = *reinterpret_cast<const float4*>(xch + (hh * P + p) * 8);
+                            const float4 v2 = *reinterpret_cast<const float4*>(xch + (hh * P + p) * 8 + 4);
+                            nst[0] += v.x;
+                            nst[1] += v.y;
+                            nst[2] += v.z;
+                            nst[3] += v.w;
+                            nsy[0] += v2.x;
+                            nsy[1] += v2.y;
+                            nsy[2] += v2.z;
+                            nsy[3] += v2.w;
+                        }
+                        rev_scales(rs, nst, nsy, lr, st, sy);
                     }
                 }
                 umma::fence_async_smem();
                 umma::fence_before();
                 __syncthreads();
+                if (last) {
+                    reduce_points(red, acc, net.soff[L - 1], net.r[L - 1], tid);
+                    if (tid == NT - 1) {
+                        float sacc = 0.f;
+                        for (int pp = 0; pp < P; ++pp) sacc += red[P * RPS + pp];
+                        acc[0] += sacc;
+                    }
+                    __syncthreads();
+                }
+                TC_MARK(6);
             }
 
-            TC_MARK(6);
-            // ---------------- output layer (M_L = 1) + residual ----------------
-            {
-                const int rL = net.r[L - 1];
-                const double* sL = sv + net.soff[L - 1];
-                if (half == 0) {
-                    float u[4] = {0.f, 0.f, 0.f, 0.f};
-                    for (int j = 0; j < rL; ++j) {
-                        float y4[4];
-                        v2::ld4(scr + net.yoff[L - 1] + (p * rL + j) * 4, y4);
-                        const float us = net.ulast[j] * float(sL[j]);
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) u[c] = fmaf(us, y4[c], u[c]);
-                    }
-                    u[0] += net.ulast[rL];
-                    const float N = u[2] + mu0 * u[1] - mu1 * u[3] - mu2 * u[0] * (1.f - u[0]);
-                    const float term = valid ? w * (N * N) : 0.f;
-                    if (valid && !isfinite(term)) atomicMin(bad, static_cast<unsigned long long>(gp));
-                    const float gN = valid ? 2.f * N * w : 0.f;
-                    const float gu[4] = {gN * (-mu2 * (1.f - 2.f * u[0])), gN * mu0, gN, -gN * mu1};
-                    red[P * RPS + p] = term;
-                    for (int j = 0; j < net.rk[L - 1]; ++j) {
-                        const float uj = j < rL ? net.ulast[j] : 0.f;
-                        const float sj = j < rL ? float(sL[j]) : 0.f;
-                        float cd = 0.f;
-                        if (j < rL) {
-                            float y4[4];
-                            v2::ld4(scr + net.yoff[L - 1] + (p * rL + j) * 4, y4);
-#pragma unroll
-                            for (int c = 0; c < 4; ++c) cd = fmaf(uj * gu[c], y4[c], cd);
-                        }
-                        red[p * RPS + j] = cd;
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) put_split(sm, c, p, j, sj * uj * gu[c]);
-                    }
-                }
-                umma::fence_async_smem();
-                __syncthreads();
-                reduce_points(red, acc, net.soff[L - 1], rL, tid);
-                if (tid == NT - 1) {
-                    float sacc = 0.f;
-                    for (int pp = 0; pp < P; ++pp) sacc += red[P * RPS + pp];
-                    acc[0] += sacc;
-                }
-                __syncthreads();
-            }
-
-            TC_MARK(7);
             // ---------------- reverse transitions ----------------
             for (int l = L - 2; l >= 0; --l) {
-                const int rkn = net.rk[l + 1], rnl = net.rn[l];
+                const int rkl = net.rk[l], rkn = net.rk[l + 1], rnl = net.rn[l], nc = net.nc[l];
+                const int bbias = 4 * KC * rkl, bu = bbias + 4 * KC + 4 * KC * rkn;  // byte offsets in the reverse block
                 float tsum[4][NG];
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
 #pragma unroll
                     for (int n = 0; n < NG; ++n) tsum[c][n] = 0.f;
-                // factor block of chunk qq: V_H | V_L (KC x rkn, rows KC) | UT_H | UT_L (rnl x KC)
-                auto bwd_p1 = [&](int64_t qq) {
-                    wait_slot(qq);
-                    mma_p1(static_cast<int>(qq % NBUF) * BUF, rkn);
-                };
-                auto bwd_p2 = [&](int64_t qq, int ch) {
-                    mma_p2(static_cast<int>(qq % NBUF) * BUF + 2 * KC * rkn, rnl, ch % YACC != 0);
-                };
-                if (warp == ISSUER) bwd_p1(q);
-                for (int ch = 0; ch < net.nc[l]; ++ch, ++q) {
-                    if (warp < NWE) {
-                        // stored pre-activations of this chunk (in flight during the MMAs)
-                        const float* Ast = ascr + net.aoff[l] + static_cast<int64_t>(ch) * (P * KC * 4);
-                        float a[4][NG];
-    #pragma unroll
-                        for (int n = 0; n < NG; ++n) {
-                            float a4[4];
-                            v2::ld4(Ast + aidx(half * NG + n, p), a4);
-    #pragma unroll
-                            for (int c = 0; c < 4; ++c) a[c][n] = a4[c];
+                if (warp == ISSUER) issue_rev_p1(q, rq, rkl, rkn);
+                for (int ch = 0; ch < nc; ++ch, ++q, ++rq) {
+                    if (warp == ISSUER) {
+                        if (ch + 1 < nc) issue_rev_p1(q + 1, rq + 1, rkl, rkn);
+                    } else if (warp == ISSUER2) {
+                        issue_p2(q, slot(q) + bu, rnl, ch % YACC != 0);
+                    } else {
+                        TC_MARK(7);
+                        wait(&rfull, rq & 1);
+                        TC_MARK(8);
+                        const float* bias = reinterpret_cast<const float*>(slot(q) + bbias);
+                        uint32_t gh[4][NG / 2], gl[4][NG / 2];
+#pragma unroll
+                        for (int hf = 0; hf < 2; ++hf) {
+                            float a[4][NG / 2], dz[4][NG / 2];
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                umma::tmem_ld4(tlane + TM_R + c * 32 + NG * h + 4 * hf, a[c]);
+                                umma::tmem_ld4(tlane + TM_R + 128 + c * 32 + NG * h + 4 * hf, dz[c]);
+                            }
+                            umma::tmem_ld_wait();
+                            if (hf == 1) signal(BAR_RFREE);  // A / DZ consumed: the next chunk's MMAs may start
+#pragma unroll
+                            for (int n = 0; n < NG / 2; n += 2) {
+                                float gg[2][4];
+#pragma unroll
+                                for (int i = 0; i < 2; ++i) {
+                                    const int k = NG * h + 4 * hf + n + i;
+                                    const float av = fmaf(a[0][n + i], rs.ia[0], bias[k]);
+                                    const float ax = a[1][n + i] * rs.ia[1], at = a[2][n + i] * rs.ia[2];
+                                    const float aw = a[3][n + i] * rs.ia[3];
+                                    const float g0 = dz[0][n + i] * rs.id[0], g1 = dz[1][n + i] * rs.id[1];
+                                    const float g2 = dz[2][n + i] * rs.id[2], g3 = dz[3][n + i] * rs.id[3];
+                                    float sg, d1, d2, d3;
+                                    act3f<ACT, FAST>(av, sg, d1, d2, d3);
+                                    gg[i][0] = g0 * d1 + g1 * d2 * ax + g2 * d2 * at + g3 * (d3 * ax * ax + d2 * aw);
+                                    gg[i][1] = g1 * d1 + g3 * 2.f * d2 * ax;
+                                    gg[i][2] = g2 * d1;
+                                    gg[i][3] = g3 * d1;
+                                }
+#pragma unroll
+                                for (int c = 0; c < 4; ++c) {
+                                    const float s = umma::exp2i(rs.eg[c]);
+                                    umma::split16x2(gg[0][c] * s, gg[1][c] * s, gh[c][2 * hf + n / 2],
+                                                    gl[c][2 * hf + n / 2]);
+                                }
+                            }
                         }
                         TC_MARK(9);
-                        wait_mma1();
-                        TC_MARK(10);
-                        if (ch == 0 && tid == 0) issue(q + NBUF - 1);
-                        {
-                            float dz[4][NG];
-                            ld_p1_halves(tlane + TM_P1 + half * NG, dz);
-    #pragma unroll
-                            for (int n = 0; n < NG; ++n) {
-                                if (n == NG / 2) {
-                                    umma::tmem_ld_wait();
-                                    signal(&p1free);
-                                }
-                                const float av = a[0][n], ax = a[1][n], at = a[2][n], aw = a[3][n];
-                                const float g0 = dz[0][n], g1 = dz[1][n], g2 = dz[2][n], g3 = dz[3][n];
-                                float sg, d1, d2, d3;
-                                act3f<ACT, FAST>(av, sg, d1, d2, d3);
-                                dz[0][n] = g0 * d1 + g1 * d2 * ax + g2 * d2 * at + g3 * (d3 * ax * ax + d2 * aw);
-                                dz[1][n] = g1 * d1 + g3 * 2.f * d2 * ax;
-                                dz[2][n] = g2 * d1;
-                                dz[3][n] = g3 * d1;
-                            }
-                            TC_MARK(11);
-                            if (ch > 0) {
-                                wait_mma2();  // P2(ch-1): G free, its T product ready
-                                if (tid == 0) issue(q + NBUF - 1);
-                                if (ch % YACC == 0) add_y(tlane + TM_Y + half * NG, tsum);
-                            }
-                            TC_MARK(8);
-    #pragma unroll
-                            for (int c = 0; c < 4; ++c) {
-                                float hi[NG], lo[NG];
-    #pragma unroll
-                                for (int n = 0; n < NG; ++n) umma::split_tf32(dz[c][n], hi[n], lo[n]);
-                                tst(tlane + TM_ZH + c * KC + half * NG, hi);
-                                tst(tlane + TM_ZL + c * KC + half * NG, lo);
-                            }
-                            umma::tmem_st_wait();
-                            signal(&zready);
+                        if (ch > 0) {
+                            wait(&zfree, zw & 1);  // P2r(q - 1): G free, its T product ready
+                            ++zw;
+                            if (ch % YACC == 0) add_acc(tlane + TM_Y + NG * h, rs.it, tsum);
                         }
-                    }
-                    TC_MARK(12);
-                    if (warp == ISSUER) {
-                        await(&p1free, phf);  // every chunk (keeps the phase count)
-                        if (ch + 1 < net.nc[l]) bwd_p1(q + 1);
-                    }
-                    if (warp == ISSUER2) {
-                        await(&zready, phz);
-                        bwd_p2(q, ch);
+                        TC_MARK(10);
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const uint32_t zc = tlane + TM_Z + c * 32 + (NG / 2) * h;
+                            umma::tmem_st4u(zc, gh[c][0], gh[c][1], gh[c][2], gh[c][3]);
+                            umma::tmem_st4u(zc + 16, gl[c][0], gl[c][1], gl[c][2], gl[c][3]);
+                        }
+                        umma::tmem_st_wait();
+                        signal(BAR_ZFULL);
+                        TC_MARK(11);
                     }
                 }
-                // transition end: T -> dL/ds_l partials, ST = s_l (.) T (smem hi / lo)
-                TC_MARK(8);
+                // transition end: T -> dL/ds_l partials; ST_l and SY_{l-1} for the next reverse transition
+                const int rl = net.r[l];
+                const double* sl = sv + net.soff[l];
                 if (warp < NWE) {
-                    const double* sl = sv + net.soff[l];
-                    const int rtrue = net.r[l];
-                    // this thread's y_l (scratch, usually an L2 / HBM round trip): all loads issued
-                    // together and before the wait for the last phase-2 product
                     float4 yv[NG];
 #pragma unroll
                     for (int n = 0; n < NG; ++n) {
-                        const int j = half * NG + n;
-                        yv[n] = j < rtrue ? *reinterpret_cast<const float4*>(scr + net.yoff[l] + (p * rtrue + j) * 4)
-                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+                        const int j = NG * h + n;
+                        yv[n] = j < rl ? *reinterpret_cast<const float4*>(scr + net.yoff[l] + (p * rl + j) * 4)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
                     }
-                    wait_mma2();
-                    TC_MARK(13);
-                    float (&tt)[4][NG] = tsum;
-                    add_y(tlane + TM_Y + half * NG, tt);
+                    wait(&zfree, zw & 1);
+                    ++zw;
+                    add_acc(tlane + TM_Y + NG * h, rs.it, tsum);
+                    TC_MARK(14);
+                    float ss[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                    for (int n4 = 0; n4 < NG / 4; ++n4) {
-                        const int j0 = half * NG + 4 * n4;
-                        if (j0 < net.rk[l]) {  // rk is a multiple of 8
-                            float sj[4];
+                    for (int n = 0; n < NG; ++n) {
+                        const int j = NG * h + n;
+                        const float sj = j < rl ? float(sl[j]) : 0.f;
+                        float cd = tsum[0][n] * yv[n].x;
+                        cd = fmaf(tsum[1][n], yv[n].y, cd);
+                        cd = fmaf(tsum[2][n], yv[n].z, cd);
+                        cd = fmaf(tsum[3][n], yv[n].w, cd);
+                        if (j < RP) red[p * RPS + j] = cd;
 #pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                const int j = j0 + i, n = 4 * n4 + i;
-                                float cd = 0.f;
-                                sj[i] = 0.f;
-                                if (j < rtrue) {
-                                    sj[i] = float(sl[j]);
-                                    const float y4[4] = {yv[n].x, yv[n].y, yv[n].z, yv[n].w};
-#pragma unroll
-                                    for (int c = 0; c < 4; ++c) cd = fmaf(tt[c][n], y4[c], cd);
-                                }
-                                red[p * RPS + j] = cd;
-                            }
-#pragma unroll
-                            for (int c = 0; c < 4; ++c)
-                                put_split4(sm, c, p, j0, sj[0] * tt[c][4 * n4], sj[1] * tt[c][4 * n4 + 1],
-                                           sj[2] * tt[c][4 * n4 + 2], sj[3] * tt[c][4 * n4 + 3]);
+                        for (int c = 0; c < 4; ++c) {
+                            tsum[c][n] *= sj;  // ST_l
+                            ss[c] = fmaf(tsum[c][n], tsum[c][n], ss[c]);
                         }
                     }
+                    if (l >= 1) {
+                        const int rr = net.r[l - 1];
+                        const double* sr = sv + net.soff[l - 1];
+                        float sy[4][NG];
+                        float ssy[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                        for (int n = 0; n < NG; ++n) {
+                            const int j = NG * h + n;
+                            float y4[4] = {0.f, 0.f, 0.f, 0.f};
+                            float sj = 0.f;
+                            if (j < rr) {
+                                v2::ld4(scr + net.yoff[l - 1] + (p * rr + j) * 4, y4);
+                                sj = float(sr[j]);
+                            }
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                sy[c][n] = sj * y4[c];
+                                ssy[c] = fmaf(sy[c][n], sy[c][n], ssy[c]);
+                            }
+                        }
+                        *reinterpret_cast<float4*>(xch + (h * P + p) * 8) = make_float4(ss[0], ss[1], ss[2], ss[3]);
+                        *reinterpret_cast<float4*>(xch + (h * P + p) * 8 + 4) = make_float4(ssy[0], ssy[1], ssy[2], ssy[3]);
+                        named_bar_epi();
+                        float nst[4] = {0.f, 0.f, 0.f, 0.f}, nsy[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                        for (int hh = 0; hh < 4; ++hh) {
+                            const float4 v = *reinterpret_cast<const float4*>(xch + (hh * P + p) * 8);
+                            const float4 v2 = *reinterpret_cast<const float4*>(xch + (hh * P + p) * 8 + 4);
+                            nst[0] += v.x;
+                            nst[1] += v.y;
+                            nst[2] += v.z;
+                            nst[3] += v.w;
+                            nsy[0] += v2.x;
+                            nsy[1] += v2.y;
+                            nsy[2] += v2.z;
+                            nsy[3] += v2.w;
+                        }
+                        rev_scales(rs, nst, nsy, l - 1, tsum, sy);
+                    }
                 }
+                TC_MARK(15);
                 umma::fence_async_smem();
                 umma::fence_before();
                 __syncthreads();
-                reduce_points(red, acc, net.soff[l], net.r[l], tid);
+                reduce_points(red, acc, net.soff[l], rl, tid);
                 __syncthreads();
-                TC_MARK(14);
+                TC_MARK(12);
             }
         }
         for (int k = tid; k < R1; k += NT) {
@@ -709,21 +830,12 @@ pinn_tc_kernel(const NetTC<> net, const RunGeom g, const double* __restrict__ pt
         __syncthreads();
         unit = next_unit;
     }
-    if (tid == 0)
-        for (int64_t qq = q; qq < q + NBUF - 1; ++qq) wait_slot(qq);  // prefetches past the last chunk
+    if (producer)
+        for (int64_t qq = q; qq < q + NBUF - 1; ++qq) wait_slot(qq);  // copies past the last chunk
     TC_FLUSH();
     umma::fence_before();
     __syncthreads();
     if (warp == 0) umma::tmem_dealloc<512>(tbase);
-#ifdef TC_CTA_TIMES
-    if (tid == 0) {
-        unsigned long long _t_end;
-        unsigned _smid;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t_end));
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(_smid));
-        printf("CTA %d %u %llu %llu %lld\n", blockIdx.x, _smid, _t_start, _t_end, (long long)total_tiles);
-    }
-#endif
 }
 
 }  // namespace tc

@@ -16,6 +16,7 @@
 //     32*(w%4) .. 32*(w%4)+31.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -159,6 +160,69 @@ __device__ __forceinline__ void mma_commit_w(uint64_t* mbar) {
         : "memory");
 }
 
+// ---- kind::f16 (FP16 operands, FP32 accumulate), issued by one elected lane ----
+// instruction descriptor: c_format F32 = 1 << 4, a / b format F16 = 0, K-major A and B
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+    return (1u << 4) | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
+}
+// D[tmem] (+)= A[smem desc] * B[smem desc]; descriptors = 32-bit low words + shared high word
+__device__ __forceinline__ void mma16_ss(uint32_t d, uint32_t a_lo, uint32_t b_lo, uint32_t hi, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b64 da, db;\n\t"
+        "mov.b64 da, {%1, %5};\n\t"
+        "mov.b64 db, {%2, %5};\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %3, p;\n\t}" ::"r"(d),
+        "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(accumulate), "r"(hi)
+        : "memory");
+}
+// D[tmem] (+)= A[tmem: lane = row, two 16-bit K elements per column, low half first] * B[smem desc]
+__device__ __forceinline__ void mma16_ts(uint32_t d, uint32_t a_tmem, uint32_t b_lo, uint32_t hi, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b64 db;\n\t"
+        "mov.b64 db, {%2, %4};\n\t"
+        "setp.ne.b32 p, %3, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], db, %5, p;\n\t}" ::"r"(d),
+        "r"(a_tmem), "r"(b_lo), "r"(accumulate), "r"(hi), "r"(idesc)
+        : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+    uint32_t e;
+    asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(e));
+    return e != 0;
+}
+
+// byte offset of (row, k) in a K-major SWIZZLE_NONE canonical tile of 16-bit elements
+// with `rows` rows: core matrices of 8 rows x 16 B, stored [K/8][rows/8][8][8];
+// LBO = (rows / 8) * 128 B (K direction), SBO = 128 B (8-row groups).  A K step of 16
+// elements starts 2 * LBO bytes further (descriptor low word + rows * 2).
+__host__ __device__ __forceinline__ int kmaj16_off(int row, int k, int rows) {
+    return ((((k >> 3) * (rows >> 3) + (row >> 3)) << 3) + (row & 7)) * 16 + (k & 7) * 2;
+}
+
+// FP16 two-term split of x (already scaled so |x| <= 2^14): hi = fp16(x), lo = fp16(x - hi);
+// two values per 32-bit word (first value in the low half).  hi*hi + hi*lo + lo*hi
+// reproduces an FP32 product to ~2^-22 (scripts/umma_f16_test.cu).
+__device__ __forceinline__ void split16x2(float x0, float x1, uint32_t& h, uint32_t& l) {
+    uint32_t hh, ll;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hh) : "f"(x1), "f"(x0));
+    float f0, f1;
+    asm("{\n\t.reg .f16 a, b;\n\tmov.b32 {a, b}, %2;\n\tcvt.f32.f16 %0, a;\n\tcvt.f32.f16 %1, b;\n\t}"
+        : "=f"(f0), "=f"(f1)
+        : "r"(hh));
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(ll) : "f"(x1 - f1), "f"(x0 - f0));
+    h = hh;
+    l = ll;
+}
+// power-of-two scale 2^k for a non-negative bound b: b * 2^k < 2^15, k clamped to [-100, 100]
+__device__ __forceinline__ int pow2_exp(float b) {
+    const int E = static_cast<int>((__float_as_uint(b) >> 23) & 0xff);  // b < 2^(E - 126)
+    return max(-100, min(100, 140 - E));
+}
+__device__ __forceinline__ float exp2i(int k) { return __uint_as_float(static_cast<uint32_t>(127 + k) << 23); }
+
 // ---- TMEM <-> registers (warp-collective) ----
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     uint32_t r[16];
@@ -197,6 +261,13 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const float (&v)[8]) {
                  "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
                  "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
                  : "memory");
+}
+__device__ __forceinline__ void tmem_st4u(uint32_t taddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_st2u(uint32_t taddr, uint32_t a, uint32_t b) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr), "r"(a), "r"(b) : "memory");
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 

@@ -17,15 +17,15 @@ out = (C.c_ulonglong * 16)()
 lib.lrnr_dev_tc_timing(out)
 ctx.loss_grad_s(pkg.MODEL_LRNR, c['s'], c['mu'])
 lib.lrnr_dev_tc_timing(out)
-names = ["fwd: wait P2(ch-1) + add_y", "fwd: P1/P2 issue -> chunk top", "fwd: wait mma1 (P1)", "fwd: epilogue act jet + A store",
-         "fwd: Z split/st + sync", "fwd: issuer block (skip) + trans-end wait P2", "fwd: trans end Y->SY", "output layer",
-         "bwd: wait P2(ch-1) + add_t", "bwd: chunk top + A loads", "bwd: wait mma1 (P1)", "bwd: epilogue VJP",
-         "bwd: G split/st + sync", "bwd: trans-end wait P2", "bwd: trans end + ds reduce", "-"]
-tot = sum(out[:15])
+names = ["fwd: wait P2(ch-1) + add_y", "fwd: chunk top", "fwd: wait P1", "fwd: epilogue act jet + Z split",
+         "fwd: Z store + signal", "fwd: trans end (Y, exchange)", "fwd: trans end (SY / output layer)",
+         "bwd: chunk top", "bwd: wait A / DZ", "bwd: epilogue VJP + G split", "bwd: wait P2r(ch-1) + add_t",
+         "bwd: G store + signal", "bwd: trans end: syncs + reduce_points", "fwd: trans end: wait P2 + add_y",
+         "bwd: trans end: wait P2r + add_t", "bwd: trans end: ds, y loads, exchange, ST / SY"]
+tot = sum(out[:16])
 tiles = 4
-for i in range(15):
+for i in range(16):
     print(f"{names[i]:40s} {out[i]/tiles:12.0f} cycles/tile  {out[i]/tot*100:5.1f}%")
-print(f"tid0 fwd issue P1+P2 (incl. weight wait): {out[15]/tiles/48:.0f} cycles/chunk")
 print("total cycles per tile", tot / tiles, " chunks per tile", 96)
 import time
 import torch
