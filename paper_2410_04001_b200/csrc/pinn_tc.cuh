@@ -64,9 +64,8 @@ constexpr int OFF_W = OFF_X + 4 * OPD_SLOT;    // reverse: SY_l for the recomput
 constexpr int BUF = 3 * (4 * KC * RP) + 4 * KC;  // largest chunk block: three fp16 hi / lo 32 x 32 tiles + bias
 constexpr int NBUF = 4;
 constexpr int OFF_B0 = OFF_W + 4 * OPD_SLOT;
-constexpr int OFF_RED = OFF_B0 + NBUF * BUF;   // floats: [P][RPS] + P (loss) + [NWE][RP] partials
-constexpr int RPS = RP + 1;                    // odd point stride: conflict-free column writes
-constexpr int OFF_XCH = OFF_RED + (P * RPS + P + NWE * RP) * 4;  // floats [4 groups][P][8]
+constexpr int OFF_RED = OFF_B0 + NBUF * BUF;   // floats: per-warp-quarter partials [layer][4][RP], loss [4]
+constexpr int OFF_XCH = OFF_RED + (kMaxL * 4 * RP + 4) * 4;  // floats [4 groups][P][8]
 constexpr int OFF_ACC = OFF_XCH + 4 * P * 8 * 4;
 constexpr int SMEM_BYTES = OFF_ACC + 1024 * 4;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
@@ -80,7 +79,7 @@ struct NetTC {
     int rn[kMaxL];         // padded rank as MMA N (16 or 32)
     int nc[kMaxL];
     int soff[kMaxL + 1];
-    int yoff[kMaxL];       // y_l in per-CTA scratch: [p][j (r_l)][4]
+    int yoff[kMaxL];       // y_l in per-CTA scratch: [j (r_l)][p][4] (a layer is one contiguous block)
     int ystride;
     float isU[kMaxL];      // 1 / (power-of-two scale of U_l) and of V_l
     float isV[kMaxL];
@@ -124,26 +123,21 @@ __device__ unsigned long long g_tc_timing[16];
 #define TC_FLUSH()
 #endif
 
-// acc[1 + off + j] += sum_p red[p][j] for j < r, fixed order: NWE groups of P / NWE
-// points in parallel (one thread per (group, rank)), then the partials.
-__device__ __forceinline__ void reduce_points(float* red, float* acc, int off, int r, int tid) {
-    float* part = red + P * RPS + P;
-    if (tid < NWE * RP) {
-        const int j = tid % RP, g = tid / RP;
-        float s = 0.f;
-        if (j < r)
+// Sum of v[0..7] over the warp's 32 lanes (points), fixed butterfly order: lanes with
+// (lane & 3) == 0 return the sum of value ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1).
+__device__ __forceinline__ float warp_sum8(const float (&v)[8], int lane) {
+    float a[4], b[2];
+    const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4;
 #pragma unroll
-            for (int i = 0; i < P / NWE; ++i) s += red[((P / NWE) * g + i) * RPS + j];
-        part[g * RP + j] = s;
-    }
-    __syncthreads();
-    if (tid < r) {
-        float s = 0.f;
+    for (int i = 0; i < 4; ++i) a[i] = (u16 ? v[i + 4] : v[i]) + __shfl_xor_sync(0xffffffffu, u16 ? v[i] : v[i + 4], 16);
 #pragma unroll
-        for (int g = 0; g < NWE; ++g) s += part[g * RP + tid];
-        acc[1 + off + tid] += s;
-    }
+    for (int i = 0; i < 2; ++i) b[i] = (u8 ? a[i + 2] : a[i]) + __shfl_xor_sync(0xffffffffu, u8 ? a[i] : a[i + 2], 8);
+    float c = (u4 ? b[1] : b[0]) + __shfl_xor_sync(0xffffffffu, u4 ? b[0] : b[1], 4);
+    c += __shfl_xor_sync(0xffffffffu, c, 2);
+    c += __shfl_xor_sync(0xffffffffu, c, 1);
+    return c;
 }
+__device__ __forceinline__ int warp_sum8_index(int lane) { return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1); }
 
 // acc[c][n] += iv[c] * TMEM[taddr + c * 32 + n] (YACC chunks of phase-2 products, unscaled)
 __device__ __forceinline__ void add_acc(uint32_t taddr, const float (&iv)[4], float (&acc)[4][NG]) {
@@ -200,7 +194,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                const double* __restrict__ mus, const float w, float* __restrict__ scratch, float* __restrict__ part,
                unsigned long long* __restrict__ bad, unsigned long long* __restrict__ unit_ctr) {
     extern __shared__ __align__(1024) unsigned char smb[];
-    float* red = reinterpret_cast<float*>(smb + OFF_RED);
+    float* tpart = reinterpret_cast<float*>(smb + OFF_RED);  // [layer][quarter][rank], then loss [quarter]
     float* xch = reinterpret_cast<float*>(smb + OFF_XCH);
     float* acc = reinterpret_cast<float*>(smb + OFF_ACC);
     unsigned char* X = smb + OFF_X;
@@ -209,6 +203,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
     __shared__ __align__(8) uint64_t p1full[2];  // forward P1 buffers written (tcgen05.commit)
     __shared__ __align__(8) uint64_t rfull;      // reverse A / DZ written
     __shared__ __align__(8) uint64_t zfree;      // P2 done: Z / G free, Y / T product ready
+    __shared__ __align__(8) uint64_t ybar;       // y_l block copied into W (TMA)
     __shared__ uint32_t tmem_base;
     __shared__ int64_t next_unit;
 
@@ -227,6 +222,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
         for (int i = 0; i < 2; ++i) umma::mbar_init(&p1full[i], 1);
         umma::mbar_init(&rfull, 1);
         umma::mbar_init(&zfree, 1);
+        umma::mbar_init(&ybar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     umma::fence_before();
@@ -348,6 +344,18 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
         __syncwarp();
     };
 
+    // ISSUER lane 0: copy the y_l block of this CTA's scratch into W (the epilogue builds
+    // SY_l there); the writers fenced their stores for the async proxy
+    uint32_t yq = 0;  // ybar uses (issuer and epilogue count alike)
+    auto prefetch_y = [&](int l) {
+        if (lane == 0) {
+            const uint32_t bytes = static_cast<uint32_t>(P * net.r[l] * 16);
+            v2::mbar_expect_tx(&ybar, bytes);
+            v2::bulk_g2s(W, scr + net.yoff[l], bytes, &ybar);
+        }
+        __syncwarp();
+    };
+
     // Reverse scales of transition lr from the exchanged squared row norms of ST_{lr+1}
     // (nst) and SY_lr (nsy); writes this thread's K block of ST_{lr+1} into X and of
     // SY_lr into W.  G bound (|sigma'|, |sigma''| <= 1, |sigma'''| <= c3, |DZ_c| <= |ST_c| muV,
@@ -413,7 +421,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                             y4[1] = v0;
                             y4[2] = v1;
                             sj = float(sv[j]);
-                            v2::st4(scr + net.yoff[0] + (p * r0 + j) * 4, y4[0], y4[1], y4[2], y4[3]);
+                            v2::st4(scr + net.yoff[0] + (j * P + p) * 4, y4[0], y4[1], y4[2], y4[3]);
                         }
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
@@ -422,6 +430,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                         }
                     }
                     *reinterpret_cast<float4*>(xch + (h * P + p) * 8) = make_float4(ss[0], ss[1], ss[2], ss[3]);
+                    asm volatile("fence.proxy.async.global;" ::: "memory");  // y_0 may be read by a bulk copy
                 }
                 __syncthreads();
                 if (warp < NWE) {
@@ -464,7 +473,10 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                 for (int c = 0; c < 4; ++c)
 #pragma unroll
                     for (int n = 0; n < NG; ++n) ysum[c][n] = 0.f;
-                if (warp == ISSUER) issue_fwd_p1(q, fq, rk);
+                if (warp == ISSUER) {
+                    if (l + 2 == L) prefetch_y(L - 2);  // W is free in the forward sweep
+                    issue_fwd_p1(q, fq, rk);
+                }
                 for (int ch = 0; ch < nc; ++ch, ++q, ++fq) {
                     if (warp == ISSUER) {
                         if (ch + 1 < nc) issue_fwd_p1(q + 1, fq + 1, rk);
@@ -537,7 +549,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                         const int j = NG * h + n;
                         float sj = 0.f;
                         if (j < rtrue) {
-                            v2::st4(scr + net.yoff[l + 1] + (p * rtrue + j) * 4, ysum[0][n], ysum[1][n], ysum[2][n],
+                            v2::st4(scr + net.yoff[l + 1] + (j * P + p) * 4, ysum[0][n], ysum[1][n], ysum[2][n],
                                     ysum[3][n]);
                             sj = float(sl[j]);
                             if (last) sj *= net.ulast[j];
@@ -550,6 +562,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                         }
                     }
                     *reinterpret_cast<float4*>(xch + (h * P + p) * 8) = make_float4(pr[0], pr[1], pr[2], pr[3]);
+                    asm volatile("fence.proxy.async.global;" ::: "memory");  // y_{l+1} may be read by a bulk copy
                 }
                 TC_MARK(5);
                 __syncthreads();
@@ -587,39 +600,48 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                         const float term = valid ? w * (N * N) : 0.f;
                         if (h == 0) {
                             if (valid && !isfinite(term)) atomicMin(bad, static_cast<unsigned long long>(gp));
-                            red[P * RPS + p] = term;
+                            float tsm = term;
+#pragma unroll
+                            for (int o = 16; o >= 1; o >>= 1) tsm += __shfl_xor_sync(0xffffffffu, tsm, o);
+                            if (lane == 0) tpart[kMaxL * 4 * RP + quarter] = tsm;
                         }
                         const float gN = valid ? 2.f * N * w : 0.f;
                         const float gu[4] = {gN * (-mu2 * (1.f - 2.f * u[0])), gN * mu0, gN, -gN * mu1};
                         // ST_{L-1} (own ranks) and the dL/ds_{L-1} partials; y_{L-1} is ysum
-                        float st[4][NG];
+                        float st[4][NG], cd[NG];
                         float ss[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                         for (int n = 0; n < NG; ++n) {
                             const int j = NG * h + n;
                             const float uj = j < rtrue ? net.ulast[j] : 0.f;
                             const float sj = j < rtrue ? float(sl[j]) : 0.f;
-                            float cd = 0.f;
+                            cd[n] = 0.f;
 #pragma unroll
                             for (int c = 0; c < 4; ++c) {
-                                cd = fmaf(uj * gu[c], ysum[c][n], cd);
+                                cd[n] = fmaf(uj * gu[c], ysum[c][n], cd[n]);
                                 st[c][n] = sj * uj * gu[c];
                                 ss[c] = fmaf(st[c][n], st[c][n], ss[c]);
                             }
-                            if (j < RP) red[p * RPS + j] = cd;
                         }
-                        // SY_{L-2} from y_{L-2} (the first reverse transition recomputes A_{L-2})
+                        {
+                            const float v = warp_sum8(cd, lane);
+                            if ((lane & 3) == 0) tpart[((L - 1) * 4 + quarter) * RP + NG * h + warp_sum8_index(lane)] = v;
+                        }
+                        // SY_{L-2} from y_{L-2} (copied into W during the last forward transition);
+                        // the first reverse transition recomputes A_{L-2} from it
                         const int lr = L - 2, rr = net.r[lr];
                         const double* sr = sv + net.soff[lr];
                         float sy[4][NG];
                         float ssy[4] = {0.f, 0.f, 0.f, 0.f};
+                        wait(&ybar, yq & 1);
+                        ++yq;
 #pragma unroll
                         for (int n = 0; n < NG; ++n) {
                             const int j = NG * h + n;
                             float y4[4] = {0.f, 0.f, 0.f, 0.f};
                             float sj = 0.f;
                             if (j < rr) {
-                                v2::ld4(scr + net.yoff[lr] + (p * rr + j) * 4, y4);
+                                v2::ld4(reinterpret_cast<const float*>(W) + (j * P + p) * 4, y4);
                                 sj = float(sr[j]);
                             }
 #pragma unroll
@@ -628,7 +650,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                                 ssy[c] = fmaf(sy[c][n], sy[c][n], ssy[c]);
                             }
                         }
-                        named_bar_epi();  // every epilogue thread has read the u partials
+                        named_bar_epi();  // every epilogue thread has read the u partials and y_{L-2}
                         *reinterpret_cast<float4*>(xch + (h * P + p) * 8) = make_float4(ss[0], ss[1], ss[2], ss[3]);
                         *reinterpret_cast<float4*>(xch + (h * P + p) * 8 + 4) = make_float4(ssy[0], ssy[1], ssy[2], ssy[3]);
                         named_bar_epi();
@@ -652,15 +674,6 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                 umma::fence_async_smem();
                 umma::fence_before();
                 __syncthreads();
-                if (last) {
-                    reduce_points(red, acc, net.soff[L - 1], net.r[L - 1], tid);
-                    if (tid == NT - 1) {
-                        float sacc = 0.f;
-                        for (int pp = 0; pp < P; ++pp) sacc += red[P * RPS + pp];
-                        acc[0] += sacc;
-                    }
-                    __syncthreads();
-                }
                 TC_MARK(6);
             }
 
@@ -747,7 +760,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
 #pragma unroll
                     for (int n = 0; n < NG; ++n) {
                         const int j = NG * h + n;
-                        yv[n] = j < rl ? *reinterpret_cast<const float4*>(scr + net.yoff[l] + (p * rl + j) * 4)
+                        yv[n] = j < rl ? *reinterpret_cast<const float4*>(scr + net.yoff[l] + (j * P + p) * 4)
                                        : make_float4(0.f, 0.f, 0.f, 0.f);
                     }
                     wait(&zfree, zw & 1);
@@ -755,15 +768,22 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                     add_acc(tlane + TM_Y + NG * h, rs.it, tsum);
                     TC_MARK(14);
                     float ss[4] = {0.f, 0.f, 0.f, 0.f};
+                    {
+                        float cd[NG];
+#pragma unroll
+                        for (int n = 0; n < NG; ++n) {
+                            cd[n] = tsum[0][n] * yv[n].x;
+                            cd[n] = fmaf(tsum[1][n], yv[n].y, cd[n]);
+                            cd[n] = fmaf(tsum[2][n], yv[n].z, cd[n]);
+                            cd[n] = fmaf(tsum[3][n], yv[n].w, cd[n]);
+                        }
+                        const float v = warp_sum8(cd, lane);
+                        if ((lane & 3) == 0) tpart[(l * 4 + quarter) * RP + NG * h + warp_sum8_index(lane)] = v;
+                    }
 #pragma unroll
                     for (int n = 0; n < NG; ++n) {
                         const int j = NG * h + n;
                         const float sj = j < rl ? float(sl[j]) : 0.f;
-                        float cd = tsum[0][n] * yv[n].x;
-                        cd = fmaf(tsum[1][n], yv[n].y, cd);
-                        cd = fmaf(tsum[2][n], yv[n].z, cd);
-                        cd = fmaf(tsum[3][n], yv[n].w, cd);
-                        if (j < RP) red[p * RPS + j] = cd;
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
                             tsum[c][n] *= sj;  // ST_l
@@ -775,13 +795,15 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                         const double* sr = sv + net.soff[l - 1];
                         float sy[4][NG];
                         float ssy[4] = {0.f, 0.f, 0.f, 0.f};
+                        wait(&ybar, yq & 1);  // y_{l-1} copied into W
+                        ++yq;
 #pragma unroll
                         for (int n = 0; n < NG; ++n) {
                             const int j = NG * h + n;
                             float y4[4] = {0.f, 0.f, 0.f, 0.f};
                             float sj = 0.f;
                             if (j < rr) {
-                                v2::ld4(scr + net.yoff[l - 1] + (p * rr + j) * 4, y4);
+                                v2::ld4(reinterpret_cast<const float*>(W) + (j * P + p) * 4, y4);
                                 sj = float(sr[j]);
                             }
 #pragma unroll
@@ -792,7 +814,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                         }
                         *reinterpret_cast<float4*>(xch + (h * P + p) * 8) = make_float4(ss[0], ss[1], ss[2], ss[3]);
                         *reinterpret_cast<float4*>(xch + (h * P + p) * 8 + 4) = make_float4(ssy[0], ssy[1], ssy[2], ssy[3]);
-                        named_bar_epi();
+                        named_bar_epi();  // also: every thread has read its y_{l-1} from W
                         float nst[4] = {0.f, 0.f, 0.f, 0.f}, nsy[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                         for (int hh = 0; hh < 4; ++hh) {
@@ -809,15 +831,27 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                         }
                         rev_scales(rs, nst, nsy, l - 1, tsum, sy);
                     }
+                } else if (warp == ISSUER && l >= 1) {
+                    wait(&rfull, (rq - 1) & 1);  // the last A MMAs of this transition have read W
+                    prefetch_y(l - 1);
                 }
                 TC_MARK(15);
                 umma::fence_async_smem();
                 umma::fence_before();
                 __syncthreads();
-                reduce_points(red, acc, net.soff[l], rl, tid);
-                __syncthreads();
                 TC_MARK(12);
             }
+            // the tile's dL/ds partials (per warp quarter, fixed order) -> acc
+            for (int l = 0; l < L; ++l)
+                for (int j = tid; j < net.r[l]; j += NT) {
+                    const float* t = tpart + l * 4 * RP + j;
+                    acc[1 + net.soff[l] + j] += ((t[0] + t[RP]) + t[2 * RP]) + t[3 * RP];
+                }
+            if (tid == NT - 1) {
+                const float* t = tpart + kMaxL * 4 * RP;
+                acc[0] += ((t[0] + t[1]) + t[2]) + t[3];
+            }
+            __syncthreads();
         }
         for (int k = tid; k < R1; k += NT) {
             part[unit * R1 + k] = acc[k];
