@@ -107,7 +107,8 @@ void launch_fast(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const d
 
 bool dispatch_fast(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
                    double* dev_out) {
-    if (!m.fk.ok || !(ctx->opt_kernel == 0 || ctx->opt_kernel == 5)) return false;
+    // forced (5), or auto when the tensor-core kernel cannot take the model
+    if (!m.fk.ok || !(ctx->opt_kernel == 5 || (ctx->opt_kernel == 0 && !m.tc.ok))) return false;
     const bool fast = ctx->opt_fast_sincos != 0;
     if (m.act == LRNR_ACT_SIN) {
         if (fast) launch_fast<1, true>(ctx, m, s_dev, mu_dev, w, dev_out);

@@ -445,9 +445,10 @@ void launch_tc(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
 
 bool dispatch_tc(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
                  double* dev_out) {
-    // auto (0): the tensor-core kernel for the wide FP32 LRNR; the narrow FastLRNR
-    // stays on the FMA tile kernel (measured faster there).  2 forces it.
-    const bool want = ctx->opt_kernel == 2 || (ctx->opt_kernel == 0 && m.kind == LRNR_MODEL_LRNR);
+    // auto (0): the tensor-core kernel for every eligible FP32 model (ranks <= 32): the
+    // c2 LRNR, and the FastLRNR too (c2 r_hat 32: 5.1 vs 6.1 ms on the narrow FMA kernel;
+    // c3: 80 vs 106 ms; scripts/fast_ab.py, scripts/c3_ab.py).  2 forces it.
+    const bool want = ctx->opt_kernel == 2 || ctx->opt_kernel == 0;
     if (!m.tc.ok || !want) return false;
     const bool fast = ctx->opt_fast_sincos != 0;
     if (m.act == LRNR_ACT_SIN) {

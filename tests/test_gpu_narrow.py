@@ -1,5 +1,5 @@
-"""B200: the narrow-network kernel (csrc/pinn_fast.cuh), the auto choice for FP32
-FastLRNR: against the FP64 C oracle (emit_fast_jet + run_batch_gradient
+"""B200: the narrow-network FMA kernel (csrc/pinn_fast.cuh; auto takes the tensor-core
+kernel for FP32 FastLRNR, this kernel stays selectable with LRNR_OPT_KERNEL 5): against the FP64 C oracle (emit_fast_jet + run_batch_gradient
 restated) and the FMA tile kernel, on ragged tiles, several instances, both
 activations and sincos modes, odd reduced widths, term specs, non-finite input
 and bitwise reproducibility."""
@@ -40,7 +40,8 @@ def test_c2_fast_matches_oracle(narrow, oracle, act, fast_sincos, n):
     assert normwise(got["grad_s"], want["grad_s"]) <= TOL32_NORM
 
 
-def test_auto_picks_narrow_and_agrees_with_fma_tile(gpu):
+def test_auto_agrees_with_fma_tile(gpu):
+    # auto = the tcgen05 FP16-split kernel (~8e-6 from the FP64 oracle), the FMA tile kernel ~2e-6
     c = pkg.config2(n_points=20000, act=pkg.ACT_SIN)
     gpu.set_fast(c["fast"], pkg.F32)
     gpu.set_points(c["pts"])
@@ -50,8 +51,8 @@ def test_auto_picks_narrow_and_agrees_with_fma_tile(gpu):
         tile = gpu.loss_grad_s(pkg.MODEL_FAST, c["s"], c["mu"])
     finally:
         gpu.set_option(pkg.OPT_KERNEL, pkg.KERNEL_AUTO)
-    assert abs(auto["value"] - tile["value"]) <= 1e-5 * abs(tile["value"])
-    assert normwise(auto["grad_s"], tile["grad_s"]) <= 1e-5
+    assert abs(auto["value"] - tile["value"]) <= 5e-5 * abs(tile["value"])
+    assert normwise(auto["grad_s"], tile["grad_s"]) <= 5e-5
 
 
 def test_odd_widths_and_ranks(narrow, oracle):

@@ -19,9 +19,8 @@ TOL32_NORM = 1e-4
 TOL32_LOSS = 1e-4
 
 
-# FP32 kernel choices (LRNR_OPT_KERNEL): auto = tcgen05 for the LRNR + the
-# narrow-network kernel for FastLRNR; forced tcgen05 (FastLRNR too); FMA tile;
-# per-point streaming; small-batch; forced narrow-network kernel
+# FP32 kernel choices (LRNR_OPT_KERNEL): auto = tcgen05 (LRNR and FastLRNR, ranks <= 32);
+# forced tcgen05; FMA tile; per-point streaming; small-batch; forced narrow-network FMA kernel
 FP32_KERNELS = [pkg.KERNEL_AUTO, pkg.KERNEL_TC, pkg.KERNEL_FMA_TILE, pkg.KERNEL_STREAM, pkg.KERNEL_SMALL,
                 pkg.KERNEL_NARROW]
 
