@@ -387,20 +387,21 @@ def headline(env, pkg, args, ctx):
               "cosine": float(np.dot(g_f[1:], g_l[1:]) / (np.linalg.norm(g_f[1:]) * np.linalg.norm(g_l[1:]))),
               "what": f"FastLRNR (r_hat {list(map(int, f.red_ranks))}) vs full-LRNR loss and dL/ds on the step's points"}
 
-    # roofline of the dominant kernel (the LRNR sweep on the tcgen05 tensor pipe, 3xTF32)
+    # roofline of the dominant kernel (the LRNR sweep on the tcgen05 tensor pipe): every
+    # FP32-accurate multiply-add is 3 FP16 products (hi*hi + hi*lo + lo*hi) at the f16 rate
     bf16, bf16_src = measured_peak("bf16_tflops", 1590.0)
     fp32_peak, fp32_src = fma_peak(ctx, pkg, pkg.F32)
     k_ms = kern[0]
     achieved = flops[0] * n / (k_ms * 1e-3) / 1e12
-    tc_peak = bf16 / 2 / 3
+    tc_peak = bf16 / 3
     lrnr_on_tc = args.kernel in (pkg.KERNEL_AUTO, pkg.KERNEL_TC)
     if lrnr_on_tc:
         roofline = {"bound": "tensor", "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
                     "frac": achieved / tc_peak, "traffic": traffic_per_launch("pinn_tc_kernel", n),
-                    "kernel": "pinn_tc_kernel (tcgen05 kind::tf32, 3xTF32 split = FP32-accurate products)",
+                    "kernel": "pinn_tc_kernel (tcgen05 kind::f16, FP16 two-term split = FP32-accurate products)",
                     "flop_per_point": flops[0], "points_per_launch": n,
-                    "peak_source": f"{bf16_src} {bf16:.1f} TFLOP/s (bf16 dense, burst) / 2 (tf32) / 3 (3 products "
-                                   f"per FP32 multiply-add); the kernel is timed alone per step",
+                    "peak_source": f"{bf16_src} {bf16:.1f} TFLOP/s (f16 / bf16 dense, burst) / 3 (3 FP16 products "
+                                   f"per FP32-accurate multiply-add); the kernel is timed alone per step",
                     "fp32_fma_equivalent": {"peak": fp32_peak, "frac": achieved / fp32_peak,
                                             "peak_source": fp32_src}}
     else:
@@ -413,11 +414,15 @@ def headline(env, pkg, args, ctx):
         per_kernel["lrnr" if model == pkg.MODEL_LRNR else "fast"] = {
             "ms": kern[i], "point_evals_per_s": env.world * n / (kern[i] * 1e-3), "tflops": tf,
             "frac_of_fp32_fma": tf / fp32_peak, "flop_per_point": flops[i],
-            "kernel": ("pinn_tc_kernel (tcgen05 3xTF32)" if model == pkg.MODEL_LRNR else
-                       "pinn_fast_kernel (narrow network, FP32 FMA)")}
-    per_kernel["fast"]["roofline"] = {"bound": "fp32-fma", "peak": fp32_peak,
-                                      "traffic": traffic_per_launch("pinn_fast_kernel", n),
-                                      "frac": per_kernel["fast"]["tflops"] / fp32_peak}
+            "kernel": ("pinn_tc_kernel (tcgen05, FP16 two-term split)" if lrnr_on_tc else
+                       f"LRNR_OPT_KERNEL {args.kernel}")}
+    if lrnr_on_tc:
+        per_kernel["fast"]["roofline"] = {"bound": "tensor", "peak": tc_peak,
+                                          "traffic": traffic_per_launch("pinn_tc_kernel_fast", n),
+                                          "frac": per_kernel["fast"]["tflops"] / tc_peak}
+    else:
+        per_kernel["fast"]["roofline"] = {"bound": "fp32-fma", "peak": fp32_peak, "traffic": None,
+                                          "frac": per_kernel["fast"]["tflops"] / fp32_peak}
 
     # end to end through the public host-buffer C ABI: H2D of the step's points from pinned
     # memory, both gradient calls with host outputs (D2H), every step
@@ -592,6 +597,8 @@ def config_c3(env, pkg, args):
     launches = ctx.launches - l0
     fl = pkg.fast_flops_per_point(f.ranks, f.red_ranks)
     peak, src = fma_peak(ctx, pkg, pkg.F32)
+    bf16, tsrc = measured_peak("bf16_tflops", 1590.0)
+    tpk = bf16 / 3
     n_all = N_INST * PER
     tf = fl * n_all / (ms * 1e-3) / 1e12
     line = {"workload": f"c3: 1024 mu ~ U[1,40]xU[0,0.1]xU[0,10] x 16384 pts, hypernetwork 3-64-64-163 (FP64) -> "
@@ -600,10 +607,12 @@ def config_c3(env, pkg, args):
             "dtype": "f32", "instances_per_gpu": b - a,
             "collective": "ncclAllReduce of dL/dtheta (15,011 doubles) + the loss, by the contexts" if env.world > 1
             else None,
-            "roofline": {"bound": "fp32-fma", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
-                         "flop_per_point": fl, "points_per_launch": (b - a) * PER, "peak_source": src,
-                         "kernel": "pinn_fast_kernel (narrow network, FP32 FMA) + FP64 hypernetwork fwd / VJP",
-                         "traffic": traffic_per_launch("pinn_fast_kernel", (b - a) * PER)},
+            "roofline": {"bound": "tensor", "achieved": tf, "peak": tpk, "unit": "TFLOP/s", "frac": tf / tpk,
+                         "flop_per_point": fl, "points_per_launch": (b - a) * PER,
+                         "peak_source": f"{tsrc} {bf16:.1f} TFLOP/s (f16 dense) / 3 (FP16 two-term split)",
+                         "kernel": "pinn_tc_kernel (tcgen05, FP16 two-term split) + FP64 hypernetwork fwd / VJP",
+                         "traffic": traffic_per_launch("pinn_tc_kernel_c3", (b - a) * PER),
+                         "fp32_fma_equivalent": {"peak": peak, "frac": tf / peak, "peak_source": src}},
             "gpu_launches": launches,
             "l2": "inputs (268 MB of points) larger than L2; no flush"}
     if not args.no_e2e:

@@ -112,7 +112,8 @@ struct Model {
     struct TC {
         bool ok = false;
         std::vector<int> rk, rn, nc, yoff;
-        std::vector<float> isU, isV, muU, muV;
+        std::vector<int> kU, kV;  // factor scales 2^k (FP16 split)
+        std::vector<float> muU, muV;
         int ystride = 0;
         std::vector<unsigned char> blocks;  // fp16 hi / lo factor tiles + FP32 biases
         std::vector<int64_t> sched_off;

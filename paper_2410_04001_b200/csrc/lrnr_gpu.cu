@@ -256,8 +256,8 @@ void build_tc(Model& m) {
     }
     v.nc.assign(L, 0);
     v.yoff.assign(L, 0);
-    v.isU.assign(L, 1.f);
-    v.isV.assign(L, 1.f);
+    v.kU.assign(L, 0);
+    v.kV.assign(L, 0);
     v.muU.assign(L, 0.f);
     v.muV.assign(L, 0.f);
     int yo = 0;
@@ -277,11 +277,11 @@ void build_tc(Model& m) {
         std::memcpy(hi + o, &hh, 2);
         std::memcpy(hi + lo_off + o, &ll, 2);
     };
-    auto pow2_for = [](double amax) {  // S = 2^e with amax * S < 2^15
-        if (!(amax > 0.0) || !std::isfinite(amax)) return 1.f;
+    auto pow2_for = [](double amax) {  // k with amax * 2^k < 2^15
+        if (!(amax > 0.0) || !std::isfinite(amax)) return 0;
         int e;
         std::frexp(amax, &e);  // amax < 2^e
-        return static_cast<float>(std::ldexp(1.0, 14 - e));
+        return 14 - e;
     };
     for (int l = 0; l + 1 < L; ++l) {
         const int rl = m.r[l], rn = m.r[l + 1], M = m.M[l + 1];
@@ -311,9 +311,9 @@ void build_tc(Model& m) {
             un = std::max(un, su);
             vn = std::max(vn, svv);
         }
-        const float SU = pow2_for(umax), SV = pow2_for(vmax);
-        v.isU[l] = 1.f / SU;
-        v.isV[l] = 1.f / SV;
+        v.kU[l] = pow2_for(umax);
+        v.kV[l] = pow2_for(vmax);
+        const float SU = static_cast<float>(std::ldexp(1.0, v.kU[l])), SV = static_cast<float>(std::ldexp(1.0, v.kV[l]));
         // bounds are used as upper bounds: round the norms up a little
         v.muU[l] = static_cast<float>(std::sqrt(un) * (1.0 + 1e-6));
         v.muV[l] = static_cast<float>(std::sqrt(vn) * (1.0 + 1e-6));
@@ -420,8 +420,8 @@ void launch_tc(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
         net.rn[l] = v.rn[l];
         net.nc[l] = v.nc[l];
         net.yoff[l] = v.yoff[l];
-        net.isU[l] = v.isU[l];
-        net.isV[l] = v.isV[l];
+        net.kU[l] = v.kU[l];
+        net.kV[l] = v.kV[l];
         net.muU[l] = v.muU[l];
         net.muV[l] = v.muV[l];
     }

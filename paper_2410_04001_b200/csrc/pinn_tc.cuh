@@ -81,8 +81,8 @@ struct NetTC {
     int soff[kMaxL + 1];
     int yoff[kMaxL];       // y_l in per-CTA scratch: [j (r_l)][p][4] (a layer is one contiguous block)
     int ystride;
-    float isU[kMaxL];      // 1 / (power-of-two scale of U_l) and of V_l
-    float isV[kMaxL];
+    int kU[kMaxL];         // factor scales 2^kU (U_l) and 2^kV (V_l)
+    int kV[kMaxL];
     float muU[kMaxL];      // max row 2-norm of U_l / V_l (bounds of the pre-activation jets)
     float muV[kMaxL];
     float c3;              // max |sigma'''| (1 sin, 2 tanh)
@@ -175,18 +175,45 @@ __device__ __forceinline__ void act3f(float a, float& sg, float& d1, float& d2, 
     v2::act3<ACT, FAST>(a, sg, d1, d2, d3);
 }
 
-// Per-point scales of one transition (exponents / unscale factors), all 4 jet slots.
+// 2^k for an integer exponent, clamped to the normal range
+__device__ __forceinline__ float exp2c(int k) { return umma::exp2i(max(-126, min(127, k))); }
+
+// Per-point constants of one transition with the power-of-two unscale (P1 / P2 products)
+// and scale (Z / G operands) factors folded in.  Exponents: eS = SY / ST row scale,
+// kU / kV = factor scales, ez / eg = Z / G row scales.
 struct FwdScales {
-    float ia[4];   // P1 unscale: 2^-eSY * isU
-    int ez[4];     // Z scale exponents
-    float iy[4];   // Y unscale: 2^-ez * isV
+    float ia0;          // A_v = P1_v 2^-(eS0 + kU) + b
+    float f1, f2, f3;   // Z_c 2^ez_c = d1 P1_c f_c (c = 1, 2), d1 P1_3 f3 for the u_w term
+    float g3;           // Z_3 2^ez3 = d2 P1_1^2 g3 + d1 P1_3 f3
+    float s0;           // Z_0 2^ez0 = sigma s0
+    float iy[4];        // Y unscale 2^-(ez_c + kV)
 };
 struct RevScales {
-    float ia[4];   // recomputed A unscale
-    float id[4];   // DZ unscale: 2^-eST * isV
-    int eg[4];     // G scale exponents
-    float it[4];   // T unscale: 2^-eg * isU
+    float ia0;                           // A_v = P1r_v 2^-(eSY0 + kU) + b
+    float k0, k01, k02, k03, k04;        // G0 2^eg0 = d1 e0 k0 + d2 (e1 k01 r1 + e2 k02 r2 + e3 k03 r3) + d3 e3 k04 r1^2
+    float k1, k13, k2, k3;               // G1 2^eg1 = d1 e1 k1 + d2 r1 e3 k13; G2 = d1 e2 k2; G3 = d1 e3 k3
+    float it[4];                         // T unscale 2^-(eg_c + kU)
 };
+// (r = recomputed P1r columns, e = DZ columns, both still scaled)
+
+// Forward constants from the exact SY row norms (slot c exponent eS[c]) of transition l.
+__device__ __forceinline__ void fwd_scales(FwdScales& f, const NetTC& net, int l, const float (&nr)[4], const int (&eS)[4]) {
+    const int kU = net.kU[l], kV = net.kV[l];
+    const float mu = net.muU[l];
+    const float bx = nr[1] * mu, bt = nr[2] * mu, bw = nr[3] * mu;
+    const int ez0 = umma::pow2_exp(1.f), ez1 = umma::pow2_exp(bx), ez2 = umma::pow2_exp(bt);
+    const int ez3 = umma::pow2_exp(fmaf(bx, bx, bw));
+    f.ia0 = exp2c(-eS[0] - kU);
+    f.f1 = exp2c(ez1 - eS[1] - kU);
+    f.f2 = exp2c(ez2 - eS[2] - kU);
+    f.f3 = exp2c(ez3 - eS[3] - kU);
+    f.g3 = exp2c(ez3 - 2 * (eS[1] + kU));
+    f.s0 = exp2c(ez0);
+    f.iy[0] = exp2c(-ez0 - kV);
+    f.iy[1] = exp2c(-ez1 - kV);
+    f.iy[2] = exp2c(-ez2 - kV);
+    f.iy[3] = exp2c(-ez3 - kV);
+}
 
 template <int ACT, bool FAST>
 __global__ void __launch_bounds__(NT, 1)
@@ -369,20 +396,33 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
             nsy[c] = sqrtf(nsy[c]);
             est[c] = umma::pow2_exp(nst[c]);
             esy[c] = umma::pow2_exp(nsy[c]);
-            r.id[c] = umma::exp2i(-est[c]) * net.isV[lr];
-            r.ia[c] = umma::exp2i(-esy[c]) * net.isU[lr];
         }
         if (NG * h < net.rk[lr + 1]) put_rows(X, p, h, st, est);
         if (NG * h < net.rk[lr]) put_rows(W, p, h, sy, esy);
+        const int kU = net.kU[lr], kV = net.kV[lr];
         const float mu = net.muU[lr], mv = net.muV[lr];
         const float bx = nsy[1] * mu, bt = nsy[2] * mu, bw = nsy[3] * mu;
         const float B0 = nst[0] * mv, B1 = nst[1] * mv, B2 = nst[2] * mv, B3 = nst[3] * mv;
-        r.eg[0] = umma::pow2_exp(B0 + B1 * bx + B2 * bt + B3 * fmaf(net.c3 * bx, bx, bw));
-        r.eg[1] = umma::pow2_exp(fmaf(2.f * B3, bx, B1));
-        r.eg[2] = umma::pow2_exp(B2);
-        r.eg[3] = umma::pow2_exp(B3);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) r.it[c] = umma::exp2i(-r.eg[c]) * net.isU[lr];
+        const int eg0 = umma::pow2_exp(B0 + B1 * bx + B2 * bt + B3 * fmaf(net.c3 * bx, bx, bw));
+        const int eg1 = umma::pow2_exp(fmaf(2.f * B3, bx, B1));
+        const int eg2 = umma::pow2_exp(B2), eg3 = umma::pow2_exp(B3);
+        // unscale exponents: DZ_c -> -(est_c + kV), A_c -> -(esy_c + kU)
+        const int d0 = -est[0] - kV, d1 = -est[1] - kV, d2 = -est[2] - kV, d3 = -est[3] - kV;
+        const int a1 = -esy[1] - kU, a2 = -esy[2] - kU, a3 = -esy[3] - kU;
+        r.ia0 = exp2c(-esy[0] - kU);
+        r.k0 = exp2c(eg0 + d0);
+        r.k01 = exp2c(eg0 + d1 + a1);
+        r.k02 = exp2c(eg0 + d2 + a2);
+        r.k03 = exp2c(eg0 + d3 + a3);
+        r.k04 = exp2c(eg0 + d3 + 2 * a1);
+        r.k1 = exp2c(eg1 + d1);
+        r.k13 = 2.f * exp2c(eg1 + d3 + a1);
+        r.k2 = exp2c(eg2 + d2);
+        r.k3 = exp2c(eg3 + d3);
+        r.it[0] = exp2c(-eg0 - kU);
+        r.it[1] = exp2c(-eg1 - kU);
+        r.it[2] = exp2c(-eg2 - kU);
+        r.it[3] = exp2c(-eg3 - kU);
     };
 
     TC_T0();
@@ -448,16 +488,9 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                     for (int c = 0; c < 4; ++c) {
                         nr[c] = sqrtf(nr[c]);
                         e[c] = umma::pow2_exp(nr[c]);
-                        fs.ia[c] = umma::exp2i(-e[c]) * net.isU[0];
                     }
                     if (NG * h < net.rk[0]) put_rows(X, p, h, sy, e);
-                    const float bx = nr[1] * net.muU[0], bt = nr[2] * net.muU[0], bw = nr[3] * net.muU[0];
-                    fs.ez[0] = umma::pow2_exp(1.f);
-                    fs.ez[1] = umma::pow2_exp(bx);
-                    fs.ez[2] = umma::pow2_exp(bt);
-                    fs.ez[3] = umma::pow2_exp(fmaf(bx, bx, bw));
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) fs.iy[c] = umma::exp2i(-fs.ez[c]) * net.isV[0];
+                    fwd_scales(fs, net, 0, nr, e);
                 }
                 umma::fence_async_smem();
                 __syncthreads();
@@ -499,22 +532,17 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                             float z[2][4];
 #pragma unroll
                             for (int i = 0; i < 2; ++i) {
-                                const int k = NG * h + n + i;
-                                const float av = fmaf(a[0][n + i], fs.ia[0], bias[k]);
-                                const float ax = a[1][n + i] * fs.ia[1], at = a[2][n + i] * fs.ia[2];
-                                const float aw = a[3][n + i] * fs.ia[3];
+                                const float r1 = a[1][n + i], r2 = a[2][n + i], r3 = a[3][n + i];
+                                const float av = fmaf(a[0][n + i], fs.ia0, bias[NG * h + n + i]);
                                 float sg, d1, d2, d3;
                                 act3f<ACT, FAST>(av, sg, d1, d2, d3);
-                                z[i][0] = sg;
-                                z[i][1] = d1 * ax;
-                                z[i][2] = d1 * at;
-                                z[i][3] = fmaf(d2 * ax, ax, d1 * aw);
+                                z[i][0] = sg * fs.s0;
+                                z[i][1] = d1 * (r1 * fs.f1);
+                                z[i][2] = d1 * (r2 * fs.f2);
+                                z[i][3] = fmaf(d2 * r1, r1 * fs.g3, d1 * (r3 * fs.f3));
                             }
 #pragma unroll
-                            for (int c = 0; c < 4; ++c) {
-                                const float s = umma::exp2i(fs.ez[c]);
-                                umma::split16x2(z[0][c] * s, z[1][c] * s, zh[c][n / 2], zl[c][n / 2]);
-                            }
+                            for (int c = 0; c < 4; ++c) umma::split16x2(z[0][c], z[1][c], zh[c][n / 2], zl[c][n / 2]);
                         }
                         TC_MARK(3);
                         if (ch > 0) {
@@ -582,17 +610,9 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                         for (int c = 0; c < 4; ++c) {
                             nr[c] = sqrtf(nr[c]);
                             e[c] = umma::pow2_exp(nr[c]);
-                            fs.ia[c] = umma::exp2i(-e[c]) * net.isU[l + 1];
                         }
                         if (NG * h < net.rk[l + 1]) put_rows(X, p, h, ysum, e);
-                        const float mu = net.muU[l + 1];
-                        const float bx = nr[1] * mu, bt = nr[2] * mu, bw = nr[3] * mu;
-                        fs.ez[0] = umma::pow2_exp(1.f);
-                        fs.ez[1] = umma::pow2_exp(bx);
-                        fs.ez[2] = umma::pow2_exp(bt);
-                        fs.ez[3] = umma::pow2_exp(fmaf(bx, bx, bw));
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) fs.iy[c] = umma::exp2i(-fs.ez[c]) * net.isV[l + 1];
+                        fwd_scales(fs, net, l + 1, nr, e);
                     } else {
                         // ---------------- output layer (M_L = 1) + residual ----------------
                         float u[4] = {nr[0] + net.ulast[rtrue], nr[1], nr[2], nr[3]};
@@ -713,25 +733,23 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                                 float gg[2][4];
 #pragma unroll
                                 for (int i = 0; i < 2; ++i) {
-                                    const int k = NG * h + 4 * hf + n + i;
-                                    const float av = fmaf(a[0][n + i], rs.ia[0], bias[k]);
-                                    const float ax = a[1][n + i] * rs.ia[1], at = a[2][n + i] * rs.ia[2];
-                                    const float aw = a[3][n + i] * rs.ia[3];
-                                    const float g0 = dz[0][n + i] * rs.id[0], g1 = dz[1][n + i] * rs.id[1];
-                                    const float g2 = dz[2][n + i] * rs.id[2], g3 = dz[3][n + i] * rs.id[3];
+                                    const float r1 = a[1][n + i], r2 = a[2][n + i], r3 = a[3][n + i];
+                                    const float e0 = dz[0][n + i], e1 = dz[1][n + i], e2 = dz[2][n + i], e3 = dz[3][n + i];
+                                    const float av = fmaf(a[0][n + i], rs.ia0, bias[NG * h + 4 * hf + n + i]);
                                     float sg, d1, d2, d3;
                                     act3f<ACT, FAST>(av, sg, d1, d2, d3);
-                                    gg[i][0] = g0 * d1 + g1 * d2 * ax + g2 * d2 * at + g3 * (d3 * ax * ax + d2 * aw);
-                                    gg[i][1] = g1 * d1 + g3 * 2.f * d2 * ax;
-                                    gg[i][2] = g2 * d1;
-                                    gg[i][3] = g3 * d1;
+                                    float wv = (e3 * rs.k03) * r3;
+                                    wv = fmaf(e2 * rs.k02, r2, wv);
+                                    wv = fmaf(e1 * rs.k01, r1, wv);
+                                    const float xv = ((e3 * rs.k04) * r1) * r1;
+                                    gg[i][0] = fmaf(d1, e0 * rs.k0, fmaf(d2, wv, d3 * xv));
+                                    gg[i][1] = fmaf(d1, e1 * rs.k1, (d2 * r1) * (e3 * rs.k13));
+                                    gg[i][2] = d1 * (e2 * rs.k2);
+                                    gg[i][3] = d1 * (e3 * rs.k3);
                                 }
 #pragma unroll
-                                for (int c = 0; c < 4; ++c) {
-                                    const float s = umma::exp2i(rs.eg[c]);
-                                    umma::split16x2(gg[0][c] * s, gg[1][c] * s, gh[c][2 * hf + n / 2],
-                                                    gl[c][2 * hf + n / 2]);
-                                }
+                                for (int c = 0; c < 4; ++c)
+                                    umma::split16x2(gg[0][c], gg[1][c], gh[c][2 * hf + n / 2], gl[c][2 * hf + n / 2]);
                             }
                         }
                         TC_MARK(9);
