@@ -175,6 +175,55 @@ def test_c3_hyper_fast_matches_oracle(gpu, oracle):
     assert normwise(got["grad_theta"], gth) <= TOL32_NORM
 
 
+def test_c3_full_points_per_instance_matches_oracle(gpu, oracle):
+    """c3 at BASELINE's 16,384 points per instance, on three of the 1024 mu (first, middle, last),
+    against the FP64 oracle per instance (points sampled exactly as bench.py does)."""
+    per = 16384
+    c = pkg.config3(n_inst=1024, pts_per_inst=0, act=pkg.ACT_SIN)
+    f, h = c["fast"], c["hyper"]
+    idx = [0, 511, 1023]
+    pts = np.concatenate([pkg.sample_collocation(5000 + i, per) for i in idx])
+    mus = np.ascontiguousarray(c["mus"][idx])
+    gpu.set_fast(f, pkg.F32)
+    gpu.set_hyper(h)
+    gpu.set_points(pts, n_inst=len(idx))
+    w = 1.0 / (1024 * per)
+    got = gpu.hyper_loss_grad(pkg.MODEL_FAST, mus, w)
+    for k, i in enumerate(idx):
+        s_i = oracle.hyper_forward(h.hw, h.params, h.lo, h.hi, mus[k])
+        r = oracle.fast_grad(f.ranks, f.red_ranks, f.fparams, s_i, mus[k], pts[k * per:(k + 1) * per], w=w,
+                             act=pkg.ACT_SIN)
+        assert normwise(got["grad_s"][k], r["grad_s"]) <= TOL32_NORM
+
+
+def test_c3_full_config_shard_invariant(gpu):
+    """The full c3 step (1024 mu x 16,384 points): each instance's dL/ds row is the same when the
+    instances run in two halves (what a 2-GPU shard computes; only the tile grouping of the FP32
+    partial sums differs), and dL/dtheta is the sum of the halves' (a size-independent property at
+    BASELINE's size)."""
+    import torch
+    per, n = 16384, 1024
+    c = pkg.config3(n_inst=n, pts_per_inst=0, act=pkg.ACT_SIN)
+    pts = np.concatenate([pkg.sample_collocation(5000 + i, per) for i in range(n)])
+    pts_dev = torch.from_numpy(pts).to("cuda")
+    gpu.set_fast(c["fast"], pkg.F32)
+    gpu.set_hyper(c["hyper"])
+    w = 1.0 / (n * per)
+    gpu.set_points_device(pts_dev.data_ptr(), n * per, n_inst=n)
+    full = gpu.hyper_loss_grad(pkg.MODEL_FAST, c["mus"], w)
+    halves = []
+    for a, b in ((0, n // 2), (n // 2, n)):
+        sub = pts_dev[a * per:b * per]
+        gpu.set_points_device(sub.data_ptr(), (b - a) * per, n_inst=b - a)
+        halves.append(gpu.hyper_loss_grad(pkg.MODEL_FAST, np.ascontiguousarray(c["mus"][a:b]), w))
+    assert np.isfinite(full["value"]) and np.all(np.isfinite(full["grad_theta"]))
+    cat = np.concatenate([hh["grad_s"] for hh in halves])
+    assert max(normwise(full["grad_s"][i], cat[i]) for i in range(n)) <= 1e-5
+    th = halves[0]["grad_theta"] + halves[1]["grad_theta"]
+    assert normwise(full["grad_theta"], th) <= 1e-5
+    assert abs(full["value"] - (halves[0]["value"] + halves[1]["value"])) <= 1e-5 * abs(full["value"])
+
+
 def test_hyper_forward_vjp_match_reference(gpu, golden):
     """Hypernetwork forward + VJP (c3 shape) against the reference (FP64 path)."""
     split = golden["c2_ranks"]
