@@ -7,7 +7,7 @@
 // 4 jet slots (u, u_x, u_t, u_xx) are 4 independent MMAs, so the epilogue thread that
 // owns a point sees all 4 slots of each of its neurons without shuffles.  Per chunk of
 // KC = 32 neurons of transition l:
-//   forward   P1  A_c  = SY_c U^T          SS: A = SY (smem), B = U^T chunk (ring)  -> TMEM (2 buffers)
+//   forward   P1  A_c  = SY_c U^T          TS: A = SY (TMEM), B = U^T chunk (ring)  -> TMEM
 //             epilogue: A -> (+b) sigma-jet Z_c -> TMEM (fp16 hi | lo)
 //             P2  Y_c += Z_c V             TS: A = Z (TMEM),  B = V chunk           -> TMEM
 //   reverse   P1r A_c  = SY_c U^T (recomputed from SY_l in smem, no stash in HBM)
@@ -24,7 +24,7 @@
 // bytes of the SS MMAs (which are shared-memory bound at N = 32: 42 cycles for
 // tf32 K8 vs 42 for f16 K16, scripts/umma_issue_tf32.cu) and let SY_l stay resident
 // for the reverse recompute.
-// TMEM (512 columns): forward P1 x2 | Z | Y;  reverse A | DZ | G | T.
+// TMEM (512 columns): forward P1 | SY | Z | Y;  reverse A | DZ | G | T.
 // Warp roles: 16 epilogue warps; warp 16 issues P1-type MMAs; warp 17 issues P2-type
 // MMAs and the factor-chunk TMA bulk copies (4-slot ring).
 #pragma once
@@ -48,7 +48,8 @@ constexpr int ISSUER2 = NWE + 1;  // P2-type MMAs + TMA producer
 constexpr int NT = 32 * (NWE + 2);
 constexpr int NG = 8;             // neurons / ranks per epilogue thread
 // TMEM columns
-constexpr int TM_R = 0;     // forward: P1 buffers at 0 / 128 (chunk parity); reverse: A at 0, DZ at 128
+constexpr int TM_R = 0;     // forward: P1; reverse: A at 0, DZ at 128
+constexpr int TM_SY = 128;  // forward: SY (fp16 hi | lo per slot, like Z): the A operand of P1 (TS)
 constexpr int TM_Z = 256;   // Z / G: per slot 32 columns = fp16 hi (16 columns) | lo (16 columns)
 constexpr int TM_Y = 384;   // Y / T: per slot 32 fp32 columns
 // Phase-2 products of YACC consecutive chunks accumulate in TMEM before the epilogue
@@ -170,6 +171,20 @@ __device__ __forceinline__ void put_rows(unsigned char* buf, int p, int h, const
 // named barrier over the 16 epilogue warps (the issuer warps keep running)
 __device__ __forceinline__ void named_bar_epi() { asm volatile("bar.sync 1, %0;" ::"n"(NWE * 32) : "memory"); }
 
+// The same 8 values into the forward SY operand in TMEM (this thread's lane = point p,
+// K block h): per slot, 4 packed hi columns at c * 32 + 4h and 4 lo columns 16 further.
+__device__ __forceinline__ void put_rows_tmem(uint32_t tsy, int h, const float (&v)[4][NG], const int (&e)[4]) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const float s = umma::exp2i(e[c]);
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) umma::split16x2(v[c][2 * i] * s, v[c][2 * i + 1] * s, hw[i], lw[i]);
+        umma::tmem_st4u(tsy + c * 32 + 4 * h, hw[0], hw[1], hw[2], hw[3]);
+        umma::tmem_st4u(tsy + c * 32 + 16 + 4 * h, lw[0], lw[1], lw[2], lw[3]);
+    }
+}
+
 template <int ACT, bool FAST>
 __device__ __forceinline__ void act3f(float a, float& sg, float& d1, float& d2, float& d3) {
     v2::act3<ACT, FAST>(a, sg, d1, d2, d3);
@@ -227,7 +242,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
     unsigned char* X = smb + OFF_X;
     unsigned char* W = smb + OFF_W;
     __shared__ __align__(8) uint64_t wbar[NBUF];           // ring slot filled (TMA)
-    __shared__ __align__(8) uint64_t p1full[2];  // forward P1 buffers written (tcgen05.commit)
+    __shared__ __align__(8) uint64_t p1full;     // forward P1 written (tcgen05.commit)
     __shared__ __align__(8) uint64_t rfull;      // reverse A / DZ written
     __shared__ __align__(8) uint64_t zfree;      // P2 done: Z / G free, Y / T product ready
     __shared__ __align__(8) uint64_t ybar;       // y_l block copied into W (TMA)
@@ -246,7 +261,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
     if (warp == 0) umma::tmem_alloc<512>(&tmem_base);
     if (tid == 0) {
         for (int i = 0; i < NBUF; ++i) umma::mbar_init(&wbar[i], 1);
-        for (int i = 0; i < 2; ++i) umma::mbar_init(&p1full[i], 1);
+        umma::mbar_init(&p1full, 1);
         umma::mbar_init(&rfull, 1);
         umma::mbar_init(&zfree, 1);
         umma::mbar_init(&ybar, 1);
@@ -313,6 +328,20 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
             }
         }
     };
+    // forward P1 (TS): A = SY in TMEM (fp16 hi / lo columns per slot), B = U^T chunk; K = rk
+    auto mma_p1_ts = [&](const unsigned char* bsrc, int rk) {
+        const uint32_t bh = dlo(bsrc, KC), bl = dlo(bsrc + 2 * KC * rk, KC);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const uint32_t d = tbase + TM_R + c * 32, ay = tbase + TM_SY + c * 32;
+            for (int s = 0; s < rk / 16; ++s) {
+                const uint32_t sb = s * 2 * KC;
+                umma::mma16_ts(d, ay + 8 * s, bh + sb, dhi, idP1, s > 0);
+                umma::mma16_ts(d, ay + 8 * s, bl + sb, dhi, idP1, 1);
+                umma::mma16_ts(d, ay + 16 + 8 * s, bh + sb, dhi, idP1, 1);
+            }
+        }
+    };
     // P2-type MMAs (TS): D = TM_Y, A = Z / G in TMEM, B = fp16 hi / lo tile of rn rows x KC at bsrc
     auto mma_p2 = [&](const unsigned char* bsrc, int rn, bool acc0) {
         const uint32_t id2 = umma::idesc_f16(P, rn);
@@ -350,11 +379,10 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
     // ISSUER: forward P1 of chunk qq into buffer fq & 1
     auto issue_fwd_p1 = [&](int64_t qq, uint32_t fqq, int rk) {
         wait_slot(qq);
-        const uint32_t b = fqq & 1, k = fqq >> 1;
-        if (k >= 1) await(BAR_P1FREE + b);
+        if (fqq >= 1) await(BAR_P1FREE);  // the epilogue has read P1(qq - 1)
         if (umma::elect_one()) {
-            mma_p1(tbase + TM_R + 128 * b, X, slot(qq), rk);
-            umma::mma_commit_1(&p1full[b]);
+            mma_p1_ts(slot(qq), rk);
+            umma::mma_commit_1(&p1full);
         }
         __syncwarp();
     };
@@ -489,10 +517,11 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                         nr[c] = sqrtf(nr[c]);
                         e[c] = umma::pow2_exp(nr[c]);
                     }
-                    if (NG * h < net.rk[0]) put_rows(X, p, h, sy, e);
+                    if (NG * h < net.rk[0]) put_rows_tmem(tlane + TM_SY, h, sy, e);
+                    umma::tmem_st_wait();
                     fwd_scales(fs, net, 0, nr, e);
                 }
-                umma::fence_async_smem();
+                umma::fence_before();  // SY in TMEM -> the first P1
                 __syncthreads();
             }
 
@@ -517,15 +546,14 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                         issue_p2(q, slot(q) + fv, rnn, ch % YACC != 0);
                     } else {
                         TC_MARK(1);
-                        const uint32_t b = fq & 1;
-                        wait(&p1full[b], (fq >> 1) & 1);
+                        wait(&p1full, fq & 1);
                         TC_MARK(2);
                         const float* bias = reinterpret_cast<const float*>(slot(q) + fbias);
                         float a[4][NG];
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) umma::tmem_ld8(tlane + TM_R + 128 * b + c * 32 + NG * h, a[c]);
+                        for (int c = 0; c < 4; ++c) umma::tmem_ld8(tlane + TM_R + c * 32 + NG * h, a[c]);
                         umma::tmem_ld_wait();
-                        signal(BAR_P1FREE + b);  // the buffer may take P1(q + 2)
+                        signal(BAR_P1FREE);  // P1 may take chunk q + 1
                         uint32_t zh[4][NG / 2], zl[4][NG / 2];
 #pragma unroll
                         for (int n = 0; n < NG; n += 2) {
@@ -611,7 +639,8 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                             nr[c] = sqrtf(nr[c]);
                             e[c] = umma::pow2_exp(nr[c]);
                         }
-                        if (NG * h < net.rk[l + 1]) put_rows(X, p, h, ysum, e);
+                        if (NG * h < net.rk[l + 1]) put_rows_tmem(tlane + TM_SY, h, ysum, e);
+                        umma::tmem_st_wait();
                         fwd_scales(fs, net, l + 1, nr, e);
                     } else {
                         // ---------------- output layer (M_L = 1) + residual ----------------
