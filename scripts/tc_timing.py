@@ -7,15 +7,21 @@ import paper_2410_04001_b200 as pkg
 from paper_2410_04001_b200 import _lib
 lib = _lib.load()
 n = 148 * 128 * 4
-c = pkg.config2(n_points=n, with_fast=False)
+model_fast = len(sys.argv) > 2 and sys.argv[2] == "fast"
+c = pkg.config2(n_points=n, with_fast=model_fast)
 ctx = pkg.GpuContext(0)
 ctx.set_option(_lib.OPT_KERNEL, 2)
 ctx.set_option(_lib.OPT_FAST_SINCOS, int(sys.argv[1]) if len(sys.argv) > 1 else 0)
-ctx.set_lrnr(c['model'], pkg.F32); ctx.set_points(c['pts'])
-ctx.loss_grad_s(pkg.MODEL_LRNR, c['s'], c['mu'])
+if model_fast:
+    ctx.set_fast(c['fast'], pkg.F32)
+else:
+    ctx.set_lrnr(c['model'], pkg.F32)
+ctx.set_points(c['pts'])
+MODEL = pkg.MODEL_FAST if model_fast else pkg.MODEL_LRNR
+ctx.loss_grad_s(MODEL, c['s'], c['mu'])
 out = (C.c_ulonglong * 16)()
 lib.lrnr_dev_tc_timing(out)
-ctx.loss_grad_s(pkg.MODEL_LRNR, c['s'], c['mu'])
+ctx.loss_grad_s(MODEL, c['s'], c['mu'])
 lib.lrnr_dev_tc_timing(out)
 names = ["fwd: wait P2(ch-1) + add_y", "fwd: chunk top", "fwd: wait P1", "fwd: epilogue act jet + Z split",
          "fwd: Z store + signal", "fwd: trans end (Y, exchange)", "fwd: trans end (SY / output layer)",
@@ -26,10 +32,10 @@ tot = sum(out[:16])
 tiles = 4
 for i in range(16):
     print(f"{names[i]:40s} {out[i]/tiles:12.0f} cycles/tile  {out[i]/tot*100:5.1f}%")
-print("total cycles per tile", tot / tiles, " chunks per tile", 96)
+print("total cycles per tile", tot / tiles)
 import time
 import torch
-for _ in range(2): ctx.loss_grad_s(pkg.MODEL_LRNR, c['s'], c['mu'])
+for _ in range(2): ctx.loss_grad_s(MODEL, c['s'], c['mu'])
 torch.cuda.synchronize(); t0 = time.perf_counter()
-for _ in range(5): ctx.loss_grad_s(pkg.MODEL_LRNR, c['s'], c['mu'])
+for _ in range(5): ctx.loss_grad_s(MODEL, c['s'], c['mu'])
 print(f"host-timed per call (n={n}): {(time.perf_counter()-t0)/5*1e3:.3f} ms")
