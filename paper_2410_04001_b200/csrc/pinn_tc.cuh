@@ -170,6 +170,9 @@ __device__ __forceinline__ void put_rows(unsigned char* buf, int p, int h, const
 
 // named barrier over the 16 epilogue warps (the issuer warps keep running)
 __device__ __forceinline__ void named_bar_epi() { asm volatile("bar.sync 1, %0;" ::"n"(NWE * 32) : "memory"); }
+// named barrier over the 4 epilogue warps that share a TMEM lane quarter (the same 32 points):
+// enough for the per-point norm exchanges through xch
+__device__ __forceinline__ void quarter_bar(int quarter) { asm volatile("bar.sync %0, 128;" ::"r"(8 + quarter) : "memory"); }
 
 // The same 8 values into the forward SY operand in TMEM (this thread's lane = point p,
 // K block h): per slot, 4 packed hi columns at c * 32 + 4h and 4 lo columns 16 further.
@@ -499,8 +502,8 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                     }
                     *reinterpret_cast<float4*>(xch + (h * P + p) * 8) = make_float4(ss[0], ss[1], ss[2], ss[3]);
                     asm volatile("fence.proxy.async.global;" ::: "memory");  // y_0 may be read by a bulk copy
+                    quarter_bar(quarter);
                 }
-                __syncthreads();
                 if (warp < NWE) {
                     float nr[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -619,9 +622,9 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                     }
                     *reinterpret_cast<float4*>(xch + (h * P + p) * 8) = make_float4(pr[0], pr[1], pr[2], pr[3]);
                     asm volatile("fence.proxy.async.global;" ::: "memory");  // y_{l+1} may be read by a bulk copy
+                    quarter_bar(quarter);
                 }
                 TC_MARK(5);
-                __syncthreads();
                 if (warp < NWE) {
                     float nr[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -702,7 +705,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                         named_bar_epi();  // every epilogue thread has read the u partials and y_{L-2}
                         *reinterpret_cast<float4*>(xch + (h * P + p) * 8) = make_float4(ss[0], ss[1], ss[2], ss[3]);
                         *reinterpret_cast<float4*>(xch + (h * P + p) * 8 + 4) = make_float4(ssy[0], ssy[1], ssy[2], ssy[3]);
-                        named_bar_epi();
+                        quarter_bar(quarter);
                         float nst[4] = {0.f, 0.f, 0.f, 0.f}, nsy[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                         for (int hh = 0; hh < 4; ++hh) {
