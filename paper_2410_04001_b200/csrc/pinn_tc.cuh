@@ -82,7 +82,8 @@ constexpr int OFF_B0 = OFF_W + 4 * OPD_SLOT;
 constexpr int OFF_RED = OFF_B0 + NBUF * BUF;   // floats: per-warp-quarter partials [layer][4][RP], loss [4]
 constexpr int OFF_XCH = OFF_RED + (kMaxL * 4 * RP + 4) * 4;  // floats [4 groups][P][8]
 constexpr int OFF_ACC = OFF_XCH + 4 * P * 8 * 4;
-constexpr int SMEM_BYTES = OFF_ACC + 1024 * 4;
+constexpr int OFF_S = OFF_ACC + 1024 * 4;      // the unit's s vector (FP32)
+constexpr int SMEM_BYTES = OFF_S + 1024 * 4;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
 static_assert(BUF % 16 == 0 && OFF_B0 % 1024 == 0, "alignment");
 
@@ -256,6 +257,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
     float* tpart = reinterpret_cast<float*>(smb + OFF_RED);  // [layer][quarter][rank], then loss [quarter]
     float* xch = reinterpret_cast<float*>(smb + OFF_XCH);
     float* acc = reinterpret_cast<float*>(smb + OFF_ACC);
+    float* ssm = reinterpret_cast<float*>(smb + OFF_S);
     unsigned char* X = smb + OFF_X;
     unsigned char* W = smb + OFF_W;
     __shared__ __align__(8) uint64_t wbar[NBUF];           // ring slot filled (TMA)
@@ -479,7 +481,10 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
         const int seg = static_cast<int>(unit % g.units_per_inst);
         const int t_lo = seg * g.tiles_per_unit;
         const int t_hi = min(g.tiles_per_inst, t_lo + g.tiles_per_unit);
-        const double* sv = svec + inst * net.rtotal;
+        // the instance's s coefficients in shared memory (read at every transition end)
+        for (int k = tid; k < net.rtotal; k += NT) ssm[k] = static_cast<float>(svec[inst * net.rtotal + k]);
+        __syncthreads();
+        const float* sv = ssm;
         const float mu0 = float(mus[3 * inst]), mu1 = float(mus[3 * inst + 1]), mu2 = float(mus[3 * inst + 2]);
 
         for (int tile = t_lo; tile < t_hi; ++tile) {
@@ -609,7 +614,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                 }
                 // transition end: Y -> y_{l+1} (scratch), then SY_{l+1} or the output layer
                 const bool last = l + 2 == L;
-                const double* sl = sv + net.soff[l + 1];
+                const float* sl = sv + net.soff[l + 1];
                 const int rtrue = net.r[l + 1];
                 if (warp < NWE) {
                     wait(&zfree, zw & 1);
@@ -696,7 +701,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                         // SY_{L-2} from y_{L-2} (copied into W during the last forward transition);
                         // the first reverse transition recomputes A_{L-2} from it
                         const int lr = L - 2, rr = net.r[lr];
-                        const double* sr = sv + net.soff[lr];
+                        const float* sr = sv + net.soff[lr];
                         float sy[4][NG];
                         float ssy[4] = {0.f, 0.f, 0.f, 0.f};
                         wait(&ybar, yq & 1);
@@ -853,7 +858,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                 }
                 // transition end: T -> dL/ds_l partials; ST_l and SY_{l-1} for the next reverse transition
                 const int rl = net.r[l];
-                const double* sl = sv + net.soff[l];
+                const float* sl = sv + net.soff[l];
                 if (warp < NWE) {
                     float4 yv[NG];
 #pragma unroll
@@ -891,7 +896,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                     }
                     if (l >= 1) {
                         const int rr = net.r[l - 1];
-                        const double* sr = sv + net.soff[l - 1];
+                        const float* sr = sv + net.soff[l - 1];
                         float sy[4][NG];
                         float ssy[4] = {0.f, 0.f, 0.f, 0.f};
                         wait(&ybar, yq & 1);  // y_{l-1} copied into W
