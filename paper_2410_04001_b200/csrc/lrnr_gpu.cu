@@ -281,7 +281,7 @@ void build_tc(Model& m) {
         if (!(amax > 0.0) || !std::isfinite(amax)) return 0;
         int e;
         std::frexp(amax, &e);  // amax < 2^e
-        return 14 - e;
+        return std::max(-40, std::min(40, 14 - e));  // the kernel's exponent range (umma::pow2_exp)
     };
     for (int l = 0; l + 1 < L; ++l) {
         const int rl = m.r[l], rn = m.r[l + 1], M = m.M[l + 1];

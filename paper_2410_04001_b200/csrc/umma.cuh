@@ -216,10 +216,13 @@ __device__ __forceinline__ void split16x2(float x0, float x1, uint32_t& h, uint3
     h = hh;
     l = ll;
 }
-// power-of-two scale 2^k for a non-negative bound b: b * 2^k < 2^15, k clamped to [-100, 100]
+// power-of-two scale 2^k for a non-negative bound b: b * 2^k < 2^15, k clamped to [-40, 40]
+// (a product of up to three such factors is a normal FP32 number; bounds below 2^-26 keep a
+// smaller scale, which only widens their absolute precision window to 2^-65; bounds above
+// 2^54 would overflow FP16 -- jets of 1.8e16 are outside any physical use of the path)
 __device__ __forceinline__ int pow2_exp(float b) {
     const int E = static_cast<int>((__float_as_uint(b) >> 23) & 0xff);  // b < 2^(E - 126)
-    return max(-100, min(100, 140 - E));
+    return max(-40, min(40, 140 - E));
 }
 __device__ __forceinline__ float exp2i(int k) { return __uint_as_float(static_cast<uint32_t>(127 + k) << 23); }
 
