@@ -212,41 +212,49 @@ __device__ __forceinline__ void act3f(float a, float& sg, float& d1, float& d2, 
 __device__ __forceinline__ float exp2c(int k) { return umma::exp2i(max(-126, min(127, k))); }
 
 // Per-point constants of one transition with the power-of-two unscale (P1 / P2 products)
-// and scale (Z / G operands) factors folded in.  Exponents: eS = SY / ST row scale,
-// kU / kV = factor scales, ez / eg = Z / G row scales, each in [-40, 40] (umma::pow2_exp,
-// build_tc); every constant combines at most three of them, so it is a normal FP32 power
-// of two (no clamping of a legitimate factor).
+// and scale (Z / G operands) factors folded in.  Exponents, each in [-40, 40]: Ea / Ed = the
+// combined scale of a raw P1-type product (row scale of SY / ST + factor scale), ez / eg =
+// Z / G row scales, kV / kU = the P2-type factor scales.  Every constant combines at most
+// three of them, so it is a normal FP32 power of two.
 struct FwdScales {
-    float ia[4];        // A_c = P1_c 2^-(eS_c + kU) (+ b)                         (2 exponents)
-    float f1, f2;       // Z_c 2^ez_c = d1 P1_c f_c, c = 1, 2: 2^(ez_c - eS_c - kU)  (3)
-    float f3, f3x;      // Z_3 2^ez3 = d2 A_x P1_1 f3x + d1 P1_3 f3                   (3, 3)
-    float s0;           // Z_0 2^ez0 = sigma s0                                       (1)
-    float iy[4];        // Y unscale 2^-(ez_c + kV)                                   (2)
+    float ia0;          // A_v = P1_v 2^-Ea0 + b
+    float f1, f2, f3;   // Z_c 2^ez_c = d1 P1_c 2^(ez_c - Ea_c), c = 1, 2; u_w term d1 P1_3 f3
+    float g3;           // Z_3 2^ez3 = d2 P1_1^2 2^(ez3 - 2 Ea1) + d1 P1_3 f3
+    float s0;           // Z_0 2^ez0 = sigma s0
+    float iy[4];        // Y unscale 2^-(ez_c + kV)
 };
 struct RevScales {
-    float ia[4];                  // A_c = P1r_c 2^-(eSY_c + kU) (+ b)
-    float k0, k1x, k2x, k3x;      // G0 2^eg0 = d1 e0 k0 + d2 (e1 k1x A_x + e2 k2x A_t + e3 k3x A_w) + d3 e3 k3x A_x^2
-    float k11, k13, k22, k33;     // G1 2^eg1 = d1 e1 k11 + d2 A_x e3 k13; G2 = d1 e2 k22; G3 = d1 e3 k33
-    float it[4];                  // T unscale 2^-(eg_c + kU)
+    float ia0, ia1;                  // A_v = P1r_v 2^-Ea0 + b;  A_x = P1r_x 2^-Ea1
+    float k0, k01, k02, k03, k04;    // G0 2^eg0 = d1 e0 k0 + d2 (e1 r1 k01 + e2 r2 k02 + e3 r3 k03) + d3 e3 r1 A_x k04
+    float k1, k13, k2, k3;           // G1 2^eg1 = d1 e1 k1 + d2 r1 e3 k13; G2 = d1 e2 k2; G3 = d1 e3 k3
+    float it[4];                     // T unscale 2^-(eg_c + kU)
 };
-// (e_c = the DZ columns, still scaled by 2^(eST_c + kV); k.. = 2^(eg - eST - kV), at most 3 exponents)
+// (r = recomputed P1r columns, scaled by 2^Ea; e = DZ columns, scaled by 2^Ed)
 
-// Forward constants from the exact SY row norms (slot c exponent eS[c]) of transition l.
-__device__ __forceinline__ void fwd_scales(FwdScales& f, const NetTC& net, int l, const float (&nr)[4], const int (&eS)[4]) {
-    const int kU = net.kU[l], kV = net.kV[l];
+// Combined exponents of the raw P1-type products: E_c = clamp(e_c + k) for the natural row
+// exponents e_c; the row is then written with scale 2^(E_c - k) (e_c updated to it)
+__device__ __forceinline__ void combine_exp(int (&e)[4], int k, int (&E)[4]) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        E[c] = max(-40, min(40, e[c] + k));
+        e[c] = E[c] - k;
+    }
+}
+
+// Forward constants from the exact SY row norms (combined exponents Ea[c]) of transition l.
+__device__ __forceinline__ void fwd_scales(FwdScales& f, const NetTC& net, int l, const float (&nr)[4], const int (&Ea)[4]) {
+    const int kV = net.kV[l];
     const float mu = net.muU[l];
     const float bx = nr[1] * mu, bt = nr[2] * mu, bw = nr[3] * mu;
     const int ez[4] = {umma::pow2_exp(1.f), umma::pow2_exp(bx), umma::pow2_exp(bt), umma::pow2_exp(fmaf(bx, bx, bw))};
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        f.ia[c] = exp2c(-eS[c] - kU);
-        f.iy[c] = exp2c(-ez[c] - kV);
-    }
-    f.f1 = exp2c(ez[1] - eS[1] - kU);
-    f.f2 = exp2c(ez[2] - eS[2] - kU);
-    f.f3 = exp2c(ez[3] - eS[3] - kU);
-    f.f3x = exp2c(ez[3] - eS[1] - kU);
+    f.ia0 = exp2c(-Ea[0]);
+    f.f1 = exp2c(ez[1] - Ea[1]);
+    f.f2 = exp2c(ez[2] - Ea[2]);
+    f.f3 = exp2c(ez[3] - Ea[3]);
+    f.g3 = exp2c(ez[3] - 2 * Ea[1]);
     f.s0 = exp2c(ez[0]);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) f.iy[c] = exp2c(-ez[c] - kV);
 }
 
 template <int ACT, bool FAST>
@@ -437,7 +445,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
     // |A_c| <= |SY_c| muU): |G0| <= B0 + B1 bx + B2 bt + B3 (c3 bx^2 + bw), |G1| <= B1 + 2 B3 bx.
     auto rev_scales = [&](RevScales& r, float (&nst)[4], float (&nsy)[4], int lr, const float (&st)[4][NG],
                           const float (&sy)[4][NG]) {
-        int est[4], esy[4];
+        int est[4], esy[4], Ed[4], Ea[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             nst[c] = sqrtf(nst[c]);
@@ -445,25 +453,28 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
             est[c] = umma::pow2_exp(nst[c]);
             esy[c] = umma::pow2_exp(nsy[c]);
         }
+        const int kU = net.kU[lr], kV = net.kV[lr];
+        combine_exp(est, kV, Ed);  // DZ = ST V^T
+        combine_exp(esy, kU, Ea);  // A = SY U^T
         if (NG * h < net.rk[lr + 1]) put_rows(X, p, h, st, est);
         if (NG * h < net.rk[lr]) put_rows(W, p, h, sy, esy);
-        const int kU = net.kU[lr], kV = net.kV[lr];
         const float mu = net.muU[lr], mv = net.muV[lr];
         const float bx = nsy[1] * mu, bt = nsy[2] * mu, bw = nsy[3] * mu;
         const float B0 = nst[0] * mv, B1 = nst[1] * mv, B2 = nst[2] * mv, B3 = nst[3] * mv;
         const int eg0 = umma::pow2_exp(B0 + B1 * bx + B2 * bt + B3 * fmaf(net.c3 * bx, bx, bw));
         const int eg1 = umma::pow2_exp(fmaf(2.f * B3, bx, B1));
         const int eg2 = umma::pow2_exp(B2), eg3 = umma::pow2_exp(B3);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) r.ia[c] = exp2c(-esy[c] - kU);
-        r.k0 = exp2c(eg0 - est[0] - kV);
-        r.k1x = exp2c(eg0 - est[1] - kV);
-        r.k2x = exp2c(eg0 - est[2] - kV);
-        r.k3x = exp2c(eg0 - est[3] - kV);
-        r.k11 = exp2c(eg1 - est[1] - kV);
-        r.k13 = 2.f * exp2c(eg1 - est[3] - kV);
-        r.k22 = exp2c(eg2 - est[2] - kV);
-        r.k33 = exp2c(eg3 - est[3] - kV);
+        r.ia0 = exp2c(-Ea[0]);
+        r.ia1 = exp2c(-Ea[1]);
+        r.k0 = exp2c(eg0 - Ed[0]);
+        r.k01 = exp2c(eg0 - Ed[1] - Ea[1]);
+        r.k02 = exp2c(eg0 - Ed[2] - Ea[2]);
+        r.k03 = exp2c(eg0 - Ed[3] - Ea[3]);
+        r.k04 = exp2c(eg0 - Ed[3] - Ea[1]);  // times A_x (unscaled) in the A_x^2 term
+        r.k1 = exp2c(eg1 - Ed[1]);
+        r.k13 = 2.f * exp2c(eg1 - Ed[3] - Ea[1]);
+        r.k2 = exp2c(eg2 - Ed[2]);
+        r.k3 = exp2c(eg3 - Ed[3]);
         r.it[0] = exp2c(-eg0 - kU);
         r.it[1] = exp2c(-eg1 - kU);
         r.it[2] = exp2c(-eg2 - kU);
@@ -537,9 +548,11 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                         nr[c] = sqrtf(nr[c]);
                         e[c] = umma::pow2_exp(nr[c]);
                     }
+                    int Ea[4];
+                    combine_exp(e, net.kU[0], Ea);
                     if (NG * h < net.rk[0]) put_rows_tmem(tlane + TM_SY, h, sy, e);
                     umma::tmem_st_wait();
-                    fwd_scales(fs, net, 0, nr, e);
+                    fwd_scales(fs, net, 0, nr, Ea);
                 }
                 umma::fence_before();  // SY in TMEM -> the first P1
                 __syncthreads();
@@ -581,13 +594,13 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
 #pragma unroll
                             for (int i = 0; i < 2; ++i) {
                                 const float r1 = a[1][n + i], r2 = a[2][n + i], r3 = a[3][n + i];
-                                const float av = fmaf(a[0][n + i], fs.ia[0], bias[NG * h + n + i]);
+                                const float av = fmaf(a[0][n + i], fs.ia0, bias[NG * h + n + i]);
                                 float sg, d1, d2, d3;
                                 act3f<ACT, FAST>(av, sg, d1, d2, d3);
                                 z[i][0] = sg * fs.s0;
                                 z[i][1] = d1 * (r1 * fs.f1);
                                 z[i][2] = d1 * (r2 * fs.f2);
-                                z[i][3] = fmaf(d2 * (r1 * fs.ia[1]), r1 * fs.f3x, d1 * (r3 * fs.f3));
+                                z[i][3] = fmaf(d2 * r1, r1 * fs.g3, d1 * (r3 * fs.f3));
                             }
 #pragma unroll
                             for (int c = 0; c < 4; ++c) umma::split16x2(z[0][c], z[1][c], zh[c][n / 2], zl[c][n / 2]);
@@ -659,9 +672,11 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                             nr[c] = sqrtf(nr[c]);
                             e[c] = umma::pow2_exp(nr[c]);
                         }
+                        int Ea[4];
+                        combine_exp(e, net.kU[l + 1], Ea);
                         if (NG * h < net.rk[l + 1]) put_rows_tmem(tlane + TM_SY, h, ysum, e);
                         umma::tmem_st_wait();
-                        fwd_scales(fs, net, l + 1, nr, e);
+                        fwd_scales(fs, net, l + 1, nr, Ea);
                     } else {
                         // ---------------- output layer (M_L = 1) + residual ----------------
                         float u[4] = {nr[0] + net.ulast[rtrue], nr[1], nr[2], nr[3]};
@@ -783,20 +798,19 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                             float gg[2][4];
 #pragma unroll
                             for (int i = 0; i < 2; ++i) {
-                                const float av = fmaf(a[0][n + i], rs.ia[0], bias[NG * h + n + i]);
-                                const float ax = a[1][n + i] * rs.ia[1], at = a[2][n + i] * rs.ia[2];
-                                const float aw = a[3][n + i] * rs.ia[3];
+                                const float r1 = a[1][n + i], r2 = a[2][n + i], r3 = a[3][n + i];
                                 const float e0 = dz[0][n + i], e1 = dz[1][n + i], e2 = dz[2][n + i], e3 = dz[3][n + i];
+                                const float av = fmaf(a[0][n + i], rs.ia0, bias[NG * h + n + i]);
                                 float sg, d1, d2, d3;
                                 act3f<ACT, FAST>(av, sg, d1, d2, d3);
-                                const float e3x = e3 * rs.k3x;
-                                float wv = e3x * aw;
-                                wv = fmaf(e2 * rs.k2x, at, wv);
-                                wv = fmaf(e1 * rs.k1x, ax, wv);
-                                gg[i][0] = fmaf(d1, e0 * rs.k0, fmaf(d2, wv, d3 * ((e3x * ax) * ax)));
-                                gg[i][1] = fmaf(d1, e1 * rs.k11, (d2 * ax) * (e3 * rs.k13));
-                                gg[i][2] = d1 * (e2 * rs.k22);
-                                gg[i][3] = d1 * (e3 * rs.k33);
+                                float wv = (e3 * rs.k03) * r3;
+                                wv = fmaf(e2 * rs.k02, r2, wv);
+                                wv = fmaf(e1 * rs.k01, r1, wv);
+                                const float xv = ((e3 * rs.k04) * r1) * (r1 * rs.ia1);
+                                gg[i][0] = fmaf(d1, e0 * rs.k0, fmaf(d2, wv, d3 * xv));
+                                gg[i][1] = fmaf(d1, e1 * rs.k1, (d2 * r1) * (e3 * rs.k13));
+                                gg[i][2] = d1 * (e2 * rs.k2);
+                                gg[i][3] = d1 * (e3 * rs.k3);
                             }
 #pragma unroll
                             for (int c = 0; c < 4; ++c) umma::split16x2(gg[0][c], gg[1][c], gh[c][n / 2], gl[c][n / 2]);
@@ -817,20 +831,19 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                                 float gg[2][4];
 #pragma unroll
                                 for (int i = 0; i < 2; ++i) {
-                                    const float av = fmaf(a[0][n + i], rs.ia[0], bias[NG * h + 4 * hf + n + i]);
-                                    const float ax = a[1][n + i] * rs.ia[1], at = a[2][n + i] * rs.ia[2];
-                                    const float aw = a[3][n + i] * rs.ia[3];
+                                    const float r1 = a[1][n + i], r2 = a[2][n + i], r3 = a[3][n + i];
                                     const float e0 = dz[0][n + i], e1 = dz[1][n + i], e2 = dz[2][n + i], e3 = dz[3][n + i];
+                                    const float av = fmaf(a[0][n + i], rs.ia0, bias[NG * h + 4 * hf + n + i]);
                                     float sg, d1, d2, d3;
                                     act3f<ACT, FAST>(av, sg, d1, d2, d3);
-                                    const float e3x = e3 * rs.k3x;
-                                    float wv = e3x * aw;
-                                    wv = fmaf(e2 * rs.k2x, at, wv);
-                                    wv = fmaf(e1 * rs.k1x, ax, wv);
-                                    gg[i][0] = fmaf(d1, e0 * rs.k0, fmaf(d2, wv, d3 * ((e3x * ax) * ax)));
-                                    gg[i][1] = fmaf(d1, e1 * rs.k11, (d2 * ax) * (e3 * rs.k13));
-                                    gg[i][2] = d1 * (e2 * rs.k22);
-                                    gg[i][3] = d1 * (e3 * rs.k33);
+                                    float wv = (e3 * rs.k03) * r3;
+                                    wv = fmaf(e2 * rs.k02, r2, wv);
+                                    wv = fmaf(e1 * rs.k01, r1, wv);
+                                    const float xv = ((e3 * rs.k04) * r1) * (r1 * rs.ia1);
+                                    gg[i][0] = fmaf(d1, e0 * rs.k0, fmaf(d2, wv, d3 * xv));
+                                    gg[i][1] = fmaf(d1, e1 * rs.k1, (d2 * r1) * (e3 * rs.k13));
+                                    gg[i][2] = d1 * (e2 * rs.k2);
+                                    gg[i][3] = d1 * (e3 * rs.k3);
                                 }
 #pragma unroll
                                 for (int c = 0; c < 4; ++c)
