@@ -139,6 +139,15 @@ int lrnr_gpu_set_hyper(lrnr_gpu_ctx* ctx, int n_layers, const int64_t* hw, const
 int lrnr_gpu_set_points(lrnr_gpu_ctx* ctx, const double* xt, int64_t n_inst, int64_t n_per_inst);
 int lrnr_gpu_set_points_device(lrnr_gpu_ctx* ctx, const void* xt_dev, int64_t n_inst,
                                int64_t n_per_inst);
+/* Double-buffered host points for a training loop: lrnr_gpu_stage_points copies
+ * the NEXT batch (host pointer, best pinned) into a staging buffer on an internal
+ * copy stream and returns at once, so the copy overlaps the gradient calls of the
+ * current batch; the host buffer must stay valid and unmodified until the
+ * following lrnr_gpu_use_staged_points returns.  lrnr_gpu_use_staged_points makes
+ * the staged batch current (later work on the context's stream waits for the
+ * copy).  Same point layout and counts as lrnr_gpu_set_points. */
+int lrnr_gpu_stage_points(lrnr_gpu_ctx* ctx, const double* xt, int64_t n_inst, int64_t n_per_inst);
+int lrnr_gpu_use_staged_points(lrnr_gpu_ctx* ctx);
 
 /* ---- per-step gradient calls (host buffers; synchronous) ----
  *

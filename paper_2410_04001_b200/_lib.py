@@ -15,7 +15,8 @@ LIB_PATH = os.environ.get("LRNR_GPU_LIB") or os.path.join(PKG, "liblrnr_gpu.so")
 EXPORTS = (
     "lrnr_gpu_create", "lrnr_gpu_destroy", "lrnr_gpu_last_error", "lrnr_gpu_last_layer_tag",
     "lrnr_gpu_set_stream", "lrnr_gpu_set_option", "lrnr_gpu_launch_count", "lrnr_gpu_set_lrnr", "lrnr_gpu_set_fast",
-    "lrnr_gpu_set_hyper", "lrnr_gpu_set_points", "lrnr_gpu_set_points_device", "lrnr_gpu_loss_grad_s",
+    "lrnr_gpu_set_hyper", "lrnr_gpu_set_points", "lrnr_gpu_set_points_device", "lrnr_gpu_stage_points",
+    "lrnr_gpu_use_staged_points", "lrnr_gpu_loss_grad_s",
     "lrnr_gpu_set_boundary", "lrnr_gpu_terms_grad", "lrnr_gpu_meta_terms_grad", "lrnr_gpu_set_meta_boundary", "lrnr_gpu_fine_tune",
     "lrnr_gpu_fast_solve", "lrnr_host_epoch_seed", "lrnr_host_sample_batch", "lrnr_gpu_l1_error",
     "lrnr_ckpt_last_error", "lrnr_ckpt_create", "lrnr_ckpt_load", "lrnr_ckpt_save", "lrnr_ckpt_free",
@@ -66,6 +67,8 @@ def load() -> C.CDLL:
     lib.lrnr_gpu_set_hyper.argtypes = [vp, ip, dp, dp, dp, dp]
     lib.lrnr_gpu_set_points.argtypes = [vp, dp, i64, i64]
     lib.lrnr_gpu_set_points_device.argtypes = [vp, vp, i64, i64]
+    lib.lrnr_gpu_stage_points.argtypes = [vp, dp, i64, i64]
+    lib.lrnr_gpu_use_staged_points.argtypes = [vp]
     lib.lrnr_gpu_loss_grad_s.argtypes = [vp, ip, dp, dp, C.c_double, dp, dp, dp]
     lib.lrnr_gpu_set_boundary.argtypes = [vp, dp, i64, dp, i64]
     lib.lrnr_gpu_terms_grad.argtypes = [vp, ip, dp, dp, ip, C.c_double, C.c_double, C.c_double, dp, C.c_double,

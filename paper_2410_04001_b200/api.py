@@ -335,6 +335,22 @@ class GpuContext:
         self._rc(self.lib.lrnr_gpu_set_points(self.h, _p(xt), n_inst, n // n_inst), "set_points")
         self.n_points, self.n_inst = n, n_inst
 
+    def stage_points(self, xt, n_inst: int = 1):
+        """Copy the NEXT batch asynchronously (lrnr_gpu_stage_points); keep xt unmodified until
+        use_staged_points() returns (pinned memory makes the copy overlap current work)."""
+        xt = _f64(xt).reshape(-1, 2)
+        n = xt.shape[0]
+        if n % n_inst:
+            raise ValueError("points not divisible into instances")
+        self._keep_stage = xt
+        self._rc(self.lib.lrnr_gpu_stage_points(self.h, _p(xt), n_inst, n // n_inst), "stage_points")
+        self._stage_counts = (n, n_inst)
+
+    def use_staged_points(self):
+        self._rc(self.lib.lrnr_gpu_use_staged_points(self.h), "use_staged_points")
+        self._keep_pts, self._keep_stage = self._keep_stage, None
+        self.n_points, self.n_inst = self._stage_counts
+
     def set_points_device(self, ptr: int, n_points: int, n_inst: int = 1):
         self._rc(self.lib.lrnr_gpu_set_points_device(self.h, C.c_void_p(ptr), n_inst, n_points // n_inst),
                  "set_points_device")

@@ -206,6 +206,11 @@ struct lrnr_gpu_ctx {
     lrnr_b200::detail::Hyper hyper;
     // points (double, device)
     lrnr_b200::detail::DevBuf pts_own;
+    // staged next batch (lrnr_gpu_stage_points), copied on copy_stream
+    lrnr_b200::detail::DevBuf pts_stage;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t stage_done = nullptr, stage_free = nullptr;
+    int64_t stage_inst = -1, stage_per = 0;
     const double* pts = nullptr;
     int64_t n_inst = 0, n_per = 0;
     // coefficients (double, device)

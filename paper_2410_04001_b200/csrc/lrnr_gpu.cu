@@ -939,7 +939,13 @@ int lrnr_gpu_destroy(lrnr_gpu_ctx* ctx) {
     comm_release(ctx);
     for (auto& m : ctx->models) release_model(m);
     ctx->hyper.dev.release();
-    for (DevBuf* b : {&ctx->pts_own, &ctx->s_dev, &ctx->mu_dev, &ctx->scratch, &ctx->ascratch, &ctx->part, &ctx->out, &ctx->bad,
+    if (ctx->copy_stream) {
+        cudaStreamSynchronize(ctx->copy_stream);
+        cudaStreamDestroy(ctx->copy_stream);
+        cudaEventDestroy(ctx->stage_done);
+        cudaEventDestroy(ctx->stage_free);
+    }
+    for (DevBuf* b : {&ctx->pts_own, &ctx->pts_stage, &ctx->s_dev, &ctx->mu_dev, &ctx->scratch, &ctx->ascratch, &ctx->part, &ctx->out, &ctx->bad,
                       &ctx->acts, &ctx->G, &ctx->hgrad, &ctx->jets, &ctx->meta_ws, &ctx->gram_ws, &ctx->bnd_pts,
                       &ctx->bnd_x, &ctx->bnd_spec, &ctx->bnd_jets, &ctx->solve_rows, &ctx->solve_state, &ctx->solve_m,
                       &ctx->solve_v, &ctx->solve_best, &ctx->solve_s0, &ctx->solve_bt, &ctx->solve_losses,
@@ -1131,6 +1137,44 @@ int lrnr_gpu_set_points(lrnr_gpu_ctx* ctx, const double* xt, int64_t n_inst, int
         ctx->pts = ctx->pts_own.as<double>();
         ctx->n_inst = n_inst;
         ctx->n_per = n_per;
+        ++ctx->comm_gen;
+    });
+}
+
+int lrnr_gpu_stage_points(lrnr_gpu_ctx* ctx, const double* xt, int64_t n_inst, int64_t n_per) {
+    return guarded(ctx, [&] {
+        require(n_inst >= 1 && n_per >= 0, "bad point counts");
+        require(xt || n_per == 0, "null points");
+        if (!ctx->copy_stream) {
+            CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&ctx->stage_done, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ctx->stage_free, cudaEventDisableTiming));
+        }
+        const size_t bytes = static_cast<size_t>(n_inst * n_per * 2) * sizeof(double);
+        if (ctx->pts_stage.bytes < bytes + 16) {  // (re)allocation: nothing may use the old buffer
+            CK(cudaStreamSynchronize(ctx->copy_stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            ctx->pts_stage.ensure(bytes + 16);
+        }
+        // the staging buffer may still be read by work already submitted on the compute stream
+        CK(cudaEventRecord(ctx->stage_free, ctx->stream));
+        CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->stage_free, 0));
+        if (bytes) CK(cudaMemcpyAsync(ctx->pts_stage.p, xt, bytes, cudaMemcpyHostToDevice, ctx->copy_stream));
+        CK(cudaEventRecord(ctx->stage_done, ctx->copy_stream));
+        ctx->stage_inst = n_inst;
+        ctx->stage_per = n_per;
+    });
+}
+
+int lrnr_gpu_use_staged_points(lrnr_gpu_ctx* ctx) {
+    return guarded(ctx, [&] {
+        require(ctx->stage_inst >= 1, "no staged points (lrnr_gpu_stage_points first)");
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->stage_done, 0));
+        std::swap(ctx->pts_own, ctx->pts_stage);
+        ctx->pts = ctx->pts_own.as<double>();
+        ctx->n_inst = ctx->stage_inst;
+        ctx->n_per = ctx->stage_per;
+        ctx->stage_inst = -1;
         ++ctx->comm_gen;
     });
 }

@@ -224,6 +224,31 @@ def test_c3_full_config_shard_invariant(gpu):
     assert abs(full["value"] - (halves[0]["value"] + halves[1]["value"])) <= 1e-5 * abs(full["value"])
 
 
+def test_staged_points_double_buffer(gpu):
+    """lrnr_gpu_stage_points / lrnr_gpu_use_staged_points (the double-buffered host upload of a
+    training loop): alternating batches, each staged while the previous one is in use, give
+    bitwise the results of lrnr_gpu_set_points; the staged host buffer may then be reused."""
+    c = pkg.config2(n_points=0, act=pkg.ACT_SIN, with_fast=False)
+    gpu.set_lrnr(c["model"], pkg.F32)
+    batches = [pkg.sample_collocation(300 + k, 5000 + 700 * k) for k in range(3)]
+    want = []
+    for b in batches:
+        gpu.set_points(b)
+        want.append(gpu.loss_grad_s(pkg.MODEL_LRNR, c["s"], c["mu"]))
+    buf = np.array(batches[0])
+    gpu.stage_points(buf)
+    for k in range(len(batches)):
+        gpu.use_staged_points()
+        if k + 1 < len(batches):
+            buf = np.array(batches[k + 1])  # a new host buffer each step
+            gpu.stage_points(buf)
+        got = gpu.loss_grad_s(pkg.MODEL_LRNR, c["s"], c["mu"])
+        assert got["value"] == want[k]["value"]
+        assert np.array_equal(got["grad_s"], want[k]["grad_s"])
+    with pytest.raises(ValueError):
+        gpu.use_staged_points()  # nothing staged (LRNR_EINVAL)
+
+
 def test_hyper_forward_vjp_match_reference(gpu, golden):
     """Hypernetwork forward + VJP (c3 shape) against the reference (FP64 path)."""
     split = golden["c2_ranks"]
