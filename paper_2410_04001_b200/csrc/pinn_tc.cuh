@@ -55,21 +55,12 @@ constexpr int TM_Y = 384;   // Y / T: per slot 32 fp32 columns
 // Phase-2 products of YACC consecutive chunks accumulate in TMEM before the epilogue
 // adds them to its FP32 running sum (a long tensor-core accumulation loses precision:
 // K = 256 in one accumulator reached 1.2e-4 with 3xTF32).
-#ifndef TC_YACC
-#define TC_YACC 2
-#endif
-constexpr int YACC = TC_YACC;
+constexpr int YACC = 2;
 // reverse: T products of YACC_R chunks per accumulator.  Measured on c2 (scripts/c2_err.py):
 // the reverse tolerates a whole transition (8 chunks) in one accumulator with no change in
 // the error (dL/ds 7.8e-6), the forward does not (8 chunks: dL/ds 3.3e-5, loss 6.4e-5), so
 // YACC = 2, YACC_R = 8 (c2 LRNR 13.18 -> 12.87 ms: no running T sum live in the chunk loop)
-#ifndef TC_YACC_R
-#define TC_YACC_R 8
-#endif
-constexpr int YACC_R = TC_YACC_R;
-#ifndef TC_REV_LOADALL
-#define TC_REV_LOADALL 0
-#endif
+constexpr int YACC_R = 8;
 
 // shared memory (bytes)
 constexpr int OPD_HALF = P * RP * 2;           // one fp16 tile of a jet slot (128 rows x 32 K)
@@ -782,40 +773,6 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                         TC_MARK(8);
                         const float* bias = reinterpret_cast<const float*>(slot(q) + bbias);
                         uint32_t gh[4][NG / 2], gl[4][NG / 2];
-#if TC_REV_LOADALL
-                        // all of A / DZ up front (the running T sum is not live inside the chunk loop
-                        // when YACC_R >= nc): the next chunk's MMAs may start before the VJP math
-                        float a[4][NG], dz[4][NG];
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            umma::tmem_ld8(tlane + TM_R + c * 32 + NG * h, a[c]);
-                            umma::tmem_ld8(tlane + TM_R + 128 + c * 32 + NG * h, dz[c]);
-                        }
-                        umma::tmem_ld_wait();
-                        signal(BAR_RFREE);
-#pragma unroll
-                        for (int n = 0; n < NG; n += 2) {
-                            float gg[2][4];
-#pragma unroll
-                            for (int i = 0; i < 2; ++i) {
-                                const float r1 = a[1][n + i], r2 = a[2][n + i], r3 = a[3][n + i];
-                                const float e0 = dz[0][n + i], e1 = dz[1][n + i], e2 = dz[2][n + i], e3 = dz[3][n + i];
-                                const float av = fmaf(a[0][n + i], rs.ia0, bias[NG * h + n + i]);
-                                float sg, d1, d2, d3;
-                                act3f<ACT, FAST>(av, sg, d1, d2, d3);
-                                float wv = (e3 * rs.k03) * r3;
-                                wv = fmaf(e2 * rs.k02, r2, wv);
-                                wv = fmaf(e1 * rs.k01, r1, wv);
-                                const float xv = ((e3 * rs.k04) * r1) * (r1 * rs.ia1);
-                                gg[i][0] = fmaf(d1, e0 * rs.k0, fmaf(d2, wv, d3 * xv));
-                                gg[i][1] = fmaf(d1, e1 * rs.k1, (d2 * r1) * (e3 * rs.k13));
-                                gg[i][2] = d1 * (e2 * rs.k2);
-                                gg[i][3] = d1 * (e3 * rs.k3);
-                            }
-#pragma unroll
-                            for (int c = 0; c < 4; ++c) umma::split16x2(gg[0][c], gg[1][c], gh[c][n / 2], gl[c][n / 2]);
-                        }
-#else
 #pragma unroll
                         for (int hf = 0; hf < 2; ++hf) {
                             float a[4][NG / 2], dz[4][NG / 2];
@@ -850,7 +807,6 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                                     umma::split16x2(gg[0][c], gg[1][c], gh[c][2 * hf + n / 2], gl[c][2 * hf + n / 2]);
                             }
                         }
-#endif
                         TC_MARK(9);
                         if (ch > 0) {
                             wait(&zfree, zw & 1);  // P2r(q - 1): G free, its T product ready

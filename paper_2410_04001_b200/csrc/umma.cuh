@@ -302,11 +302,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 #ifndef UMMA_WAIT_HINT_NS
 #define UMMA_WAIT_HINT_NS 1000000
 #endif
-#ifndef UMMA_WAIT_MODE
-#define UMMA_WAIT_MODE 0
-#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-#if UMMA_WAIT_MODE == 0
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "WAIT_%=:\n\t"
@@ -314,26 +310,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
         "r"(parity), "n"(UMMA_WAIT_HINT_NS)
         : "memory");
-#elif UMMA_WAIT_MODE == 1
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
-        "r"(parity)
-        : "memory");
-#else
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok) : "r"(smem_addr(bar)), "r"(parity) : "memory");
-    while (!ok) {
-        __nanosleep(UMMA_WAIT_MODE);
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok) : "r"(smem_addr(bar)), "r"(parity) : "memory");
-    }
-#endif
 }
 
 // fp32 -> (hi, lo) with hi exactly representable in TF32 (10-bit mantissa,
