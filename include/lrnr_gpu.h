@@ -89,11 +89,10 @@ int lrnr_gpu_set_stream(lrnr_gpu_ctx* ctx, void* cuda_stream);
 /* Options.  LRNR_OPT_FAST_SINCOS (FP32 sin networks): 1 = sin/cos from the SFU
  * approximations after a Cody-Waite reduction (~4e-7 absolute), 0 = polynomial
  * sin/cos after a 3-term reduction (~1.5 ulp, default).  LRNR_OPT_KERNEL:
- * 0 = auto (default): FP32 nets whose hidden widths and ranks are all <= 32
- * (the FastLRNR) on the narrow-network kernel (lane pairs per point, whole net
- * in shared memory), FP32 LRNR with ranks <= 32 on the tcgen05 tensor-core
- * tile kernel (3xTF32), other FP32/FP64 shapes with ranks <= 64 on the FMA
- * tile-GEMM kernel, the rest on the per-point streaming kernel;
+ * 0 = auto (default): every FP32 model with ranks <= 32 (the LRNR and the
+ * FastLRNR) on the tcgen05 tensor-core tile kernel (FP16 two-term split
+ * operands, FP32 accumulation), other FP32/FP64 shapes with ranks <= 64 on
+ * the FMA tile-GEMM kernel, the rest on the per-point streaming kernel;
  * batches below ~16 points per SM on the small-batch latency kernel (one CTA
  * per point, threads across neurons / ranks);
  * 1 = force the streaming kernel, 2 = tensor-core kernel wherever it applies
@@ -441,6 +440,20 @@ int lrnr_host_eim_greedy(int64_t m, int64_t n_cols, const double* snapshots, int
 int lrnr_host_build_fastparams(int depth, const int64_t* widths, const int64_t* ranks, const double* params,
                                int act, int64_t r_hat, const int64_t* red, const int64_t* indices,
                                const double* xi, double* out_fparams);
+
+/* Q-DEIM index selection (BASELINE.json configs[1]: "indices from pivoted QR of U^l";
+ * SURVEY.md Appendix A.3).  The reference selects by greedy EIM on harvested snapshots
+ * (reduction.cpp:176-232) and has no pivoted-QR mode, so only the selection is new:
+ * lrnr_host_qdeim returns the rows a column-pivoted QR of xi^T picks (xi m x r row-major;
+ * largest residual norm first, lowest index on ties; out_idx r entries, -1 padded,
+ * out_count = rank found).  lrnr_host_build_fast_qdeim builds, per inner layer,
+ * EimBasis{xi = U^l, indices = qdeim(U^l)} with r_hat_l = r_l and runs the reference's
+ * build_fastparams (reduction.cpp:240-283) on it; r_hat >= max r_l sizes out_indices
+ * ((L-1) x r_hat, -1 padded).  Outputs as lrnr_host_build_fast. */
+int lrnr_host_qdeim(int64_t m, int64_t r, const double* xi, int64_t* out_idx, int64_t* out_count);
+int lrnr_host_build_fast_qdeim(int depth, const int64_t* widths, const int64_t* ranks, const double* params,
+                               int act, int64_t r_hat, int64_t* out_red, int64_t* out_indices,
+                               double* out_fparams);
 
 /* ---- FastLRNR construction on the device ---------
  * lrnr_gpu_eim_greedy replaces reduction::eim_greedy (reduction.cpp:150-238):

@@ -30,6 +30,7 @@ EXPORTS = (
     "lrnr_gpu_eim_greedy", "lrnr_gpu_build_fast", "lrnr_gpu_harvest_snapshots",
     "lrnr_gpu_comm_unique_id", "lrnr_gpu_comm_init", "lrnr_gpu_set_comm", "lrnr_gpu_comm_info", "lrnr_gpu_allreduce",
     "lrnr_gpu_values", "lrnr_gpu_loss_tune", "lrnr_gpu_loss_fast", "lrnr_gpu_loss_meta", "lrnr_host_hyper_forward",
+    "lrnr_host_qdeim", "lrnr_host_build_fast_qdeim",
 )
 
 LRNR_OK, LRNR_EINVAL, LRNR_ENONFINITE, LRNR_ECUDA, LRNR_ENOMEM, LRNR_ESTATE, LRNR_ENCCL = range(7)
@@ -115,6 +116,8 @@ def load() -> C.CDLL:
     lib.lrnr_host_harvest_points.argtypes = [dp, i64, i64, i64, C.c_double, C.c_uint64, dp]
     lib.lrnr_host_eim_greedy.argtypes = [i64, i64, dp, i64, dp, dp, dp, dp]
     lib.lrnr_host_build_fastparams.argtypes = [ip, dp, dp, dp, ip, i64, dp, dp, dp, dp]
+    lib.lrnr_host_qdeim.argtypes = [i64, i64, dp, dp, dp]
+    lib.lrnr_host_build_fast_qdeim.argtypes = [ip, dp, dp, dp, ip, i64, dp, dp, dp]
     lib.lrnr_gpu_eim_greedy.argtypes = [vp, i64, i64, dp, i64, dp, dp, dp, dp]
     lib.lrnr_gpu_harvest_snapshots.argtypes = [vp, ip, dp, dp, dp, ip, dp, i64, dp, i64, i64, C.c_double,
                                                C.c_uint64, dp]

@@ -259,6 +259,32 @@ def build_fastparams(model: LrnrParams, bases, r_hat=None) -> FastParams:
     return _fast_result(model, r_hat, red, idx, F, exh)
 
 
+def qdeim(xi):
+    """Q-DEIM rows of the basis xi (M x r): the rows a column-pivoted QR of xi^T picks, in
+    selection order (BASELINE configs[1] wording; no reference counterpart)."""
+    X = _f64(xi)
+    if X.ndim != 2:
+        raise ValueError("qdeim: xi must be a 2-D (M x r) array")
+    m, r = X.shape
+    idx = np.zeros(max(r, 1), np.int64)
+    cnt = C.c_int64(0)
+    if _lib.load().lrnr_host_qdeim(m, r, _p(X), _p(idx), C.byref(cnt)) != 0:
+        raise ValueError("qdeim: bad sizes")
+    return idx[:cnt.value].copy()
+
+
+def build_fast_qdeim(model: LrnrParams) -> FastParams:
+    """FastLRNR with Q-DEIM indices: per inner layer EimBasis{xi = U^l, indices = qdeim(U^l)},
+    r_hat_l = r_l, then the reference's build_fastparams (reduction.cpp:240-283)."""
+    r_hat = int(max(model.ranks[:-1]))
+    red, idx, F, exh = _fast_buffers(model, r_hat)
+    rc = _lib.load().lrnr_host_build_fast_qdeim(model.depth, _p(model.widths), _p(model.ranks),
+                                                _p(_f64(model.params)), model.act, r_hat, _p(red), _p(idx), _p(F))
+    if rc != 0:
+        raise ValueError("build_fast_qdeim: rank-deficient U^l or singular interpolation block")
+    return _fast_result(model, r_hat, red, idx, F, exh)
+
+
 # ---------------------------------------------------------------------------
 # device context
 # ---------------------------------------------------------------------------
