@@ -16,7 +16,8 @@
 //             dU   dU_c[n, :] += G[:, n]^T SY_l                (M 128 neurons, N rp_l, K 128 rows)
 //             dV   dV_c[n, :] += Z[:, n]^T ST_{l+1}            (M 128 neurons, N rp_{l+1}, K 128 rows)
 //   dU / dV accumulate in TMEM over both halves of the tile and are flushed once
-//   per chunk into this CTA's partial (red.global.add, one writer per address).
+//   per chunk into this CTA's partial (red.global.add of whole 128-byte lines through a
+//   per-warp staging tile, one writer per address).
 // Per 128 neurons x 32 points: forward 12 MMAs, reverse 32 (v1: 320 N = 16 / M = 64 MMAs).
 // Shared memory (bf16, canonical no-swizzle core matrices of 8 rows x 16 B):
 //   SY / ST per half  [rank grp][row grp][8 rows][8 ranks]            16 KB each
@@ -76,7 +77,13 @@ constexpr int OFF_RING = OFF_G + ZT;
 constexpr int OFF_ACC = OFF_RING + NBUF * BLKS;
 constexpr int MAX_R1 = 512;
 constexpr int OFF_S = OFF_ACC + 4 * MAX_R1 * 4;  // the unit's s vector (fp32)
-constexpr int SMEM_BYTES = OFF_S + MAX_R1 * 4;
+// dU / dV flush staging: per epilogue warp 8 rows x (128 B + 16 B pad), so that the partial-gradient
+// reductions leave the SM as whole 128-byte lines (8 lanes x 16 B per neuron row)
+constexpr int STG_ROW = 144;
+constexpr int STG_WARP = 8 * STG_ROW;
+constexpr int OFF_STG = OFF_S + MAX_R1 * 4;
+constexpr int SMEM_BYTES = OFF_STG + NWE * STG_WARP;
+static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
 constexpr uint32_t TM_P1 = 0, TM_DZ = 128, TM_Y = 256, TM_DU = 384, TM_DV = 448;
 constexpr uint32_t HK = (128u >> 4) | (1u << 14);   // SBO 128 B
 constexpr uint32_t HM = (2048u >> 4) | (1u << 14);  // SBO 2048 B
@@ -375,24 +382,49 @@ meta_tc2_kernel(const MetaNet2 net, const RunGeom g, const double* __restrict__ 
                          y[8 * e + 3], y[8 * e + 4], y[8 * e + 5], y[8 * e + 6], y[8 * e + 7]);
             }
         };
-        // flush the dU / dV chunk of reverse chunk rr (transition l, chunk ch): this thread's
-        // neuron, ranks RW grp .. RW grp + RW - 1
+        // flush the dU / dV chunk of reverse chunk rr (transition l, chunk ch) into this CTA's
+        // partial.  Warp groups 0 / 1 take dU ranks 0-31 / 32-63 of the warp's 32 neurons, groups
+        // 2 / 3 the same of dV: a thread reads one 128-byte line of its neuron's row from TMEM.  The
+        // rows go through a per-warp staging tile, 8 at a time, so that 8 consecutive lanes reduce one
+        // whole line (4 lines per instruction; one 16-byte request per lane and neuron row before:
+        // the flush was bound by the request count, 4096 per chunk, not by bytes).  Every address
+        // keeps a single writer thread, so the sum order is fixed.
+        static_assert(NGRP == 4, "flush: 4 warp groups (dU lo / hi, dV lo / hi)");
+        unsigned char* stg = sm + OFF_STG + warp * STG_WARP;
         auto flush = [&](uint32_t rr, int l, int ch) {
             MT(8, wait(&dready, rr & 1));
-            float du[RW], dv[RW];
-            tld_rw(tl + TM_DU + RW * grp, du);
-            tld_rw(tl + TM_DV + RW * grp, dv);
+            const bool isv = grp >= 2;
+            const int c0 = 32 * (grp & 1);
+            float a[32];
+            const uint32_t src = tl + (isv ? TM_DV : TM_DU) + c0;
+            umma::tmem_ld16(src, *reinterpret_cast<float(*)[16]>(a));
+            umma::tmem_ld16(src + 16, *reinterpret_cast<float(*)[16]>(a + 16));
             umma::tmem_ld_wait();
             signal(&dfree);
-            float* base = wg + net.gbase[l] + static_cast<int64_t>(ch) * 16384 + kn * 64 + RW * grp;
             if (MTC_SKIP & 2) return;
-            if (RW * grp < net.rp[l])
+            const int nvalid = isv ? net.rp[l + 1] : net.rp[l];
+            if (c0 >= nvalid) return;  // warp-uniform
+            const int pc = lane & 7, rsub = lane >> 3;
+            float* base = wg + net.gbase[l] + static_cast<int64_t>(ch) * 16384 + (isv ? 8192 : 0) +
+                          (quarter * 32) * 64 + c0 + 4 * pc;
+            const bool on = c0 + 4 * pc < nvalid;
 #pragma unroll
-                for (int i = 0; i < RW / 4; ++i) red4(base + 4 * i, du[4 * i], du[4 * i + 1], du[4 * i + 2], du[4 * i + 3]);
-            if (RW * grp < net.rp[l + 1])
+            for (int j = 0; j < 4; ++j) {
+                if (rsub == j) {
 #pragma unroll
-                for (int i = 0; i < RW / 4; ++i)
-                    red4(base + 8192 + 4 * i, dv[4 * i], dv[4 * i + 1], dv[4 * i + 2], dv[4 * i + 3]);
+                    for (int q4 = 0; q4 < 8; ++q4)
+                        *reinterpret_cast<float4*>(stg + pc * STG_ROW + q4 * 16) =
+                            make_float4(a[4 * q4], a[4 * q4 + 1], a[4 * q4 + 2], a[4 * q4 + 3]);
+                }
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int r = 4 * i + rsub;
+                    const float4 v = *reinterpret_cast<const float4*>(stg + r * STG_ROW + pc * 16);
+                    if (on) red4(base + (8 * j + r) * 64, v.x, v.y, v.z, v.w);
+                }
+                __syncwarp();
+            }
         };
 
         for (int64_t unit = blockIdx.x; unit < g.n_units; unit += gridDim.x) {
