@@ -168,14 +168,12 @@ __device__ __forceinline__ void put_rows(unsigned char* buf, int p, int h, const
         const float s = umma::exp2i(e[c]);
         uint32_t hw[4], lw[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) umma::split16x2(v[c][2 * i] * s, v[c][2 * i + 1] * s, hw[i], lw[i]);
+        for (int i = 0; i < 4; ++i) umma::split16x2_fh(v[c][2 * i] * s, v[c][2 * i + 1] * s, hw[i], lw[i]);
         *reinterpret_cast<uint4*>(buf + c * OPD_SLOT + o) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
         *reinterpret_cast<uint4*>(buf + c * OPD_SLOT + OPD_HALF + o) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
     }
 }
 
-// named barrier over the 16 epilogue warps (the issuer warps keep running)
-__device__ __forceinline__ void named_bar_epi() { asm volatile("bar.sync 1, %0;" ::"n"(NWE * 32) : "memory"); }
 // named barrier over the 4 epilogue warps that share a TMEM lane quarter (the same 32 points):
 // enough for the per-point norm exchanges through xch
 __device__ __forceinline__ void quarter_bar(int quarter) { asm volatile("bar.sync %0, 128;" ::"r"(8 + quarter) : "memory"); }
@@ -188,7 +186,7 @@ __device__ __forceinline__ void put_rows_tmem(uint32_t tsy, int h, const float (
         const float s = umma::exp2i(e[c]);
         uint32_t hw[4], lw[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) umma::split16x2(v[c][2 * i] * s, v[c][2 * i + 1] * s, hw[i], lw[i]);
+        for (int i = 0; i < 4; ++i) umma::split16x2_fh(v[c][2 * i] * s, v[c][2 * i + 1] * s, hw[i], lw[i]);
         umma::tmem_st4u(tsy + c * 32 + 4 * h, hw[0], hw[1], hw[2], hw[3]);
         umma::tmem_st4u(tsy + c * 32 + 16 + 4 * h, lw[0], lw[1], lw[2], lw[3]);
     }
@@ -725,7 +723,10 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                                 ssy[c] = fmaf(sy[c][n], sy[c][n], ssy[c]);
                             }
                         }
-                        named_bar_epi();  // every epilogue thread has read the u partials and y_{L-2}
+                        // the 4 warps of this lane quarter have read the u partials and their y_{L-2}
+                        // (the y block and the SY operand tiles both keep a point's bytes at p * 16 of
+                        // every 2 KB row block, so a quarter only ever touches its own 512-byte columns of W)
+                        quarter_bar(quarter);
                         *reinterpret_cast<float4*>(xch + (h * P + p) * 8) = make_float4(ss[0], ss[1], ss[2], ss[3]);
                         *reinterpret_cast<float4*>(xch + (h * P + p) * 8 + 4) = make_float4(ssy[0], ssy[1], ssy[2], ssy[3]);
                         quarter_bar(quarter);
@@ -887,7 +888,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                         }
                         *reinterpret_cast<float4*>(xch + (h * P + p) * 8) = make_float4(ss[0], ss[1], ss[2], ss[3]);
                         *reinterpret_cast<float4*>(xch + (h * P + p) * 8 + 4) = make_float4(ssy[0], ssy[1], ssy[2], ssy[3]);
-                        named_bar_epi();  // also: every thread has read its y_{l-1} from W
+                        quarter_bar(quarter);  // also: this quarter's threads have read their y_{l-1} from W
                         float nst[4] = {0.f, 0.f, 0.f, 0.f}, nsy[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                         for (int hh = 0; hh < 4; ++hh) {

@@ -216,6 +216,22 @@ __device__ __forceinline__ void split16x2(float x0, float x1, uint32_t& h, uint3
     h = hh;
     l = ll;
 }
+// The same bits with x - hi as one mixed-precision FMA per value (fma.rn.f32.f16 = FHFMA on
+// sm_100a: hi * -1 + x, exact): a shorter dependency chain for the latency-bound transition
+// ends (c2 FastLRNR 4.61 -> 4.49 ms); in the issue-bound chunk loops it measured no faster
+// than cvt + sub (c2 LRNR 12.76 vs 12.80 ms), so those keep split16x2.
+__device__ __forceinline__ void split16x2_fh(float x0, float x1, uint32_t& h, uint32_t& l) {
+    uint32_t hh, ll;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hh) : "f"(x1), "f"(x0));
+    float r0, r1;
+    asm("{\n\t.reg .f16 a, b, m;\n\tmov.b32 {a, b}, %2;\n\tmov.b16 m, 0xBC00;\n\t"
+        "fma.rn.f32.f16 %0, a, m, %3;\n\tfma.rn.f32.f16 %1, b, m, %4;\n\t}"
+        : "=f"(r0), "=f"(r1)
+        : "r"(hh), "f"(x0), "f"(x1));
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(ll) : "f"(r1), "f"(r0));
+    h = hh;
+    l = ll;
+}
 // power-of-two scale 2^k for a non-negative bound b: b * 2^k < 2^15, k clamped to [-40, 40]
 // (a product of up to three such factors is a normal FP32 number; bounds below 2^-26 keep a
 // smaller scale, which only widens their absolute precision window to 2^-65; bounds above
