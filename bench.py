@@ -539,6 +539,7 @@ def single_gpu_fp64(env, pkg, args, key):
                          "flop_per_point": fl, "points_per_launch": n, "peak_source": src,
                          "kernel": "pinn_tile_kernel (FMA tile GEMM, FP64)" if key == "c0" else
                          "pinn_tile_kernel (FastLRNR, FP64)",
+                         "traffic": traffic_per_launch("pinn_tile_kernel" if key == "c0" else "pinn_tile_kernel_c1", n),
                          "note": "4096 points = 28 per SM: latency-bound by construction (SURVEY 7)"},
             "gpu_launches_per_step": launches_per_call}
     if not args.no_e2e:

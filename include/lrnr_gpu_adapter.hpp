@@ -385,6 +385,26 @@ public:
         return b;
     }
 
+    // Q-DEIM basis (BASELINE configs[1]: "indices from pivoted QR of U^l"; no reference
+    // counterpart): EimBasis{xi, indices = pivoted-QR rows of xi, block_lu = lu(P^T xi)},
+    // ready for the reference's own reduction::build_fastparams (reduction.cpp:240-283).
+    static reduction::EimBasis qdeim_basis(const DenseMatrix& xi) {
+        std::vector<int64_t> idx(xi.cols > 0 ? xi.cols : 1);
+        int64_t count = 0;
+        if (lrnr_host_qdeim(static_cast<int64_t>(xi.rows), static_cast<int64_t>(xi.cols), xi.data.data(), idx.data(),
+                            &count) != 0 ||
+            count != static_cast<int64_t>(xi.cols))
+            throw std::invalid_argument("qdeim_basis: empty or rank-deficient basis");
+        reduction::EimBasis b;
+        b.xi = xi;
+        for (int64_t k = 0; k < count; ++k) b.indices.push_back(static_cast<std::size_t>(idx[k]));
+        DenseMatrix block(b.indices.size(), b.indices.size());
+        for (std::size_t i = 0; i < b.indices.size(); ++i)
+            for (std::size_t j = 0; j < b.indices.size(); ++j) block.at(i, j) = b.xi.at(b.indices[i], j);
+        b.block_lu = lu_factor(block);
+        return b;
+    }
+
     lrnr_gpu_ctx* handle() { return ctx_; }
 
 private:

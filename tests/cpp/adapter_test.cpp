@@ -126,6 +126,32 @@ int main() {
         std::printf("FastLRNR construction: %zu snapshot / %zu basis / %zu factor mismatches (%zu columns)\n",
                     snap_diff, basis_diff, fast_diff, ref_snaps.tags.size());
         eim_ok = snap_diff == 0 && basis_diff == 0 && fast_diff == 0;
+
+        // Q-DEIM bases (pivoted-QR rows of U^l) through the reference's own eim_apply and
+        // build_fastparams: interpolation is exact on range(U^l), u_hat = the selected rows
+        std::vector<reduction::EimBasis> qb;
+        double q_err = 0.0;
+        std::size_t q_rows = 0;
+        for (std::size_t l = 0; l + 1 < p2.depth(); ++l) {
+            qb.push_back(lrnr::gpu::Engine::qdeim_basis(p2.u[l]));
+            const reduction::EimBasis& b = qb.back();
+            DenseVector z(p2.u[l].rows), sampled(b.dim());
+            for (std::size_t i = 0; i < z.len(); ++i) {
+                double acc = 0.0;
+                for (std::size_t j = 0; j < p2.u[l].cols; ++j) acc += p2.u[l].at(i, j) * (0.3 + 0.1 * static_cast<double>(j));
+                z[i] = acc;
+            }
+            for (std::size_t k = 0; k < b.dim(); ++k) sampled[k] = z[b.indices[k]];
+            const DenseVector back = reduction::eim_apply(b, sampled);
+            for (std::size_t i = 0; i < z.len(); ++i) q_err = std::max(q_err, std::abs(back[i] - z[i]));
+        }
+        const FastParams fq = reduction::build_fastparams(p2, qb);
+        for (std::size_t l = 0; l + 1 < p2.depth(); ++l)
+            for (std::size_t k = 0; k < qb[l].dim(); ++k)
+                for (std::size_t j = 0; j < p2.u[l].cols; ++j)
+                    q_rows += fq.u_hat[l].at(k, j) != p2.u[l].at(qb[l].indices[k], j);
+        std::printf("Q-DEIM bases: interpolation error on range(U) %.2e, %zu u_hat mismatches\n", q_err, q_rows);
+        eim_ok = eim_ok && q_err <= 1e-10 && q_rows == 0;
     }
 
     // full fine-tune batch: interior + initial + periodic terms (PinnTermEmitter,
