@@ -129,7 +129,9 @@ void build_v2(Model& m, bool meta) {
     v.RPMAX = maxr <= 32 ? 32 : 64;
     // rank classes: 4 (first / last layers: r <= 4) or RPMAX
     v.rp.resize(L);
-    for (int l = 0; l < L; ++l) v.rp[l] = m.r[l] <= 4 ? 4 : v.RPMAX;
+    // (FP64 gradient sweeps also have a class of 16: c0 / c1's rank 10 would otherwise pad to 32)
+    const bool r16 = m.dtype == LRNR_F64 && !meta;
+    for (int l = 0; l < L; ++l) v.rp[l] = m.r[l] <= 4 ? 4 : (r16 && m.r[l] <= 16 ? 16 : v.RPMAX);
     if (m.dtype == LRNR_F64 || meta) {
         v.P = 32;
         v.NG = 8;

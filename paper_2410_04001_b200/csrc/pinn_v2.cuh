@@ -412,6 +412,7 @@ pinn_tile_kernel(const NetV2<T> net, const RunGeom g, const double* __restrict__
     constexpr int NT = K::NT;
     constexpr int KC = K::KC;
     constexpr int NJ = K::NJ;
+    constexpr bool R16 = sizeof(T) == 8 && !META;  // the host pads ranks 5..16 to 16 for these (build_v2)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* sm = reinterpret_cast<T*>(smem_raw);
     T* Zg = sm + S::OFF_Z;
@@ -534,14 +535,18 @@ pinn_tile_kernel(const NetV2<T> net, const RunGeom g, const double* __restrict__
         case 3: K::template fwd_phase1<RLV, 3>(UT, bb, SY, Zg, ng, pg, Ast); break;          \
         default: K::template fwd_phase1<RLV, 4>(UT, bb, SY, Zg, ng, pg, Ast); break;         \
     }
+                    // rank classes 4 / RPMAX, and 16 for FP64 (R16: c0 / c1's rank 10 pads to 16, not 32)
                     if (rl == 4) {
                         V2_FWD1(4)
+                    } else if (R16 && rl == 16) {
+                        if constexpr (R16) { V2_FWD1(16) }
                     } else {
                         V2_FWD1(RPMAX)
                     }
 #undef V2_FWD1
                     __syncthreads();
                     if (rn == 4) K::template phase2<4>(Zg, Vm, yacc, p2, jg, kc);
+                    else if (R16 && rn == 16) K::template phase2<R16 ? 16 : RPMAX>(Zg, Vm, yacc, p2, jg, kc);
                     else K::template phase2<RPMAX>(Zg, Vm, yacc, p2, jg, kc);
                     __syncthreads();
                 }
@@ -696,12 +701,15 @@ pinn_tile_kernel(const NetV2<T> net, const RunGeom g, const double* __restrict__
     }
                     if (rn == 4) {
                         V2_BWD1(4)
+                    } else if (R16 && rn == 16) {
+                        if constexpr (R16) { V2_BWD1(16) }
                     } else {
                         V2_BWD1(RPMAX)
                     }
 #undef V2_BWD1
                     __syncthreads();
                     if (rl == 4) K::template phase2<4>(Zg, Um, tacc, p2, jg, kc);
+                    else if (R16 && rl == 16) K::template phase2<R16 ? 16 : RPMAX>(Zg, Um, tacc, p2, jg, kc);
                     else K::template phase2<RPMAX>(Zg, Um, tacc, p2, jg, kc);
                     if constexpr (META) {
                         const int k0 = ch * KC;
