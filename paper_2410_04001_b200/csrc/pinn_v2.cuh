@@ -155,6 +155,16 @@ __device__ __forceinline__ void poly_sincos(float a, float& s, float& c) {
     c = ((q + 1) & 2) ? -cv : cv;
 }
 
+// tanh jet from its value (the same expressions as act3<0>)
+template <typename T>
+__device__ __forceinline__ void act3_from_value(T s, T& sg, T& d1, T& d2, T& d3) {
+    const T e = T(1) - s * s;
+    sg = s;
+    d1 = e;
+    d2 = T(-2) * s * e;
+    d3 = T(-2) * e * e + T(4) * s * s * e;
+}
+
 template <int ACT, bool FAST, typename T>
 __device__ __forceinline__ void act3(T a, T& sg, T& d1, T& d2, T& d3) {
     if constexpr (ACT == 0) {
@@ -245,9 +255,11 @@ struct Tile {
             for (int kk = 0; kk < KK; ++kk) {
                 const T av = a1[i][0][kk] + bias[kk], ax = a1[i][1][kk];
                 const T at = a1[i][2][kk], aw = a1[i][3][kk];
-                st4(Ast + ((pg * PT1 + i) * KC + ng + NG * kk) * 4, av, ax, at, aw);
                 T sg, d1, d2, d3;
                 act3<ACT, FAST>(av, sg, d1, d2, d3);
+                // tanh: the reverse sweep needs only sigma (its derivatives are polynomials in it, the
+                // reference's d*_from_value, autodiff.cpp:655-657), so sigma is stashed instead of a
+                st4(Ast + ((pg * PT1 + i) * KC + ng + NG * kk) * 4, ACT == 0 ? sg : av, ax, at, aw);
                 st4(Zg + (pg * PT1 + i) * S::ZS + (ng + NG * kk) * 4, sg, d1 * ax, d1 * at, d2 * ax * ax + d1 * aw);
             }
     }
@@ -297,7 +309,8 @@ struct Tile {
                 const T at = a1[i][2][kk], aw = a1[i][3][kk];
                 const T g0 = dz[i][0][kk], g1 = dz[i][1][kk], g2 = dz[i][2][kk], g3 = dz[i][3][kk];
                 T sg, d1, d2, d3;
-                act3<ACT, FAST>(av, sg, d1, d2, d3);
+                if constexpr (ACT == 0) act3_from_value(av, sg, d1, d2, d3);  // the stash holds sigma
+                else act3<ACT, FAST>(av, sg, d1, d2, d3);
                 const T gav = g0 * d1 + g1 * d2 * ax + g2 * d2 * at + g3 * (d3 * ax * ax + d2 * aw);
                 const T gax = g1 * d1 + g3 * T(2) * d2 * ax;
                 st4(Zg + (pg * PT1 + i) * S::ZS + (ng + NG * kk) * 4, gav, gax, g2 * d1, g3 * d1);
