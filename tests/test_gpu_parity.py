@@ -795,6 +795,22 @@ def test_unaligned_shapes_fp32_match_oracle(gpu, oracle, opts, kernel, act):
     assert normwise(got["grad_s"], want["grad_s"]) <= TOL32_NORM
 
 
+@pytest.mark.parametrize("act", [pkg.ACT_TANH, pkg.ACT_SIN])
+@pytest.mark.parametrize("ranks", [[2, 5, 16, 1], [2, 17, 4, 1], [2, 16, 32, 1], [2, 12, 9, 1]])
+def test_fp64_rank_classes_match_oracle(gpu, oracle, ranks, act):
+    """FP64 FMA tile kernel over its rank classes (4 / 16 / 32: ranks 5..16 pad to 16) with ragged
+    widths and a partial last tile; tanh runs the sigma stash (derivatives from the value)."""
+    m, s = pkg.make_baseline_model([2, 70, 33, 100, 1], ranks, 77, act)
+    pts = pkg.sample_collocation(4003, 1000)
+    mu = np.array([12.0, 0.03, 2.0])
+    gpu.set_lrnr(m, pkg.F64)
+    gpu.set_points(pts)
+    got = gpu.loss_grad_s(pkg.MODEL_LRNR, s, mu)
+    want = oracle.lrnr_grad(m.widths, m.ranks, m.params, s, mu, pts, act=act)
+    assert abs(got["value"] - want["value"]) <= 1e-12 * abs(want["value"])
+    assert floor_rel(got["grad_s"], want["grad_s"]) <= TOL64
+
+
 def test_context_lifecycle_does_not_leak(golden):
     """create -> every feature -> destroy, repeated: device memory returns to its baseline."""
     import torch
