@@ -383,7 +383,7 @@ namespace detail {
 // ---------------------------------------------------------------------------
 // launch planning
 // ---------------------------------------------------------------------------
-template <int ACT, bool FAST>
+template <int ACT, bool FAST, bool NARROW>
 void launch_tc(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const double* mu_dev, double w,
                double* dev_out) {
     const auto& v = m.tc;
@@ -391,7 +391,7 @@ void launch_tc(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const dou
     const int R1 = 1 + m.rtotal;
     if (R1 > 1024) throw InvalidArg("tensor-core path supports r_total < 1024");
     const size_t smem = static_cast<size_t>(tc::SMEM_BYTES);
-    auto kern = tc::pinn_tc_kernel<ACT, FAST>;
+    auto kern = tc::pinn_tc_kernel<ACT, FAST, NARROW>;
     ctx->unit_ctr.ensure(sizeof(unsigned long long));
     CK(cudaMemsetAsync(ctx->unit_ctr.p, 0xff, sizeof(unsigned long long), ctx->stream));
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -453,12 +453,20 @@ bool dispatch_tc(lrnr_gpu_ctx* ctx, const Model& m, const double* s_dev, const d
     const bool want = ctx->opt_kernel == 2 || ctx->opt_kernel == 0;
     if (!m.tc.ok || !want) return false;
     const bool fast = ctx->opt_fast_sincos != 0;
+    bool narrow = true;  // one chunk per transition (the FastLRNR)
+    for (int l = 0; l + 1 < m.L; ++l) narrow = narrow && m.tc.nc[l] == 1;
+#define TC_GO(A_, F_)                                                             \
+    do {                                                                          \
+        if (narrow) launch_tc<A_, F_, true>(ctx, m, s_dev, mu_dev, w, dev_out);    \
+        else launch_tc<A_, F_, false>(ctx, m, s_dev, mu_dev, w, dev_out);          \
+    } while (0)
     if (m.act == LRNR_ACT_SIN) {
-        if (fast) launch_tc<1, true>(ctx, m, s_dev, mu_dev, w, dev_out);
-        else launch_tc<1, false>(ctx, m, s_dev, mu_dev, w, dev_out);
+        if (fast) TC_GO(1, true);
+        else TC_GO(1, false);
     } else {
-        launch_tc<0, false>(ctx, m, s_dev, mu_dev, w, dev_out);
+        TC_GO(0, false);
     }
+#undef TC_GO
     return true;
 }
 

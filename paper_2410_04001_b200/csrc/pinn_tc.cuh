@@ -246,7 +246,10 @@ __device__ __forceinline__ void fwd_scales(FwdScales& f, const NetTC& net, int l
     for (int c = 0; c < 4; ++c) f.iy[c] = exp2c(-ez[c] - kV);
 }
 
-template <int ACT, bool FAST>
+// NARROW: every transition is a single chunk (the FastLRNR).  The chunk-loop operand splits then
+// use the mixed-precision FMA form as well: those sweeps are latency-bound (c2 FastLRNR 4.55 ->
+// 4.49 ms), while the issue-bound wide sweeps keep cvt + sub (c2 LRNR 12.66 vs 12.80 ms).
+template <int ACT, bool FAST, bool NARROW>
 __global__ void __launch_bounds__(NT, 1)
 pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts, const double* __restrict__ svec,
                const double* __restrict__ mus, const float w, float* __restrict__ scratch, float* __restrict__ part,
@@ -592,7 +595,10 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                                 z[i][3] = fmaf(d2 * r1, r1 * fs.g3, d1 * (r3 * fs.f3));
                             }
 #pragma unroll
-                            for (int c = 0; c < 4; ++c) umma::split16x2(z[0][c], z[1][c], zh[c][n / 2], zl[c][n / 2]);
+                            for (int c = 0; c < 4; ++c) {
+                                if constexpr (NARROW) umma::split16x2_fh(z[0][c], z[1][c], zh[c][n / 2], zl[c][n / 2]);
+                                else umma::split16x2(z[0][c], z[1][c], zh[c][n / 2], zl[c][n / 2]);
+                            }
                         }
                         TC_MARK(3);
                         if (ch > 0) {
@@ -804,8 +810,12 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                                     gg[i][3] = d1 * (e3 * rs.k3);
                                 }
 #pragma unroll
-                                for (int c = 0; c < 4; ++c)
-                                    umma::split16x2(gg[0][c], gg[1][c], gh[c][2 * hf + n / 2], gl[c][2 * hf + n / 2]);
+                                for (int c = 0; c < 4; ++c) {
+                                    if constexpr (NARROW)
+                                        umma::split16x2_fh(gg[0][c], gg[1][c], gh[c][2 * hf + n / 2], gl[c][2 * hf + n / 2]);
+                                    else
+                                        umma::split16x2(gg[0][c], gg[1][c], gh[c][2 * hf + n / 2], gl[c][2 * hf + n / 2]);
+                                }
                             }
                         }
                         TC_MARK(9);
