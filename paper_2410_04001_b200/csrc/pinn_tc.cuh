@@ -264,6 +264,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
     __shared__ __align__(8) uint64_t wbar[NBUF];           // ring slot filled (TMA)
     __shared__ __align__(8) uint64_t p1full;     // forward P1 written (tcgen05.commit)
     __shared__ __align__(8) uint64_t rfull;      // reverse A / DZ written
+    __shared__ __align__(8) uint64_t afull;      // reverse A written (the DZ MMAs still run)
     __shared__ __align__(8) uint64_t zfree;      // P2 done: Z / G free, Y / T product ready
     __shared__ __align__(8) uint64_t ybar;       // y_l block copied into W (TMA)
     __shared__ uint32_t tmem_base;
@@ -283,6 +284,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
         for (int i = 0; i < NBUF; ++i) umma::mbar_init(&wbar[i], 1);
         umma::mbar_init(&p1full, 1);
         umma::mbar_init(&rfull, 1);
+        umma::mbar_init(&afull, 1);
         umma::mbar_init(&zfree, 1);
         umma::mbar_init(&ybar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -413,6 +415,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
         if (umma::elect_one()) {
             const unsigned char* b = slot(qq);
             mma_p1(tbase + TM_R, W, b, rkl);                               // A = SY_l U^T
+            umma::mma_commit_1(&afull);  // the epilogue starts the activation jets of its first neurons on A
             mma_p1(tbase + TM_R + 128, X, b + 4 * KC * rkl + 4 * KC, rkn);  // DZ = ST_{l+1} V^T
             umma::mma_commit_1(&rfull);
         }
@@ -776,19 +779,34 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                         issue_p2(q, slot(q) + bu, rnl, ch % YACC_R != 0);
                     } else {
                         TC_MARK(7);
-                        wait(&rfull, rq & 1);
-                        TC_MARK(8);
                         const float* bias = reinterpret_cast<const float*>(slot(q) + bbias);
                         uint32_t gh[4][NG / 2], gl[4][NG / 2];
+                        // A lands first: the activation jets of the first 4 neurons overlap the DZ MMAs
+                        float a0[4][NG / 2], j0[NG / 2][4];
+                        wait(&afull, rq & 1);
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) umma::tmem_ld4(tlane + TM_R + c * 32 + NG * h, a0[c]);
+                        umma::tmem_ld_wait();
+#pragma unroll
+                        for (int n = 0; n < NG / 2; ++n)
+                            act3f<ACT, FAST>(fmaf(a0[0][n], rs.ia0, bias[NG * h + n]), j0[n][0], j0[n][1], j0[n][2], j0[n][3]);
+                        wait(&rfull, rq & 1);
+                        TC_MARK(8);
 #pragma unroll
                         for (int hf = 0; hf < 2; ++hf) {
                             float a[4][NG / 2], dz[4][NG / 2];
 #pragma unroll
                             for (int c = 0; c < 4; ++c) {
-                                umma::tmem_ld4(tlane + TM_R + c * 32 + NG * h + 4 * hf, a[c]);
+                                if (hf == 1) umma::tmem_ld4(tlane + TM_R + c * 32 + NG * h + 4 * hf, a[c]);
                                 umma::tmem_ld4(tlane + TM_R + 128 + c * 32 + NG * h + 4 * hf, dz[c]);
                             }
                             umma::tmem_ld_wait();
+                            if (hf == 0) {
+#pragma unroll
+                                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                                    for (int n = 0; n < NG / 2; ++n) a[c][n] = a0[c][n];
+                            }
                             if (hf == 1) signal(BAR_RFREE);  // A / DZ consumed: the next chunk's MMAs may start
 #pragma unroll
                             for (int n = 0; n < NG / 2; n += 2) {
@@ -797,9 +815,16 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                                 for (int i = 0; i < 2; ++i) {
                                     const float r1 = a[1][n + i], r2 = a[2][n + i], r3 = a[3][n + i];
                                     const float e0 = dz[0][n + i], e1 = dz[1][n + i], e2 = dz[2][n + i], e3 = dz[3][n + i];
-                                    const float av = fmaf(a[0][n + i], rs.ia0, bias[NG * h + 4 * hf + n + i]);
                                     float sg, d1, d2, d3;
-                                    act3f<ACT, FAST>(av, sg, d1, d2, d3);
+                                    if (hf == 0) {
+                                        sg = j0[n + i][0];
+                                        d1 = j0[n + i][1];
+                                        d2 = j0[n + i][2];
+                                        d3 = j0[n + i][3];
+                                    } else {
+                                        const float av = fmaf(a[0][n + i], rs.ia0, bias[NG * h + 4 * hf + n + i]);
+                                        act3f<ACT, FAST>(av, sg, d1, d2, d3);
+                                    }
                                     float wv = (e3 * rs.k03) * r3;
                                     wv = fmaf(e2 * rs.k02, r2, wv);
                                     wv = fmaf(e1 * rs.k01, r1, wv);
