@@ -17,7 +17,7 @@ ctx.set_lrnr(m, pkg.F32)
 ctx.set_hyper(h)
 ctx.set_points(c["pts"], n_inst=n_inst)
 out = {}
-for prec in ([1, 2, 0] if with_fp32 else [1, 2]):
+for prec in ([1, 0] if with_fp32 else [1]):
     ctx.set_option(pkg.OPT_META_PREC, prec)
     r = ctx.meta_loss_grad(c["mus"], m.params.size)
     torch.cuda.synchronize()
@@ -27,6 +27,6 @@ for prec in ([1, 2, 0] if with_fp32 else [1, 2]):
         r = ctx.meta_loss_grad(c["mus"], m.params.size)
     dt = (time.perf_counter() - t0) / K
     n = n_inst * per
-    out[{1: "bf16_tc_v2", 2: "bf16_tc_v1", 0: "fp32_fma"}[prec]] = dict(ms=dt * 1e3, point_evals_per_s=n / dt, tflops=fl * n / dt / 1e12,
+    out[{1: "bf16_tc_v2", 0: "fp32_fma"}[prec]] = dict(ms=dt * 1e3, point_evals_per_s=n / dt, tflops=fl * n / dt / 1e12,
                                                  loss=r["value"], gnorm=float(np.linalg.norm(r["grad"])))
 print(json.dumps(out))
