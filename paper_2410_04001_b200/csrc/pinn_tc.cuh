@@ -197,6 +197,14 @@ __device__ __forceinline__ void act3f(float a, float& sg, float& d1, float& d2, 
     v2::act3<ACT, FAST>(a, sg, d1, d2, d3);
 }
 
+// Row norms only select power-of-two scales and bounds (one bit of FP16 headroom is kept), so the
+// SFU square root (2 ulp) replaces the correctly rounded sequence at the transition ends.
+__device__ __forceinline__ float sqrt_fast(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // 2^k for an integer exponent, clamped to the normal range
 __device__ __forceinline__ float exp2c(int k) { return umma::exp2i(max(-126, min(127, k))); }
 
@@ -443,8 +451,8 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
         int est[4], esy[4], Ed[4], Ea[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            nst[c] = sqrtf(nst[c]);
-            nsy[c] = sqrtf(nsy[c]);
+            nst[c] = sqrt_fast(nst[c]);
+            nsy[c] = sqrt_fast(nsy[c]);
             est[c] = umma::pow2_exp(nst[c]);
             esy[c] = umma::pow2_exp(nsy[c]);
         }
@@ -480,14 +488,18 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
     // claims: the counter starts at all-ones (memset 0xff), so the first claim returns unit gridDim.x
     unsigned long long claim = 0;
     if (tid == 0) claim = atomicAdd(unit_ctr, 1ull) + 1ull + gridDim.x;
+    int64_t s_inst = -1;  // the instance whose s vector is staged
     for (int64_t unit = blockIdx.x; unit < g.n_units;) {
         const int64_t inst = unit / g.units_per_inst;
         const int seg = static_cast<int>(unit % g.units_per_inst);
         const int t_lo = seg * g.tiles_per_unit;
         const int t_hi = min(g.tiles_per_inst, t_lo + g.tiles_per_unit);
         // the instance's s coefficients in shared memory (read at every transition end)
-        for (int k = tid; k < net.rtotal; k += NT) ssm[k] = static_cast<float>(svec[inst * net.rtotal + k]);
-        __syncthreads();
+        if (inst != s_inst) {
+            for (int k = tid; k < net.rtotal; k += NT) ssm[k] = static_cast<float>(svec[inst * net.rtotal + k]);
+            s_inst = inst;
+            __syncthreads();
+        }
         const float* sv = ssm;
         const float mu0 = float(mus[3 * inst]), mu1 = float(mus[3 * inst + 1]), mu2 = float(mus[3 * inst + 2]);
 
@@ -540,7 +552,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                     int e[4];
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
-                        nr[c] = sqrtf(nr[c]);
+                        nr[c] = sqrt_fast(nr[c]);
                         e[c] = umma::pow2_exp(nr[c]);
                     }
                     int Ea[4];
@@ -667,7 +679,7 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
                         int e[4];
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
-                            nr[c] = sqrtf(nr[c]);
+                            nr[c] = sqrt_fast(nr[c]);
                             e[c] = umma::pow2_exp(nr[c]);
                         }
                         int Ea[4];
