@@ -399,11 +399,12 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
     // then issue the phase-2 MMAs
     auto issue_p2 = [&](int64_t qq, const unsigned char* bsrc, int rn, bool acc0) {
         await(BAR_ZFULL);
-        if (lane == 0 && qq >= 1) tma(qq - 1 + NBUF);
         if (umma::elect_one()) {
             mma_p2(bsrc, rn, acc0);
             umma::mma_commit_1(&zfree);
         }
+        __syncwarp();
+        if (lane == 0 && qq >= 1) tma(qq - 1 + NBUF);  // after the MMAs: the epilogue may be waiting for them
         __syncwarp();
     };
     // ISSUER: forward P1 of chunk qq into buffer fq & 1
@@ -576,8 +577,8 @@ pinn_tc_kernel(const NetTC net, const RunGeom g, const double* __restrict__ pts,
 #pragma unroll
                     for (int n = 0; n < NG; ++n) ysum[c][n] = 0.f;
                 if (warp == ISSUER) {
-                    if (l + 2 == L) prefetch_y(L - 2);  // W is free in the forward sweep
                     issue_fwd_p1(q, fq, rk);
+                    if (l + 2 == L) prefetch_y(L - 2);  // W is free in the forward sweep (after the MMAs: the epilogue waits for them)
                 }
                 for (int ch = 0; ch < nc; ++ch, ++q, ++fq) {
                     if (warp == ISSUER) {
