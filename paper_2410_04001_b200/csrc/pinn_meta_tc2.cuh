@@ -48,10 +48,7 @@ constexpr int ROWS = 4 * PH;      // jet rows per half (MMA N of P1, M of P2)
 constexpr int PT = 2 * PH;        // points per tile
 constexpr int KC = 128;           // neurons per chunk
 constexpr int RP = 64;            // max padded rank
-#ifndef MTC2_NWE
-#define MTC2_NWE 16
-#endif
-constexpr int NWE = MTC2_NWE;     // epilogue warps (32 + 2 would exceed 1024 threads per CTA)
+constexpr int NWE = 16;           // epilogue warps: 4 TMEM lane quarters x 4 column / rank groups
 constexpr int NGRP = NWE / 4;     // warps per TMEM lane quarter
 constexpr int CW = ROWS / NGRP;   // P1 columns (jet rows) per warp per half-step: 32 or 16
 constexpr int RW = 64 / NGRP;     // ranks per warp at the transition ends: 16 or 8
